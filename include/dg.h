@@ -1,0 +1,197 @@
+/*
+ * dg.h — C ABI of the B200-native 2-bit LUT GEMM / convolution library
+ * (libdg.so), after DeepGEMM, arXiv 2304.09049.
+ *
+ * Citation convention: "P:NNN" = line NNN of the paper text,
+ * "S:NNN" = line NNN of SPEC.md, "BJ" = BASELINE.json, "Qn" = reading n of
+ * DESIGN.md §3.
+ *
+ * ---------------------------------------------------------------------------
+ * Conventions (all calls)
+ *  - Every call returns dg_status.  No C++ exception crosses the ABI.
+ *  - Pointers prefixed d_ are DEVICE pointers owned by the caller; the library
+ *    never allocates, frees or synchronises.  Workspace needs are queried
+ *    with *_workspace_size.  Device calls are asynchronous on `stream` (a
+ *    cudaStream_t passed as void*, NULL = legacy default stream).
+ *  - Validation reads no device memory: out-of-range codes inside device
+ *    buffers are masked with &3 (and counted in d_err_count where offered).
+ *  - Codes are unsigned 2-bit patterns 0..3.  Signed levels exist only in
+ *    the level/product tables (reading Q2).
+ *
+ * Packed format (Fig. 1a caption, §3.1: 2-bit values packed into
+ * bytes with shift/OR; bit layout reading Q20 = S:129):
+ *  - row-major; each row holds K codes in ceil(K/4) bytes; code k of a row
+ *    sits in byte k>>2, bits [2(k&3), 2(k&3)+1] (LSB first);
+ *  - rows are `ld` bytes apart, ld >= ceil(K/4), ld % 16 == 0 (so every row
+ *    starts 16-byte aligned for 128-bit loads and TMA);
+ *  - codes k in [K, 4*ld) MUST be 0.  dg_pack_* and dg_im2col write them as
+ *    0; the GEMM kernels rely on it and correct for them exactly (Q10).
+ *
+ * GEMM orientation (BJ naming, reading Q1): C[m][n] = sum_{k<K} T[(W[m][k]<<2) | A[k][n]]
+ *  with both operands stored K-major: W as [M][ldw] packed rows, A as its
+ *  transpose At [N][lda] packed rows (an im2col row = one output pixel).
+ * ---------------------------------------------------------------------------
+ */
+#ifndef DG_H_
+#define DG_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define DG_API __attribute__((visibility("default")))
+#else
+#define DG_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t dg_status;
+#define DG_OK 0
+#define DG_ERR_INVALID_ARG (-1)  /* null pointer, bad enum, misaligned ld          */
+#define DG_ERR_SHAPE (-2)        /* non-positive / inconsistent dimensions          */
+#define DG_ERR_RANGE (-3)        /* parameter outside its documented range          */
+#define DG_ERR_OVERFLOW (-4)     /* table entry does not fit entry_bits, or the
+                                    worst-case |accumulator| reaches 2^31           */
+#define DG_ERR_UNSUPPORTED (-5)  /* e.g. tc variant forced on a non-product table   */
+#define DG_ERR_CUDA (-6)         /* a CUDA launch / driver call failed              */
+#define DG_ERR_WORKSPACE (-7)    /* workspace too small                             */
+
+/* Static string for a status code (never NULL). */
+DG_API const char *dg_status_string(dg_status s);
+
+/* ABI version of this header (bumped on any signature change). */
+#define DG_ABI_VERSION 1
+DG_API int32_t dg_abi_version(void);
+
+/* ---------------------------------------------------------------------------
+ * S4 — LUT build.  LUT-16 (§3.2): "The values stored in the LUT are all
+ * possible results of w·a"; index = weight code concatenated above the
+ * activation code (Alg. 1 line 9; reading Q7):
+ *        entries[(i<<2)|j] = wl[i] * al[j].
+ * Passed BY VALUE (by pointer to a host struct) to the GEMM calls.
+ */
+typedef struct {
+    int32_t entries[16];  /* T[(w<<2)|a], sign-extended                               */
+    int32_t entry_bits;   /* 8 | 16 | 32: declared storage width of the entries       */
+    int32_t is_product;   /* 1 iff entries == wl (x) al exactly (enables the tc path)  */
+    int32_t wl[4];        /* weight levels per code   (valid iff is_product)          */
+    int32_t al[4];        /* activation levels per code (valid iff is_product)        */
+} dg_lut;
+
+/* Host.  Builds the product table from integer levels.  entry_bits must be 8,
+ * 16 or 32; DG_ERR_OVERFLOW if any product does not fit a signed integer of
+ * that width ("will not overflow 8 bits", is enforced). */
+DG_API dg_status dg_build_lut(const int32_t wl[4], const int32_t al[4], int32_t entry_bits, dg_lut *out);
+
+/* Host.  Wraps an arbitrary 16-entry table (LUT-16 with any precomputed
+ * entries, §5.3 "flexibility"); is_product is detected exactly
+ * (entries == wl (x) al for some integer levels is NOT searched: is_product=0). */
+DG_API dg_status dg_lut_from_table(const int32_t entries[16], int32_t entry_bits, dg_lut *out);
+
+/* Bytes per packed row for K codes: roundup(ceil(K/4), 16). */
+DG_API int64_t dg_packed_ld(int64_t K);
+
+/* ---------------------------------------------------------------------------
+ * S1/S2 — packing (Fig. 1a).  d_codes is [rows][ld_codes] bytes,
+ * one code per byte (values > 3 are masked with &3 and counted into
+ * *d_err_count when it is non-NULL); d_packed is [rows][ld] in the packed
+ * format above, zero-filled beyond K.  dg_pack_weights is the same operation
+ * for the (offline) weight operand.                                   */
+DG_API dg_status dg_pack_codes(const uint8_t *d_codes, int64_t rows, int64_t K, int64_t ld_codes,
+                        uint8_t *d_packed, int64_t ld, int32_t *d_err_count, void *stream);
+DG_API dg_status dg_pack_weights(const uint8_t *d_codes, int64_t rows, int64_t K, int64_t ld_codes,
+                          uint8_t *d_packed, int64_t ld, int32_t *d_err_count, void *stream);
+
+/* Device unpack (inverse of pack; test/debug aid): d_codes [rows][K]. */
+DG_API dg_status dg_unpack_codes(const uint8_t *d_packed, int64_t rows, int64_t K, int64_t ld,
+                          uint8_t *d_codes, void *stream);
+
+/* S2 — Eq. 1 activation quantisation + pack:
+ *      q    = clip(round(fma(scale, x, zero_point)), qmin, qmax)
+ *      code = q - qmin                (offset-binary code, reading Q2)
+ * round = half away from zero (Q5); requires 0 <= qmax - qmin <= 3.
+ * d_x is fp32 [rows][K] (row stride K); output packed [rows][ld].           */
+DG_API dg_status dg_quantize_pack_activations(const float *d_x, int64_t rows, int64_t K, float scale,
+                                       float zero_point, int32_t qmin, int32_t qmax,
+                                       uint8_t *d_packed, int64_t ld, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * S3 — im2col over packed NHWC codes (the conv -> (M,N,K) GEMM lowering the
+ * paper benchmarks on, §5.1).  d_x is [B][H][W][C/4] packed bytes
+ * (C % 4 == 0: channels padded by the caller); row r = (b*Ho + ho)*Wo + wo of
+ * d_cols ([B*Ho*Wo][ld]) holds the codes x(b, ho*stride-pad+r', wo*stride-pad+s', c)
+ * in (r', s', c) order with c fastest, K = kh*kw*C; out-of-image taps hold
+ * pad_code (reading Q21).                                                   */
+DG_API dg_status dg_im2col(const uint8_t *d_x, int32_t B, int32_t H, int32_t W, int32_t C, int32_t kh,
+                    int32_t kw, int32_t stride, int32_t pad, uint8_t pad_code, uint8_t *d_cols,
+                    int64_t ld, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * S7 — integer requantisation (Eq. 1 applied to the int32 accumulator with
+ * s realised as mult*2^-shift, reading Q11; Q5 tie rule):
+ *      v    = acc + res + bias
+ *      q    = clip(rhaz(v*mult / 2^shift) + zp, qmin, qmax)      (int64 exact)
+ *      code = q - qmin                                           (0 <= qmax-qmin <= 3)
+ * where res = res_int32[r][c]  (d_res, a downsample shortcut's accumulator)
+ *          or res_levels[res_code[r][c]] * res_mult (d_res_codes, identity
+ *             shortcut over packed codes, reading Q13), and bias = bias[c]
+ * (bias_axis 0) or bias[r] (bias_axis 1).  0 <= shift <= 62.                 */
+typedef struct {
+    int32_t mult, shift, zp, qmin, qmax;
+    const int32_t *d_bias;       /* nullable                                       */
+    int32_t bias_axis;           /* 0: bias[col], 1: bias[row]                     */
+    const int32_t *d_res;        /* nullable int32 residual [rows][ld_res]         */
+    int64_t ld_res;              /* elements                                       */
+    const uint8_t *d_res_codes;  /* nullable packed residual codes [rows][ld_res_codes] */
+    int64_t ld_res_codes;        /* bytes                                          */
+    int32_t res_mult;
+    int32_t res_levels[4];
+} dg_requant;
+
+/* Standalone requant: d_acc [rows][ld_acc] int32 -> d_out packed codes
+ * [rows][ld_out] (4 consecutive columns per byte, LSB first; cols % 4 == 0
+ * not required, tail codes are 0). */
+DG_API dg_status dg_requantize(const int32_t *d_acc, int64_t rows, int64_t cols, int64_t ld_acc,
+                        const dg_requant *rq, uint8_t *d_out, int64_t ld_out, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * S5/S6/S7/S8 — LUT GEMM (Alg. 1; §3.1):
+ *      C[m][n] = sum_{k<K} lut.entries[(W[m][k] << 2) | A[k][n]]     (int32, exact)
+ * d_w [M][ldw], d_at [N][lda] packed (K-major, see above).
+ * Output: rq == NULL -> int32 C at d_c[m*ldc + n];
+ *         rq != NULL -> requantised codes (S7 fused), packed 4 columns (n) per
+ *                       byte: d_c is uint8 [M][ldc bytes]; N % 4 == 0.
+ * variant: 0 auto, 1 cc (CUDA-core PRMT lookups, any table),
+ *          2 tc (tcgen05 kind::i8 over the product factorisation;
+ *            DG_ERR_UNSUPPORTED unless lut->is_product and levels fit int8).
+ * DG_ERR_OVERFLOW if K * max|entry| >= 2^31.                                 */
+DG_API dg_status dg_lut_gemm(const uint8_t *d_w, int64_t ldw, const uint8_t *d_at, int64_t lda, int64_t M,
+                      int64_t N, int64_t K, const dg_lut *lut, void *d_c, int64_t ldc,
+                      const dg_requant *rq, int32_t variant, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * Convolution over packed NHWC codes = im2col (S3) + LUT GEMM (S5) + fused
+ * requant (S7), output NHWC (conv layers are run as (M,N,K) GEMMs):
+ *      out[b][ho][wo][co] = sum_{r,s,c} T[(w[co][r][s][c] << 2) | x(b, ho*st-pad+r, wo*st-pad+s, c)]
+ * d_x: [B][H][W][C/4] packed; d_w: [Cout][ldw] packed rows of K = kh*kw*C codes
+ * in (r,s,c) order.  Output: rq == NULL -> int32 [B*Ho*Wo][Cout];
+ * rq != NULL -> packed codes [B*Ho*Wo][Cout/4] (Cout % 4 == 0), the next
+ * layer's NHWC input.  Residuals / bias in rq are indexed [pixel][cout].    */
+typedef struct {
+    int32_t B, H, W, C, Cout, kh, kw, stride, pad;
+    int32_t pad_code;
+    int64_t ldw;
+} dg_conv_params;
+
+DG_API size_t dg_lut_conv2d_workspace_size(const dg_conv_params *p);
+DG_API dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_lut *lut,
+                        const dg_conv_params *p, const dg_requant *rq, void *d_out, void *d_ws,
+                        size_t ws_bytes, int32_t variant, void *stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DG_H_ */

@@ -1,0 +1,189 @@
+// api.cu — the C ABI of libdg (include/dg.h): host-side validation, LUT build (S4),
+// variant dispatch and the conv orchestration (im2col + LUT GEMM + fused requant).
+#include <string.h>
+
+#include "common.cuh"
+
+using namespace dg;
+
+namespace {
+
+bool fits_bits(int64_t v, int32_t bits) {
+    if (bits >= 32) return v >= INT32_MIN && v <= INT32_MAX;
+    const int64_t lo = -((int64_t)1 << (bits - 1)), hi = ((int64_t)1 << (bits - 1)) - 1;
+    return v >= lo && v <= hi;
+}
+
+bool aligned16(const void *p) { return ((uintptr_t)p & 15) == 0; }
+
+int64_t max_abs_entry(const int32_t *e) {
+    int64_t m = 0;
+    for (int i = 0; i < 16; ++i) {
+        int64_t a = e[i] < 0 ? -(int64_t)e[i] : e[i];
+        m = a > m ? a : m;
+    }
+    return m;
+}
+
+bool levels_fit_i8(const int32_t *l) {
+    for (int i = 0; i < 4; ++i)
+        if (l[i] < -128 || l[i] > 127) return false;
+    return true;
+}
+
+dg_status check_rq(const dg_requant *rq) {
+    if (!rq) return DG_OK;
+    if (rq->qmax < rq->qmin || rq->qmax - rq->qmin > 3 || rq->shift < 0 || rq->shift > 62)
+        return DG_ERR_RANGE;
+    if (rq->bias_axis != 0 && rq->bias_axis != 1) return DG_ERR_INVALID_ARG;
+    return DG_OK;
+}
+
+// D[p][q] = sum_k Tt[(P<<2)|Q]; pl/ql = per-code levels of P/Q (valid iff product).
+dg_status gemm_dispatch(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t ldq, int64_t np,
+                        int64_t nq, int64_t K, const int32_t Tt[16], bool is_product,
+                        const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd,
+                        const dg_requant *rq, int32_t variant, cudaStream_t st) {
+    RequantArgs a{};
+    const RequantArgs *ap = nullptr;
+    if (rq) { a = to_args(rq); ap = &a; }
+    const bool tc_ok = is_product && levels_fit_i8(pl) && levels_fit_i8(ql) && tc_available();
+    if (variant == 2 && !tc_ok) return DG_ERR_UNSUPPORTED;
+    if (variant == 2 || (variant == 0 && tc_ok))
+        return lut_gemm_tc(P, ldp, Q, ldq, np, nq, K, pl, ql, D, ldd, ap, st);
+    return lut_gemm_cc(P, ldp, Q, ldq, np, nq, K, Tt, D, ldd, ap, st);
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *dg_status_string(dg_status s) {
+    switch (s) {
+        case DG_OK: return "DG_OK";
+        case DG_ERR_INVALID_ARG: return "DG_ERR_INVALID_ARG";
+        case DG_ERR_SHAPE: return "DG_ERR_SHAPE";
+        case DG_ERR_RANGE: return "DG_ERR_RANGE";
+        case DG_ERR_OVERFLOW: return "DG_ERR_OVERFLOW";
+        case DG_ERR_UNSUPPORTED: return "DG_ERR_UNSUPPORTED";
+        case DG_ERR_CUDA: return "DG_ERR_CUDA";
+        case DG_ERR_WORKSPACE: return "DG_ERR_WORKSPACE";
+        default: return "DG_ERR_UNKNOWN";
+    }
+}
+
+int32_t dg_abi_version(void) { return DG_ABI_VERSION; }
+
+dg_status dg_build_lut(const int32_t wl[4], const int32_t al[4], int32_t entry_bits, dg_lut *out) {
+    if (!wl || !al || !out) return DG_ERR_INVALID_ARG;
+    if (entry_bits != 8 && entry_bits != 16 && entry_bits != 32) return DG_ERR_INVALID_ARG;
+    dg_lut t;
+    memset(&t, 0, sizeof(t));
+    for (int i = 0; i < 4; ++i)
+        for (int j = 0; j < 4; ++j) {
+            const int64_t v = (int64_t)wl[i] * al[j];  // LUT-16 entry: w·a
+            if (!fits_bits(v, entry_bits)) return DG_ERR_OVERFLOW;
+            t.entries[(i << 2) | j] = (int32_t)v;
+        }
+    t.entry_bits = entry_bits;
+    t.is_product = 1;
+    for (int i = 0; i < 4; ++i) { t.wl[i] = wl[i]; t.al[i] = al[i]; }
+    *out = t;
+    return DG_OK;
+}
+
+dg_status dg_lut_from_table(const int32_t entries[16], int32_t entry_bits, dg_lut *out) {
+    if (!entries || !out) return DG_ERR_INVALID_ARG;
+    if (entry_bits != 8 && entry_bits != 16 && entry_bits != 32) return DG_ERR_INVALID_ARG;
+    dg_lut t;
+    memset(&t, 0, sizeof(t));
+    for (int e = 0; e < 16; ++e) {
+        if (!fits_bits(entries[e], entry_bits)) return DG_ERR_OVERFLOW;
+        t.entries[e] = entries[e];
+    }
+    t.entry_bits = entry_bits;
+    t.is_product = 0;
+    *out = t;
+    return DG_OK;
+}
+
+dg_status dg_lut_gemm(const uint8_t *d_w, int64_t ldw, const uint8_t *d_at, int64_t lda, int64_t M,
+                      int64_t N, int64_t K, const dg_lut *lut, void *d_c, int64_t ldc,
+                      const dg_requant *rq, int32_t variant, void *stream) {
+    if (!d_w || !d_at || !lut || !d_c) return DG_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 2) return DG_ERR_INVALID_ARG;
+    if (M <= 0 || N <= 0 || K <= 0) return DG_ERR_SHAPE;
+    if (ldw % 16 || lda % 16 || ldw * 4 < K || lda * 4 < K) return DG_ERR_SHAPE;
+    if (!aligned16(d_w) || !aligned16(d_at)) return DG_ERR_INVALID_ARG;
+    if (rq ? (ldc * 4 < N) : (ldc < N)) return DG_ERR_SHAPE;
+    dg_status s = check_rq(rq);
+    if (s != DG_OK) return s;
+    if ((int64_t)K * max_abs_entry(lut->entries) >= ((int64_t)1 << 31)) return DG_ERR_OVERFLOW;
+    // P = W (rows m), Q = At (rows n): D[m][n] = C[m][n], table index (w<<2)|a as is.
+    return gemm_dispatch(d_w, ldw, d_at, lda, M, N, K, lut->entries, lut->is_product != 0, lut->wl,
+                         lut->al, d_c, ldc, rq, variant, (cudaStream_t)stream);
+}
+
+static bool conv_is_direct(const dg_conv_params *p) {
+    // a 1x1 / stride-1 / unpadded conv reads the NHWC tensor as its own im2col matrix
+    return p->kh == 1 && p->kw == 1 && p->stride == 1 && p->pad == 0 && (p->C / 4) % 16 == 0;
+}
+
+size_t dg_lut_conv2d_workspace_size(const dg_conv_params *p) {
+    if (!p || p->B <= 0 || p->H <= 0 || p->W <= 0 || p->C <= 0 || p->kh <= 0 || p->kw <= 0 ||
+        p->stride <= 0)
+        return 0;
+    if (conv_is_direct(p)) return 0;
+    const int64_t Ho = (p->H + 2 * p->pad - p->kh) / p->stride + 1;
+    const int64_t Wo = (p->W + 2 * p->pad - p->kw) / p->stride + 1;
+    const int64_t K = (int64_t)p->kh * p->kw * p->C;
+    return (size_t)((int64_t)p->B * Ho * Wo * dg_packed_ld(K) + 256);
+}
+
+dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_lut *lut,
+                        const dg_conv_params *p, const dg_requant *rq, void *d_out, void *d_ws,
+                        size_t ws_bytes, int32_t variant, void *stream) {
+    if (!d_x || !d_w || !lut || !p || !d_out) return DG_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 2) return DG_ERR_INVALID_ARG;
+    if (p->B <= 0 || p->H <= 0 || p->W <= 0 || p->C <= 0 || p->Cout <= 0 || p->kh <= 0 ||
+        p->kw <= 0 || p->stride <= 0 || p->pad < 0)
+        return DG_ERR_SHAPE;
+    if (p->C % 4 || p->pad_code < 0 || p->pad_code > 3) return DG_ERR_RANGE;
+    if (rq && p->Cout % 4) return DG_ERR_SHAPE;
+    const int64_t Ho = (p->H + 2 * p->pad - p->kh) / p->stride + 1;
+    const int64_t Wo = (p->W + 2 * p->pad - p->kw) / p->stride + 1;
+    if (Ho <= 0 || Wo <= 0) return DG_ERR_SHAPE;
+    const int64_t K = (int64_t)p->kh * p->kw * p->C;
+    if (p->ldw % 16 || p->ldw * 4 < K || !aligned16(d_w)) return DG_ERR_SHAPE;
+    dg_status s = check_rq(rq);
+    if (s != DG_OK) return s;
+    if (K * max_abs_entry(lut->entries) >= ((int64_t)1 << 31)) return DG_ERR_OVERFLOW;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t rows = (int64_t)p->B * Ho * Wo;
+    const uint8_t *P;
+    int64_t ldp;
+    if (conv_is_direct(p) && aligned16(d_x)) {
+        P = d_x;
+        ldp = p->C / 4;
+    } else {
+        const int64_t ld = dg_packed_ld(K);
+        if (!d_ws || (int64_t)ws_bytes < rows * ld) return DG_ERR_WORKSPACE;
+        uint8_t *cols = (uint8_t *)(((uintptr_t)d_ws + 15) & ~(uintptr_t)15);
+        if ((int64_t)ws_bytes - (int64_t)(cols - (uint8_t *)d_ws) < rows * ld) return DG_ERR_WORKSPACE;
+        s = dg_im2col(d_x, p->B, p->H, p->W, p->C, p->kh, p->kw, p->stride, p->pad,
+                      (uint8_t)p->pad_code, cols, ld, stream);
+        if (s != DG_OK) return s;
+        P = cols;
+        ldp = ld;
+    }
+    // P = pixels (activation codes), Q = weights: D[pixel][cout] is the NHWC output; the
+    // table is transposed so that the index stays (w<<2)|a: Tt[(a<<2)|w] = T[(w<<2)|a].
+    int32_t Tt[16];
+    for (int a = 0; a < 4; ++a)
+        for (int w = 0; w < 4; ++w) Tt[(a << 2) | w] = lut->entries[(w << 2) | a];
+    const int64_t ldd = rq ? p->Cout / 4 : p->Cout;
+    return gemm_dispatch(P, ldp, d_w, p->ldw, rows, p->Cout, K, Tt, lut->is_product != 0, lut->al,
+                         lut->wl, d_out, ldd, rq, variant, st);
+}
+
+}  // extern "C"

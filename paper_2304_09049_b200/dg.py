@@ -1,0 +1,275 @@
+"""Thin ctypes binding of libdg.so (include/dg.h).  Argument marshalling only.
+
+Device buffers are torch tensors; every call passes ``tensor.data_ptr()`` and
+``torch.cuda.current_stream().cuda_stream``.  All arithmetic of the hot path
+runs in the CUDA kernels of ``csrc/``.  There is no CPU fallback: if the
+library is missing or a call fails, a ``DGError`` is raised.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+from dataclasses import dataclass, field
+
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libdg.so")
+
+DG_OK = 0
+VARIANTS = {"auto": 0, "cc": 1, "tc": 2}
+
+
+class DGError(RuntimeError):
+    pass
+
+
+class dg_lut(ctypes.Structure):
+    _fields_ = [("entries", ctypes.c_int32 * 16), ("entry_bits", ctypes.c_int32),
+                ("is_product", ctypes.c_int32), ("wl", ctypes.c_int32 * 4), ("al", ctypes.c_int32 * 4)]
+
+    @property
+    def table(self):
+        return list(self.entries)
+
+
+class dg_requant(ctypes.Structure):
+    _fields_ = [("mult", ctypes.c_int32), ("shift", ctypes.c_int32), ("zp", ctypes.c_int32),
+                ("qmin", ctypes.c_int32), ("qmax", ctypes.c_int32), ("d_bias", ctypes.c_void_p),
+                ("bias_axis", ctypes.c_int32), ("d_res", ctypes.c_void_p), ("ld_res", ctypes.c_int64),
+                ("d_res_codes", ctypes.c_void_p), ("ld_res_codes", ctypes.c_int64),
+                ("res_mult", ctypes.c_int32), ("res_levels", ctypes.c_int32 * 4)]
+
+
+class dg_conv_params(ctypes.Structure):
+    _fields_ = [("B", ctypes.c_int32), ("H", ctypes.c_int32), ("W", ctypes.c_int32),
+                ("C", ctypes.c_int32), ("Cout", ctypes.c_int32), ("kh", ctypes.c_int32),
+                ("kw", ctypes.c_int32), ("stride", ctypes.c_int32), ("pad", ctypes.c_int32),
+                ("pad_code", ctypes.c_int32), ("ldw", ctypes.c_int64)]
+
+
+_lib = None
+
+
+def lib():
+    """Load libdg.so (fails loudly when the CUDA extension is missing)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DGError(f"libdg.so not built ({LIB_PATH}); run paper_2304_09049_b200/build.py")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i64, i32, u8 = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int32, ctypes.c_uint8
+        sig = {
+            "dg_status_string": ([i32], ctypes.c_char_p),
+            "dg_abi_version": ([], i32),
+            "dg_build_lut": ([P, P, i32, P], i32),
+            "dg_lut_from_table": ([P, i32, P], i32),
+            "dg_packed_ld": ([i64], i64),
+            "dg_pack_codes": ([P, i64, i64, i64, P, i64, P, P], i32),
+            "dg_pack_weights": ([P, i64, i64, i64, P, i64, P, P], i32),
+            "dg_unpack_codes": ([P, i64, i64, i64, P, P], i32),
+            "dg_quantize_pack_activations": ([P, i64, i64, ctypes.c_float, ctypes.c_float, i32, i32,
+                                              P, i64, P], i32),
+            "dg_im2col": ([P, i32, i32, i32, i32, i32, i32, i32, i32, u8, P, i64, P], i32),
+            "dg_requantize": ([P, i64, i64, i64, P, P, i64, P], i32),
+            "dg_lut_gemm": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, i32, P], i32),
+            "dg_lut_conv2d_workspace_size": ([P], ctypes.c_size_t),
+            "dg_lut_conv2d": ([P, P, P, P, P, P, P, ctypes.c_size_t, i32, P], i32),
+        }
+        for name, (args, res) in sig.items():
+            f = getattr(L, name)
+            f.argtypes = args
+            f.restype = res
+        _lib = L
+    return _lib
+
+
+def _check(status: int, what: str):
+    if status != DG_OK:
+        raise DGError(f"{what}: {lib().dg_status_string(status).decode()} ({status})")
+
+
+def _stream(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def _ptr(t):
+    return ctypes.c_void_p(t.data_ptr()) if t is not None else None
+
+
+def _dev(t, dtype, name):
+    if not (t.is_cuda and t.dtype == dtype and t.is_contiguous()):
+        raise DGError(f"{name}: expected a contiguous CUDA {dtype} tensor")
+
+
+# ---------------------------------------------------------------- LUT (host)
+def build_lut(wl, al, entry_bits: int = 8) -> dg_lut:
+    out = dg_lut()
+    w = (ctypes.c_int32 * 4)(*[int(v) for v in wl])
+    a = (ctypes.c_int32 * 4)(*[int(v) for v in al])
+    _check(lib().dg_build_lut(w, a, entry_bits, ctypes.byref(out)), "dg_build_lut")
+    return out
+
+
+def lut_from_table(entries, entry_bits: int = 32) -> dg_lut:
+    out = dg_lut()
+    e = (ctypes.c_int32 * 16)(*[int(v) for v in entries])
+    _check(lib().dg_lut_from_table(e, entry_bits, ctypes.byref(out)), "dg_lut_from_table")
+    return out
+
+
+def packed_ld(K: int) -> int:
+    return int(lib().dg_packed_ld(K))
+
+
+# ---------------------------------------------------------------- pack / unpack
+def pack_codes(codes: torch.Tensor, K: int | None = None, out: torch.Tensor | None = None,
+               err: torch.Tensor | None = None, weights: bool = False, stream=None) -> torch.Tensor:
+    """codes: uint8 [rows][ld_codes] one code per byte -> packed uint8 [rows][packed_ld(K)]."""
+    _dev(codes, torch.uint8, "codes")
+    rows, ldc = codes.shape
+    K = ldc if K is None else K
+    ld = packed_ld(K)
+    if out is None:
+        out = torch.empty((rows, ld), dtype=torch.uint8, device=codes.device)
+    fn = lib().dg_pack_weights if weights else lib().dg_pack_codes
+    _check(fn(_ptr(codes), rows, K, ldc, _ptr(out), out.shape[1], _ptr(err), _stream(stream)), "dg_pack")
+    return out
+
+
+def pack_weights(codes, K=None, out=None, err=None, stream=None):
+    return pack_codes(codes, K, out, err, weights=True, stream=stream)
+
+
+def unpack_codes(packed: torch.Tensor, K: int, stream=None) -> torch.Tensor:
+    _dev(packed, torch.uint8, "packed")
+    rows, ld = packed.shape
+    out = torch.empty((rows, K), dtype=torch.uint8, device=packed.device)
+    _check(lib().dg_unpack_codes(_ptr(packed), rows, K, ld, _ptr(out), _stream(stream)), "dg_unpack_codes")
+    return out
+
+
+def quantize_pack_activations(x: torch.Tensor, scale: float, zero_point: float, qmin: int, qmax: int,
+                              out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    _dev(x, torch.float32, "x")
+    rows, K = x.shape
+    ld = packed_ld(K)
+    if out is None:
+        out = torch.empty((rows, ld), dtype=torch.uint8, device=x.device)
+    _check(lib().dg_quantize_pack_activations(_ptr(x), rows, K, scale, zero_point, qmin, qmax, _ptr(out),
+                                              out.shape[1], _stream(stream)), "dg_quantize_pack_activations")
+    return out
+
+
+def im2col(x: torch.Tensor, B, H, W, C, kh, kw, stride, pad, pad_code=0, out=None, stream=None):
+    _dev(x, torch.uint8, "x")
+    Ho = (H + 2 * pad - kh) // stride + 1
+    Wo = (W + 2 * pad - kw) // stride + 1
+    ld = packed_ld(kh * kw * C)
+    if out is None:
+        out = torch.empty((B * Ho * Wo, ld), dtype=torch.uint8, device=x.device)
+    _check(lib().dg_im2col(_ptr(x), B, H, W, C, kh, kw, stride, pad, pad_code, _ptr(out), out.shape[1],
+                           _stream(stream)), "dg_im2col")
+    return out
+
+
+# ---------------------------------------------------------------- requant
+@dataclass
+class Requant:
+    """Host description of dg_requant (S7).  Tensors must stay alive across the call."""
+    mult: int
+    shift: int
+    zp: int = 0
+    qmin: int = 0
+    qmax: int = 3
+    bias: torch.Tensor | None = None        # int32
+    bias_axis: int = 0
+    res: torch.Tensor | None = None         # int32 [rows][ld_res]
+    res_codes: torch.Tensor | None = None   # uint8 packed [rows][ld_res_codes]
+    res_mult: int = 0
+    res_levels: tuple = (0, 0, 0, 0)
+
+    def c(self) -> dg_requant:
+        r = dg_requant()
+        r.mult, r.shift, r.zp, r.qmin, r.qmax = self.mult, self.shift, self.zp, self.qmin, self.qmax
+        if self.bias is not None:
+            _dev(self.bias, torch.int32, "bias")
+            r.d_bias = self.bias.data_ptr()
+        r.bias_axis = self.bias_axis
+        if self.res is not None:
+            _dev(self.res, torch.int32, "res")
+            r.d_res = self.res.data_ptr()
+            r.ld_res = self.res.shape[-1]
+        if self.res_codes is not None:
+            _dev(self.res_codes, torch.uint8, "res_codes")
+            r.d_res_codes = self.res_codes.data_ptr()
+            r.ld_res_codes = self.res_codes.shape[-1]
+        r.res_mult = self.res_mult
+        for i in range(4):
+            r.res_levels[i] = int(self.res_levels[i])
+        return r
+
+
+def requantize(acc: torch.Tensor, rq: Requant, out: torch.Tensor | None = None, stream=None):
+    _dev(acc, torch.int32, "acc")
+    rows, cols = acc.shape
+    if out is None:
+        out = torch.empty((rows, (cols + 3) // 4), dtype=torch.uint8, device=acc.device)
+    r = rq.c()
+    _check(lib().dg_requantize(_ptr(acc), rows, cols, cols, ctypes.byref(r), _ptr(out), out.shape[1],
+                               _stream(stream)), "dg_requantize")
+    return out
+
+
+# ---------------------------------------------------------------- GEMM / conv
+def lut_gemm(w: torch.Tensor, at: torch.Tensor, M: int, N: int, K: int, lut: dg_lut,
+             rq: Requant | None = None, variant: str | int = "auto", out: torch.Tensor | None = None,
+             stream=None) -> torch.Tensor:
+    """C[m][n] = sum_k T[(W[m][k]<<2)|A[k][n]] over packed W [M][ldw], At [N][lda]."""
+    _dev(w, torch.uint8, "w")
+    _dev(at, torch.uint8, "at")
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    if out is None:
+        out = (torch.empty((M, (N + 3) // 4), dtype=torch.uint8, device=w.device) if rq is not None
+               else torch.empty((M, N), dtype=torch.int32, device=w.device))
+    r = rq.c() if rq is not None else None
+    _check(lib().dg_lut_gemm(_ptr(w), w.shape[1], _ptr(at), at.shape[1], M, N, K, ctypes.byref(lut),
+                             _ptr(out), out.shape[1], ctypes.byref(r) if r is not None else None, v,
+                             _stream(stream)), "dg_lut_gemm")
+    return out
+
+
+def conv_params(B, H, W, C, Cout, kh, kw, stride, pad, pad_code=0, ldw=None) -> dg_conv_params:
+    p = dg_conv_params()
+    p.B, p.H, p.W, p.C, p.Cout, p.kh, p.kw, p.stride, p.pad = B, H, W, C, Cout, kh, kw, stride, pad
+    p.pad_code = pad_code
+    p.ldw = packed_ld(kh * kw * C) if ldw is None else ldw
+    return p
+
+
+def conv_workspace_size(p: dg_conv_params) -> int:
+    return int(lib().dg_lut_conv2d_workspace_size(ctypes.byref(p)))
+
+
+def lut_conv2d(x: torch.Tensor, w: torch.Tensor, lut: dg_lut, p: dg_conv_params, rq: Requant | None = None,
+               variant: str | int = "auto", out: torch.Tensor | None = None, ws: torch.Tensor | None = None,
+               stream=None) -> torch.Tensor:
+    """NHWC packed conv: x [B*H*W][C/4] (or any contiguous view), w [Cout][ldw] packed."""
+    _dev(x, torch.uint8, "x")
+    _dev(w, torch.uint8, "w")
+    v = VARIANTS[variant] if isinstance(variant, str) else int(variant)
+    Ho = (p.H + 2 * p.pad - p.kh) // p.stride + 1
+    Wo = (p.W + 2 * p.pad - p.kw) // p.stride + 1
+    rows = p.B * Ho * Wo
+    if out is None:
+        out = (torch.empty((rows, p.Cout // 4), dtype=torch.uint8, device=x.device) if rq is not None
+               else torch.empty((rows, p.Cout), dtype=torch.int32, device=x.device))
+    need = conv_workspace_size(p)
+    if ws is None and need > 0:
+        ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+    r = rq.c() if rq is not None else None
+    _check(lib().dg_lut_conv2d(_ptr(x), _ptr(w), ctypes.byref(lut), ctypes.byref(p),
+                               ctypes.byref(r) if r is not None else None, _ptr(out), _ptr(ws),
+                               ws.numel() if ws is not None else 0, v, _stream(stream)), "dg_lut_conv2d")
+    return out

@@ -1,0 +1,52 @@
+"""CPU-side checks of the C ABI boundary: the library builds, loads and exports every
+symbol include/dg.h declares; host-only calls (LUT build, status strings) work without a GPU."""
+import ctypes
+import os
+import re
+
+import pytest
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+def declared_functions():
+    src = open(os.path.join(ROOT, "include", "dg.h")).read()
+    return sorted(set(re.findall(r"^DG_API [^(]*?\b(dg_\w+)\(", src, re.M)))
+
+
+@pytest.fixture(scope="module")
+def lib():
+    from paper_2304_09049_b200 import build
+    path = build.build()
+    return ctypes.CDLL(path)
+
+
+def test_header_declares_the_boundary():
+    names = declared_functions()
+    for required in ["dg_build_lut", "dg_pack_weights", "dg_quantize_pack_activations", "dg_im2col",
+                     "dg_lut_gemm", "dg_lut_conv2d", "dg_requantize"]:
+        assert required in names
+
+
+def test_every_declared_symbol_is_exported(lib):
+    for name in declared_functions():
+        assert hasattr(lib, name), name
+
+
+def test_host_calls_without_gpu():
+    from paper_2304_09049_b200 import dg
+    L = dg.lib()
+    assert L.dg_abi_version() == 1
+    assert L.dg_status_string(-4) == b"DG_ERR_OVERFLOW"
+    lut = dg.build_lut([-2, -1, 0, 1], [0, 1, 2, 3], 8)
+    assert lut.is_product == 1
+    assert [lut.entries[(i << 2) | j] for i in range(4) for j in range(4)] == \
+        [w * a for w in (-2, -1, 0, 1) for a in (0, 1, 2, 3)]
+    with pytest.raises(dg.DGError, match="OVERFLOW"):
+        dg.build_lut([-128, 0, 0, 0], [127, 0, 0, 0], 8)
+    lut16 = dg.build_lut([-127, 0, 0, 127], [0, 1, 2, 127], 16)
+    assert min(lut16.entries) == -16129
+    t = dg.lut_from_table(list(range(16)), 8)
+    assert t.is_product == 0
+    assert dg.packed_ld(1) == 16 and dg.packed_ld(64) == 16 and dg.packed_ld(65) == 32
+    assert dg.packed_ld(576) == 144

@@ -1,0 +1,299 @@
+"""GPU parity: the CUDA path (through the C ABI) against the CPU oracle, bit-exact.
+
+Every output is integer (codes, int32 accumulators), so the bar is exact equality
+(DESIGN.md §4).  Inputs come from seeded generators; expected values come only from
+oracle/.
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+
+import oracle  # noqa: E402
+
+pytestmark = pytest.mark.gpu
+
+if not torch.cuda.is_available():  # pragma: no cover
+    pytest.skip("no CUDA device", allow_module_level=True)
+
+from paper_2304_09049_b200 import dg  # noqa: E402
+
+DEV = "cuda"
+VARIANTS = ["cc", "tc"]
+WL, AL = [-2, -1, 0, 1], [0, 1, 2, 3]
+
+
+def gpu_pack(codes_np, weights=False):
+    c = torch.from_numpy(np.ascontiguousarray(codes_np, dtype=np.uint8)).to(DEV)
+    return dg.pack_codes(c, weights=weights)
+
+
+def host(t):
+    torch.cuda.synchronize()
+    return t.cpu().numpy()
+
+
+def oracle_codes_of(packed_gpu, rows, K):
+    p = host(packed_gpu)
+    return oracle.unpack_codes(p, rows, K, p.shape[1])
+
+
+def variant_ok(variant, lut):
+    if variant == "tc" and not (lut.is_product and dg.lib() and _tc_available()):
+        return False
+    return True
+
+
+def _tc_available():
+    # probe: a tiny tc GEMM either runs or reports DG_ERR_UNSUPPORTED
+    lut = dg.build_lut(WL, AL, 8)
+    w = gpu_pack(np.zeros((1, 4), np.uint8))
+    try:
+        dg.lut_gemm(w, w, 1, 1, 4, lut, variant="tc")
+        return True
+    except dg.DGError as e:
+        if "UNSUPPORTED" in str(e):
+            return False
+        raise
+
+
+# ---------------------------------------------------------------- pack / quantize
+@pytest.mark.parametrize("K", [1, 3, 4, 63, 64, 65, 130, 576, 1001])
+def test_pack_matches_oracle_unpack(K):
+    g = np.random.default_rng(K)
+    codes = g.integers(0, 4, (37, K), dtype=np.uint8)
+    packed = gpu_pack(codes)
+    assert packed.shape[1] % 16 == 0
+    p = host(packed)
+    assert np.array_equal(oracle.unpack_codes(p, 37, K, p.shape[1]), codes)
+    # codes beyond K are zero (dg.h contract)
+    full = oracle.unpack_codes(p, 37, p.shape[1] * 4, p.shape[1])
+    assert not full[:, K:].any()
+    # device unpack is the inverse
+    assert np.array_equal(host(dg.unpack_codes(packed, K)), codes)
+
+
+def test_pack_error_count():
+    codes = np.array([[0, 1, 4, 3, 255, 2, 3, 1]], np.uint8)
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    packed = dg.pack_codes(torch.from_numpy(codes).to(DEV), err=err)
+    assert int(host(err)[0]) == 2
+    assert oracle_codes_of(packed, 1, 8).tolist() == [[0, 1, 0, 3, 3, 2, 3, 1]]
+
+
+@pytest.mark.parametrize("qmin,qmax", [(0, 3), (-2, 1)])
+def test_quantize_pack_vs_oracle(qmin, qmax):
+    g = np.random.default_rng(5)
+    x = g.normal(0, 1.5, (19, 77)).astype(np.float32)
+    x[0, :8] = np.array([0.25, -0.25, 0.75, -0.75, 1.25, 100, -100, 0], np.float32)  # ties, clips
+    s, z = 2.0, 0.5
+    packed = dg.quantize_pack_activations(torch.from_numpy(x).to(DEV), s, z, qmin, qmax)
+    q = oracle.quantize(x, s, z, qmin, qmax) - qmin
+    assert np.array_equal(oracle_codes_of(packed, 19, 77), q.astype(np.uint8))
+
+
+# ---------------------------------------------------------------- requant
+def test_requant_vs_oracle():
+    g = np.random.default_rng(6)
+    acc = g.integers(-5000, 5000, (33, 45)).astype(np.int32)
+    res = g.integers(-300, 300, (33, 45)).astype(np.int32)
+    bias = g.integers(-100, 100, 45).astype(np.int32)
+    rq = dg.Requant(mult=20180, shift=20, zp=1, qmin=0, qmax=3,
+                    bias=torch.from_numpy(bias).to(DEV), bias_axis=0,
+                    res=torch.from_numpy(res).to(DEV))
+    out = dg.requantize(torch.from_numpy(acc).to(DEV), rq)
+    exp = oracle.requantize(acc, 20180, 20, 1, 0, 3, res=res, bias=bias, bias_axis=0)
+    assert np.array_equal(oracle_codes_of(out, 33, 45), exp)
+
+
+def test_requant_ties_exhaustive():
+    acc = np.arange(-(1 << 12), 1 << 12, dtype=np.int32).reshape(-1, 64)
+    for mult, shift, zp, qmin, qmax in [(1 << 19, 20, 0, -2, 1), (3, 2, 1, 0, 3), (-7, 3, 0, -1, 2)]:
+        rq = dg.Requant(mult=mult, shift=shift, zp=zp, qmin=qmin, qmax=qmax)
+        out = dg.requantize(torch.from_numpy(acc).to(DEV), rq)
+        exp = oracle.requantize(acc, mult, shift, zp, qmin, qmax).view(np.int8).astype(np.int32) - qmin
+        assert np.array_equal(oracle_codes_of(out, acc.shape[0], 64), exp.astype(np.uint8))
+
+
+# ---------------------------------------------------------------- LUT GEMM
+def run_gemm(W, A, lut, variant, rq=None):
+    M, K = W.shape
+    N = A.shape[1]
+    w = gpu_pack(W, weights=True)
+    at = gpu_pack(np.ascontiguousarray(A.T))
+    return dg.lut_gemm(w, at, M, N, K, lut, rq=rq, variant=variant)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_gemm_config1(variant):
+    """BJ configs[0]: M=64, N=196, K=576; int8 product table; int32 + requant codes."""
+    import synth
+    lut = dg.build_lut(WL, AL, 8)
+    if not variant_ok(variant, lut):
+        pytest.skip("tc variant unavailable")
+    W = synth.uniform_codes((64, 576), 1, 0, synth.T_W)
+    A = synth.uniform_codes((576, 196), 1, 0, synth.T_A)
+    T = oracle.build_lut16(WL, AL)
+    C = host(run_gemm(W, A, lut, variant))
+    exp = oracle.lut_gemm(W, A, T)
+    assert np.array_equal(C, exp)
+    rq = synth.CFG1_RQ
+    bias = np.full(64, rq.bias, np.int32)
+    out = run_gemm(W, A, lut, variant, rq=dg.Requant(rq.mult, rq.shift, rq.zp, rq.qmin, rq.qmax,
+                                                     bias=torch.from_numpy(bias).to(DEV), bias_axis=1))
+    expc = oracle.requantize(exp, rq.mult, rq.shift, rq.zp, rq.qmin, rq.qmax, bias=bias, bias_axis=1)
+    assert np.array_equal(oracle_codes_of(out, 64, 196), expc)
+
+
+SHAPES = [(1, 1, 1), (1, 1, 4), (3, 5, 7), (64, 64, 128), (65, 63, 129), (130, 200, 300), (7, 300, 1000),
+          (200, 9, 2049), (257, 129, 4608)]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("M,N,K", SHAPES)
+def test_gemm_random_product(variant, M, N, K):
+    lut = dg.build_lut(WL, AL, 8)
+    if not variant_ok(variant, lut):
+        pytest.skip("tc variant unavailable")
+    g = np.random.default_rng(M * 1000 + N * 10 + K)
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    assert np.array_equal(host(run_gemm(W, A, lut, variant)), oracle.lut_gemm(W, A, oracle.build_lut16(WL, AL)))
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_gemm_non_product_tables_cc(seed):
+    """Arbitrary tables (LUT-16 with any precomputed entries): cc variant only."""
+    g = np.random.default_rng(100 + seed)
+    amp = [5, 60, 127, 1000, 16129, 1 << 20][seed]
+    T = g.integers(-amp, amp + 1, 16).astype(np.int32)
+    M, N, K = [(31, 17, 100), (64, 130, 257), (5, 64, 1024), (96, 40, 333), (80, 80, 2000), (33, 65, 513)][seed]
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    lut = dg.lut_from_table(T, 32)
+    assert np.array_equal(host(run_gemm(W, A, lut, "cc")), oracle.lut_gemm(W, A, T))
+    with pytest.raises(dg.DGError, match="UNSUPPORTED"):
+        run_gemm(W, A, lut, "tc")
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_gemm_config5_levels_small(variant):
+    """Config 5 table (reading Q17: learned-style levels, int16 product table) at a small size."""
+    import synth
+    wl, al = synth.learned_levels(5, 0, synth.T_LEVELS)
+    lut = dg.build_lut(wl, al, 16)
+    if not variant_ok(variant, lut):
+        pytest.skip("tc variant unavailable")
+    g = np.random.default_rng(55)
+    M, N, K = 160, 144, 1024
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    assert np.array_equal(host(run_gemm(W, A, lut, variant)), oracle.lut_gemm(W, A, oracle.build_lut16(wl, al)))
+
+
+def test_gemm_errors():
+    lut = dg.build_lut(WL, AL, 8)
+    w = gpu_pack(np.zeros((4, 8), np.uint8))
+    with pytest.raises(dg.DGError, match="SHAPE"):
+        dg.lut_gemm(w, w, 4, 4, 0, lut)
+    with pytest.raises(dg.DGError, match="OVERFLOW"):
+        dg.build_lut([127, 0, 0, 0], [127, 0, 0, 0], 8)
+    big = dg.lut_from_table([1 << 30] * 16, 32)
+    with pytest.raises(dg.DGError, match="OVERFLOW"):
+        dg.lut_gemm(w, w, 4, 4, 8, big)
+
+
+# ---------------------------------------------------------------- conv
+def nhwc_pack(x):
+    B, H, W, C = x.shape
+    Cp = (C + 3) // 4 * 4
+    xc = np.zeros((B * H * W, Cp), np.uint8)
+    xc[:, :C] = x.reshape(-1, C)
+    # pack rows of Cp codes into exactly Cp/4 bytes (NHWC packed), via the GPU packer
+    p = gpu_pack(xc)
+    return p[:, :Cp // 4].contiguous(), Cp
+
+
+def conv_weights_pack(w, Cp, wpad=2):
+    Cout, kh, kw, C = w.shape
+    wc = np.full((Cout, kh, kw, Cp), wpad, np.uint8)
+    wc[..., :C] = w
+    return gpu_pack(wc.reshape(Cout, -1), weights=True)
+
+
+CONVS = [  # B, H, W, C, Cout, k, stride, pad, pad_code
+    (1, 8, 8, 16, 16, 3, 1, 1, 0),
+    (2, 9, 7, 12, 20, 3, 2, 1, 0),
+    (2, 6, 6, 64, 32, 1, 1, 0, 0),     # direct (no im2col) path
+    (2, 7, 7, 64, 64, 1, 2, 0, 0),     # strided 1x1 (downsample)
+    (1, 10, 10, 3, 16, 3, 1, 1, 0),    # VGG conv1_1-like, Cin=3 padded to 4
+    (1, 5, 5, 8, 8, 3, 1, 1, 2),       # non-zero pad code
+    (3, 14, 14, 128, 64, 3, 1, 1, 0),
+]
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+@pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", CONVS)
+def test_conv_vs_oracle(variant, B, H, W, C, Cout, k, stride, pad, pad_code):
+    lut = dg.build_lut(WL, AL, 8)
+    if not variant_ok(variant, lut):
+        pytest.skip("tc variant unavailable")
+    g = np.random.default_rng(B * 7 + H + C + Cout + k)
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, k, k, C), dtype=np.uint8)
+    T = oracle.build_lut16(WL, AL)
+    exp = oracle.conv2d_direct(x, w, T, stride, pad, pad_code)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    p = dg.conv_params(B, H, W, Cp, Cout, k, k, stride, pad, pad_code, ldw=wp.shape[1])
+    try:
+        out = dg.lut_conv2d(xp, wp, lut, p, variant=variant)
+    except dg.DGError as e:
+        if variant == "tc" and pad_code != 0 and "UNSUPPORTED" in str(e):
+            pytest.skip("tc conv requires pad level 0")
+        raise
+    assert np.array_equal(host(out).reshape(exp.shape), exp)
+    # fused requant with a per-channel bias
+    bias = g.integers(-50, 50, Cout).astype(np.int32)
+    rq = dg.Requant(mult=30000, shift=20, zp=1, bias=torch.from_numpy(bias).to(DEV), bias_axis=0)
+    outc = dg.lut_conv2d(xp, wp, lut, p, rq=rq, variant=variant)
+    expc = oracle.requantize(exp.reshape(-1, Cout), 30000, 20, 1, 0, 3, bias=bias, bias_axis=0)
+    assert np.array_equal(oracle_codes_of(outc, expc.shape[0], Cout), expc)
+
+
+@pytest.mark.parametrize("variant", VARIANTS)
+def test_conv_residual_identity_and_downsample(variant):
+    """O-RES (reading Q13): identity shortcut r = al[x]*res_mult over packed codes, and a
+    downsample shortcut r = int32 accumulator of a 1x1 stride-2 conv."""
+    lut = dg.build_lut(WL, AL, 8)
+    if not variant_ok(variant, lut):
+        pytest.skip("tc variant unavailable")
+    g = np.random.default_rng(77)
+    T = oracle.build_lut16(WL, AL)
+    B, H, C = 2, 8, 64
+    x = g.integers(0, 4, (B, H, H, C), dtype=np.uint8)
+    w = g.integers(0, 4, (C, 3, 3, C), dtype=np.uint8)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    p = dg.conv_params(B, H, H, C, C, 3, 3, 1, 1, 0, ldw=wp.shape[1])
+    acc = oracle.conv2d_direct(x, w, T, 1, 1, 0).reshape(-1, C)
+    res_mult = 37
+    rq = dg.Requant(mult=15000, shift=20, zp=0, res_codes=xp, res_mult=res_mult, res_levels=AL)
+    out = dg.lut_conv2d(xp, wp, lut, p, rq=rq, variant=variant)
+    r = (np.array(AL)[x.reshape(-1, C)] * res_mult).astype(np.int32)
+    exp = oracle.requantize(acc, 15000, 20, 0, 0, 3, res=r)
+    assert np.array_equal(oracle_codes_of(out, exp.shape[0], C), exp)
+    # downsample: 1x1 stride 2 conv accumulators as the residual of a stride-2 3x3 conv
+    C2 = 128
+    w2 = g.integers(0, 4, (C2, 3, 3, C), dtype=np.uint8)
+    wd = g.integers(0, 4, (C2, 1, 1, C), dtype=np.uint8)
+    w2p, wdp = conv_weights_pack(w2, Cp), conv_weights_pack(wd, Cp)
+    pd = dg.conv_params(B, H, H, C, C2, 1, 1, 2, 0, 0, ldw=wdp.shape[1])
+    p2 = dg.conv_params(B, H, H, C, C2, 3, 3, 2, 1, 0, ldw=w2p.shape[1])
+    racc = dg.lut_conv2d(xp, wdp, lut, pd, variant=variant)
+    out2 = dg.lut_conv2d(xp, w2p, lut, p2, rq=dg.Requant(mult=12000, shift=20, res=racc), variant=variant)
+    a2 = oracle.conv2d_direct(x, w2, T, 2, 1, 0).reshape(-1, C2)
+    rd = oracle.conv2d_direct(x, wd, T, 2, 0, 0).reshape(-1, C2)
+    assert np.array_equal(host(racc), rd)
+    exp2 = oracle.requantize(a2, 12000, 20, 0, 0, 3, res=rd)
+    assert np.array_equal(oracle_codes_of(out2, exp2.shape[0], C2), exp2)

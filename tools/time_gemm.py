@@ -1,0 +1,40 @@
+"""Quick CUDA-event timing of dg_lut_gemm variants on synthetic square / conv-like shapes."""
+import argparse
+import os
+import sys
+
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402
+
+from paper_2304_09049_b200 import dg  # noqa: E402
+
+ap = argparse.ArgumentParser()
+ap.add_argument("--shapes", default="4096x4096x4096,64x802816x576,256x50176x2304")
+ap.add_argument("--variants", default="cc,tc")
+ap.add_argument("--iters", type=int, default=10)
+a = ap.parse_args()
+lut = dg.build_lut([-2, -1, 0, 1], [0, 1, 2, 3], 8)
+for s in a.shapes.split(","):
+    M, N, K = map(int, s.split("x"))
+    ld = dg.packed_ld(K)
+    w = torch.randint(0, 256, (M, ld), dtype=torch.uint8, device="cuda")
+    at = torch.randint(0, 256, (N, ld), dtype=torch.uint8, device="cuda")
+    if K % 64:
+        pass
+    out = torch.empty((M, N), dtype=torch.int32, device="cuda")
+    for v in a.variants.split(","):
+        try:
+            dg.lut_gemm(w, at, M, N, ld * 4, lut, variant=v, out=out)
+        except dg.DGError as e:
+            print(f"{s} {v}: {e}")
+            continue
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(a.iters):
+            dg.lut_gemm(w, at, M, N, ld * 4, lut, variant=v, out=out)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / a.iters
+        ops = 2 * M * N * ld * 4
+        print(f"{s} {v}: {ms:.3f} ms  {ops / ms / 1e9:.1f} TOPS")
