@@ -36,6 +36,11 @@ dg_status check_rq(const dg_requant *rq) {
     if (rq->qmax < rq->qmin || rq->qmax - rq->qmin > 3 || rq->shift < 0 || rq->shift > 62)
         return DG_ERR_RANGE;
     if (rq->bias_axis != 0 && rq->bias_axis != 1) return DG_ERR_INVALID_ARG;
+    if (rq->d_res_codes)
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = (int64_t)rq->res_levels[i] * rq->res_mult;
+            if (r > INT32_MAX || r < INT32_MIN) return DG_ERR_RANGE;   // keeps |v| < 2^34
+        }
     return DG_OK;
 }
 

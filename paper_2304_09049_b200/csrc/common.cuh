@@ -22,27 +22,142 @@ struct RequantArgs {
     int64_t ld_res_codes;
     int32_t res_mult;
     int32_t res_levels[4];
+    // Exact threshold form of the requant map (computed on the host by to_args):
+    // code(v) = sum_j [v >= thr[j]] (dir > 0)  or  sum_j [v <= thr[j]] (dir < 0).
+    int64_t thr[3];
+    int32_t dir;
 };
 
 DG_DEV int64_t rhaz(int64_t p, int32_t shift) {
-    if (shift == 0) return p;
-    const int64_t half = (int64_t)1 << (shift - 1);
-    return p >= 0 ? ((p + half) >> shift) : -((-p + half) >> shift);
+    // round half away from zero of p / 2^shift, branch-free on the magnitude
+    const int64_t sgn = p >> 63;                       // 0 or -1
+    const int64_t mag = (p ^ sgn) - sgn;
+    const int64_t half = shift > 0 ? ((int64_t)1 << (shift - 1)) : 0;
+    const int64_t r = (mag + half) >> shift;
+    return (r ^ sgn) - sgn;
 }
 
-// v already includes acc; adds residual and bias of element (r, c) and returns the code.
+DG_DEV int32_t res_level(const RequantArgs &q, uint32_t code) {
+    return (code & 2u) ? ((code & 1u) ? q.res_levels[3] : q.res_levels[2])
+                       : ((code & 1u) ? q.res_levels[1] : q.res_levels[0]);
+}
+
+// v = acc (+ residual + bias already added by the caller) -> code (S7; dg.h dg_requant).
+// code(v) = clip(rhaz(v*mult/2^shift) + zp, qmin, qmax) - qmin is monotone in v, so it is
+// evaluated exactly as a count of host-precomputed integer thresholds (no 64-bit multiply).
+DG_DEV uint32_t requant_value(const RequantArgs &q, int64_t v) {
+    if (q.dir > 0)
+        return (uint32_t)(v >= q.thr[0]) + (uint32_t)(v >= q.thr[1]) + (uint32_t)(v >= q.thr[2]);
+    return (uint32_t)(v <= q.thr[0]) + (uint32_t)(v <= q.thr[1]) + (uint32_t)(v <= q.thr[2]);
+}
+
+// Requantisation of one accumulator element (r, c): adds residual and bias, returns the code.
 DG_DEV uint32_t requant_one(const RequantArgs &q, int64_t acc, int64_t r, int64_t c) {
     int64_t v = acc;
     if (q.res) v += q.res[r * q.ld_res + c];
     if (q.res_codes) {
         uint32_t b = q.res_codes[r * q.ld_res_codes + (c >> 2)];
-        uint32_t code = (b >> (2 * (c & 3))) & 3u;
-        v += (int64_t)q.res_levels[code] * q.res_mult;
+        v += (int64_t)res_level(q, (b >> (2 * (c & 3))) & 3u) * q.res_mult;
     }
     if (q.bias) v += q.bias[q.bias_axis == 0 ? c : r];
-    int64_t t = rhaz(v * (int64_t)q.mult, q.shift) + q.zp;
-    t = t < q.qmin ? q.qmin : (t > q.qmax ? q.qmax : t);
-    return (uint32_t)(t - q.qmin);
+    return requant_value(q, v);
+}
+
+// Requantise 32 consecutive columns [c0, c0+32) of row r (all valid) -> 64 bits of codes,
+// 4 columns per byte LSB first.  Vectorised loads of bias / residuals where aligned.
+DG_DEV uint2 requant_row32(const RequantArgs &q, const int32_t (&acc)[32], int64_t r, int64_t c0) {
+    int64_t v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = acc[j];
+    if (q.bias) {
+        if (q.bias_axis == 1) {
+            const int64_t b = q.bias[r];
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += b;
+        } else if ((((uintptr_t)(q.bias + c0)) & 15) == 0) {
+            const int4 *b4 = reinterpret_cast<const int4 *>(q.bias + c0);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int4 b = __ldg(b4 + j);
+                v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += __ldg(q.bias + c0 + j);
+        }
+    }
+    if (q.res) {
+        const int32_t *rp = q.res + r * q.ld_res + c0;
+        if ((((uintptr_t)rp) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const int4 b = __ldg(reinterpret_cast<const int4 *>(rp) + j);
+                v[4 * j] += b.x; v[4 * j + 1] += b.y; v[4 * j + 2] += b.z; v[4 * j + 3] += b.w;
+            }
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) v[j] += __ldg(rp + j);
+        }
+    }
+    if (q.res_codes) {
+        const uint8_t *cp = q.res_codes + r * q.ld_res_codes + (c0 >> 2);
+        uint32_t w[2];
+        if ((((uintptr_t)cp) & 7) == 0) {
+            const uint2 t = *reinterpret_cast<const uint2 *>(cp);
+            w[0] = t.x; w[1] = t.y;
+        } else {
+            w[0] = cp[0] | (cp[1] << 8) | (cp[2] << 16) | ((uint32_t)cp[3] << 24);
+            w[1] = cp[4] | (cp[5] << 8) | (cp[6] << 16) | ((uint32_t)cp[7] << 24);
+        }
+#pragma unroll
+        for (int j = 0; j < 32; ++j)
+            v[j] += (int64_t)res_level(q, (w[j >> 4] >> (2 * (j & 15))) & 3u) * q.res_mult;
+    }
+    uint32_t o0 = 0, o1 = 0;
+#pragma unroll
+    for (int j = 0; j < 16; ++j) o0 |= requant_value(q, v[j]) << (2 * j);
+#pragma unroll
+    for (int j = 0; j < 16; ++j) o1 |= requant_value(q, v[16 + j]) << (2 * j);
+    return make_uint2(o0, o1);
+}
+
+// Host: the requant map evaluated exactly (128-bit product), reference for the thresholds.
+inline int64_t requant_code_host(const dg_requant *rq, int64_t v) {
+    __int128 p = (__int128)v * rq->mult;
+    __int128 mag = p < 0 ? -p : p;
+    __int128 half = rq->shift > 0 ? ((__int128)1 << (rq->shift - 1)) : 0;
+    __int128 r = (mag + half) >> rq->shift;
+    __int128 t = (p < 0 ? -r : r) + rq->zp;
+    if (t < rq->qmin) t = rq->qmin;
+    if (t > rq->qmax) t = rq->qmax;
+    return (int64_t)(t - rq->qmin);
+}
+
+inline void requant_thresholds(const dg_requant *rq, RequantArgs &a) {
+    const int64_t LO = -((int64_t)1 << 40), HI = ((int64_t)1 << 40);   // |acc+res+bias| < 2^34
+    const int64_t NEVER = INT64_MAX, ALWAYS = INT64_MIN;
+    a.dir = rq->mult >= 0 ? 1 : -1;
+    for (int j = 1; j <= 3; ++j) {
+        int64_t t;
+        if (a.dir > 0) {   // smallest v with code(v) >= j (code non-decreasing)
+            if (requant_code_host(rq, HI) < j) t = NEVER;
+            else if (requant_code_host(rq, LO) >= j) t = ALWAYS;
+            else {
+                int64_t lo = LO, hi = HI;          // code(lo) < j <= code(hi)
+                while (hi - lo > 1) { int64_t m = lo + (hi - lo) / 2; (requant_code_host(rq, m) >= j ? hi : lo) = m; }
+                t = hi;
+            }
+        } else {           // largest v with code(v) >= j (code non-increasing)
+            if (requant_code_host(rq, LO) < j) t = ALWAYS;
+            else if (requant_code_host(rq, HI) >= j) t = NEVER;
+            else {
+                int64_t lo = LO, hi = HI;          // code(lo) >= j > code(hi)
+                while (hi - lo > 1) { int64_t m = lo + (hi - lo) / 2; (requant_code_host(rq, m) >= j ? lo : hi) = m; }
+                t = lo;
+            }
+        }
+        a.thr[j - 1] = t;
+    }
 }
 
 inline RequantArgs to_args(const dg_requant *rq) {
@@ -60,6 +175,7 @@ inline RequantArgs to_args(const dg_requant *rq) {
     a.ld_res_codes = rq->ld_res_codes;
     a.res_mult = rq->res_mult;
     for (int i = 0; i < 4; ++i) a.res_levels[i] = rq->res_levels[i];
+    requant_thresholds(rq, a);
     return a;
 }
 

@@ -43,7 +43,7 @@ template <int NCH, int F>
 __global__ void __launch_bounds__(256) lut_gemm_cc_kernel(
     const uint8_t *__restrict__ P, int64_t ldp, const uint8_t *__restrict__ Q, int64_t ldq,
     int64_t np, int64_t nq, int64_t nchunks, CcTable tab, int64_t corr, void *__restrict__ D,
-    int64_t ldd, RequantArgs rq, int has_rq) {
+    int64_t ldd, const __grid_constant__ RequantArgs rq, int has_rq) {
     __shared__ __align__(16) uint32_t Ps[2][KC_WORDS][SROW];
     __shared__ __align__(16) uint32_t Qs[2][KC_WORDS][SROW];
 

@@ -26,13 +26,17 @@ namespace {
 constexpr int BM = 128;        // TMEM lanes / P rows per tile
 constexpr int KS = 128;        // codes per pipeline stage (one 128-byte SW128 row of int8)
 constexpr int PKB = KS / 4;    // packed bytes per row per stage
-constexpr int SP = 4;          // packed ring depth
-constexpr int SU = 2;          // unpacked (int8) ring depth
-constexpr int NT = 192;
+constexpr int NUM_UNPACK_WARPS = 4;
+constexpr int NUM_EPI_WARPS = 8;       // 2 per TMEM lane quarter, each owning half the columns
+constexpr int UNPACK_WARP0 = 2;
+constexpr int EPI_WARP0 = UNPACK_WARP0 + NUM_UNPACK_WARPS;
+constexpr int NT = 32 * (EPI_WARP0 + NUM_EPI_WARPS);   // 448 threads
 
 template <int BN>
-struct Layout {
-    static constexpr int UNP_P = BM * KS;          // bytes per unpacked P stage
+struct Cfg {
+    static constexpr int SU = BN == 64 ? 4 : 3;            // unpacked (int8) ring depth
+    static constexpr int SP = BN == 256 ? 4 : (BN == 128 ? 6 : 8);  // packed ring depth
+    static constexpr int UNP_P = BM * KS;                  // bytes per unpacked P stage
     static constexpr int UNP_Q = BN * KS;
     static constexpr int PK_P = BM * PKB;
     static constexpr int PK_Q = BN * PKB;
@@ -41,10 +45,11 @@ struct Layout {
     static constexpr int OFF_PP = OFF_UQ + SU * UNP_Q;
     static constexpr int OFF_PQ = OFF_PP + SP * PK_P;
     static constexpr int OFF_BAR = OFF_PQ + SP * PK_Q;
-    static constexpr int NBAR = 2 * SP + 2 * SU + 1;
+    static constexpr int NBAR = 2 * SP + 2 * SU + 4;
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr int BYTES = OFF_TMEM + 16;
-    static constexpr int ALLOC = BYTES + 1024;     // slack for 1024-byte alignment
+    static constexpr int ALLOC = BYTES + 1024;             // slack for 1024-byte alignment
+    static constexpr int TMEM_COLS = 2 * BN;               // double-buffered accumulator
 };
 
 DG_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -59,25 +64,44 @@ DG_DEV uint4 unpack16(uint32_t x, uint32_t L) {
     return make_uint4(prmt(L, L, X), prmt(L, L, X >> 16), prmt(L, L, Y), prmt(L, L, Y >> 16));
 }
 
+struct TileArgs {
+    int64_t np, nq;
+    int32_t nstages;       // K stages of 128 codes
+    int32_t last_ksteps;   // MMA k-steps (32 codes) issued in the last stage: 1..4
+    int32_t ntp, ntq;      // tiles along P and Q
+    uint32_t lp, lq;       // int8 level tables of P / Q codes (4 bytes)
+    int64_t corr;          // exact correction for codes in [K, K_mma): (K_mma-K)*pl[0]*ql[0]
+    void *D;
+    int64_t ldd;
+    int32_t has_rq;
+    int32_t fast_rq;       // requant with at most a bias: int32 threshold compares
+    int32_t thr[3];        // int32 thresholds on acc_raw + bias (K-pad correction folded in)
+    int32_t dir;
+};
+
+// Persistent warp-specialised kernel, one CTA per SM.
+//   warp 0: TMA producer   warp 1: MMA issuer   warps 2..9: unpack   warps 10..13: epilogue
 template <int BN>
 __global__ void __launch_bounds__(NT, 1)
 lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_q,
-                   int64_t np, int64_t nq, int32_t nstages, uint32_t lp, uint32_t lq, int64_t corr,
-                   void *__restrict__ D, int64_t ldd, RequantArgs rq, int has_rq) {
-    using Lt = Layout<BN>;
+                   const __grid_constant__ TileArgs ta,
+                   const __grid_constant__ RequantArgs rq) {
+    using C = Cfg<BN>;
+    constexpr int SP = C::SP, SU = C::SU;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = ptx::smem_u32(smem);
-    const uint32_t bar0 = sbase + Lt::OFF_BAR;
+    const uint32_t bar0 = sbase + C::OFF_BAR;
     auto full_p = [&](int s) { return bar0 + 8 * s; };
     auto empty_p = [&](int s) { return bar0 + 8 * (SP + s); };
     auto full_u = [&](int s) { return bar0 + 8 * (2 * SP + s); };
     auto empty_u = [&](int s) { return bar0 + 8 * (2 * SP + SU + s); };
-    const uint32_t acc_full = bar0 + 8 * (2 * SP + 2 * SU);
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + Lt::OFF_TMEM);
+    auto acc_full = [&](int a) { return bar0 + 8 * (2 * SP + 2 * SU + a); };
+    auto acc_empty = [&](int a) { return bar0 + 8 * (2 * SP + 2 * SU + 2 + a); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::OFF_TMEM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int64_t p0 = (int64_t)blockIdx.x * BM, q0 = (int64_t)blockIdx.y * BN;
+    const int ntiles = ta.ntp * ta.ntq;
 
     if (warp == 0) {
         if (lane == 0) {
@@ -85,17 +109,20 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             ptx::tma_prefetch(&tm_q);
             for (int s = 0; s < SP; ++s) {
                 ptx::mbar_init(full_p(s), 1);
-                ptx::mbar_init(empty_p(s), 4);
+                ptx::mbar_init(empty_p(s), NUM_UNPACK_WARPS);
             }
             for (int s = 0; s < SU; ++s) {
-                ptx::mbar_init(full_u(s), 4);
+                ptx::mbar_init(full_u(s), NUM_UNPACK_WARPS);
                 ptx::mbar_init(empty_u(s), 1);
             }
-            ptx::mbar_init(acc_full, 1);
+            for (int a = 0; a < 2; ++a) {
+                ptx::mbar_init(acc_full(a), 1);
+                ptx::mbar_init(acc_empty(a), NUM_EPI_WARPS);
+            }
             ptx::fence_mbar_init();
         }
         __syncwarp();
-        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), BN);   // BN int32 columns x 128 lanes
+        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), C::TMEM_COLS);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -103,107 +130,189 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- TMA producer
+        // ---------------- TMA producer: packed 2-bit tiles
         if (lane == 0) {
-            for (int s = 0; s < nstages; ++s) {
-                const int slot = s % SP;
-                const uint32_t ph = (uint32_t)(s / SP) & 1u;
-                ptx::mbar_wait(empty_p(slot), ph ^ 1u);
-                ptx::mbar_arrive_expect_tx(full_p(slot), Lt::PK_P + Lt::PK_Q);
-                ptx::tma_load_2d(sbase + Lt::OFF_PP + slot * Lt::PK_P, &tm_p, full_p(slot), s * PKB, (int32_t)p0);
-                ptx::tma_load_2d(sbase + Lt::OFF_PQ + slot * Lt::PK_Q, &tm_q, full_p(slot), s * PKB, (int32_t)q0);
+            uint32_t g = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int32_t yp = (t / ta.ntq) * BM, yq = (t % ta.ntq) * BN;
+                for (int s = 0; s < ta.nstages; ++s, ++g) {
+                    const int slot = g % SP;
+                    ptx::mbar_wait(empty_p(slot), ((g / SP) & 1u) ^ 1u);
+                    ptx::mbar_arrive_expect_tx(full_p(slot), C::PK_P + C::PK_Q);
+                    ptx::tma_load_2d(sbase + C::OFF_PP + slot * C::PK_P, &tm_p, full_p(slot), s * PKB, yp);
+                    ptx::tma_load_2d(sbase + C::OFF_PQ + slot * C::PK_Q, &tm_q, full_p(slot), s * PKB, yq);
+                }
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer
+        // ---------------- MMA issuer (single thread)
         if (lane == 0) {
             constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
-            for (int s = 0; s < nstages; ++s) {
-                const int slot = s % SU;
-                const uint32_t ph = (uint32_t)(s / SU) & 1u;
-                ptx::mbar_wait(full_u(slot), ph);
+            uint32_t g = 0, tl = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+                const uint32_t acc = tl & 1u;
+                ptx::mbar_wait(acc_empty(acc), ((tl >> 1) & 1u) ^ 1u);
                 ptx::tc_fence_after();
-                const uint32_t a = sbase + Lt::OFF_UP + slot * Lt::UNP_P;
-                const uint32_t b = sbase + Lt::OFF_UQ + slot * Lt::UNP_Q;
+                const uint32_t dt = tmem + acc * BN;
+                for (int s = 0; s < ta.nstages; ++s, ++g) {
+                    const int slot = g % SU;
+                    ptx::mbar_wait(full_u(slot), (g / SU) & 1u);
+                    ptx::tc_fence_after();
+                    const uint32_t a = sbase + C::OFF_UP + slot * C::UNP_P;
+                    const uint32_t b = sbase + C::OFF_UQ + slot * C::UNP_Q;
+                    const int ksteps = (s == ta.nstages - 1) ? ta.last_ksteps : KS / 32;
 #pragma unroll
-                for (int k = 0; k < KS / 32; ++k)
-                    ptx::mma_i8_ss(tmem, ptx::desc_k_sw128(a + 32 * k), ptx::desc_k_sw128(b + 32 * k), idesc,
-                                   (s > 0 || k > 0) ? 1u : 0u);
-                ptx::mma_commit(empty_u(slot));
+                    for (int k = 0; k < KS / 32; ++k)
+                        if (k < ksteps)
+                            ptx::mma_i8_ss(dt, ptx::desc_k_sw128(a + 32 * k), ptx::desc_k_sw128(b + 32 * k), idesc,
+                                           (s > 0 || k > 0) ? 1u : 0u);
+                    ptx::mma_commit(empty_u(slot));
+                }
+                ptx::mma_commit(acc_full(acc));
             }
-            ptx::mma_commit(acc_full);
+        }
+    } else if (warp < EPI_WARP0) {
+        // ---------------- unpackers: packed smem -> int8 levels in the SW128 K-major layout
+        const int ut = threadIdx.x - 32 * UNPACK_WARP0;
+        constexpr int NU = 32 * NUM_UNPACK_WARPS;
+        constexpr int ITEMS = (BM + BN) * 2;     // 16-byte packed chunks (64 codes) per stage
+        uint32_t g = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int s = 0; s < ta.nstages; ++s, ++g) {
+                const int sp = g % SP, su = g % SU;
+                // 16-byte chunk h covers MMA k-steps 2h, 2h+1: skip chunks no MMA reads
+                const int hmax = (s == ta.nstages - 1) ? (ta.last_ksteps + 1) / 2 : 2;
+                ptx::mbar_wait(full_p(sp), (g / SP) & 1u);
+                ptx::mbar_wait(empty_u(su), ((g / SU) & 1u) ^ 1u);
+                const uint8_t *pk_p = smem + C::OFF_PP + sp * C::PK_P;
+                const uint8_t *pk_q = smem + C::OFF_PQ + sp * C::PK_Q;
+                uint8_t *up = smem + C::OFF_UP + su * C::UNP_P;
+                uint8_t *uq = smem + C::OFF_UQ + su * C::UNP_Q;
+#pragma unroll
+                for (int it0 = 0; it0 < ITEMS; it0 += NU) {
+                    const int it = it0 + ut;
+                    if (it >= ITEMS) break;
+                    const int row = it >> 1, h = it & 1;
+                    if (h >= hmax) continue;
+                    const bool isp = row < BM;
+                    const int r = isp ? row : row - BM;
+                    const uint4 v = *reinterpret_cast<const uint4 *>((isp ? pk_p : pk_q) + r * PKB + h * 16);
+                    const uint32_t L = isp ? ta.lp : ta.lq;
+                    uint8_t *dst = (isp ? up : uq) + (r >> 3) * 1024 + (r & 7) * 128;
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const int chunk = (h * 4 + j) ^ (r & 7);
+                        *reinterpret_cast<uint4 *>(dst + chunk * 16) = unpack16(w[j], L);
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(empty_p(sp));
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(full_u(su));
+            }
         }
     } else {
-        // ---------------- unpackers (warps 2..5, 128 threads)
-        const int ut = threadIdx.x - 64;
-        constexpr int ITEMS = (BM + BN) * 2;   // 16-byte packed chunks per stage
-        for (int s = 0; s < nstages; ++s) {
-            const int sp = s % SP, su = s % SU;
-            ptx::mbar_wait(full_p(sp), (uint32_t)(s / SP) & 1u);
-            ptx::mbar_wait(empty_u(su), ((uint32_t)(s / SU) & 1u) ^ 1u);
-            const uint8_t *pk_p = smem + Lt::OFF_PP + sp * Lt::PK_P;
-            const uint8_t *pk_q = smem + Lt::OFF_PQ + sp * Lt::PK_Q;
-            uint8_t *up = smem + Lt::OFF_UP + su * Lt::UNP_P;
-            uint8_t *uq = smem + Lt::OFF_UQ + su * Lt::UNP_Q;
-#pragma unroll 2
-            for (int it = ut; it < ITEMS; it += 128) {
-                const int row = it >> 1, h = it & 1;
-                const bool isp = row < BM;
-                const int r = isp ? row : row - BM;
-                const uint4 v = *reinterpret_cast<const uint4 *>((isp ? pk_p : pk_q) + r * PKB + h * 16);
-                const uint32_t L = isp ? lp : lq;
-                uint8_t *dst = (isp ? up : uq) + (r >> 3) * 1024 + (r & 7) * 128;
-                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        // ---------------- epilogue: TMEM -> registers -> (requant) -> global
+        // 8 warps: lane quarter = warp % 4 (TMEM access rule), column half = (warp - EPI_WARP0) / 4
+        constexpr int HALF = BN / 2, NCH = HALF / 32;
+        const int quarter = warp & 3, half = (warp - EPI_WARP0) >> 2;
+        uint32_t tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const uint32_t acc = tl & 1u;
+            const int64_t p = (int64_t)(t / ta.ntq) * BM + quarter * 32 + lane;
+            const int64_t q0 = (int64_t)(t % ta.ntq) * BN + half * HALF;
+            ptx::mbar_wait(acc_full(acc), (tl >> 1) & 1u);
+            ptx::tc_fence_after();
+            const uint32_t trow = tmem + acc * BN + half * HALF + ((uint32_t)(quarter * 32) << 16);
+            uint32_t codes[NCH * 2];
+            uint32_t r[2][32];
+            ptx::tmem_ld_32x32b_x32(trow, r[0]);
 #pragma unroll
-                for (int j = 0; j < 4; ++j) {
-                    const int chunk = (h * 4 + j) ^ (r & 7);
-                    *reinterpret_cast<uint4 *>(dst + chunk * 16) = unpack16(w[j], L);
+            for (int c = 0; c < NCH; ++c) {
+                ptx::tmem_ld_wait();
+                if (c + 1 < NCH) ptx::tmem_ld_32x32b_x32(trow + (c + 1) * 32, r[(c + 1) & 1]);
+                const uint32_t(&rr)[32] = r[c & 1];
+                const int64_t qc = q0 + c * 32;
+                codes[2 * c] = codes[2 * c + 1] = 0;
+                if (p >= ta.np || qc >= ta.nq) continue;
+                if (ta.fast_rq && qc + 32 <= ta.nq) {
+                    // v = acc_raw + bias[col]; code = #thresholds passed (exact, see requant_thresholds)
+                    const bool col_bias = rq.bias && rq.bias_axis == 0;
+                    const int32_t rb = (rq.bias && rq.bias_axis == 1) ? __ldg(rq.bias + p) : 0;
+                    const int4 *b4 = reinterpret_cast<const int4 *>(rq.bias + qc);
+                    uint32_t o0 = 0, o1 = 0;
+#pragma unroll
+                    for (int j4 = 0; j4 < 8; ++j4) {
+                        const int4 bx = col_bias ? __ldg(b4 + j4) : make_int4(rb, rb, rb, rb);
+                        const int32_t bj[4] = {bx.x, bx.y, bx.z, bx.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const int j = 4 * j4 + i;
+                            const int32_t v = (int32_t)rr[j] + bj[i];
+                            uint32_t cd;
+                            if (ta.dir > 0)
+                                cd = (uint32_t)(v > ta.thr[0]) + (uint32_t)(v > ta.thr[1]) + (uint32_t)(v > ta.thr[2]);
+                            else
+                                cd = (uint32_t)(v <= ta.thr[0]) + (uint32_t)(v <= ta.thr[1]) + (uint32_t)(v <= ta.thr[2]);
+                            if (j < 16) o0 |= cd << (2 * j);
+                            else o1 |= cd << (2 * (j - 16));
+                        }
+                    }
+                    codes[2 * c] = o0;
+                    codes[2 * c + 1] = o1;
+                    continue;
+                }
+                int32_t v[32];
+#pragma unroll
+                for (int j = 0; j < 32; ++j) v[j] = (int32_t)rr[j] - (int32_t)ta.corr;
+                if (!ta.has_rq) {
+                    int32_t *dp = reinterpret_cast<int32_t *>(ta.D) + p * ta.ldd + qc;
+                    if (qc + 32 <= ta.nq && (ta.ldd & 3) == 0 && ((reinterpret_cast<uintptr_t>(ta.D) & 15) == 0)) {
+#pragma unroll
+                        for (int j = 0; j < 32; j += 4)
+                            *reinterpret_cast<int4 *>(dp + j) = make_int4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    } else {
+                        for (int j = 0; j < 32; ++j)
+                            if (qc + j < ta.nq) dp[j] = v[j];
+                    }
+                } else if (qc + 32 <= ta.nq) {
+                    const uint2 o = requant_row32(rq, v, p, qc);
+                    codes[2 * c] = o.x;
+                    codes[2 * c + 1] = o.y;
+                } else {
+                    uint32_t o0 = 0, o1 = 0;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        if (qc + j < ta.nq) {
+                            const uint32_t cd = requant_one(rq, v[j], p, qc + j);
+                            if (j < 16) o0 |= cd << (2 * j);
+                            else o1 |= cd << (2 * (j - 16));
+                        }
+                    }
+                    codes[2 * c] = o0;
+                    codes[2 * c + 1] = o1;
                 }
             }
+            ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(empty_p(sp));
-            ptx::fence_proxy_async_smem();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(full_u(su));
-        }
-
-        // ---------------- epilogue: TMEM -> registers -> global
-        ptx::mbar_wait(acc_full, 0);
-        ptx::tc_fence_after();
-        const int quarter = warp & 3;
-        const int64_t p = p0 + quarter * 32 + lane;
-        const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
-#pragma unroll 1
-        for (int c = 0; c < BN / 32; ++c) {
-            uint32_t r[32];
-            ptx::tmem_ld_32x32b_x32(trow + c * 32, r);
-            ptx::tmem_ld_wait();
-            const int64_t qc = q0 + c * 32;
-            if (p >= np || qc >= nq) continue;
-            int32_t v[32];
+            if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
+            if (ta.has_rq && p < ta.np && q0 < ta.nq) {
+                uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (q0 >> 2);
+                const int64_t nbytes = ((ta.nq - q0 < HALF ? ta.nq - q0 : HALF) + 3) / 4;
+                if (nbytes == HALF / 4 && ((reinterpret_cast<uintptr_t>(dp) & 15) == 0)) {
 #pragma unroll
-            for (int j = 0; j < 32; ++j) v[j] = (int32_t)((int64_t)(int32_t)r[j] - corr);
-            if (!has_rq) {
-                int32_t *dp = reinterpret_cast<int32_t *>(D) + p * ldd + qc;
-                if (qc + 32 <= nq && (ldd & 3) == 0 && ((reinterpret_cast<uintptr_t>(D) & 15) == 0)) {
-#pragma unroll
-                    for (int j = 0; j < 32; j += 4)
-                        *reinterpret_cast<int4 *>(dp + j) = make_int4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+                    for (int i = 0; i < HALF / 64; ++i)
+                        *reinterpret_cast<uint4 *>(dp + 16 * i) =
+                            make_uint4(codes[4 * i], codes[4 * i + 1], codes[4 * i + 2], codes[4 * i + 3]);
+                    if constexpr (HALF % 64 != 0)
+                        *reinterpret_cast<uint2 *>(dp + (HALF / 64) * 16) =
+                            make_uint2(codes[NCH * 2 - 2], codes[NCH * 2 - 1]);
                 } else {
-                    for (int j = 0; j < 32; ++j)
-                        if (qc + j < nq) dp[j] = v[j];
-                }
-            } else {
-                uint32_t o[2] = {0, 0};
 #pragma unroll
-                for (int j = 0; j < 32; ++j)
-                    if (qc + j < nq) o[j >> 4] |= requant_one(rq, v[j], p, qc + j) << (2 * (j & 15));
-                uint8_t *dp = reinterpret_cast<uint8_t *>(D) + p * ldd + (qc >> 2);
-                const int nbytes = (int)((nq - qc) >= 32 ? 8 : ((nq - qc) + 3) / 4);
-                if (nbytes == 8 && ((reinterpret_cast<uintptr_t>(dp) & 7) == 0)) {
-                    *reinterpret_cast<uint2 *>(dp) = make_uint2(o[0], o[1]);
-                } else {
-                    for (int b = 0; b < nbytes; ++b) dp[b] = (uint8_t)(o[b >> 2] >> (8 * (b & 3)));
+                    for (int b = 0; b < HALF / 4; ++b)
+                        if (b < nbytes) dp[b] = (uint8_t)(codes[b >> 2] >> (8 * (b & 3)));
                 }
             }
         }
@@ -211,7 +320,7 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 0) ptx::tmem_dealloc(tmem, BN);
+    if (warp == 0) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
 // ---------------------------------------------------------------- host
@@ -257,22 +366,46 @@ dg_status launch(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t ldq, i
                  cudaStream_t st) {
     CUtensorMap mp, mq;
     if (!make_map(&mp, P, ldp, np, BM) || !make_map(&mq, Q, ldq, nq, BN)) return DG_ERR_CUDA;
-    const int32_t nstages = (int32_t)((K + KS - 1) / KS);
-    const int64_t Kp = (int64_t)nstages * KS;
-    const int64_t corr = (Kp - K) * (int64_t)pl[0] * (int64_t)ql[0];
+    TileArgs ta{};
+    ta.np = np;
+    ta.nq = nq;
+    ta.nstages = (int32_t)((K + KS - 1) / KS);
+    const int64_t kmma = (K + 31) / 32 * 32;
+    ta.last_ksteps = (int32_t)((kmma - (int64_t)(ta.nstages - 1) * KS) / 32);
+    ta.ntp = (int32_t)((np + BM - 1) / BM);
+    ta.ntq = (int32_t)((nq + BN - 1) / BN);
+    ta.lp = pack_levels(pl);
+    ta.lq = pack_levels(ql);
+    ta.corr = (kmma - K) * (int64_t)pl[0] * (int64_t)ql[0];
+    ta.D = D;
+    ta.ldd = ldd;
+    ta.has_rq = rq ? 1 : 0;
+    ta.fast_rq = 0;
+    if (rq && !rq->res && !rq->res_codes &&
+        (!rq->bias || rq->bias_axis == 1 || (((uintptr_t)rq->bias) & 15) == 0)) {
+        // x = acc_raw + bias with acc_raw = acc + corr:  acc + bias >= t  <=>  x > t + corr - 1
+        ta.fast_rq = 1;
+        ta.dir = rq->dir;
+        for (int j = 0; j < 3; ++j) {
+            const int64_t t = rq->thr[j];
+            int64_t u;
+            if (t == INT64_MAX || t == INT64_MIN) u = t;   // never / always sentinels
+            else u = rq->dir > 0 ? t + ta.corr - 1 : t + ta.corr;
+            ta.thr[j] = (int32_t)(u > INT32_MAX ? INT32_MAX : (u < INT32_MIN ? INT32_MIN : u));
+        }
+    }
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(lut_gemm_tc_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 Layout<BN>::ALLOC) != cudaSuccess)
+                                 Cfg<BN>::ALLOC) != cudaSuccess)
             return DG_ERR_CUDA;
         attr_set = true;
     }
     RequantArgs dummy{};
-    dim3 grid((unsigned)((np + BM - 1) / BM), (unsigned)((nq + BN - 1) / BN));
-    if (grid.y > 65535) return DG_ERR_SHAPE;
-    lut_gemm_tc_kernel<BN><<<grid, NT, Layout<BN>::ALLOC, st>>>(mp, mq, np, nq, nstages, pack_levels(pl),
-                                                                 pack_levels(ql), corr, D, ldd,
-                                                                 rq ? *rq : dummy, rq ? 1 : 0);
+    const int64_t ntiles = (int64_t)ta.ntp * ta.ntq;
+    if (ntiles > INT32_MAX) return DG_ERR_SHAPE;
+    const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
+    lut_gemm_tc_kernel<BN><<<grid, NT, Cfg<BN>::ALLOC, st>>>(mp, mq, ta, rq ? *rq : dummy);
     return launch_status();
 }
 

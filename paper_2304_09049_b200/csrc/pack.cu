@@ -146,7 +146,8 @@ __global__ void im2col_kernel(const uint8_t *__restrict__ x, int32_t B, int32_t 
 
 // ---- S7 standalone: one thread per output byte (4 columns).
 __global__ void requant_kernel(const int32_t *__restrict__ acc, int64_t rows, int64_t cols,
-                               int64_t ld_acc, RequantArgs q, uint8_t *__restrict__ out, int64_t ld_out) {
+                               int64_t ld_acc, const __grid_constant__ RequantArgs q, uint8_t *__restrict__ out,
+                               int64_t ld_out) {
     const int64_t bytes_per_row = (cols + 3) / 4;
     const int64_t total = rows * bytes_per_row;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
@@ -251,6 +252,11 @@ dg_status dg_requantize(const int32_t *d_acc, int64_t rows, int64_t cols, int64_
     if (rows < 0 || cols <= 0 || ld_acc < cols || ld_out * 4 < cols) return DG_ERR_SHAPE;
     if (rq->qmax < rq->qmin || rq->qmax - rq->qmin > 3 || rq->shift < 0 || rq->shift > 62)
         return DG_ERR_RANGE;
+    if (rq->d_res_codes)
+        for (int i = 0; i < 4; ++i) {
+            const int64_t r = (int64_t)rq->res_levels[i] * rq->res_mult;
+            if (r > INT32_MAX || r < INT32_MIN) return DG_ERR_RANGE;
+        }
     if (rows == 0) return DG_OK;
     RequantArgs a = to_args(rq);
     requant_kernel<<<grid_for(rows * ((cols + 3) / 4)), kThreads, 0, (cudaStream_t)stream>>>(

@@ -1,0 +1,161 @@
+"""Layer-by-layer runner for the conv workloads (BASELINE configs 3 and 4) on one GPU.
+
+Builds every layer's packed weights, packed NHWC input codes, requant parameters and
+output buffers in HBM, then runs one *step* = every LUT conv of the network over the
+local batch shard (reading Q16: per-layer independent inputs).  Each layer is
+im2col (S3, when the layer is not a plain 1x1/stride-1 conv) -> LUT GEMM with the
+fused requant epilogue (S5-S7), issued through the C ABI (dg_im2col, dg_lut_gemm), or
+through dg_lut_conv2d for the user-level path.
+
+Inputs are drawn with synth.counter_codes (the same counter-based generator the oracle
+side uses), indexed by global image id, so any shard of images is reproducible.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import dg
+
+
+def _synth():
+    import synth  # seeded input generators (no method arithmetic), repo root
+    return synth
+
+
+@dataclass
+class LayerPlan:
+    name: str
+    layer: object
+    params: object
+    lut: object            # product table, index (w<<2)|a (dg_lut_conv2d orientation)
+    lut_t: object          # transposed table, index (a<<2)|w (dg_lut_gemm with P = pixels)
+    rq: object
+    w: torch.Tensor        # packed weights [Cout][ldw]
+    x: torch.Tensor        # packed NHWC input [B*H*W][Cp/4]
+    out: torch.Tensor      # packed NHWC output codes [B*Ho*Wo][Cout/4]
+    rows: int              # B*Ho*Wo  (GEMM rows on the P side)
+    K: int                 # computed reduction length (padded channels)
+    direct: bool           # 1x1 / stride 1 / unpadded: the input is its own im2col matrix
+    ops: int               # algorithmic 2*M*N*K with the unpadded K
+
+    @property
+    def cols_ld(self) -> int:
+        return dg.packed_ld(self.K)
+
+
+def input_codes(cfg: int, li: int, layer, images, device):
+    """NHWC codes [len(images)][h][h][cin] of layer li for global image ids `images`
+    (contiguous ids), drawn with the counter generator."""
+    s = _synth()
+    per = layer.h * layer.h * layer.cin
+    b0 = int(images[0])
+    n = len(images)
+    c = s.counter_codes(b0 * per, n * per, (cfg, li, s.T_X), "relu", device)
+    return c.view(n, layer.h, layer.h, layer.cin)
+
+
+def weight_codes(cfg: int, li: int, layer, device):
+    s = _synth()
+    n = layer.cout * layer.k * layer.k * layer.cin
+    return s.counter_codes(0, n, (cfg, li, s.T_W), "uniform", device).view(layer.cout, layer.k, layer.k, layer.cin)
+
+
+def pack_nhwc(codes: torch.Tensor) -> torch.Tensor:
+    """[B][H][W][C] codes -> packed NHWC [B*H*W][Cp/4] (Cp = roundup(C,4); pad channels code 0)."""
+    B, H, W, C = codes.shape
+    Cp = (C + 3) // 4 * 4
+    flat = codes.reshape(-1, C)
+    if Cp != C:
+        z = torch.zeros((flat.shape[0], Cp), dtype=torch.uint8, device=codes.device)
+        z[:, :C] = flat
+        flat = z
+    packed = dg.pack_codes(flat.contiguous())
+    if packed.shape[1] != Cp // 4:
+        packed = packed[:, :Cp // 4].contiguous()
+    return packed
+
+
+def pack_conv_weights(w: torch.Tensor, wpad_code: int = 2) -> torch.Tensor:
+    """[Cout][k][k][C] -> packed [Cout][ldw] over K = k*k*Cp; pad channels get a zero-level code."""
+    Cout, kh, kw, C = w.shape
+    Cp = (C + 3) // 4 * 4
+    if Cp != C:
+        z = torch.full((Cout, kh, kw, Cp), wpad_code, dtype=torch.uint8, device=w.device)
+        z[..., :C] = w
+        w = z
+    return dg.pack_weights(w.reshape(Cout, -1).contiguous())
+
+
+class NetRunner:
+    def __init__(self, cfg: int, images, device="cuda", variant="auto", layers=None):
+        s = _synth()
+        self.cfg = cfg
+        self.images = list(images)
+        self.B = len(self.images)
+        self.device = device
+        self.variant = variant
+        all_layers = s.CONFIG_LAYERS[cfg]()
+        self.layer_ids = list(range(len(all_layers))) if layers is None else list(layers)
+        wl, al = s.WL_UNIFORM, s.AL_UNIFORM
+        lut = dg.build_lut(wl, al, 8)
+        lut_t = dg.build_lut(al, wl, 8)
+        self.plans: list[LayerPlan] = []
+        ws_need = 0
+        for li in self.layer_ids:
+            L = all_layers[li]
+            Cp = (L.cin + 3) // 4 * 4
+            K = L.k * L.k * Cp
+            wq = pack_conv_weights(weight_codes(cfg, li, L, device))
+            xq = pack_nhwc(input_codes(cfg, li, L, self.images, device))
+            params = dg.conv_params(self.B, L.h, L.h, Cp, L.cout, L.k, L.k, L.stride, L.pad, 0, ldw=wq.shape[1])
+            rows = self.B * L.ho * L.ho
+            r = s.conv_requant(L)
+            bias = torch.full((L.cout,), r.bias, dtype=torch.int32, device=device)
+            rq = dg.Requant(r.mult, r.shift, r.zp, r.qmin, r.qmax, bias=bias, bias_axis=0)
+            out = torch.empty((rows, L.cout // 4), dtype=torch.uint8, device=device)
+            direct = L.k == 1 and L.stride == 1 and L.pad == 0 and (Cp // 4) % 16 == 0
+            plan = LayerPlan(L.name, L, params, lut, lut_t, rq, wq, xq, out, rows, K, direct,
+                             2 * L.cout * rows * L.k * L.k * L.cin)
+            if not direct:
+                ws_need = max(ws_need, rows * plan.cols_ld)
+            self.plans.append(plan)
+        self.ws = torch.empty(max(ws_need, 16), dtype=torch.uint8, device=device)
+        self.total_ops = sum(p.ops for p in self.plans)
+
+    # -- the step, split into C-ABI calls so the GEMM launches can be bracketed by events
+    def step(self, gemm_events=None, stream=None):
+        n = 0
+        for i, p in enumerate(self.plans):
+            L = p.layer
+            if p.direct:
+                P = p.x
+            else:
+                ld = p.cols_ld
+                P = self.ws[: p.rows * ld].view(p.rows, ld)
+                dg.im2col(p.x, self.B, L.h, L.h, p.params.C, L.k, L.k, L.stride, L.pad, 0, out=P, stream=stream)
+                n += 1
+            if gemm_events is not None:
+                gemm_events[i][0].record()
+            dg.lut_gemm(P, p.w, p.rows, L.cout, p.K, p.lut_t, rq=p.rq, variant=self.variant, out=p.out,
+                        stream=stream)
+            if gemm_events is not None:
+                gemm_events[i][1].record()
+            n += 1
+        return n  # kernel launches issued
+
+    # -- the user-level path: one dg_lut_conv2d per layer
+    def step_conv2d(self, stream=None):
+        for p in self.plans:
+            dg.lut_conv2d(p.x, p.w, p.lut, p.params, rq=p.rq, variant=self.variant, out=p.out, ws=self.ws,
+                          stream=stream)
+
+    def input_bytes(self) -> int:
+        return sum(p.x.numel() for p in self.plans)
+
+    def output_bytes(self) -> int:
+        return sum(p.out.numel() for p in self.plans)
+
+    def weight_bytes(self) -> int:
+        return sum(p.w.numel() for p in self.plans)

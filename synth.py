@@ -202,3 +202,58 @@ def conv_input_codes(cfg: int, li: int, layer: ConvLayer, images) -> np.ndarray:
 def conv_weight_codes(cfg: int, li: int, layer: ConvLayer) -> np.ndarray:
     """[cout][k][k][cin] codes, uniform."""
     return uniform_codes((layer.cout, layer.k, layer.k, layer.cin), cfg, li, T_W)
+
+
+# ---------------------------------------------------------------------------
+# Counter-based generator for the large workloads (configs 2-5).  Implemented once in
+# torch integer ops, so the SAME code produces identical codes on CPU (oracle side,
+# for sampled images) and on the GPU (bench inputs): code[i] = f(hash(key, i)).
+# splitmix64 finaliser with logical shifts emulated on int64.
+
+_M64 = (1 << 64) - 1
+
+
+def _s64(v: int) -> int:
+    v &= _M64
+    return v - (1 << 64) if v >= (1 << 63) else v
+
+
+_GOLD = _s64(0x9E3779B97F4A7C15)
+_MIX1 = _s64(0xBF58476D1CE4E5B9)
+_MIX2 = _s64(0x94D049BB133111EB)
+
+
+def _key64(key) -> int:
+    h = MASTER_SEED
+    for k in key:
+        h = (h * 0x100000001B3 + int(k) + 0x9E37) & _M64
+        h ^= h >> 29
+    return _s64(h)
+
+
+def _lsr(t, s: int):
+    import torch
+    return (t >> s) & ((1 << (64 - s)) - 1)
+
+
+def counter_hash(start: int, count: int, key, device="cpu"):
+    """64-bit hashes of element indices [start, start+count) under `key` (int64 tensor)."""
+    import torch
+    idx = torch.arange(start, start + count, dtype=torch.int64, device=device)
+    z = idx * _GOLD + _key64(key)
+    z = (z ^ _lsr(z, 30)) * _MIX1
+    z = (z ^ _lsr(z, 27)) * _MIX2
+    return z ^ _lsr(z, 31)
+
+
+def counter_codes(start: int, count: int, key, dist: str = "uniform", device="cpu"):
+    """uint8 codes for flat element indices [start, start+count).
+    dist 'uniform': U{0..3};  'relu': P(0)=1/2, else U{1,2,3} (up to 2^-31 bias)."""
+    import torch
+    z = counter_hash(start, count, key, device)
+    r = z & 0xFFFFFFFF
+    if dist == "uniform":
+        return (r & 3).to(torch.uint8)
+    half = 1 << 31
+    nz = 1 + (((r - half).clamp(min=0) * 3) >> 31)
+    return torch.where(r < half, torch.zeros_like(r), nz).to(torch.uint8)
