@@ -79,6 +79,54 @@ struct TileArgs {
     int32_t dir;
 };
 
+DG_DEV void store_codes32(uint8_t *dp, uint32_t o0, uint32_t o1, int nbytes) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+        if (b < nbytes) dp[b] = (uint8_t)((b < 4 ? o0 : o1) >> (8 * (b & 3)));
+}
+
+// Epilogue for one 32-column chunk of row p: int32 output, or requant with residuals /
+// partial chunks.  Kept out of line so the hot requant loop stays small in the I-cache.
+__device__ __noinline__ void epilogue_general(const TileArgs &ta, const RequantArgs &rq, uint32_t taddr,
+                                              int64_t p, int64_t qc) {
+    uint32_t rr[32];
+    ptx::tmem_ld_32x32b_x32(taddr, rr);
+    ptx::tmem_ld_wait();
+    if (p >= ta.np || qc >= ta.nq) return;
+    int32_t v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = (int32_t)rr[j] - (int32_t)ta.corr;
+    if (!ta.has_rq) {
+        int32_t *dp = reinterpret_cast<int32_t *>(ta.D) + p * ta.ldd + qc;
+        if (qc + 32 <= ta.nq && (ta.ldd & 3) == 0 && ((reinterpret_cast<uintptr_t>(ta.D) & 15) == 0)) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                *reinterpret_cast<int4 *>(dp + j) = make_int4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+            for (int j = 0; j < 32; ++j)
+                if (qc + j < ta.nq) dp[j] = v[j];
+        }
+        return;
+    }
+    uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
+    if (qc + 32 <= ta.nq) {
+        const uint2 o = requant_row32(rq, v, p, qc);
+        if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = o;
+        else store_codes32(dp, o.x, o.y, 8);
+        return;
+    }
+    uint32_t o0 = 0, o1 = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        if (qc + j < ta.nq) {
+            const uint32_t cd = requant_one(rq, v[j], p, qc + j);
+            if (j < 16) o0 |= cd << (2 * j);
+            else o1 |= cd << (2 * (j - 16));
+        }
+    }
+    store_codes32(dp, o0, o1, (int)((ta.nq - qc + 3) / 4));
+}
+
 // Persistent warp-specialised kernel, one CTA per SM.
 //   warp 0: TMA producer   warp 1: MMA issuer   warps 2..9: unpack   warps 10..13: epilogue
 template <int BN>
@@ -218,6 +266,7 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         // 8 warps: lane quarter = warp % 4 (TMEM access rule), column half = (warp - EPI_WARP0) / 4
         constexpr int HALF = BN / 2, NCH = HALF / 32;
         const int quarter = warp & 3, half = (warp - EPI_WARP0) >> 2;
+        const bool col_bias = rq.bias && rq.bias_axis == 0;
         uint32_t tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl & 1u;
@@ -226,95 +275,60 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             ptx::mbar_wait(acc_full(acc), (tl >> 1) & 1u);
             ptx::tc_fence_after();
             const uint32_t trow = tmem + acc * BN + half * HALF + ((uint32_t)(quarter * 32) << 16);
-            uint32_t codes[NCH * 2];
-            uint32_t r[2][32];
-            ptx::tmem_ld_32x32b_x32(trow, r[0]);
+            const bool fast = ta.fast_rq && q0 + HALF <= ta.nq;
+            const int32_t rb = (fast && rq.bias && rq.bias_axis == 1 && p < ta.np) ? __ldg(rq.bias + p) : 0;
+            if (!fast) {
+                // int32 output / residual requant / ragged tail: out of line, reloads TMEM itself
+#pragma unroll 1
+                for (int c = 0; c < NCH; ++c) epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
+            } else {
+                uint32_t r[2][32];
+                ptx::tmem_ld_32x32b_x32(trow, r[0]);
 #pragma unroll
-            for (int c = 0; c < NCH; ++c) {
-                ptx::tmem_ld_wait();
-                if (c + 1 < NCH) ptx::tmem_ld_32x32b_x32(trow + (c + 1) * 32, r[(c + 1) & 1]);
-                const uint32_t(&rr)[32] = r[c & 1];
-                const int64_t qc = q0 + c * 32;
-                codes[2 * c] = codes[2 * c + 1] = 0;
-                if (p >= ta.np || qc >= ta.nq) continue;
-                if (ta.fast_rq && qc + 32 <= ta.nq) {
-                    // v = acc_raw + bias[col]; code = #thresholds passed (exact, see requant_thresholds)
-                    const bool col_bias = rq.bias && rq.bias_axis == 0;
-                    const int32_t rb = (rq.bias && rq.bias_axis == 1) ? __ldg(rq.bias + p) : 0;
-                    const int4 *b4 = reinterpret_cast<const int4 *>(rq.bias + qc);
+                for (int c = 0; c < NCH; ++c) {
+                    const int64_t qc = q0 + c * 32;
+                    int4 bx[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)   // warp-uniform bias loads, issued before the TMEM wait
+                        bx[j] = col_bias ? __ldg(reinterpret_cast<const int4 *>(rq.bias + qc) + j) : make_int4(rb, rb, rb, rb);
+                    ptx::tmem_ld_wait();
+                    if (c + 1 < NCH) ptx::tmem_ld_32x32b_x32(trow + (c + 1) * 32, r[(c + 1) & 1]);
+                    if (p >= ta.np) continue;
+                    // v = acc_raw + bias; code = number of exact thresholds passed, counted from
+                    // sign bits: (t - v) < 0 <=> v > t  (|t|, |v| < 2^30: no overflow)
                     uint32_t o0 = 0, o1 = 0;
+                    if (ta.dir > 0) {
 #pragma unroll
-                    for (int j4 = 0; j4 < 8; ++j4) {
-                        const int4 bx = col_bias ? __ldg(b4 + j4) : make_int4(rb, rb, rb, rb);
-                        const int32_t bj[4] = {bx.x, bx.y, bx.z, bx.w};
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const int j = 4 * j4 + i;
-                            const int32_t v = (int32_t)rr[j] + bj[i];
-                            uint32_t cd;
-                            if (ta.dir > 0)
-                                cd = (uint32_t)(v > ta.thr[0]) + (uint32_t)(v > ta.thr[1]) + (uint32_t)(v > ta.thr[2]);
-                            else
-                                cd = (uint32_t)(v <= ta.thr[0]) + (uint32_t)(v <= ta.thr[1]) + (uint32_t)(v <= ta.thr[2]);
-                            if (j < 16) o0 |= cd << (2 * j);
-                            else o1 |= cd << (2 * (j - 16));
+                        for (int j = 0; j < 32; ++j) {
+                            const int4 b4 = bx[j >> 2];
+                            const int32_t b = (j & 3) == 0 ? b4.x : (j & 3) == 1 ? b4.y : (j & 3) == 2 ? b4.z : b4.w;
+                            const int32_t v = (int32_t)r[c & 1][j];
+                            const uint32_t cd = ((uint32_t)(ta.thr[0] - v - b) >> 31) + ((uint32_t)(ta.thr[1] - v - b) >> 31) +
+                                                ((uint32_t)(ta.thr[2] - v - b) >> 31);
+                            if (j < 16) o0 += cd << (2 * j);
+                            else o1 += cd << (2 * (j - 16));
                         }
-                    }
-                    codes[2 * c] = o0;
-                    codes[2 * c + 1] = o1;
-                    continue;
-                }
-                int32_t v[32];
-#pragma unroll
-                for (int j = 0; j < 32; ++j) v[j] = (int32_t)rr[j] - (int32_t)ta.corr;
-                if (!ta.has_rq) {
-                    int32_t *dp = reinterpret_cast<int32_t *>(ta.D) + p * ta.ldd + qc;
-                    if (qc + 32 <= ta.nq && (ta.ldd & 3) == 0 && ((reinterpret_cast<uintptr_t>(ta.D) & 15) == 0)) {
-#pragma unroll
-                        for (int j = 0; j < 32; j += 4)
-                            *reinterpret_cast<int4 *>(dp + j) = make_int4(v[j], v[j + 1], v[j + 2], v[j + 3]);
                     } else {
-                        for (int j = 0; j < 32; ++j)
-                            if (qc + j < ta.nq) dp[j] = v[j];
-                    }
-                } else if (qc + 32 <= ta.nq) {
-                    const uint2 o = requant_row32(rq, v, p, qc);
-                    codes[2 * c] = o.x;
-                    codes[2 * c + 1] = o.y;
-                } else {
-                    uint32_t o0 = 0, o1 = 0;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        if (qc + j < ta.nq) {
-                            const uint32_t cd = requant_one(rq, v[j], p, qc + j);
-                            if (j < 16) o0 |= cd << (2 * j);
-                            else o1 |= cd << (2 * (j - 16));
+                        for (int j = 0; j < 32; ++j) {
+                            const int4 b4 = bx[j >> 2];
+                            const int32_t b = (j & 3) == 0 ? b4.x : (j & 3) == 1 ? b4.y : (j & 3) == 2 ? b4.z : b4.w;
+                            const int32_t v = (int32_t)r[c & 1][j];
+                            const uint32_t cd = ((uint32_t)(v + b - ta.thr[0] - 1) >> 31) +
+                                                ((uint32_t)(v + b - ta.thr[1] - 1) >> 31) +
+                                                ((uint32_t)(v + b - ta.thr[2] - 1) >> 31);
+                            if (j < 16) o0 += cd << (2 * j);
+                            else o1 += cd << (2 * (j - 16));
                         }
                     }
-                    codes[2 * c] = o0;
-                    codes[2 * c + 1] = o1;
+                    uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
+                    if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = make_uint2(o0, o1);
+                    else store_codes32(dp, o0, o1, 8);
                 }
             }
             ptx::tc_fence_before();
             __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
-            if (ta.has_rq && p < ta.np && q0 < ta.nq) {
-                uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (q0 >> 2);
-                const int64_t nbytes = ((ta.nq - q0 < HALF ? ta.nq - q0 : HALF) + 3) / 4;
-                if (nbytes == HALF / 4 && ((reinterpret_cast<uintptr_t>(dp) & 15) == 0)) {
-#pragma unroll
-                    for (int i = 0; i < HALF / 64; ++i)
-                        *reinterpret_cast<uint4 *>(dp + 16 * i) =
-                            make_uint4(codes[4 * i], codes[4 * i + 1], codes[4 * i + 2], codes[4 * i + 3]);
-                    if constexpr (HALF % 64 != 0)
-                        *reinterpret_cast<uint2 *>(dp + (HALF / 64) * 16) =
-                            make_uint2(codes[NCH * 2 - 2], codes[NCH * 2 - 1]);
-                } else {
-#pragma unroll
-                    for (int b = 0; b < HALF / 4; ++b)
-                        if (b < nbytes) dp[b] = (uint8_t)(codes[b >> 2] >> (8 * (b & 3)));
-                }
-            }
+            if (lane == 0) ptx::mbar_arrive(acc_empty(acc));   // accumulator buffer drained
         }
     }
 
@@ -364,6 +378,13 @@ template <int BN>
 dg_status launch(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t ldq, int64_t np, int64_t nq, int64_t K,
                  const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                  cudaStream_t st) {
+    int64_t acc_bound = 0;   // K * max |pl[a] * ql[b]|
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+            const int64_t e = (int64_t)pl[a] * ql[b];
+            acc_bound = (e < 0 ? -e : e) > acc_bound ? (e < 0 ? -e : e) : acc_bound;
+        }
+    acc_bound *= K;
     CUtensorMap mp, mq;
     if (!make_map(&mp, P, ldp, np, BM) || !make_map(&mq, Q, ldq, nq, BN)) return DG_ERR_CUDA;
     TileArgs ta{};
@@ -381,7 +402,7 @@ dg_status launch(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t ldq, i
     ta.ldd = ldd;
     ta.has_rq = rq ? 1 : 0;
     ta.fast_rq = 0;
-    if (rq && !rq->res && !rq->res_codes &&
+    if (rq && !rq->res && !rq->res_codes && acc_bound < ((int64_t)1 << 29) &&
         (!rq->bias || rq->bias_axis == 1 || (((uintptr_t)rq->bias) & 15) == 0)) {
         // x = acc_raw + bias with acc_raw = acc + corr:  acc + bias >= t  <=>  x > t + corr - 1
         ta.fast_rq = 1;
@@ -391,7 +412,8 @@ dg_status launch(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t ldq, i
             int64_t u;
             if (t == INT64_MAX || t == INT64_MIN) u = t;   // never / always sentinels
             else u = rq->dir > 0 ? t + ta.corr - 1 : t + ta.corr;
-            ta.thr[j] = (int32_t)(u > INT32_MAX ? INT32_MAX : (u < INT32_MIN ? INT32_MIN : u));
+            const int64_t LIM = (int64_t)1 << 30;          // |acc + bias| < 2^30 (dg.h)
+            ta.thr[j] = (int32_t)(u > LIM ? LIM : (u < -LIM ? -LIM : u));
         }
     }
     static bool attr_set = false;
