@@ -16,6 +16,7 @@
 // The PRMT unpack emits the 16 codes of a 32-bit word in the order 0,2,4,6,8,..,1,3,..; the
 // same permutation is applied to both operands, so the dot product is unchanged.
 #include <cuda.h>
+#include <string.h>
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
@@ -24,9 +25,12 @@ namespace dg {
 namespace {
 
 constexpr int BM = 128;        // TMEM lanes / P rows per tile
-constexpr int KS = 128;        // codes per pipeline stage (one 128-byte SW128 row of int8)
-constexpr int PKB = KS / 4;    // packed bytes per row per stage
-constexpr int NUM_UNPACK_WARPS = 4;
+constexpr int KS = 128;        // codes per unpacked stage (one 128-byte SW128 row of int8)
+constexpr int PKB = KS / 4;    // packed bytes per row per unpacked stage
+constexpr int PKS_MAX = 128;   // packed bytes per row per packed (TMA / bulk) stage: up to 4 unpacked stages
+constexpr int NUM_UNPACK_WARPS = 6;
+constexpr int NUM_UGROUPS = 2;         // unpack groups own alternate stages (in order within a group)
+constexpr int UGROUP_WARPS = NUM_UNPACK_WARPS / NUM_UGROUPS;
 constexpr int NUM_EPI_WARPS = 8;       // 2 per TMEM lane quarter, each owning half the columns
 constexpr int UNPACK_WARP0 = 2;
 constexpr int EPI_WARP0 = UNPACK_WARP0 + NUM_UNPACK_WARPS;
@@ -34,22 +38,25 @@ constexpr int NT = 32 * (EPI_WARP0 + NUM_EPI_WARPS);   // 448 threads
 
 template <int BN>
 struct Cfg {
-    static constexpr int SU = BN == 64 ? 4 : 3;            // unpacked (int8) ring depth
-    static constexpr int SP = BN == 256 ? 4 : (BN == 128 ? 6 : 8);  // packed ring depth
+    // Ring depths are multiples of NUM_UGROUPS so that a group, which consumes its stages in
+    // order, can never run a full phase ahead on a slot (mbarrier parity aliasing).
+    static constexpr int SU = BN == 256 ? 2 : 4;            // unpacked (int8) ring depth
+    static constexpr int SP = BN == 256 ? 2 : (BN == 128 ? 2 : 4);  // packed ring depth (128 B/row stages)
     static constexpr int UNP_P = BM * KS;                  // bytes per unpacked P stage
     static constexpr int UNP_Q = BN * KS;
-    static constexpr int PK_P = BM * PKB;
-    static constexpr int PK_Q = BN * PKB;
+    static constexpr int PK_P = BM * PKS_MAX;
+    static constexpr int PK_Q = BN * PKS_MAX;
     static constexpr int OFF_UP = 0;
     static constexpr int OFF_UQ = OFF_UP + SU * UNP_P;
     static constexpr int OFF_PP = OFF_UQ + SU * UNP_Q;
     static constexpr int OFF_PQ = OFF_PP + SP * PK_P;
     static constexpr int OFF_BAR = OFF_PQ + SP * PK_Q;
-    static constexpr int NBAR = 2 * SP + 2 * SU + 4;
+    static constexpr int NACC = BN == 256 ? 2 : 4;          // TMEM accumulator buffers
+    static constexpr int NBAR = 2 * SP + 2 * SU + 2 * NACC;
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr int BYTES = OFF_TMEM + 16;
     static constexpr int ALLOC = BYTES + 1024;             // slack for 1024-byte alignment
-    static constexpr int TMEM_COLS = 2 * BN;               // double-buffered accumulator
+    static constexpr int TMEM_COLS = NACC * BN;            // multi-buffered accumulator (<= 512)
 };
 
 DG_DEV uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel) {
@@ -64,6 +71,24 @@ DG_DEV uint4 unpack16(uint32_t x, uint32_t L) {
     return make_uint4(prmt(L, L, X), prmt(L, L, X >> 16), prmt(L, L, Y), prmt(L, L, Y >> 16));
 }
 
+#ifdef DG_TRACE
+// Debug timeline (compile with -DDG_TRACE): CTA 0 records %globaltimer at pipeline events.
+__device__ unsigned long long *g_dg_trace = nullptr;
+DG_DEV unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+    return t;
+}
+#define DG_TR(ev, idx)                                                                 \
+    do {                                                                               \
+        if (g_dg_trace && blockIdx.x == 0 && (idx) < 64) g_dg_trace[(ev) * 64 + (idx)] = gtimer(); \
+    } while (0)
+#else
+#define DG_TR(ev, idx) \
+    do {               \
+    } while (0)
+#endif
+
 struct TileArgs {
     int64_t np, nq;
     int32_t nstages;       // K stages of 128 codes
@@ -77,6 +102,11 @@ struct TileArgs {
     int32_t fast_rq;       // requant with at most a bias: int32 threshold compares
     int32_t thr[3];        // int32 thresholds on acc_raw + bias (K-pad correction folded in)
     int32_t dir;
+    int32_t pks;           // packed bytes per row per packed stage (smem row pitch), <= 128
+    int32_t nps;           // packed stages per tile
+    int32_t bulk;          // 1: each packed stage is one contiguous tile -> cp.async.bulk
+    const uint8_t *P, *Q;  // operand bases (bulk mode)
+    int64_t ldp, ldq;
 };
 
 DG_DEV void store_codes32(uint8_t *dp, uint32_t o0, uint32_t o1, int nbytes) {
@@ -144,8 +174,9 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     auto empty_p = [&](int s) { return bar0 + 8 * (SP + s); };
     auto full_u = [&](int s) { return bar0 + 8 * (2 * SP + s); };
     auto empty_u = [&](int s) { return bar0 + 8 * (2 * SP + SU + s); };
+    constexpr int NACC = C::NACC;
     auto acc_full = [&](int a) { return bar0 + 8 * (2 * SP + 2 * SU + a); };
-    auto acc_empty = [&](int a) { return bar0 + 8 * (2 * SP + 2 * SU + 2 + a); };
+    auto acc_empty = [&](int a) { return bar0 + 8 * (2 * SP + 2 * SU + NACC + a); };
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::OFF_TMEM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -157,13 +188,13 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             ptx::tma_prefetch(&tm_q);
             for (int s = 0; s < SP; ++s) {
                 ptx::mbar_init(full_p(s), 1);
-                ptx::mbar_init(empty_p(s), NUM_UNPACK_WARPS);
+                ptx::mbar_init(empty_p(s), (PKS_MAX / PKB) * UGROUP_WARPS);   // per sub-stage, per warp
             }
             for (int s = 0; s < SU; ++s) {
-                ptx::mbar_init(full_u(s), NUM_UNPACK_WARPS);
+                ptx::mbar_init(full_u(s), UGROUP_WARPS);     // the warps of the owning group
                 ptx::mbar_init(empty_u(s), 1);
             }
-            for (int a = 0; a < 2; ++a) {
+            for (int a = 0; a < NACC; ++a) {
                 ptx::mbar_init(acc_full(a), 1);
                 ptx::mbar_init(acc_empty(a), NUM_EPI_WARPS);
             }
@@ -178,17 +209,28 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     const uint32_t tmem = *tmem_slot;
 
     if (warp == 0) {
-        // ---------------- TMA producer: packed 2-bit tiles
+        // ---------------- producer: packed 2-bit tiles (TMA 2-D boxes, or 1-D bulk copies when the
+        // whole K extent of a tile is contiguous)
         if (lane == 0) {
             uint32_t g = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const int32_t yp = (t / ta.ntq) * BM, yq = (t % ta.ntq) * BN;
-                for (int s = 0; s < ta.nstages; ++s, ++g) {
+                const int64_t p0 = (int64_t)(t / ta.ntq) * BM, q0 = (int64_t)(t % ta.ntq) * BN;
+                for (int s = 0; s < ta.nps; ++s, ++g) {
                     const int slot = g % SP;
                     ptx::mbar_wait(empty_p(slot), ((g / SP) & 1u) ^ 1u);
-                    ptx::mbar_arrive_expect_tx(full_p(slot), C::PK_P + C::PK_Q);
-                    ptx::tma_load_2d(sbase + C::OFF_PP + slot * C::PK_P, &tm_p, full_p(slot), s * PKB, yp);
-                    ptx::tma_load_2d(sbase + C::OFF_PQ + slot * C::PK_Q, &tm_q, full_p(slot), s * PKB, yq);
+                    DG_TR(0, g);
+                    const uint32_t dp = sbase + C::OFF_PP + slot * C::PK_P, dq = sbase + C::OFF_PQ + slot * C::PK_Q;
+                    if (ta.bulk) {
+                        const int64_t rp = ta.np - p0 < BM ? ta.np - p0 : BM, rq_ = ta.nq - q0 < BN ? ta.nq - q0 : BN;
+                        const uint32_t bp = (uint32_t)(rp * ta.ldp), bq = (uint32_t)(rq_ * ta.ldq);
+                        ptx::mbar_arrive_expect_tx(full_p(slot), bp + bq);
+                        ptx::bulk_load(dp, ta.P + p0 * ta.ldp, bp, full_p(slot));
+                        ptx::bulk_load(dq, ta.Q + q0 * ta.ldq, bq, full_p(slot));
+                    } else {
+                        ptx::mbar_arrive_expect_tx(full_p(slot), (uint32_t)((BM + BN) * ta.pks));
+                        ptx::tma_load_2d(dp, &tm_p, full_p(slot), s * ta.pks, (int32_t)p0);
+                        ptx::tma_load_2d(dq, &tm_q, full_p(slot), s * ta.pks, (int32_t)q0);
+                    }
                 }
             }
         }
@@ -198,13 +240,15 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
             uint32_t g = 0, tl = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-                const uint32_t acc = tl & 1u;
-                ptx::mbar_wait(acc_empty(acc), ((tl >> 1) & 1u) ^ 1u);
+                const uint32_t acc = tl % NACC;
+                ptx::mbar_wait(acc_empty(acc), ((tl / NACC) & 1u) ^ 1u);
+                DG_TR(1, tl);
                 ptx::tc_fence_after();
                 const uint32_t dt = tmem + acc * BN;
                 for (int s = 0; s < ta.nstages; ++s, ++g) {
                     const int slot = g % SU;
                     ptx::mbar_wait(full_u(slot), (g / SU) & 1u);
+                    DG_TR(2, g);
                     ptx::tc_fence_after();
                     const uint32_t a = sbase + C::OFF_UP + slot * C::UNP_P;
                     const uint32_t b = sbase + C::OFF_UQ + slot * C::UNP_Q;
@@ -220,31 +264,42 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
         }
     } else if (warp < EPI_WARP0) {
-        // ---------------- unpackers: packed smem -> int8 levels in the SW128 K-major layout
-        const int ut = threadIdx.x - 32 * UNPACK_WARP0;
-        constexpr int NU = 32 * NUM_UNPACK_WARPS;
-        constexpr int ITEMS = (BM + BN) * 2;     // 16-byte packed chunks (64 codes) per stage
-        uint32_t g = 0;
+        // ---------------- unpackers: packed smem -> int8 levels in the SW128 K-major layout.
+        // Group j (UGROUP_WARPS warps) owns unpacked stages g = j, j + NUM_UGROUPS, ... so that
+        // NUM_UGROUPS stages are in flight and the per-stage handoff latency overlaps.
+        const int uw = warp - UNPACK_WARP0;
+        const int grp = uw / UGROUP_WARPS, gt = (uw % UGROUP_WARPS) * 32 + lane;
+        constexpr int ITEMS = (BM + BN) * 2;     // 16-byte packed chunks (64 codes) per unpacked stage
+        const int nsub = (ta.pks + PKB - 1) / PKB;
+        uint32_t g = 0, gp = 0;                  // global unpacked / packed stage counters
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             for (int s = 0; s < ta.nstages; ++s, ++g) {
-                const int sp = g % SP, su = g % SU;
+                const int sub = s % nsub;
+                const bool last_sub = sub == nsub - 1 || s == ta.nstages - 1;
+                const uint32_t my_gp = gp;
+                if (last_sub) ++gp;
+                if ((int)(g % NUM_UGROUPS) != grp) continue;
+                const int sp = my_gp % SP, su = g % SU;
                 // 16-byte chunk h covers MMA k-steps 2h, 2h+1: skip chunks no MMA reads
                 const int hmax = (s == ta.nstages - 1) ? (ta.last_ksteps + 1) / 2 : 2;
-                ptx::mbar_wait(full_p(sp), (g / SP) & 1u);
+                ptx::mbar_wait(full_p(sp), (my_gp / SP) & 1u);
+                if (gt == 0) DG_TR(3, g);
                 ptx::mbar_wait(empty_u(su), ((g / SU) & 1u) ^ 1u);
+                if (gt == 0) DG_TR(4, g);
                 const uint8_t *pk_p = smem + C::OFF_PP + sp * C::PK_P;
                 const uint8_t *pk_q = smem + C::OFF_PQ + sp * C::PK_Q;
                 uint8_t *up = smem + C::OFF_UP + su * C::UNP_P;
                 uint8_t *uq = smem + C::OFF_UQ + su * C::UNP_Q;
-#pragma unroll
-                for (int it0 = 0; it0 < ITEMS; it0 += NU) {
-                    const int it = it0 + ut;
-                    if (it >= ITEMS) break;
+#pragma unroll 2
+                for (int it = gt; it < ITEMS; it += 32 * UGROUP_WARPS) {
                     const int row = it >> 1, h = it & 1;
                     if (h >= hmax) continue;
                     const bool isp = row < BM;
                     const int r = isp ? row : row - BM;
-                    const uint4 v = *reinterpret_cast<const uint4 *>((isp ? pk_p : pk_q) + r * PKB + h * 16);
+                    // tensor mode: the TMA wrote 128-byte rows with the 128B swizzle (16-byte chunk
+                    // index XOR row%8), which makes this column read conflict-free
+                    const int cidx = ta.bulk ? (sub * 2 + h) : ((sub * 2 + h) ^ (r & 7));
+                    const uint4 v = *reinterpret_cast<const uint4 *>((isp ? pk_p : pk_q) + r * ta.pks + cidx * 16);
                     const uint32_t L = isp ? ta.lp : ta.lq;
                     uint8_t *dst = (isp ? up : uq) + (r >> 3) * 1024 + (r & 7) * 128;
                     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
@@ -254,11 +309,19 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         *reinterpret_cast<uint4 *>(dst + chunk * 16) = unpack16(w[j], L);
                     }
                 }
-                __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(empty_p(sp));
+                if (gt == 0) DG_TR(9, g);
                 ptx::fence_proxy_async_smem();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(full_u(su));
+                if (gt == 0) DG_TR(10, g);
+                if (lane == 0) {
+                    ptx::mbar_arrive(full_u(su));
+                    // release the packed slot once per sub-stage; a short final packed stage
+                    // releases the sub-stages it does not have as well
+                    const int extra = (s == ta.nstages - 1) ? (PKS_MAX / PKB - 1 - sub) : (sub == nsub - 1 ? PKS_MAX / PKB - nsub : 0);
+                    ptx::mbar_arrive(empty_p(sp));
+                    for (int e = 0; e < extra; ++e) ptx::mbar_arrive(empty_p(sp));
+                }
+                if (gt == 0) DG_TR(5, g);
             }
         }
     } else {
@@ -269,10 +332,11 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const bool col_bias = rq.bias && rq.bias_axis == 0;
         uint32_t tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-            const uint32_t acc = tl & 1u;
+            const uint32_t acc = tl % NACC;
             const int64_t p = (int64_t)(t / ta.ntq) * BM + quarter * 32 + lane;
             const int64_t q0 = (int64_t)(t % ta.ntq) * BN + half * HALF;
-            ptx::mbar_wait(acc_full(acc), (tl >> 1) & 1u);
+            ptx::mbar_wait(acc_full(acc), (tl / NACC) & 1u);
+            if (warp == EPI_WARP0 && lane == 0) DG_TR(6, tl);
             ptx::tc_fence_after();
             const uint32_t trow = tmem + acc * BN + half * HALF + ((uint32_t)(quarter * 32) << 16);
             const bool fast = ta.fast_rq && q0 + HALF <= ta.nq;
@@ -281,6 +345,9 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 // int32 output / residual requant / ragged tail: out of line, reloads TMEM itself
 #pragma unroll 1
                 for (int c = 0; c < NCH; ++c) epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(acc_empty(acc));   // accumulator buffer drained
             } else {
                 uint32_t r[2][32];
                 ptx::tmem_ld_32x32b_x32(trow, r[0]);
@@ -293,6 +360,12 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         bx[j] = col_bias ? __ldg(reinterpret_cast<const int4 *>(rq.bias + qc) + j) : make_int4(rb, rb, rb, rb);
                     ptx::tmem_ld_wait();
                     if (c + 1 < NCH) ptx::tmem_ld_32x32b_x32(trow + (c + 1) * 32, r[(c + 1) & 1]);
+                    if (c == NCH - 1) {   // all of this warp's columns are in registers: free the buffer
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
+                        if (warp == EPI_WARP0 && lane == 0) DG_TR(7, tl);
+                    }
                     if (p >= ta.np) continue;
                     // v = acc_raw + bias; code = number of exact thresholds passed, counted from
                     // sign bits: (t - v) < 0 <=> v > t  (|t|, |v| < 2^30: no overflow)
@@ -326,9 +399,6 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     else store_codes32(dp, o0, o1, 8);
                 }
             }
-            ptx::tc_fence_before();
-            __syncwarp();
-            if (lane == 0) ptx::mbar_arrive(acc_empty(acc));   // accumulator buffer drained
         }
     }
 
@@ -356,15 +426,16 @@ EncodeTiledFn encode_fn() {
     return fn;
 }
 
-bool make_map(CUtensorMap *m, const uint8_t *base, int64_t ld, int64_t rows, int box_rows) {
+bool make_map(CUtensorMap *m, const uint8_t *base, int64_t ld, int64_t rows, int box_rows, int box_inner) {
     EncodeTiledFn fn = encode_fn();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)ld};
-    cuuint32_t box[2] = {(cuuint32_t)PKB, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t *>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, box_inner == 128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+              CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -386,7 +457,14 @@ dg_status launch(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t ldq, i
         }
     acc_bound *= K;
     CUtensorMap mp, mq;
-    if (!make_map(&mp, P, ldp, np, BM) || !make_map(&mq, Q, ldq, nq, BN)) return DG_ERR_CUDA;
+    memset(&mp, 0, sizeof(mp));
+    memset(&mq, 0, sizeof(mq));
+    // A packed stage carries up to 128 B (512 codes) of every row.  When both operands' rows fit
+    // one packed stage and the row pitches match, each tile is one contiguous span -> bulk copy.
+    // (only rows of <= 32 B: wider rows are read column-wise from smem and need the TMA swizzle)
+    const bool bulk = ldp == ldq && ldp <= 32 && (((uintptr_t)P | (uintptr_t)Q) & 15) == 0;
+    const int pks = bulk ? (int)ldp : PKS_MAX;
+    if (!bulk && (!make_map(&mp, P, ldp, np, BM, pks) || !make_map(&mq, Q, ldq, nq, BN, pks))) return DG_ERR_CUDA;
     TileArgs ta{};
     ta.np = np;
     ta.nq = nq;
@@ -400,6 +478,13 @@ dg_status launch(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t ldq, i
     ta.corr = (kmma - K) * (int64_t)pl[0] * (int64_t)ql[0];
     ta.D = D;
     ta.ldd = ldd;
+    ta.pks = pks;
+    ta.bulk = bulk ? 1 : 0;
+    ta.P = P;
+    ta.Q = Q;
+    ta.ldp = ldp;
+    ta.ldq = ldq;
+    ta.nps = (int32_t)((ta.nstages + (pks + PKB - 1) / PKB - 1) / ((pks + PKB - 1) / PKB));
     ta.has_rq = rq ? 1 : 0;
     ta.fast_rq = 0;
     if (rq && !rq->res && !rq->res_codes && acc_bound < ((int64_t)1 << 29) &&
@@ -432,6 +517,13 @@ dg_status launch(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t ldq, i
 }
 
 }  // namespace
+
+#ifdef DG_TRACE
+extern "C" __attribute__((visibility("default"))) int dg_debug_set_trace(void *dev_buf) {
+    unsigned long long *p = (unsigned long long *)dev_buf;
+    return cudaMemcpyToSymbol(g_dg_trace, &p, sizeof(p)) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 bool tc_available() {
     static int ok = -1;

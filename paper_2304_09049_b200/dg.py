@@ -14,7 +14,7 @@ from dataclasses import dataclass, field
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libdg.so")
+LIB_PATH = os.environ.get("DG_LIB_PATH", os.path.join(_HERE, "libdg.so"))
 
 DG_OK = 0
 VARIANTS = {"auto": 0, "cc": 1, "tc": 2}
