@@ -63,7 +63,7 @@ typedef int32_t dg_status;
 DG_API const char *dg_status_string(dg_status s);
 
 /* ABI version of this header (bumped on any signature change). */
-#define DG_ABI_VERSION 1
+#define DG_ABI_VERSION 2
 DG_API int32_t dg_abi_version(void);
 
 /* ---------------------------------------------------------------------------
@@ -163,14 +163,36 @@ DG_API dg_status dg_requantize(const int32_t *d_acc, int64_t rows, int64_t cols,
  * d_w [M][ldw], d_at [N][lda] packed (K-major, see above).
  * Output: rq == NULL -> int32 C at d_c[m*ldc + n];
  *         rq != NULL -> requantised codes (S7 fused), packed 4 columns (n) per
- *                       byte: d_c is uint8 [M][ldc bytes]; N % 4 == 0.
+ *                       byte: d_c is uint8 [M][ldc bytes].
  * variant: 0 auto, 1 cc (CUDA-core PRMT lookups, any table),
- *          2 tc (tcgen05 kind::i8 over the product factorisation;
- *            DG_ERR_UNSUPPORTED unless lut->is_product and levels fit int8).
- * DG_ERR_OVERFLOW if K * max|entry| >= 2^31.                                 */
+ *          2 tc (tcgen05 kind::i8, A operand unpacked into tensor memory; needs
+ *            lut->is_product with int8 levels, else DG_ERR_UNSUPPORTED; uses
+ *            d_ws for the int8 expansion of At: dg_lut_gemm_workspace_size bytes),
+ *          3 tc_ss (earlier tcgen05 variant: both operands unpacked to shared memory).
+ * DG_ERR_OVERFLOW if K * max|entry| >= 2^31.  With rq, |acc + bias| < 2^30 is
+ * required for the fused fast path's int32 threshold compare (else exact int64). */
+DG_API size_t dg_lut_gemm_workspace_size(int64_t N, int64_t K);
 DG_API dg_status dg_lut_gemm(const uint8_t *d_w, int64_t ldw, const uint8_t *d_at, int64_t lda, int64_t M,
                       int64_t N, int64_t K, const dg_lut *lut, void *d_c, int64_t ldc,
-                      const dg_requant *rq, int32_t variant, void *stream);
+                      const dg_requant *rq, void *d_ws, size_t ws_bytes, int32_t variant, void *stream);
+
+/* Offline operand expansion for the tensor-core path: packed codes [rows][ld] ->
+ * int8 levels [rows][ld_out] (ld_out >= dg_expand_ld(K), a multiple of 128), with
+ * levels[code] in the byte order documented in csrc/unpack.cuh (the 16 codes of a
+ * 32-bit word as 0,2,..,14,1,3,..,15; the same order the kernel gives the other
+ * operand) and 0 for every k >= K.  Like the paper's offline weight packing and
+ * reordering this is done once per weight tensor. */
+DG_API int64_t dg_expand_ld(int64_t K);
+DG_API dg_status dg_expand_operand(const uint8_t *d_packed, int64_t rows, int64_t K, int64_t ld,
+                            const int32_t levels[4], int8_t *d_out, int64_t ld_out, void *stream);
+
+/* LUT GEMM with a prepared second operand (tc path only):
+ *      C[m][n] = sum_{k<K} lut.entries[(W[m][k] << 2) | A[k][n]]
+ * d_w packed [M][ldw]; d_at8 = dg_expand_operand(At, levels = lut->al) [N][ld8].
+ * Requires lut->is_product with int8 levels.  Output as dg_lut_gemm.       */
+DG_API dg_status dg_lut_gemm_prepared(const uint8_t *d_w, int64_t ldw, const int8_t *d_at8, int64_t ld8,
+                               int64_t M, int64_t N, int64_t K, const dg_lut *lut, void *d_c, int64_t ldc,
+                               const dg_requant *rq, void *stream);
 
 /* ---------------------------------------------------------------------------
  * Convolution over packed NHWC codes = im2col (S3) + LUT GEMM (S5) + fused

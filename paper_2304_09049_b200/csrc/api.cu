@@ -45,17 +45,25 @@ dg_status check_rq(const dg_requant *rq) {
 }
 
 // D[p][q] = sum_k Tt[(P<<2)|Q]; pl/ql = per-code levels of P/Q (valid iff product).
+// variant 2 (tc) expands Q into the workspace, then runs the TMEM-A kernel.
 dg_status gemm_dispatch(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t ldq, int64_t np,
                         int64_t nq, int64_t K, const int32_t Tt[16], bool is_product,
                         const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd,
-                        const dg_requant *rq, int32_t variant, cudaStream_t st) {
+                        const dg_requant *rq, void *ws, size_t ws_bytes, int32_t variant, cudaStream_t st) {
     RequantArgs a{};
     const RequantArgs *ap = nullptr;
     if (rq) { a = to_args(rq); ap = &a; }
     const bool tc_ok = is_product && levels_fit_i8(pl) && levels_fit_i8(ql) && tc_available();
-    if (variant == 2 && !tc_ok) return DG_ERR_UNSUPPORTED;
-    if (variant == 2 || (variant == 0 && tc_ok))
-        return lut_gemm_tc(P, ldp, Q, ldq, np, nq, K, pl, ql, D, ldd, ap, st);
+    if ((variant == 2 || variant == 3) && !tc_ok) return DG_ERR_UNSUPPORTED;
+    if (variant == 3) return lut_gemm_tc(P, ldp, Q, ldq, np, nq, K, pl, ql, D, ldd, ap, st);
+    if (variant == 2 || (variant == 0 && tc_ok)) {
+        const int64_t ld8 = expand_ld(K);
+        int8_t *q8 = (int8_t *)(((uintptr_t)ws + 127) & ~(uintptr_t)127);
+        if (!ws || (int64_t)ws_bytes - (int64_t)((uint8_t *)q8 - (uint8_t *)ws) < nq * ld8) return DG_ERR_WORKSPACE;
+        dg_status s = expand_operand(Q, nq, K, ldq, ql, q8, ld8, st);
+        if (s != DG_OK) return s;
+        return lut_gemm_ts(P, ldp, q8, ld8, np, nq, K, pl, ql, D, ldd, ap, st);
+    }
     return lut_gemm_cc(P, ldp, Q, ldq, np, nq, K, Tt, D, ldd, ap, st);
 }
 
@@ -112,11 +120,16 @@ dg_status dg_lut_from_table(const int32_t entries[16], int32_t entry_bits, dg_lu
     return DG_OK;
 }
 
+size_t dg_lut_gemm_workspace_size(int64_t N, int64_t K) {
+    if (N <= 0 || K <= 0) return 0;
+    return (size_t)(N * expand_ld(K) + 128);
+}
+
 dg_status dg_lut_gemm(const uint8_t *d_w, int64_t ldw, const uint8_t *d_at, int64_t lda, int64_t M,
                       int64_t N, int64_t K, const dg_lut *lut, void *d_c, int64_t ldc,
-                      const dg_requant *rq, int32_t variant, void *stream) {
+                      const dg_requant *rq, void *d_ws, size_t ws_bytes, int32_t variant, void *stream) {
     if (!d_w || !d_at || !lut || !d_c) return DG_ERR_INVALID_ARG;
-    if (variant < 0 || variant > 2) return DG_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 3) return DG_ERR_INVALID_ARG;
     if (M <= 0 || N <= 0 || K <= 0) return DG_ERR_SHAPE;
     if (ldw % 16 || lda % 16 || ldw * 4 < K || lda * 4 < K) return DG_ERR_SHAPE;
     if (!aligned16(d_w) || !aligned16(d_at)) return DG_ERR_INVALID_ARG;
@@ -126,7 +139,37 @@ dg_status dg_lut_gemm(const uint8_t *d_w, int64_t ldw, const uint8_t *d_at, int6
     if ((int64_t)K * max_abs_entry(lut->entries) >= ((int64_t)1 << 31)) return DG_ERR_OVERFLOW;
     // P = W (rows m), Q = At (rows n): D[m][n] = C[m][n], table index (w<<2)|a as is.
     return gemm_dispatch(d_w, ldw, d_at, lda, M, N, K, lut->entries, lut->is_product != 0, lut->wl,
-                         lut->al, d_c, ldc, rq, variant, (cudaStream_t)stream);
+                         lut->al, d_c, ldc, rq, d_ws, ws_bytes, variant, (cudaStream_t)stream);
+}
+
+int64_t dg_expand_ld(int64_t K) { return K <= 0 ? 0 : expand_ld(K); }
+
+dg_status dg_expand_operand(const uint8_t *d_packed, int64_t rows, int64_t K, int64_t ld,
+                            const int32_t levels[4], int8_t *d_out, int64_t ld_out, void *stream) {
+    if (!d_packed || !levels || !d_out) return DG_ERR_INVALID_ARG;
+    if (rows < 0 || K <= 0 || ld % 16 || ld * 4 < K || ld_out < expand_ld(K) || ld_out % 128) return DG_ERR_SHAPE;
+    if (!levels_fit_i8(levels)) return DG_ERR_RANGE;
+    if (!aligned16(d_packed) || ((uintptr_t)d_out & 127)) return DG_ERR_INVALID_ARG;
+    return expand_operand(d_packed, rows, K, ld, levels, d_out, ld_out, (cudaStream_t)stream);
+}
+
+dg_status dg_lut_gemm_prepared(const uint8_t *d_w, int64_t ldw, const int8_t *d_at8, int64_t ld8,
+                               int64_t M, int64_t N, int64_t K, const dg_lut *lut, void *d_c, int64_t ldc,
+                               const dg_requant *rq, void *stream) {
+    if (!d_w || !d_at8 || !lut || !d_c) return DG_ERR_INVALID_ARG;
+    if (M <= 0 || N <= 0 || K <= 0) return DG_ERR_SHAPE;
+    if (ldw % 16 || ldw * 4 < K || ld8 < expand_ld(K) || ld8 % 128) return DG_ERR_SHAPE;
+    if (!aligned16(d_w) || ((uintptr_t)d_at8 & 127)) return DG_ERR_INVALID_ARG;
+    if (rq ? (ldc * 4 < N) : (ldc < N)) return DG_ERR_SHAPE;
+    dg_status s = check_rq(rq);
+    if (s != DG_OK) return s;
+    if (!lut->is_product || !levels_fit_i8(lut->wl) || !levels_fit_i8(lut->al) || !tc_available())
+        return DG_ERR_UNSUPPORTED;
+    if ((int64_t)K * max_abs_entry(lut->entries) >= ((int64_t)1 << 31)) return DG_ERR_OVERFLOW;
+    RequantArgs a{};
+    if (rq) a = to_args(rq);
+    return lut_gemm_ts(d_w, ldw, d_at8, ld8, M, N, K, lut->wl, lut->al, d_c, ldc, rq ? &a : nullptr,
+                       (cudaStream_t)stream);
 }
 
 static bool conv_is_direct(const dg_conv_params *p) {
@@ -138,18 +181,18 @@ size_t dg_lut_conv2d_workspace_size(const dg_conv_params *p) {
     if (!p || p->B <= 0 || p->H <= 0 || p->W <= 0 || p->C <= 0 || p->kh <= 0 || p->kw <= 0 ||
         p->stride <= 0)
         return 0;
-    if (conv_is_direct(p)) return 0;
     const int64_t Ho = (p->H + 2 * p->pad - p->kh) / p->stride + 1;
     const int64_t Wo = (p->W + 2 * p->pad - p->kw) / p->stride + 1;
     const int64_t K = (int64_t)p->kh * p->kw * p->C;
-    return (size_t)((int64_t)p->B * Ho * Wo * dg_packed_ld(K) + 256);
+    const int64_t cols = conv_is_direct(p) ? 0 : (int64_t)p->B * Ho * Wo * dg_packed_ld(K);
+    return (size_t)((cols + 127) / 128 * 128 + (int64_t)p->Cout * expand_ld(K) + 256);
 }
 
 dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_lut *lut,
                         const dg_conv_params *p, const dg_requant *rq, void *d_out, void *d_ws,
                         size_t ws_bytes, int32_t variant, void *stream) {
     if (!d_x || !d_w || !lut || !p || !d_out) return DG_ERR_INVALID_ARG;
-    if (variant < 0 || variant > 2) return DG_ERR_INVALID_ARG;
+    if (variant < 0 || variant > 3) return DG_ERR_INVALID_ARG;
     if (p->B <= 0 || p->H <= 0 || p->W <= 0 || p->C <= 0 || p->Cout <= 0 || p->kh <= 0 ||
         p->kw <= 0 || p->stride <= 0 || p->pad < 0)
         return DG_ERR_SHAPE;
@@ -173,7 +216,7 @@ dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_lut *lu
     } else {
         const int64_t ld = dg_packed_ld(K);
         if (!d_ws || (int64_t)ws_bytes < rows * ld) return DG_ERR_WORKSPACE;
-        uint8_t *cols = (uint8_t *)(((uintptr_t)d_ws + 15) & ~(uintptr_t)15);
+        uint8_t *cols = (uint8_t *)(((uintptr_t)d_ws + 127) & ~(uintptr_t)127);
         if ((int64_t)ws_bytes - (int64_t)(cols - (uint8_t *)d_ws) < rows * ld) return DG_ERR_WORKSPACE;
         s = dg_im2col(d_x, p->B, p->H, p->W, p->C, p->kh, p->kw, p->stride, p->pad,
                       (uint8_t)p->pad_code, cols, ld, stream);
@@ -187,8 +230,16 @@ dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_lut *lu
     for (int a = 0; a < 4; ++a)
         for (int w = 0; w < 4; ++w) Tt[(a << 2) | w] = lut->entries[(w << 2) | a];
     const int64_t ldd = rq ? p->Cout / 4 : p->Cout;
+    // the rest of the workspace (after the im2col matrix) holds the expanded weights
+    uint8_t *ws_rest = (uint8_t *)d_ws;
+    size_t rest = ws_bytes;
+    if (P != d_x) {
+        const int64_t used = (int64_t)(((uintptr_t)P - (uintptr_t)d_ws) + rows * ldp);
+        ws_rest = (uint8_t *)d_ws + used;
+        rest = ws_bytes > (size_t)used ? ws_bytes - (size_t)used : 0;
+    }
     return gemm_dispatch(P, ldp, d_w, p->ldw, rows, p->Cout, K, Tt, lut->is_product != 0, lut->al,
-                         lut->wl, d_out, ldd, rq, variant, st);
+                         lut->wl, d_out, ldd, rq, ws_rest, rest, variant, st);
 }
 
 }  // extern "C"

@@ -1,0 +1,498 @@
+// lut_gemm_ts.cu — the tensor-core LUT-16 GEMM for PRODUCT tables, "TS" form:
+//
+//   D[p][q] = sum_{k<K} pl[P[p][k]] * ql[Q[q][k]]  ==  sum_k T[(P<<2)|Q]      (Alg. 1)
+//
+// as a tcgen05 kind::i8 GEMM (exact s32 accumulation in TMEM) where
+//   * the A operand (P, the packed 2-bit activations / im2col rows) is unpacked ON CHIP, one
+//     thread per row, straight into TENSOR MEMORY with tcgen05.st (the paper's unpack step,
+//     P:123, producing int8 levels): no shared-memory write of the 4x expanded data;
+//   * the B operand (Q) is the int8 level expansion of the packed weights made ONCE by
+//     dg_expand_operand (an offline weight transform, like the paper's offline weight packing
+//     and reordering, P:143 / P:298), fed by TMA with the 128B swizzle into shared memory.
+//
+// Persistent, warp-specialised, one CTA per SM:
+//   warp 0        producer: packed P stages (128 B = 512 codes per row, TMA SWIZZLE_128B or a
+//                 contiguous bulk copy when rows are <= 32 B) and int8 B stages (TMA, SW128)
+//   warp 1        MMA issuer (one thread): tcgen05.mma [D], [A_tmem], B_desc, 4 k-steps/stage
+//   warps 2..9    unpackers: two groups of 4 warps (one warp per TMEM lane quarter) owning
+//                 alternate stages; thread = row of the 128-row tile
+//   warps 10..13  epilogue: TMEM accumulators -> exact requant (S7) or int32 -> global
+#include <cuda.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "tc_ptx.cuh"
+#include "unpack.cuh"
+
+namespace dg {
+namespace {
+
+constexpr int BM = 128;          // TMEM lanes / P rows per tile
+constexpr int KS = 128;          // codes per stage (= one 128-byte int8 B row, 32 TMEM columns of A)
+constexpr int PKS_MAX = 128;     // packed bytes per row per packed stage (512 codes)
+constexpr int NSUB_MAX = PKS_MAX * 4 / KS;   // 4 stages per packed stage
+constexpr int NUM_UNPACK_WARPS = 8;
+constexpr int NUM_UGROUPS = 2;
+constexpr int NUM_EPI_WARPS = 4;
+constexpr int UNPACK_WARP0 = 2;
+constexpr int EPI_WARP0 = UNPACK_WARP0 + NUM_UNPACK_WARPS;
+constexpr int NT = 32 * (EPI_WARP0 + NUM_EPI_WARPS);   // 448 threads
+
+template <int BN>
+struct TsCfg {
+    static constexpr int NACC = BN == 128 ? 3 : 4;          // accumulator buffers (TMEM cols NACC*BN)
+    static constexpr int SA = 4;                            // A stages in TMEM (32 cols each)
+    static constexpr int SB = 4;                            // B (int8) smem stages
+    static constexpr int SP = 4;                            // packed P smem stages
+    static constexpr int TMEM_A0 = NACC * BN;               // first A column
+    static constexpr int TMEM_COLS = 512;
+    static constexpr int B_BYTES = BN * KS;
+    static constexpr int P_BYTES = BM * PKS_MAX;
+    static constexpr int OFF_B = 0;                          // 1024-aligned (SW128)
+    static constexpr int OFF_P = OFF_B + SB * B_BYTES;
+    static constexpr int OFF_BAR = OFF_P + SP * P_BYTES;
+    static constexpr int NBAR = 2 * SP + 2 * SB + 2 * SA + 2 * NACC;
+    static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
+    static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
+    static_assert(TMEM_A0 + SA * 32 <= TMEM_COLS, "TMEM budget");
+};
+
+struct TsArgs {
+    int64_t np, nq;
+    int32_t nstages, last_ksteps, ntp, ntq;
+    int32_t pks, bulk;     // packed P stage bytes per row (smem pitch); bulk copy mode
+    const uint8_t *P;      // packed P (bulk mode)
+    int64_t ldp;
+    uint32_t lp;           // int8 levels of P codes
+    void *D;
+    int64_t ldd;
+    int32_t has_rq, fast_rq, dir;
+    int32_t thr[3];
+};
+
+DG_DEV void store_codes32_ts(uint8_t *dp, uint32_t o0, uint32_t o1, int nbytes) {
+#pragma unroll
+    for (int b = 0; b < 8; ++b)
+        if (b < nbytes) dp[b] = (uint8_t)((b < 4 ? o0 : o1) >> (8 * (b & 3)));
+}
+
+// int32 output / residual requant / ragged tail for one 32-column chunk (out of line)
+__device__ __noinline__ void ts_epilogue_general(const TsArgs &ta, const RequantArgs &rq, uint32_t taddr, int64_t p,
+                                                 int64_t qc) {
+    uint32_t rr[32];
+    ptx::tmem_ld_32x32b_x32(taddr, rr);
+    ptx::tmem_ld_wait();
+    if (p >= ta.np || qc >= ta.nq) return;
+    int32_t v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = (int32_t)rr[j];
+    if (!ta.has_rq) {
+        int32_t *dp = reinterpret_cast<int32_t *>(ta.D) + p * ta.ldd + qc;
+        if (qc + 32 <= ta.nq && (ta.ldd & 3) == 0 && ((reinterpret_cast<uintptr_t>(ta.D) & 15) == 0)) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4) *reinterpret_cast<int4 *>(dp + j) = make_int4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        } else {
+            for (int j = 0; j < 32; ++j)
+                if (qc + j < ta.nq) dp[j] = v[j];
+        }
+        return;
+    }
+    uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
+    if (qc + 32 <= ta.nq) {
+        const uint2 o = requant_row32(rq, v, p, qc);
+        if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = o;
+        else store_codes32_ts(dp, o.x, o.y, 8);
+        return;
+    }
+    uint32_t o0 = 0, o1 = 0;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+        if (qc + j < ta.nq) {
+            const uint32_t cd = requant_one(rq, v[j], p, qc + j);
+            if (j < 16) o0 |= cd << (2 * j);
+            else o1 |= cd << (2 * (j - 16));
+        }
+    }
+    store_codes32_ts(dp, o0, o1, (int)((ta.nq - qc + 3) / 4));
+}
+
+template <int BN>
+__global__ void __launch_bounds__(NT, 1)
+lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
+                   const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
+    using C = TsCfg<BN>;
+    constexpr int SP = C::SP, SB = C::SB, SA = C::SA, NACC = C::NACC;
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = ptx::smem_u32(smem);
+    const uint32_t bar0 = sbase + C::OFF_BAR;
+    auto full_p = [&](int s) { return bar0 + 8 * s; };
+    auto empty_p = [&](int s) { return bar0 + 8 * (SP + s); };
+    auto full_b = [&](int s) { return bar0 + 8 * (2 * SP + s); };
+    auto empty_b = [&](int s) { return bar0 + 8 * (2 * SP + SB + s); };
+    auto full_a = [&](int s) { return bar0 + 8 * (2 * SP + 2 * SB + s); };
+    auto empty_a = [&](int s) { return bar0 + 8 * (2 * SP + 2 * SB + SA + s); };
+    auto acc_full = [&](int a) { return bar0 + 8 * (2 * SP + 2 * SB + 2 * SA + a); };
+    auto acc_empty = [&](int a) { return bar0 + 8 * (2 * SP + 2 * SB + 2 * SA + NACC + a); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::OFF_TMEM);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = ta.ntp * ta.ntq;
+    const int nsub = (ta.pks * 4 + KS - 1) / KS;   // stages per packed stage
+
+    if (warp == 0) {
+        if (lane == 0) {
+            if (!ta.bulk) ptx::tma_prefetch(&tm_p);
+            ptx::tma_prefetch(&tm_b);
+            for (int s = 0; s < SP; ++s) {
+                ptx::mbar_init(full_p(s), 1);
+                ptx::mbar_init(empty_p(s), NSUB_MAX * 4);   // 4 warps per stage, NSUB_MAX stages
+            }
+            for (int s = 0; s < SB; ++s) {
+                ptx::mbar_init(full_b(s), 1);
+                ptx::mbar_init(empty_b(s), 1);
+            }
+            for (int s = 0; s < SA; ++s) {
+                ptx::mbar_init(full_a(s), 4);
+                ptx::mbar_init(empty_a(s), 1);
+            }
+            for (int a = 0; a < NACC; ++a) {
+                ptx::mbar_init(acc_full(a), 1);
+                ptx::mbar_init(acc_empty(a), NUM_EPI_WARPS);
+            }
+            ptx::fence_mbar_init();
+        }
+        __syncwarp();
+        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), C::TMEM_COLS);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 0) {
+        // ---------------- producer
+        if (lane == 0) {
+            uint32_t gp = 0, gb = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                const int64_t p0 = (int64_t)(t / ta.ntq) * BM, q0 = (int64_t)(t % ta.ntq) * BN;
+                for (int s = 0; s < ta.nstages; ++s, ++gb) {
+                    if (s % nsub == 0) {   // next packed P stage (up to 512 codes of every row)
+                        const int slot = gp % SP;
+                        ptx::mbar_wait(empty_p(slot), ((gp / SP) & 1u) ^ 1u);
+                        const uint32_t dst = sbase + C::OFF_P + slot * C::P_BYTES;
+                        if (ta.bulk) {
+                            const int64_t rows = ta.np - p0 < BM ? ta.np - p0 : BM;
+                            const uint32_t bytes = (uint32_t)(rows * ta.ldp);
+                            ptx::mbar_arrive_expect_tx(full_p(slot), bytes);
+                            ptx::bulk_load(dst, ta.P + p0 * ta.ldp, bytes, full_p(slot));
+                        } else {
+                            ptx::mbar_arrive_expect_tx(full_p(slot), (uint32_t)(BM * PKS_MAX));
+                            ptx::tma_load_2d(dst, &tm_p, full_p(slot), (s / nsub) * PKS_MAX, (int32_t)p0);
+                        }
+                        ++gp;
+                    }
+                    const int bs = gb % SB;
+                    ptx::mbar_wait(empty_b(bs), ((gb / SB) & 1u) ^ 1u);
+                    ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)C::B_BYTES);
+                    ptx::tma_load_2d(sbase + C::OFF_B + bs * C::B_BYTES, &tm_b, full_b(bs), s * KS, (int32_t)q0);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        // ---------------- MMA issuer
+        if (lane == 0) {
+            constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
+            uint32_t g = 0, tl = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+                const uint32_t acc = tl % NACC;
+                ptx::mbar_wait(acc_empty(acc), ((tl / NACC) & 1u) ^ 1u);
+                ptx::tc_fence_after();
+                const uint32_t dt = tmem + acc * BN;
+                for (int s = 0; s < ta.nstages; ++s, ++g) {
+                    const int sa = g % SA, sb = g % SB;
+                    ptx::mbar_wait(full_a(sa), (g / SA) & 1u);
+                    ptx::mbar_wait(full_b(sb), (g / SB) & 1u);
+                    ptx::tc_fence_after();
+                    const uint32_t at = tmem + C::TMEM_A0 + sa * 32;
+                    const uint32_t b = sbase + C::OFF_B + sb * C::B_BYTES;
+                    const int ksteps = (s == ta.nstages - 1) ? ta.last_ksteps : KS / 32;
+#pragma unroll
+                    for (int k = 0; k < KS / 32; ++k)
+                        if (k < ksteps)
+                            ptx::mma_i8_ts(dt, at + 8 * k, ptx::desc_k_sw128(b + 32 * k), idesc, (s > 0 || k > 0) ? 1u : 0u);
+                    ptx::mma_commit(empty_a(sa));
+                    ptx::mma_commit(empty_b(sb));
+                }
+                ptx::mma_commit(acc_full(acc));
+            }
+        }
+    } else if (warp < EPI_WARP0) {
+        // ---------------- unpackers: thread = row; packed smem -> int8 levels -> TMEM (A operand)
+        const int uw = warp - UNPACK_WARP0;
+        const int grp = uw / 4;                 // stage group
+        const int quarter = warp & 3;           // TMEM lane quarter this warp may access
+        const int r = quarter * 32 + lane;      // tile row
+        uint32_t g = 0, gp = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int s = 0; s < ta.nstages; ++s, ++g) {
+                const int sub = s % nsub;
+                const uint32_t my_gp = gp;
+                if (sub == nsub - 1 || s == ta.nstages - 1) ++gp;
+                if ((int)(g % NUM_UGROUPS) != grp) continue;
+                const int sp = my_gp % SP, sa = g % SA;
+                const bool two = (s != ta.nstages - 1) || ta.last_ksteps > 2;   // second 64-code half used
+                ptx::mbar_wait(full_p(sp), (my_gp / SP) & 1u);
+                const uint8_t *row = smem + C::OFF_P + sp * C::P_BYTES + r * ta.pks;
+                uint4 v0, v1;
+                if (ta.bulk) {
+                    v0 = *reinterpret_cast<const uint4 *>(row + sub * 32);
+                    v1 = two ? *reinterpret_cast<const uint4 *>(row + sub * 32 + 16) : make_uint4(0, 0, 0, 0);
+                } else {   // SWIZZLE_128B: 16-byte chunk c of row r lives at chunk c ^ (r % 8)
+                    v0 = *reinterpret_cast<const uint4 *>(row + (((sub * 2) ^ (r & 7)) << 4));
+                    v1 = two ? *reinterpret_cast<const uint4 *>(row + (((sub * 2 + 1) ^ (r & 7)) << 4)) : make_uint4(0, 0, 0, 0);
+                }
+                __syncwarp();
+                if (lane == 0) {   // this warp's share of the packed slot is consumed
+                    const int extra = (s == ta.nstages - 1) ? (NSUB_MAX - 1 - sub) : (sub == nsub - 1 ? NSUB_MAX - nsub : 0);
+                    ptx::mbar_arrive(empty_p(sp));
+                    for (int e = 0; e < extra; ++e) ptx::mbar_arrive(empty_p(sp));
+                }
+                uint32_t a[32];
+                const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint4 o = unpack16_levels(w[j], ta.lp);
+                    a[4 * j] = o.x; a[4 * j + 1] = o.y; a[4 * j + 2] = o.z; a[4 * j + 3] = o.w;
+                }
+                ptx::mbar_wait(empty_a(sa), ((g / SA) & 1u) ^ 1u);
+                ptx::tc_fence_after();
+                ptx::tmem_st_32x32b_x32(tmem + C::TMEM_A0 + sa * 32 + ((uint32_t)(quarter * 32) << 16), a);
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(full_a(sa));
+            }
+        }
+    } else {
+        // ---------------- epilogue (4 warps, one per lane quarter, all BN columns)
+        constexpr int NCH = BN / 32;
+        const int quarter = warp & 3;
+        const bool col_bias = rq.bias && rq.bias_axis == 0;
+        uint32_t tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const uint32_t acc = tl % NACC;
+            const int64_t p = (int64_t)(t / ta.ntq) * BM + quarter * 32 + lane;
+            const int64_t q0 = (int64_t)(t % ta.ntq) * BN;
+            ptx::mbar_wait(acc_full(acc), (tl / NACC) & 1u);
+            ptx::tc_fence_after();
+            const uint32_t trow = tmem + acc * BN + ((uint32_t)(quarter * 32) << 16);
+            const bool fast = ta.fast_rq && q0 + BN <= ta.nq;
+            const int32_t rb = (fast && rq.bias && rq.bias_axis == 1 && p < ta.np) ? __ldg(rq.bias + p) : 0;
+            if (!fast) {
+#pragma unroll 1
+                for (int c = 0; c < NCH; ++c) ts_epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
+            } else {
+                uint32_t r[2][32];
+                ptx::tmem_ld_32x32b_x32(trow, r[0]);
+#pragma unroll
+                for (int c = 0; c < NCH; ++c) {
+                    const int64_t qc = q0 + c * 32;
+                    int4 bx[8];
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        bx[j] = col_bias ? __ldg(reinterpret_cast<const int4 *>(rq.bias + qc) + j) : make_int4(rb, rb, rb, rb);
+                    ptx::tmem_ld_wait();
+                    if (c + 1 < NCH) ptx::tmem_ld_32x32b_x32(trow + (c + 1) * 32, r[(c + 1) & 1]);
+                    if (c == NCH - 1) {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
+                    }
+                    if (p >= ta.np) continue;
+                    // code = number of exact thresholds passed, from sign bits (|t|, |v| < 2^30)
+                    uint32_t o0 = 0, o1 = 0;
+                    if (ta.dir > 0) {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int4 b4 = bx[j >> 2];
+                            const int32_t b = (j & 3) == 0 ? b4.x : (j & 3) == 1 ? b4.y : (j & 3) == 2 ? b4.z : b4.w;
+                            const int32_t v = (int32_t)r[c & 1][j];
+                            const uint32_t cd = ((uint32_t)(ta.thr[0] - v - b) >> 31) + ((uint32_t)(ta.thr[1] - v - b) >> 31) +
+                                                ((uint32_t)(ta.thr[2] - v - b) >> 31);
+                            if (j < 16) o0 += cd << (2 * j);
+                            else o1 += cd << (2 * (j - 16));
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 32; ++j) {
+                            const int4 b4 = bx[j >> 2];
+                            const int32_t b = (j & 3) == 0 ? b4.x : (j & 3) == 1 ? b4.y : (j & 3) == 2 ? b4.z : b4.w;
+                            const int32_t v = (int32_t)r[c & 1][j];
+                            const uint32_t cd = ((uint32_t)(v + b - ta.thr[0] - 1) >> 31) + ((uint32_t)(v + b - ta.thr[1] - 1) >> 31) +
+                                                ((uint32_t)(v + b - ta.thr[2] - 1) >> 31);
+                            if (j < 16) o0 += cd << (2 * j);
+                            else o1 += cd << (2 * (j - 16));
+                        }
+                    }
+                    uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
+                    if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = make_uint2(o0, o1);
+                    else store_codes32_ts(dp, o0, o1, 8);
+                }
+            }
+        }
+    }
+
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+}
+
+// ---- Q expansion: packed codes -> int8 levels in the unpack16_levels order, zero beyond K.
+// One thread per 16-byte packed chunk (64 codes -> 64 bytes).
+__global__ void expand_operand_kernel(const uint8_t *__restrict__ packed, int64_t rows, int64_t K, int64_t ld,
+                                      uint32_t L, int8_t *__restrict__ out, int64_t ld8) {
+    const int64_t chunks = ld8 / 64;
+    const int64_t total = rows * chunks;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / chunks, c = i - r * chunks;
+        const int64_t k0 = c * 64;
+        uint4 v = make_uint4(0, 0, 0, 0);
+        if (c * 16 + 16 <= ld) v = __ldg(reinterpret_cast<const uint4 *>(packed + r * ld + c * 16));
+        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+        uint4 *dst = reinterpret_cast<uint4 *>(out + r * ld8 + k0);
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            uint4 o = unpack16_levels(w[j], L);
+            const int64_t kw = k0 + 16 * j;
+            if (kw + 16 > K) {   // zero the bytes of codes >= K (no correction term needed)
+                uint32_t ow[4] = {o.x, o.y, o.z, o.w};
+#pragma unroll
+                for (int b = 0; b < 16; ++b) {
+                    const int code = b < 8 ? 2 * b : 2 * (b - 8) + 1;   // inverse of the unpack order
+                    if (kw + code >= K) ow[b >> 2] &= ~(0xFFu << (8 * (b & 3)));
+                }
+                o = make_uint4(ow[0], ow[1], ow[2], ow[3]);
+            }
+            dst[j] = o;
+        }
+    }
+}
+
+// ---------------------------------------------------------------- host
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                                  CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+EncodeTiledFn encode_fn_ts() {
+    static EncodeTiledFn fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<EncodeTiledFn>(p);
+    }
+    return fn;
+}
+
+// 2-D uint8 map over [rows][ld] with a {128 B, box_rows} box and the 128-byte swizzle
+bool make_map_sw128(CUtensorMap *m, const void *base, int64_t ld, int64_t rows, int box_rows) {
+    EncodeTiledFn fn = encode_fn_ts();
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {128u, (cuuint32_t)box_rows};
+    cuuint32_t estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+template <int BN>
+dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
+                    const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
+                    cudaStream_t st) {
+    using C = TsCfg<BN>;
+    int64_t acc_bound = 0;   // K * max |pl[a] * ql[b]|
+    for (int a = 0; a < 4; ++a)
+        for (int b = 0; b < 4; ++b) {
+            const int64_t e = (int64_t)pl[a] * ql[b];
+            acc_bound = (e < 0 ? -e : e) > acc_bound ? (e < 0 ? -e : e) : acc_bound;
+        }
+    acc_bound *= K;
+    TsArgs ta{};
+    ta.np = np;
+    ta.nq = nq;
+    ta.nstages = (int32_t)((K + KS - 1) / KS);
+    const int64_t kmma = (K + 31) / 32 * 32;
+    ta.last_ksteps = (int32_t)((kmma - (int64_t)(ta.nstages - 1) * KS) / 32);
+    ta.ntp = (int32_t)((np + BM - 1) / BM);
+    ta.ntq = (int32_t)((nq + BN - 1) / BN);
+    ta.bulk = (ldp <= 32 && ((uintptr_t)P & 15) == 0) ? 1 : 0;
+    ta.pks = ta.bulk ? (int32_t)ldp : PKS_MAX;
+    ta.P = P;
+    ta.ldp = ldp;
+    ta.lp = pack_levels_i8(pl);
+    ta.D = D;
+    ta.ldd = ldd;
+    ta.has_rq = rq ? 1 : 0;
+    if (rq && !rq->res && !rq->res_codes && acc_bound < ((int64_t)1 << 29) &&
+        (!rq->bias || rq->bias_axis == 1 || (((uintptr_t)rq->bias) & 15) == 0)) {
+        ta.fast_rq = 1;      // acc is exact (no correction term): acc + bias >= t <=> x > t - 1
+        ta.dir = rq->dir;
+        for (int j = 0; j < 3; ++j) {
+            const int64_t t = rq->thr[j];
+            int64_t u = (t == INT64_MAX || t == INT64_MIN) ? t : (rq->dir > 0 ? t - 1 : t);
+            const int64_t LIM = (int64_t)1 << 30;
+            ta.thr[j] = (int32_t)(u > LIM ? LIM : (u < -LIM ? -LIM : u));
+        }
+    }
+    CUtensorMap mp, mb;
+    memset(&mp, 0, sizeof(mp));
+    if (!ta.bulk && !make_map_sw128(&mp, P, ldp, np, BM)) return DG_ERR_CUDA;
+    if (!make_map_sw128(&mb, Q8, ld8, nq, BN)) return DG_ERR_CUDA;
+    static bool attr_set = false;
+    if (!attr_set) {
+        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
+            cudaSuccess)
+            return DG_ERR_CUDA;
+        attr_set = true;
+    }
+    RequantArgs dummy{};
+    const int64_t ntiles = (int64_t)ta.ntp * ta.ntq;
+    if (ntiles > INT32_MAX) return DG_ERR_SHAPE;
+    const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
+    lut_gemm_ts_kernel<BN><<<grid, NT, C::ALLOC, st>>>(mp, mb, ta, rq ? *rq : dummy);
+    return launch_status();
+}
+
+}  // namespace
+
+int64_t expand_ld(int64_t K) { return (K + KS - 1) / KS * KS; }
+
+dg_status expand_operand(const uint8_t *packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],
+                         int8_t *out, int64_t ld8, cudaStream_t st) {
+    if (rows == 0) return DG_OK;
+    const int64_t work = rows * (ld8 / 64);
+    int64_t blocks = (work + 255) / 256;
+    const int64_t cap = (int64_t)num_sms() * 8;
+    if (blocks > cap) blocks = cap;
+    expand_operand_kernel<<<(int)blocks, 256, 0, st>>>(packed, rows, K, ld, pack_levels_i8(levels), out, ld8);
+    return launch_status();
+}
+
+dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
+                      const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
+                      cudaStream_t st) {
+    if (np > ((int64_t)1 << 31) - 1 || nq > ((int64_t)1 << 31) - 1) return DG_ERR_SHAPE;
+    if (nq > 64) return launch_ts<128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
+    return launch_ts<64>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
+}
+
+}  // namespace dg

@@ -17,7 +17,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DG_LIB_PATH", os.path.join(_HERE, "libdg.so"))
 
 DG_OK = 0
-VARIANTS = {"auto": 0, "cc": 1, "tc": 2}
+VARIANTS = {"auto": 0, "cc": 1, "tc": 2, "tc_ss": 3}
 
 
 class DGError(RuntimeError):
@@ -72,7 +72,11 @@ def lib():
                                               P, i64, P], i32),
             "dg_im2col": ([P, i32, i32, i32, i32, i32, i32, i32, i32, u8, P, i64, P], i32),
             "dg_requantize": ([P, i64, i64, i64, P, P, i64, P], i32),
-            "dg_lut_gemm": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, i32, P], i32),
+            "dg_lut_gemm_workspace_size": ([i64, i64], ctypes.c_size_t),
+            "dg_lut_gemm": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, P, ctypes.c_size_t, i32, P], i32),
+            "dg_expand_ld": ([i64], i64),
+            "dg_expand_operand": ([P, i64, i64, i64, P, P, i64, P], i32),
+            "dg_lut_gemm_prepared": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, P], i32),
             "dg_lut_conv2d_workspace_size": ([P], ctypes.c_size_t),
             "dg_lut_conv2d": ([P, P, P, P, P, P, P, ctypes.c_size_t, i32, P], i32),
         }
@@ -223,9 +227,13 @@ def requantize(acc: torch.Tensor, rq: Requant, out: torch.Tensor | None = None, 
 
 
 # ---------------------------------------------------------------- GEMM / conv
+def gemm_workspace_size(N: int, K: int) -> int:
+    return int(lib().dg_lut_gemm_workspace_size(N, K))
+
+
 def lut_gemm(w: torch.Tensor, at: torch.Tensor, M: int, N: int, K: int, lut: dg_lut,
              rq: Requant | None = None, variant: str | int = "auto", out: torch.Tensor | None = None,
-             stream=None) -> torch.Tensor:
+             ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
     """C[m][n] = sum_k T[(W[m][k]<<2)|A[k][n]] over packed W [M][ldw], At [N][lda]."""
     _dev(w, torch.uint8, "w")
     _dev(at, torch.uint8, "at")
@@ -233,10 +241,43 @@ def lut_gemm(w: torch.Tensor, at: torch.Tensor, M: int, N: int, K: int, lut: dg_
     if out is None:
         out = (torch.empty((M, (N + 3) // 4), dtype=torch.uint8, device=w.device) if rq is not None
                else torch.empty((M, N), dtype=torch.int32, device=w.device))
+    if ws is None:
+        ws = torch.empty(gemm_workspace_size(N, K), dtype=torch.uint8, device=w.device)
     r = rq.c() if rq is not None else None
     _check(lib().dg_lut_gemm(_ptr(w), w.shape[1], _ptr(at), at.shape[1], M, N, K, ctypes.byref(lut),
-                             _ptr(out), out.shape[1], ctypes.byref(r) if r is not None else None, v,
-                             _stream(stream)), "dg_lut_gemm")
+                             _ptr(out), out.shape[1], ctypes.byref(r) if r is not None else None,
+                             _ptr(ws), ws.numel(), v, _stream(stream)), "dg_lut_gemm")
+    return out
+
+
+def expand_ld(K: int) -> int:
+    return int(lib().dg_expand_ld(K))
+
+
+def expand_operand(packed: torch.Tensor, K: int, levels, out: torch.Tensor | None = None, stream=None):
+    """Packed codes [rows][ld] -> int8 levels [rows][expand_ld(K)] (tensor-core operand order)."""
+    _dev(packed, torch.uint8, "packed")
+    rows, ld = packed.shape
+    if out is None:
+        out = torch.empty((rows, expand_ld(K)), dtype=torch.int8, device=packed.device)
+    lv = (ctypes.c_int32 * 4)(*[int(x) for x in levels])
+    _check(lib().dg_expand_operand(_ptr(packed), rows, K, ld, lv, _ptr(out), out.shape[1], _stream(stream)),
+           "dg_expand_operand")
+    return out
+
+
+def lut_gemm_prepared(w: torch.Tensor, at8: torch.Tensor, M: int, N: int, K: int, lut: dg_lut,
+                      rq: Requant | None = None, out: torch.Tensor | None = None, stream=None):
+    """As lut_gemm with At pre-expanded by expand_operand(At, K, lut.al)."""
+    _dev(w, torch.uint8, "w")
+    _dev(at8, torch.int8, "at8")
+    if out is None:
+        out = (torch.empty((M, (N + 3) // 4), dtype=torch.uint8, device=w.device) if rq is not None
+               else torch.empty((M, N), dtype=torch.int32, device=w.device))
+    r = rq.c() if rq is not None else None
+    _check(lib().dg_lut_gemm_prepared(_ptr(w), w.shape[1], _ptr(at8), at8.shape[1], M, N, K, ctypes.byref(lut),
+                                      _ptr(out), out.shape[1], ctypes.byref(r) if r is not None else None,
+                                      _stream(stream)), "dg_lut_gemm_prepared")
     return out
 
 

@@ -33,6 +33,7 @@ class LayerPlan:
     lut_t: object          # transposed table, index (a<<2)|w (dg_lut_gemm with P = pixels)
     rq: object
     w: torch.Tensor        # packed weights [Cout][ldw]
+    w8: torch.Tensor | None  # int8 level expansion of w (offline, tc path), dg_expand_operand
     x: torch.Tensor        # packed NHWC input [B*H*W][Cp/4]
     out: torch.Tensor      # packed NHWC output codes [B*Ho*Wo][Cout/4]
     rows: int              # B*Ho*Wo  (GEMM rows on the P side)
@@ -116,12 +117,14 @@ class NetRunner:
             rq = dg.Requant(r.mult, r.shift, r.zp, r.qmin, r.qmax, bias=bias, bias_axis=0)
             out = torch.empty((rows, L.cout // 4), dtype=torch.uint8, device=device)
             direct = L.k == 1 and L.stride == 1 and L.pad == 0 and (Cp // 4) % 16 == 0
-            plan = LayerPlan(L.name, L, params, lut, lut_t, rq, wq, xq, out, rows, K, direct,
+            w8 = dg.expand_operand(wq, K, wl) if variant in ("auto", "tc") else None
+            plan = LayerPlan(L.name, L, params, lut, lut_t, rq, wq, w8, xq, out, rows, K, direct,
                              2 * L.cout * rows * L.k * L.k * L.cin)
-            if not direct:
-                ws_need = max(ws_need, rows * plan.cols_ld)
+            ws_need = max(ws_need, dg.conv_workspace_size(params), (0 if direct else rows * plan.cols_ld),
+                          dg.gemm_workspace_size(L.cout, K))
             self.plans.append(plan)
         self.ws = torch.empty(max(ws_need, 16), dtype=torch.uint8, device=device)
+        self.ws_gemm = self.ws
         self.total_ops = sum(p.ops for p in self.plans)
 
     # -- the step, split into C-ABI calls so the GEMM launches can be bracketed by events
@@ -134,12 +137,18 @@ class NetRunner:
             else:
                 ld = p.cols_ld
                 P = self.ws[: p.rows * ld].view(p.rows, ld)
+                if p.w8 is None:   # packed-weights GEMM needs its own workspace after the columns
+                    off = (p.rows * ld + 127) // 128 * 128
+                    self.ws_gemm = self.ws[off:]
                 dg.im2col(p.x, self.B, L.h, L.h, p.params.C, L.k, L.k, L.stride, L.pad, 0, out=P, stream=stream)
                 n += 1
             if gemm_events is not None:
                 gemm_events[i][0].record()
-            dg.lut_gemm(P, p.w, p.rows, L.cout, p.K, p.lut_t, rq=p.rq, variant=self.variant, out=p.out,
-                        stream=stream)
+            if p.w8 is not None:   # tensor-core path with the offline-expanded weights
+                dg.lut_gemm_prepared(P, p.w8, p.rows, L.cout, p.K, p.lut_t, rq=p.rq, out=p.out, stream=stream)
+            else:
+                dg.lut_gemm(P, p.w, p.rows, L.cout, p.K, p.lut_t, rq=p.rq, variant=self.variant, out=p.out,
+                            ws=self.ws_gemm, stream=stream)
             if gemm_events is not None:
                 gemm_events[i][1].record()
             n += 1

@@ -19,7 +19,7 @@ if not torch.cuda.is_available():  # pragma: no cover
 from paper_2304_09049_b200 import dg  # noqa: E402
 
 DEV = "cuda"
-VARIANTS = ["cc", "tc"]
+VARIANTS = ["cc", "tc", "tc_ss"]
 WL, AL = [-2, -1, 0, 1], [0, 1, 2, 3]
 
 
@@ -39,7 +39,7 @@ def oracle_codes_of(packed_gpu, rows, K):
 
 
 def variant_ok(variant, lut):
-    if variant == "tc" and not (lut.is_product and dg.lib() and _tc_available()):
+    if variant.startswith("tc") and not (lut.is_product and dg.lib() and _tc_available()):
         return False
     return True
 
@@ -172,8 +172,9 @@ def test_gemm_non_product_tables_cc(seed):
     A = g.integers(0, 4, (K, N), dtype=np.uint8)
     lut = dg.lut_from_table(T, 32)
     assert np.array_equal(host(run_gemm(W, A, lut, "cc")), oracle.lut_gemm(W, A, T))
-    with pytest.raises(dg.DGError, match="UNSUPPORTED"):
-        run_gemm(W, A, lut, "tc")
+    for v in ("tc", "tc_ss"):
+        with pytest.raises(dg.DGError, match="UNSUPPORTED"):
+            run_gemm(W, A, lut, v)
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -249,7 +250,7 @@ def test_conv_vs_oracle(variant, B, H, W, C, Cout, k, stride, pad, pad_code):
     try:
         out = dg.lut_conv2d(xp, wp, lut, p, variant=variant)
     except dg.DGError as e:
-        if variant == "tc" and pad_code != 0 and "UNSUPPORTED" in str(e):
+        if variant.startswith("tc") and pad_code != 0 and "UNSUPPORTED" in str(e):
             pytest.skip("tc conv requires pad level 0")
         raise
     assert np.array_equal(host(out).reshape(exp.shape), exp)
@@ -297,3 +298,29 @@ def test_conv_residual_identity_and_downsample(variant):
     assert np.array_equal(host(racc), rd)
     exp2 = oracle.requantize(a2, 12000, 20, 0, 0, 3, res=rd)
     assert np.array_equal(oracle_codes_of(out2, exp2.shape[0], C2), exp2)
+
+
+@pytest.mark.parametrize("M,N,K", [(130, 70, 300), (256, 256, 1024), (77, 129, 64), (128, 64, 4608)])
+def test_gemm_prepared_and_expand(M, N, K):
+    """dg_expand_operand + dg_lut_gemm_prepared (offline-expanded second operand) vs the oracle;
+    the expansion itself is checked against the levels (zero beyond K) up to the documented order."""
+    import synth
+    wl, al = synth.learned_levels(5, 1, synth.T_LEVELS)
+    lut = dg.build_lut(wl, al, 16)
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    g = np.random.default_rng(M + N + K)
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    w = gpu_pack(W, weights=True)
+    at = gpu_pack(np.ascontiguousarray(A.T))
+    at8 = dg.expand_operand(at, K, al)
+    e = host(at8).astype(np.int64)
+    assert e.shape[1] % 128 == 0 and not e[:, K + (-K) % 16:].any()
+    # per 16-code word the multiset of levels is preserved (order: 0,2,..,14,1,3,..,15)
+    perm = [0, 2, 4, 6, 8, 10, 12, 14, 1, 3, 5, 7, 9, 11, 13, 15]
+    Kw = K // 16 * 16
+    lv = np.array(al, np.int64)[A.T[:, :Kw]].reshape(N, -1, 16)[:, :, perm]
+    assert np.array_equal(e[:, :Kw].reshape(N, -1, 16), lv)
+    C = host(dg.lut_gemm_prepared(w, at8, M, N, K, lut))
+    assert np.array_equal(C, oracle.lut_gemm(W, A, oracle.build_lut16(wl, al)))

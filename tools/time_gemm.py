@@ -9,8 +9,8 @@ import torch  # noqa: E402
 from paper_2304_09049_b200 import dg  # noqa: E402
 
 ap = argparse.ArgumentParser()
-ap.add_argument("--shapes", default="4096x4096x4096,64x802816x576,256x50176x2304")
-ap.add_argument("--variants", default="cc,tc")
+ap.add_argument("--shapes", default="4096x4096x4096,8192x8192x8192,802816x64x576,50176x256x2304")
+ap.add_argument("--variants", default="cc,tc,tc_ss,prepared")
 ap.add_argument("--iters", type=int, default=10)
 a = ap.parse_args()
 lut = dg.build_lut([-2, -1, 0, 1], [0, 1, 2, 3], 8)
@@ -19,12 +19,18 @@ for s in a.shapes.split(","):
     ld = dg.packed_ld(K)
     w = torch.randint(0, 256, (M, ld), dtype=torch.uint8, device="cuda")
     at = torch.randint(0, 256, (N, ld), dtype=torch.uint8, device="cuda")
-    if K % 64:
-        pass
     out = torch.empty((M, N), dtype=torch.int32, device="cuda")
+    ws = torch.empty(dg.gemm_workspace_size(N, ld * 4), dtype=torch.uint8, device="cuda")
+    at8 = dg.expand_operand(at, ld * 4, lut.al)
     for v in a.variants.split(","):
+        if v == "cc" and M * N * K > 2 ** 36:
+            continue
+        if v == "prepared":
+            f = lambda: dg.lut_gemm_prepared(w, at8, M, N, ld * 4, lut, out=out)
+        else:
+            f = lambda: dg.lut_gemm(w, at, M, N, ld * 4, lut, variant=v, out=out, ws=ws)
         try:
-            dg.lut_gemm(w, at, M, N, ld * 4, lut, variant=v, out=out)
+            f()
         except dg.DGError as e:
             print(f"{s} {v}: {e}")
             continue
@@ -32,7 +38,7 @@ for s in a.shapes.split(","):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record()
         for _ in range(a.iters):
-            dg.lut_gemm(w, at, M, N, ld * 4, lut, variant=v, out=out)
+            f()
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.iters
