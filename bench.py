@@ -209,7 +209,7 @@ def run_conv(args, ws, rank, local):
     if os.path.exists(TRAFFIC):
         with open(TRAFFIC) as f:
             tr = json.load(f).get(args.workload)
-    roof = {"bound": "tensor", "kernel": "lut_gemm_tc_kernel (tcgen05 kind::i8)",
+    roof = {"bound": "tensor", "kernel": "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)",
             "achieved": round(achieved, 1), "peak": round(pk["i8_sustained"], 1), "unit": "TOPS",
             "frac": round(achieved / pk["i8_sustained"], 4),
             "frac_vs_burst_peak": round(achieved / pk["i8_burst"], 4),

@@ -11,12 +11,13 @@
 //     and reordering, P:143 / P:298), fed by TMA with the 128B swizzle into shared memory.
 //
 // Persistent, warp-specialised, one CTA per SM:
-//   warp 0        producer: packed P stages (128 B = 512 codes per row, TMA SWIZZLE_128B or a
-//                 contiguous bulk copy when rows are <= 32 B) and int8 B stages (TMA, SW128)
-//   warp 1        MMA issuer (one thread): tcgen05.mma [D], [A_tmem], B_desc, 4 k-steps/stage
-//   warps 2..9    unpackers: two groups of 4 warps (one warp per TMEM lane quarter) owning
+//   warps 0..3    epilogue: TMEM accumulators -> exact requant (S7) or int32 -> global
+//   warps 4..11   unpackers: two groups of 4 warps (one warp per TMEM lane quarter) owning
 //                 alternate stages; thread = row of the 128-row tile
-//   warps 10..13  epilogue: TMEM accumulators -> exact requant (S7) or int32 -> global
+//   warp 12       producer: packed P stages (128 B = 512 codes per row, TMA SWIZZLE_128B or a
+//                 contiguous bulk copy when rows are <= 32 B) and int8 B stages (TMA, SW128)
+//   warp 13       waiter: waits on the MMA-side mbarriers, hands stages to warp 14 by bar.sync
+//   warp 14       MMA issuer (one thread): tcgen05.mma [D], [A_tmem], B_desc, 4 k-steps/stage
 #include <cuda.h>
 #include <string.h>
 
@@ -31,12 +32,29 @@ constexpr int BM = 128;          // TMEM lanes / P rows per tile
 constexpr int KS = 128;          // codes per stage (= one 128-byte int8 B row, 32 TMEM columns of A)
 constexpr int PKS_MAX = 128;     // packed bytes per row per packed stage (512 codes)
 constexpr int NSUB_MAX = PKS_MAX * 4 / KS;   // 4 stages per packed stage
+// Warp roles.  The SM sub-partition scheduler prefers the highest warp id among eligible
+// warps, so the latency-critical single-thread roles (TMA producer, MMA issuer) take the
+// highest ids and are never starved by the ALU-heavy unpack / epilogue warps.
+// NEPI (template) epilogue warps: 4 (one per TMEM lane quarter, all columns; more registers
+// for long-K tiles) or 8 (two per quarter, half the columns each; for short-K tiles, where
+// the epilogue dominates).
 constexpr int NUM_UNPACK_WARPS = 8;
 constexpr int NUM_UGROUPS = 2;
-constexpr int NUM_EPI_WARPS = 4;
-constexpr int UNPACK_WARP0 = 2;
-constexpr int EPI_WARP0 = UNPACK_WARP0 + NUM_UNPACK_WARPS;
-constexpr int NT = 32 * (EPI_WARP0 + NUM_EPI_WARPS);   // 448 threads
+template <int NEPI>
+struct Roles {
+    static constexpr int EPI_WARP0 = 0;                                   // lane quarter = warp % 4
+    static constexpr int UNPACK_WARP0 = EPI_WARP0 + NEPI;                 // lane quarter = warp % 4
+    static constexpr int PRODUCER_WARP = UNPACK_WARP0 + NUM_UNPACK_WARPS;
+    static constexpr int WAITER_WARP = PRODUCER_WARP + 1;
+    static constexpr int MMA_WARP = WAITER_WARP + 1;
+    static constexpr int NT = 32 * (MMA_WARP + 1);                        // 480 or 608 threads
+};
+// An mbarrier probe (or any shared-memory load) issued by the warp that issues tcgen05.mma
+// waits behind that warp's queued MMAs (measured ~670 cycles per probe, tools/mma_bench.cu),
+// which drains the tensor pipe once per stage.  So the MMA warp never waits on an mbarrier:
+// the waiter warp does, and hands each stage over with a named-barrier rendezvous, which does
+// not stall the MMA queue (measured: 64 cycles per 128x128x32 MMA either way).
+constexpr int HANDOFF_BAR = 1;
 
 template <int BN>
 struct TsCfg {
@@ -56,6 +74,18 @@ struct TsCfg {
     static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
     static_assert(TMEM_A0 + SA * 32 <= TMEM_COLS, "TMEM budget");
 };
+
+#ifdef DG_EXP_NOST
+__device__ uint32_t ta_dummy_sink;
+#endif
+#ifdef DG_TRACE
+__device__ unsigned long long g_ts_prof[16];   // CTA 0 cycle counters (tools/trace_ts.py)
+#define TS_PROF_ADD(i, v) do { if (blockIdx.x == 0) atomicAdd(&g_ts_prof[i], (unsigned long long)(v)); } while (0)
+#define TS_CLK() clock64()
+#else
+#define TS_PROF_ADD(i, v) do { } while (0)
+#define TS_CLK() 0ll
+#endif
 
 struct TsArgs {
     int64_t np, nq;
@@ -116,12 +146,15 @@ __device__ __noinline__ void ts_epilogue_general(const TsArgs &ta, const Requant
     store_codes32_ts(dp, o0, o1, (int)((ta.nq - qc + 3) / 4));
 }
 
-template <int BN>
-__global__ void __launch_bounds__(NT, 1)
+template <int BN, int NEPI>
+__global__ void __launch_bounds__(Roles<NEPI>::NT, 1)
 lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
     using C = TsCfg<BN>;
+    using R = Roles<NEPI>;
     constexpr int SP = C::SP, SB = C::SB, SA = C::SA, NACC = C::NACC;
+    constexpr int NUM_EPI_WARPS = NEPI, EPI_WARP0 = R::EPI_WARP0, UNPACK_WARP0 = R::UNPACK_WARP0,
+                  PRODUCER_WARP = R::PRODUCER_WARP, WAITER_WARP = R::WAITER_WARP, MMA_WARP = R::MMA_WARP;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = ptx::smem_u32(smem);
@@ -140,7 +173,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     const int ntiles = ta.ntp * ta.ntq;
     const int nsub = (ta.pks * 4 + KS - 1) / KS;   // stages per packed stage
 
-    if (warp == 0) {
+    if (warp == PRODUCER_WARP) {
         if (lane == 0) {
             if (!ta.bulk) ptx::tma_prefetch(&tm_p);
             ptx::tma_prefetch(&tm_b);
@@ -170,14 +203,15 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
 
-    if (warp == 0) {
+    if (warp == PRODUCER_WARP) {
         // ---------------- producer
         if (lane == 0) {
             uint32_t gp = 0, gb = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 const int64_t p0 = (int64_t)(t / ta.ntq) * BM, q0 = (int64_t)(t % ta.ntq) * BN;
+                int sub = 0, ps = 0;
                 for (int s = 0; s < ta.nstages; ++s, ++gb) {
-                    if (s % nsub == 0) {   // next packed P stage (up to 512 codes of every row)
+                    if (sub == 0) {   // next packed P stage (up to 512 codes of every row)
                         const int slot = gp % SP;
                         ptx::mbar_wait(empty_p(slot), ((gp / SP) & 1u) ^ 1u);
                         const uint32_t dst = sbase + C::OFF_P + slot * C::P_BYTES;
@@ -188,10 +222,12 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                             ptx::bulk_load(dst, ta.P + p0 * ta.ldp, bytes, full_p(slot));
                         } else {
                             ptx::mbar_arrive_expect_tx(full_p(slot), (uint32_t)(BM * PKS_MAX));
-                            ptx::tma_load_2d(dst, &tm_p, full_p(slot), (s / nsub) * PKS_MAX, (int32_t)p0);
+                            ptx::tma_load_2d(dst, &tm_p, full_p(slot), ps * PKS_MAX, (int32_t)p0);
                         }
                         ++gp;
+                        ++ps;
                     }
+                    if (++sub == nsub) sub = 0;
                     const int bs = gb % SB;
                     ptx::mbar_wait(empty_b(bs), ((gb / SB) & 1u) ^ 1u);
                     ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)C::B_BYTES);
@@ -199,35 +235,59 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
             }
         }
-    } else if (warp == 1) {
-        // ---------------- MMA issuer
-        if (lane == 0) {
-            constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
-            uint32_t g = 0, tl = 0;
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-                const uint32_t acc = tl % NACC;
-                ptx::mbar_wait(acc_empty(acc), ((tl / NACC) & 1u) ^ 1u);
-                ptx::tc_fence_after();
-                const uint32_t dt = tmem + acc * BN;
-                for (int s = 0; s < ta.nstages; ++s, ++g) {
-                    const int sa = g % SA, sb = g % SB;
-                    ptx::mbar_wait(full_a(sa), (g / SA) & 1u);
-                    ptx::mbar_wait(full_b(sb), (g / SB) & 1u);
-                    ptx::tc_fence_after();
-                    const uint32_t at = tmem + C::TMEM_A0 + sa * 32;
-                    const uint32_t b = sbase + C::OFF_B + sb * C::B_BYTES;
-                    const int ksteps = (s == ta.nstages - 1) ? ta.last_ksteps : KS / 32;
-#pragma unroll
-                    for (int k = 0; k < KS / 32; ++k)
-                        if (k < ksteps)
-                            ptx::mma_i8_ts(dt, at + 8 * k, ptx::desc_k_sw128(b + 32 * k), idesc, (s > 0 || k > 0) ? 1u : 0u);
-                    ptx::mma_commit(empty_a(sa));
-                    ptx::mma_commit(empty_b(sb));
-                }
-                ptx::mma_commit(acc_full(acc));
+    } else if (warp == WAITER_WARP) {
+        // ---------------- waiter: acc_empty / full_a / full_b, then rendezvous with the MMA warp
+        uint32_t g = 0, tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            ptx::mbar_wait(acc_empty(tl % NACC), ((tl / NACC) & 1u) ^ 1u);
+            for (int s = 0; s < ta.nstages; ++s, ++g) {
+                const long long c0 = TS_CLK();
+                ptx::mbar_wait(full_a(g % SA), (g / SA) & 1u);
+                const long long c1 = TS_CLK();
+                ptx::mbar_wait(full_b(g % SB), (g / SB) & 1u);
+                const long long c2 = TS_CLK();
+                if (lane == 0) { TS_PROF_ADD(4, c1 - c0); TS_PROF_ADD(5, c2 - c1); }
+                ptx::named_bar_sync(HANDOFF_BAR, 64);
             }
         }
-    } else if (warp < EPI_WARP0) {
+    } else if (warp == MMA_WARP) {
+        // ---------------- MMA issuer: no mbarrier waits here (see HANDOFF_BAR)
+        constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
+        const uint64_t bdesc0 = ptx::desc_k_sw128(sbase + C::OFF_B);
+        uint32_t g = 0, tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const uint32_t acc = tl % NACC;
+            const uint32_t dt = tmem + acc * BN;
+            for (int s = 0; s < ta.nstages; ++s, ++g) {
+                const int sa = g % SA, sb = g % SB;
+                const long long c0 = TS_CLK();
+                ptx::named_bar_sync(HANDOFF_BAR, 64);
+                const long long c1 = TS_CLK();
+                ptx::tc_fence_after();
+                if (lane == 0) {
+                    const uint32_t at = tmem + C::TMEM_A0 + sa * 32;
+                    const uint64_t bd = bdesc0 + (uint64_t)((sb * C::B_BYTES) >> 4);   // +32 B per k-step = +2
+                    if (s < ta.nstages - 1 || ta.last_ksteps == KS / 32) {
+                        ptx::mma_i8_ts(dt, at, bd, idesc, s > 0 ? 1u : 0u);
+                        ptx::mma_i8_ts(dt, at + 8, bd + 2, idesc, 1u);
+                        ptx::mma_i8_ts(dt, at + 16, bd + 4, idesc, 1u);
+                        ptx::mma_i8_ts(dt, at + 24, bd + 6, idesc, 1u);
+                    } else {
+                        for (int k = 0; k < ta.last_ksteps; ++k)
+                            ptx::mma_i8_ts(dt, at + 8 * k, bd + 2 * k, idesc, (s > 0 || k > 0) ? 1u : 0u);
+                    }
+                    ptx::mma_commit(empty_a(sa));
+                    ptx::mma_commit(empty_b(sb));
+                    if (s == ta.nstages - 1) ptx::mma_commit(acc_full(acc));
+                    const long long c2 = TS_CLK();
+                    TS_PROF_ADD(0, c1 - c0);
+                    TS_PROF_ADD(2, c2 - c1);
+                    TS_PROF_ADD(3, 1);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp >= UNPACK_WARP0) {
         // ---------------- unpackers: thread = row; packed smem -> int8 levels -> TMEM (A operand)
         const int uw = warp - UNPACK_WARP0;
         const int grp = uw / 4;                 // stage group
@@ -235,26 +295,28 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const int r = quarter * 32 + lane;      // tile row
         uint32_t g = 0, gp = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            int sub = 0;
             for (int s = 0; s < ta.nstages; ++s, ++g) {
-                const int sub = s % nsub;
                 const uint32_t my_gp = gp;
-                if (sub == nsub - 1 || s == ta.nstages - 1) ++gp;
-                if ((int)(g % NUM_UGROUPS) != grp) continue;
+                const int this_sub = sub;
+                if (sub == nsub - 1 || s == ta.nstages - 1) { ++gp; sub = 0; } else { ++sub; }
+                if ((int)(g & (NUM_UGROUPS - 1)) != grp) continue;
                 const int sp = my_gp % SP, sa = g % SA;
                 const bool two = (s != ta.nstages - 1) || ta.last_ksteps > 2;   // second 64-code half used
                 ptx::mbar_wait(full_p(sp), (my_gp / SP) & 1u);
+                const int sub_ = this_sub;
                 const uint8_t *row = smem + C::OFF_P + sp * C::P_BYTES + r * ta.pks;
                 uint4 v0, v1;
                 if (ta.bulk) {
-                    v0 = *reinterpret_cast<const uint4 *>(row + sub * 32);
-                    v1 = two ? *reinterpret_cast<const uint4 *>(row + sub * 32 + 16) : make_uint4(0, 0, 0, 0);
+                    v0 = *reinterpret_cast<const uint4 *>(row + sub_ * 32);
+                    v1 = two ? *reinterpret_cast<const uint4 *>(row + sub_ * 32 + 16) : make_uint4(0, 0, 0, 0);
                 } else {   // SWIZZLE_128B: 16-byte chunk c of row r lives at chunk c ^ (r % 8)
-                    v0 = *reinterpret_cast<const uint4 *>(row + (((sub * 2) ^ (r & 7)) << 4));
-                    v1 = two ? *reinterpret_cast<const uint4 *>(row + (((sub * 2 + 1) ^ (r & 7)) << 4)) : make_uint4(0, 0, 0, 0);
+                    v0 = *reinterpret_cast<const uint4 *>(row + (((sub_ * 2) ^ (r & 7)) << 4));
+                    v1 = two ? *reinterpret_cast<const uint4 *>(row + (((sub_ * 2 + 1) ^ (r & 7)) << 4)) : make_uint4(0, 0, 0, 0);
                 }
                 __syncwarp();
                 if (lane == 0) {   // this warp's share of the packed slot is consumed
-                    const int extra = (s == ta.nstages - 1) ? (NSUB_MAX - 1 - sub) : (sub == nsub - 1 ? NSUB_MAX - nsub : 0);
+                    const int extra = (s == ta.nstages - 1) ? (NSUB_MAX - 1 - sub_) : (sub_ == nsub - 1 ? NSUB_MAX - nsub : 0);
                     ptx::mbar_arrive(empty_p(sp));
                     for (int e = 0; e < extra; ++e) ptx::mbar_arrive(empty_p(sp));
                 }
@@ -267,28 +329,39 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
                 ptx::mbar_wait(empty_a(sa), ((g / SA) & 1u) ^ 1u);
                 ptx::tc_fence_after();
+#ifndef DG_EXP_NOST
                 ptx::tmem_st_32x32b_x32(tmem + C::TMEM_A0 + sa * 32 + ((uint32_t)(quarter * 32) << 16), a);
                 ptx::tmem_st_wait();
+#else
+                if (a[0] == 0x12345678u && a[5] == 7u) ta_dummy_sink = a[3];
+#endif
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(full_a(sa));
             }
         }
     } else {
-        // ---------------- epilogue (4 warps, one per lane quarter, all BN columns)
-        constexpr int NCH = BN / 32;
-        const int quarter = warp & 3;
+        // ---------------- epilogue (lane quarter = warp % 4, column part = warp / 4)
+        constexpr int HALF = BN / (NEPI / 4), NCH = HALF / 32;
+        const int quarter = warp & 3, half = (warp - EPI_WARP0) >> 2;
         const bool col_bias = rq.bias && rq.bias_axis == 0;
         uint32_t tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl % NACC;
             const int64_t p = (int64_t)(t / ta.ntq) * BM + quarter * 32 + lane;
-            const int64_t q0 = (int64_t)(t % ta.ntq) * BN;
+            const int64_t q0 = (int64_t)(t % ta.ntq) * BN + half * HALF;
             ptx::mbar_wait(acc_full(acc), (tl / NACC) & 1u);
             ptx::tc_fence_after();
-            const uint32_t trow = tmem + acc * BN + ((uint32_t)(quarter * 32) << 16);
-            const bool fast = ta.fast_rq && q0 + BN <= ta.nq;
+            const uint32_t trow = tmem + acc * BN + half * HALF + ((uint32_t)(quarter * 32) << 16);
+            const bool fast = ta.fast_rq && q0 + HALF <= ta.nq;
             const int32_t rb = (fast && rq.bias && rq.bias_axis == 1 && p < ta.np) ? __ldg(rq.bias + p) : 0;
+#ifdef DG_EXP_NOEPI
+            if (true) {
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
+            } else
+#endif
             if (!fast) {
 #pragma unroll 1
                 for (int c = 0; c < NCH; ++c) ts_epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
@@ -296,17 +369,16 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
             } else {
-                uint32_t r[2][32];
-                ptx::tmem_ld_32x32b_x32(trow, r[0]);
-#pragma unroll
+                uint32_t r[32];
+#pragma unroll 1
                 for (int c = 0; c < NCH; ++c) {
                     const int64_t qc = q0 + c * 32;
                     int4 bx[8];
 #pragma unroll
                     for (int j = 0; j < 8; ++j)
                         bx[j] = col_bias ? __ldg(reinterpret_cast<const int4 *>(rq.bias + qc) + j) : make_int4(rb, rb, rb, rb);
+                    ptx::tmem_ld_32x32b_x32(trow + c * 32, r);
                     ptx::tmem_ld_wait();
-                    if (c + 1 < NCH) ptx::tmem_ld_32x32b_x32(trow + (c + 1) * 32, r[(c + 1) & 1]);
                     if (c == NCH - 1) {
                         ptx::tc_fence_before();
                         __syncwarp();
@@ -320,7 +392,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         for (int j = 0; j < 32; ++j) {
                             const int4 b4 = bx[j >> 2];
                             const int32_t b = (j & 3) == 0 ? b4.x : (j & 3) == 1 ? b4.y : (j & 3) == 2 ? b4.z : b4.w;
-                            const int32_t v = (int32_t)r[c & 1][j];
+                            const int32_t v = (int32_t)r[j];
                             const uint32_t cd = ((uint32_t)(ta.thr[0] - v - b) >> 31) + ((uint32_t)(ta.thr[1] - v - b) >> 31) +
                                                 ((uint32_t)(ta.thr[2] - v - b) >> 31);
                             if (j < 16) o0 += cd << (2 * j);
@@ -331,7 +403,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         for (int j = 0; j < 32; ++j) {
                             const int4 b4 = bx[j >> 2];
                             const int32_t b = (j & 3) == 0 ? b4.x : (j & 3) == 1 ? b4.y : (j & 3) == 2 ? b4.z : b4.w;
-                            const int32_t v = (int32_t)r[c & 1][j];
+                            const int32_t v = (int32_t)r[j];
                             const uint32_t cd = ((uint32_t)(v + b - ta.thr[0] - 1) >> 31) + ((uint32_t)(v + b - ta.thr[1] - 1) >> 31) +
                                                 ((uint32_t)(v + b - ta.thr[2] - 1) >> 31);
                             if (j < 16) o0 += cd << (2 * j);
@@ -348,7 +420,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 
     ptx::tc_fence_before();
     __syncthreads();
-    if (warp == 0) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+    if (warp == PRODUCER_WARP) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
 // ---- Q expansion: packed codes -> int8 levels in the unpack16_levels order, zero beyond K.
@@ -402,6 +474,16 @@ EncodeTiledFn encode_fn_ts() {
 }
 
 // 2-D uint8 map over [rows][ld] with a {128 B, box_rows} box and the 128-byte swizzle
+#ifdef DG_TRACE
+extern "C" __attribute__((visibility("default"))) int dg_debug_ts_prof(unsigned long long *host16, int reset) {
+    if (reset) {
+        unsigned long long z[16] = {0};
+        return cudaMemcpyToSymbol(g_ts_prof, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+    }
+    return cudaMemcpyFromSymbol(host16, g_ts_prof, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : -1;
+}
+#endif
+
 bool make_map_sw128(CUtensorMap *m, const void *base, int64_t ld, int64_t rows, int box_rows) {
     EncodeTiledFn fn = encode_fn_ts();
     if (!fn) return false;
@@ -414,7 +496,7 @@ bool make_map_sw128(CUtensorMap *m, const void *base, int64_t ld, int64_t rows, 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN>
+template <int BN, int NEPI>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                     cudaStream_t st) {
@@ -459,7 +541,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     if (!make_map_sw128(&mb, Q8, ld8, nq, BN)) return DG_ERR_CUDA;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
+        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
             cudaSuccess)
             return DG_ERR_CUDA;
         attr_set = true;
@@ -468,7 +550,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     const int64_t ntiles = (int64_t)ta.ntp * ta.ntq;
     if (ntiles > INT32_MAX) return DG_ERR_SHAPE;
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
-    lut_gemm_ts_kernel<BN><<<grid, NT, C::ALLOC, st>>>(mp, mb, ta, rq ? *rq : dummy);
+    lut_gemm_ts_kernel<BN, NEPI><<<grid, Roles<NEPI>::NT, C::ALLOC, st>>>(mp, mb, ta, rq ? *rq : dummy);
     return launch_status();
 }
 
@@ -491,8 +573,14 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
                       const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                       cudaStream_t st) {
     if (np > ((int64_t)1 << 31) - 1 || nq > ((int64_t)1 << 31) - 1) return DG_ERR_SHAPE;
-    if (nq > 64) return launch_ts<128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
-    return launch_ts<64>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
+    // short K (<= 2 stages): the epilogue dominates -> 8 epilogue warps
+    const bool short_k = K <= 2 * KS;
+    if (nq > 64) {
+        if (short_k) return launch_ts<128, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
+        return launch_ts<128, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
+    }
+    if (short_k) return launch_ts<64, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
+    return launch_ts<64, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
 }
 
 }  // namespace dg

@@ -57,6 +57,11 @@ DG_DEV void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t ba
                  : "memory");
 }
 
+// ---------------------------------------------------------------- named barriers
+DG_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
+    asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
 // ---------------------------------------------------------------- proxy fences
 DG_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 

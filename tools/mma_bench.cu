@@ -1,0 +1,181 @@
+// mma_bench.cu — tcgen05.mma kind::i8 throughput microbenchmark (one CTA per SM, all SMs).
+// Issues NITER back-to-back MMAs (M=128, N in {64,128,256}, K=32) from one thread with A from
+// TMEM (TS) or shared memory (SS), commits once, waits, and reports cycles per MMA and the
+// chip-wide int8 TOPS.  Operand contents are zero (throughput does not depend on values).
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o mma_bench tools/mma_bench.cu
+#include <cstdio>
+#include <cstdint>
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include "../paper_2304_09049_b200/csrc/tc_ptx.cuh"
+
+using namespace dg;
+
+// MODE 0: MMA only; 1: + 4 warps of tcgen05.st (32 cols) loops; 2: + 4 warps of LDS.128 loops;
+// 3: + 4 warps of tcgen05.ld (32 cols) loops; 4: commit every 4 MMAs; 5: 4 + try_wait on a
+// completed barrier + fence::after_thread_sync every 4 MMAs; 6: two commits every 4 MMAs
+template <int N, bool TS, int MODE>
+__global__ void __launch_bounds__(256, 1) bench(int niter, unsigned long long *cycles) {
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    __shared__ uint32_t tslot;
+    __shared__ __align__(8) uint64_t bar, bar2[4], bar_done;
+    const int warp = threadIdx.x >> 5;
+    for (int i = threadIdx.x; i < (128 + N) * 128 / 16; i += blockDim.x) reinterpret_cast<uint4 *>(smem)[i] = make_uint4(0, 0, 0, 0);
+    if (threadIdx.x == 0) {
+        ptx::mbar_init(ptx::smem_u32(&bar), 1);
+        ptx::mbar_init(ptx::smem_u32(&bar_done), 1);
+        for (int j = 0; j < 4; ++j) ptx::mbar_init(ptx::smem_u32(&bar2[j]), 1);
+        ptx::fence_mbar_init();
+    }
+    if (warp == 0) ptx::tmem_alloc(ptx::smem_u32(&tslot), 512);
+    ptx::fence_proxy_async_smem();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = tslot;
+    __shared__ volatile int done;
+    if (threadIdx.x == 0) done = 0;
+    __syncthreads();
+    if (threadIdx.x == 0) ptx::mbar_arrive(ptx::smem_u32(&bar_done));   // phase 0 complete
+    __syncthreads();
+    if (warp >= 4 && MODE >= 1 && MODE <= 3) {   // interference warps, lane quarter = warp % 4
+        const uint32_t taddr = tmem + 448 + ((uint32_t)((warp & 3) * 32) << 16);
+        uint32_t r[32];
+        for (int j = 0; j < 32; ++j) r[j] = j;
+        unsigned acc = 0;
+        int it = 0;
+        while (!done) {
+            if (MODE == 1) {
+                ptx::tmem_st_32x32b_x32(taddr, r);
+                ptx::tmem_st_wait();
+            } else if (MODE == 2) {
+                const uint4 v = reinterpret_cast<const uint4 *>(smem)[((it * 37 + threadIdx.x) & 1023)];
+                acc += v.x ^ v.y;
+            } else {
+                ptx::tmem_ld_32x32b_x32(taddr, r);
+                ptx::tmem_ld_wait();
+                acc += r[3];
+            }
+            ++it;
+        }
+        if (acc == 12345) cycles[3] = acc;
+    }
+    if (MODE == 13 && warp == 1) {
+        for (int i = 0; i < niter; i += 4) {
+            ptx::mbar_wait(ptx::smem_u32(&bar_done), 0);
+            asm volatile("bar.sync 2, 64;" ::: "memory");
+        }
+    }
+    if (MODE >= 11 && warp == 0) {
+        const uint32_t a = ptx::smem_u32(smem), b = a + 128 * 128;
+        constexpr uint32_t idesc = ptx::idesc_i8(128, N);
+        const long long c0 = clock64();
+        for (int i = 0; i < niter; ++i) {
+            const int k = i & 3;
+            if (k == 0) {
+                if (MODE == 11) ptx::mbar_wait(ptx::smem_u32(&bar_done), 0);
+                if (MODE == 12) asm volatile("bar.sync 1, 32;" ::: "memory");
+                if (MODE == 13) asm volatile("bar.sync 2, 64;" ::: "memory");
+                ptx::tc_fence_after();
+            }
+            if (threadIdx.x == 0) ptx::mma_i8_ts(tmem, tmem + 256 + 8 * k, ptx::desc_k_sw128(b + 32 * k), idesc, i > 0);
+            __syncwarp();
+        }
+        const long long c1 = clock64();
+        if (threadIdx.x == 0) {
+            ptx::mma_commit(ptx::smem_u32(&bar));
+            ptx::mbar_wait(ptx::smem_u32(&bar), 0);
+        }
+        __syncwarp();
+        const long long c2 = clock64();
+        if (blockIdx.x == 0 && threadIdx.x == 0) {
+            cycles[0] = c1 - c0;
+            cycles[1] = c2 - c0;
+        }
+        if (threadIdx.x == 0) done = 1;
+    }
+    if (threadIdx.x == 0 && MODE < 11) {
+        const uint32_t a = ptx::smem_u32(smem), b = a + 128 * 128;
+        constexpr uint32_t idesc = ptx::idesc_i8(128, N);
+        const long long c0 = clock64();
+        for (int i = 0; i < niter; ++i) {
+            const int k = i & 3;
+            if (MODE == 5 && k == 0) {
+                ptx::mbar_wait(ptx::smem_u32(&bar_done), 0);
+                ptx::tc_fence_after();
+            }
+            if (MODE == 7 && k == 0) ptx::mbar_wait(ptx::smem_u32(&bar_done), 0);
+            if (MODE == 8 && k == 0) ptx::tc_fence_after();
+            if (MODE == 9 && k == 0) {   // test_wait (non-blocking probe) instead of try_wait
+                uint32_t ok;
+                asm volatile("{\n\t.reg .pred p;\n\tmbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\tselp.u32 %0, 1, 0, p;\n\t}"
+                             : "=r"(ok) : "r"(ptx::smem_u32(&bar_done)), "r"(0u) : "memory");
+                if (!ok) ptx::mbar_wait(ptx::smem_u32(&bar_done), 0);
+            }
+            if (MODE == 10 && k == 0) {   // volatile smem flag poll instead of an mbarrier
+                while (done == 7) {}
+            }
+            if (TS)
+                ptx::mma_i8_ts(tmem, tmem + 256 + 8 * k, ptx::desc_k_sw128(b + 32 * k), idesc, i > 0);
+            else
+                ptx::mma_i8_ss(tmem, ptx::desc_k_sw128(a + 32 * k), ptx::desc_k_sw128(b + 32 * k), idesc, i > 0);
+            if ((MODE == 4 || MODE == 5 || MODE == 6) && k == 3) ptx::mma_commit(ptx::smem_u32(&bar2[(i >> 2) & 3]));
+            if (MODE == 6 && k == 3) ptx::mma_commit(ptx::smem_u32(&bar2[((i >> 2) + 1) & 3]));
+        }
+        const long long c1 = clock64();
+        ptx::mma_commit(ptx::smem_u32(&bar));
+        ptx::mbar_wait(ptx::smem_u32(&bar), 0);
+        const long long c2 = clock64();
+        if (blockIdx.x == 0) {
+            cycles[0] = c1 - c0;
+            cycles[1] = c2 - c0;
+        }
+        done = 1;
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == 0) ptx::tmem_dealloc(tmem, 512);
+}
+
+template <int N, bool TS, int MODE = 0>
+void run(int sms) {
+    const int niter = 20000;
+    unsigned long long *d;
+    cudaMalloc(&d, 16);
+    const int smem = (128 + N) * 128 + 2048;
+    cudaFuncSetAttribute(bench<N, TS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    bench<N, TS, MODE><<<sms, 256, smem>>>(100, d);
+    cudaEvent_t e0, e1;
+    cudaEventCreate(&e0);
+    cudaEventCreate(&e1);
+    cudaEventRecord(e0);
+    bench<N, TS, MODE><<<sms, 256, smem>>>(niter, d);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, e0, e1);
+    unsigned long long h[2];
+    cudaMemcpy(h, d, 16, cudaMemcpyDeviceToHost);
+    const double ops = 2.0 * 128 * N * 32 * (double)niter * sms;
+    printf("N %d mode=%d kind::i8 M=128 %s: issue %.1f cyc/mma, complete %.1f cyc/mma, %.1f TOPS chip (%d CTAs, %.3f ms) %s\n", N,
+           MODE, TS ? "A=TMEM" : "A=SMEM", (double)h[0] / niter, (double)h[1] / niter, ops / (ms * 1e-3) / 1e12, sms, ms,
+           cudaGetErrorString(cudaGetLastError()));
+    cudaFree(d);
+}
+
+int main() {
+    int sms = 0;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    run<64, true>(sms);
+    run<128, true>(sms);
+    run<256, true>(sms);
+    run<128, false>(sms);
+    run<256, false>(sms);
+    run<128, true, 7>(sms);
+    run<128, true, 11>(sms);
+    run<128, true, 12>(sms);
+    run<128, true, 13>(sms);
+    return 0;
+}
