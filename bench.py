@@ -208,14 +208,18 @@ def run_conv(args, ws, rank, local):
     tr = None
     if os.path.exists(TRAFFIC):
         with open(TRAFFIC) as f:
-            tr = json.load(f).get(args.workload)
+            t = json.load(f).get(args.workload)
+            tr = t["bytes_per_launch"] if t else None
+    # algorithmic bytes of a GEMM launch: packed input + packed weights + packed output
+    alg_bytes = (runner.input_bytes() + runner.weight_bytes() + runner.output_bytes()) / nl
     roof = {"bound": "tensor", "kernel": "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)",
             "achieved": round(achieved, 1), "peak": round(pk["i8_sustained"], 1), "unit": "TOPS",
             "frac": round(achieved / pk["i8_sustained"], 4),
             "frac_vs_burst_peak": round(achieved / pk["i8_burst"], 4),
             "peak_src": pk["src"] + ": int8 = 2 x bf16 sustained (nominal 4.5/2.25)",
             "gemm_share_of_step": round(gemm_total_ms / ms, 3),
-            "traffic": tr}
+            "traffic": tr, "alg_bytes_per_launch": round(alg_bytes),
+            "traffic_src": "profiles/traffic.json (ncu dram__bytes_read+write, mean per GEMM launch)"}
 
     # ---- end to end through the public C ABI (dg_lut_conv2d) with host buffers
     e2e = None
