@@ -288,6 +288,150 @@ def run_conv(args, ws, rank, local):
         print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- config 2: ResNet-18 b1 chain
+def run_resnet18(args, ws, rank, local):
+    """BJ configs[1]: the 19 LUT convs of ResNet-18 at batch 1, chained with int32 residual adds.
+    Latency-bound, so the whole chain is one CUDA graph; every rank runs an independent replica
+    (replicas only: batch 1 does not shard)."""
+    from paper_2304_09049_b200 import netrun
+    r = netrun.ResNet18Runner("cuda", variant=args.variant, batch=args.batch or 1)
+    for _ in range(max(1, args.warmup)):
+        r.step()
+    torch.cuda.synchronize()
+    graph = torch.cuda.CUDAGraph()
+    with torch.cuda.graph(graph):
+        r.step()
+    for _ in range(args.warmup):
+        graph.replay()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        e0.record()
+        for _ in range(args.steps):
+            graph.replay()
+        e1.record()
+        torch.cuda.synchronize()
+    barrier(ws)
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps, ws)
+    value = r.total_ops * ws / (ms * 1e-3) / 1e12
+    if rank == 0:
+        pk = peaks()
+        line = {"metric": METRIC, "value": round(value, 2), "unit": "TOPS", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms, 4), "us_per_image": round(ms * 1e3 / r.B, 2),
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int8",
+                "data": "synthetic (seeded counter-based 2-bit codes; calibrated requant, synth_data/)",
+                "config": {"workload": f"resnet18_b{r.B}_chain (BASELINE configs[1])", "layers": len(r.layers),
+                           "parallelism": f"{ws} independent replicas"},
+                "roofline": {"bound": "latency", "achieved": round(value / ws, 2), "peak": round(pk["i8_sustained"], 1),
+                             "unit": "TOPS", "frac": round(value / ws / pk["i8_sustained"], 5)},
+                "gpu_launches": r.launches() * args.steps, "clocks": clk.summary()}
+        print(json.dumps(line), flush=True)
+
+
+# ---------------------------------------------------------------- config 5: square LUT-GEMM
+def run_gemm(args, ws, rank, local):
+    """BJ configs[4]: C[n][n] = sum_k T[(W<<2)|A] with learned-style int16 levels (Q17), int32 out.
+    Output channels (rows of W / C) are split across ranks; the int32 row blocks are all-gathered
+    over NCCL so every rank holds C.  Reports compute-only and end-to-end TOPS."""
+    import synth
+    from paper_2304_09049_b200 import dg
+    n = args.n
+    if n % ws:
+        raise SystemExit("n must be divisible by the number of GPUs")
+    m_loc = n // ws
+    wl, al = synth.learned_levels(5, 0, synth.T_LEVELS)
+    lut = dg.build_lut(wl, al, 16)
+    dev = "cuda"
+    ld = dg.packed_ld(n)
+    # codes: W rows [rank*m_loc, (rank+1)*m_loc), A^T all n rows; counter generator (same on CPU)
+    w_codes = synth.counter_codes(rank * m_loc * n, m_loc * n, (5, n, synth.T_W), "uniform", dev).view(m_loc, n)
+    w = dg.pack_weights(w_codes)
+    del w_codes
+    at = torch.empty((n, ld), dtype=torch.uint8, device=dev)
+    chunk = max(1, (1 << 26) // n)
+    for r0 in range(0, n, chunk):
+        r1 = min(n, r0 + chunk)
+        c = synth.counter_codes(r0 * n, (r1 - r0) * n, (5, n, synth.T_A), "uniform", dev).view(r1 - r0, n)
+        dg.pack_codes(c, out=at[r0:r1])
+    at8 = dg.expand_operand(at, n, al)          # offline expansion of the second operand
+    c_loc = torch.empty((m_loc, n), dtype=torch.int32, device=dev)
+    c_full = torch.empty((n, n), dtype=torch.int32, device=dev) if ws > 1 else c_loc
+    ops_total = 2 * n * n * n
+
+    def step(gather=True):
+        dg.lut_gemm_prepared(w, at8, m_loc, n, n, lut, out=c_loc)
+        if ws > 1 and gather:
+            import torch.distributed as dist
+            dist.all_gather_into_tensor(c_full, c_loc)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    # L2 is flushed between steps by the 1 GiB int32 output of n=16384 itself; for smaller n a
+    # 256 MB scratch write is issued between steps (outside the events).
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if n < 16384 else None
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t_comp = 0.0
+    t_all = 0.0
+    barrier(ws)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        for _ in range(args.steps):
+            if flush is not None:
+                flush.zero_()
+            barrier(ws)
+            e0.record()
+            dg.lut_gemm_prepared(w, at8, m_loc, n, n, lut, out=c_loc)
+            e1.record()
+            if ws > 1:
+                import torch.distributed as dist
+                dist.all_gather_into_tensor(c_full, c_loc)
+            g1.record()
+            torch.cuda.synchronize()
+            t_comp += e0.elapsed_time(e1)
+            t_all += e0.elapsed_time(g1)
+    barrier(ws)
+    ms_comp = max_over_ranks(t_comp / args.steps, ws)
+    ms_all = max_over_ranks(t_all / args.steps, ws)
+    pk = peaks()
+    value = ops_total / (ms_all * 1e-3) / 1e12
+    comp_tops = ops_total / (ms_comp * 1e-3) / 1e12
+    per_gpu = (2 * m_loc * n * n) / (t_comp / args.steps * 1e-3) / 1e12
+    # parity: exact Freivalds check of this rank's rows (4 trials) + 2 sampled rows vs the oracle
+    parity = None
+    if not args.no_oracle and rank == 0:
+        import oracle
+        C = c_loc.cpu().numpy()
+        Wc = synth.counter_codes(rank * m_loc * n, m_loc * n, (5, n, synth.T_W), "uniform", "cpu").view(m_loc, n).numpy()
+        Atc = synth.counter_codes(0, n * n, (5, n, synth.T_A), "uniform", "cpu").view(n, n).numpy()
+        T = oracle.build_lut16(wl, al)
+        bad = oracle.freivalds_rows(Wc, Atc, C, T, trials=2)
+        rows = [0, m_loc - 1]
+        ref = oracle.lut_gemm(Wc[rows], np.ascontiguousarray(Atc.T), T)
+        parity = {"freivalds_bad_rows": bad, "sampled_rows_equal": bool(np.array_equal(ref, C[rows])),
+                  "status": "bit-exact" if bad == 0 and np.array_equal(ref, C[rows]) else "MISMATCH"}
+    if rank == 0:
+        alg_bytes = m_loc * ld + n * ld + 4 * m_loc * n
+        line = {"metric": METRIC, "value": round(value, 2), "unit": "TOPS", "n_gpus": ws, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": round(ms_all, 4), "higher_is_better": True,
+                "scaling": "strong", "vs_baseline": None, "dtype": "int8",
+                "data": "synthetic (seeded counter-based 2-bit codes; learned-style int16 levels, Q17)",
+                "config": {"workload": f"square_gemm_n{n} (BASELINE configs[4])", "n": n,
+                           "split": f"output channels / {ws} + NCCL all_gather of int32 rows" if ws > 1 else "none",
+                           "l2": "1 GiB int32 output per step (> L2)" if flush is None else "256 MB L2 flush between steps"},
+                "compute_only": {"value": round(comp_tops, 2), "ms": round(ms_comp, 4), "per_gpu_tops": round(per_gpu, 2)},
+                "roofline": {"bound": "tensor", "kernel": "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)",
+                             "achieved": round(per_gpu, 1), "peak": round(pk["i8_sustained"], 1), "unit": "TOPS",
+                             "frac": round(per_gpu / pk["i8_sustained"], 4),
+                             "frac_vs_burst_peak": round(per_gpu / pk["i8_burst"], 4),
+                             "alg_bytes_per_launch": alg_bytes, "traffic": None},
+                "gpu_launches": args.steps, "clocks": clk.summary(), "parity": parity}
+        print(json.dumps(line), flush=True)
+
+
 # ---------------------------------------------------------------- reference arm (the oracle)
 def run_reference(args, ws, rank):
     """--impl reference: the oracle as it stands, on the host cores, on the same config /
@@ -324,10 +468,11 @@ def run_reference(args, ws, rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--workload", default="resnet50", choices=["resnet50", "vgg16"])
+    ap.add_argument("--workload", default="resnet50", choices=["resnet50", "vgg16", "gemm", "resnet18"])
+    ap.add_argument("--n", type=int, default=16384, help="config 5 GEMM size (4096 / 8192 / 16384)")
     ap.add_argument("--variant", default="auto", choices=["auto", "cc", "tc"])
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
@@ -342,7 +487,12 @@ def main():
         import torch.distributed as dist
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     try:
-        run_conv(args, ws, rank, local)
+        if args.workload == "gemm":
+            run_gemm(args, ws, rank, local)
+        elif args.workload == "resnet18":
+            run_resnet18(args, ws, rank, local)
+        else:
+            run_conv(args, ws, rank, local)
     finally:
         if ws > 1:
             import torch.distributed as dist

@@ -168,3 +168,78 @@ class NetRunner:
 
     def weight_bytes(self) -> int:
         return sum(p.w.numel() for p in self.plans)
+
+
+class ResNet18Runner:
+    """BASELINE config 2: the 19 LUT convs of ResNet-18 at batch 1, CHAINED: each basic block is
+    conv1 (fused requant) -> conv2 (+ residual in int32, fused requant); the residual is the
+    block input's levels x res_mult (identity, over packed codes) or the int32 accumulator of
+    the 1x1 stride-2 downsample conv (reading Q13).  All through dg_lut_conv2d."""
+
+    def __init__(self, device="cuda", variant="auto", batch: int = 1):
+        s = _synth()
+        self.cfg = 2
+        self.B = batch
+        self.variant = variant
+        self.layers = s.resnet18_layers()
+        self.blocks = s.resnet18_blocks()
+        rqs = s.resnet18_requants()
+        wl, al = s.WL_UNIFORM, s.AL_UNIFORM
+        self.lut = dg.build_lut(wl, al, 8)
+        self.w = {}
+        self.params = {}
+        self.rq = {}
+        self.res_mult = {}
+        self.bias = {}
+        ws_need = 0
+        for li, L in enumerate(self.layers):
+            self.w[li] = pack_conv_weights(weight_codes(2, li, L, device))
+            p = dg.conv_params(batch, L.h, L.h, L.cin, L.cout, L.k, L.k, L.stride, L.pad, 0, ldw=self.w[li].shape[1])
+            self.params[li] = p
+            ws_need = max(ws_need, dg.conv_workspace_size(p))
+            r, rm = rqs[li]
+            self.rq[li] = r
+            self.res_mult[li] = rm
+            if r is not None:
+                self.bias[li] = torch.full((L.cout,), r.bias, dtype=torch.int32, device=device)
+        self.ws = torch.empty(ws_need, dtype=torch.uint8, device=device)
+        L0 = self.layers[0]
+        self.x0 = pack_nhwc(input_codes(2, 0, L0, list(range(batch)), device))   # stands in for the stem output (Q14)
+        self.bufs = []
+        for c1, c2, ds in self.blocks:
+            L1, L2 = self.layers[c1], self.layers[c2]
+            y1 = torch.empty((batch * L1.ho * L1.ho, L1.cout // 4), dtype=torch.uint8, device=device)
+            out = torch.empty((batch * L2.ho * L2.ho, L2.cout // 4), dtype=torch.uint8, device=device)
+            racc = None
+            if ds is not None:
+                Ld = self.layers[ds]
+                racc = torch.empty((batch * Ld.ho * Ld.ho, Ld.cout), dtype=torch.int32, device=device)
+            self.bufs.append((y1, out, racc))
+        self.total_ops = sum(2 * L.cout * batch * L.ho * L.ho * L.K for L in self.layers)
+
+    def _rq(self, li, **kw):
+        r = self.rq[li]
+        return dg.Requant(r.mult, r.shift, r.zp, r.qmin, r.qmax, bias=self.bias[li], bias_axis=0, **kw)
+
+    def step(self, stream=None):
+        x = self.x0
+        for (c1, c2, ds), (y1, out, racc) in zip(self.blocks, self.bufs):
+            dg.lut_conv2d(x, self.w[c1], self.lut, self.params[c1], rq=self._rq(c1), variant=self.variant,
+                          out=y1, ws=self.ws, stream=stream)
+            if ds is not None:
+                dg.lut_conv2d(x, self.w[ds], self.lut, self.params[ds], rq=None, variant=self.variant, out=racc,
+                              ws=self.ws, stream=stream)
+                rq2 = self._rq(c2, res=racc)
+            else:
+                rq2 = self._rq(c2, res_codes=x, res_mult=self.res_mult[c2], res_levels=_synth().AL_UNIFORM)
+            dg.lut_conv2d(y1, self.w[c2], self.lut, self.params[c2], rq=rq2, variant=self.variant, out=out,
+                          ws=self.ws, stream=stream)
+            x = out
+        return x
+
+    def launches(self) -> int:
+        n = 0
+        for li, L in enumerate(self.layers):
+            direct = L.k == 1 and L.stride == 1 and L.pad == 0 and (L.cin // 4) % 16 == 0
+            n += 2 if direct else 3    # (im2col) + weight expansion + GEMM
+        return n

@@ -257,3 +257,61 @@ def counter_codes(start: int, count: int, key, dist: str = "uniform", device="cp
     half = 1 << 31
     nz = 1 + (((r - half).clamp(min=0) * 3) >> 31)
     return torch.where(r < half, torch.zeros_like(r), nz).to(torch.uint8)
+
+
+def counter_codes_chunked(start: int, count: int, key, dist: str = "uniform", device="cpu", chunk: int = 1 << 24):
+    """counter_codes for large counts without int64 temporaries of the full size."""
+    import torch
+    out = torch.empty(count, dtype=torch.uint8, device=device)
+    for s in range(0, count, chunk):
+        e = min(count, s + chunk)
+        out[s:e] = counter_codes(start + s, e - s, key, dist, device)
+    return out
+
+
+# ---------------------------------------------------------------------------
+# Config 2 (ResNet-18 at batch 1, chained, residual adds in int32 before requant; Q13)
+
+def resnet18_blocks():
+    """[(conv1, conv2, downsample_or_None)] of the 8 basic blocks (indices into resnet18_layers())."""
+    L = resnet18_layers()
+    blocks, i = [], 0
+    while i < len(L):
+        c1, c2 = i, i + 1
+        ds = i + 2 if i + 2 < len(L) and L[i + 2].role == "ds" else None
+        blocks.append((c1, c2, ds))
+        i += 3 if ds is not None else 2
+    return blocks
+
+
+def resnet18_requants():
+    """Per-layer requant (Q12) and per-block residual scale (Q13).  Uses the calibration in
+    synth_data/resnet18_requant.json (written by tools/calibrate_resnet18.py from the CPU oracle
+    chain only) when present; otherwise analytic values from the input distribution."""
+    import json
+    import os
+    path = os.path.join(os.path.dirname(os.path.abspath(__file__)), "synth_data", "resnet18_requant.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)["layers"]
+        return {int(k): ((None if v["mult"] == 0 else Requant(v["mult"], v["shift"], v["zp"], 0, 3, v["bias"])),
+                         v["res_mult"]) for k, v in d.items()}
+    L = resnet18_layers()
+    out = {}
+    ea, ea2 = level_moments(AL_UNIFORM, P_RELU)
+    var_a = ea2 - ea * ea
+    ew, ew2 = level_moments(WL_UNIFORM, P_UNIFORM)
+    for c1, c2, ds in resnet18_blocks():
+        out[c1] = (conv_requant(L[c1]), 0)
+        K2 = L[c2].K
+        sig2 = math.sqrt(K2 * (ew2 * ea2 - (ew * ea) ** 2))
+        if ds is None:
+            res_mult = max(1, int(round(sig2 / math.sqrt(var_a))))
+            extra_mean, extra_var = res_mult * ea, res_mult * res_mult * var_a
+        else:
+            res_mult = 0
+            Kd = L[ds].K
+            extra_mean, extra_var = Kd * ew * ea, Kd * (ew2 * ea2 - (ew * ea) ** 2)
+            out[ds] = (None, 0)
+        out[c2] = (requant_for(K2, P_RELU, 1.5, zp=0, extra_var=extra_var, extra_mean=extra_mean), res_mult)
+    return out
