@@ -110,12 +110,8 @@ def dist_env():
 
 
 def max_over_ranks(v: float, ws: int) -> float:
-    if ws == 1:
-        return v
-    import torch.distributed as dist
-    t = torch.tensor([v], dtype=torch.float64, device="cuda")
-    dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    return float(t.item())
+    from paper_2304_09049_b200 import shard
+    return shard.max_over_ranks(v, ws, device="cuda")
 
 
 def barrier(ws):
@@ -164,7 +160,8 @@ def run_conv(args, ws, rank, local):
     from paper_2304_09049_b200 import dg, netrun
     cfg = {"resnet50": 3, "vgg16": 4}[args.workload]
     batch = args.batch or synth.CONFIG_BATCH[cfg]
-    images = list(range(rank * batch, (rank + 1) * batch))   # weak scaling: disjoint shards
+    from paper_2304_09049_b200 import shard
+    images = list(shard.batch_shard(rank, ws, batch))         # weak scaling: disjoint shards
     torch.cuda.synchronize()
     runner = netrun.NetRunner(cfg, images, "cuda", variant=args.variant)
     nl = len(runner.plans)
@@ -336,11 +333,10 @@ def run_gemm(args, ws, rank, local):
     Output channels (rows of W / C) are split across ranks; the int32 row blocks are all-gathered
     over NCCL so every rank holds C.  Reports compute-only and end-to-end TOPS."""
     import synth
-    from paper_2304_09049_b200 import dg
+    from paper_2304_09049_b200 import dg, shard
     n = args.n
-    if n % ws:
-        raise SystemExit("n must be divisible by the number of GPUs")
-    m_loc = n // ws
+    r0, r1 = shard.row_shard(rank, ws, n)
+    m_loc = r1 - r0
     wl, al = synth.learned_levels(5, 0, synth.T_LEVELS)
     lut = dg.build_lut(wl, al, 16)
     dev = "cuda"
@@ -363,8 +359,7 @@ def run_gemm(args, ws, rank, local):
     def step(gather=True):
         dg.lut_gemm_prepared(w, at8, m_loc, n, n, lut, out=c_loc)
         if ws > 1 and gather:
-            import torch.distributed as dist
-            dist.all_gather_into_tensor(c_full, c_loc)
+            shard.gather_rows(c_loc, ws, out=c_full)
 
     for _ in range(args.warmup):
         step()
@@ -387,8 +382,7 @@ def run_gemm(args, ws, rank, local):
             dg.lut_gemm_prepared(w, at8, m_loc, n, n, lut, out=c_loc)
             e1.record()
             if ws > 1:
-                import torch.distributed as dist
-                dist.all_gather_into_tensor(c_full, c_loc)
+                shard.gather_rows(c_loc, ws, out=c_full)
             g1.record()
             torch.cuda.synchronize()
             t_comp += e0.elapsed_time(e1)
