@@ -100,48 +100,56 @@ __global__ void quantize_pack_kernel(const float *__restrict__ x, int64_t rows, 
 }
 
 // ---- S3: packed im2col.  Each output row = kh*kw taps of C/4 bytes, then zeros to ld.
-// V = bytes moved per thread (16 when C/4 % 16 == 0, 4 when % 4 == 0, else 1).
+// Block = (VPR vectors of V bytes per row) x (rows); 32-bit index math; the (b, ho, wo)
+// decomposition is done once per row.  V = 16 when C/4 % 16 == 0, 4 when % 4 == 0, else 1.
 template <int V>
-__global__ void im2col_kernel(const uint8_t *__restrict__ x, int32_t B, int32_t H, int32_t W,
-                              int32_t Cb, int32_t kh, int32_t kw, int32_t stride, int32_t pad,
-                              uint32_t pad_byte, int32_t Ho, int32_t Wo, uint8_t *__restrict__ cols,
-                              int64_t ld) {
-    const int64_t vec_per_row = ld / V;
-    const int64_t total = (int64_t)B * Ho * Wo * vec_per_row;
-    const int64_t kb = (int64_t)kh * kw * Cb;  // valid bytes per row
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total;
-         i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t row = i / vec_per_row;
-        const int64_t byte = (i - row * vec_per_row) * V;
-        uint8_t *dst = cols + row * ld + byte;
+__global__ void __launch_bounds__(256) im2col_kernel(const uint8_t *__restrict__ x, int32_t H, int32_t W, int32_t Cb,
+                                                     int32_t kw, int32_t stride, int32_t pad, uint32_t pad_byte,
+                                                     int32_t Ho, int32_t Wo, int32_t rows, int32_t kb,
+                                                     uint8_t *__restrict__ cols, int32_t ld) {
+    const uint32_t vpr = (uint32_t)(ld / V);
+    const uint32_t total = (uint32_t)rows * vpr;
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+        const uint32_t row = i / vpr;
+        const int32_t byte = (int32_t)(i - row * vpr) * V;
+        uint8_t *dst = cols + (int64_t)row * ld + byte;
         if (byte >= kb) {  // K tail: zero codes (dg.h contract)
             if constexpr (V == 16) *reinterpret_cast<uint4 *>(dst) = make_uint4(0, 0, 0, 0);
             else if constexpr (V == 4) *reinterpret_cast<uint32_t *>(dst) = 0;
             else *dst = 0;
             continue;
         }
-        const int32_t wo = (int32_t)(row % Wo);
-        const int64_t t = row / Wo;
-        const int32_t ho = (int32_t)(t % Ho);
-        const int32_t b = (int32_t)(t / Ho);
-        const int32_t tap = (int32_t)(byte / Cb);
-        const int32_t cb = (int32_t)(byte - (int64_t)tap * Cb);
-        const int32_t r = tap / kw, s = tap - (tap / kw) * kw;
+        const uint32_t t = row / (uint32_t)Wo;
+        const int32_t wo = (int32_t)(row - t * (uint32_t)Wo);
+        const uint32_t b = t / (uint32_t)Ho;
+        const int32_t ho = (int32_t)(t - b * (uint32_t)Ho);
+        const int32_t tap = byte / Cb;
+        const int32_t cb = byte - tap * Cb;
+        const int32_t r = tap / kw, s = tap - r * kw;
         const int32_t hi = ho * stride - pad + r, wi = wo * stride - pad + s;
-        const bool in = hi >= 0 && hi < H && wi >= 0 && wi < W;
+        const bool in = (uint32_t)hi < (uint32_t)H && (uint32_t)wi < (uint32_t)W;
         const uint8_t *src = x + (((int64_t)b * H + hi) * W + wi) * Cb + cb;
         if constexpr (V == 16) {
-            uint4 v = in ? __ldg(reinterpret_cast<const uint4 *>(src))
-                         : make_uint4(pad_byte, pad_byte, pad_byte, pad_byte);
-            *reinterpret_cast<uint4 *>(dst) = v;
+            const uint4 val = in ? __ldg(reinterpret_cast<const uint4 *>(src)) : make_uint4(pad_byte, pad_byte, pad_byte, pad_byte);
+            *reinterpret_cast<uint4 *>(dst) = val;
         } else if constexpr (V == 4) {
             *reinterpret_cast<uint32_t *>(dst) = in ? __ldg(reinterpret_cast<const uint32_t *>(src)) : pad_byte;
         } else {
-            // a byte may straddle the valid-K boundary only if Cb is not a whole byte multiple;
-            // Cb is whole bytes (C % 4 == 0), so no partial bytes exist.
             *dst = in ? __ldg(src) : (uint8_t)pad_byte;
         }
     }
+}
+
+template <int V>
+void launch_im2col(const uint8_t *x, int32_t B, int32_t H, int32_t W, int32_t Cb, int32_t kh, int32_t kw, int32_t stride,
+                   int32_t pad, uint32_t pad_byte, int32_t Ho, int32_t Wo, uint8_t *cols, int64_t ld, cudaStream_t st) {
+    const int32_t rows = B * Ho * Wo;
+    const int64_t total = (int64_t)rows * (ld / V);
+    int64_t blocks = (total + 255) / 256;
+    const int64_t cap = (int64_t)num_sms() * 16;
+    if (blocks > cap) blocks = cap;
+    im2col_kernel<V><<<(int)blocks, 256, 0, st>>>(x, H, W, Cb, kw, stride, pad, pad_byte, Ho, Wo, rows, kh * kw * Cb,
+                                                  cols, (int32_t)ld);
 }
 
 // ---- S7 standalone: one thread per output byte (4 columns).
@@ -232,16 +240,14 @@ dg_status dg_im2col(const uint8_t *d_x, int32_t B, int32_t H, int32_t W, int32_t
     if (ld % 16 != 0 || ld < (int64_t)kh * kw * Cb || ((uintptr_t)d_cols & 15)) return DG_ERR_INVALID_ARG;
     const uint32_t pb = pad_code | (pad_code << 2) | (pad_code << 4) | (pad_code << 6);
     const int64_t rows = (int64_t)B * Ho * Wo;
+    if (rows * (ld / 1) > (int64_t)UINT32_MAX || ld > INT32_MAX / 2) return DG_ERR_SHAPE;
     cudaStream_t st = (cudaStream_t)stream;
     if (Cb % 16 == 0 && ((uintptr_t)d_x & 15) == 0) {
-        im2col_kernel<16><<<grid_for(rows * (ld / 16)), kThreads, 0, st>>>(
-            d_x, B, H, W, Cb, kh, kw, stride, pad, pb * 0x01010101u, Ho, Wo, d_cols, ld);
+        launch_im2col<16>(d_x, B, H, W, Cb, kh, kw, stride, pad, pb * 0x01010101u, Ho, Wo, d_cols, ld, st);
     } else if (Cb % 4 == 0 && ((uintptr_t)d_x & 3) == 0) {
-        im2col_kernel<4><<<grid_for(rows * (ld / 4)), kThreads, 0, st>>>(
-            d_x, B, H, W, Cb, kh, kw, stride, pad, pb * 0x01010101u, Ho, Wo, d_cols, ld);
+        launch_im2col<4>(d_x, B, H, W, Cb, kh, kw, stride, pad, pb * 0x01010101u, Ho, Wo, d_cols, ld, st);
     } else {
-        im2col_kernel<1><<<grid_for(rows * ld), kThreads, 0, st>>>(d_x, B, H, W, Cb, kh, kw, stride,
-                                                                    pad, pb, Ho, Wo, d_cols, ld);
+        launch_im2col<1>(d_x, B, H, W, Cb, kh, kw, stride, pad, pb, Ho, Wo, d_cols, ld, st);
     }
     return launch_status();
 }
