@@ -196,7 +196,9 @@ DG_API dg_status dg_lut_gemm_prepared(const uint8_t *d_w, int64_t ldw, const int
 
 /* ---------------------------------------------------------------------------
  * Convolution over packed NHWC codes = im2col (S3) + LUT GEMM (S5) + fused
- * requant (S7), output NHWC (conv layers are run as (M,N,K) GEMMs):
+ * requant (S7), output NHWC (conv layers are run as (M,N,K) GEMMs).
+ * On the tc path, convs whose C/4 is a power of two >= 16 skip the im2col matrix
+ * (implicit GEMM: the kernel gathers each output pixel's taps):
  *      out[b][ho][wo][co] = sum_{r,s,c} T[(w[co][r][s][c] << 2) | x(b, ho*st-pad+r, wo*st-pad+s, c)]
  * d_x: [B][H][W][C/4] packed; d_w: [Cout][ldw] packed rows of K = kh*kw*C codes
  * in (r,s,c) order.  Output: rq == NULL -> int32 [B*Ho*Wo][Cout];
@@ -212,6 +214,14 @@ DG_API size_t dg_lut_conv2d_workspace_size(const dg_conv_params *p);
 DG_API dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_lut *lut,
                         const dg_conv_params *p, const dg_requant *rq, void *d_out, void *d_ws,
                         size_t ws_bytes, int32_t variant, void *stream);
+
+/* Convolution with offline-expanded weights (tc path only): d_w8 = dg_expand_operand(weights,
+ * levels = lut->wl) [Cout][ld8].  1x1/stride-1 convs read x directly; convs whose C/4 is a
+ * power of two >= 16 run as an implicit GEMM (the kernel gathers each output pixel's taps from
+ * x; no im2col matrix); others use dg_im2col into d_ws (dg_lut_conv2d_workspace_size bytes). */
+DG_API dg_status dg_lut_conv2d_prepared(const uint8_t *d_x, const int8_t *d_w8, int64_t ld8, const dg_lut *lut,
+                                 const dg_conv_params *p, const dg_requant *rq, void *d_out, void *d_ws,
+                                 size_t ws_bytes, void *stream);
 
 #ifdef __cplusplus
 }

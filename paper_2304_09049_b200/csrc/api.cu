@@ -172,6 +172,13 @@ dg_status dg_lut_gemm_prepared(const uint8_t *d_w, int64_t ldw, const int8_t *d_
                        (cudaStream_t)stream);
 }
 
+static bool conv_implicit_ok(const dg_conv_params *p, const uint8_t *d_x) {
+    // the tensor-core kernel gathers im2col rows itself when a tap is a power-of-two number of
+    // 16-byte chunks (C = 64, 128, 256, ... channels)
+    const int32_t cb = p->C / 4;
+    return cb >= 16 && (cb & (cb - 1)) == 0 && aligned16(d_x) && p->kh * p->kw <= 64;
+}
+
 static bool conv_is_direct(const dg_conv_params *p) {
     // a 1x1 / stride-1 / unpadded conv reads the NHWC tensor as its own im2col matrix
     return p->kh == 1 && p->kw == 1 && p->stride == 1 && p->pad == 0 && (p->C / 4) % 16 == 0;
@@ -184,7 +191,7 @@ size_t dg_lut_conv2d_workspace_size(const dg_conv_params *p) {
     const int64_t Ho = (p->H + 2 * p->pad - p->kh) / p->stride + 1;
     const int64_t Wo = (p->W + 2 * p->pad - p->kw) / p->stride + 1;
     const int64_t K = (int64_t)p->kh * p->kw * p->C;
-    const int64_t cols = conv_is_direct(p) ? 0 : (int64_t)p->B * Ho * Wo * dg_packed_ld(K);
+    const int64_t cols = conv_is_direct(p) ? 0 : (int64_t)p->B * Ho * Wo * dg_packed_ld(K);   // upper bound
     return (size_t)((cols + 127) / 128 * 128 + (int64_t)p->Cout * expand_ld(K) + 256);
 }
 
@@ -208,6 +215,20 @@ dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_lut *lu
     if (K * max_abs_entry(lut->entries) >= ((int64_t)1 << 31)) return DG_ERR_OVERFLOW;
     cudaStream_t st = (cudaStream_t)stream;
     const int64_t rows = (int64_t)p->B * Ho * Wo;
+    const bool tc_ok = lut->is_product && levels_fit_i8(lut->wl) && levels_fit_i8(lut->al) && tc_available();
+    if ((variant == 0 || variant == 2) && tc_ok && !conv_is_direct(p) && conv_implicit_ok(p, d_x)) {
+        // implicit GEMM: no im2col matrix; weights expanded into the workspace
+        const int64_t ld8 = expand_ld(K);
+        int8_t *w8 = (int8_t *)(((uintptr_t)d_ws + 127) & ~(uintptr_t)127);
+        if (!d_ws || (int64_t)ws_bytes - (int64_t)((uint8_t *)w8 - (uint8_t *)d_ws) < p->Cout * ld8) return DG_ERR_WORKSPACE;
+        s = expand_operand(d_w, p->Cout, K, p->ldw, lut->wl, w8, ld8, st);
+        if (s != DG_OK) return s;
+        RequantArgs ra{};
+        if (rq) ra = to_args(rq);
+        TsConv cv{d_x, p->H, p->W, p->C / 4, p->kh, p->kw, p->stride, p->pad, (int32_t)Ho, (int32_t)Wo, p->pad_code};
+        return lut_gemm_ts(nullptr, 0, w8, ld8, rows, p->Cout, K, lut->al, lut->wl, d_out, rq ? p->Cout / 4 : p->Cout,
+                           rq ? &ra : nullptr, st, &cv);
+    }
     const uint8_t *P;
     int64_t ldp;
     if (conv_is_direct(p) && aligned16(d_x)) {
@@ -240,6 +261,46 @@ dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_lut *lu
     }
     return gemm_dispatch(P, ldp, d_w, p->ldw, rows, p->Cout, K, Tt, lut->is_product != 0, lut->al,
                          lut->wl, d_out, ldd, rq, ws_rest, rest, variant, st);
+}
+
+dg_status dg_lut_conv2d_prepared(const uint8_t *d_x, const int8_t *d_w8, int64_t ld8, const dg_lut *lut,
+                                 const dg_conv_params *p, const dg_requant *rq, void *d_out, void *d_ws, size_t ws_bytes,
+                                 void *stream) {
+    if (!d_x || !d_w8 || !lut || !p || !d_out) return DG_ERR_INVALID_ARG;
+    if (p->B <= 0 || p->H <= 0 || p->W <= 0 || p->C <= 0 || p->Cout <= 0 || p->kh <= 0 || p->kw <= 0 ||
+        p->stride <= 0 || p->pad < 0)
+        return DG_ERR_SHAPE;
+    if (p->C % 4 || p->pad_code < 0 || p->pad_code > 3) return DG_ERR_RANGE;
+    if (rq && p->Cout % 4) return DG_ERR_SHAPE;
+    const int64_t Ho = (p->H + 2 * p->pad - p->kh) / p->stride + 1;
+    const int64_t Wo = (p->W + 2 * p->pad - p->kw) / p->stride + 1;
+    if (Ho <= 0 || Wo <= 0) return DG_ERR_SHAPE;
+    const int64_t K = (int64_t)p->kh * p->kw * p->C;
+    if (ld8 < expand_ld(K) || ld8 % 128 || ((uintptr_t)d_w8 & 127)) return DG_ERR_SHAPE;
+    dg_status s = check_rq(rq);
+    if (s != DG_OK) return s;
+    if (!lut->is_product || !levels_fit_i8(lut->wl) || !levels_fit_i8(lut->al) || !tc_available())
+        return DG_ERR_UNSUPPORTED;
+    if (K * max_abs_entry(lut->entries) >= ((int64_t)1 << 31)) return DG_ERR_OVERFLOW;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int64_t rows = (int64_t)p->B * Ho * Wo;
+    RequantArgs ra{};
+    if (rq) ra = to_args(rq);
+    const int64_t ldd = rq ? p->Cout / 4 : p->Cout;
+    if (conv_is_direct(p) && aligned16(d_x))
+        return lut_gemm_ts(d_x, p->C / 4, d_w8, ld8, rows, p->Cout, K, lut->al, lut->wl, d_out, ldd, rq ? &ra : nullptr, st);
+    if (conv_implicit_ok(p, d_x)) {
+        TsConv cv{d_x, p->H, p->W, p->C / 4, p->kh, p->kw, p->stride, p->pad, (int32_t)Ho, (int32_t)Wo, p->pad_code};
+        return lut_gemm_ts(nullptr, 0, d_w8, ld8, rows, p->Cout, K, lut->al, lut->wl, d_out, ldd, rq ? &ra : nullptr, st,
+                           &cv);
+    }
+    // explicit im2col fallback (e.g. VGG conv1_1 with C = 4 padded channels)
+    const int64_t ld = dg_packed_ld(K);
+    uint8_t *cols = (uint8_t *)(((uintptr_t)d_ws + 127) & ~(uintptr_t)127);
+    if (!d_ws || (int64_t)ws_bytes - (int64_t)(cols - (uint8_t *)d_ws) < rows * ld) return DG_ERR_WORKSPACE;
+    s = dg_im2col(d_x, p->B, p->H, p->W, p->C, p->kh, p->kw, p->stride, p->pad, (uint8_t)p->pad_code, cols, ld, stream);
+    if (s != DG_OK) return s;
+    return lut_gemm_ts(cols, ld, d_w8, ld8, rows, p->Cout, K, lut->al, lut->wl, d_out, ldd, rq ? &ra : nullptr, st);
 }
 
 }  // extern "C"

@@ -210,7 +210,12 @@ bool tc_available();
 int64_t expand_ld(int64_t K);
 dg_status expand_operand(const uint8_t *packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],
                          int8_t *out, int64_t ld8, cudaStream_t st);
+// implicit-GEMM convolution description for the TS kernel (P = im2col of x, gathered on chip)
+struct TsConv {
+    const uint8_t *x;
+    int32_t H, W, Cb, kh, kw, stride, pad, Ho, Wo, pad_code;
+};
 dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                       const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
-                      cudaStream_t st);
+                      cudaStream_t st, const TsConv *cv = nullptr);
 }  // namespace dg

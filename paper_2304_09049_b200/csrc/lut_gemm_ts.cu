@@ -98,7 +98,26 @@ struct TsArgs {
     int64_t ldd;
     int32_t has_rq, fast_rq, dir;
     int32_t thr[3];
+    // implicit-GEMM convolution (P = im2col of an NHWC packed input, gathered per thread)
+    int32_t implicit;
+    const uint8_t *X;      // [B][H][W][Cb] packed codes, Cb = C/4 a power of two >= 16
+    int32_t H, W, Cb_log2, kw_recip, kw, stride, pad, Ho, Wo, kb;
+    uint32_t pad_word;     // pad byte replicated x4
 };
+
+// Implicit im2col: 16 bytes (64 codes) of row p at virtual-im2col byte `byte` (multiple of 16).
+// K order (r, s, c) with c fastest (dg_im2col); out-of-image taps read the pad code.
+DG_DEV uint4 implicit_chunk(const TsArgs &ta, const uint8_t *img, int32_t h0, int32_t w0, int32_t byte) {
+    if (byte >= ta.kb) return make_uint4(0, 0, 0, 0);   // beyond K: multiplied by 0 weights
+    const int32_t tap = byte >> ta.Cb_log2;
+    const int32_t off = byte & ((1 << ta.Cb_log2) - 1);
+    const int32_t rr = (tap * ta.kw_recip) >> 16;       // tap / kw (exact for kh*kw <= 64)
+    const int32_t ss = tap - rr * ta.kw;
+    const int32_t hi = h0 + rr, wi = w0 + ss;
+    if ((uint32_t)hi >= (uint32_t)ta.H || (uint32_t)wi >= (uint32_t)ta.W)
+        return make_uint4(ta.pad_word, ta.pad_word, ta.pad_word, ta.pad_word);
+    return __ldg(reinterpret_cast<const uint4 *>(img + (((int64_t)hi * ta.W + wi) << ta.Cb_log2) + off));
+}
 
 DG_DEV void store_codes32_ts(uint8_t *dp, uint32_t o0, uint32_t o1, int nbytes) {
 #pragma unroll
@@ -211,7 +230,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 const int64_t p0 = (int64_t)(t / ta.ntq) * BM, q0 = (int64_t)(t % ta.ntq) * BN;
                 int sub = 0, ps = 0;
                 for (int s = 0; s < ta.nstages; ++s, ++gb) {
-                    if (sub == 0) {   // next packed P stage (up to 512 codes of every row)
+                    if (sub == 0 && !ta.implicit) {   // next packed P stage (up to 512 codes of every row)
                         const int slot = gp % SP;
                         ptx::mbar_wait(empty_p(slot), ((gp / SP) & 1u) ^ 1u);
                         const uint32_t dst = sbase + C::OFF_P + slot * C::P_BYTES;
@@ -296,6 +315,20 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         uint32_t g = 0, gp = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             int sub = 0;
+            // implicit conv: this thread's output pixel of the tile
+            const uint8_t *img = ta.X;
+            int32_t h0 = 0, w0 = 0;
+            if (ta.implicit) {
+                const int64_t p = (int64_t)(t / ta.ntq) * BM + r;
+                const int64_t pp = p < ta.np ? p : ta.np - 1;
+                const int32_t wo = (int32_t)(pp % ta.Wo);
+                const int64_t tt = pp / ta.Wo;
+                const int32_t ho = (int32_t)(tt % ta.Ho);
+                const int64_t b = tt / ta.Ho;
+                img = ta.X + ((b * ta.H * ta.W) << ta.Cb_log2);
+                h0 = ho * ta.stride - ta.pad;
+                w0 = wo * ta.stride - ta.pad;
+            }
             for (int s = 0; s < ta.nstages; ++s, ++g) {
                 const uint32_t my_gp = gp;
                 const int this_sub = sub;
@@ -303,10 +336,14 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 if ((int)(g & (NUM_UGROUPS - 1)) != grp) continue;
                 const int sp = my_gp % SP, sa = g % SA;
                 const bool two = (s != ta.nstages - 1) || ta.last_ksteps > 2;   // second 64-code half used
+                uint4 v0, v1;
+                if (ta.implicit) {
+                    v0 = implicit_chunk(ta, img, h0, w0, s * 32);
+                    v1 = two ? implicit_chunk(ta, img, h0, w0, s * 32 + 16) : make_uint4(0, 0, 0, 0);
+                } else {
                 ptx::mbar_wait(full_p(sp), (my_gp / SP) & 1u);
                 const int sub_ = this_sub;
                 const uint8_t *row = smem + C::OFF_P + sp * C::P_BYTES + r * ta.pks;
-                uint4 v0, v1;
                 if (ta.bulk) {
                     v0 = *reinterpret_cast<const uint4 *>(row + sub_ * 32);
                     v1 = two ? *reinterpret_cast<const uint4 *>(row + sub_ * 32 + 16) : make_uint4(0, 0, 0, 0);
@@ -320,6 +357,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     ptx::mbar_arrive(empty_p(sp));
                     for (int e = 0; e < extra; ++e) ptx::mbar_arrive(empty_p(sp));
                 }
+                }   // !implicit
                 uint32_t a[32];
                 const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
@@ -499,7 +537,7 @@ bool make_map_sw128(CUtensorMap *m, const void *base, int64_t ld, int64_t rows, 
 template <int BN, int NEPI>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
-                    cudaStream_t st) {
+                    cudaStream_t st, const TsConv *cv) {
     using C = TsCfg<BN>;
     int64_t acc_bound = 0;   // K * max |pl[a] * ql[b]|
     for (int a = 0; a < 4; ++a)
@@ -535,9 +573,27 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
             ta.thr[j] = (int32_t)(u > LIM ? LIM : (u < -LIM ? -LIM : u));
         }
     }
+    if (cv) {
+        ta.implicit = 1;
+        ta.X = cv->x;
+        ta.H = cv->H;
+        ta.W = cv->W;
+        int lg = 0;
+        while ((1 << lg) < cv->Cb) ++lg;
+        ta.Cb_log2 = lg;
+        ta.kw = cv->kw;
+        ta.kw_recip = (65536 + cv->kw - 1) / cv->kw;
+        ta.stride = cv->stride;
+        ta.pad = cv->pad;
+        ta.Ho = cv->Ho;
+        ta.Wo = cv->Wo;
+        ta.kb = cv->kh * cv->kw * cv->Cb;
+        ta.pad_word = 0x01010101u * (uint32_t)(cv->pad_code | (cv->pad_code << 2) | (cv->pad_code << 4) | (cv->pad_code << 6));
+        ta.bulk = 0;
+    }
     CUtensorMap mp, mb;
     memset(&mp, 0, sizeof(mp));
-    if (!ta.bulk && !make_map_sw128(&mp, P, ldp, np, BM)) return DG_ERR_CUDA;
+    if (!cv && !ta.bulk && !make_map_sw128(&mp, P, ldp, np, BM)) return DG_ERR_CUDA;
     if (!make_map_sw128(&mb, Q8, ld8, nq, BN)) return DG_ERR_CUDA;
     static bool attr_set = false;
     if (!attr_set) {
@@ -571,16 +627,16 @@ dg_status expand_operand(const uint8_t *packed, int64_t rows, int64_t K, int64_t
 
 dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                       const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
-                      cudaStream_t st) {
+                      cudaStream_t st, const TsConv *cv) {
     if (np > ((int64_t)1 << 31) - 1 || nq > ((int64_t)1 << 31) - 1) return DG_ERR_SHAPE;
     // short K (<= 2 stages): the epilogue dominates -> 8 epilogue warps
     const bool short_k = K <= 2 * KS;
     if (nq > 64) {
-        if (short_k) return launch_ts<128, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
-        return launch_ts<128, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
+        if (short_k) return launch_ts<128, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        return launch_ts<128, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     }
-    if (short_k) return launch_ts<64, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
-    return launch_ts<64, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st);
+    if (short_k) return launch_ts<64, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    return launch_ts<64, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 }
 
 }  // namespace dg

@@ -45,6 +45,12 @@ class LayerPlan:
     def cols_ld(self) -> int:
         return dg.packed_ld(self.K)
 
+    @property
+    def implicit(self) -> bool:
+        """tc path gathers im2col rows on chip (dg_lut_conv2d_prepared): C/4 a power of two >= 16."""
+        cb = self.params.C // 4
+        return (not self.direct) and cb >= 16 and (cb & (cb - 1)) == 0 and self.layer.k * self.layer.k <= 64
+
 
 def input_codes(cfg: int, li: int, layer, images, device):
     """NHWC codes [len(images)][h][h][cin] of layer li for global image ids `images`
@@ -132,6 +138,15 @@ class NetRunner:
         n = 0
         for i, p in enumerate(self.plans):
             L = p.layer
+            if p.w8 is not None and (p.direct or p.implicit):
+                # tensor-core path without an im2col matrix (direct 1x1 or implicit GEMM)
+                if gemm_events is not None:
+                    gemm_events[i][0].record()
+                dg.lut_conv2d_prepared(p.x, p.w8, p.lut, p.params, rq=p.rq, out=p.out, stream=stream)
+                if gemm_events is not None:
+                    gemm_events[i][1].record()
+                n += 1
+                continue
             if p.direct:
                 P = p.x
             else:

@@ -230,6 +230,9 @@ CONVS = [  # B, H, W, C, Cout, k, stride, pad, pad_code
     (1, 10, 10, 3, 16, 3, 1, 1, 0),    # VGG conv1_1-like, Cin=3 padded to 4
     (1, 5, 5, 8, 8, 3, 1, 1, 2),       # non-zero pad code
     (3, 14, 14, 128, 64, 3, 1, 1, 0),
+    (2, 9, 9, 64, 32, 3, 1, 1, 2),     # implicit-GEMM path with a non-zero pad code
+    (1, 12, 12, 256, 64, 3, 2, 1, 0),  # implicit, stride 2, C/4 = 64
+    (2, 10, 10, 64, 64, 1, 2, 0, 0),   # implicit 1x1 stride 2 (downsample)
 ]
 
 
@@ -324,3 +327,23 @@ def test_gemm_prepared_and_expand(M, N, K):
     assert np.array_equal(e[:, :Kw].reshape(N, -1, 16), lv)
     C = host(dg.lut_gemm_prepared(w, at8, M, N, K, lut))
     assert np.array_equal(C, oracle.lut_gemm(W, A, oracle.build_lut16(wl, al)))
+
+
+@pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", CONVS)
+def test_conv_prepared_vs_oracle(B, H, W, C, Cout, k, stride, pad, pad_code):
+    """dg_lut_conv2d_prepared (offline-expanded weights; direct / implicit-GEMM / im2col)."""
+    lut = dg.build_lut(WL, AL, 8)
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    g = np.random.default_rng(B * 11 + H + C + Cout + k + pad_code)
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, k, k, C), dtype=np.uint8)
+    exp = oracle.conv2d_direct(x, w, oracle.build_lut16(WL, AL), stride, pad, pad_code)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    Kc = k * k * Cp
+    w8 = dg.expand_operand(wp, Kc, WL)
+    p = dg.conv_params(B, H, W, Cp, Cout, k, k, stride, pad, pad_code, ldw=wp.shape[1])
+    ws = torch.empty(dg.conv_workspace_size(p), dtype=torch.uint8, device=DEV)
+    out = dg.lut_conv2d_prepared(xp, w8, lut, p, ws=ws)
+    assert np.array_equal(host(out).reshape(exp.shape), exp)
