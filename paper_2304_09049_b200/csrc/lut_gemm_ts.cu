@@ -38,16 +38,16 @@ constexpr int NSUB_MAX = PKS_MAX * 4 / KS;   // 4 stages per packed stage
 // NEPI (template) epilogue warps: 4 (one per TMEM lane quarter, all columns; more registers
 // for long-K tiles) or 8 (two per quarter, half the columns each; for short-K tiles, where
 // the epilogue dominates).
-constexpr int NUM_UNPACK_WARPS = 8;
-constexpr int NUM_UGROUPS = 2;
-template <int NEPI>
+// NUNP (template) unpack warps: 4 (one stage group) or 8 (two groups owning alternate stages).
+template <int NEPI, int NUNP>
 struct Roles {
+    static constexpr int NUM_UGROUPS = NUNP / 4;
     static constexpr int EPI_WARP0 = 0;                                   // lane quarter = warp % 4
     static constexpr int UNPACK_WARP0 = EPI_WARP0 + NEPI;                 // lane quarter = warp % 4
-    static constexpr int PRODUCER_WARP = UNPACK_WARP0 + NUM_UNPACK_WARPS;
+    static constexpr int PRODUCER_WARP = UNPACK_WARP0 + NUNP;
     static constexpr int WAITER_WARP = PRODUCER_WARP + 1;
     static constexpr int MMA_WARP = WAITER_WARP + 1;
-    static constexpr int NT = 32 * (MMA_WARP + 1);                        // 480 or 608 threads
+    static constexpr int NT = 32 * (MMA_WARP + 1);
 };
 // An mbarrier probe (or any shared-memory load) issued by the warp that issues tcgen05.mma
 // waits behind that warp's queued MMAs (measured ~670 cycles per probe, tools/mma_bench.cu),
@@ -165,15 +165,16 @@ __device__ __noinline__ void ts_epilogue_general(const TsArgs &ta, const Requant
     store_codes32_ts(dp, o0, o1, (int)((ta.nq - qc + 3) / 4));
 }
 
-template <int BN, int NEPI>
-__global__ void __launch_bounds__(Roles<NEPI>::NT, 1)
+template <int BN, int NEPI, int NUNP>
+__global__ void __launch_bounds__(Roles<NEPI, NUNP>::NT, 1)
 lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
     using C = TsCfg<BN>;
-    using R = Roles<NEPI>;
+    using R = Roles<NEPI, NUNP>;
     constexpr int SP = C::SP, SB = C::SB, SA = C::SA, NACC = C::NACC;
     constexpr int NUM_EPI_WARPS = NEPI, EPI_WARP0 = R::EPI_WARP0, UNPACK_WARP0 = R::UNPACK_WARP0,
-                  PRODUCER_WARP = R::PRODUCER_WARP, WAITER_WARP = R::WAITER_WARP, MMA_WARP = R::MMA_WARP;
+                  PRODUCER_WARP = R::PRODUCER_WARP, WAITER_WARP = R::WAITER_WARP, MMA_WARP = R::MMA_WARP,
+                  NUM_UGROUPS = R::NUM_UGROUPS;
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = ptx::smem_u32(smem);
@@ -198,7 +199,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             ptx::tma_prefetch(&tm_b);
             for (int s = 0; s < SP; ++s) {
                 ptx::mbar_init(full_p(s), 1);
-                ptx::mbar_init(empty_p(s), NSUB_MAX * 4);   // 4 warps per stage, NSUB_MAX stages
+                ptx::mbar_init(empty_p(s), NSUB_MAX * 4);   // 4 warps (one group) per stage, NSUB_MAX stages
             }
             for (int s = 0; s < SB; ++s) {
                 ptx::mbar_init(full_b(s), 1);
@@ -336,6 +337,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 if ((int)(g & (NUM_UGROUPS - 1)) != grp) continue;
                 const int sp = my_gp % SP, sa = g % SA;
                 const bool two = (s != ta.nstages - 1) || ta.last_ksteps > 2;   // second 64-code half used
+                const long long u0 = TS_CLK();
                 uint4 v0, v1;
                 if (ta.implicit) {
                     v0 = implicit_chunk(ta, img, h0, w0, s * 32);
@@ -376,11 +378,13 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(full_a(sa));
+                if (lane == 0 && warp == UNPACK_WARP0) { TS_PROF_ADD(12, TS_CLK() - u0); TS_PROF_ADD(13, 1); }
             }
         }
     } else {
         // ---------------- epilogue (lane quarter = warp % 4, column part = warp / 4)
         constexpr int HALF = BN / (NEPI / 4), NCH = HALF / 32;
+        static_assert(HALF % 32 == 0, "epilogue column part must be a multiple of 32");
         const int quarter = warp & 3, half = (warp - EPI_WARP0) >> 2;
         const bool col_bias = rq.bias && rq.bias_axis == 0;
         uint32_t tl = 0;
@@ -388,7 +392,10 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             const uint32_t acc = tl % NACC;
             const int64_t p = (int64_t)(t / ta.ntq) * BM + quarter * 32 + lane;
             const int64_t q0 = (int64_t)(t % ta.ntq) * BN + half * HALF;
+            const long long e0 = TS_CLK();
             ptx::mbar_wait(acc_full(acc), (tl / NACC) & 1u);
+            const long long e1 = TS_CLK();
+            if (lane == 0 && warp == 0) { TS_PROF_ADD(8, e1 - e0); TS_PROF_ADD(11, 1); }
             ptx::tc_fence_after();
             const uint32_t trow = tmem + acc * BN + half * HALF + ((uint32_t)(quarter * 32) << 16);
             const bool fast = ta.fast_rq && q0 + HALF <= ta.nq;
@@ -453,6 +460,8 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     else store_codes32_ts(dp, o0, o1, 8);
                 }
             }
+            const long long e2 = TS_CLK();
+            if (lane == 0 && warp == 0) TS_PROF_ADD(9, e2 - e1);
         }
     }
 
@@ -534,7 +543,7 @@ bool make_map_sw128(CUtensorMap *m, const void *base, int64_t ld, int64_t rows, 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-template <int BN, int NEPI>
+template <int BN, int NEPI, int NUNP>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                     cudaStream_t st, const TsConv *cv) {
@@ -597,7 +606,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     if (!make_map_sw128(&mb, Q8, ld8, nq, BN)) return DG_ERR_CUDA;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
+        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
             cudaSuccess)
             return DG_ERR_CUDA;
         attr_set = true;
@@ -606,7 +615,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     const int64_t ntiles = (int64_t)ta.ntp * ta.ntq;
     if (ntiles > INT32_MAX) return DG_ERR_SHAPE;
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
-    lut_gemm_ts_kernel<BN, NEPI><<<grid, Roles<NEPI>::NT, C::ALLOC, st>>>(mp, mb, ta, rq ? *rq : dummy);
+    lut_gemm_ts_kernel<BN, NEPI, NUNP><<<grid, Roles<NEPI, NUNP>::NT, C::ALLOC, st>>>(mp, mb, ta, rq ? *rq : dummy);
     return launch_status();
 }
 
@@ -632,11 +641,11 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     // short K (<= 2 stages): the epilogue dominates -> 8 epilogue warps
     const bool short_k = K <= 2 * KS;
     if (nq > 64) {
-        if (short_k) return launch_ts<128, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
-        return launch_ts<128, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (short_k) return launch_ts<128, 16, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        return launch_ts<128, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     }
-    if (short_k) return launch_ts<64, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
-    return launch_ts<64, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    if (short_k) return launch_ts<64, 8, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    return launch_ts<64, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 }
 
 }  // namespace dg

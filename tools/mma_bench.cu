@@ -57,6 +57,10 @@ __global__ void __launch_bounds__(256, 1) bench(int niter, unsigned long long *c
                 ptx::tmem_ld_32x32b_x32(taddr, r);
                 ptx::tmem_ld_wait();
                 acc += r[3];
+                if (MODE == 16) {
+                    uint4 *gp = reinterpret_cast<uint4 *>(cycles + 64) + ((blockIdx.x * 256 + threadIdx.x) & 4095);
+                    *gp = make_uint4(r[0], r[1], r[2], r[4]);
+                }
             }
             ++it;
         }
@@ -96,7 +100,7 @@ __global__ void __launch_bounds__(256, 1) bench(int niter, unsigned long long *c
         }
         if (threadIdx.x == 0) done = 1;
     }
-    if (threadIdx.x == 0 && MODE < 11) {
+    if (threadIdx.x == 0 && (MODE < 11 || MODE >= 14)) {
         const uint32_t a = ptx::smem_u32(smem), b = a + 128 * 128;
         constexpr uint32_t idesc = ptx::idesc_i8(128, N);
         const long long c0 = clock64();
@@ -143,7 +147,7 @@ template <int N, bool TS, int MODE = 0>
 void run(int sms) {
     const int niter = 20000;
     unsigned long long *d;
-    cudaMalloc(&d, 16);
+    cudaMalloc(&d, 16 + 64 * 8 + 4096 * 16 + 1024);
     const int smem = (128 + N) * 128 + 2048;
     cudaFuncSetAttribute(bench<N, TS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     bench<N, TS, MODE><<<sms, 256, smem>>>(100, d);
@@ -173,9 +177,9 @@ int main() {
     run<256, true>(sms);
     run<128, false>(sms);
     run<256, false>(sms);
-    run<128, true, 7>(sms);
-    run<128, true, 11>(sms);
-    run<128, true, 12>(sms);
-    run<128, true, 13>(sms);
+    run<128, true, 3>(sms);
+    run<128, true, 14>(sms);
+    run<128, true, 15>(sms);
+    run<128, true, 16>(sms);
     return 0;
 }

@@ -11,13 +11,22 @@ ld = dg.packed_ld(K)
 w = torch.randint(0, 256, (M, ld), dtype=torch.uint8, device="cuda")
 at = torch.randint(0, 256, (N, ld), dtype=torch.uint8, device="cuda")
 at8 = dg.expand_operand(at, K, lut.al)
-out = torch.empty((M, N), dtype=torch.int32, device="cuda")
+RQ = "--rq" in sys.argv
+if RQ:
+    out = torch.empty((M, N // 4), dtype=torch.uint8, device="cuda")
+    bias = torch.full((N,), K // 2, dtype=torch.int32, device="cuda")
+    rq = dg.Requant(30000, 20, 0, 0, 3, bias=bias, bias_axis=0)
+else:
+    out = torch.empty((M, N), dtype=torch.int32, device="cuda")
+    rq = None
 L = dg.lib()
 buf = (ctypes.c_ulonglong * 16)()
-dg.lut_gemm_prepared(w, at8, M, N, K, lut, out=out); torch.cuda.synchronize()
+dg.lut_gemm_prepared(w, at8, M, N, K, lut, rq=rq, out=out); torch.cuda.synchronize()
 L.dg_debug_ts_prof(buf, 1)
 e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-e0.record(); dg.lut_gemm_prepared(w, at8, M, N, K, lut, out=out); e1.record(); torch.cuda.synchronize()
+e0.record(); dg.lut_gemm_prepared(w, at8, M, N, K, lut, rq=rq, out=out); e1.record(); torch.cuda.synchronize()
 L.dg_debug_ts_prof(buf, 0)
 n = buf[3]
+ntile = max(buf[11], 1)
+print(f"  epilogue warp0: wait_acc={buf[8]/ntile:.0f} work={buf[9]/ntile:.0f} cycles/tile over {ntile} tiles; unpack warp: {buf[12]/max(buf[13],1):.0f} cycles/stage")
 print(f"{M}x{N}x{K}: {e0.elapsed_time(e1):.3f} ms; CTA0 stages={n}  mma_barsync={buf[0]/n:.0f}  mma_issue={buf[2]/n:.0f}  waiter_full_a={buf[4]/n:.0f} waiter_full_b={buf[5]/n:.0f} cycles/stage")
