@@ -90,6 +90,7 @@ __device__ unsigned long long g_ts_prof[16];   // CTA 0 cycle counters (tools/tr
 struct TsArgs {
     int64_t np, nq;
     int32_t nstages, last_ksteps, ntp, ntq;
+    int32_t group;         // tile rasterisation: GROUP row blocks x all column blocks, column-major inside
     int32_t pks, bulk;     // packed P stage bytes per row (smem pitch); bulk copy mode
     const uint8_t *P;      // packed P (bulk mode)
     int64_t ldp;
@@ -104,6 +105,18 @@ struct TsArgs {
     int32_t H, W, Cb_log2, kw_recip, kw, stride, pad, Ho, Wo, kb;
     uint32_t pad_word;     // pad byte replicated x4
 };
+
+// Tile t -> (row block tp, column block tq).  Tiles are walked in groups of `group` row blocks,
+// column block outer / row block inner, so that a wave of concurrent tiles touches few B tiles
+// and few A row blocks (keeps a 256 MB int8 B operand from being re-streamed from HBM).
+DG_DEV void tile_coords(const TsArgs &ta, int t, int &tp, int &tq) {
+    const int per_group = ta.group * ta.ntq;
+    const int grp = t / per_group;
+    const int rem = t - grp * per_group;
+    const int rows_here = min(ta.group, ta.ntp - grp * ta.group);
+    tq = rem / rows_here;
+    tp = grp * ta.group + (rem - tq * rows_here);
+}
 
 // Implicit im2col: 16 bytes (64 codes) of row p at virtual-im2col byte `byte` (multiple of 16).
 // K order (r, s, c) with c fastest (dg_im2col); out-of-image taps read the pad code.
@@ -228,7 +241,9 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         if (lane == 0) {
             uint32_t gp = 0, gb = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                const int64_t p0 = (int64_t)(t / ta.ntq) * BM, q0 = (int64_t)(t % ta.ntq) * BN;
+                int tp, tq;
+                tile_coords(ta, t, tp, tq);
+                const int64_t p0 = (int64_t)tp * BM, q0 = (int64_t)tq * BN;
                 int sub = 0, ps = 0;
                 for (int s = 0; s < ta.nstages; ++s, ++gb) {
                     if (sub == 0 && !ta.implicit) {   // next packed P stage (up to 512 codes of every row)
@@ -320,7 +335,9 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             const uint8_t *img = ta.X;
             int32_t h0 = 0, w0 = 0;
             if (ta.implicit) {
-                const int64_t p = (int64_t)(t / ta.ntq) * BM + r;
+                int tp, tq;
+                tile_coords(ta, t, tp, tq);
+                const int64_t p = (int64_t)tp * BM + r;
                 const int64_t pp = p < ta.np ? p : ta.np - 1;
                 const int32_t wo = (int32_t)(pp % ta.Wo);
                 const int64_t tt = pp / ta.Wo;
@@ -361,11 +378,24 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
                 }   // !implicit
                 uint32_t a[32];
-                const uint32_t w[8] = {v0.x, v0.y, v0.z, v0.w, v1.x, v1.y, v1.z, v1.w};
+                {
+                    const uint32_t w[4] = {v0.x, v0.y, v0.z, v0.w};
 #pragma unroll
-                for (int j = 0; j < 8; ++j) {
-                    const uint4 o = unpack16_levels(w[j], ta.lp);
-                    a[4 * j] = o.x; a[4 * j + 1] = o.y; a[4 * j + 2] = o.z; a[4 * j + 3] = o.w;
+                    for (int j = 0; j < 4; ++j) {
+                        const uint4 o = unpack16_levels(w[j], ta.lp);
+                        a[4 * j] = o.x; a[4 * j + 1] = o.y; a[4 * j + 2] = o.z; a[4 * j + 3] = o.w;
+                    }
+                }
+                if (two) {
+                    const uint32_t w[4] = {v1.x, v1.y, v1.z, v1.w};
+#pragma unroll
+                    for (int j = 0; j < 4; ++j) {
+                        const uint4 o = unpack16_levels(w[j], ta.lp);
+                        a[16 + 4 * j] = o.x; a[16 + 4 * j + 1] = o.y; a[16 + 4 * j + 2] = o.z; a[16 + 4 * j + 3] = o.w;
+                    }
+                } else {
+#pragma unroll
+                    for (int j = 16; j < 32; ++j) a[j] = 0;   // k-steps 2, 3 of the last stage are not issued
                 }
                 ptx::mbar_wait(empty_a(sa), ((g / SA) & 1u) ^ 1u);
                 ptx::tc_fence_after();
@@ -390,8 +420,10 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         uint32_t tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl % NACC;
-            const int64_t p = (int64_t)(t / ta.ntq) * BM + quarter * 32 + lane;
-            const int64_t q0 = (int64_t)(t % ta.ntq) * BN + half * HALF;
+            int tp, tq;
+            tile_coords(ta, t, tp, tq);
+            const int64_t p = (int64_t)tp * BM + quarter * 32 + lane;
+            const int64_t q0 = (int64_t)tq * BN + half * HALF;
             const long long e0 = TS_CLK();
             ptx::mbar_wait(acc_full(acc), (tl / NACC) & 1u);
             const long long e1 = TS_CLK();
@@ -563,6 +595,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     ta.last_ksteps = (int32_t)((kmma - (int64_t)(ta.nstages - 1) * KS) / 32);
     ta.ntp = (int32_t)((np + BM - 1) / BM);
     ta.ntq = (int32_t)((nq + BN - 1) / BN);
+    ta.group = ta.ntq <= 4 ? 1 : (ta.ntp < 16 ? ta.ntp : 16);   // 1 = column block fastest
     ta.bulk = (ldp <= 32 && ((uintptr_t)P & 15) == 0) ? 1 : 0;
     ta.pks = ta.bulk ? (int32_t)ldp : PKS_MAX;
     ta.P = P;

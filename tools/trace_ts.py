@@ -28,5 +28,7 @@ e0.record(); dg.lut_gemm_prepared(w, at8, M, N, K, lut, rq=rq, out=out); e1.reco
 L.dg_debug_ts_prof(buf, 0)
 n = buf[3]
 ntile = max(buf[11], 1)
+ns = max(buf[13], 1)
+print(f"  unpack stage: load(+wait full_p)={buf[6]/ns:.0f} unpack={buf[7]/ns:.0f} wait_empty_a={buf[10]/ns:.0f} tmem_st+wait={buf[14]/ns:.0f}")
 print(f"  epilogue warp0: wait_acc={buf[8]/ntile:.0f} work={buf[9]/ntile:.0f} cycles/tile over {ntile} tiles; unpack warp: {buf[12]/max(buf[13],1):.0f} cycles/stage")
 print(f"{M}x{N}x{K}: {e0.elapsed_time(e1):.3f} ms; CTA0 stages={n}  mma_barsync={buf[0]/n:.0f}  mma_issue={buf[2]/n:.0f}  waiter_full_a={buf[4]/n:.0f} waiter_full_b={buf[5]/n:.0f} cycles/stage")
