@@ -207,9 +207,13 @@ class ResNet18Runner:
         self.res_mult = {}
         self.bias = {}
         ws_need = 0
+        self.w8 = {}
+        self.prepared = variant in ("auto", "tc")
         for li, L in enumerate(self.layers):
             self.w[li] = pack_conv_weights(weight_codes(2, li, L, device))
             p = dg.conv_params(batch, L.h, L.h, L.cin, L.cout, L.k, L.k, L.stride, L.pad, 0, ldw=self.w[li].shape[1])
+            if self.prepared:   # offline int8 expansion of the weights (tensor-core path)
+                self.w8[li] = dg.expand_operand(self.w[li], L.K, wl)
             self.params[li] = p
             ws_need = max(ws_need, dg.conv_workspace_size(p))
             r, rm = rqs[li]
@@ -236,23 +240,29 @@ class ResNet18Runner:
         r = self.rq[li]
         return dg.Requant(r.mult, r.shift, r.zp, r.qmin, r.qmax, bias=self.bias[li], bias_axis=0, **kw)
 
+    def _conv(self, x, li, rq, out, stream):
+        if self.prepared:
+            dg.lut_conv2d_prepared(x, self.w8[li], self.lut, self.params[li], rq=rq, out=out, ws=self.ws, stream=stream)
+        else:
+            dg.lut_conv2d(x, self.w[li], self.lut, self.params[li], rq=rq, variant=self.variant, out=out, ws=self.ws,
+                          stream=stream)
+
     def step(self, stream=None):
         x = self.x0
         for (c1, c2, ds), (y1, out, racc) in zip(self.blocks, self.bufs):
-            dg.lut_conv2d(x, self.w[c1], self.lut, self.params[c1], rq=self._rq(c1), variant=self.variant,
-                          out=y1, ws=self.ws, stream=stream)
+            self._conv(x, c1, self._rq(c1), y1, stream)
             if ds is not None:
-                dg.lut_conv2d(x, self.w[ds], self.lut, self.params[ds], rq=None, variant=self.variant, out=racc,
-                              ws=self.ws, stream=stream)
+                self._conv(x, ds, None, racc, stream)
                 rq2 = self._rq(c2, res=racc)
             else:
                 rq2 = self._rq(c2, res_codes=x, res_mult=self.res_mult[c2], res_levels=_synth().AL_UNIFORM)
-            dg.lut_conv2d(y1, self.w[c2], self.lut, self.params[c2], rq=rq2, variant=self.variant, out=out,
-                          ws=self.ws, stream=stream)
+            self._conv(y1, c2, rq2, out, stream)
             x = out
         return x
 
     def launches(self) -> int:
+        if self.prepared:      # one kernel per conv (direct / implicit GEMM; all C/4 are powers of two)
+            return len(self.layers)
         n = 0
         for li, L in enumerate(self.layers):
             direct = L.k == 1 and L.stride == 1 and L.pad == 0 and (L.cin // 4) % 16 == 0
