@@ -210,10 +210,10 @@ def run_conv(args, ws, rank, local):
     # algorithmic bytes of a GEMM launch: packed input + packed weights + packed output
     alg_bytes = (runner.input_bytes() + runner.weight_bytes() + runner.output_bytes()) / nl
     roof = {"bound": "tensor", "kernel": "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)",
-            "achieved": round(achieved, 1), "peak": round(pk["i8_sustained"], 1), "unit": "TOPS",
-            "frac": round(achieved / pk["i8_sustained"], 4),
-            "frac_vs_burst_peak": round(achieved / pk["i8_burst"], 4),
-            "peak_src": pk["src"] + ": int8 = 2 x bf16 sustained (nominal 4.5/2.25)",
+            "achieved": round(achieved, 1), "peak": round(pk["i8_burst"], 1), "unit": "TOPS",
+            "frac": round(achieved / pk["i8_burst"], 4),
+            "frac_vs_sustained_peak": round(achieved / pk["i8_sustained"], 4),
+            "peak_src": pk["src"] + ": int8 = 2 x bf16 burst (nominal 4.5/2.25); conservative vs the sustained figure",
             "gemm_share_of_step": round(gemm_total_ms / ms, 3),
             "traffic": tr, "alg_bytes_per_launch": round(alg_bytes),
             "traffic_src": "profiles/traffic.json (ncu dram__bytes_read+write, mean per GEMM launch)"}
@@ -321,8 +321,8 @@ def run_resnet18(args, ws, rank, local):
                 "data": "synthetic (seeded counter-based 2-bit codes; calibrated requant, synth_data/)",
                 "config": {"workload": f"resnet18_b{r.B}_chain (BASELINE configs[1])", "layers": len(r.layers),
                            "parallelism": f"{ws} independent replicas"},
-                "roofline": {"bound": "latency", "achieved": round(value / ws, 2), "peak": round(pk["i8_sustained"], 1),
-                             "unit": "TOPS", "frac": round(value / ws / pk["i8_sustained"], 5)},
+                "roofline": {"bound": "latency", "achieved": round(value / ws, 2), "peak": round(pk["i8_burst"], 1),
+                             "unit": "TOPS", "frac": round(value / ws / pk["i8_burst"], 5)},
                 "gpu_launches": r.launches() * args.steps, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
 
@@ -418,9 +418,10 @@ def run_gemm(args, ws, rank, local):
                            "l2": "1 GiB int32 output per step (> L2)" if flush is None else "256 MB L2 flush between steps"},
                 "compute_only": {"value": round(comp_tops, 2), "ms": round(ms_comp, 4), "per_gpu_tops": round(per_gpu, 2)},
                 "roofline": {"bound": "tensor", "kernel": "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)",
-                             "achieved": round(per_gpu, 1), "peak": round(pk["i8_sustained"], 1), "unit": "TOPS",
-                             "frac": round(per_gpu / pk["i8_sustained"], 4),
-                             "frac_vs_burst_peak": round(per_gpu / pk["i8_burst"], 4),
+                             "achieved": round(per_gpu, 1), "peak": round(pk["i8_burst"], 1), "unit": "TOPS",
+                             "frac": round(per_gpu / pk["i8_burst"], 4),
+                             "frac_vs_sustained_peak": round(per_gpu / pk["i8_sustained"], 4),
+                             "peak_src": pk["src"] + ": int8 = 2 x bf16 burst (kernel timed alone)",
                              "alg_bytes_per_launch": alg_bytes, "traffic": None},
                 "gpu_launches": args.steps, "clocks": clk.summary(), "parity": parity}
         print(json.dumps(line), flush=True)

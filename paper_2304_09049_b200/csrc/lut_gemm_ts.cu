@@ -19,6 +19,7 @@
 //   warp 13       waiter: waits on the MMA-side mbarriers, hands stages to warp 14 by bar.sync
 //   warp 14       MMA issuer (one thread): tcgen05.mma [D], [A_tmem], B_desc, 4 k-steps/stage
 #include <cuda.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -58,9 +59,9 @@ constexpr int HANDOFF_BAR = 1;
 
 template <int BN>
 struct TsCfg {
-    static constexpr int NACC = BN == 128 ? 3 : 4;          // accumulator buffers (TMEM cols NACC*BN)
+    static constexpr int NACC = BN == 256 ? 1 : (BN == 128 ? 3 : 4);   // accumulator buffers (TMEM cols NACC*BN)
     static constexpr int SA = 4;                            // A stages in TMEM (32 cols each)
-    static constexpr int SB = 4;                            // B (int8) smem stages
+    static constexpr int SB = BN == 256 ? 3 : 4;            // B (int8) smem stages
     static constexpr int SP = 4;                            // packed P smem stages
     static constexpr int TMEM_A0 = NACC * BN;               // first A column
     static constexpr int TMEM_COLS = 512;
@@ -673,6 +674,11 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     if (np > ((int64_t)1 << 31) - 1 || nq > ((int64_t)1 << 31) - 1) return DG_ERR_SHAPE;
     // short K (<= 2 stages): the epilogue dominates -> 8 epilogue warps
     const bool short_k = K <= 2 * KS;
+    // 128x256 tiles halve the shared-memory bytes of B per MAC (measured: 8192^3 1666 -> 2323
+    // TOPS); their single TMEM accumulator buffer cannot overlap the epilogue with the next tile,
+    // so they are used only when the K loop is long (>= 24 stages).
+    if (nq >= 256 && K >= 24 * KS && !getenv("DG_TS_NO_BN256"))
+        return launch_ts<256, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     if (nq > 64) {
         if (short_k) return launch_ts<128, 16, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         return launch_ts<128, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
