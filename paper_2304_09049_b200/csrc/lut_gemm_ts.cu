@@ -33,6 +33,7 @@ constexpr int BM = 128;          // TMEM lanes / P rows per tile
 constexpr int KS = 128;          // codes per stage (= one 128-byte int8 B row, 32 TMEM columns of A)
 constexpr int PKS_MAX = 128;     // packed bytes per row per packed stage (512 codes)
 constexpr int NSUB_MAX = PKS_MAX * 4 / KS;   // 4 stages per packed stage
+constexpr int TAB_PAIRS = 2048;  // per-column requant table (16-bit SIMD epilogue): nq <= 4096
 // Warp roles.  The SM sub-partition scheduler prefers the highest warp id among eligible
 // warps, so the latency-critical single-thread roles (TMA producer, MMA issuer) take the
 // highest ids and are never starved by the ALU-heavy unpack / epilogue warps.
@@ -56,6 +57,7 @@ struct Roles {
 // the waiter warp does, and hands each stage over with a named-barrier rendezvous, which does
 // not stall the MMA queue (measured: 64 cycles per 128x128x32 MMA either way).
 constexpr int HANDOFF_BAR = 1;
+constexpr int EPI_BAR = 2;       // epilogue warps only (requant table build)
 
 template <int BN>
 struct TsCfg {
@@ -72,7 +74,8 @@ struct TsCfg {
     static constexpr int OFF_BAR = OFF_P + SP * P_BYTES;
     static constexpr int NBAR = 2 * SP + 2 * SB + 2 * SA + 2 * NACC;
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
-    static constexpr int ALLOC = OFF_TMEM + 16 + 1024;
+    static constexpr int OFF_TAB = (OFF_TMEM + 16 + 15) / 16 * 16;   // 16-bit requant offsets, one u32 per column pair
+    static constexpr int ALLOC = OFF_TAB + TAB_PAIRS * 4 + 1024;
     static_assert(TMEM_A0 + SA * 32 <= TMEM_COLS, "TMEM budget");
 };
 
@@ -105,6 +108,13 @@ struct TsArgs {
     const uint8_t *X;      // [B][H][W][Cb] packed codes, Cb = C/4 a power of two >= 16
     int32_t H, W, Cb_log2, kw_recip, kw, stride, pad, Ho, Wo, kb;
     uint32_t pad_word;     // pad byte replicated x4
+    // 16-bit SIMD requant (host-verified, see f16_params): per column pair
+    //   x = clamp(acc + negA, 0, W) (one VIADDMNMX.RELU), code = (x*m + c) >> 14 (one IMAD),
+    // negA = bias - (thr0 - 1) per column (smem table), per row, or uniform.
+    int32_t f16;           // 1: usable (all codes' thresholds finite, |acc| + |negA| < 2^15)
+    int32_t f16_tab;       // 1: per-column bias -> negA table built in shared memory
+    uint32_t f16_m, f16_c2, f16_w2, f16_na2;   // m; c and W replicated in both halves; uniform negA
+    int32_t f16_thr0m1, f16_accmax;
 };
 
 // Tile t -> (row block tp, column block tq).  Tiles are walked in groups of `group` row blocks,
@@ -137,6 +147,24 @@ DG_DEV void store_codes32_ts(uint8_t *dp, uint32_t o0, uint32_t o1, int nbytes) 
 #pragma unroll
     for (int b = 0; b < 8; ++b)
         if (b < nbytes) dp[b] = (uint8_t)((b < 4 ? o0 : o1) >> (8 * (b & 3)));
+}
+
+// 16-bit SIMD requant of 32 columns (S7; the exact threshold map of reading Q23 written as one
+// clamp + one multiply-add per column PAIR).  r[i] = columns 2i | 2i+1 (tcgen05.ld pack::16b),
+// na[i] = their offsets.  The code of lane j ends in bits [14,16) of that lane; PRMT gathers the
+// four codes of 4 consecutive columns into the top bits of 4 bytes, a masked multiply by
+// 2^18+2^12+2^6+1 moves them into the top byte in LSB-first order (the cross terms land below
+// bit 24 without overlapping, or above bit 31), and two PRMT levels assemble 16 columns per word.
+DG_DEV uint2 requant16_32(const uint32_t (&r)[16], const uint32_t (&na)[16], uint32_t w2, uint32_t m, uint32_t c2) {
+    uint32_t y[16];
+#pragma unroll
+    for (int i = 0; i < 16; ++i) y[i] = __viaddmin_s16x2_relu(r[i], na[i], w2) * m + c2;
+    uint32_t u[8];
+#pragma unroll
+    for (int b = 0; b < 8; ++b) u[b] = (prmt_b32(y[2 * b], y[2 * b + 1], 0x7531u) & 0xC0C0C0C0u) * 0x41041u;
+    const uint32_t lo = prmt_b32(prmt_b32(u[0], u[1], 0x0073u), prmt_b32(u[2], u[3], 0x0073u), 0x5410u);
+    const uint32_t hi = prmt_b32(prmt_b32(u[4], u[5], 0x0073u), prmt_b32(u[6], u[7], 0x0073u), 0x5410u);
+    return make_uint2(lo, hi);
 }
 
 // int32 output / residual requant / ragged tail for one 32-column chunk (out of line)
@@ -232,6 +260,11 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         __syncwarp();
         ptx::tmem_alloc(ptx::smem_u32(tmem_slot), C::TMEM_COLS);
     }
+    uint32_t *f16tab = reinterpret_cast<uint32_t *>(smem + C::OFF_TAB);
+    volatile uint32_t *f16_flag = reinterpret_cast<volatile uint32_t *>(smem + C::OFF_TMEM + 8);
+    if (threadIdx.x == 0) *f16_flag = 0u;
+    // (with __syncthreads_or here the kernel faulted with a misaligned address when launched
+    // right after the tc_ss kernel, cause not determined: the flag goes through shared memory)
     ptx::tc_fence_before();
     __syncthreads();
     ptx::tc_fence_after();
@@ -416,6 +449,20 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         // ---------------- epilogue (lane quarter = warp % 4, column part = warp / 4)
         constexpr int HALF = BN / (NEPI / 4), NCH = HALF / 32;
         static_assert(HALF % 32 == 0, "epilogue column part must be a multiple of 32");
+        // 16-bit requant offsets per column pair (bias_axis 0): negA = bias - (thr0 - 1), checked
+        // against int16 overflow of acc + negA; any failure sends every tile to the 32-bit path
+        if (ta.f16 && ta.f16_tab) {
+            uint32_t bad = 0;
+            for (int i = threadIdx.x - EPI_WARP0 * 32; i < (int)(ta.nq >> 1); i += NEPI * 32) {
+                const int64_t n0 = (int64_t)__ldg(rq.bias + 2 * i) - ta.f16_thr0m1;
+                const int64_t n1 = (int64_t)__ldg(rq.bias + 2 * i + 1) - ta.f16_thr0m1;
+                if ((n0 < 0 ? -n0 : n0) + ta.f16_accmax > 32767 || (n1 < 0 ? -n1 : n1) + ta.f16_accmax > 32767) bad = 1;
+                f16tab[i] = ((uint32_t)n0 & 0xFFFFu) | ((uint32_t)n1 << 16);
+            }
+            if (bad) *f16_flag = 1u;
+            ptx::named_bar_sync(EPI_BAR, NEPI * 32);
+        }
+        const bool f16_ok = ta.f16 && *f16_flag == 0u;
         const int quarter = warp & 3, half = (warp - EPI_WARP0) >> 2;
         const bool col_bias = rq.bias && rq.bias_axis == 0;
         uint32_t tl = 0;
@@ -440,7 +487,45 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
             } else
 #endif
-            if (!fast) {
+            // 16-bit SIMD path (warp-uniform): per-row offsets need every lane's row in range
+            bool use16 = fast && f16_ok;
+            uint32_t na_row = ta.f16_na2;
+            if (use16 && !ta.f16_tab && rq.bias && rq.bias_axis == 1) {
+                const int64_t n = (int64_t)rb - ta.f16_thr0m1;
+                na_row = ((uint32_t)n & 0xFFFFu) * 0x10001u;
+                use16 = __all_sync(0xFFFFFFFFu, (n < 0 ? -n : n) + ta.f16_accmax <= 32767);
+            }
+            if (use16) {
+#pragma unroll 1
+                for (int c = 0; c < NCH; ++c) {
+                    const int64_t qc = q0 + c * 32;
+                    uint32_t na[16];
+                    if (ta.f16_tab) {
+                        const uint32_t ta4 = sbase + C::OFF_TAB + (uint32_t)(qc >> 1) * 4u;
+#pragma unroll
+                        for (int j = 0; j < 4; ++j) {
+                            const uint4 t4 = ptx::lds128(ta4 + 16 * j);
+                            na[4 * j] = t4.x; na[4 * j + 1] = t4.y; na[4 * j + 2] = t4.z; na[4 * j + 3] = t4.w;
+                        }
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) na[j] = na_row;
+                    }
+                    uint32_t r16[16];
+                    ptx::tmem_ld_32x32b_x16_pack16(trow + c * 32, r16);
+                    ptx::tmem_ld_wait();
+                    if (c == NCH - 1) {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
+                    }
+                    if (p >= ta.np) continue;
+                    const uint2 o = requant16_32(r16, na, ta.f16_w2, ta.f16_m, ta.f16_c2);
+                    uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
+                    if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = o;
+                    else store_codes32_ts(dp, o.x, o.y, 8);
+                }
+            } else if (!fast) {
 #pragma unroll 1
                 for (int c = 0; c < NCH; ++c) ts_epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
                 ptx::tc_fence_before();
@@ -576,6 +661,33 @@ bool make_map_sw128(CUtensorMap *m, const void *base, int64_t ld, int64_t rows, 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// 16-bit SIMD requant parameters.  With x = clamp(acc + bias - (t0 - 1), 0, W), W = t2 - t0 + 1,
+// the exact code is [x >= 1] + [x >= t1 - t0 + 1] + [x >= W]; find integers m, c with
+// floor((x*m + c) / 2^14) equal to it.  x*m + c is monotone in x, so matching at the threshold
+// boundaries suffices; the result is re-verified for every x in [0, W].
+bool f16_params(int64_t t0, int64_t t1, int64_t t2, uint32_t &m_out, uint32_t &c_out) {
+    const int64_t W = t2 - t0 + 1, X2 = t1 - t0 + 1;
+    if (W < 1 || W > 16383 || X2 < 1 || X2 > W) return false;
+    auto code = [&](int64_t x) { return (int64_t)(x >= 1) + (int64_t)(x >= X2) + (int64_t)(x >= W); };
+    const int64_t pts[7] = {0, 0, 1, X2 - 1, X2, W - 1, W};
+    for (int64_t m = 1; m * W < 65536; ++m) {
+        int64_t lo = 0, hi = 65535;
+        for (int i = 0; i < 7; ++i) {
+            const int64_t x = pts[i], k = code(x);
+            lo = lo > k * 16384 - x * m ? lo : k * 16384 - x * m;
+            hi = hi < (k + 1) * 16384 - 1 - x * m ? hi : (k + 1) * 16384 - 1 - x * m;
+        }
+        if (lo > hi) continue;
+        bool ok = true;
+        for (int64_t x = 0; x <= W && ok; ++x) ok = (x * m + lo) >> 14 == code(x) && x * m + lo < 65536;
+        if (!ok) continue;
+        m_out = (uint32_t)m;
+        c_out = (uint32_t)lo;
+        return true;
+    }
+    return false;
+}
+
 template <int BN, int NEPI, int NUNP>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
@@ -614,6 +726,28 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
             int64_t u = (t == INT64_MAX || t == INT64_MIN) ? t : (rq->dir > 0 ? t - 1 : t);
             const int64_t LIM = (int64_t)1 << 30;
             ta.thr[j] = (int32_t)(u > LIM ? LIM : (u < -LIM ? -LIM : u));
+        }
+        // 16-bit SIMD requant: |acc| < 2^15 (tcgen05.ld pack::16b keeps the low halves), finite
+        // increasing thresholds, an (m, c) pair found; offsets checked here (uniform), per row
+        // (in the epilogue) or per column (smem table at kernel start).
+        const int64_t *t = rq->thr;
+        uint32_t m16 = 0, c16 = 0;
+        if (rq->dir > 0 && acc_bound <= 32767 && t[0] > -((int64_t)1 << 30) && t[2] < ((int64_t)1 << 30) &&
+            (nq >> 1) <= TAB_PAIRS && !getenv("DG_NO_F16") && f16_params(t[0], t[1], t[2], m16, c16)) {
+            const int64_t thr0m1 = t[0] - 1;
+            ta.f16_m = m16;
+            ta.f16_c2 = c16 * 0x10001u;
+            ta.f16_w2 = (uint32_t)(t[2] - t[0] + 1) * 0x10001u;
+            ta.f16_thr0m1 = (int32_t)thr0m1;
+            ta.f16_accmax = (int32_t)acc_bound;
+            ta.f16 = 1;
+            if (rq->bias && rq->bias_axis == 0) {
+                ta.f16_tab = 1;
+            } else if (!rq->bias) {
+                const int64_t n = -thr0m1;
+                ta.f16_na2 = ((uint32_t)n & 0xFFFFu) * 0x10001u;
+                if ((n < 0 ? -n : n) + acc_bound > 32767) ta.f16 = 0;
+            }
         }
     }
     if (cv) {

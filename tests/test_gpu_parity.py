@@ -347,3 +347,60 @@ def test_conv_prepared_vs_oracle(B, H, W, C, Cout, k, stride, pad, pad_code):
     ws = torch.empty(dg.conv_workspace_size(p), dtype=torch.uint8, device=DEV)
     out = dg.lut_conv2d_prepared(xp, w8, lut, p, ws=ws)
     assert np.array_equal(host(out).reshape(exp.shape), exp)
+
+
+# ---------------------------------------------------------------- requant epilogue paths
+RQ_SWEEP = [  # mult, zp, qmin, qmax, bias kind
+    (30000, 0, 0, 3, "none"),
+    (30000, 1, 0, 3, "col"),          # per-column bias table (16-bit SIMD path)
+    (5000, 0, 0, 3, "col"),           # wide threshold spacing
+    (200000, 2, 0, 3, "uniform"),     # narrow spacing (~5 accumulator units)
+    (1 << 20, 1, 0, 3, "col"),        # spacing exactly 1: consecutive thresholds
+    (3 << 20, 0, 0, 3, "none"),       # spacing < 1: some codes unreachable / equal thresholds
+    (20180, 1, -1, 2, "col"),         # signed code range (qmin = -1)
+    (30000, 0, 0, 2, "col"),          # only 3 codes used (an infinite threshold)
+    (-30000, 0, 0, 3, "col"),         # negative multiplier (decreasing map)
+    (30000, 0, 0, 3, "colbig"),       # |bias| near 2^15: 16-bit offsets overflow -> 32-bit path
+    (30000, 1, 0, 3, "row"),          # GEMM orientation: bias per row (TMEM lane)
+]
+
+
+@pytest.mark.parametrize("mult,zp,qmin,qmax,bias_kind", RQ_SWEEP)
+@pytest.mark.parametrize("K", [64, 2304])
+def test_tc_requant_epilogue_sweep(mult, zp, qmin, qmax, bias_kind, K):
+    """Fused requant on the tensor-core path (16-bit SIMD epilogue where its host-verified
+    parameters exist, else the 32-bit threshold path) against O-REQ over the oracle's
+    accumulators, bit-exact, for spacings, signed ranges, unreachable codes, bias layouts
+    and offsets that overflow 16 bits."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    lut = dg.build_lut(WL, AL, 8)
+    T = oracle.build_lut16(WL, AL)
+    g = np.random.default_rng(K + abs(mult) % 1000 + zp + qmin)
+    M, N = 300, 96                      # M = pixels (TMEM lanes, ragged last tile), N = channels
+    A = g.integers(0, 4, (M, K), dtype=np.uint8)       # activations, K-major
+    Wt = g.integers(0, 4, (N, K), dtype=np.uint8)      # weights [channel][K]
+    acc = oracle.lut_gemm(A, np.ascontiguousarray(Wt.T), oracle.build_lut16(AL, WL))   # [M][N]
+    assert np.array_equal(acc, oracle.lut_gemm(Wt, np.ascontiguousarray(A.T), T).T)
+    mu = int(np.round(acc.mean()))
+    if bias_kind == "none":
+        bias, axis = None, 0
+    elif bias_kind == "uniform":
+        bias, axis = np.full(N, -mu, np.int32), 0
+    elif bias_kind == "col":
+        bias, axis = (-mu + g.integers(-40, 40, N)).astype(np.int32), 0
+    elif bias_kind == "colbig":
+        bias, axis = (-mu + g.integers(-40, 40, N)).astype(np.int32), 0
+        bias[5] = 32000
+    else:
+        bias, axis = (-mu + g.integers(-40, 40, M)).astype(np.int32), 1
+    a_p = gpu_pack(A)
+    w_p = gpu_pack(Wt, weights=True)
+    w8 = dg.expand_operand(w_p, K, WL)
+    lut_t = dg.build_lut(AL, WL, 8)   # index (a<<2)|w: P = activations
+    rq = dg.Requant(mult, 20, zp, qmin, qmax, bias=None if bias is None else torch.from_numpy(bias).to(DEV),
+                    bias_axis=axis)
+    got = dg.lut_gemm_prepared(a_p, w8, M, N, K, lut_t, rq=rq)
+    q = oracle.requantize(acc, mult, 20, zp, qmin, qmax, bias=bias, bias_axis=axis).view(np.int8)
+    exp = (q.astype(np.int32) - qmin).astype(np.uint8)     # dg.h: code = q - qmin
+    assert np.array_equal(oracle_codes_of(got, M, N), exp)
