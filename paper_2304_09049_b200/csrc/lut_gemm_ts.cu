@@ -33,7 +33,8 @@ constexpr int BM = 128;          // TMEM lanes / P rows per tile
 constexpr int KS = 128;          // codes per stage (= one 128-byte int8 B row, 32 TMEM columns of A)
 constexpr int PKS_MAX = 128;     // packed bytes per row per packed stage (512 codes)
 constexpr int NSUB_MAX = PKS_MAX * 4 / KS;   // 4 stages per packed stage
-constexpr int TAB_PAIRS = 2048;  // per-column requant table (16-bit SIMD epilogue): nq <= 4096
+constexpr int TAB_PAIRS = 2048;
+constexpr int SP_MAX = 32;       // packed P slots (narrow rows -> many slots in flight)  // per-column requant table (16-bit SIMD epilogue): nq <= 4096
 // Warp roles.  The SM sub-partition scheduler prefers the highest warp id among eligible
 // warps, so the latency-critical single-thread roles (TMA producer, MMA issuer) take the
 // highest ids and are never starved by the ALU-heavy unpack / epilogue warps.
@@ -63,16 +64,15 @@ template <int BN>
 struct TsCfg {
     static constexpr int NACC = BN == 256 ? 1 : (BN == 128 ? 3 : 4);   // accumulator buffers (TMEM cols NACC*BN)
     static constexpr int SA = 4;                            // A stages in TMEM (32 cols each)
-    static constexpr int SB = BN == 256 ? 3 : 4;            // B (int8) smem stages
-    static constexpr int SP = 4;                            // packed P smem stages
+    static constexpr int SB = BN == 256 ? 3 : (BN == 128 ? 4 : 6);   // B (int8) smem stages
     static constexpr int TMEM_A0 = NACC * BN;               // first A column
     static constexpr int TMEM_COLS = 512;
     static constexpr int B_BYTES = BN * KS;
-    static constexpr int P_BYTES = BM * PKS_MAX;
+    static constexpr int P_REGION = 4 * BM * PKS_MAX;      // packed P slots: ta.sp x (BM x ta.pks) bytes
     static constexpr int OFF_B = 0;                          // 1024-aligned (SW128)
     static constexpr int OFF_P = OFF_B + SB * B_BYTES;
-    static constexpr int OFF_BAR = OFF_P + SP * P_BYTES;
-    static constexpr int NBAR = 2 * SP + 2 * SB + 2 * SA + 2 * NACC;
+    static constexpr int OFF_BAR = OFF_P + P_REGION;
+    static constexpr int NBAR = 2 * SP_MAX + 2 * SB + 2 * SA + 2 * NACC;
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr int OFF_TAB = (OFF_TMEM + 16 + 15) / 16 * 16;   // 16-bit requant offsets, one u32 per column pair
     static constexpr int ALLOC = OFF_TAB + TAB_PAIRS * 4 + 1024;
@@ -91,13 +91,27 @@ __device__ unsigned long long g_ts_prof[16];   // CTA 0 cycle counters (tools/tr
 #define TS_CLK() 0ll
 #endif
 
+// n / d without a divide for 0 <= n < 2^31 (round-up multiplier; d >= 1):
+// s = ceil(log2 d), m = floor(2^32 (2^s - d) / d) + 1, q = (umulhi(n, m) + n) >> s
+struct FastDiv {
+    uint32_t m, s;
+};
+inline FastDiv make_fastdiv(uint32_t d) {
+    uint32_t s = 0;
+    while ((1ull << s) < d) ++s;
+    return FastDiv{(uint32_t)((((1ull << s) - d) << 32) / d + 1), s};
+}
+DG_DEV uint32_t fdiv(uint32_t n, FastDiv f) { return (__umulhi(n, f.m) + n) >> f.s; }
+
 struct TsArgs {
     int64_t np, nq;
     int32_t nstages, last_ksteps, ntp, ntq;
     int32_t group;         // tile rasterisation: GROUP row blocks x all column blocks, column-major inside
-    int32_t pks, bulk;     // packed P stage bytes per row (smem pitch); bulk copy mode
-    const uint8_t *P;      // packed P (bulk mode)
-    int64_t ldp;
+    int32_t last_grp, last_rows;   // index of the last row group and its row-block count
+    FastDiv fd_pg, fd_grp, fd_last;  // / (group * ntq), / group, / last_rows
+    int32_t pks;           // packed P slot bytes per row (TMA box width, smem pitch): 16, 32, 64 or 128
+    int32_t sp;            // packed P slots (SP_MAX max)
+    int32_t bres;          // 1: all ntq x nstages B tiles resident in smem (loaded once)
     uint32_t lp;           // int8 levels of P codes
     void *D;
     int64_t ldd;
@@ -121,12 +135,12 @@ struct TsArgs {
 // column block outer / row block inner, so that a wave of concurrent tiles touches few B tiles
 // and few A row blocks (keeps a 256 MB int8 B operand from being re-streamed from HBM).
 DG_DEV void tile_coords(const TsArgs &ta, int t, int &tp, int &tq) {
-    const int per_group = ta.group * ta.ntq;
-    const int grp = t / per_group;
-    const int rem = t - grp * per_group;
-    const int rows_here = min(ta.group, ta.ntp - grp * ta.group);
-    tq = rem / rows_here;
-    tp = grp * ta.group + (rem - tq * rows_here);
+    const uint32_t grp = fdiv((uint32_t)t, ta.fd_pg);
+    const uint32_t rem = (uint32_t)t - grp * (uint32_t)(ta.group * ta.ntq);
+    const bool last = (int)grp == ta.last_grp;
+    const uint32_t q = fdiv(rem, last ? ta.fd_last : ta.fd_grp);
+    tq = (int)q;
+    tp = (int)(grp * ta.group + (rem - q * (uint32_t)(last ? ta.last_rows : ta.group)));
 }
 
 // Implicit im2col: 16 bytes (64 codes) of row p at virtual-im2col byte `byte` (multiple of 16).
@@ -213,7 +227,9 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                    const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
     using C = TsCfg<BN>;
     using R = Roles<NEPI, NUNP>;
-    constexpr int SP = C::SP, SB = C::SB, SA = C::SA, NACC = C::NACC;
+    constexpr int SB = C::SB, SA = C::SA, NACC = C::NACC, SP = SP_MAX;
+    const int nsp = ta.sp;
+    const uint32_t pslot = (uint32_t)(BM * ta.pks);
     constexpr int NUM_EPI_WARPS = NEPI, EPI_WARP0 = R::EPI_WARP0, UNPACK_WARP0 = R::UNPACK_WARP0,
                   PRODUCER_WARP = R::PRODUCER_WARP, WAITER_WARP = R::WAITER_WARP, MMA_WARP = R::MMA_WARP,
                   NUM_UGROUPS = R::NUM_UGROUPS;
@@ -233,11 +249,11 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = ta.ntp * ta.ntq;
-    const int nsub = (ta.pks * 4 + KS - 1) / KS;   // stages per packed stage
+    const int nsub = (ta.pks * 4 + KS - 1) / KS;   // stages per packed slot
 
     if (warp == PRODUCER_WARP) {
         if (lane == 0) {
-            if (!ta.bulk) ptx::tma_prefetch(&tm_p);
+            if (!ta.implicit) ptx::tma_prefetch(&tm_p);
             ptx::tma_prefetch(&tm_b);
             for (int s = 0; s < SP; ++s) {
                 ptx::mbar_init(full_p(s), 1);
@@ -274,6 +290,14 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         // ---------------- producer
         if (lane == 0) {
             uint32_t gp = 0, gb = 0;
+            if (ta.bres) {   // every B tile once: slot tq * nstages + s
+                for (int tq = 0; tq < ta.ntq; ++tq)
+                    for (int s = 0; s < ta.nstages; ++s) {
+                        const int j = tq * ta.nstages + s;
+                        ptx::mbar_arrive_expect_tx(full_b(j), (uint32_t)C::B_BYTES);
+                        ptx::tma_load_2d(sbase + C::OFF_B + j * C::B_BYTES, &tm_b, full_b(j), s * KS, tq * BN);
+                    }
+            }
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
                 int tp, tq;
                 tile_coords(ta, t, tp, tq);
@@ -281,22 +305,16 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 int sub = 0, ps = 0;
                 for (int s = 0; s < ta.nstages; ++s, ++gb) {
                     if (sub == 0 && !ta.implicit) {   // next packed P stage (up to 512 codes of every row)
-                        const int slot = gp % SP;
-                        ptx::mbar_wait(empty_p(slot), ((gp / SP) & 1u) ^ 1u);
-                        const uint32_t dst = sbase + C::OFF_P + slot * C::P_BYTES;
-                        if (ta.bulk) {
-                            const int64_t rows = ta.np - p0 < BM ? ta.np - p0 : BM;
-                            const uint32_t bytes = (uint32_t)(rows * ta.ldp);
-                            ptx::mbar_arrive_expect_tx(full_p(slot), bytes);
-                            ptx::bulk_load(dst, ta.P + p0 * ta.ldp, bytes, full_p(slot));
-                        } else {
-                            ptx::mbar_arrive_expect_tx(full_p(slot), (uint32_t)(BM * PKS_MAX));
-                            ptx::tma_load_2d(dst, &tm_p, full_p(slot), ps * PKS_MAX, (int32_t)p0);
-                        }
+                        const int slot = gp % nsp;
+                        ptx::mbar_wait(empty_p(slot), ((gp / nsp) & 1u) ^ 1u);
+                        const uint32_t dst = sbase + C::OFF_P + slot * pslot;
+                        ptx::mbar_arrive_expect_tx(full_p(slot), pslot);
+                        ptx::tma_load_2d(dst, &tm_p, full_p(slot), ps * ta.pks, (int32_t)p0);
                         ++gp;
                         ++ps;
                     }
                     if (++sub == nsub) sub = 0;
+                    if (ta.bres) continue;
                     const int bs = gb % SB;
                     ptx::mbar_wait(empty_b(bs), ((gb / SB) & 1u) ^ 1u);
                     ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)C::B_BYTES);
@@ -309,11 +327,14 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             ptx::mbar_wait(acc_empty(tl % NACC), ((tl / NACC) & 1u) ^ 1u);
+            int tp, tq;
+            tile_coords(ta, t, tp, tq);
             for (int s = 0; s < ta.nstages; ++s, ++g) {
                 const long long c0 = TS_CLK();
                 ptx::mbar_wait(full_a(g % SA), (g / SA) & 1u);
                 const long long c1 = TS_CLK();
-                ptx::mbar_wait(full_b(g % SB), (g / SB) & 1u);
+                if (ta.bres) ptx::mbar_wait(full_b(tq * ta.nstages + s), 0u);
+                else ptx::mbar_wait(full_b(g % SB), (g / SB) & 1u);
                 const long long c2 = TS_CLK();
                 if (lane == 0) { TS_PROF_ADD(4, c1 - c0); TS_PROF_ADD(5, c2 - c1); }
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
@@ -327,8 +348,10 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl % NACC;
             const uint32_t dt = tmem + acc * BN;
+            int tp, tq;
+            tile_coords(ta, t, tp, tq);
             for (int s = 0; s < ta.nstages; ++s, ++g) {
-                const int sa = g % SA, sb = g % SB;
+                const int sa = g % SA, sb = ta.bres ? tq * ta.nstages + s : (int)(g % SB);
                 const long long c0 = TS_CLK();
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
                 const long long c1 = TS_CLK();
@@ -346,7 +369,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                             ptx::mma_i8_ts(dt, at + 8 * k, bd + 2 * k, idesc, (s > 0 || k > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(empty_a(sa));
-                    ptx::mma_commit(empty_b(sb));
+                    if (!ta.bres) ptx::mma_commit(empty_b(sb));
                     if (s == ta.nstages - 1) ptx::mma_commit(acc_full(acc));
                     const long long c2 = TS_CLK();
                     TS_PROF_ADD(0, c1 - c0);
@@ -386,7 +409,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 const int this_sub = sub;
                 if (sub == nsub - 1 || s == ta.nstages - 1) { ++gp; sub = 0; } else { ++sub; }
                 if ((int)(g & (NUM_UGROUPS - 1)) != grp) continue;
-                const int sp = my_gp % SP, sa = g % SA;
+                const int sp = my_gp % nsp, sa = g % SA;
                 const bool two = (s != ta.nstages - 1) || ta.last_ksteps > 2;   // second 64-code half used
                 const long long u0 = TS_CLK();
                 uint4 v0, v1;
@@ -394,16 +417,15 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     v0 = implicit_chunk(ta, img, h0, w0, s * 32);
                     v1 = two ? implicit_chunk(ta, img, h0, w0, s * 32 + 16) : make_uint4(0, 0, 0, 0);
                 } else {
-                ptx::mbar_wait(full_p(sp), (my_gp / SP) & 1u);
+                ptx::mbar_wait(full_p(sp), (my_gp / nsp) & 1u);
                 const int sub_ = this_sub;
-                const uint8_t *row = smem + C::OFF_P + sp * C::P_BYTES + r * ta.pks;
-                if (ta.bulk) {
-                    v0 = *reinterpret_cast<const uint4 *>(row + sub_ * 32);
-                    v1 = two ? *reinterpret_cast<const uint4 *>(row + sub_ * 32 + 16) : make_uint4(0, 0, 0, 0);
-                } else {   // SWIZZLE_128B: 16-byte chunk c of row r lives at chunk c ^ (r % 8)
-                    v0 = *reinterpret_cast<const uint4 *>(row + (((sub_ * 2) ^ (r & 7)) << 4));
-                    v1 = two ? *reinterpret_cast<const uint4 *>(row + (((sub_ * 2 + 1) ^ (r & 7)) << 4)) : make_uint4(0, 0, 0, 0);
-                }
+                // TMA swizzle matched to the row pitch (none / 32 / 64 / 128 B): the 16-byte unit
+                // of the slot's linear offset is XORed with bits 7.. (conflict-free LDS.128)
+                const uint32_t lin = (uint32_t)(r * ta.pks + sub_ * 32), msk = (uint32_t)(ta.pks / 16 - 1);
+                const uint32_t sw0 = lin ^ (((lin >> 7) & msk) << 4), sw1 = (lin + 16) ^ ((((lin + 16) >> 7) & msk) << 4);
+                const uint32_t pbase = sbase + C::OFF_P + sp * pslot;
+                v0 = ptx::lds128(pbase + sw0);
+                v1 = two ? ptx::lds128(pbase + sw1) : make_uint4(0, 0, 0, 0);
                 __syncwarp();
                 if (lane == 0) {   // this warp's share of the packed slot is consumed
                     const int extra = (s == ta.nstages - 1) ? (NSUB_MAX - 1 - sub_) : (sub_ == nsub - 1 ? NSUB_MAX - nsub : 0);
@@ -454,8 +476,8 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         if (ta.f16 && ta.f16_tab) {
             uint32_t bad = 0;
             for (int i = threadIdx.x - EPI_WARP0 * 32; i < (int)(ta.nq >> 1); i += NEPI * 32) {
-                const int64_t n0 = (int64_t)__ldg(rq.bias + 2 * i) - ta.f16_thr0m1;
-                const int64_t n1 = (int64_t)__ldg(rq.bias + 2 * i + 1) - ta.f16_thr0m1;
+                const int64_t n0 = (rq.bias ? (int64_t)__ldg(rq.bias + 2 * i) : 0) - ta.f16_thr0m1;
+                const int64_t n1 = (rq.bias ? (int64_t)__ldg(rq.bias + 2 * i + 1) : 0) - ta.f16_thr0m1;
                 if ((n0 < 0 ? -n0 : n0) + ta.f16_accmax > 32767 || (n1 < 0 ? -n1 : n1) + ta.f16_accmax > 32767) bad = 1;
                 f16tab[i] = ((uint32_t)n0 & 0xFFFFu) | ((uint32_t)n1 << 16);
             }
@@ -638,7 +660,7 @@ EncodeTiledFn encode_fn_ts() {
     return fn;
 }
 
-// 2-D uint8 map over [rows][ld] with a {128 B, box_rows} box and the 128-byte swizzle
+// 2-D uint8 map over [rows][ld] with a {box_bytes, box_rows} box and the 128-byte swizzle
 #ifdef DG_TRACE
 extern "C" __attribute__((visibility("default"))) int dg_debug_ts_prof(unsigned long long *host16, int reset) {
     if (reset) {
@@ -649,15 +671,19 @@ extern "C" __attribute__((visibility("default"))) int dg_debug_ts_prof(unsigned 
 }
 #endif
 
-bool make_map_sw128(CUtensorMap *m, const void *base, int64_t ld, int64_t rows, int box_rows) {
+bool make_map_sw128(CUtensorMap *m, const void *base, int64_t ld, int64_t rows, int box_rows, int box_bytes) {
+    // swizzle span = box row bytes (16: none, 32, 64, 128)
+    const CUtensorMapSwizzle sw = box_bytes >= 128 ? CU_TENSOR_MAP_SWIZZLE_128B
+                                  : box_bytes == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                  : box_bytes == 32 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_NONE;
     EncodeTiledFn fn = encode_fn_ts();
     if (!fn) return false;
     cuuint64_t dims[2] = {(cuuint64_t)ld, (cuuint64_t)rows};
     cuuint64_t strides[1] = {(cuuint64_t)ld};
-    cuuint32_t box[2] = {128u, (cuuint32_t)box_rows};
+    cuuint32_t box[2] = {(cuuint32_t)box_bytes, (cuuint32_t)box_rows};
     cuuint32_t estr[2] = {1, 1};
     return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, estr,
-              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
@@ -709,10 +735,18 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     ta.ntp = (int32_t)((np + BM - 1) / BM);
     ta.ntq = (int32_t)((nq + BN - 1) / BN);
     ta.group = ta.ntq <= 4 ? 1 : (ta.ntp < 16 ? ta.ntp : 16);   // 1 = column block fastest
-    ta.bulk = (ldp <= 32 && ((uintptr_t)P & 15) == 0) ? 1 : 0;
-    ta.pks = ta.bulk ? (int32_t)ldp : PKS_MAX;
-    ta.P = P;
-    ta.ldp = ldp;
+    ta.last_grp = (ta.ntp - 1) / ta.group;
+    ta.last_rows = ta.ntp - ta.last_grp * ta.group;
+    ta.fd_pg = make_fastdiv((uint32_t)(ta.group * ta.ntq));
+    ta.fd_grp = make_fastdiv((uint32_t)ta.group);
+    ta.fd_last = make_fastdiv((uint32_t)ta.last_rows);
+    // packed P slots: TMA box {pks bytes, 128 rows} with the 128-byte swizzle; narrow rows
+    // (short K) get many slots so that enough HBM reads are in flight per SM
+    ta.pks = 16;
+    while (ta.pks < PKS_MAX && ta.pks < ldp) ta.pks *= 2;
+    ta.sp = C::P_REGION / (BM * ta.pks);
+    if (ta.sp > SP_MAX) ta.sp = SP_MAX;
+    ta.bres = ((int64_t)ta.ntq * ta.nstages <= C::SB && !getenv("DG_NO_BRES")) ? 1 : 0;
     ta.lp = pack_levels_i8(pl);
     ta.D = D;
     ta.ldd = ldd;
@@ -741,13 +775,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
             ta.f16_thr0m1 = (int32_t)thr0m1;
             ta.f16_accmax = (int32_t)acc_bound;
             ta.f16 = 1;
-            if (rq->bias && rq->bias_axis == 0) {
-                ta.f16_tab = 1;
-            } else if (!rq->bias) {
-                const int64_t n = -thr0m1;
-                ta.f16_na2 = ((uint32_t)n & 0xFFFFu) * 0x10001u;
-                if ((n < 0 ? -n : n) + acc_bound > 32767) ta.f16 = 0;
-            }
+            ta.f16_tab = (!rq->bias || rq->bias_axis == 0) ? 1 : 0;   // else: per-row offsets
         }
     }
     if (cv) {
@@ -766,12 +794,11 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         ta.Wo = cv->Wo;
         ta.kb = cv->kh * cv->kw * cv->Cb;
         ta.pad_word = 0x01010101u * (uint32_t)(cv->pad_code | (cv->pad_code << 2) | (cv->pad_code << 4) | (cv->pad_code << 6));
-        ta.bulk = 0;
     }
     CUtensorMap mp, mb;
     memset(&mp, 0, sizeof(mp));
-    if (!cv && !ta.bulk && !make_map_sw128(&mp, P, ldp, np, BM)) return DG_ERR_CUDA;
-    if (!make_map_sw128(&mb, Q8, ld8, nq, BN)) return DG_ERR_CUDA;
+    if (!cv && !make_map_sw128(&mp, P, ldp, np, BM, ta.pks)) return DG_ERR_CUDA;
+    if (!make_map_sw128(&mb, Q8, ld8, nq, BN, 128)) return DG_ERR_CUDA;
     static bool attr_set = false;
     if (!attr_set) {
         if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
@@ -814,10 +841,10 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     if (nq >= 256 && K >= 24 * KS && !getenv("DG_TS_NO_BN256"))
         return launch_ts<256, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     if (nq > 64) {
-        if (short_k) return launch_ts<128, 16, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (short_k) return launch_ts<128, 8, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         return launch_ts<128, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     }
-    if (short_k) return launch_ts<64, 8, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    if (short_k) return launch_ts<64, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     return launch_ts<64, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 }
 
