@@ -38,9 +38,9 @@ constexpr int SP_MAX = 32;       // packed P slots (narrow rows -> many slots in
 // Warp roles.  The SM sub-partition scheduler prefers the highest warp id among eligible
 // warps, so the latency-critical single-thread roles (TMA producer, MMA issuer) take the
 // highest ids and are never starved by the ALU-heavy unpack / epilogue warps.
-// NEPI (template) epilogue warps: 4 (one per TMEM lane quarter, all columns; more registers
-// for long-K tiles) or 8 (two per quarter, half the columns each; for short-K tiles, where
-// the epilogue dominates).
+// NEPI (template) epilogue warps: 4 x EG groups; a group (one warp per TMEM lane quarter, all
+// BN columns) owns every EG-th tile, so EG = 2 keeps two tiles' epilogues in flight (short-K
+// tiles, where the epilogue dominates).
 // NUNP (template) unpack warps: 4 (one stage group) or 8 (two groups owning alternate stages).
 template <int NEPI, int NUNP>
 struct Roles {
@@ -60,10 +60,13 @@ struct Roles {
 constexpr int HANDOFF_BAR = 1;
 constexpr int EPI_BAR = 2;       // epilogue warps only (requant table build)
 
-template <int BN>
+template <int BN, int EG>
 struct TsCfg {
-    static constexpr int NACC = BN == 256 ? 1 : (BN == 128 ? 3 : 4);   // accumulator buffers (TMEM cols NACC*BN)
-    static constexpr int SA = 4;                            // A stages in TMEM (32 cols each)
+    // accumulator buffers (TMEM cols NACC*BN); a multiple of EG so that each buffer has one
+    // epilogue group (which then waits on its barrier phases in order)
+    static constexpr int NACC = BN == 256 ? 1 : (BN == 128 ? 2 : 4);
+    static_assert(NACC % EG == 0, "accumulator buffers per epilogue group");
+    static constexpr int SA = 8;                            // A stages in TMEM (32 cols each), SA/NUGROUPS per unpack group
     static constexpr int SB = BN == 256 ? 3 : (BN == 128 ? 4 : 6);   // B (int8) smem stages
     static constexpr int TMEM_A0 = NACC * BN;               // first A column
     static constexpr int TMEM_COLS = 512;
@@ -79,16 +82,14 @@ struct TsCfg {
     static_assert(TMEM_A0 + SA * 32 <= TMEM_COLS, "TMEM budget");
 };
 
-#ifdef DG_EXP_NOST
-__device__ uint32_t ta_dummy_sink;
-#endif
 #ifdef DG_TRACE
-__device__ unsigned long long g_ts_prof[16];   // CTA 0 cycle counters (tools/trace_ts.py)
-#define TS_PROF_ADD(i, v) do { if (blockIdx.x == 0) atomicAdd(&g_ts_prof[i], (unsigned long long)(v)); } while (0)
-#define TS_CLK() clock64()
+// CTA 0 event timeline (tools/trace_ts.py): [event][stage or tile index] = clock(), recorded
+// in shared memory (a global store per event perturbs the pipeline) and copied out at the end
+constexpr int TL_N = 96;
+__device__ long long g_ts_tl[16][TL_N];
+#define TS_EV(e, i) do { if ((int)(i) < TL_N) s_tl[e][i] = (uint32_t)clock(); } while (0)
 #else
-#define TS_PROF_ADD(i, v) do { } while (0)
-#define TS_CLK() 0ll
+#define TS_EV(e, i) do { } while (0)
 #endif
 
 // n / d without a divide for 0 <= n < 2^31 (round-up multiplier; d >= 1):
@@ -109,7 +110,10 @@ struct TsArgs {
     int32_t group;         // tile rasterisation: GROUP row blocks x all column blocks, column-major inside
     int32_t last_grp, last_rows;   // index of the last row group and its row-block count
     FastDiv fd_pg, fd_grp, fd_last;  // / (group * ntq), / group, / last_rows
-    int32_t pks;           // packed P slot bytes per row (TMA box width, smem pitch): 16, 32, 64 or 128
+    int32_t pks;           // packed P slot bytes per row (smem pitch): ldp <= 64 (bulk) or 128 (TMA box)
+    int32_t bulk;          // 1: a tile's P rows are one contiguous span -> one bulk copy, unswizzled
+    const uint8_t *P;
+    int64_t ldp;
     int32_t sp;            // packed P slots (SP_MAX max)
     int32_t bres;          // 1: all ntq x nstages B tiles resident in smem (loaded once)
     uint32_t lp;           // int8 levels of P codes
@@ -225,7 +229,7 @@ template <int BN, int NEPI, int NUNP>
 __global__ void __launch_bounds__(Roles<NEPI, NUNP>::NT, 1)
 lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
-    using C = TsCfg<BN>;
+    using C = TsCfg<BN, NEPI / 4>;
     using R = Roles<NEPI, NUNP>;
     constexpr int SB = C::SB, SA = C::SA, NACC = C::NACC, SP = SP_MAX;
     const int nsp = ta.sp;
@@ -234,6 +238,10 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                   PRODUCER_WARP = R::PRODUCER_WARP, WAITER_WARP = R::WAITER_WARP, MMA_WARP = R::MMA_WARP,
                   NUM_UGROUPS = R::NUM_UGROUPS;
     extern __shared__ uint8_t smem_raw[];
+#ifdef DG_TRACE
+    __shared__ uint32_t s_tl[16][TL_N];
+    for (int i = threadIdx.x; i < 16 * TL_N; i += blockDim.x) (&s_tl[0][0])[i] = 0u;
+#endif
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = ptx::smem_u32(smem);
     const uint32_t bar0 = sbase + C::OFF_BAR;
@@ -253,11 +261,11 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 
     if (warp == PRODUCER_WARP) {
         if (lane == 0) {
-            if (!ta.implicit) ptx::tma_prefetch(&tm_p);
+            if (!ta.implicit && !ta.bulk) ptx::tma_prefetch(&tm_p);
             ptx::tma_prefetch(&tm_b);
             for (int s = 0; s < SP; ++s) {
                 ptx::mbar_init(full_p(s), 1);
-                ptx::mbar_init(empty_p(s), NSUB_MAX * 4);   // 4 warps (one group) per stage, NSUB_MAX stages
+                ptx::mbar_init(empty_p(s), nsub * 4);   // 4 warps (one group) per stage, nsub stages
             }
             for (int s = 0; s < SB; ++s) {
                 ptx::mbar_init(full_b(s), 1);
@@ -269,7 +277,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
             for (int a = 0; a < NACC; ++a) {
                 ptx::mbar_init(acc_full(a), 1);
-                ptx::mbar_init(acc_empty(a), NUM_EPI_WARPS);
+                ptx::mbar_init(acc_empty(a), 4);   // the 4 warps of the owning group
             }
             ptx::fence_mbar_init();
         }
@@ -287,39 +295,57 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     const uint32_t tmem = *tmem_slot;
 
     if (warp == PRODUCER_WARP) {
-        // ---------------- producer
-        if (lane == 0) {
-            uint32_t gp = 0, gb = 0;
-            if (ta.bres) {   // every B tile once: slot tq * nstages + s
-                for (int tq = 0; tq < ta.ntq; ++tq)
-                    for (int s = 0; s < ta.nstages; ++s) {
-                        const int j = tq * ta.nstages + s;
+        // ---------------- producer.  The whole warp runs the loop (a lone lane 0 with 31 lanes
+        // parked at the final __syncthreads ran the loop several times slower); lane 0 issues.
+        uint32_t gb = 0, pslot_i = 0, pphase = 0;
+        if (ta.bres) {   // every B tile once: slot tq * nstages + s
+            for (int tq = 0; tq < ta.ntq; ++tq)
+                for (int s = 0; s < ta.nstages; ++s) {
+                    const int j = tq * ta.nstages + s;
+                    if (lane == 0) {
                         ptx::mbar_arrive_expect_tx(full_b(j), (uint32_t)C::B_BYTES);
                         ptx::tma_load_2d(sbase + C::OFF_B + j * C::B_BYTES, &tm_b, full_b(j), s * KS, tq * BN);
                     }
-            }
-            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-                int tp, tq;
-                tile_coords(ta, t, tp, tq);
-                const int64_t p0 = (int64_t)tp * BM, q0 = (int64_t)tq * BN;
-                int sub = 0, ps = 0;
-                for (int s = 0; s < ta.nstages; ++s, ++gb) {
-                    if (sub == 0 && !ta.implicit) {   // next packed P stage (up to 512 codes of every row)
-                        const int slot = gp % nsp;
-                        ptx::mbar_wait(empty_p(slot), ((gp / nsp) & 1u) ^ 1u);
+                }
+            __syncwarp();
+        }
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            int tp, tq;
+            tile_coords(ta, t, tp, tq);
+            const int64_t p0 = (int64_t)tp * BM, q0 = (int64_t)tq * BN;
+            int sub = 0, ps = 0;
+            for (int s = 0; s < ta.nstages; ++s, ++gb) {
+                if (sub == 0 && !ta.implicit) {   // next packed P slot (up to 512 codes of every row)
+                    const int slot = (int)pslot_i;
+                    if (lane == 0) TS_EV(13, gb);
+                    ptx::mbar_wait(empty_p(slot), pphase ^ 1u);
+                    if (lane == 0) {
+                        TS_EV(14, gb);
                         const uint32_t dst = sbase + C::OFF_P + slot * pslot;
-                        ptx::mbar_arrive_expect_tx(full_p(slot), pslot);
-                        ptx::tma_load_2d(dst, &tm_p, full_p(slot), ps * ta.pks, (int32_t)p0);
-                        ++gp;
-                        ++ps;
+                        if (ta.bulk) {   // (a TMA box of narrow rows issues one request per row: slow)
+                            const int64_t rows = ta.np - p0 < BM ? ta.np - p0 : BM;
+                            const uint32_t bytes = (uint32_t)(rows * ta.ldp);
+                            ptx::mbar_arrive_expect_tx(full_p(slot), bytes);
+                            ptx::bulk_load(dst, ta.P + p0 * ta.ldp, bytes, full_p(slot));
+                        } else {
+                            ptx::mbar_arrive_expect_tx(full_p(slot), pslot);
+                            ptx::tma_load_2d(dst, &tm_p, full_p(slot), ps * ta.pks, (int32_t)p0);
+                        }
+                        TS_EV(12, gb);
                     }
-                    if (++sub == nsub) sub = 0;
-                    if (ta.bres) continue;
-                    const int bs = gb % SB;
-                    ptx::mbar_wait(empty_b(bs), ((gb / SB) & 1u) ^ 1u);
+                    __syncwarp();
+                    if (++pslot_i == (uint32_t)nsp) { pslot_i = 0; pphase ^= 1u; }
+                    ++ps;
+                }
+                if (++sub == nsub) sub = 0;
+                if (ta.bres) continue;
+                const int bs = gb % SB;
+                ptx::mbar_wait(empty_b(bs), ((gb / SB) & 1u) ^ 1u);
+                if (lane == 0) {
                     ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)C::B_BYTES);
                     ptx::tma_load_2d(sbase + C::OFF_B + bs * C::B_BYTES, &tm_b, full_b(bs), s * KS, (int32_t)q0);
                 }
+                __syncwarp();
             }
         }
     } else if (warp == WAITER_WARP) {
@@ -330,14 +356,15 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             int tp, tq;
             tile_coords(ta, t, tp, tq);
             for (int s = 0; s < ta.nstages; ++s, ++g) {
-                const long long c0 = TS_CLK();
-                ptx::mbar_wait(full_a(g % SA), (g / SA) & 1u);
-                const long long c1 = TS_CLK();
+                const int sa = g % SA;
+                if (lane == 0 && s == 0) TS_EV(3, tl);
+                ptx::mbar_wait(full_a(sa), (g / SA) & 1u);
+                if (lane == 0) TS_EV(4, g);
                 if (ta.bres) ptx::mbar_wait(full_b(tq * ta.nstages + s), 0u);
                 else ptx::mbar_wait(full_b(g % SB), (g / SB) & 1u);
-                const long long c2 = TS_CLK();
-                if (lane == 0) { TS_PROF_ADD(4, c1 - c0); TS_PROF_ADD(5, c2 - c1); }
+                if (lane == 0) TS_EV(5, g);
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
+                if (lane == 0) TS_EV(6, g);   // the MMA warp finished issuing stage g - 1
             }
         }
     } else if (warp == MMA_WARP) {
@@ -351,14 +378,16 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             int tp, tq;
             tile_coords(ta, t, tp, tq);
             for (int s = 0; s < ta.nstages; ++s, ++g) {
-                const int sa = g % SA, sb = ta.bres ? tq * ta.nstages + s : (int)(g % SB);
-                const long long c0 = TS_CLK();
+                const int sa = g % SA;
+                const int sb = ta.bres ? tq * ta.nstages + s : (int)(g % SB);
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
-                const long long c1 = TS_CLK();
                 ptx::tc_fence_after();
                 if (lane == 0) {
                     const uint32_t at = tmem + C::TMEM_A0 + sa * 32;
                     const uint64_t bd = bdesc0 + (uint64_t)((sb * C::B_BYTES) >> 4);   // +32 B per k-step = +2
+#ifdef DG_EXP_NOMMA
+                    if (false) {} else
+#endif
                     if (s < ta.nstages - 1 || ta.last_ksteps == KS / 32) {
                         ptx::mma_i8_ts(dt, at, bd, idesc, s > 0 ? 1u : 0u);
                         ptx::mma_i8_ts(dt, at + 8, bd + 2, idesc, 1u);
@@ -371,23 +400,21 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     ptx::mma_commit(empty_a(sa));
                     if (!ta.bres) ptx::mma_commit(empty_b(sb));
                     if (s == ta.nstages - 1) ptx::mma_commit(acc_full(acc));
-                    const long long c2 = TS_CLK();
-                    TS_PROF_ADD(0, c1 - c0);
-                    TS_PROF_ADD(2, c2 - c1);
-                    TS_PROF_ADD(3, 1);
                 }
                 __syncwarp();
             }
         }
     } else if (warp >= UNPACK_WARP0) {
-        // ---------------- unpackers: thread = row; packed smem -> int8 levels -> TMEM (A operand)
+        // ---------------- unpackers: thread = row; packed smem -> int8 levels -> TMEM (A operand).
+        // Groups of 4 warps (one per TMEM lane quarter) take alternate stages.
         const int uw = warp - UNPACK_WARP0;
         const int grp = uw / 4;                 // stage group
         const int quarter = warp & 3;           // TMEM lane quarter this warp may access
         const int r = quarter * 32 + lane;      // tile row
-        uint32_t g = 0, gp = 0;
+        const uint32_t trow_a = tmem + C::TMEM_A0 + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t msk = ta.bulk ? 0u : 7u;
+        uint32_t g = 0, pslot_i = 0, pphase = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            int sub = 0;
             // implicit conv: this thread's output pixel of the tile
             const uint8_t *img = ta.X;
             int32_t h0 = 0, w0 = 0;
@@ -404,73 +431,77 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 h0 = ho * ta.stride - ta.pad;
                 w0 = wo * ta.stride - ta.pad;
             }
+            int sub = 0;
             for (int s = 0; s < ta.nstages; ++s, ++g) {
-                const uint32_t my_gp = gp;
-                const int this_sub = sub;
-                if (sub == nsub - 1 || s == ta.nstages - 1) { ++gp; sub = 0; } else { ++sub; }
+                const int slot = (int)pslot_i;
+                const uint32_t ph = pphase;
+                const int sub_ = sub;
+                const bool last_in_slot = (sub == nsub - 1) || (s == ta.nstages - 1);
+                if (last_in_slot) {
+                    sub = 0;
+                    if (++pslot_i == (uint32_t)nsp) { pslot_i = 0; pphase ^= 1u; }
+                } else {
+                    ++sub;
+                }
                 if ((int)(g & (NUM_UGROUPS - 1)) != grp) continue;
-                const int sp = my_gp % nsp, sa = g % SA;
+                const int sa = g % SA;
                 const bool two = (s != ta.nstages - 1) || ta.last_ksteps > 2;   // second 64-code half used
-                const long long u0 = TS_CLK();
+                if (lane == 0 && quarter == 0) TS_EV(0, g);
                 uint4 v0, v1;
                 if (ta.implicit) {
                     v0 = implicit_chunk(ta, img, h0, w0, s * 32);
                     v1 = two ? implicit_chunk(ta, img, h0, w0, s * 32 + 16) : make_uint4(0, 0, 0, 0);
                 } else {
-                ptx::mbar_wait(full_p(sp), (my_gp / nsp) & 1u);
-                const int sub_ = this_sub;
-                // TMA swizzle matched to the row pitch (none / 32 / 64 / 128 B): the 16-byte unit
-                // of the slot's linear offset is XORed with bits 7.. (conflict-free LDS.128)
-                const uint32_t lin = (uint32_t)(r * ta.pks + sub_ * 32), msk = (uint32_t)(ta.pks / 16 - 1);
-                const uint32_t sw0 = lin ^ (((lin >> 7) & msk) << 4), sw1 = (lin + 16) ^ ((((lin + 16) >> 7) & msk) << 4);
-                const uint32_t pbase = sbase + C::OFF_P + sp * pslot;
-                v0 = ptx::lds128(pbase + sw0);
-                v1 = two ? ptx::lds128(pbase + sw1) : make_uint4(0, 0, 0, 0);
-                __syncwarp();
-                if (lane == 0) {   // this warp's share of the packed slot is consumed
-                    const int extra = (s == ta.nstages - 1) ? (NSUB_MAX - 1 - sub_) : (sub_ == nsub - 1 ? NSUB_MAX - nsub : 0);
-                    ptx::mbar_arrive(empty_p(sp));
-                    for (int e = 0; e < extra; ++e) ptx::mbar_arrive(empty_p(sp));
+                    ptx::mbar_wait(full_p(slot), ph);
+                    // TMA slots carry the 128-byte swizzle: the 16-byte unit (bits 4-6) of the
+                    // slot's linear offset is XORed with bits 7-9 (conflict-free LDS.128)
+                    const uint32_t pbase = sbase + C::OFF_P + slot * pslot;
+                    const uint32_t lin = (uint32_t)(r * ta.pks + sub_ * 32);
+                    v0 = ptx::lds128(pbase + (lin ^ (((lin >> 7) & msk) << 4)));
+                    v1 = two ? ptx::lds128(pbase + ((lin + 16) ^ ((((lin + 16) >> 7) & msk) << 4))) : make_uint4(0, 0, 0, 0);
+                    __syncwarp();
+                    if (lane == 0)   // this warp's share of the slot is consumed (+ the slot's unused stages)
+                        ptx::mbar_arrive_cnt(empty_p(slot), 1u + (s == ta.nstages - 1 ? (uint32_t)(nsub - 1 - sub_) : 0u));
                 }
-                }   // !implicit
-                uint32_t a[32];
+                uint32_t a[32];   // [16, 32) only written (and stored) for a full stage
                 {
                     const uint32_t w[4] = {v0.x, v0.y, v0.z, v0.w};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint4 o = unpack16_levels(w[j], ta.lp);
-                        a[4 * j] = o.x; a[4 * j + 1] = o.y; a[4 * j + 2] = o.z; a[4 * j + 3] = o.w;
+                    for (int i = 0; i < 4; ++i) {
+                        const uint4 o = unpack16_levels(w[i], ta.lp);
+                        a[4 * i] = o.x; a[4 * i + 1] = o.y; a[4 * i + 2] = o.z; a[4 * i + 3] = o.w;
                     }
                 }
                 if (two) {
                     const uint32_t w[4] = {v1.x, v1.y, v1.z, v1.w};
 #pragma unroll
-                    for (int j = 0; j < 4; ++j) {
-                        const uint4 o = unpack16_levels(w[j], ta.lp);
-                        a[16 + 4 * j] = o.x; a[16 + 4 * j + 1] = o.y; a[16 + 4 * j + 2] = o.z; a[16 + 4 * j + 3] = o.w;
+                    for (int i = 0; i < 4; ++i) {
+                        const uint4 o = unpack16_levels(w[i], ta.lp);
+                        a[16 + 4 * i] = o.x; a[16 + 4 * i + 1] = o.y; a[16 + 4 * i + 2] = o.z; a[16 + 4 * i + 3] = o.w;
                     }
-                } else {
-#pragma unroll
-                    for (int j = 16; j < 32; ++j) a[j] = 0;   // k-steps 2, 3 of the last stage are not issued
                 }
-                ptx::mbar_wait(empty_a(sa), ((g / SA) & 1u) ^ 1u);
+                if (lane == 0 && quarter == 0) TS_EV(1, g);
+                ptx::mbar_wait(empty_a(sa), ((g / SA) & 1u) ^ 1u);   // MMA(g - SA) completed
+                if (lane == 0 && quarter == 0) TS_EV(11, g);
                 ptx::tc_fence_after();
-#ifndef DG_EXP_NOST
-                ptx::tmem_st_32x32b_x32(tmem + C::TMEM_A0 + sa * 32 + ((uint32_t)(quarter * 32) << 16), a);
+#ifndef DG_EXP_NOUNPACK
+                // a half stage (k-steps 2, 3 not issued) stores only its 16 columns
+                if (two) ptx::tmem_st_32x32b_x32(trow_a + sa * 32, a);
+                else ptx::tmem_st_32x32b_x16(trow_a + sa * 32, a);
                 ptx::tmem_st_wait();
 #else
-                if (a[0] == 0x12345678u && a[5] == 7u) ta_dummy_sink = a[3];
+                if (a[0] == 0x12345u && a[3] == 0x777u) f16tab[1] = a[2];
 #endif
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(full_a(sa));
-                if (lane == 0 && warp == UNPACK_WARP0) { TS_PROF_ADD(12, TS_CLK() - u0); TS_PROF_ADD(13, 1); }
+                if (lane == 0 && quarter == 0) TS_EV(2, g);
             }
         }
     } else {
-        // ---------------- epilogue (lane quarter = warp % 4, column part = warp / 4)
-        constexpr int HALF = BN / (NEPI / 4), NCH = HALF / 32;
-        static_assert(HALF % 32 == 0, "epilogue column part must be a multiple of 32");
+        // ---------------- epilogue (lane quarter = warp % 4, tile group = warp / 4)
+        constexpr int EG = NEPI / 4, HALF = BN, NCH = BN / 32;
+        static_assert(NCH % 2 == 0, "epilogue loads 64 columns at a time");
         // 16-bit requant offsets per column pair (bias_axis 0): negA = bias - (thr0 - 1), checked
         // against int16 overflow of acc + negA; any failure sends every tile to the 32-bit path
         if (ta.f16 && ta.f16_tab) {
@@ -485,32 +516,33 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             ptx::named_bar_sync(EPI_BAR, NEPI * 32);
         }
         const bool f16_ok = ta.f16 && *f16_flag == 0u;
-        const int quarter = warp & 3, half = (warp - EPI_WARP0) >> 2;
+        const int quarter = warp & 3, eg = (warp - EPI_WARP0) >> 2, half = 0;
         const bool col_bias = rq.bias && rq.bias_axis == 0;
         uint32_t tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            if (EG > 1 && (int)(tl % EG) != eg) continue;
             const uint32_t acc = tl % NACC;
             int tp, tq;
             tile_coords(ta, t, tp, tq);
             const int64_t p = (int64_t)tp * BM + quarter * 32 + lane;
             const int64_t q0 = (int64_t)tq * BN + half * HALF;
-            const long long e0 = TS_CLK();
+            if (lane == 0 && quarter == 0) TS_EV(8, tl);
             ptx::mbar_wait(acc_full(acc), (tl / NACC) & 1u);
-            const long long e1 = TS_CLK();
-            if (lane == 0 && warp == 0) { TS_PROF_ADD(8, e1 - e0); TS_PROF_ADD(11, 1); }
+            if (lane == 0 && quarter == 0) TS_EV(9, tl);
             ptx::tc_fence_after();
             const uint32_t trow = tmem + acc * BN + half * HALF + ((uint32_t)(quarter * 32) << 16);
             const bool fast = ta.fast_rq && q0 + HALF <= ta.nq;
             const int32_t rb = (fast && rq.bias && rq.bias_axis == 1 && p < ta.np) ? __ldg(rq.bias + p) : 0;
+            // 16-bit SIMD path (warp-uniform): per-row offsets need every lane's row in range
+            bool use16 = fast && f16_ok;
 #ifdef DG_EXP_NOEPI
-            if (true) {
+            {
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
-            } else
+                continue;
+            }
 #endif
-            // 16-bit SIMD path (warp-uniform): per-row offsets need every lane's row in range
-            bool use16 = fast && f16_ok;
             uint32_t na_row = ta.f16_na2;
             if (use16 && !ta.f16_tab && rq.bias && rq.bias_axis == 1) {
                 const int64_t n = (int64_t)rb - ta.f16_thr0m1;
@@ -519,33 +551,42 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
             if (use16) {
 #pragma unroll 1
-                for (int c = 0; c < NCH; ++c) {
-                    const int64_t qc = q0 + c * 32;
-                    uint32_t na[16];
-                    if (ta.f16_tab) {
-                        const uint32_t ta4 = sbase + C::OFF_TAB + (uint32_t)(qc >> 1) * 4u;
-#pragma unroll
-                        for (int j = 0; j < 4; ++j) {
-                            const uint4 t4 = ptx::lds128(ta4 + 16 * j);
-                            na[4 * j] = t4.x; na[4 * j + 1] = t4.y; na[4 * j + 2] = t4.z; na[4 * j + 3] = t4.w;
-                        }
-                    } else {
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) na[j] = na_row;
-                    }
-                    uint32_t r16[16];
-                    ptx::tmem_ld_32x32b_x16_pack16(trow + c * 32, r16);
+                for (int c = 0; c < NCH; c += 2) {   // 64 columns per TMEM load
+                    uint32_t r16[32];
+                    ptx::tmem_ld_32x32b_x32_pack16(trow + c * 32, r16);
                     ptx::tmem_ld_wait();
-                    if (c == NCH - 1) {
+                    if (c == NCH - 2) {
                         ptx::tc_fence_before();
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
                     }
-                    if (p >= ta.np) continue;
-                    const uint2 o = requant16_32(r16, na, ta.f16_w2, ta.f16_m, ta.f16_c2);
-                    uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
-                    if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = o;
-                    else store_codes32_ts(dp, o.x, o.y, 8);
+#pragma unroll
+                    for (int hh = 0; hh < 2; ++hh) {
+                        const int64_t qc = q0 + (c + hh) * 32;
+                        uint32_t na[16];
+                        if (ta.f16_tab) {
+                            const uint32_t ta4 = sbase + C::OFF_TAB + (uint32_t)(qc >> 1) * 4u;
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const uint4 t4 = ptx::lds128(ta4 + 16 * j);
+                                na[4 * j] = t4.x; na[4 * j + 1] = t4.y; na[4 * j + 2] = t4.z; na[4 * j + 3] = t4.w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) na[j] = na_row;
+                        }
+                        uint32_t rr[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) rr[j] = r16[16 * hh + j];
+                        if (p >= ta.np) continue;
+                        const uint2 o = requant16_32(rr, na, ta.f16_w2, ta.f16_m, ta.f16_c2);
+#ifdef DG_EXP_NOSTORE
+                        if (o.x == 0x12345678u && o.y == 0x9abcdef0u)
+#endif
+                        uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
+                        if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = o;
+                        else store_codes32_ts(dp, o.x, o.y, 8);
+                    }
                 }
             } else if (!fast) {
 #pragma unroll 1
@@ -600,13 +641,16 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     else store_codes32_ts(dp, o0, o1, 8);
                 }
             }
-            const long long e2 = TS_CLK();
-            if (lane == 0 && warp == 0) TS_PROF_ADD(9, e2 - e1);
+            if (lane == 0 && quarter == 0) TS_EV(10, tl);
         }
     }
 
     ptx::tc_fence_before();
     __syncthreads();
+#ifdef DG_TRACE
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < 16 * TL_N; i += blockDim.x) (&g_ts_tl[0][0])[i] = (&s_tl[0][0])[i];
+#endif
     if (warp == PRODUCER_WARP) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
 }
 
@@ -662,12 +706,12 @@ EncodeTiledFn encode_fn_ts() {
 
 // 2-D uint8 map over [rows][ld] with a {box_bytes, box_rows} box and the 128-byte swizzle
 #ifdef DG_TRACE
-extern "C" __attribute__((visibility("default"))) int dg_debug_ts_prof(unsigned long long *host16, int reset) {
+extern "C" __attribute__((visibility("default"))) int dg_debug_ts_timeline(long long *host, int reset) {
     if (reset) {
-        unsigned long long z[16] = {0};
-        return cudaMemcpyToSymbol(g_ts_prof, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+        static long long z[16 * TL_N];
+        return cudaMemcpyToSymbol(g_ts_tl, z, sizeof(z)) == cudaSuccess ? 0 : -1;
     }
-    return cudaMemcpyFromSymbol(host16, g_ts_prof, sizeof(unsigned long long) * 16) == cudaSuccess ? 0 : -1;
+    return cudaMemcpyFromSymbol(host, g_ts_tl, sizeof(long long) * 16 * TL_N) == cudaSuccess ? 0 : -1;
 }
 #endif
 
@@ -718,7 +762,7 @@ template <int BN, int NEPI, int NUNP>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                     cudaStream_t st, const TsConv *cv) {
-    using C = TsCfg<BN>;
+    using C = TsCfg<BN, NEPI / 4>;
     int64_t acc_bound = 0;   // K * max |pl[a] * ql[b]|
     for (int a = 0; a < 4; ++a)
         for (int b = 0; b < 4; ++b) {
@@ -742,8 +786,10 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     ta.fd_last = make_fastdiv((uint32_t)ta.last_rows);
     // packed P slots: TMA box {pks bytes, 128 rows} with the 128-byte swizzle; narrow rows
     // (short K) get many slots so that enough HBM reads are in flight per SM
-    ta.pks = 16;
-    while (ta.pks < PKS_MAX && ta.pks < ldp) ta.pks *= 2;
+    ta.bulk = (!cv && ldp <= 64 && ((uintptr_t)P & 15) == 0) ? 1 : 0;
+    ta.pks = ta.bulk ? (int32_t)ldp : PKS_MAX;
+    ta.P = P;
+    ta.ldp = ldp;
     ta.sp = C::P_REGION / (BM * ta.pks);
     if (ta.sp > SP_MAX) ta.sp = SP_MAX;
     ta.bres = ((int64_t)ta.ntq * ta.nstages <= C::SB && !getenv("DG_NO_BRES")) ? 1 : 0;
@@ -797,7 +843,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     }
     CUtensorMap mp, mb;
     memset(&mp, 0, sizeof(mp));
-    if (!cv && !make_map_sw128(&mp, P, ldp, np, BM, ta.pks)) return DG_ERR_CUDA;
+    if (!cv && !ta.bulk && !make_map_sw128(&mp, P, ldp, np, BM, ta.pks)) return DG_ERR_CUDA;
     if (!make_map_sw128(&mb, Q8, ld8, nq, BN, 128)) return DG_ERR_CUDA;
     static bool attr_set = false;
     if (!attr_set) {
@@ -844,7 +890,8 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
         if (short_k) return launch_ts<128, 8, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         return launch_ts<128, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     }
-    if (short_k) return launch_ts<64, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    if (short_k && getenv("DG_TS_UNP4")) return launch_ts<64, 8, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    if (short_k) return launch_ts<64, 8, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     return launch_ts<64, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 }
 

@@ -169,7 +169,7 @@ void run(int sms) {
     cudaFree(d);
 }
 
-int main() {
+int main(int argc, char **argv) {
     int sms = 0;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
     run<64, true>(sms);
@@ -177,9 +177,17 @@ int main() {
     run<256, true>(sms);
     run<128, false>(sms);
     run<256, false>(sms);
-    run<128, true, 3>(sms);
-    run<128, true, 14>(sms);
-    run<128, true, 15>(sms);
-    run<128, true, 16>(sms);
+    if (argc > 1) {   // pipeline-interaction modes (see MODE above)
+        run<64, true, 1>(sms);
+        run<64, true, 3>(sms);
+        run<64, true, 4>(sms);
+        run<64, true, 5>(sms);
+        run<64, true, 6>(sms);
+        run<64, true, 8>(sms);
+        run<64, true, 13>(sms);
+        run<128, true, 1>(sms);
+        run<128, true, 4>(sms);
+        run<128, true, 5>(sms);
+    }
     return 0;
 }
