@@ -30,11 +30,10 @@ namespace dg {
 namespace {
 
 constexpr int BM = 128;          // TMEM lanes / P rows per tile
-constexpr int KS = 128;          // codes per stage (= one 128-byte int8 B row, 32 TMEM columns of A)
-constexpr int PKS_MAX = 128;     // packed bytes per row per packed stage (512 codes)
-constexpr int NSUB_MAX = PKS_MAX * 4 / KS;   // 4 stages per packed stage
-constexpr int TAB_PAIRS = 2048;
-constexpr int SP_MAX = 32;       // packed P slots (narrow rows -> many slots in flight)  // per-column requant table (16-bit SIMD epilogue): nq <= 4096
+constexpr int KA = 128;          // codes per B "atom": one 128-byte SW128 int8 row, 32 TMEM columns of A
+constexpr int PKS_MAX = 128;     // packed bytes per row per packed slot (512 codes)
+constexpr int TAB_PAIRS = 2048;  // per-column requant table (16-bit SIMD epilogue): nq <= 4096
+constexpr int SP_MAX = 32;       // packed P slots (narrow rows -> many slots in flight)
 // Warp roles.  The SM sub-partition scheduler prefers the highest warp id among eligible
 // warps, so the latency-critical single-thread roles (TMA producer, MMA issuer) take the
 // highest ids and are never starved by the ALU-heavy unpack / epilogue warps.
@@ -60,17 +59,25 @@ struct Roles {
 constexpr int HANDOFF_BAR = 1;
 constexpr int EPI_BAR = 2;       // epilogue warps only (requant table build)
 
-template <int BN, int EG>
+// KST (template): codes per pipeline stage, 128 or 256.  Every stage costs a fixed number of
+// mbarrier / named-barrier hops (~150 cycles each, tools/sync_bench.cu) in the unpack, waiter and
+// MMA roles, so long-K tiles use 256-code stages (8 MMAs of K = 32 per hand-off).
+template <int BN, int EG, int KST>
 struct TsCfg {
+    static constexpr int KSTEPS = KST / 32;                 // MMAs (K = 32) per stage
+    static constexpr int ACOLS = KST / 4;                   // TMEM columns of one A stage
+    static constexpr int HALVES = KST / KA;                 // 128-code halves (B atoms, 32-column A parts)
     // accumulator buffers (TMEM cols NACC*BN); a multiple of EG so that each buffer has one
     // epilogue group (which then waits on its barrier phases in order)
     static constexpr int NACC = BN == 256 ? 1 : (BN == 128 ? 2 : 4);
     static_assert(NACC % EG == 0, "accumulator buffers per epilogue group");
-    static constexpr int SA = 8;                            // A stages in TMEM (32 cols each), SA/NUGROUPS per unpack group
-    static constexpr int SB = BN == 256 ? 3 : (BN == 128 ? 4 : 6);   // B (int8) smem stages
+    static constexpr int SA = (512 - NACC * BN) / ACOLS > 8 ? 8 : (512 - NACC * BN) / ACOLS;   // A stages in TMEM
+    static constexpr int B_ATOM = BN * KA;                  // bytes of one 128-code B atom
+    static constexpr int B_BYTES = BN * KST;
+    static constexpr int SB_RAW = (BN == 64 ? 98304 : 131072) / B_BYTES;
+    static constexpr int SB = SB_RAW > 8 ? 8 : SB_RAW;      // B (int8) smem stages
     static constexpr int TMEM_A0 = NACC * BN;               // first A column
     static constexpr int TMEM_COLS = 512;
-    static constexpr int B_BYTES = BN * KS;
     static constexpr int P_REGION = 4 * BM * PKS_MAX;      // packed P slots: ta.sp x (BM x ta.pks) bytes
     static constexpr int OFF_B = 0;                          // 1024-aligned (SW128)
     static constexpr int OFF_P = OFF_B + SB * B_BYTES;
@@ -79,7 +86,7 @@ struct TsCfg {
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr int OFF_TAB = (OFF_TMEM + 16 + 15) / 16 * 16;   // 16-bit requant offsets, one u32 per column pair
     static constexpr int ALLOC = OFF_TAB + TAB_PAIRS * 4 + 1024;
-    static_assert(TMEM_A0 + SA * 32 <= TMEM_COLS, "TMEM budget");
+    static_assert(TMEM_A0 + SA * ACOLS <= TMEM_COLS && SA >= 2, "TMEM budget");
 };
 
 #ifdef DG_TRACE
@@ -225,11 +232,11 @@ __device__ __noinline__ void ts_epilogue_general(const TsArgs &ta, const Requant
     store_codes32_ts(dp, o0, o1, (int)((ta.nq - qc + 3) / 4));
 }
 
-template <int BN, int NEPI, int NUNP>
+template <int BN, int NEPI, int NUNP, int KST>
 __global__ void __launch_bounds__(Roles<NEPI, NUNP>::NT, 1)
 lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
-    using C = TsCfg<BN, NEPI / 4>;
+    using C = TsCfg<BN, NEPI / 4, KST>;
     using R = Roles<NEPI, NUNP>;
     constexpr int SB = C::SB, SA = C::SA, NACC = C::NACC, SP = SP_MAX;
     const int nsp = ta.sp;
@@ -257,7 +264,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int ntiles = ta.ntp * ta.ntq;
-    const int nsub = (ta.pks * 4 + KS - 1) / KS;   // stages per packed slot
+    const int nsub = (ta.pks * 4 + KST - 1) / KST;   // stages per packed slot
 
     if (warp == PRODUCER_WARP) {
         if (lane == 0) {
@@ -304,7 +311,10 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     const int j = tq * ta.nstages + s;
                     if (lane == 0) {
                         ptx::mbar_arrive_expect_tx(full_b(j), (uint32_t)C::B_BYTES);
-                        ptx::tma_load_2d(sbase + C::OFF_B + j * C::B_BYTES, &tm_b, full_b(j), s * KS, tq * BN);
+#pragma unroll
+                        for (int h = 0; h < C::HALVES; ++h)
+                            ptx::tma_load_2d(sbase + C::OFF_B + j * C::B_BYTES + h * C::B_ATOM, &tm_b, full_b(j),
+                                             s * KST + h * KA, tq * BN);
                     }
                 }
             __syncwarp();
@@ -343,7 +353,10 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 ptx::mbar_wait(empty_b(bs), ((gb / SB) & 1u) ^ 1u);
                 if (lane == 0) {
                     ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)C::B_BYTES);
-                    ptx::tma_load_2d(sbase + C::OFF_B + bs * C::B_BYTES, &tm_b, full_b(bs), s * KS, (int32_t)q0);
+#pragma unroll
+                    for (int h = 0; h < C::HALVES; ++h)
+                        ptx::tma_load_2d(sbase + C::OFF_B + bs * C::B_BYTES + h * C::B_ATOM, &tm_b, full_b(bs),
+                                         s * KST + h * KA, (int32_t)q0);
                 }
                 __syncwarp();
             }
@@ -383,19 +396,21 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
                 ptx::tc_fence_after();
                 if (lane == 0) {
-                    const uint32_t at = tmem + C::TMEM_A0 + sa * 32;
-                    const uint64_t bd = bdesc0 + (uint64_t)((sb * C::B_BYTES) >> 4);   // +32 B per k-step = +2
+                    const uint32_t at = tmem + C::TMEM_A0 + sa * C::ACOLS;
+                    const uint64_t bd = bdesc0 + (uint64_t)((sb * C::B_BYTES) >> 4);
+                    // k-step k: A columns 8k, B atom k/4 (+B_ATOM bytes), 32 bytes (+2) per k-step inside
 #ifdef DG_EXP_NOMMA
                     if (false) {} else
 #endif
-                    if (s < ta.nstages - 1 || ta.last_ksteps == KS / 32) {
-                        ptx::mma_i8_ts(dt, at, bd, idesc, s > 0 ? 1u : 0u);
-                        ptx::mma_i8_ts(dt, at + 8, bd + 2, idesc, 1u);
-                        ptx::mma_i8_ts(dt, at + 16, bd + 4, idesc, 1u);
-                        ptx::mma_i8_ts(dt, at + 24, bd + 6, idesc, 1u);
+                    if (s < ta.nstages - 1 || ta.last_ksteps == C::KSTEPS) {
+#pragma unroll
+                        for (int k = 0; k < C::KSTEPS; ++k)
+                            ptx::mma_i8_ts(dt, at + 8 * k, bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3), idesc,
+                                           (s > 0 || k > 0) ? 1u : 0u);
                     } else {
                         for (int k = 0; k < ta.last_ksteps; ++k)
-                            ptx::mma_i8_ts(dt, at + 8 * k, bd + 2 * k, idesc, (s > 0 || k > 0) ? 1u : 0u);
+                            ptx::mma_i8_ts(dt, at + 8 * k, bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3), idesc,
+                                           (s > 0 || k > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(empty_a(sa));
                     if (!ta.bres) ptx::mma_commit(empty_b(sb));
@@ -445,53 +460,58 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
                 if ((int)(g & (NUM_UGROUPS - 1)) != grp) continue;
                 const int sa = g % SA;
-                const bool two = (s != ta.nstages - 1) || ta.last_ksteps > 2;   // second 64-code half used
+                // 16-byte chunks (64 codes, 2 k-steps) of this stage that the MMA reads
+                const int nchunk = (s != ta.nstages - 1) ? 2 * C::HALVES : (ta.last_ksteps + 1) / 2;
                 if (lane == 0 && quarter == 0) TS_EV(0, g);
-                uint4 v0, v1;
+                uint4 v[2 * C::HALVES];
                 if (ta.implicit) {
-                    v0 = implicit_chunk(ta, img, h0, w0, s * 32);
-                    v1 = two ? implicit_chunk(ta, img, h0, w0, s * 32 + 16) : make_uint4(0, 0, 0, 0);
+#pragma unroll
+                    for (int c = 0; c < 2 * C::HALVES; ++c)
+                        v[c] = c < nchunk ? implicit_chunk(ta, img, h0, w0, s * (KST / 4) + 16 * c) : make_uint4(0, 0, 0, 0);
                 } else {
                     ptx::mbar_wait(full_p(slot), ph);
                     // TMA slots carry the 128-byte swizzle: the 16-byte unit (bits 4-6) of the
                     // slot's linear offset is XORed with bits 7-9 (conflict-free LDS.128)
                     const uint32_t pbase = sbase + C::OFF_P + slot * pslot;
-                    const uint32_t lin = (uint32_t)(r * ta.pks + sub_ * 32);
-                    v0 = ptx::lds128(pbase + (lin ^ (((lin >> 7) & msk) << 4)));
-                    v1 = two ? ptx::lds128(pbase + ((lin + 16) ^ ((((lin + 16) >> 7) & msk) << 4))) : make_uint4(0, 0, 0, 0);
+                    const uint32_t lin0 = (uint32_t)(r * ta.pks + sub_ * (KST / 4));
+#pragma unroll
+                    for (int c = 0; c < 2 * C::HALVES; ++c) {
+                        const uint32_t lin = lin0 + 16 * c;
+                        v[c] = c < nchunk ? ptx::lds128(pbase + (lin ^ (((lin >> 7) & msk) << 4))) : make_uint4(0, 0, 0, 0);
+                    }
                     __syncwarp();
                     if (lane == 0)   // this warp's share of the slot is consumed (+ the slot's unused stages)
                         ptx::mbar_arrive_cnt(empty_p(slot), 1u + (s == ta.nstages - 1 ? (uint32_t)(nsub - 1 - sub_) : 0u));
-                }
-                uint32_t a[32];   // [16, 32) only written (and stored) for a full stage
-                {
-                    const uint32_t w[4] = {v0.x, v0.y, v0.z, v0.w};
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint4 o = unpack16_levels(w[i], ta.lp);
-                        a[4 * i] = o.x; a[4 * i + 1] = o.y; a[4 * i + 2] = o.z; a[4 * i + 3] = o.w;
-                    }
-                }
-                if (two) {
-                    const uint32_t w[4] = {v1.x, v1.y, v1.z, v1.w};
-#pragma unroll
-                    for (int i = 0; i < 4; ++i) {
-                        const uint4 o = unpack16_levels(w[i], ta.lp);
-                        a[16 + 4 * i] = o.x; a[16 + 4 * i + 1] = o.y; a[16 + 4 * i + 2] = o.z; a[16 + 4 * i + 3] = o.w;
-                    }
                 }
                 if (lane == 0 && quarter == 0) TS_EV(1, g);
                 ptx::mbar_wait(empty_a(sa), ((g / SA) & 1u) ^ 1u);   // MMA(g - SA) completed
                 if (lane == 0 && quarter == 0) TS_EV(11, g);
                 ptx::tc_fence_after();
+#pragma unroll
+                for (int h = 0; h < C::HALVES; ++h) {
+                    if (2 * h >= nchunk) break;
+                    uint32_t a[32];   // [16, 32) only written (and stored) when the second chunk is read
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        if (c == 1 && 2 * h + 1 >= nchunk) break;
+                        const uint4 vv = v[2 * h + c];
+                        const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const uint4 o = unpack16_levels(w[i], ta.lp);
+                            a[16 * c + 4 * i] = o.x; a[16 * c + 4 * i + 1] = o.y; a[16 * c + 4 * i + 2] = o.z;
+                            a[16 * c + 4 * i + 3] = o.w;
+                        }
+                    }
 #ifndef DG_EXP_NOUNPACK
-                // a half stage (k-steps 2, 3 not issued) stores only its 16 columns
-                if (two) ptx::tmem_st_32x32b_x32(trow_a + sa * 32, a);
-                else ptx::tmem_st_32x32b_x16(trow_a + sa * 32, a);
-                ptx::tmem_st_wait();
+                    const uint32_t ta_col = trow_a + sa * C::ACOLS + h * 32;
+                    if (2 * h + 1 < nchunk) ptx::tmem_st_32x32b_x32(ta_col, a);
+                    else ptx::tmem_st_32x32b_x16(ta_col, a);   // a half part: only its 16 columns are read
 #else
-                if (a[0] == 0x12345u && a[3] == 0x777u) f16tab[1] = a[2];
+                    if (a[0] == 0x12345u && a[3] == 0x777u) f16tab[1] = a[2];
 #endif
+                }
+                ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(full_a(sa));
@@ -758,11 +778,11 @@ bool f16_params(int64_t t0, int64_t t1, int64_t t2, uint32_t &m_out, uint32_t &c
     return false;
 }
 
-template <int BN, int NEPI, int NUNP>
+template <int BN, int NEPI, int NUNP, int KST>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                     cudaStream_t st, const TsConv *cv) {
-    using C = TsCfg<BN, NEPI / 4>;
+    using C = TsCfg<BN, NEPI / 4, KST>;
     int64_t acc_bound = 0;   // K * max |pl[a] * ql[b]|
     for (int a = 0; a < 4; ++a)
         for (int b = 0; b < 4; ++b) {
@@ -773,9 +793,9 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     TsArgs ta{};
     ta.np = np;
     ta.nq = nq;
-    ta.nstages = (int32_t)((K + KS - 1) / KS);
+    ta.nstages = (int32_t)((K + KST - 1) / KST);
     const int64_t kmma = (K + 31) / 32 * 32;
-    ta.last_ksteps = (int32_t)((kmma - (int64_t)(ta.nstages - 1) * KS) / 32);
+    ta.last_ksteps = (int32_t)((kmma - (int64_t)(ta.nstages - 1) * KST) / 32);
     ta.ntp = (int32_t)((np + BM - 1) / BM);
     ta.ntq = (int32_t)((nq + BN - 1) / BN);
     ta.group = ta.ntq <= 4 ? 1 : (ta.ntp < 16 ? ta.ntp : 16);   // 1 = column block fastest
@@ -847,7 +867,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     if (!make_map_sw128(&mb, Q8, ld8, nq, BN, 128)) return DG_ERR_CUDA;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
+        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP, KST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
             cudaSuccess)
             return DG_ERR_CUDA;
         attr_set = true;
@@ -856,13 +876,13 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     const int64_t ntiles = (int64_t)ta.ntp * ta.ntq;
     if (ntiles > INT32_MAX) return DG_ERR_SHAPE;
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
-    lut_gemm_ts_kernel<BN, NEPI, NUNP><<<grid, Roles<NEPI, NUNP>::NT, C::ALLOC, st>>>(mp, mb, ta, rq ? *rq : dummy);
+    lut_gemm_ts_kernel<BN, NEPI, NUNP, KST><<<grid, Roles<NEPI, NUNP>::NT, C::ALLOC, st>>>(mp, mb, ta, rq ? *rq : dummy);
     return launch_status();
 }
 
 }  // namespace
 
-int64_t expand_ld(int64_t K) { return (K + KS - 1) / KS * KS; }
+int64_t expand_ld(int64_t K) { return (K + KA - 1) / KA * KA; }
 
 dg_status expand_operand(const uint8_t *packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],
                          int8_t *out, int64_t ld8, cudaStream_t st) {
@@ -879,20 +899,26 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
                       const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                       cudaStream_t st, const TsConv *cv) {
     if (np > ((int64_t)1 << 31) - 1 || nq > ((int64_t)1 << 31) - 1) return DG_ERR_SHAPE;
-    // short K (<= 2 stages): the epilogue dominates -> 8 epilogue warps
-    const bool short_k = K <= 2 * KS;
+    // short K (<= 256 codes): the epilogue dominates -> two epilogue groups (EG = 2).
+    // Stages of 256 codes (8 MMAs per hand-off) except where K <= 128 or BN = 256 (whose 128-code
+    // stages already carry 512 MMA cycles).
+    const bool short_k = K <= 2 * KA;
+    const bool k256 = K > KA && !getenv("DG_TS_K128");
     // 128x256 tiles halve the shared-memory bytes of B per MAC (measured: 8192^3 1666 -> 2323
     // TOPS); their single TMEM accumulator buffer cannot overlap the epilogue with the next tile,
-    // so they are used only when the K loop is long (>= 24 stages).
-    if (nq >= 256 && K >= 24 * KS && !getenv("DG_TS_NO_BN256"))
-        return launch_ts<256, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    // so they are used only when the K loop is long (>= 24 x 128 codes).
+    if (nq >= 256 && K >= 24 * KA && !getenv("DG_TS_NO_BN256"))
+        return launch_ts<256, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     if (nq > 64) {
-        if (short_k) return launch_ts<128, 8, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
-        return launch_ts<128, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (short_k && !k256) return launch_ts<128, 8, 4, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (short_k) return launch_ts<128, 8, 4, 256>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (!k256) return launch_ts<128, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        return launch_ts<128, 4, 8, 256>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     }
-    if (short_k && getenv("DG_TS_UNP4")) return launch_ts<64, 8, 4>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
-    if (short_k) return launch_ts<64, 8, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
-    return launch_ts<64, 4, 8>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    if (short_k && !k256) return launch_ts<64, 8, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    if (short_k) return launch_ts<64, 8, 8, 256>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    if (!k256) return launch_ts<64, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    return launch_ts<64, 4, 8, 256>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 }
 
 }  // namespace dg
