@@ -128,11 +128,14 @@ struct TsArgs {
     int64_t ldd;
     int32_t has_rq, fast_rq, dir;
     int32_t thr[3];
-    // implicit-GEMM convolution (P = im2col of an NHWC packed input, gathered per thread)
+    // implicit-GEMM convolution: P = im2col of an NHWC packed input; every unpack thread gathers
+    // its own row's taps with 16-byte cp.async copies IG_DEPTH stages ahead (group-private ring
+    // in the packed-slot region)
     int32_t implicit;
     const uint8_t *X;      // [B][H][W][Cb] packed codes, Cb = C/4 a power of two >= 16
     int32_t H, W, Cb_log2, kw_recip, kw, stride, pad, Ho, Wo, kb;
-    uint32_t pad_word;     // pad byte replicated x4
+    const uint8_t *padsrc; // 16 bytes of the pad code (out-of-image taps); padsrc + 16: zeros (beyond K)
+    FastDiv fd_wo, fd_ho;
     // 16-bit SIMD requant (host-verified, see f16_params): per column pair
     //   x = clamp(acc + negA, 0, W) (one VIADDMNMX.RELU), code = (x*m + c) >> 14 (one IMAD),
     // negA = bias - (thr0 - 1) per column (smem table), per row, or uniform.
@@ -154,19 +157,52 @@ DG_DEV void tile_coords(const TsArgs &ta, int t, int &tp, int &tq) {
     tp = (int)(grp * ta.group + (rem - q * (uint32_t)(last ? ta.last_rows : ta.group)));
 }
 
-// Implicit im2col: 16 bytes (64 codes) of row p at virtual-im2col byte `byte` (multiple of 16).
-// K order (r, s, c) with c fastest (dg_im2col); out-of-image taps read the pad code.
-DG_DEV uint4 implicit_chunk(const TsArgs &ta, const uint8_t *img, int32_t h0, int32_t w0, int32_t byte) {
-    if (byte >= ta.kb) return make_uint4(0, 0, 0, 0);   // beyond K: multiplied by 0 weights
-    const int32_t tap = byte >> ta.Cb_log2;
-    const int32_t off = byte & ((1 << ta.Cb_log2) - 1);
-    const int32_t rr = (tap * ta.kw_recip) >> 16;       // tap / kw (exact for kh*kw <= 64)
-    const int32_t ss = tap - rr * ta.kw;
-    const int32_t hi = h0 + rr, wi = w0 + ss;
-    if ((uint32_t)hi >= (uint32_t)ta.H || (uint32_t)wi >= (uint32_t)ta.W)
-        return make_uint4(ta.pad_word, ta.pad_word, ta.pad_word, ta.pad_word);
-    return __ldg(reinterpret_cast<const uint4 *>(img + (((int64_t)hi * ta.W + wi) << ta.Cb_log2) + off));
-}
+// Implicit im2col gather cursor of one unpack thread (row r of its tiles): walks the thread's
+// group's stages (every NUM_UGROUPS-th stage across tiles) and issues each stage's 16-byte chunks
+// (64 codes each) as cp.async copies into one slot of the group's ring.  K order (r, s, c) with c
+// fastest (dg_im2col); out-of-image taps copy the pad code, bytes beyond K copy zeros.
+struct GatherCursor {
+    int t, s;                 // tile and stage of the next fetch
+    const uint8_t *img;
+    int32_t h0, w0;
+    DG_DEV void pixel(const TsArgs &ta, int r) {
+        int tp, tq;
+        tile_coords(ta, t, tp, tq);
+        const int64_t p = (int64_t)tp * BM + r;
+        const uint32_t pp = (uint32_t)(p < ta.np ? p : ta.np - 1);
+        const uint32_t tt = fdiv(pp, ta.fd_wo), b = fdiv(tt, ta.fd_ho);
+        img = ta.X + (((int64_t)b * ta.H * ta.W) << ta.Cb_log2);
+        h0 = (int32_t)(tt - b * (uint32_t)ta.Ho) * ta.stride - ta.pad;
+        w0 = (int32_t)(pp - tt * (uint32_t)ta.Wo) * ta.stride - ta.pad;
+    }
+    DG_DEV void advance(const TsArgs &ta, int by, int r, int ntiles) {
+        s += by;
+        bool moved = false;
+        while (s >= ta.nstages) { s -= ta.nstages; t += gridDim.x; moved = true; }
+        if (moved && t < ntiles) pixel(ta, r);
+    }
+    template <int NCH>
+    DG_DEV void issue(const TsArgs &ta, uint32_t dst_row, int r, int ntiles, int bytes_per_stage) {
+        if (t < ntiles) {
+#pragma unroll
+            for (int c = 0; c < NCH; ++c) {
+                const int32_t byte = s * bytes_per_stage + 16 * c;
+                const int32_t tap = byte >> ta.Cb_log2;
+                const int32_t off = byte & ((1 << ta.Cb_log2) - 1);
+                const int32_t rr = (tap * ta.kw_recip) >> 16;   // tap / kw (exact for kh*kw <= 64)
+                const int32_t ss = tap - rr * ta.kw;
+                const int32_t hi = h0 + rr, wi = w0 + ss;
+                const uint8_t *src = byte >= ta.kb ? ta.padsrc + 16
+                                     : ((uint32_t)hi < (uint32_t)ta.H && (uint32_t)wi < (uint32_t)ta.W)
+                                           ? img + ((((int64_t)hi * ta.W + wi) << ta.Cb_log2) + off)
+                                           : ta.padsrc;
+                // 64-byte row pitch, 16-byte unit c at c ^ ((r >> 1) & 3): conflict-free LDS.128
+                ptx::cp_async16(dst_row + ((c ^ ((r >> 1) & 3)) << 4), src);
+            }
+        }
+        ptx::cp_async_commit();
+    }
+};
 
 DG_DEV void store_codes32_ts(uint8_t *dp, uint32_t o0, uint32_t o1, int nbytes) {
 #pragma unroll
@@ -429,23 +465,20 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const uint32_t trow_a = tmem + C::TMEM_A0 + ((uint32_t)(quarter * 32) << 16);
         const uint32_t msk = ta.bulk ? 0u : 7u;
         uint32_t g = 0, pslot_i = 0, pphase = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            // implicit conv: this thread's output pixel of the tile
-            const uint8_t *img = ta.X;
-            int32_t h0 = 0, w0 = 0;
-            if (ta.implicit) {
-                int tp, tq;
-                tile_coords(ta, t, tp, tq);
-                const int64_t p = (int64_t)tp * BM + r;
-                const int64_t pp = p < ta.np ? p : ta.np - 1;
-                const int32_t wo = (int32_t)(pp % ta.Wo);
-                const int64_t tt = pp / ta.Wo;
-                const int32_t ho = (int32_t)(tt % ta.Ho);
-                const int64_t b = tt / ta.Ho;
-                img = ta.X + ((b * ta.H * ta.W) << ta.Cb_log2);
-                h0 = ho * ta.stride - ta.pad;
-                w0 = wo * ta.stride - ta.pad;
+        // implicit conv: group-private ring of IG_DEPTH stages (64 bytes per row each)
+        constexpr int IG_DEPTH = C::P_REGION / (NUM_UGROUPS * BM * 64);
+        const uint32_t ring = sbase + C::OFF_P + (uint32_t)(grp * IG_DEPTH * BM * 64) + (uint32_t)(r * 64);
+        GatherCursor gc{blockIdx.x, grp, ta.X, 0, 0};
+        uint32_t consumed = 0;
+        if (ta.implicit) {
+            gc.advance(ta, 0, r, ntiles);
+            if (gc.t < ntiles) gc.pixel(ta, r);
+            for (int i = 0; i < IG_DEPTH; ++i) {
+                gc.issue<2 * C::HALVES>(ta, ring + (uint32_t)(i * BM * 64), r, ntiles, KST / 4);
+                gc.advance(ta, NUM_UGROUPS, r, ntiles);
             }
+        }
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             int sub = 0;
             for (int s = 0; s < ta.nstages; ++s, ++g) {
                 const int slot = (int)pslot_i;
@@ -465,9 +498,11 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 if (lane == 0 && quarter == 0) TS_EV(0, g);
                 uint4 v[2 * C::HALVES];
                 if (ta.implicit) {
+                    ptx::cp_async_wait<IG_DEPTH - 1>();   // this stage's copies (the oldest group) landed
+                    const uint32_t row = ring + (uint32_t)((consumed % IG_DEPTH) * BM * 64);
 #pragma unroll
                     for (int c = 0; c < 2 * C::HALVES; ++c)
-                        v[c] = c < nchunk ? implicit_chunk(ta, img, h0, w0, s * (KST / 4) + 16 * c) : make_uint4(0, 0, 0, 0);
+                        v[c] = c < nchunk ? ptx::lds128(row + ((c ^ ((r >> 1) & 3)) << 4)) : make_uint4(0, 0, 0, 0);
                 } else {
                     ptx::mbar_wait(full_p(slot), ph);
                     // TMA slots carry the 128-byte swizzle: the 16-byte unit (bits 4-6) of the
@@ -483,6 +518,25 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     if (lane == 0)   // this warp's share of the slot is consumed (+ the slot's unused stages)
                         ptx::mbar_arrive_cnt(empty_p(slot), 1u + (s == ta.nstages - 1 ? (uint32_t)(nsub - 1 - sub_) : 0u));
                 }
+                // unpack the whole stage into registers before waiting for the A buffer, so that the
+                // wait overlaps the ALU work (a[32 h + j]: 32-column half h)
+                uint32_t a[32 * C::HALVES];
+#pragma unroll
+                for (int c = 0; c < 2 * C::HALVES; ++c) {
+                    if (c >= nchunk) break;
+                    const uint32_t w[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        const uint4 o = unpack16_levels(w[i], ta.lp);
+                        a[16 * c + 4 * i] = o.x; a[16 * c + 4 * i + 1] = o.y; a[16 * c + 4 * i + 2] = o.z;
+                        a[16 * c + 4 * i + 3] = o.w;
+                    }
+                }
+                if (ta.implicit) {   // the ring slot's data is consumed (values in registers): refill it
+                    gc.issue<2 * C::HALVES>(ta, ring + (uint32_t)((consumed % IG_DEPTH) * BM * 64), r, ntiles, KST / 4);
+                    gc.advance(ta, NUM_UGROUPS, r, ntiles);
+                    ++consumed;
+                }
                 if (lane == 0 && quarter == 0) TS_EV(1, g);
                 ptx::mbar_wait(empty_a(sa), ((g / SA) & 1u) ^ 1u);   // MMA(g - SA) completed
                 if (lane == 0 && quarter == 0) TS_EV(11, g);
@@ -490,25 +544,15 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 #pragma unroll
                 for (int h = 0; h < C::HALVES; ++h) {
                     if (2 * h >= nchunk) break;
-                    uint32_t a[32];   // [16, 32) only written (and stored) when the second chunk is read
+                    uint32_t ah[32];
 #pragma unroll
-                    for (int c = 0; c < 2; ++c) {
-                        if (c == 1 && 2 * h + 1 >= nchunk) break;
-                        const uint4 vv = v[2 * h + c];
-                        const uint32_t w[4] = {vv.x, vv.y, vv.z, vv.w};
-#pragma unroll
-                        for (int i = 0; i < 4; ++i) {
-                            const uint4 o = unpack16_levels(w[i], ta.lp);
-                            a[16 * c + 4 * i] = o.x; a[16 * c + 4 * i + 1] = o.y; a[16 * c + 4 * i + 2] = o.z;
-                            a[16 * c + 4 * i + 3] = o.w;
-                        }
-                    }
+                    for (int j = 0; j < 32; ++j) ah[j] = a[32 * h + j];
 #ifndef DG_EXP_NOUNPACK
                     const uint32_t ta_col = trow_a + sa * C::ACOLS + h * 32;
-                    if (2 * h + 1 < nchunk) ptx::tmem_st_32x32b_x32(ta_col, a);
-                    else ptx::tmem_st_32x32b_x16(ta_col, a);   // a half part: only its 16 columns are read
+                    if (2 * h + 1 < nchunk) ptx::tmem_st_32x32b_x32(ta_col, ah);
+                    else ptx::tmem_st_32x32b_x16(ta_col, ah);   // a half part: only its 16 columns are read
 #else
-                    if (a[0] == 0x12345u && a[3] == 0x777u) f16tab[1] = a[2];
+                    if (ah[0] == 0x12345u && ah[3] == 0x777u) f16tab[1] = ah[2];
 #endif
                 }
                 ptx::tmem_st_wait();
@@ -706,6 +750,23 @@ __global__ void expand_operand_kernel(const uint8_t *__restrict__ packed, int64_
 }
 
 // ---------------------------------------------------------------- host
+// Device copies of 16 pad-code bytes per pad code, each followed by 16 zero bytes (the cp.async
+// sources of out-of-image and beyond-K taps of the implicit gather).
+__device__ __align__(16) uint8_t g_pad_src[4][32];
+
+const uint8_t *pad_source(int pad_code) {
+    static const uint8_t *base = nullptr;
+    if (!base) {
+        uint8_t h[4][32] = {};
+        for (int c = 0; c < 4; ++c)
+            for (int i = 0; i < 16; ++i) h[c][i] = (uint8_t)(c | (c << 2) | (c << 4) | (c << 6));
+        if (cudaMemcpyToSymbol(g_pad_src, h, sizeof(h)) != cudaSuccess) return nullptr;
+        void *p = nullptr;
+        if (cudaGetSymbolAddress(&p, g_pad_src) != cudaSuccess) return nullptr;
+        base = reinterpret_cast<const uint8_t *>(p);
+    }
+    return base + 32 * (pad_code & 3);
+}
 typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
                                   const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
                                   CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -859,7 +920,11 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         ta.Ho = cv->Ho;
         ta.Wo = cv->Wo;
         ta.kb = cv->kh * cv->kw * cv->Cb;
-        ta.pad_word = 0x01010101u * (uint32_t)(cv->pad_code | (cv->pad_code << 2) | (cv->pad_code << 4) | (cv->pad_code << 6));
+        ta.padsrc = pad_source(cv->pad_code);
+        if (!ta.padsrc) return DG_ERR_CUDA;
+        ta.fd_wo = make_fastdiv((uint32_t)cv->Wo);
+        ta.fd_ho = make_fastdiv((uint32_t)cv->Ho);
+        if (np >= ((int64_t)1 << 31)) return DG_ERR_SHAPE;
     }
     CUtensorMap mp, mb;
     memset(&mp, 0, sizeof(mp));

@@ -76,6 +76,15 @@ DG_DEV void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t ba
                  : "memory");
 }
 
+// 16-byte global -> shared copy through L1 (cp.async.ca, LDGSTS), tracked per thread in commit
+// groups (cp_async_commit / cp_async_wait<N>: all but the N most recent groups have landed)
+DG_DEV void cp_async16(uint32_t dst, const void *src) {
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(dst), "l"(reinterpret_cast<uint64_t>(src)) : "memory");
+}
+DG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+DG_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // ---------------------------------------------------------------- named barriers
 DG_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");

@@ -90,6 +90,8 @@ int main() {
     run<0, 16>("ld 32x32b.x32");
     run<1, 8>("ld 32x32b.x16");
     run<2, 8>("ld 32x32b.x16.pack::16b");
-    run<3, 8>("st 32x32b.x32");
+    run<3, 4>("st 32x32b.x32 + wait");
+    run<3, 8>("st 32x32b.x32 + wait");
+    run<3, 16>("st 32x32b.x32 + wait");
     return 0;
 }

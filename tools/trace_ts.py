@@ -11,8 +11,13 @@ os.environ["DG_LIB_PATH"] = os.path.join(ROOT, "paper_2304_09049_b200", os.envir
 import numpy as np
 import torch
 from paper_2304_09049_b200 import dg
-M, N, K = map(int, (sys.argv[1] if len(sys.argv) > 1 else "802816x64x64").split("x"))
+CONV = sys.argv[1].startswith("conv") if len(sys.argv) > 1 else False   # conv<layer>: ResNet-50 layer via netrun
+M, N, K = (1, 1, 1) if CONV else map(int, (sys.argv[1] if len(sys.argv) > 1 else "802816x64x64").split("x"))
 lut = dg.build_lut([0, 1, 2, 3], [-2, -1, 0, 1], 8)
+if CONV:
+    from paper_2304_09049_b200 import netrun
+    runner = netrun.NetRunner(3, range(256), "cuda", layers=[int(sys.argv[1][4:])])
+    M, N, K = runner.plans[0].rows, runner.plans[0].layer.cout, runner.plans[0].K
 ld = dg.packed_ld(K)
 w = torch.randint(0, 256, (M, ld), dtype=torch.uint8, device="cuda")
 at = torch.randint(0, 256, (N, ld), dtype=torch.uint8, device="cuda")
@@ -29,7 +34,12 @@ buf = (ctypes.c_longlong * (16 * TLN))()
 for it in range(2):
     L.dg_debug_ts_timeline(buf, 1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record(); dg.lut_gemm_prepared(w, at8, M, N, K, lut, rq=rq, out=out); e1.record(); torch.cuda.synchronize()
+    e0.record()
+    if CONV:
+        runner.step()
+    else:
+        dg.lut_gemm_prepared(w, at8, M, N, K, lut, rq=rq, out=out)
+    e1.record(); torch.cuda.synchronize()
 L.dg_debug_ts_timeline(buf, 0)
 a = np.frombuffer(buf, dtype=np.int64).reshape(16, TLN).astype(np.int64)
 print(f"{M}x{N}x{K}: {e0.elapsed_time(e1):.3f} ms")
