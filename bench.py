@@ -209,12 +209,21 @@ def run_conv(args, ws, rank, local):
             tr = t["bytes_per_launch"] if t else None
     # algorithmic bytes of a GEMM launch: packed input + packed weights + packed output
     alg_bytes = (runner.input_bytes() + runner.weight_bytes() + runner.output_bytes()) / nl
+    # per-layer roofline t_roof = max(ops / int8 peak, algorithmic bytes / HBM): the fraction of it
+    # the measured GEMM times reach (HBM-bound 1x1 layers count against bandwidth)
+    t_roof = 0.0
+    for p_ in runner.plans:
+        lb = p_.x.numel() + p_.w.numel() + p_.out.numel()
+        t_roof += max(p_.ops / (pk["i8_burst"] * 1e12), lb / (pk["hbm_gbs"] * 1e9))
+    frac_layer = t_roof / (gemm_total_ms * 1e-3)
     roof = {"bound": "tensor", "kernel": "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)",
             "achieved": round(achieved, 1), "peak": round(pk["i8_burst"], 1), "unit": "TOPS",
             "frac": round(achieved / pk["i8_burst"], 4),
             "frac_vs_sustained_peak": round(achieved / pk["i8_sustained"], 4),
             "peak_src": pk["src"] + ": int8 = 2 x bf16 burst (nominal 4.5/2.25); conservative vs the sustained figure",
             "gemm_share_of_step": round(gemm_total_ms / ms, 3),
+            "frac_vs_layer_roofline": round(frac_layer, 4),
+            "layer_roofline_ms": round(t_roof * 1e3, 4),
             "traffic": tr, "alg_bytes_per_launch": round(alg_bytes),
             "traffic_src": "profiles/traffic.json (ncu dram__bytes_read+write, mean per GEMM launch)"}
 

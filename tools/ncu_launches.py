@@ -16,7 +16,7 @@ for r in rows[hdr_i + 1:]:
     import re
     m = re.findall(r"([A-Za-z_]\w*)(?:<[^()]*>)?\(", d["Kernel Name"])
     name = m[0] if m else d["Kernel Name"][:40]
-    if ONLY_OURS and not (d["Kernel Name"].startswith("void dg::") or "dg::" in d["Kernel Name"][:30]):
+    if ONLY_OURS and not ("dg::" in d["Kernel Name"][:40] or "unnamed>::" in d["Kernel Name"][:30]):
         continue
     try:
         v = float(d["Metric Value"].replace(",", ""))
