@@ -62,7 +62,11 @@ constexpr int EPI_BAR = 2;       // epilogue warps only (requant table build)
 // KST (template): codes per pipeline stage, 128 or 256.  Every stage costs a fixed number of
 // mbarrier / named-barrier hops (~150 cycles each, tools/sync_bench.cu) in the unpack, waiter and
 // MMA roles, so long-K tiles use 256-code stages (8 MMAs of K = 32 per hand-off).
-template <int BN, int EG, int KST>
+// WIN (template): direct 3x3 / stride-1 convolution.  The A operand is an unpacked window of
+// padded input pixels in shared memory (no-swizzle K-major layout) and every tap's MMA reads it
+// through a row-shifted descriptor, so each input pixel is unpacked once per tile instead of
+// once per tap (im2col row).
+template <int BN, int EG, int KST, bool WIN = false>
 struct TsCfg {
     static constexpr int KSTEPS = KST / 32;                 // MMAs (K = 32) per stage
     static constexpr int ACOLS = KST / 4;                   // TMEM columns of one A stage
@@ -74,11 +78,11 @@ struct TsCfg {
     static constexpr int SA = (512 - NACC * BN) / ACOLS > 8 ? 8 : (512 - NACC * BN) / ACOLS;   // A stages in TMEM
     static constexpr int B_ATOM = BN * KA;                  // bytes of one 128-code B atom
     static constexpr int B_BYTES = BN * KST;
-    static constexpr int SB_RAW = (BN == 64 ? 98304 : 131072) / B_BYTES;
+    static constexpr int SB_RAW = (BN == 64 || WIN ? 98304 : 131072) / B_BYTES;
     static constexpr int SB = SB_RAW > 8 ? 8 : SB_RAW;      // B (int8) smem stages
     static constexpr int TMEM_A0 = NACC * BN;               // first A column
     static constexpr int TMEM_COLS = 512;
-    static constexpr int P_REGION = 4 * BM * PKS_MAX;      // packed P slots: ta.sp x (BM x ta.pks) bytes
+    static constexpr int P_REGION = WIN ? 106496 : 4 * BM * PKS_MAX;   // packed P slots / WIN: packed ring + windows
     static constexpr int OFF_B = 0;                          // 1024-aligned (SW128)
     static constexpr int OFF_P = OFF_B + SB * B_BYTES;
     static constexpr int OFF_BAR = OFF_P + P_REGION;
@@ -87,6 +91,7 @@ struct TsCfg {
     static constexpr int OFF_TAB = (OFF_TMEM + 16 + 15) / 16 * 16;   // 16-bit requant offsets, one u32 per column pair
     static constexpr int ALLOC = OFF_TAB + TAB_PAIRS * 4 + 1024;
     static_assert(TMEM_A0 + SA * ACOLS <= TMEM_COLS && SA >= 2, "TMEM budget");
+    static_assert(ALLOC <= 232448, "shared memory budget");
 };
 
 #ifdef DG_TRACE
@@ -136,6 +141,12 @@ struct TsArgs {
     int32_t H, W, Cb_log2, kw_recip, kw, stride, pad, Ho, Wo, kb;
     const uint8_t *padsrc; // 16 bytes of the pad code (out-of-image taps); padsrc + 16: zeros (beyond K)
     FastDiv fd_wo, fd_ho;
+    // WIN (direct 3x3 conv): tiles run over the padded pixel space q = (b*Hp + hp)*Wp + wp
+    // (Hp = H+2, Wp = W+2); window row i of a tile = padded pixel q0 - Wp - 1 + i
+    int32_t win, Wp, WR, lbo, wslot, wbytes, nwin, clog2;   // WR window rows, lbo = WR*16
+    int64_t nqv;           // B*Hp*Wp
+    FastDiv fd_hpwp, fd_wp;
+    uint16_t koff[72];     // A descriptor start offset (16-byte units) of k-step j: chunk and tap shift
     // 16-bit SIMD requant (host-verified, see f16_params): per column pair
     //   x = clamp(acc + negA, 0, W) (one VIADDMNMX.RELU), code = (x*m + c) >> 14 (one IMAD),
     // negA = bias - (thr0 - 1) per column (smem table), per row, or uniform.
@@ -268,11 +279,11 @@ __device__ __noinline__ void ts_epilogue_general(const TsArgs &ta, const Requant
     store_codes32_ts(dp, o0, o1, (int)((ta.nq - qc + 3) / 4));
 }
 
-template <int BN, int NEPI, int NUNP, int KST>
+template <int BN, int NEPI, int NUNP, int KST, bool WIN>
 __global__ void __launch_bounds__(Roles<NEPI, NUNP>::NT, 1)
 lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
-    using C = TsCfg<BN, NEPI / 4, KST>;
+    using C = TsCfg<BN, NEPI / 4, KST, WIN>;
     using R = Roles<NEPI, NUNP>;
     constexpr int SB = C::SB, SA = C::SA, NACC = C::NACC, SP = SP_MAX;
     const int nsp = ta.sp;
@@ -314,8 +325,8 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 ptx::mbar_init(full_b(s), 1);
                 ptx::mbar_init(empty_b(s), 1);
             }
-            for (int s = 0; s < SA; ++s) {
-                ptx::mbar_init(full_a(s), 4);
+            for (int s = 0; s < SA; ++s) {   // WIN: window buffers, filled by all unpack warps
+                ptx::mbar_init(full_a(s), WIN ? NUNP : 4);
                 ptx::mbar_init(empty_a(s), 1);
             }
             for (int a = 0; a < NACC; ++a) {
@@ -361,7 +372,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             const int64_t p0 = (int64_t)tp * BM, q0 = (int64_t)tq * BN;
             int sub = 0, ps = 0;
             for (int s = 0; s < ta.nstages; ++s, ++gb) {
-                if (sub == 0 && !ta.implicit) {   // next packed P slot (up to 512 codes of every row)
+                if (sub == 0 && !ta.implicit && !WIN) {   // next packed P slot (up to 512 codes of every row)
                     const int slot = (int)pslot_i;
                     if (lane == 0) TS_EV(13, gb);
                     ptx::mbar_wait(empty_p(slot), pphase ^ 1u);
@@ -404,10 +415,12 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             ptx::mbar_wait(acc_empty(tl % NACC), ((tl / NACC) & 1u) ^ 1u);
             int tp, tq;
             tile_coords(ta, t, tp, tq);
+            if (WIN) ptx::mbar_wait(full_a(tl % ta.nwin), (tl / ta.nwin) & 1u);   // the tile's window
+            if (WIN && lane == 0) TS_EV(13, tl);
             for (int s = 0; s < ta.nstages; ++s, ++g) {
                 const int sa = g % SA;
                 if (lane == 0 && s == 0) TS_EV(3, tl);
-                ptx::mbar_wait(full_a(sa), (g / SA) & 1u);
+                if (!WIN) ptx::mbar_wait(full_a(sa), (g / SA) & 1u);
                 if (lane == 0) TS_EV(4, g);
                 if (ta.bres) ptx::mbar_wait(full_b(tq * ta.nstages + s), 0u);
                 else ptx::mbar_wait(full_b(g % SB), (g / SB) & 1u);
@@ -431,7 +444,38 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 const int sb = ta.bres ? tq * ta.nstages + s : (int)(g % SB);
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
                 ptx::tc_fence_after();
-                if (lane == 0) {
+                if (lane == 0 && WIN) {
+                    TS_EV(14, g);
+                    // k = tap*C + c: A = the window shifted by r*Wp + s rows (tap = 3r + s), K chunk c/16;
+                    // the per-k-step start offsets come precomputed from the host (ta.koff)
+                    const uint32_t wbase = sbase + C::OFF_P + (uint32_t)(2 * ta.wslot + (int)(tl % ta.nwin) * ta.wbytes);
+                    const uint64_t ad = ptx::desc_k_none(wbase, (uint32_t)ta.lbo);
+                    const uint64_t bd = bdesc0 + (uint64_t)((sb * C::B_BYTES) >> 4);
+                    const int j0 = s * C::KSTEPS;
+                    // all offsets into registers first: a parameter load between two tcgen05.mma
+                    // (asm with a memory clobber) serialises the issue (~150 cycles per MMA measured)
+                    uint32_t ko[C::KSTEPS];
+#pragma unroll
+                    for (int k = 0; k < C::KSTEPS; ++k) ko[k] = ta.koff[j0 + k < 72 ? j0 + k : 71];
+                    if (s < ta.nstages - 1 || ta.last_ksteps == C::KSTEPS) {
+#pragma unroll
+                        for (int k = 0; k < C::KSTEPS; ++k)
+                            ptx::mma_i8_ss(dt, ad + ko[k], bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
+                                           idesc, (s > 0 || k > 0) ? 1u : 0u);
+                    } else {
+#pragma unroll
+                        for (int k = 0; k < C::KSTEPS; ++k)
+                            if (k < ta.last_ksteps)
+                                ptx::mma_i8_ss(dt, ad + ko[k], bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
+                                               idesc, (s > 0 || k > 0) ? 1u : 0u);
+                    }
+                    if (!ta.bres) ptx::mma_commit(empty_b(sb));
+                    if (s == ta.nstages - 1) {
+                        ptx::mma_commit(empty_a(tl % ta.nwin));   // the window is free again
+                        ptx::mma_commit(acc_full(acc));
+                    }
+                    TS_EV(15, g);
+                } else if (lane == 0) {
                     const uint32_t at = tmem + C::TMEM_A0 + sa * C::ACOLS;
                     const uint64_t bd = bdesc0 + (uint64_t)((sb * C::B_BYTES) >> 4);
                     // k-step k: A columns 8k, B atom k/4 (+B_ATOM bytes), 32 bytes (+2) per k-step inside
@@ -454,6 +498,73 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
                 __syncwarp();
             }
+        }
+    } else if (warp >= UNPACK_WARP0 && WIN) {
+        // ---------------- WIN: fill each tile's window of padded input pixels.  Thread = window row:
+        // its packed pixel (C/4 bytes) arrives by cp.async two tiles ahead (ring of 2 slots), is
+        // unpacked to int8 levels and stored as C/16 16-byte K chunks (chunk j at j*lbo + row*16).
+        constexpr int WRING = 2;
+        const int tid = (warp - UNPACK_WARP0) * 32 + lane;
+        const bool has_row = tid < ta.WR;
+        const int cb = 1 << (ta.clog2 - 2), nch = cb >> 4;   // packed bytes per pixel, 16-byte chunks
+        const uint32_t ring = sbase + C::OFF_P, wins = ring + WRING * ta.wslot;
+        auto fetch = [&](int t, int slot) {
+            if (has_row && t < ntiles) {
+                int tp, tq;
+                tile_coords(ta, t, tp, tq);
+                const int64_t q = (int64_t)tp * BM - (ta.Wp + 1) + tid;   // padded pixel of this row
+                const uint8_t *src = nullptr;
+                if (q >= 0 && q < ta.nqv) {
+                    const uint32_t b = fdiv((uint32_t)q, ta.fd_hpwp);
+                    const uint32_t rem = (uint32_t)q - b * (uint32_t)((ta.H + 2) * ta.Wp);
+                    const uint32_t hp = fdiv(rem, ta.fd_wp), wp = rem - hp * (uint32_t)ta.Wp;
+                    if (hp >= 1 && hp <= (uint32_t)ta.H && wp >= 1 && wp <= (uint32_t)ta.W)
+                        src = ta.X + ((((int64_t)b * ta.H + hp - 1) * ta.W + wp - 1) << (ta.clog2 - 2));
+                }
+                const uint32_t dst = ring + (uint32_t)(slot * ta.wslot + tid * cb);
+                for (int c = 0; c < nch; ++c) ptx::cp_async16(dst + 16 * c, src ? src + 16 * c : ta.padsrc);
+            }
+            ptx::cp_async_commit();
+        };
+        fetch(blockIdx.x, 0);
+        fetch(blockIdx.x + gridDim.x, 1);
+        uint32_t tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const int slot = (int)(tl & 1u), wb = (int)(tl % ta.nwin);
+            if (tid == 0) TS_EV(0, tl);
+            ptx::cp_async_wait<WRING - 1>();
+            if (tid == 0) TS_EV(12, tl);
+            uint32_t a[64];
+            const uint32_t src = ring + (uint32_t)(slot * ta.wslot + tid * cb);
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (c >= nch) break;
+                const uint4 v = has_row ? ptx::lds128(src + 16 * c) : make_uint4(0, 0, 0, 0);
+                const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                for (int i = 0; i < 4; ++i) {
+                    const uint4 o = unpack16_levels(w[i], ta.lp);
+                    a[16 * c + 4 * i] = o.x; a[16 * c + 4 * i + 1] = o.y; a[16 * c + 4 * i + 2] = o.z; a[16 * c + 4 * i + 3] = o.w;
+                }
+            }
+            fetch(t + 2 * (int)gridDim.x, slot);   // the slot's bytes are consumed: refill it
+            if (tid == 0) TS_EV(1, tl);
+            ptx::mbar_wait(empty_a(wb), ((tl / ta.nwin) & 1u) ^ 1u);   // the window's previous tile finished
+            if (tid == 0) TS_EV(11, tl);
+            if (has_row) {
+                const uint32_t wdst = wins + (uint32_t)(wb * ta.wbytes + tid * 16);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    if (j >= 4 * nch) break;
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(wdst + (uint32_t)(j * ta.lbo)),
+                                 "r"(a[4 * j]), "r"(a[4 * j + 1]), "r"(a[4 * j + 2]), "r"(a[4 * j + 3])
+                                 : "memory");
+                }
+            }
+            ptx::fence_proxy_async_smem();   // generic-proxy stores -> visible to the tensor core
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(full_a(wb));
+            if (tid == 0) TS_EV(2, tl);
         }
     } else if (warp >= UNPACK_WARP0) {
         // ---------------- unpackers: thread = row; packed smem -> int8 levels -> TMEM (A operand).
@@ -588,7 +699,18 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             const uint32_t acc = tl % NACC;
             int tp, tq;
             tile_coords(ta, t, tp, tq);
-            const int64_t p = (int64_t)tp * BM + quarter * 32 + lane;
+            int64_t p = (int64_t)tp * BM + quarter * 32 + lane;
+            if (WIN) {   // padded pixel -> output pixel row, or np (not stored) for a padding position
+                const int64_t q = p;
+                p = ta.np;
+                if (q < ta.nqv) {
+                    const uint32_t b = fdiv((uint32_t)q, ta.fd_hpwp);
+                    const uint32_t rem = (uint32_t)q - b * (uint32_t)((ta.H + 2) * ta.Wp);
+                    const uint32_t hp = fdiv(rem, ta.fd_wp), wp = rem - hp * (uint32_t)ta.Wp;
+                    if (hp >= 1 && hp <= (uint32_t)ta.H && wp >= 1 && wp <= (uint32_t)ta.W)
+                        p = ((int64_t)b * ta.H + hp - 1) * ta.W + wp - 1;
+                }
+            }
             const int64_t q0 = (int64_t)tq * BN + half * HALF;
             if (lane == 0 && quarter == 0) TS_EV(8, tl);
             ptx::mbar_wait(acc_full(acc), (tl / NACC) & 1u);
@@ -839,11 +961,11 @@ bool f16_params(int64_t t0, int64_t t1, int64_t t2, uint32_t &m_out, uint32_t &c
     return false;
 }
 
-template <int BN, int NEPI, int NUNP, int KST>
+template <int BN, int NEPI, int NUNP, int KST, bool WIN = false>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                     cudaStream_t st, const TsConv *cv) {
-    using C = TsCfg<BN, NEPI / 4, KST>;
+    using C = TsCfg<BN, NEPI / 4, KST, WIN>;
     int64_t acc_bound = 0;   // K * max |pl[a] * ql[b]|
     for (int a = 0; a < 4; ++a)
         for (int b = 0; b < 4; ++b) {
@@ -858,6 +980,32 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     const int64_t kmma = (K + 31) / 32 * 32;
     ta.last_ksteps = (int32_t)((kmma - (int64_t)(ta.nstages - 1) * KST) / 32);
     ta.ntp = (int32_t)((np + BM - 1) / BM);
+    if (WIN) {   // direct 3x3 conv: tiles over the padded pixel space
+        const int64_t Wp = cv->W + 2, Hp = cv->H + 2, B = np / ((int64_t)cv->H * cv->W);
+        ta.win = 1;
+        ta.Wp = (int32_t)Wp;
+        ta.nqv = B * Hp * Wp;
+        if (ta.nqv >= ((int64_t)1 << 31)) return DG_ERR_SHAPE;
+        ta.ntp = (int32_t)((ta.nqv + BM - 1) / BM);
+        ta.WR = (BM + 2 * (int32_t)Wp + 2 + 7) / 8 * 8;   // multiple of 8: LBO a multiple of 128 B
+        if (ta.WR > NUNP * 32) return DG_ERR_UNSUPPORTED;   // one window row per unpack thread
+        ta.lbo = ta.WR * 16;
+        int lg = 0;
+        while ((1 << lg) < 4 * cv->Cb) ++lg;
+        ta.clog2 = lg;
+        ta.wslot = (ta.WR * cv->Cb + 127) / 128 * 128;
+        ta.wbytes = (cv->Cb / 4) * ta.lbo;
+        ta.nwin = (2 * ta.wslot + 3 * ta.wbytes <= C::P_REGION && C::SA >= 3) ? 3 : 2;
+        if (2 * ta.wslot + ta.nwin * ta.wbytes > C::P_REGION || ta.nwin > C::SA) return DG_ERR_UNSUPPORTED;
+        ta.fd_hpwp = make_fastdiv((uint32_t)(Hp * Wp));
+        ta.fd_wp = make_fastdiv((uint32_t)Wp);
+        const int C = 4 * cv->Cb, nk = (int)(K / 32);
+        if (nk > 72) return DG_ERR_UNSUPPORTED;
+        for (int j = 0; j < nk; ++j) {
+            const int tap = (32 * j) / C, c0 = (32 * j) % C, r = tap / 3, s = tap % 3;
+            ta.koff[j] = (uint16_t)(((c0 / 16) * ta.lbo + (r * (int)Wp + s) * 16) >> 4);
+        }
+    }
     ta.ntq = (int32_t)((nq + BN - 1) / BN);
     ta.group = ta.ntq <= 4 ? 1 : (ta.ntp < 16 ? ta.ntp : 16);   // 1 = column block fastest
     ta.last_grp = (ta.ntp - 1) / ta.group;
@@ -906,7 +1054,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         }
     }
     if (cv) {
-        ta.implicit = 1;
+        ta.implicit = WIN ? 0 : 1;
         ta.X = cv->x;
         ta.H = cv->H;
         ta.W = cv->W;
@@ -932,7 +1080,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     if (!make_map_sw128(&mb, Q8, ld8, nq, BN, 128)) return DG_ERR_CUDA;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP, KST>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
+        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
             cudaSuccess)
             return DG_ERR_CUDA;
         attr_set = true;
@@ -941,7 +1089,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     const int64_t ntiles = (int64_t)ta.ntp * ta.ntq;
     if (ntiles > INT32_MAX) return DG_ERR_SHAPE;
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
-    lut_gemm_ts_kernel<BN, NEPI, NUNP, KST><<<grid, Roles<NEPI, NUNP>::NT, C::ALLOC, st>>>(mp, mb, ta, rq ? *rq : dummy);
+    lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN><<<grid, Roles<NEPI, NUNP>::NT, C::ALLOC, st>>>(mp, mb, ta, rq ? *rq : dummy);
     return launch_status();
 }
 
@@ -964,6 +1112,15 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
                       const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                       cudaStream_t st, const TsConv *cv) {
     if (np > ((int64_t)1 << 31) - 1 || nq > ((int64_t)1 << 31) - 1) return DG_ERR_SHAPE;
+    // direct 3x3 / stride 1 / pad 1 convs with C = 64, 128, 256: shifted-window kernel (DG_WIN=1; it
+    // unpacks each input pixel once per tile instead of once per tap, but measured no faster than
+    // the implicit gather on the ResNet-50 shapes)
+    if (cv && cv->kh == 3 && cv->kw == 3 && cv->stride == 1 && cv->pad == 1 && cv->Cb >= 16 && cv->Cb <= 64 &&
+        (cv->Cb & (cv->Cb - 1)) == 0 && getenv("DG_WIN")) {
+        const dg_status s = nq > 64 ? launch_ts<128, 4, 8, 256, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv)
+                                    : launch_ts<64, 4, 8, 256, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (s != DG_ERR_UNSUPPORTED) return s;
+    }
     // short K (<= 256 codes): the epilogue dominates -> two epilogue groups (EG = 2).
     // Stages of 256 codes (8 MMAs per hand-off) except where K <= 128 or BN = 256 (whose 128-code
     // stages already carry 512 MMA cycles).
@@ -972,7 +1129,9 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     // 128x256 tiles halve the shared-memory bytes of B per MAC (measured: 8192^3 1666 -> 2323
     // TOPS); their single TMEM accumulator buffer cannot overlap the epilogue with the next tile,
     // so they are used only when the K loop is long (>= 24 x 128 codes).
-    if (nq >= 256 && K >= 24 * KA && !getenv("DG_TS_NO_BN256"))
+    // 128x256 tiles for K >= 512 (measured: ResNet-50 stage-3 3x3 46 -> 35 us, downsamples -10%)
+    static const int64_t bn256_k = getenv("DG_BN256_K") ? atoll(getenv("DG_BN256_K")) : 4 * KA;
+    if (nq >= 256 && K >= bn256_k && !getenv("DG_TS_NO_BN256"))
         return launch_ts<256, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 
     if (nq > 64) {

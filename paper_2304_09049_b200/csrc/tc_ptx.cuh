@@ -208,6 +208,18 @@ DG_DEV uint64_t desc_k_sw128(uint32_t saddr) {
     return d;
 }
 
+// UMMA shared-memory descriptor, K-major, no swizzle: "core matrices" of 8 rows x 16 bytes; with
+// SBO = 128 B the rows of a 16-byte K chunk are contiguous 16-byte records (row i at +16 i), so a
+// view may start at ANY row (tools/shift_desc_test.cu); LBO = byte stride between K chunks.
+DG_DEV uint64_t desc_k_none(uint32_t saddr, uint32_t lbo) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)(128 >> 4) << 32;         // SBO: 8 rows x 16 B
+    d |= (uint64_t)1 << 46;                  // descriptor version (Blackwell); layout type 0 = none
+    return d;
+}
+
 // Instruction descriptor, kind::i8: s32 accumulate, signed int8 A and B, both K-major.
 __host__ __device__ constexpr uint32_t idesc_i8(int M, int N) {
     return (2u << 4)                          // c_format = S32

@@ -404,3 +404,38 @@ def test_tc_requant_epilogue_sweep(mult, zp, qmin, qmax, bias_kind, K):
     q = oracle.requantize(acc, mult, 20, zp, qmin, qmax, bias=bias, bias_axis=axis).view(np.int8)
     exp = (q.astype(np.int32) - qmin).astype(np.uint8)     # dg.h: code = q - qmin
     assert np.array_equal(oracle_codes_of(got, M, N), exp)
+
+
+WIN_CONVS = [  # B, H, W, C, Cout, pad_code: 3x3 / stride 1 / pad 1 shapes of the shifted-window path
+    (2, 9, 9, 64, 32, 0),
+    (3, 14, 14, 128, 64, 0),
+    (1, 7, 11, 256, 128, 2),      # non-square, non-zero pad code
+    (2, 56, 56, 64, 64, 0),       # ResNet-50 stage-1 width (window of 248 rows)
+]
+
+
+@pytest.mark.parametrize("B,H,W,C,Cout,pad_code", WIN_CONVS)
+def test_conv_window_path_vs_oracle(monkeypatch, B, H, W, C, Cout, pad_code):
+    """Direct 3x3 conv through the shifted-window kernel (DG_WIN=1: one unpacked window of padded
+    input pixels per tile, every tap an MMA on a row-shifted shared-memory descriptor) vs O-CONV,
+    int32 and fused requant."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    monkeypatch.setenv("DG_WIN", "1")
+    lut = dg.build_lut(WL, AL, 8)
+    g = np.random.default_rng(B + H + W + C + Cout + pad_code)
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, 3, 3, C), dtype=np.uint8)
+    exp = oracle.conv2d_direct(x, w, oracle.build_lut16(WL, AL), 1, 1, pad_code)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    w8 = dg.expand_operand(wp, 9 * Cp, WL)
+    p = dg.conv_params(B, H, W, Cp, Cout, 3, 3, 1, 1, pad_code, ldw=wp.shape[1])
+    ws = torch.empty(dg.conv_workspace_size(p), dtype=torch.uint8, device=DEV)
+    out = dg.lut_conv2d_prepared(xp, w8, lut, p, ws=ws)
+    assert np.array_equal(host(out).reshape(exp.shape), exp)
+    bias = g.integers(-50, 50, Cout).astype(np.int32)
+    rq = dg.Requant(mult=30000, shift=20, zp=1, bias=torch.from_numpy(bias).to(DEV), bias_axis=0)
+    outc = dg.lut_conv2d_prepared(xp, w8, lut, p, rq=rq, ws=ws)
+    expc = oracle.requantize(exp.reshape(-1, Cout), 30000, 20, 1, 0, 3, bias=bias, bias_axis=0)
+    assert np.array_equal(oracle_codes_of(outc, expc.shape[0], Cout), expc)

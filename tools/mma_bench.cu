@@ -40,6 +40,18 @@ __global__ void __launch_bounds__(256, 1) bench(int niter, unsigned long long *c
     __syncthreads();
     if (threadIdx.x == 0) ptx::mbar_arrive(ptx::smem_u32(&bar_done));   // phase 0 complete
     __syncthreads();
+    if (warp >= 4 && (MODE == 22 || MODE == 23)) {   // smem store / load traffic from other warps
+        uint32_t *buf = reinterpret_cast<uint32_t *>(smem + (128 + N) * 128);   // 16 KB after the operands
+        unsigned acc = 0;
+        int it = 0;
+        while (!done) {
+            const int o = ((it * 64 + (threadIdx.x - 128) * 4) & 4095);
+            if (MODE == 22) *reinterpret_cast<uint4 *>(buf + o) = make_uint4(it, it, it, it);
+            else { const uint4 v = *reinterpret_cast<const uint4 *>(buf + o); acc += v.x; }
+            ++it;
+        }
+        if (acc == 12345) cycles[3] = acc;
+    }
     if (warp >= 4 && MODE >= 1 && MODE <= 3) {   // interference warps, lane quarter = warp % 4
         const uint32_t taddr = tmem + 448 + ((uint32_t)((warp & 3) * 32) << 16);
         uint32_t r[32];
@@ -72,7 +84,7 @@ __global__ void __launch_bounds__(256, 1) bench(int niter, unsigned long long *c
             asm volatile("bar.sync 2, 64;" ::: "memory");
         }
     }
-    if (MODE >= 11 && warp == 0) {
+    if (MODE >= 11 && MODE <= 13 && warp == 0) {
         const uint32_t a = ptx::smem_u32(smem), b = a + 128 * 128;
         constexpr uint32_t idesc = ptx::idesc_i8(128, N);
         const long long c0 = clock64();
@@ -123,6 +135,10 @@ __global__ void __launch_bounds__(256, 1) bench(int niter, unsigned long long *c
             }
             if (TS)
                 ptx::mma_i8_ts(tmem, tmem + 256 + 8 * k, ptx::desc_k_sw128(b + 32 * k), idesc, i > 0);
+            else if (MODE == 20)   // A in the no-swizzle K-major layout (16-byte rows, LBO = 128 rows * 16 B)
+                ptx::mma_i8_ss(tmem, ptx::desc_k_none(a + (uint32_t)(k & 1) * 2 * 2048, 2048), ptx::desc_k_sw128(b + 32 * k), idesc, i > 0);
+            else if (MODE == 21 || MODE == 22 || MODE == 23)   // A no-swizzle, shifted by 57 rows (window view)
+                ptx::mma_i8_ss(tmem, ptx::desc_k_none(a + 57 * 16 + (uint32_t)(k & 1) * 2 * 2048, 2048), ptx::desc_k_sw128(b + 32 * k), idesc, i > 0);
             else
                 ptx::mma_i8_ss(tmem, ptx::desc_k_sw128(a + 32 * k), ptx::desc_k_sw128(b + 32 * k), idesc, i > 0);
             if ((MODE == 4 || MODE == 5 || MODE == 6) && k == 3) ptx::mma_commit(ptx::smem_u32(&bar2[(i >> 2) & 3]));
@@ -148,7 +164,7 @@ void run(int sms) {
     const int niter = 20000;
     unsigned long long *d;
     cudaMalloc(&d, 16 + 64 * 8 + 4096 * 16 + 1024);
-    const int smem = (128 + N) * 128 + 2048;
+    const int smem = (128 + N) * 128 + 16384;
     cudaFuncSetAttribute(bench<N, TS, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     bench<N, TS, MODE><<<sms, 256, smem>>>(100, d);
     cudaEvent_t e0, e1;
@@ -177,6 +193,12 @@ int main(int argc, char **argv) {
     run<256, true>(sms);
     run<128, false>(sms);
     run<256, false>(sms);
+    run<64, false, 20>(sms);
+    run<128, false, 20>(sms);
+    run<64, false, 21>(sms);
+    run<64, false>(sms);
+    run<64, false, 22>(sms);
+    run<64, false, 23>(sms);
     if (argc > 1) {   // pipeline-interaction modes (see MODE above)
         run<64, true, 1>(sms);
         run<64, true, 3>(sms);

@@ -50,6 +50,13 @@ names = {13: "P_loop", 14: "P_slot", 12: "P_tma", 0: "unp0", 1: "unp_rdy", 11: "
 print("stage " + " ".join(f"{v:>8s}" for v in names.values()))
 for g in list(range(0, 40)):
     print(f"{g:5d} " + " ".join(f"{a[e][g]:8d}" for e in names))
+if len(sys.argv) > 2 and sys.argv[2] == "--win":
+    print("stage: waiter_fullA w_fullB handoff mma_start mma_end")
+    for g in range(0, 30):
+        print(f"{g:4d} " + " ".join(f"{a[e][g]:8d}" for e in (4, 5, 6, 14, 15)))
+    print("tile unp0 cpa_ok unp_done emptyW fullW_arr waiter_fullW  w_start epi0 epi_accfull epi_done")
+    for t in range(0, 40):
+        print(f"{t:4d} " + " ".join(f"{a[e][t]:8d}" for e in (0, 12, 1, 11, 2, 13, 3, 8, 9, 10)))
 print("tile  w_start  epi0   epi_accfull  epi_done")
 for t in list(range(0, 16)) + list(range(38, 43)):
     print(f"{t:4d} {a[3][t]:8d} {a[8][t]:8d} {a[9][t]:8d} {a[10][t]:8d}")
