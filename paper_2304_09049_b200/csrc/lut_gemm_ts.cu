@@ -347,11 +347,16 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     __syncthreads();
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
+    // programmatic dependent launch: the next layer's CTAs may start (prologue) as ours exit; every
+    // role waits for the previous grid before touching activations / outputs (weights and the
+    // requant table are set-up data and are read before the wait)
+    if (threadIdx.x == 0) ptx::griddep_launch_dependents();
 
     if (warp == PRODUCER_WARP) {
         // ---------------- producer.  The whole warp runs the loop (a lone lane 0 with 31 lanes
         // parked at the final __syncthreads ran the loop several times slower); lane 0 issues.
         uint32_t gb = 0, pslot_i = 0, pphase = 0;
+        if (!ta.bres) ptx::griddep_wait();
         if (ta.bres) {   // every B tile once: slot tq * nstages + s
             for (int tq = 0; tq < ta.ntq; ++tq)
                 for (int s = 0; s < ta.nstages; ++s) {
@@ -365,6 +370,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     }
                 }
             __syncwarp();
+            ptx::griddep_wait();
         }
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             int tp, tq;
@@ -410,6 +416,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         }
     } else if (warp == WAITER_WARP) {
         // ---------------- waiter: acc_empty / full_a / full_b, then rendezvous with the MMA warp
+        ptx::griddep_wait();
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             ptx::mbar_wait(acc_empty(tl % NACC), ((tl / NACC) & 1u) ^ 1u);
@@ -503,6 +510,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         // ---------------- WIN: fill each tile's window of padded input pixels.  Thread = window row:
         // its packed pixel (C/4 bytes) arrives by cp.async two tiles ahead (ring of 2 slots), is
         // unpacked to int8 levels and stored as C/16 16-byte K chunks (chunk j at j*lbo + row*16).
+        ptx::griddep_wait();
         constexpr int WRING = 2;
         const int tid = (warp - UNPACK_WARP0) * 32 + lane;
         const bool has_row = tid < ta.WR;
@@ -569,6 +577,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     } else if (warp >= UNPACK_WARP0) {
         // ---------------- unpackers: thread = row; packed smem -> int8 levels -> TMEM (A operand).
         // Groups of 4 warps (one per TMEM lane quarter) take alternate stages.
+        ptx::griddep_wait();
         const int uw = warp - UNPACK_WARP0;
         const int grp = uw / 4;                 // stage group
         const int quarter = warp & 3;           // TMEM lane quarter this warp may access
@@ -691,6 +700,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             ptx::named_bar_sync(EPI_BAR, NEPI * 32);
         }
         const bool f16_ok = ta.f16 && *f16_flag == 0u;
+        ptx::griddep_wait();
         const int quarter = warp & 3, eg = (warp - EPI_WARP0) >> 2, half = 0;
         const bool col_bias = rq.bias && rq.bias_axis == 0;
         uint32_t tl = 0;
@@ -1089,7 +1099,19 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     const int64_t ntiles = (int64_t)ta.ntp * ta.ntq;
     if (ntiles > INT32_MAX) return DG_ERR_SHAPE;
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
-    lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN><<<grid, Roles<NEPI, NUNP>::NT, C::ALLOC, st>>>(mp, mb, ta, rq ? *rq : dummy);
+    const RequantArgs rqv = rq ? *rq : dummy;
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)grid);
+    lc.blockDim = dim3((unsigned)Roles<NEPI, NUNP>::NT);
+    lc.dynamicSmemBytes = C::ALLOC;
+    lc.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = getenv("DG_NO_PDL") ? 0 : 1;
+    lc.attrs = la;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN>, mp, mb, ta, rqv) != cudaSuccess)
+        return DG_ERR_CUDA;
     return launch_status();
 }
 
@@ -1131,7 +1153,8 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     // so they are used only when the K loop is long (>= 24 x 128 codes).
     // 128x256 tiles for K >= 512 (measured: ResNet-50 stage-3 3x3 46 -> 35 us, downsamples -10%)
     static const int64_t bn256_k = getenv("DG_BN256_K") ? atoll(getenv("DG_BN256_K")) : 4 * KA;
-    if (nq >= 256 && K >= bn256_k && !getenv("DG_TS_NO_BN256"))
+    const int64_t tiles256 = ((np + BM - 1) / BM) * ((nq + 255) / 256);
+    if (nq >= 256 && K >= bn256_k && (tiles256 >= num_sms() || K >= 24 * KA) && !getenv("DG_TS_NO_BN256"))
         return launch_ts<256, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 
     if (nq > 64) {

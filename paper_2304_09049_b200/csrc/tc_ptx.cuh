@@ -85,6 +85,12 @@ DG_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memor
 template <int N>
 DG_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
 
+// ---------------------------------------------------------------- programmatic dependent launch
+// wait: block until the preceding grid in the stream completed and its writes are visible;
+// launch_dependents: allow the next grid (launched with programmatic stream serialisation) to start
+DG_DEV void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+DG_DEV void griddep_launch_dependents() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---------------------------------------------------------------- named barriers
 DG_DEV void named_bar_sync(uint32_t id, uint32_t nthreads) {
     asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
