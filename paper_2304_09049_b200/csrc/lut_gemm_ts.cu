@@ -417,6 +417,10 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     } else if (warp == WAITER_WARP) {
         // ---------------- waiter: acc_empty / full_a / full_b, then rendezvous with the MMA warp
         ptx::griddep_wait();
+        // resident B: wait for all of it once (each mbarrier probe costs ~150 cycles even when the
+        // phase completed long ago, and the waiter's probes are on the critical path of short tiles)
+        if (ta.bres)
+            for (int j = 0; j < ta.ntq * ta.nstages; ++j) ptx::mbar_wait(full_b(j), 0u);
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             ptx::mbar_wait(acc_empty(tl % NACC), ((tl / NACC) & 1u) ^ 1u);
@@ -429,8 +433,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 if (lane == 0 && s == 0) TS_EV(3, tl);
                 if (!WIN) ptx::mbar_wait(full_a(sa), (g / SA) & 1u);
                 if (lane == 0) TS_EV(4, g);
-                if (ta.bres) ptx::mbar_wait(full_b(tq * ta.nstages + s), 0u);
-                else ptx::mbar_wait(full_b(g % SB), (g / SB) & 1u);
+                if (!ta.bres) ptx::mbar_wait(full_b(g % SB), (g / SB) & 1u);
                 if (lane == 0) TS_EV(5, g);
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
                 if (lane == 0) TS_EV(6, g);   // the MMA warp finished issuing stage g - 1
@@ -590,6 +593,62 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const uint32_t ring = sbase + C::OFF_P + (uint32_t)(grp * IG_DEPTH * BM * 64) + (uint32_t)(r * 64);
         GatherCursor gc{blockIdx.x, grp, ta.X, 0, 0};
         uint32_t consumed = 0;
+        if (KST == 128 && ta.nstages == 1 && !ta.implicit) {
+            // one-stage tiles (K <= 128): a group unpacks two of its tiles per round of mbarrier
+            // hand-offs (each hop ~150 cycles, tools/sync_bench.cu), halving the per-tile chain
+            const int nch = (ta.last_ksteps + 1) / 2;   // 16-byte chunks read (1 or 2)
+            for (uint32_t tl0 = grp; blockIdx.x + tl0 * gridDim.x < (uint32_t)ntiles; tl0 += 2 * NUM_UGROUPS) {
+                const uint32_t tl1 = tl0 + NUM_UGROUPS;
+                const bool has1 = blockIdx.x + tl1 * gridDim.x < (uint32_t)ntiles;
+                uint4 v[2][2];
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const uint32_t tl = b ? tl1 : tl0;
+                    if (b && !has1) break;
+                    const int slot = (int)(tl % (uint32_t)nsp);
+                    ptx::mbar_wait(full_p(slot), (tl / (uint32_t)nsp) & 1u);
+                    const uint32_t pbase = sbase + C::OFF_P + slot * pslot, lin = (uint32_t)(r * ta.pks);
+                    v[b][0] = ptx::lds128(pbase + (lin ^ (((lin >> 7) & msk) << 4)));
+                    v[b][1] = nch > 1 ? ptx::lds128(pbase + ((lin + 16) ^ ((((lin + 16) >> 7) & msk) << 4))) : make_uint4(0, 0, 0, 0);
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive_cnt(empty_p((int)(tl0 % (uint32_t)nsp)), (uint32_t)nsub);
+                    if (has1) ptx::mbar_arrive_cnt(empty_p((int)(tl1 % (uint32_t)nsp)), (uint32_t)nsub);
+                }
+                uint32_t a[2][32];
+#pragma unroll
+                for (int b = 0; b < 2; ++b)
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        if (c >= nch) break;
+                        const uint32_t w[4] = {v[b][c].x, v[b][c].y, v[b][c].z, v[b][c].w};
+#pragma unroll
+                        for (int i = 0; i < 4; ++i) {
+                            const uint4 o = unpack16_levels(w[i], ta.lp);
+                            a[b][16 * c + 4 * i] = o.x; a[b][16 * c + 4 * i + 1] = o.y; a[b][16 * c + 4 * i + 2] = o.z;
+                            a[b][16 * c + 4 * i + 3] = o.w;
+                        }
+                    }
+#pragma unroll
+                for (int b = 0; b < 2; ++b) {
+                    const uint32_t tl = b ? tl1 : tl0;
+                    if (b && !has1) break;
+                    const int sa = (int)(tl % SA);
+                    ptx::mbar_wait(empty_a(sa), ((tl / SA) & 1u) ^ 1u);   // MMA(tl - SA) completed
+                    ptx::tc_fence_after();
+                    if (nch > 1) ptx::tmem_st_32x32b_x32(trow_a + sa * C::ACOLS, a[b]);
+                    else ptx::tmem_st_32x32b_x16(trow_a + sa * C::ACOLS, a[b]);
+                }
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) {
+                    ptx::mbar_arrive(full_a((int)(tl0 % SA)));
+                    if (has1) ptx::mbar_arrive(full_a((int)(tl1 % SA)));
+                }
+            }
+        } else {
         if (ta.implicit) {
             gc.advance(ta, 0, r, ntiles);
             if (gc.t < ntiles) gc.pixel(ta, r);
@@ -682,6 +741,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 if (lane == 0 && quarter == 0) TS_EV(2, g);
             }
         }
+        }   // general stages
     } else {
         // ---------------- epilogue (lane quarter = warp % 4, tile group = warp / 4)
         constexpr int EG = NEPI / 4, HALF = BN, NCH = BN / 32;
@@ -746,19 +806,24 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 use16 = __all_sync(0xFFFFFFFFu, (n < 0 ? -n : n) + ta.f16_accmax <= 32767);
             }
             if (use16) {
+                // all of the tile's accumulators (up to 128 columns as 16-bit pairs) are loaded
+                // before any requant work, so the TMEM buffer goes back to the MMA as early as
+                // possible (the accumulator ring is only NACC = 2 deep for 128-column tiles)
+                constexpr int NLD = NCH / 2 < 2 ? NCH / 2 : 2;   // 64-column loads held in registers
 #pragma unroll 1
-                for (int c = 0; c < NCH; c += 2) {   // 64 columns per TMEM load
-                    uint32_t r16[32];
-                    ptx::tmem_ld_32x32b_x32_pack16(trow + c * 32, r16);
+                for (int c0 = 0; c0 < NCH; c0 += 2 * NLD) {
+                    uint32_t r16[NLD][32];
+#pragma unroll
+                    for (int l = 0; l < NLD; ++l) ptx::tmem_ld_32x32b_x32_pack16(trow + (c0 + 2 * l) * 32, r16[l]);
                     ptx::tmem_ld_wait();
-                    if (c == NCH - 2) {
+                    if (c0 + 2 * NLD >= NCH) {
                         ptx::tc_fence_before();
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
                     }
 #pragma unroll
-                    for (int hh = 0; hh < 2; ++hh) {
-                        const int64_t qc = q0 + (c + hh) * 32;
+                    for (int hh = 0; hh < 2 * NLD; ++hh) {
+                        const int64_t qc = q0 + (c0 + hh) * 32;
                         uint32_t na[16];
                         if (ta.f16_tab) {
                             const uint32_t ta4 = sbase + C::OFF_TAB + (uint32_t)(qc >> 1) * 4u;
@@ -773,12 +838,9 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         }
                         uint32_t rr[16];
 #pragma unroll
-                        for (int j = 0; j < 16; ++j) rr[j] = r16[16 * hh + j];
+                        for (int j = 0; j < 16; ++j) rr[j] = r16[hh >> 1][16 * (hh & 1) + j];
                         if (p >= ta.np) continue;
                         const uint2 o = requant16_32(rr, na, ta.f16_w2, ta.f16_m, ta.f16_c2);
-#ifdef DG_EXP_NOSTORE
-                        if (o.x == 0x12345678u && o.y == 0x9abcdef0u)
-#endif
                         uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
                         if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = o;
                         else store_codes32_ts(dp, o.x, o.y, 8);
