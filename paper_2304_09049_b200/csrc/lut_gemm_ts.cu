@@ -66,31 +66,36 @@ constexpr int EPI_BAR = 2;       // epilogue warps only (requant table build)
 // padded input pixels in shared memory (no-swizzle K-major layout) and every tap's MMA reads it
 // through a row-shifted descriptor, so each input pixel is unpacked once per tile instead of
 // once per tap (im2col row).
-template <int BN, int EG, int KST, bool WIN = false>
+// ASM (template): the A operand in SHARED memory (no-swizzle K-major stages written by the unpack
+// warps, SS MMA) instead of tensor memory, which leaves all 512 TMEM columns to two 128x256
+// accumulators: short-K, wide-output layers, whose cost is a fixed chain of hand-offs per tile.
+template <int BN, int EG, int KST, bool WIN = false, bool ASM = false>
 struct TsCfg {
     static constexpr int KSTEPS = KST / 32;                 // MMAs (K = 32) per stage
     static constexpr int ACOLS = KST / 4;                   // TMEM columns of one A stage
     static constexpr int HALVES = KST / KA;                 // 128-code halves (B atoms, 32-column A parts)
     // accumulator buffers (TMEM cols NACC*BN); a multiple of EG so that each buffer has one
     // epilogue group (which then waits on its barrier phases in order)
-    static constexpr int NACC = BN == 256 ? 1 : (BN == 128 ? 2 : 4);
+    static constexpr int NACC = ASM ? 512 / BN : (BN == 256 ? 1 : (BN == 128 ? 2 : 4));
     static_assert(NACC % EG == 0, "accumulator buffers per epilogue group");
-    static constexpr int SA = (512 - NACC * BN) / ACOLS > 8 ? 8 : (512 - NACC * BN) / ACOLS;   // A stages in TMEM
+    static constexpr int SA = ASM ? 4 : ((512 - NACC * BN) / ACOLS > 8 ? 8 : (512 - NACC * BN) / ACOLS);   // A stages
     static constexpr int B_ATOM = BN * KA;                  // bytes of one 128-code B atom
     static constexpr int B_BYTES = BN * KST;
-    static constexpr int SB_RAW = (BN == 64 || WIN ? 98304 : 131072) / B_BYTES;
+    static constexpr int SB_RAW = (BN == 64 || WIN || ASM ? 98304 : 131072) / B_BYTES;
     static constexpr int SB = SB_RAW > 8 ? 8 : SB_RAW;      // B (int8) smem stages
     static constexpr int TMEM_A0 = NACC * BN;               // first A column
     static constexpr int TMEM_COLS = 512;
-    static constexpr int P_REGION = WIN ? 106496 : 4 * BM * PKS_MAX;   // packed P slots / WIN: packed ring + windows
+    static constexpr int P_REGION = WIN ? 106496 : (ASM ? 32768 : 4 * BM * PKS_MAX);   // packed P / WIN ring + windows
+    static constexpr int A_STAGE = ASM ? BM * KST : 0;       // ASM: one A stage, 16-byte K chunk j of row r at j*BM*16 + r*16
     static constexpr int OFF_B = 0;                          // 1024-aligned (SW128)
     static constexpr int OFF_P = OFF_B + SB * B_BYTES;
-    static constexpr int OFF_BAR = OFF_P + P_REGION;
+    static constexpr int OFF_A = OFF_P + P_REGION;
+    static constexpr int OFF_BAR = OFF_A + SA * A_STAGE;
     static constexpr int NBAR = 2 * SP_MAX + 2 * SB + 2 * SA + 2 * NACC;
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr int OFF_TAB = (OFF_TMEM + 16 + 15) / 16 * 16;   // 16-bit requant offsets, one u32 per column pair
     static constexpr int ALLOC = OFF_TAB + TAB_PAIRS * 4 + 1024;
-    static_assert(TMEM_A0 + SA * ACOLS <= TMEM_COLS && SA >= 2, "TMEM budget");
+    static_assert((ASM ? NACC * BN : TMEM_A0 + SA * ACOLS) <= TMEM_COLS && SA >= 2, "TMEM budget");
     static_assert(ALLOC <= 232448, "shared memory budget");
 };
 
@@ -279,11 +284,11 @@ __device__ __noinline__ void ts_epilogue_general(const TsArgs &ta, const Requant
     store_codes32_ts(dp, o0, o1, (int)((ta.nq - qc + 3) / 4));
 }
 
-template <int BN, int NEPI, int NUNP, int KST, bool WIN>
+template <int BN, int NEPI, int NUNP, int KST, bool WIN, bool ASM>
 __global__ void __launch_bounds__(Roles<NEPI, NUNP>::NT, 1)
 lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
-    using C = TsCfg<BN, NEPI / 4, KST, WIN>;
+    using C = TsCfg<BN, NEPI / 4, KST, WIN, ASM>;
     using R = Roles<NEPI, NUNP>;
     constexpr int SB = C::SB, SA = C::SA, NACC = C::NACC, SP = SP_MAX;
     const int nsp = ta.sp;
@@ -485,6 +490,23 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         ptx::mma_commit(acc_full(acc));
                     }
                     TS_EV(15, g);
+                } else if (lane == 0 && ASM) {
+                    const uint64_t ad = ptx::desc_k_none(sbase + C::OFF_A + (uint32_t)(sa * C::A_STAGE), BM * 16);
+                    const uint64_t bd = bdesc0 + (uint64_t)((sb * C::B_BYTES) >> 4);
+                    // k-step k: A K-chunks 2k, 2k+1 (+2k * BM*16 bytes), B atom k/4, +32 B per k-step inside
+                    if (s < ta.nstages - 1 || ta.last_ksteps == C::KSTEPS) {
+#pragma unroll
+                        for (int k = 0; k < C::KSTEPS; ++k)
+                            ptx::mma_i8_ss(dt, ad + (uint64_t)((2 * k * BM * 16) >> 4), bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
+                                           idesc, (s > 0 || k > 0) ? 1u : 0u);
+                    } else {
+                        for (int k = 0; k < ta.last_ksteps; ++k)
+                            ptx::mma_i8_ss(dt, ad + (uint64_t)((2 * k * BM * 16) >> 4), bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
+                                           idesc, (s > 0 || k > 0) ? 1u : 0u);
+                    }
+                    ptx::mma_commit(empty_a(sa));
+                    if (!ta.bres) ptx::mma_commit(empty_b(sb));
+                    if (s == ta.nstages - 1) ptx::mma_commit(acc_full(acc));
                 } else if (lane == 0) {
                     const uint32_t at = tmem + C::TMEM_A0 + sa * C::ACOLS;
                     const uint64_t bd = bdesc0 + (uint64_t)((sb * C::B_BYTES) >> 4);
@@ -600,6 +622,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             for (uint32_t tl0 = grp; blockIdx.x + tl0 * gridDim.x < (uint32_t)ntiles; tl0 += 2 * NUM_UGROUPS) {
                 const uint32_t tl1 = tl0 + NUM_UGROUPS;
                 const bool has1 = blockIdx.x + tl1 * gridDim.x < (uint32_t)ntiles;
+                if (lane == 0 && quarter == 0) TS_EV(0, tl0);
                 uint4 v[2][2];
 #pragma unroll
                 for (int b = 0; b < 2; ++b) {
@@ -636,17 +659,29 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     if (b && !has1) break;
                     const int sa = (int)(tl % SA);
                     ptx::mbar_wait(empty_a(sa), ((tl / SA) & 1u) ^ 1u);   // MMA(tl - SA) completed
-                    ptx::tc_fence_after();
-                    if (nch > 1) ptx::tmem_st_32x32b_x32(trow_a + sa * C::ACOLS, a[b]);
-                    else ptx::tmem_st_32x32b_x16(trow_a + sa * C::ACOLS, a[b]);
+                    if (ASM) {   // shared-memory A stage: K chunk j (16 codes) of row r at j*BM*16 + r*16
+                        const uint32_t ab = sbase + C::OFF_A + (uint32_t)(sa * C::A_STAGE) + (uint32_t)(r * 16);
+#pragma unroll
+                        for (int j = 0; j < 8; ++j) {
+                            if (j >= 4 * nch) break;
+                            asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(ab + (uint32_t)(j * BM * 16)),
+                                         "r"(a[b][4 * j]), "r"(a[b][4 * j + 1]), "r"(a[b][4 * j + 2]), "r"(a[b][4 * j + 3]) : "memory");
+                        }
+                    } else {
+                        ptx::tc_fence_after();
+                        if (nch > 1) ptx::tmem_st_32x32b_x32(trow_a + sa * C::ACOLS, a[b]);
+                        else ptx::tmem_st_32x32b_x16(trow_a + sa * C::ACOLS, a[b]);
+                    }
                 }
-                ptx::tmem_st_wait();
+                if (ASM) ptx::fence_proxy_async_smem();   // generic stores -> visible to the tensor core
+                else ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) {
                     ptx::mbar_arrive(full_a((int)(tl0 % SA)));
                     if (has1) ptx::mbar_arrive(full_a((int)(tl1 % SA)));
                 }
+                if (lane == 0 && quarter == 0) { TS_EV(2, tl0); TS_EV(2, tl1); }
             }
         } else {
         if (ta.implicit) {
@@ -720,6 +755,16 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 ptx::mbar_wait(empty_a(sa), ((g / SA) & 1u) ^ 1u);   // MMA(g - SA) completed
                 if (lane == 0 && quarter == 0) TS_EV(11, g);
                 ptx::tc_fence_after();
+                if (ASM) {   // shared-memory A stage: K chunk j (16 codes) of row r at j*BM*16 + r*16
+                    const uint32_t ab = sbase + C::OFF_A + (uint32_t)(sa * C::A_STAGE) + (uint32_t)(r * 16);
+#pragma unroll
+                    for (int j = 0; j < 8 * C::HALVES; ++j) {
+                        if (j >= 4 * nchunk) break;
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(ab + (uint32_t)(j * BM * 16)),
+                                     "r"(a[4 * j]), "r"(a[4 * j + 1]), "r"(a[4 * j + 2]), "r"(a[4 * j + 3]) : "memory");
+                    }
+                    ptx::fence_proxy_async_smem();
+                } else {
 #pragma unroll
                 for (int h = 0; h < C::HALVES; ++h) {
                     if (2 * h >= nchunk) break;
@@ -735,6 +780,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 #endif
                 }
                 ptx::tmem_st_wait();
+                }
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(full_a(sa));
@@ -1033,11 +1079,11 @@ bool f16_params(int64_t t0, int64_t t1, int64_t t2, uint32_t &m_out, uint32_t &c
     return false;
 }
 
-template <int BN, int NEPI, int NUNP, int KST, bool WIN = false>
+template <int BN, int NEPI, int NUNP, int KST, bool WIN = false, bool ASM = false>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                     cudaStream_t st, const TsConv *cv) {
-    using C = TsCfg<BN, NEPI / 4, KST, WIN>;
+    using C = TsCfg<BN, NEPI / 4, KST, WIN, ASM>;
     int64_t acc_bound = 0;   // K * max |pl[a] * ql[b]|
     for (int a = 0; a < 4; ++a)
         for (int b = 0; b < 4; ++b) {
@@ -1152,7 +1198,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     if (!make_map_sw128(&mb, Q8, ld8, nq, BN, 128)) return DG_ERR_CUDA;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
+        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
             cudaSuccess)
             return DG_ERR_CUDA;
         attr_set = true;
@@ -1172,7 +1218,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     la[0].val.programmaticStreamSerializationAllowed = getenv("DG_NO_PDL") ? 0 : 1;
     lc.attrs = la;
     lc.numAttrs = 1;
-    if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN>, mp, mb, ta, rqv) != cudaSuccess)
+    if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM>, mp, mb, ta, rqv) != cudaSuccess)
         return DG_ERR_CUDA;
     return launch_status();
 }
@@ -1210,6 +1256,10 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     // stages already carry 512 MMA cycles).
     const bool short_k = K <= 2 * KA;
     const bool k256 = K > KA && !getenv("DG_TS_K128");
+    // short K, wide output: 128x256 tiles with the A operand in shared memory and two TMEM accumulators
+    // (measured: narrower ASM tiles with 128-code stages lose to the TMEM-A kernel at K = 256)
+    if (short_k && nq >= 256 && !getenv("DG_NO_ASM"))
+        return launch_ts<256, 8, 4, 128, false, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     // 128x256 tiles halve the shared-memory bytes of B per MAC (measured: 8192^3 1666 -> 2323
     // TOPS); their single TMEM accumulator buffer cannot overlap the epilogue with the next tile,
     // so they are used only when the K loop is long (>= 24 x 128 codes).
@@ -1219,7 +1269,7 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     if (nq >= 256 && K >= bn256_k && (tiles256 >= num_sms() || K >= 24 * KA) && !getenv("DG_TS_NO_BN256"))
         return launch_ts<256, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 
-    if (nq > 64) {
+    if (nq > 64 && !(short_k && getenv("DG_BN64_SHORT"))) {
         if (short_k && !k256) return launch_ts<128, 8, 4, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         if (short_k) return launch_ts<128, 8, 4, 256>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         if (!k256) return launch_ts<128, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);

@@ -53,9 +53,25 @@ DG_DEV bool mbar_try_wait(uint32_t bar, uint32_t parity) {
 #endif
     return ok != 0;
 }
+DG_DEV bool mbar_test_wait(uint32_t bar, uint32_t parity) {
+    uint32_t ok;
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.test_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(ok)
+        : "r"(bar), "r"(parity)
+        : "memory");
+    return ok != 0;
+}
 DG_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
+#ifdef DG_MBAR_SPIN
+    while (!mbar_test_wait(bar, parity)) {   // non-suspending probe loop
+    }
+#else
     while (!mbar_try_wait(bar, parity)) {
     }
+#endif
 }
 
 // ---------------------------------------------------------------- TMA

@@ -50,6 +50,10 @@ names = {13: "P_loop", 14: "P_slot", 12: "P_tma", 0: "unp0", 1: "unp_rdy", 11: "
 print("stage " + " ".join(f"{v:>8s}" for v in names.values()))
 for g in list(range(0, 40)):
     print(f"{g:5d} " + " ".join(f"{a[e][g]:8d}" for e in names))
+if len(sys.argv) > 2 and sys.argv[2] == "--short":
+    print("tile  P_loop P_tma unp0 unp_done w_start w_fullA handoff epi0 epi_accfull epi_done")
+    for t in range(0, 40):
+        print(f"{t:4d} " + " ".join(f"{a[e][t]:8d}" for e in (13, 12, 0, 2, 3, 4, 6, 8, 9, 10)))
 if len(sys.argv) > 2 and sys.argv[2] == "--win":
     print("stage: waiter_fullA w_fullB handoff mma_start mma_end")
     for g in range(0, 30):
