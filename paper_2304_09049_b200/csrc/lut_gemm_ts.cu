@@ -159,6 +159,11 @@ struct TsArgs {
     int32_t f16_tab;       // 1: per-column bias -> negA table built in shared memory
     uint32_t f16_m, f16_c2, f16_w2, f16_na2;   // m; c and W replicated in both halves; uniform negA
     int32_t f16_thr0m1, f16_accmax;
+    // residual in the 16-bit path (S7 with reading Q13): 1 = identity shortcut over packed codes,
+    // r = res_levels[code]*res_mult (pair table res_pair[16] in smem); 2 = int32 residual
+    // (downsample accumulators), packed to 16-bit pairs with a per-warp range check
+    int32_t f16_res;
+    uint32_t res_pair[16];    // (r[c0] & 0xFFFF) | r[c1] << 16 for the 4-bit pair index c0 | c1 << 2
 };
 
 // Tile t -> (row block tp, column block tq).  Tiles are walked in groups of `group` row blocks,
@@ -794,6 +799,8 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         static_assert(NCH % 2 == 0, "epilogue loads 64 columns at a time");
         // 16-bit requant offsets per column pair (bias_axis 0): negA = bias - (thr0 - 1), checked
         // against int16 overflow of acc + negA; any failure sends every tile to the 32-bit path
+        if (ta.f16 && ta.f16_res == 1 && threadIdx.x - EPI_WARP0 * 32 < 16)   // residual pair table (smem)
+            f16tab[TAB_PAIRS - 16 + threadIdx.x - EPI_WARP0 * 32] = ta.res_pair[threadIdx.x - EPI_WARP0 * 32];
         if (ta.f16 && ta.f16_tab) {
             uint32_t bad = 0;
             for (int i = threadIdx.x - EPI_WARP0 * 32; i < (int)(ta.nq >> 1); i += NEPI * 32) {
@@ -803,8 +810,8 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 f16tab[i] = ((uint32_t)n0 & 0xFFFFu) | ((uint32_t)n1 << 16);
             }
             if (bad) *f16_flag = 1u;
-            ptx::named_bar_sync(EPI_BAR, NEPI * 32);
         }
+        if (ta.f16 && (ta.f16_tab || ta.f16_res == 1)) ptx::named_bar_sync(EPI_BAR, NEPI * 32);
         const bool f16_ok = ta.f16 && *f16_flag == 0u;
         ptx::griddep_wait();
         const int quarter = warp & 3, eg = (warp - EPI_WARP0) >> 2, half = 0;
@@ -833,7 +840,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             if (lane == 0 && quarter == 0) TS_EV(9, tl);
             ptx::tc_fence_after();
             const uint32_t trow = tmem + acc * BN + half * HALF + ((uint32_t)(quarter * 32) << 16);
-            const bool fast = ta.fast_rq && q0 + HALF <= ta.nq;
+            const bool fast = (ta.fast_rq || ta.f16_res) && q0 + HALF <= ta.nq;
             const int32_t rb = (fast && rq.bias && rq.bias_axis == 1 && p < ta.np) ? __ldg(rq.bias + p) : 0;
             // 16-bit SIMD path (warp-uniform): per-row offsets need every lane's row in range
             bool use16 = fast && f16_ok;
@@ -862,7 +869,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 #pragma unroll
                     for (int l = 0; l < NLD; ++l) ptx::tmem_ld_32x32b_x32_pack16(trow + (c0 + 2 * l) * 32, r16[l]);
                     ptx::tmem_ld_wait();
-                    if (c0 + 2 * NLD >= NCH) {
+                    if (c0 + 2 * NLD >= NCH && ta.f16_res != 2) {   // (int32 residual: kept for an exact redo)
                         ptx::tc_fence_before();
                         __syncwarp();
                         if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
@@ -885,6 +892,33 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         uint32_t rr[16];
 #pragma unroll
                         for (int j = 0; j < 16; ++j) rr[j] = r16[hh >> 1][16 * (hh & 1) + j];
+                        if (ta.f16_res == 1) {   // identity shortcut: pair residuals from the packed codes
+                            const uint2 rc = p < ta.np ? *reinterpret_cast<const uint2 *>(rq.res_codes + p * rq.ld_res_codes + (qc >> 2))
+                                                       : make_uint2(0, 0);
+                            const uint32_t rt = sbase + C::OFF_TAB + 4u * (TAB_PAIRS - 16);
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) {
+                                uint32_t rp;
+                                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(rp) : "r"(rt + 4u * (((j < 8 ? rc.x : rc.y) >> (4 * (j & 7))) & 15u)));
+                                rr[j] = __vadd2(rr[j], rp);
+                            }
+                        } else if (ta.f16_res == 2) {   // int32 residual -> 16-bit pairs (|r| < 2^14 checked)
+                            uint32_t bad = 0;
+                            if (p < ta.np) {
+                                const int4 *rp = reinterpret_cast<const int4 *>(rq.res + p * rq.ld_res + qc);
+#pragma unroll
+                                for (int j = 0; j < 8; ++j) {
+                                    const int4 v = __ldg(rp + j);
+                                    bad |= (uint32_t)(v.x + 16384) | (uint32_t)(v.y + 16384) | (uint32_t)(v.z + 16384) | (uint32_t)(v.w + 16384);
+                                    rr[2 * j] = __vadd2(rr[2 * j], prmt_b32((uint32_t)v.x, (uint32_t)v.y, 0x5410u));
+                                    rr[2 * j + 1] = __vadd2(rr[2 * j + 1], prmt_b32((uint32_t)v.z, (uint32_t)v.w, 0x5410u));
+                                }
+                            }
+                            if (__any_sync(0xFFFFFFFFu, (bad >> 15) != 0u)) {   // exact redo of this chunk (TMEM still held)
+                                ts_epilogue_general(ta, rq, trow + (uint32_t)((c0 + hh) * 32), p, qc);
+                                continue;
+                            }
+                        }
                         if (p >= ta.np) continue;
                         const uint2 o = requant16_32(rr, na, ta.f16_w2, ta.f16_m, ta.f16_c2);
                         uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
@@ -892,7 +926,12 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         else store_codes32_ts(dp, o.x, o.y, 8);
                     }
                 }
-            } else if (!fast) {
+                if (ta.f16_res == 2) {
+                    ptx::tc_fence_before();
+                    __syncwarp();
+                    if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
+                }
+            } else if (!fast || !ta.fast_rq) {   // (residuals outside the 16-bit path: exact general path)
 #pragma unroll 1
                 for (int c = 0; c < NCH; ++c) ts_epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
                 ptx::tc_fence_before();
@@ -1144,9 +1183,16 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     ta.D = D;
     ta.ldd = ldd;
     ta.has_rq = rq ? 1 : 0;
-    if (rq && !rq->res && !rq->res_codes && acc_bound < ((int64_t)1 << 29) &&
+    const bool has_res = rq && (rq->res || rq->res_codes);
+    int64_t res_bound = 0;   // max |residual| for the 16-bit range check (int32 residuals: checked per warp)
+    if (rq && rq->res_codes)
+        for (int c = 0; c < 4; ++c) {
+            const int64_t v = (int64_t)rq->res_levels[c] * rq->res_mult;
+            res_bound = (v < 0 ? -v : v) > res_bound ? (v < 0 ? -v : v) : res_bound;
+        }
+    if (rq && acc_bound < ((int64_t)1 << 29) &&
         (!rq->bias || rq->bias_axis == 1 || (((uintptr_t)rq->bias) & 15) == 0)) {
-        ta.fast_rq = 1;      // acc is exact (no correction term): acc + bias >= t <=> x > t - 1
+        ta.fast_rq = has_res ? 0 : 1;   // acc is exact (no correction term): acc + bias >= t <=> x > t - 1
         ta.dir = rq->dir;
         for (int j = 0; j < 3; ++j) {
             const int64_t t = rq->thr[j];
@@ -1159,15 +1205,29 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         // (in the epilogue) or per column (smem table at kernel start).
         const int64_t *t = rq->thr;
         uint32_t m16 = 0, c16 = 0;
-        if (rq->dir > 0 && acc_bound <= 32767 && t[0] > -((int64_t)1 << 30) && t[2] < ((int64_t)1 << 30) &&
-            (nq >> 1) <= TAB_PAIRS && !getenv("DG_NO_F16") && f16_params(t[0], t[1], t[2], m16, c16)) {
+        const bool res_ok = !has_res ||
+                            (rq->res_codes && !rq->res && res_bound <= 16383 && (rq->ld_res_codes & 7) == 0 &&
+                             (((uintptr_t)rq->res_codes) & 7) == 0) ||
+                            (rq->res && !rq->res_codes && (rq->ld_res & 3) == 0 && (((uintptr_t)rq->res) & 15) == 0);
+        if (rq->res && !rq->res_codes) res_bound = 16384;   // int32 residuals: |r| < 2^14 checked per chunk
+        if (rq->dir > 0 && acc_bound + res_bound <= 32767 && t[0] > -((int64_t)1 << 30) && t[2] < ((int64_t)1 << 30) &&
+            res_ok && (nq >> 1) <= TAB_PAIRS - 16 && !getenv("DG_NO_F16") && f16_params(t[0], t[1], t[2], m16, c16)) {
             const int64_t thr0m1 = t[0] - 1;
             ta.f16_m = m16;
             ta.f16_c2 = c16 * 0x10001u;
             ta.f16_w2 = (uint32_t)(t[2] - t[0] + 1) * 0x10001u;
             ta.f16_thr0m1 = (int32_t)thr0m1;
-            ta.f16_accmax = (int32_t)acc_bound;
+            ta.f16_accmax = (int32_t)(acc_bound + res_bound);
             ta.f16 = 1;
+            if (rq->res_codes) {
+                ta.f16_res = 1;
+                for (int i = 0; i < 16; ++i) {
+                    const int32_t r0 = rq->res_levels[i & 3] * rq->res_mult, r1 = rq->res_levels[i >> 2] * rq->res_mult;
+                    ta.res_pair[i] = ((uint32_t)r0 & 0xFFFFu) | ((uint32_t)r1 << 16);
+                }
+            } else if (rq->res) {
+                ta.f16_res = 2;
+            }
             ta.f16_tab = (!rq->bias || rq->bias_axis == 0) ? 1 : 0;   // else: per-row offsets
         }
     }

@@ -439,3 +439,47 @@ def test_conv_window_path_vs_oracle(monkeypatch, B, H, W, C, Cout, pad_code):
     outc = dg.lut_conv2d_prepared(xp, w8, lut, p, rq=rq, ws=ws)
     expc = oracle.requantize(exp.reshape(-1, Cout), 30000, 20, 1, 0, 3, bias=bias, bias_axis=0)
     assert np.array_equal(oracle_codes_of(outc, expc.shape[0], Cout), expc)
+
+
+@pytest.mark.parametrize("C2,res_mult", [(64, 37), (128, 900), (64, 20000)])
+def test_conv_residual_16bit_path(C2, res_mult):
+    """Residual requant (reading Q13) through the tensor-core 16-bit epilogue: identity shortcut
+    over packed codes (pair table) and int32 downsample shortcut (|r| < 2^14 fast, else exact
+    redo); res_mult 20000 exceeds the 16-bit range and must take the exact path."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    lut = dg.build_lut(WL, AL, 8)
+    T = oracle.build_lut16(WL, AL)
+    g = np.random.default_rng(C2 + res_mult)
+    B, H, C = 2, 10, 64
+    x = g.integers(0, 4, (B, H, H, C), dtype=np.uint8)
+    w = g.integers(0, 4, (C, 3, 3, C), dtype=np.uint8)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    w8 = dg.expand_operand(wp, 9 * Cp, WL)
+    p = dg.conv_params(B, H, H, C, C, 3, 3, 1, 1, 0, ldw=wp.shape[1])
+    ws = torch.empty(dg.conv_workspace_size(p), dtype=torch.uint8, device=DEV)
+    acc = oracle.conv2d_direct(x, w, T, 1, 1, 0).reshape(-1, C)
+    bias = g.integers(-60, 60, C).astype(np.int32)
+    rq = dg.Requant(mult=15000, shift=20, zp=0, bias=torch.from_numpy(bias).to(DEV), bias_axis=0,
+                    res_codes=xp, res_mult=res_mult, res_levels=AL)
+    out = dg.lut_conv2d_prepared(xp, w8, lut, p, rq=rq, ws=ws)
+    r = (np.array(AL)[x.reshape(-1, C)] * res_mult).astype(np.int32)
+    exp = oracle.requantize(acc, 15000, 20, 0, 0, 3, res=r, bias=bias, bias_axis=0)
+    assert np.array_equal(oracle_codes_of(out, exp.shape[0], C), exp)
+    # int32 residual: a 1x1 stride-2 downsample's accumulators, scaled to reach the 2^14 limit
+    w2 = g.integers(0, 4, (C2, 3, 3, C), dtype=np.uint8)
+    wd = g.integers(0, 4, (C2, 1, 1, C), dtype=np.uint8)
+    w2p, wdp = conv_weights_pack(w2, Cp), conv_weights_pack(wd, Cp)
+    w28, wd8 = dg.expand_operand(w2p, 9 * Cp, WL), dg.expand_operand(wdp, Cp, WL)
+    pd = dg.conv_params(B, H, H, C, C2, 1, 1, 2, 0, 0, ldw=wdp.shape[1])
+    p2 = dg.conv_params(B, H, H, C, C2, 3, 3, 2, 1, 0, ldw=w2p.shape[1])
+    racc = dg.lut_conv2d_prepared(xp, wd8, lut, pd, ws=ws)
+    rd = oracle.conv2d_direct(x, wd, T, 2, 0, 0).reshape(-1, C2)
+    assert np.array_equal(host(racc), rd)
+    scale = max(1, res_mult // 100)
+    racc_s = (racc * scale).contiguous()
+    out2 = dg.lut_conv2d_prepared(xp, w28, lut, p2, rq=dg.Requant(mult=12000, shift=20, res=racc_s), ws=ws)
+    a2 = oracle.conv2d_direct(x, w2, T, 2, 1, 0).reshape(-1, C2)
+    exp2 = oracle.requantize(a2, 12000, 20, 0, 0, 3, res=(rd * scale).astype(np.int32))
+    assert np.array_equal(oracle_codes_of(out2, exp2.shape[0], C2), exp2)
