@@ -184,6 +184,17 @@ static bool conv_is_direct(const dg_conv_params *p) {
     return p->kh == 1 && p->kw == 1 && p->stride == 1 && p->pad == 0 && (p->C / 4) % 16 == 0;
 }
 
+// Split-K region at the tail of the conv workspace: int32 partial-sum slices [<= 8][rows][Cout],
+// only for convs with few output tiles (the kernel splits K when tiles <= SMs / 2).  No
+// initialisation needed: each split overwrites its slice, the reduce kernel reads them back.
+static int64_t splitk_bytes(const dg_conv_params *p) {
+    const int64_t Ho = (p->H + 2 * p->pad - p->kh) / p->stride + 1;
+    const int64_t Wo = (p->W + 2 * p->pad - p->kw) / p->stride + 1;
+    const int64_t rows = (int64_t)p->B * Ho * Wo, tiles = ((rows + 127) / 128) * ((p->Cout + 63) / 64);
+    if (tiles * 2 > num_sms() * 4) return 0;   // (tile count with 64-column tiles, 4x margin)
+    return (8 * rows * p->Cout * 4 + 15) / 16 * 16;   // up to 8 split slices
+}
+
 size_t dg_lut_conv2d_workspace_size(const dg_conv_params *p) {
     if (!p || p->B <= 0 || p->H <= 0 || p->W <= 0 || p->C <= 0 || p->kh <= 0 || p->kw <= 0 ||
         p->stride <= 0)
@@ -192,7 +203,8 @@ size_t dg_lut_conv2d_workspace_size(const dg_conv_params *p) {
     const int64_t Wo = (p->W + 2 * p->pad - p->kw) / p->stride + 1;
     const int64_t K = (int64_t)p->kh * p->kw * p->C;
     const int64_t cols = conv_is_direct(p) ? 0 : (int64_t)p->B * Ho * Wo * dg_packed_ld(K);   // upper bound
-    return (size_t)((cols + 127) / 128 * 128 + (int64_t)p->Cout * expand_ld(K) + 256);
+    const int64_t a = (cols + 127) / 128 * 128 + (int64_t)p->Cout * expand_ld(K) + 256;
+    return (size_t)(a + splitk_bytes(p));
 }
 
 dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_lut *lut,
@@ -287,12 +299,20 @@ dg_status dg_lut_conv2d_prepared(const uint8_t *d_x, const int8_t *d_w8, int64_t
     RequantArgs ra{};
     if (rq) ra = to_args(rq);
     const int64_t ldd = rq ? p->Cout / 4 : p->Cout;
+    // (direct / implicit paths: d_ws, if given, serves split-K; it must be zero and is left zero)
+    const int64_t skb = splitk_bytes(p);
+    void *skws = nullptr;
+    if (d_ws && skb > 0 && (int64_t)ws_bytes >= skb) {
+        const uintptr_t tail = ((uintptr_t)d_ws + ws_bytes - (size_t)skb) & ~(uintptr_t)15;
+        if (tail >= (uintptr_t)d_ws) skws = reinterpret_cast<void *>(tail);
+    }
     if (conv_is_direct(p) && aligned16(d_x))
-        return lut_gemm_ts(d_x, p->C / 4, d_w8, ld8, rows, p->Cout, K, lut->al, lut->wl, d_out, ldd, rq ? &ra : nullptr, st);
+        return lut_gemm_ts(d_x, p->C / 4, d_w8, ld8, rows, p->Cout, K, lut->al, lut->wl, d_out, ldd, rq ? &ra : nullptr, st,
+                           nullptr, skws, (size_t)skb);
     if (conv_implicit_ok(p, d_x)) {
         TsConv cv{d_x, p->H, p->W, p->C / 4, p->kh, p->kw, p->stride, p->pad, (int32_t)Ho, (int32_t)Wo, p->pad_code};
         return lut_gemm_ts(nullptr, 0, d_w8, ld8, rows, p->Cout, K, lut->al, lut->wl, d_out, ldd, rq ? &ra : nullptr, st,
-                           &cv);
+                           &cv, skws, (size_t)skb);
     }
     // explicit im2col fallback (e.g. VGG conv1_1 with C = 4 padded channels)
     const int64_t ld = dg_packed_ld(K);

@@ -125,6 +125,12 @@ struct TsArgs {
     int64_t np, nq;
     int32_t nstages, last_ksteps, ntp, ntq;
     int32_t group;         // tile rasterisation: GROUP row blocks x all column blocks, column-major inside
+    // split-K (few output tiles, long K): work item t = output tile t / sk, K stages of split t % sk;
+    // each split stores its partial sums to its own slice ws_acc[ks] (int32 [sk][np][nq]); the
+    // splitk_reduce_kernel launched right behind sums the slices and requantises / stores
+    int32_t sk, nwork;   // nwork = ntp * ntq * sk work items
+    FastDiv fd_sk;
+    int32_t *ws_acc;
     int32_t last_grp, last_rows;   // index of the last row group and its row-block count
     FastDiv fd_pg, fd_grp, fd_last;  // / (group * ntq), / group, / last_rows
     int32_t pks;           // packed P slot bytes per row (smem pitch): ldp <= 64 (bulk) or 128 (TMA box)
@@ -178,17 +184,35 @@ DG_DEV void tile_coords(const TsArgs &ta, int t, int &tp, int &tq) {
     tp = (int)(grp * ta.group + (rem - q * (uint32_t)(last ? ta.last_rows : ta.group)));
 }
 
+// Work item t -> output tile (tp, tq) and its stages [sb, se) (all stages unless split-K)
+// (SK: the kernel instance supports split-K; the others compile the plain tile walk)
+template <bool SK>
+DG_DEV void work_item(const TsArgs &ta, int t, int &tp, int &tq, int &sb, int &se) {
+    if (SK && ta.sk > 1) {
+        const int ot = (int)fdiv((uint32_t)t, ta.fd_sk), ks = t - ot * ta.sk;
+        tile_coords(ta, ot, tp, tq);
+        sb = ks * ta.nstages / ta.sk;
+        se = (ks + 1) * ta.nstages / ta.sk;
+    } else {
+        tile_coords(ta, t, tp, tq);
+        sb = 0;
+        se = ta.nstages;
+    }
+}
+
 // Implicit im2col gather cursor of one unpack thread (row r of its tiles): walks the thread's
 // group's stages (every NUM_UGROUPS-th stage across tiles) and issues each stage's 16-byte chunks
 // (64 codes each) as cp.async copies into one slot of the group's ring.  K order (r, s, c) with c
 // fastest (dg_im2col); out-of-image taps copy the pad code, bytes beyond K copy zeros.
+template <bool SK>
 struct GatherCursor {
-    int t, s;                 // tile and stage of the next fetch
+    int t, s;                 // work item and (absolute) stage of the next fetch
     const uint8_t *img;
     int32_t h0, w0;
+    int se;                   // end of the work item's stage range
     DG_DEV void pixel(const TsArgs &ta, int r) {
-        int tp, tq;
-        tile_coords(ta, t, tp, tq);
+        int tp, tq, sb;
+        work_item<SK>(ta, t, tp, tq, sb, se);
         const int64_t p = (int64_t)tp * BM + r;
         const uint32_t pp = (uint32_t)(p < ta.np ? p : ta.np - 1);
         const uint32_t tt = fdiv(pp, ta.fd_wo), b = fdiv(tt, ta.fd_ho);
@@ -198,9 +222,21 @@ struct GatherCursor {
     }
     DG_DEV void advance(const TsArgs &ta, int by, int r, int ntiles) {
         s += by;
-        bool moved = false;
-        while (s >= ta.nstages) { s -= ta.nstages; t += gridDim.x; moved = true; }
-        if (moved && t < ntiles) pixel(ta, r);
+        if constexpr (!SK) {
+            bool moved = false;
+            while (s >= ta.nstages) { s -= ta.nstages; t += gridDim.x; moved = true; }
+            if (moved && t < ntiles) pixel(ta, r);
+        } else {
+            while (s >= se && t < ntiles) {   // into the next work item of this CTA
+                const int over = s - se;
+                t += gridDim.x;
+                if (t >= ntiles) break;
+                pixel(ta, r);   // sets se
+                int tp, tq, sb, se2;
+                work_item<SK>(ta, t, tp, tq, sb, se2);
+                s = sb + over;
+            }
+        }
     }
     template <int NCH>
     DG_DEV void issue(const TsArgs &ta, uint32_t dst_row, int r, int ntiles, int bytes_per_stage) {
@@ -249,16 +285,10 @@ DG_DEV uint2 requant16_32(const uint32_t (&r)[16], const uint32_t (&na)[16], uin
     return make_uint2(lo, hi);
 }
 
-// int32 output / residual requant / ragged tail for one 32-column chunk (out of line)
-__device__ __noinline__ void ts_epilogue_general(const TsArgs &ta, const RequantArgs &rq, uint32_t taddr, int64_t p,
-                                                 int64_t qc) {
-    uint32_t rr[32];
-    ptx::tmem_ld_32x32b_x32(taddr, rr);
-    ptx::tmem_ld_wait();
+// int32 output / residual requant / ragged tail for one 32-column chunk of accumulator values
+__device__ __forceinline__ void ts_epilogue_values(const TsArgs &ta, const RequantArgs &rq, const int32_t (&v)[32], int64_t p,
+                                                int64_t qc) {
     if (p >= ta.np || qc >= ta.nq) return;
-    int32_t v[32];
-#pragma unroll
-    for (int j = 0; j < 32; ++j) v[j] = (int32_t)rr[j];
     if (!ta.has_rq) {
         int32_t *dp = reinterpret_cast<int32_t *>(ta.D) + p * ta.ldd + qc;
         if (qc + 32 <= ta.nq && (ta.ldd & 3) == 0 && ((reinterpret_cast<uintptr_t>(ta.D) & 15) == 0)) {
@@ -289,7 +319,219 @@ __device__ __noinline__ void ts_epilogue_general(const TsArgs &ta, const Requant
     store_codes32_ts(dp, o0, o1, (int)((ta.nq - qc + 3) / 4));
 }
 
-template <int BN, int NEPI, int NUNP, int KST, bool WIN, bool ASM>
+// the same from tensor memory (warp-collective load)
+__device__ __noinline__ void ts_epilogue_general(const TsArgs &ta, const RequantArgs &rq, uint32_t taddr, int64_t p,
+                                                 int64_t qc) {
+    uint32_t rr[32];
+    ptx::tmem_ld_32x32b_x32(taddr, rr);
+    ptx::tmem_ld_wait();
+    int32_t v[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) v[j] = (int32_t)rr[j];
+    ts_epilogue_values(ta, rq, v, p, qc);
+}
+
+// split-K partial tile: this split's accumulators go to its own slice ws_acc[ks][np][nq]; each
+// lane writes whole 128-byte row segments (measured: scattered int32 atomics into one shared
+// partial, or a last-arriver reduction by the 32-lane quarter that owns the rows, both cost more
+// than the split saved — the reduction is latency-bound per lane; a separate grid-wide reduce
+// kernel is one round trip)
+__device__ __noinline__ void ts_epilogue_splitk(const TsArgs &ta, uint32_t trow, int nch, int64_t p, int64_t q0, int ks,
+                                                int lane, uint32_t acc_bar) {
+    const bool vec = (ta.nq & 3) == 0;
+    int32_t *row = ta.ws_acc + ks * ta.np * ta.nq + p * ta.nq;
+    for (int c = 0; c < nch; ++c) {
+        uint32_t rr[32];
+        ptx::tmem_ld_32x32b_x32(trow + c * 32, rr);
+        ptx::tmem_ld_wait();
+        if (c == nch - 1) {   // the accumulator buffer is free again
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(acc_bar);
+        }
+        const int64_t qc = q0 + c * 32;
+        if (p >= ta.np || qc >= ta.nq) continue;
+        if (vec && qc + 32 <= ta.nq) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+                __stcg(reinterpret_cast<int4 *>(row + qc + j),
+                       make_int4((int32_t)rr[j], (int32_t)rr[j + 1], (int32_t)rr[j + 2], (int32_t)rr[j + 3]));
+        } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+                if (qc + j < ta.nq) __stcg(row + qc + j, (int32_t)rr[j]);
+        }
+    }
+}
+
+// split-K reduction: one thread per (row p, 4 consecutive columns): sum the sk <= 8 slices (all
+// loads in flight at once), then requantise to one byte of codes (4 columns, LSB first; columns
+// past nq give zero bits, as the fused epilogue writes them) or store the int32 sums.
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const int32_t *__restrict__ ws, int64_t np, int64_t nq,
+                                                            int32_t sk, void *D, int64_t ldd, int32_t has_rq,
+                                                            RequantArgs rq) {
+    ptx::griddep_wait();   // the split-K GEMM's slices are complete and visible
+    const int64_t ng = (nq + 3) >> 2, n = np * ng, slice = np * nq;
+    const bool vec = (nq & 3) == 0;
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t p = i / ng, q = (i - p * ng) * 4;
+        const int32_t *src = ws + p * nq + q;
+        int32_t v[4] = {0, 0, 0, 0};
+        if (vec) {
+            int4 t[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) t[k] = k < sk ? __ldcg(reinterpret_cast<const int4 *>(src + k * slice)) : make_int4(0, 0, 0, 0);
+#pragma unroll
+            for (int k = 0; k < 8; ++k) { v[0] += t[k].x; v[1] += t[k].y; v[2] += t[k].z; v[3] += t[k].w; }
+        } else {
+            for (int k = 0; k < sk; ++k)
+#pragma unroll
+                for (int j = 0; j < 4; ++j)
+                    if (q + j < nq) v[j] += __ldcg(src + k * slice + j);
+        }
+        if (!has_rq) {
+            int32_t *dp = reinterpret_cast<int32_t *>(D) + p * ldd + q;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (q + j < nq) dp[j] = v[j];
+        } else {
+            uint32_t b = 0;
+#pragma unroll
+            for (int j = 0; j < 4; ++j)
+                if (q + j < nq) b |= requant_one(rq, v[j], p, q + j) << (2 * j);
+            reinterpret_cast<uint8_t *>(D)[p * ldd + (q >> 2)] = (uint8_t)b;
+        }
+    }
+}
+
+// 16-bit SIMD requant of one tile (S7): RES = 0 no residual, 1 identity shortcut over packed
+// codes (pair table in smem), 2 int32 residual (exact redo of a chunk where |r| >= 2^14).  The
+// residual forms are compiled out of the RES = 0 instance (they cost registers / spills there).
+template <int BN, int RES>
+__device__ __forceinline__ void epi16_tile(const TsArgs &ta, const RequantArgs &rq, uint32_t trow, int64_t p, int64_t q0,
+                                           uint32_t na_row, uint32_t tab, int lane, uint32_t acc_bar) {
+    constexpr int NCH = BN / 32;
+    // all of the tile's accumulators (up to 128 columns as 16-bit pairs) are loaded
+    // before any requant work, so the TMEM buffer goes back to the MMA as early as
+    // possible (the accumulator ring is only NACC = 2 deep for 128-column tiles)
+    constexpr int NLD = NCH / 2 < 2 ? NCH / 2 : 2;   // 64-column loads held in registers
+#pragma unroll 1
+    for (int c0 = 0; c0 < NCH; c0 += 2 * NLD) {
+        uint32_t r16[NLD][32];
+#pragma unroll
+        for (int l = 0; l < NLD; ++l) ptx::tmem_ld_32x32b_x32_pack16(trow + (c0 + 2 * l) * 32, r16[l]);
+        ptx::tmem_ld_wait();
+        if (c0 + 2 * NLD >= NCH && RES != 2) {   // (int32 residual: kept for an exact redo)
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(acc_bar);
+        }
+#pragma unroll
+        for (int hh = 0; hh < 2 * NLD; ++hh) {
+            const int64_t qc = q0 + (c0 + hh) * 32;
+            uint32_t na[16];
+            if (ta.f16_tab) {
+                const uint32_t ta4 = tab + (uint32_t)(qc >> 1) * 4u;
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    const uint4 t4 = ptx::lds128(ta4 + 16 * j);
+                    na[4 * j] = t4.x; na[4 * j + 1] = t4.y; na[4 * j + 2] = t4.z; na[4 * j + 3] = t4.w;
+                }
+            } else {
+#pragma unroll
+                for (int j = 0; j < 16; ++j) na[j] = na_row;
+            }
+            uint32_t rr[16];
+#pragma unroll
+            for (int j = 0; j < 16; ++j) rr[j] = r16[hh >> 1][16 * (hh & 1) + j];
+            if constexpr (RES == 1) {   // identity shortcut: pair residuals from the packed codes
+                const uint2 rc = p < ta.np ? *reinterpret_cast<const uint2 *>(rq.res_codes + p * rq.ld_res_codes + (qc >> 2))
+                                           : make_uint2(0, 0);
+                const uint32_t rt = tab + 4u * (TAB_PAIRS - 16);
+#pragma unroll
+                for (int j = 0; j < 16; ++j) {
+                    uint32_t rp;
+                    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(rp) : "r"(rt + 4u * (((j < 8 ? rc.x : rc.y) >> (4 * (j & 7))) & 15u)));
+                    rr[j] = __vadd2(rr[j], rp);
+                }
+            } else if constexpr (RES == 2) {   // int32 residual -> 16-bit pairs (|r| < 2^14 checked)
+                uint32_t bad = 0;
+                if (p < ta.np) {
+                    const int4 *rp = reinterpret_cast<const int4 *>(rq.res + p * rq.ld_res + qc);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) {
+                        const int4 v = __ldg(rp + j);
+                        bad |= (uint32_t)(v.x + 16384) | (uint32_t)(v.y + 16384) | (uint32_t)(v.z + 16384) | (uint32_t)(v.w + 16384);
+                        rr[2 * j] = __vadd2(rr[2 * j], prmt_b32((uint32_t)v.x, (uint32_t)v.y, 0x5410u));
+                        rr[2 * j + 1] = __vadd2(rr[2 * j + 1], prmt_b32((uint32_t)v.z, (uint32_t)v.w, 0x5410u));
+                    }
+                }
+                if (__any_sync(0xFFFFFFFFu, (bad >> 15) != 0u)) {   // exact redo of this chunk (TMEM still held)
+                    ts_epilogue_general(ta, rq, trow + (uint32_t)((c0 + hh) * 32), p, qc);
+                    continue;
+                }
+            }
+            if (p >= ta.np) continue;
+            const uint2 o = requant16_32(rr, na, ta.f16_w2, ta.f16_m, ta.f16_c2);
+            uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
+            if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = o;
+            else store_codes32_ts(dp, o.x, o.y, 8);
+        }
+    }
+    if constexpr (RES == 2) {
+        ptx::tc_fence_before();
+        __syncwarp();
+        if (lane == 0) ptx::mbar_arrive(acc_bar);
+    }
+}
+
+// Epilogue tile loop for the launch-uniform rare modes — split-K partial tiles, and 16-bit
+// requant with a residual — kept out of line: inlined, their code raised register pressure in the
+// common loop past the 128-register cap and its spills cost ~40% on short-K layers (measured).
+template <int BN, int NACC, int EG, bool WIN>
+__device__ __noinline__ void epilogue_loop_rare(const TsArgs &ta, const RequantArgs &rq, uint32_t tmem, uint32_t tab,
+                                                uint32_t acc_bar0, int ntiles, int warp, int lane, bool f16_ok) {
+    constexpr int NCH = BN / 32;
+    const int quarter = warp & 3, eg = warp >> 2;
+    uint32_t tl = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        if (EG > 1 && (int)(tl % EG) != eg) continue;
+        const uint32_t acc = tl % NACC;
+        const uint32_t acc_full = acc_bar0 + 8 * acc, acc_empty = acc_bar0 + 8 * (NACC + acc);
+        int tp, tq, sb_, se_;
+        work_item<true>(ta, t, tp, tq, sb_, se_);
+        const int64_t p = (int64_t)tp * BM + quarter * 32 + lane;
+        const int64_t q0 = (int64_t)tq * BN;
+        ptx::mbar_wait(acc_full, (tl / NACC) & 1u);
+        ptx::tc_fence_after();
+        const uint32_t trow = tmem + acc * BN + ((uint32_t)(quarter * 32) << 16);
+        if (ta.sk > 1) {
+            ts_epilogue_splitk(ta, trow, NCH, p, q0, (int)(t - (int)fdiv((uint32_t)t, ta.fd_sk) * ta.sk), lane, acc_empty);
+            continue;
+        }
+        // residual in the 16-bit path (every lane's row offset must fit int16 for bias_axis 1)
+        bool use16 = f16_ok && q0 + BN <= ta.nq;
+        uint32_t na_row = ta.f16_na2;
+        if (use16 && !ta.f16_tab && rq.bias && rq.bias_axis == 1) {
+            const int64_t n = (int64_t)(p < ta.np ? __ldg(rq.bias + p) : 0) - ta.f16_thr0m1;
+            na_row = ((uint32_t)n & 0xFFFFu) * 0x10001u;
+            use16 = __all_sync(0xFFFFFFFFu, (n < 0 ? -n : n) + ta.f16_accmax <= 32767);
+        }
+        if (use16 && ta.f16_res == 1) {
+            epi16_tile<BN, 1>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
+        } else if (use16 && ta.f16_res == 2) {
+            epi16_tile<BN, 2>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
+        } else {
+#pragma unroll 1
+            for (int c = 0; c < NCH; ++c) ts_epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
+            ptx::tc_fence_before();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(acc_empty);
+        }
+    }
+}
+
+template <int BN, int NEPI, int NUNP, int KST, bool WIN, bool ASM, bool SK>
 __global__ void __launch_bounds__(Roles<NEPI, NUNP>::NT, 1)
 lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
@@ -320,7 +562,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + C::OFF_TMEM);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntiles = ta.ntp * ta.ntq;
+    const int ntiles = ta.nwork;   // work items (split-K: sk per output tile; a param-space operand, never spilled)
     const int nsub = (ta.pks * 4 + KST - 1) / KST;   // stages per packed slot
 
     if (warp == PRODUCER_WARP) {
@@ -383,11 +625,11 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             ptx::griddep_wait();
         }
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            int tp, tq;
-            tile_coords(ta, t, tp, tq);
+            int tp, tq, sb, se;
+            work_item<SK>(ta, t, tp, tq, sb, se);
             const int64_t p0 = (int64_t)tp * BM, q0 = (int64_t)tq * BN;
             int sub = 0, ps = 0;
-            for (int s = 0; s < ta.nstages; ++s, ++gb) {
+            for (int s = sb; s < se; ++s, ++gb) {
                 if (sub == 0 && !ta.implicit && !WIN) {   // next packed P slot (up to 512 codes of every row)
                     const int slot = (int)pslot_i;
                     if (lane == 0) TS_EV(13, gb);
@@ -402,7 +644,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                             ptx::bulk_load(dst, ta.P + p0 * ta.ldp, bytes, full_p(slot));
                         } else {
                             ptx::mbar_arrive_expect_tx(full_p(slot), pslot);
-                            ptx::tma_load_2d(dst, &tm_p, full_p(slot), ps * ta.pks, (int32_t)p0);
+                            ptx::tma_load_2d(dst, &tm_p, full_p(slot), sb * (KST / 4) + ps * ta.pks, (int32_t)p0);
                         }
                         TS_EV(12, gb);
                     }
@@ -434,13 +676,13 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             ptx::mbar_wait(acc_empty(tl % NACC), ((tl / NACC) & 1u) ^ 1u);
-            int tp, tq;
-            tile_coords(ta, t, tp, tq);
+            int tp, tq, sb, se;
+            work_item<SK>(ta, t, tp, tq, sb, se);
             if (WIN) ptx::mbar_wait(full_a(tl % ta.nwin), (tl / ta.nwin) & 1u);   // the tile's window
             if (WIN && lane == 0) TS_EV(13, tl);
-            for (int s = 0; s < ta.nstages; ++s, ++g) {
+            for (int s = sb; s < se; ++s, ++g) {
                 const int sa = g % SA;
-                if (lane == 0 && s == 0) TS_EV(3, tl);
+                if (lane == 0 && s == sb) TS_EV(3, tl);
                 if (!WIN) ptx::mbar_wait(full_a(sa), (g / SA) & 1u);
                 if (lane == 0) TS_EV(4, g);
                 if (!ta.bres) ptx::mbar_wait(full_b(g % SB), (g / SB) & 1u);
@@ -457,11 +699,11 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl % NACC;
             const uint32_t dt = tmem + acc * BN;
-            int tp, tq;
-            tile_coords(ta, t, tp, tq);
-            for (int s = 0; s < ta.nstages; ++s, ++g) {
+            int tp, tq, sb, se;
+            work_item<SK>(ta, t, tp, tq, sb, se);
+            for (int s = sb; s < se; ++s, ++g) {
                 const int sa = g % SA;
-                const int sb = ta.bres ? tq * ta.nstages + s : (int)(g % SB);
+                const int bsl = ta.bres ? tq * ta.nstages + s : (int)(g % SB);   // B smem stage
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
                 ptx::tc_fence_after();
                 if (lane == 0 && WIN) {
@@ -470,7 +712,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     // the per-k-step start offsets come precomputed from the host (ta.koff)
                     const uint32_t wbase = sbase + C::OFF_P + (uint32_t)(2 * ta.wslot + (int)(tl % ta.nwin) * ta.wbytes);
                     const uint64_t ad = ptx::desc_k_none(wbase, (uint32_t)ta.lbo);
-                    const uint64_t bd = bdesc0 + (uint64_t)((sb * C::B_BYTES) >> 4);
+                    const uint64_t bd = bdesc0 + (uint64_t)((bsl * C::B_BYTES) >> 4);
                     const int j0 = s * C::KSTEPS;
                     // all offsets into registers first: a parameter load between two tcgen05.mma
                     // (asm with a memory clobber) serialises the issue (~150 cycles per MMA measured)
@@ -481,40 +723,40 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 #pragma unroll
                         for (int k = 0; k < C::KSTEPS; ++k)
                             ptx::mma_i8_ss(dt, ad + ko[k], bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
-                                           idesc, (s > 0 || k > 0) ? 1u : 0u);
+                                           idesc, (s > sb || k > 0) ? 1u : 0u);
                     } else {
 #pragma unroll
                         for (int k = 0; k < C::KSTEPS; ++k)
                             if (k < ta.last_ksteps)
                                 ptx::mma_i8_ss(dt, ad + ko[k], bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
-                                               idesc, (s > 0 || k > 0) ? 1u : 0u);
+                                               idesc, (s > sb || k > 0) ? 1u : 0u);
                     }
-                    if (!ta.bres) ptx::mma_commit(empty_b(sb));
-                    if (s == ta.nstages - 1) {
+                    if (!ta.bres) ptx::mma_commit(empty_b(bsl));
+                    if (s == se - 1) {
                         ptx::mma_commit(empty_a(tl % ta.nwin));   // the window is free again
                         ptx::mma_commit(acc_full(acc));
                     }
                     TS_EV(15, g);
                 } else if (lane == 0 && ASM) {
                     const uint64_t ad = ptx::desc_k_none(sbase + C::OFF_A + (uint32_t)(sa * C::A_STAGE), BM * 16);
-                    const uint64_t bd = bdesc0 + (uint64_t)((sb * C::B_BYTES) >> 4);
+                    const uint64_t bd = bdesc0 + (uint64_t)((bsl * C::B_BYTES) >> 4);
                     // k-step k: A K-chunks 2k, 2k+1 (+2k * BM*16 bytes), B atom k/4, +32 B per k-step inside
                     if (s < ta.nstages - 1 || ta.last_ksteps == C::KSTEPS) {
 #pragma unroll
                         for (int k = 0; k < C::KSTEPS; ++k)
                             ptx::mma_i8_ss(dt, ad + (uint64_t)((2 * k * BM * 16) >> 4), bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
-                                           idesc, (s > 0 || k > 0) ? 1u : 0u);
+                                           idesc, (s > sb || k > 0) ? 1u : 0u);
                     } else {
                         for (int k = 0; k < ta.last_ksteps; ++k)
                             ptx::mma_i8_ss(dt, ad + (uint64_t)((2 * k * BM * 16) >> 4), bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
-                                           idesc, (s > 0 || k > 0) ? 1u : 0u);
+                                           idesc, (s > sb || k > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(empty_a(sa));
-                    if (!ta.bres) ptx::mma_commit(empty_b(sb));
-                    if (s == ta.nstages - 1) ptx::mma_commit(acc_full(acc));
+                    if (!ta.bres) ptx::mma_commit(empty_b(bsl));
+                    if (s == se - 1) ptx::mma_commit(acc_full(acc));
                 } else if (lane == 0) {
                     const uint32_t at = tmem + C::TMEM_A0 + sa * C::ACOLS;
-                    const uint64_t bd = bdesc0 + (uint64_t)((sb * C::B_BYTES) >> 4);
+                    const uint64_t bd = bdesc0 + (uint64_t)((bsl * C::B_BYTES) >> 4);
                     // k-step k: A columns 8k, B atom k/4 (+B_ATOM bytes), 32 bytes (+2) per k-step inside
 #ifdef DG_EXP_NOMMA
                     if (false) {} else
@@ -523,15 +765,15 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 #pragma unroll
                         for (int k = 0; k < C::KSTEPS; ++k)
                             ptx::mma_i8_ts(dt, at + 8 * k, bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3), idesc,
-                                           (s > 0 || k > 0) ? 1u : 0u);
+                                           (s > sb || k > 0) ? 1u : 0u);
                     } else {
                         for (int k = 0; k < ta.last_ksteps; ++k)
                             ptx::mma_i8_ts(dt, at + 8 * k, bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3), idesc,
-                                           (s > 0 || k > 0) ? 1u : 0u);
+                                           (s > sb || k > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit(empty_a(sa));
-                    if (!ta.bres) ptx::mma_commit(empty_b(sb));
-                    if (s == ta.nstages - 1) ptx::mma_commit(acc_full(acc));
+                    if (!ta.bres) ptx::mma_commit(empty_b(bsl));
+                    if (s == se - 1) ptx::mma_commit(acc_full(acc));
                 }
                 __syncwarp();
             }
@@ -618,7 +860,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         // implicit conv: group-private ring of IG_DEPTH stages (64 bytes per row each)
         constexpr int IG_DEPTH = C::P_REGION / (NUM_UGROUPS * BM * 64);
         const uint32_t ring = sbase + C::OFF_P + (uint32_t)(grp * IG_DEPTH * BM * 64) + (uint32_t)(r * 64);
-        GatherCursor gc{blockIdx.x, grp, ta.X, 0, 0};
+        GatherCursor<SK> gc{(int)blockIdx.x, 0, ta.X, 0, 0, 0};
         uint32_t consumed = 0;
         if (KST == 128 && ta.nstages == 1 && !ta.implicit) {
             // one-stage tiles (K <= 128): a group unpacks two of its tiles per round of mbarrier
@@ -690,20 +932,26 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
         } else {
         if (ta.implicit) {
-            gc.advance(ta, 0, r, ntiles);
-            if (gc.t < ntiles) gc.pixel(ta, r);
+            if (gc.t < ntiles) {   // first work item: start at its first stage, then this group's offset
+                gc.pixel(ta, r);
+                int tp, tq, sb, se2;
+                work_item<SK>(ta, gc.t, tp, tq, sb, se2);
+                gc.s = sb;
+            }
+            gc.advance(ta, grp, r, ntiles);
             for (int i = 0; i < IG_DEPTH; ++i) {
                 gc.issue<2 * C::HALVES>(ta, ring + (uint32_t)(i * BM * 64), r, ntiles, KST / 4);
                 gc.advance(ta, NUM_UGROUPS, r, ntiles);
             }
         }
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
-            int sub = 0;
-            for (int s = 0; s < ta.nstages; ++s, ++g) {
+            int sub = 0, tp_, tq_, sb, se;
+            work_item<SK>(ta, t, tp_, tq_, sb, se);
+            for (int s = sb; s < se; ++s, ++g) {
                 const int slot = (int)pslot_i;
                 const uint32_t ph = pphase;
                 const int sub_ = sub;
-                const bool last_in_slot = (sub == nsub - 1) || (s == ta.nstages - 1);
+                const bool last_in_slot = (sub == nsub - 1) || (s == se - 1);
                 if (last_in_slot) {
                     sub = 0;
                     if (++pslot_i == (uint32_t)nsp) { pslot_i = 0; pphase ^= 1u; }
@@ -735,7 +983,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     }
                     __syncwarp();
                     if (lane == 0)   // this warp's share of the slot is consumed (+ the slot's unused stages)
-                        ptx::mbar_arrive_cnt(empty_p(slot), 1u + (s == ta.nstages - 1 ? (uint32_t)(nsub - 1 - sub_) : 0u));
+                        ptx::mbar_arrive_cnt(empty_p(slot), 1u + (s == se - 1 ? (uint32_t)(nsub - 1 - sub_) : 0u));
                 }
                 // unpack the whole stage into registers before waiting for the A buffer, so that the
                 // wait overlaps the ALU work (a[32 h + j]: 32-column half h)
@@ -814,6 +1062,10 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         if (ta.f16 && (ta.f16_tab || ta.f16_res == 1)) ptx::named_bar_sync(EPI_BAR, NEPI * 32);
         const bool f16_ok = ta.f16 && *f16_flag == 0u;
         ptx::griddep_wait();
+        if (!WIN && ((SK && ta.sk > 1) || ta.f16_res)) {
+            epilogue_loop_rare<BN, NACC, EG, WIN>(ta, rq, tmem, sbase + C::OFF_TAB, acc_full(0), ntiles, warp - EPI_WARP0,
+                                                  lane, f16_ok);
+        } else {
         const int quarter = warp & 3, eg = (warp - EPI_WARP0) >> 2, half = 0;
         const bool col_bias = rq.bias && rq.bias_axis == 0;
         uint32_t tl = 0;
@@ -840,7 +1092,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             if (lane == 0 && quarter == 0) TS_EV(9, tl);
             ptx::tc_fence_after();
             const uint32_t trow = tmem + acc * BN + half * HALF + ((uint32_t)(quarter * 32) << 16);
-            const bool fast = (ta.fast_rq || ta.f16_res) && q0 + HALF <= ta.nq;
+            const bool fast = ta.fast_rq && q0 + HALF <= ta.nq;
             const int32_t rb = (fast && rq.bias && rq.bias_axis == 1 && p < ta.np) ? __ldg(rq.bias + p) : 0;
             // 16-bit SIMD path (warp-uniform): per-row offsets need every lane's row in range
             bool use16 = fast && f16_ok;
@@ -859,79 +1111,8 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 use16 = __all_sync(0xFFFFFFFFu, (n < 0 ? -n : n) + ta.f16_accmax <= 32767);
             }
             if (use16) {
-                // all of the tile's accumulators (up to 128 columns as 16-bit pairs) are loaded
-                // before any requant work, so the TMEM buffer goes back to the MMA as early as
-                // possible (the accumulator ring is only NACC = 2 deep for 128-column tiles)
-                constexpr int NLD = NCH / 2 < 2 ? NCH / 2 : 2;   // 64-column loads held in registers
-#pragma unroll 1
-                for (int c0 = 0; c0 < NCH; c0 += 2 * NLD) {
-                    uint32_t r16[NLD][32];
-#pragma unroll
-                    for (int l = 0; l < NLD; ++l) ptx::tmem_ld_32x32b_x32_pack16(trow + (c0 + 2 * l) * 32, r16[l]);
-                    ptx::tmem_ld_wait();
-                    if (c0 + 2 * NLD >= NCH && ta.f16_res != 2) {   // (int32 residual: kept for an exact redo)
-                        ptx::tc_fence_before();
-                        __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
-                    }
-#pragma unroll
-                    for (int hh = 0; hh < 2 * NLD; ++hh) {
-                        const int64_t qc = q0 + (c0 + hh) * 32;
-                        uint32_t na[16];
-                        if (ta.f16_tab) {
-                            const uint32_t ta4 = sbase + C::OFF_TAB + (uint32_t)(qc >> 1) * 4u;
-#pragma unroll
-                            for (int j = 0; j < 4; ++j) {
-                                const uint4 t4 = ptx::lds128(ta4 + 16 * j);
-                                na[4 * j] = t4.x; na[4 * j + 1] = t4.y; na[4 * j + 2] = t4.z; na[4 * j + 3] = t4.w;
-                            }
-                        } else {
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) na[j] = na_row;
-                        }
-                        uint32_t rr[16];
-#pragma unroll
-                        for (int j = 0; j < 16; ++j) rr[j] = r16[hh >> 1][16 * (hh & 1) + j];
-                        if (ta.f16_res == 1) {   // identity shortcut: pair residuals from the packed codes
-                            const uint2 rc = p < ta.np ? *reinterpret_cast<const uint2 *>(rq.res_codes + p * rq.ld_res_codes + (qc >> 2))
-                                                       : make_uint2(0, 0);
-                            const uint32_t rt = sbase + C::OFF_TAB + 4u * (TAB_PAIRS - 16);
-#pragma unroll
-                            for (int j = 0; j < 16; ++j) {
-                                uint32_t rp;
-                                asm volatile("ld.shared.u32 %0, [%1];" : "=r"(rp) : "r"(rt + 4u * (((j < 8 ? rc.x : rc.y) >> (4 * (j & 7))) & 15u)));
-                                rr[j] = __vadd2(rr[j], rp);
-                            }
-                        } else if (ta.f16_res == 2) {   // int32 residual -> 16-bit pairs (|r| < 2^14 checked)
-                            uint32_t bad = 0;
-                            if (p < ta.np) {
-                                const int4 *rp = reinterpret_cast<const int4 *>(rq.res + p * rq.ld_res + qc);
-#pragma unroll
-                                for (int j = 0; j < 8; ++j) {
-                                    const int4 v = __ldg(rp + j);
-                                    bad |= (uint32_t)(v.x + 16384) | (uint32_t)(v.y + 16384) | (uint32_t)(v.z + 16384) | (uint32_t)(v.w + 16384);
-                                    rr[2 * j] = __vadd2(rr[2 * j], prmt_b32((uint32_t)v.x, (uint32_t)v.y, 0x5410u));
-                                    rr[2 * j + 1] = __vadd2(rr[2 * j + 1], prmt_b32((uint32_t)v.z, (uint32_t)v.w, 0x5410u));
-                                }
-                            }
-                            if (__any_sync(0xFFFFFFFFu, (bad >> 15) != 0u)) {   // exact redo of this chunk (TMEM still held)
-                                ts_epilogue_general(ta, rq, trow + (uint32_t)((c0 + hh) * 32), p, qc);
-                                continue;
-                            }
-                        }
-                        if (p >= ta.np) continue;
-                        const uint2 o = requant16_32(rr, na, ta.f16_w2, ta.f16_m, ta.f16_c2);
-                        uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
-                        if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = o;
-                        else store_codes32_ts(dp, o.x, o.y, 8);
-                    }
-                }
-                if (ta.f16_res == 2) {
-                    ptx::tc_fence_before();
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
-                }
-            } else if (!fast || !ta.fast_rq) {   // (residuals outside the 16-bit path: exact general path)
+                epi16_tile<BN, 0>(ta, rq, trow, p, q0, na_row, sbase + C::OFF_TAB, lane, acc_empty(acc));
+            } else if (!fast) {
 #pragma unroll 1
                 for (int c = 0; c < NCH; ++c) ts_epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
                 ptx::tc_fence_before();
@@ -986,6 +1167,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
             if (lane == 0 && quarter == 0) TS_EV(10, tl);
         }
+        }   // common modes
     }
 
     ptx::tc_fence_before();
@@ -1118,10 +1300,10 @@ bool f16_params(int64_t t0, int64_t t1, int64_t t2, uint32_t &m_out, uint32_t &c
     return false;
 }
 
-template <int BN, int NEPI, int NUNP, int KST, bool WIN = false, bool ASM = false>
+template <int BN, int NEPI, int NUNP, int KST, bool WIN = false, bool ASM = false, bool SK = false>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
-                    cudaStream_t st, const TsConv *cv) {
+                    cudaStream_t st, const TsConv *cv, void *skws = nullptr, size_t skws_bytes = 0) {
     using C = TsCfg<BN, NEPI / 4, KST, WIN, ASM>;
     int64_t acc_bound = 0;   // K * max |pl[a] * ql[b]|
     for (int a = 0; a < 4; ++a)
@@ -1219,7 +1401,8 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
             ta.f16_thr0m1 = (int32_t)thr0m1;
             ta.f16_accmax = (int32_t)(acc_bound + res_bound);
             ta.f16 = 1;
-            if (rq->res_codes) {
+            if (WIN) {   // (the out-of-line residual loop has no padded-window row map)
+            } else if (rq->res_codes) {
                 ta.f16_res = 1;
                 for (int i = 0; i < 16; ++i) {
                     const int32_t r0 = rq->res_levels[i & 3] * rq->res_mult, r1 = rq->res_levels[i >> 2] * rq->res_mult;
@@ -1258,14 +1441,29 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     if (!make_map_sw128(&mb, Q8, ld8, nq, BN, 128)) return DG_ERR_CUDA;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
+        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
             cudaSuccess)
             return DG_ERR_CUDA;
         attr_set = true;
     }
+    // split-K when the output tiles cannot fill the GPU and K is long (workspace for the slices given)
+    ta.sk = 1;
+    const int64_t otiles = (int64_t)ta.ntp * ta.ntq;
+    if (SK && !ta.bulk && skws && otiles * 2 <= num_sms() && ta.nstages >= 4) {
+        int64_t sk = num_sms() / otiles;
+        sk = sk < ta.nstages / 2 ? sk : ta.nstages / 2;
+        sk = sk < 8 ? sk : 8;
+        const size_t need = (size_t)(sk * np * nq * 4);
+        if (sk >= 2 && need <= skws_bytes) {
+            ta.sk = (int32_t)sk;
+            ta.fd_sk = make_fastdiv((uint32_t)sk);
+            ta.ws_acc = reinterpret_cast<int32_t *>(skws);
+        }
+    }
     RequantArgs dummy{};
-    const int64_t ntiles = (int64_t)ta.ntp * ta.ntq;
+    const int64_t ntiles = otiles * ta.sk;
     if (ntiles > INT32_MAX) return DG_ERR_SHAPE;
+    ta.nwork = (int32_t)ntiles;
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
     const RequantArgs rqv = rq ? *rq : dummy;
     cudaLaunchConfig_t lc = {};
@@ -1278,8 +1476,19 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     la[0].val.programmaticStreamSerializationAllowed = getenv("DG_NO_PDL") ? 0 : 1;
     lc.attrs = la;
     lc.numAttrs = 1;
-    if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM>, mp, mb, ta, rqv) != cudaSuccess)
+    if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK>, mp, mb, ta, rqv) != cudaSuccess)
         return DG_ERR_CUDA;
+    if (ta.sk > 1) {
+        const int64_t thr = np * ((nq + 3) >> 2);
+        int64_t blocks = (thr + 255) / 256;
+        if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
+        lc.gridDim = dim3((unsigned)blocks);
+        lc.blockDim = dim3(256);
+        lc.dynamicSmemBytes = 0;
+        if (cudaLaunchKernelEx(&lc, splitk_reduce_kernel, (const int32_t *)ta.ws_acc, np, nq, ta.sk, D, ldd,
+                               (int32_t)(rq != nullptr), rqv) != cudaSuccess)
+            return DG_ERR_CUDA;
+    }
     return launch_status();
 }
 
@@ -1300,7 +1509,7 @@ dg_status expand_operand(const uint8_t *packed, int64_t rows, int64_t K, int64_t
 
 dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                       const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
-                      cudaStream_t st, const TsConv *cv) {
+                      cudaStream_t st, const TsConv *cv, void *skws, size_t skws_bytes) {
     if (np > ((int64_t)1 << 31) - 1 || nq > ((int64_t)1 << 31) - 1) return DG_ERR_SHAPE;
     // direct 3x3 / stride 1 / pad 1 convs with C = 64, 128, 256: shifted-window kernel (DG_WIN=1; it
     // unpacks each input pixel once per tile instead of once per tap, but measured no faster than
@@ -1315,6 +1524,11 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     // Stages of 256 codes (8 MMAs per hand-off) except where K <= 128 or BN = 256 (whose 128-code
     // stages already carry 512 MMA cycles).
     const bool short_k = K <= 2 * KA;
+    // split-K candidates (few output tiles, K of >= 4 stages, workspace given): the SK instances
+    static const bool no_sk = getenv("DG_NO_SPLITK") != nullptr;
+    auto few = [&](int64_t bn) {
+        return skws && !no_sk && !short_k && ((np + BM - 1) / BM) * ((nq + bn - 1) / bn) * 2 <= num_sms();
+    };
     const bool k256 = K > KA && !getenv("DG_TS_K128");
     // short K, wide output: 128x256 tiles with the A operand in shared memory and two TMEM accumulators
     // (measured: narrower ASM tiles with 128-code stages lose to the TMEM-A kernel at K = 256)
@@ -1327,16 +1541,23 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     static const int64_t bn256_k = getenv("DG_BN256_K") ? atoll(getenv("DG_BN256_K")) : 4 * KA;
     const int64_t tiles256 = ((np + BM - 1) / BM) * ((nq + 255) / 256);
     if (nq >= 256 && K >= bn256_k && (tiles256 >= num_sms() || K >= 24 * KA) && !getenv("DG_TS_NO_BN256"))
-        return launch_ts<256, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        return few(256) ? launch_ts<256, 4, 8, 128, false, false, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv, skws, skws_bytes)
+                        : launch_ts<256, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 
     if (nq > 64 && !(short_k && getenv("DG_BN64_SHORT"))) {
         if (short_k && !k256) return launch_ts<128, 8, 4, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         if (short_k) return launch_ts<128, 8, 4, 256>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (few(128))
+            return !k256 ? launch_ts<128, 4, 8, 128, false, false, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv, skws, skws_bytes)
+                         : launch_ts<128, 4, 8, 256, false, false, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv, skws, skws_bytes);
         if (!k256) return launch_ts<128, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         return launch_ts<128, 4, 8, 256>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     }
     if (short_k && !k256) return launch_ts<64, 8, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     if (short_k) return launch_ts<64, 8, 8, 256>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    if (few(64))
+        return !k256 ? launch_ts<64, 4, 8, 128, false, false, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv, skws, skws_bytes)
+                     : launch_ts<64, 4, 8, 256, false, false, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv, skws, skws_bytes);
     if (!k256) return launch_ts<64, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     return launch_ts<64, 4, 8, 256>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 }

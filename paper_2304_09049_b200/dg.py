@@ -309,7 +309,7 @@ def lut_conv2d(x: torch.Tensor, w: torch.Tensor, lut: dg_lut, p: dg_conv_params,
                else torch.empty((rows, p.Cout), dtype=torch.int32, device=x.device))
     need = conv_workspace_size(p)
     if ws is None and need > 0:
-        ws = torch.empty(need, dtype=torch.uint8, device=x.device)
+        ws = torch.zeros(need, dtype=torch.uint8, device=x.device)
     r = rq.c() if rq is not None else None
     _check(lib().dg_lut_conv2d(_ptr(x), _ptr(w), ctypes.byref(lut), ctypes.byref(p),
                                ctypes.byref(r) if r is not None else None, _ptr(out), _ptr(ws),

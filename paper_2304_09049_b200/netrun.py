@@ -129,7 +129,7 @@ class NetRunner:
             ws_need = max(ws_need, dg.conv_workspace_size(params), (0 if direct else rows * plan.cols_ld),
                           dg.gemm_workspace_size(L.cout, K))
             self.plans.append(plan)
-        self.ws = torch.empty(max(ws_need, 16), dtype=torch.uint8, device=device)
+        self.ws = torch.zeros(max(ws_need, 16), dtype=torch.uint8, device=device)
         self.ws_gemm = self.ws
         self.total_ops = sum(p.ops for p in self.plans)
 
@@ -221,7 +221,7 @@ class ResNet18Runner:
             self.res_mult[li] = rm
             if r is not None:
                 self.bias[li] = torch.full((L.cout,), r.bias, dtype=torch.int32, device=device)
-        self.ws = torch.empty(ws_need, dtype=torch.uint8, device=device)
+        self.ws = torch.zeros(ws_need, dtype=torch.uint8, device=device)
         L0 = self.layers[0]
         self.x0 = pack_nhwc(input_codes(2, 0, L0, list(range(batch)), device))   # stands in for the stem output (Q14)
         self.bufs = []

@@ -483,3 +483,47 @@ def test_conv_residual_16bit_path(C2, res_mult):
     a2 = oracle.conv2d_direct(x, w2, T, 2, 1, 0).reshape(-1, C2)
     exp2 = oracle.requantize(a2, 12000, 20, 0, 0, 3, res=(rd * scale).astype(np.int32))
     assert np.array_equal(oracle_codes_of(out2, exp2.shape[0], C2), exp2)
+
+
+SPLITK_CONVS = [  # B, H, C, Cout, k, stride: few output tiles, long K -> split-K partial sums
+    (1, 14, 256, 256, 3, 1),
+    (1, 7, 512, 512, 3, 1),
+    (1, 14, 256, 512, 1, 2),
+    (2, 7, 128, 64, 3, 1),
+    (1, 7, 256, 70, 3, 1),        # ragged Cout (int32 output only)
+]
+
+
+@pytest.mark.parametrize("B,H,C,Cout,k,stride", SPLITK_CONVS)
+def test_conv_splitk_vs_oracle(B, H, C, Cout, k, stride):
+    """Small-batch convs (ResNet-18 b1 shapes) whose few output tiles run as split-K: each split
+    writes its int32 partial slice into the workspace tail (garbage on entry), the reduce kernel
+    sums them and requantises; int32 output, fused requant and an int32 residual."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    lut = dg.build_lut(WL, AL, 8)
+    T = oracle.build_lut16(WL, AL)
+    g = np.random.default_rng(B * 100 + H + C + Cout + k)
+    pad = k // 2
+    x = g.integers(0, 4, (B, H, H, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, k, k, C), dtype=np.uint8)
+    exp = oracle.conv2d_direct(x, w, T, stride, pad, 0)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    w8 = dg.expand_operand(wp, k * k * Cp, WL)
+    p = dg.conv_params(B, H, H, Cp, Cout, k, k, stride, pad, 0, ldw=wp.shape[1])
+    ws = torch.full((dg.conv_workspace_size(p),), 0xA5, dtype=torch.uint8, device=DEV)
+    out = dg.lut_conv2d_prepared(xp, w8, lut, p, ws=ws)
+    assert np.array_equal(host(out).reshape(exp.shape), exp)
+    if Cout % 4:
+        return
+    bias = g.integers(-50, 50, Cout).astype(np.int32)
+    rq = dg.Requant(mult=30000, shift=20, zp=1, bias=torch.from_numpy(bias).to(DEV), bias_axis=0)
+    outc = dg.lut_conv2d_prepared(xp, w8, lut, p, rq=rq, ws=ws)
+    e2 = exp.reshape(-1, Cout)
+    expc = oracle.requantize(e2, 30000, 20, 1, 0, 3, bias=bias, bias_axis=0)
+    assert np.array_equal(oracle_codes_of(outc, expc.shape[0], Cout), expc)
+    res = g.integers(-3000, 3000, e2.shape).astype(np.int32)
+    outr = dg.lut_conv2d_prepared(xp, w8, lut, p, rq=dg.Requant(mult=20000, shift=20, res=torch.from_numpy(res).to(DEV)), ws=ws)
+    expr = oracle.requantize(e2, 20000, 20, 0, 0, 3, res=res)
+    assert np.array_equal(oracle_codes_of(outr, expr.shape[0], Cout), expr)
