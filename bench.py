@@ -174,9 +174,10 @@ def run_conv(args, ws, rank, local):
     gev = [(torch.cuda.Event(enable_timing=True, external=True), torch.cuda.Event(enable_timing=True, external=True))
            for _ in range(nl)]
     graph = torch.cuda.CUDAGraph()
-    launches_per_step = 0
+    n0 = dg.kernel_launches()   # native counter of libdg launches (each captured launch counts once)
     with torch.cuda.graph(graph):
-        launches_per_step = runner.step(gemm_events=gev)
+        runner.step(gemm_events=gev)
+    launches_per_step = dg.kernel_launches() - n0
     for _ in range(args.warmup):
         graph.replay()
     torch.cuda.synchronize()
@@ -299,14 +300,16 @@ def run_resnet18(args, ws, rank, local):
     """BJ configs[1]: the 19 LUT convs of ResNet-18 at batch 1, chained with int32 residual adds.
     Latency-bound, so the whole chain is one CUDA graph; every rank runs an independent replica
     (replicas only: batch 1 does not shard)."""
-    from paper_2304_09049_b200 import netrun
+    from paper_2304_09049_b200 import dg, netrun
     r = netrun.ResNet18Runner("cuda", variant=args.variant, batch=args.batch or 1)
     for _ in range(max(1, args.warmup)):
         r.step()
     torch.cuda.synchronize()
     graph = torch.cuda.CUDAGraph()
+    n0 = dg.kernel_launches()
     with torch.cuda.graph(graph):
         r.step()
+    launches_per_step = dg.kernel_launches() - n0   # (split-K convs add a reduce kernel)
     for _ in range(args.warmup):
         graph.replay()
     torch.cuda.synchronize()
@@ -332,7 +335,7 @@ def run_resnet18(args, ws, rank, local):
                            "parallelism": f"{ws} independent replicas"},
                 "roofline": {"bound": "latency", "achieved": round(value / ws, 2), "peak": round(pk["i8_burst"], 1),
                              "unit": "TOPS", "frac": round(value / ws / pk["i8_burst"], 5)},
-                "gpu_launches": r.launches() * args.steps, "clocks": clk.summary()}
+                "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary()}
         print(json.dumps(line), flush=True)
 
 
@@ -382,6 +385,7 @@ def run_gemm(args, ws, rank, local):
     t_all = 0.0
     barrier(ws)
     torch.cuda.synchronize()
+    n0 = dg.kernel_launches()
     with ClockSampler(local) as clk:
         for _ in range(args.steps):
             if flush is not None:
@@ -396,6 +400,7 @@ def run_gemm(args, ws, rank, local):
             torch.cuda.synchronize()
             t_comp += e0.elapsed_time(e1)
             t_all += e0.elapsed_time(g1)
+    launches = dg.kernel_launches() - n0
     barrier(ws)
     ms_comp = max_over_ranks(t_comp / args.steps, ws)
     ms_all = max_over_ranks(t_all / args.steps, ws)
@@ -432,7 +437,7 @@ def run_gemm(args, ws, rank, local):
                              "frac_vs_sustained_peak": round(per_gpu / pk["i8_sustained"], 4),
                              "peak_src": pk["src"] + ": int8 = 2 x bf16 burst (kernel timed alone)",
                              "alg_bytes_per_launch": alg_bytes, "traffic": None},
-                "gpu_launches": args.steps, "clocks": clk.summary(), "parity": parity}
+                "gpu_launches": launches, "clocks": clk.summary(), "parity": parity}
         print(json.dumps(line), flush=True)
 
 

@@ -66,6 +66,12 @@ DG_API const char *dg_status_string(dg_status s);
 #define DG_ABI_VERSION 2
 DG_API int32_t dg_abi_version(void);
 
+/* Number of CUDA kernels this library has enqueued since it was loaded (all
+ * entry points, all streams; a launch recorded into a CUDA graph under stream
+ * capture counts once, at capture).  Process-wide, thread-safe; for the
+ * benchmark's launch count (kernels per step = difference across one step). */
+DG_API uint64_t dg_kernel_launches(void);
+
 /* ---------------------------------------------------------------------------
  * S4 — LUT build.  LUT-16 (§3.2): "The values stored in the LUT are all
  * possible results of w·a"; index = weight code concatenated above the

@@ -6,6 +6,11 @@
 
 using namespace dg;
 
+uint64_t &dg::launch_counter() {
+    static uint64_t n = 0;
+    return n;
+}
+
 namespace {
 
 bool fits_bits(int64_t v, int32_t bits) {
@@ -86,6 +91,8 @@ const char *dg_status_string(dg_status s) {
 }
 
 int32_t dg_abi_version(void) { return DG_ABI_VERSION; }
+
+uint64_t dg_kernel_launches(void) { return __atomic_load_n(&dg::launch_counter(), __ATOMIC_RELAXED); }
 
 dg_status dg_build_lut(const int32_t wl[4], const int32_t al[4], int32_t entry_bits, dg_lut *out) {
     if (!wl || !al || !out) return DG_ERR_INVALID_ARG;

@@ -179,8 +179,11 @@ inline RequantArgs to_args(const dg_requant *rq) {
     return a;
 }
 
-inline dg_status launch_status() {
+// process-wide count of kernels enqueued by the library (dg_kernel_launches)
+uint64_t &launch_counter();
+inline dg_status launch_status(int nlaunched = 1) {
     cudaError_t e = cudaGetLastError();
+    if (e == cudaSuccess) __atomic_fetch_add(&launch_counter(), (uint64_t)nlaunched, __ATOMIC_RELAXED);
     return e == cudaSuccess ? DG_OK : DG_ERR_CUDA;
 }
 

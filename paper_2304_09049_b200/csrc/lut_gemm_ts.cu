@@ -1489,7 +1489,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
                                (int32_t)(rq != nullptr), rqv) != cudaSuccess)
             return DG_ERR_CUDA;
     }
-    return launch_status();
+    return launch_status(ta.sk > 1 ? 2 : 1);
 }
 
 }  // namespace

@@ -62,6 +62,7 @@ def lib():
         sig = {
             "dg_status_string": ([i32], ctypes.c_char_p),
             "dg_abi_version": ([], i32),
+            "dg_kernel_launches": ([], ctypes.c_uint64),
             "dg_build_lut": ([P, P, i32, P], i32),
             "dg_lut_from_table": ([P, i32, P], i32),
             "dg_packed_ld": ([i64], i64),
@@ -87,6 +88,11 @@ def lib():
             f.restype = res
         _lib = L
     return _lib
+
+
+def kernel_launches() -> int:
+    """Kernels enqueued by libdg so far (dg_kernel_launches; graph capture counts each once)."""
+    return int(lib().dg_kernel_launches())
 
 
 def _check(status: int, what: str):

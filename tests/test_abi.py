@@ -37,6 +37,7 @@ def test_host_calls_without_gpu():
     from paper_2304_09049_b200 import dg
     L = dg.lib()
     assert L.dg_abi_version() == 2
+    assert isinstance(dg.kernel_launches(), int) and dg.kernel_launches() >= 0
     assert L.dg_status_string(-4) == b"DG_ERR_OVERFLOW"
     lut = dg.build_lut([-2, -1, 0, 1], [0, 1, 2, 3], 8)
     assert lut.is_product == 1

@@ -513,7 +513,10 @@ def test_conv_splitk_vs_oracle(B, H, C, Cout, k, stride):
     w8 = dg.expand_operand(wp, k * k * Cp, WL)
     p = dg.conv_params(B, H, H, Cp, Cout, k, k, stride, pad, 0, ldw=wp.shape[1])
     ws = torch.full((dg.conv_workspace_size(p),), 0xA5, dtype=torch.uint8, device=DEV)
+    n0 = dg.kernel_launches()
     out = dg.lut_conv2d_prepared(xp, w8, lut, p, ws=ws)
+    if k == 3:   # implicit GEMM split over K + the reduce kernel
+        assert dg.kernel_launches() - n0 == 2
     assert np.array_equal(host(out).reshape(exp.shape), exp)
     if Cout % 4:
         return
