@@ -407,7 +407,10 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const int32_t *__res
 // 16-bit SIMD requant of one tile (S7): RES = 0 no residual, 1 identity shortcut over packed
 // codes (pair table in smem), 2 int32 residual (exact redo of a chunk where |r| >= 2^14).  The
 // residual forms are compiled out of the RES = 0 instance (they cost registers / spills there).
-template <int BN, int RES>
+// TAB: per-column offsets from the shared-memory table, else one offset per row (na_row); a
+// runtime branch here made the compiler merge the two na[] arrays with ~64 register moves per
+// 32 columns (measured 8% of the K = 64 layers' instructions).
+template <int BN, int RES, bool TAB>
 __device__ __forceinline__ void epi16_tile(const TsArgs &ta, const RequantArgs &rq, uint32_t trow, int64_t p, int64_t q0,
                                            uint32_t na_row, uint32_t tab, int lane, uint32_t acc_bar) {
     constexpr int NCH = BN / 32;
@@ -430,7 +433,7 @@ __device__ __forceinline__ void epi16_tile(const TsArgs &ta, const RequantArgs &
         for (int hh = 0; hh < 2 * NLD; ++hh) {
             const int64_t qc = q0 + (c0 + hh) * 32;
             uint32_t na[16];
-            if (ta.f16_tab) {
+            if constexpr (TAB) {
                 const uint32_t ta4 = tab + (uint32_t)(qc >> 1) * 4u;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -518,9 +521,11 @@ __device__ __noinline__ void epilogue_loop_rare(const TsArgs &ta, const RequantA
             use16 = __all_sync(0xFFFFFFFFu, (n < 0 ? -n : n) + ta.f16_accmax <= 32767);
         }
         if (use16 && ta.f16_res == 1) {
-            epi16_tile<BN, 1>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
+            if (ta.f16_tab) epi16_tile<BN, 1, true>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
+            else epi16_tile<BN, 1, false>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
         } else if (use16 && ta.f16_res == 2) {
-            epi16_tile<BN, 2>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
+            if (ta.f16_tab) epi16_tile<BN, 2, true>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
+            else epi16_tile<BN, 2, false>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
         } else {
 #pragma unroll 1
             for (int c = 0; c < NCH; ++c) ts_epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
@@ -1111,7 +1116,8 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 use16 = __all_sync(0xFFFFFFFFu, (n < 0 ? -n : n) + ta.f16_accmax <= 32767);
             }
             if (use16) {
-                epi16_tile<BN, 0>(ta, rq, trow, p, q0, na_row, sbase + C::OFF_TAB, lane, acc_empty(acc));
+                if (ta.f16_tab) epi16_tile<BN, 0, true>(ta, rq, trow, p, q0, na_row, sbase + C::OFF_TAB, lane, acc_empty(acc));
+                else epi16_tile<BN, 0, false>(ta, rq, trow, p, q0, na_row, sbase + C::OFF_TAB, lane, acc_empty(acc));
             } else if (!fast) {
 #pragma unroll 1
                 for (int c = 0; c < NCH; ++c) ts_epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
