@@ -364,14 +364,38 @@ def run_gemm(args, ws, rank, local):
         c = synth.counter_codes(r0 * n, (r1 - r0) * n, (5, n, synth.T_A), "uniform", dev).view(r1 - r0, n)
         dg.pack_codes(c, out=at[r0:r1])
     at8 = dg.expand_operand(at, n, al)          # offline expansion of the second operand
-    c_loc = torch.empty((m_loc, n), dtype=torch.int32, device=dev)
-    c_full = torch.empty((n, n), dtype=torch.int32, device=dev) if ws > 1 else c_loc
+    # N > 1: fused GEMM + all-gather (the epilogue stores each tile into every rank's C over
+    # NVLink P2P, symmetric memory) when available, else GEMM then NCCL all_gather_into_tensor
+    peer = None
+    if ws > 1 and not args.nccl_gather:
+        try:
+            peer = shard.PeerRows((n, n), torch.int32, dev, rank, ws, rank * m_loc)
+        except Exception as e:  # (no P2P / symmetric memory on this node)
+            print(f"[bench] fused all-gather unavailable ({type(e).__name__}: {e}); using NCCL", file=sys.stderr)
+    if peer is not None:
+        c_full = peer.full
+        c_loc = c_full[rank * m_loc:(rank + 1) * m_loc]
+    else:
+        c_loc = torch.empty((m_loc, n), dtype=torch.int32, device=dev)
+        c_full = torch.empty((n, n), dtype=torch.int32, device=dev) if ws > 1 else c_loc
     ops_total = 2 * n * n * n
 
-    def step(gather=True):
-        dg.lut_gemm_prepared(w, at8, m_loc, n, n, lut, out=c_loc)
-        if ws > 1 and gather:
+    def gemm():
+        if peer is not None:
+            dg.lut_gemm_prepared_allgather(w, at8, m_loc, n, n, lut, c_loc, peer.peers)
+        else:
+            dg.lut_gemm_prepared(w, at8, m_loc, n, n, lut, out=c_loc)
+
+    def gather():
+        if peer is not None:
+            peer.barrier()
+        elif ws > 1:
             shard.gather_rows(c_loc, ws, out=c_full)
+
+    def step(gather_too=True):
+        gemm()
+        if gather_too:
+            gather()
 
     for _ in range(args.warmup):
         step()
@@ -392,10 +416,9 @@ def run_gemm(args, ws, rank, local):
                 flush.zero_()
             barrier(ws)
             e0.record()
-            dg.lut_gemm_prepared(w, at8, m_loc, n, n, lut, out=c_loc)
+            gemm()
             e1.record()
-            if ws > 1:
-                shard.gather_rows(c_loc, ws, out=c_full)
+            gather()
             g1.record()
             torch.cuda.synchronize()
             t_comp += e0.elapsed_time(e1)
@@ -428,7 +451,7 @@ def run_gemm(args, ws, rank, local):
                 "scaling": "strong", "vs_baseline": None, "dtype": "int8",
                 "data": "synthetic (seeded counter-based 2-bit codes; learned-style int16 levels, Q17)",
                 "config": {"workload": f"square_gemm_n{n} (BASELINE configs[4])", "n": n,
-                           "split": f"output channels / {ws} + NCCL all_gather of int32 rows" if ws > 1 else "none",
+                           "split": (f"output channels / {ws}; " + ("fused all-gather: epilogue stores every tile into all ranks' C (NVLink P2P, symmetric memory)" if peer is not None else "NCCL all_gather of int32 rows")) if ws > 1 else "none",
                            "l2": "1 GiB int32 output per step (> L2)" if flush is None else "256 MB L2 flush between steps"},
                 "compute_only": {"value": round(comp_tops, 2), "ms": round(ms_comp, 4), "per_gpu_tops": round(per_gpu, 2)},
                 "roofline": {"bound": "tensor", "kernel": "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)",
@@ -487,6 +510,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--oracle-budget", type=float, default=20.0)
     ap.add_argument("--no-oracle", action="store_true")
+    ap.add_argument("--nccl-gather", action="store_true", help="config 5 at N > 1: GEMM then NCCL all_gather (baseline)")
     args = ap.parse_args()
     ws, rank, local = dist_env()
     if args.impl == "reference":

@@ -192,6 +192,20 @@ DG_API int64_t dg_expand_ld(int64_t K);
 DG_API dg_status dg_expand_operand(const uint8_t *d_packed, int64_t rows, int64_t K, int64_t ld,
                             const int32_t levels[4], int8_t *d_out, int64_t ld_out, void *stream);
 
+/* Fused LUT GEMM + all-gather (config 5's exchange step): computes this
+ * rank's row block exactly as dg_lut_gemm_prepared with int32 output and no requant,
+ * and the epilogue stores every output tile to d_c AND to each of the npeers (<= 7)
+ * extra destinations d_c_peers[i] (host array of device pointers: the other ranks'
+ * C buffers mapped peer-to-peer, e.g. CUDA IPC / symmetric memory), all with the
+ * same row pitch ldc and already offset to this rank's first row.  The exchange thus
+ * overlaps the math tile by tile instead of following it as a separate collective.
+ * Every destination must have the 16-byte alignment of d_c.  The caller orders
+ * completion before peers read (e.g. a barrier on the same stream after the call);
+ * the kernel fences system-wide before it exits.  DG_ERR_UNSUPPORTED if npeers > 7. */
+DG_API dg_status dg_lut_gemm_prepared_allgather(const uint8_t *d_w, int64_t ldw, const int8_t *d_at8, int64_t ld8,
+                                         int64_t M, int64_t N, int64_t K, const dg_lut *lut, int32_t *d_c,
+                                         int64_t ldc, int32_t *const *d_c_peers, int32_t npeers, void *stream);
+
 /* LUT GEMM with a prepared second operand (tc path only):
  *      C[m][n] = sum_{k<K} lut.entries[(W[m][k] << 2) | A[k][n]]
  * d_w packed [M][ldw]; d_at8 = dg_expand_operand(At, levels = lut->al) [N][ld8].

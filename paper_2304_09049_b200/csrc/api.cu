@@ -179,6 +179,23 @@ dg_status dg_lut_gemm_prepared(const uint8_t *d_w, int64_t ldw, const int8_t *d_
                        (cudaStream_t)stream);
 }
 
+dg_status dg_lut_gemm_prepared_allgather(const uint8_t *d_w, int64_t ldw, const int8_t *d_at8, int64_t ld8,
+                                         int64_t M, int64_t N, int64_t K, const dg_lut *lut, int32_t *d_c,
+                                         int64_t ldc, int32_t *const *d_c_peers, int32_t npeers, void *stream) {
+    if (!d_w || !d_at8 || !lut || !d_c || (npeers > 0 && !d_c_peers) || npeers < 0) return DG_ERR_INVALID_ARG;
+    if (npeers > 7) return DG_ERR_UNSUPPORTED;
+    if (M <= 0 || N <= 0 || K <= 0) return DG_ERR_SHAPE;
+    if (ldw % 16 || ldw * 4 < K || ld8 < expand_ld(K) || ld8 % 128 || ldc < N) return DG_ERR_SHAPE;
+    if (!aligned16(d_w) || ((uintptr_t)d_at8 & 127)) return DG_ERR_INVALID_ARG;
+    for (int i = 0; i < npeers; ++i)
+        if (!d_c_peers[i]) return DG_ERR_INVALID_ARG;
+    if (!lut->is_product || !levels_fit_i8(lut->wl) || !levels_fit_i8(lut->al) || !tc_available())
+        return DG_ERR_UNSUPPORTED;
+    if ((int64_t)K * max_abs_entry(lut->entries) >= ((int64_t)1 << 31)) return DG_ERR_OVERFLOW;
+    return lut_gemm_ts(d_w, ldw, d_at8, ld8, M, N, K, lut->wl, lut->al, d_c, ldc, nullptr, (cudaStream_t)stream,
+                       nullptr, nullptr, 0, d_c_peers, npeers);
+}
+
 static bool conv_implicit_ok(const dg_conv_params *p, const uint8_t *d_x) {
     // the tensor-core kernel gathers im2col rows itself when a tap is a power-of-two number of
     // 16-byte chunks (C = 64, 128, 256, ... channels)

@@ -220,5 +220,6 @@ struct TsConv {
 };
 dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                       const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
-                      cudaStream_t st, const TsConv *cv = nullptr, void *skws = nullptr, size_t skws_bytes = 0);
+                      cudaStream_t st, const TsConv *cv = nullptr, void *skws = nullptr, size_t skws_bytes = 0,
+                      int32_t *const *peers = nullptr, int32_t npeers = 0);
 }  // namespace dg

@@ -129,6 +129,10 @@ struct TsArgs {
     // each split stores its partial sums to its own slice ws_acc[ks] (int32 [sk][np][nq]); the
     // splitk_reduce_kernel launched right behind sums the slices and requantises / stores
     int32_t sk, nwork;   // nwork = ntp * ntq * sk work items
+    // fused all-gather (int32 output): every output tile is also stored to npeer extra
+    // destinations (peer GPUs' C buffers, P2P-mapped, already offset to this rank's rows)
+    int32_t npeer;
+    int32_t *peer[7];
     FastDiv fd_sk;
     int32_t *ws_acc;
     int32_t last_grp, last_rows;   // index of the last row group and its row-block count
@@ -290,13 +294,16 @@ __device__ __forceinline__ void ts_epilogue_values(const TsArgs &ta, const Requa
                                                 int64_t qc) {
     if (p >= ta.np || qc >= ta.nq) return;
     if (!ta.has_rq) {
-        int32_t *dp = reinterpret_cast<int32_t *>(ta.D) + p * ta.ldd + qc;
-        if (qc + 32 <= ta.nq && (ta.ldd & 3) == 0 && ((reinterpret_cast<uintptr_t>(ta.D) & 15) == 0)) {
+        const bool vec = qc + 32 <= ta.nq && (ta.ldd & 3) == 0 && ((reinterpret_cast<uintptr_t>(ta.D) & 15) == 0);
+        for (int d = -1; d < ta.npeer; ++d) {   // own output, then the all-gather peers (same offsets)
+            int32_t *dp = (d < 0 ? reinterpret_cast<int32_t *>(ta.D) : ta.peer[d]) + p * ta.ldd + qc;
+            if (vec) {
 #pragma unroll
-            for (int j = 0; j < 32; j += 4) *reinterpret_cast<int4 *>(dp + j) = make_int4(v[j], v[j + 1], v[j + 2], v[j + 3]);
-        } else {
-            for (int j = 0; j < 32; ++j)
-                if (qc + j < ta.nq) dp[j] = v[j];
+                for (int j = 0; j < 32; j += 4) *reinterpret_cast<int4 *>(dp + j) = make_int4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+            } else {
+                for (int j = 0; j < 32; ++j)
+                    if (qc + j < ta.nq) dp[j] = v[j];
+            }
         }
         return;
     }
@@ -1174,6 +1181,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             if (lane == 0 && quarter == 0) TS_EV(10, tl);
         }
         }   // common modes
+        if (ta.npeer) __threadfence_system();   // peer stores visible system-wide before the grid completes
     }
 
     ptx::tc_fence_before();
@@ -1306,6 +1314,10 @@ bool f16_params(int64_t t0, int64_t t1, int64_t t2, uint32_t &m_out, uint32_t &c
     return false;
 }
 
+// extra all-gather destinations of the current lut_gemm_ts call (set there, read by launch_ts)
+thread_local int32_t *const *g_peers = nullptr;
+thread_local int32_t g_npeers = 0;
+
 template <int BN, int NEPI, int NUNP, int KST, bool WIN = false, bool ASM = false, bool SK = false>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
@@ -1371,6 +1383,15 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     ta.D = D;
     ta.ldd = ldd;
     ta.has_rq = rq ? 1 : 0;
+    ta.npeer = 0;
+    if (g_npeers > 0) {   // fused all-gather: int32 output only, 16-byte aligned like D
+        if (rq || g_npeers > 7) return DG_ERR_UNSUPPORTED;
+        ta.npeer = g_npeers;
+        for (int i = 0; i < g_npeers; ++i) {
+            if (!g_peers[i] || (((uintptr_t)g_peers[i] ^ (uintptr_t)D) & 15)) return DG_ERR_INVALID_ARG;
+            ta.peer[i] = g_peers[i];
+        }
+    }
     const bool has_res = rq && (rq->res || rq->res_codes);
     int64_t res_bound = 0;   // max |residual| for the 16-bit range check (int32 residuals: checked per warp)
     if (rq && rq->res_codes)
@@ -1515,8 +1536,12 @@ dg_status expand_operand(const uint8_t *packed, int64_t rows, int64_t K, int64_t
 
 dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                       const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
-                      cudaStream_t st, const TsConv *cv, void *skws, size_t skws_bytes) {
+                      cudaStream_t st, const TsConv *cv, void *skws, size_t skws_bytes, int32_t *const *peers,
+                      int32_t npeers) {
     if (np > ((int64_t)1 << 31) - 1 || nq > ((int64_t)1 << 31) - 1) return DG_ERR_SHAPE;
+    g_peers = peers;
+    g_npeers = peers ? npeers : 0;
+    struct Reset { ~Reset() { g_peers = nullptr; g_npeers = 0; } } reset;
     // direct 3x3 / stride 1 / pad 1 convs with C = 64, 128, 256: shifted-window kernel (DG_WIN=1; it
     // unpacks each input pixel once per tile instead of once per tap, but measured no faster than
     // the implicit gather on the ResNet-50 shapes)

@@ -68,6 +68,10 @@ DG_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
 #ifdef DG_MBAR_SPIN
     while (!mbar_test_wait(bar, parity)) {   // non-suspending probe loop
     }
+#elif defined(DG_MBAR_BACKOFF)
+    while (!mbar_try_wait(bar, parity)) {   // back off: a spinning warp takes issue slots from its neighbours
+        __nanosleep(DG_MBAR_BACKOFF);
+    }
 #else
     while (!mbar_try_wait(bar, parity)) {
     }

@@ -78,6 +78,7 @@ def lib():
             "dg_expand_ld": ([i64], i64),
             "dg_expand_operand": ([P, i64, i64, i64, P, P, i64, P], i32),
             "dg_lut_gemm_prepared": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, P], i32),
+            "dg_lut_gemm_prepared_allgather": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, i32, P], i32),
             "dg_lut_conv2d_workspace_size": ([P], ctypes.c_size_t),
             "dg_lut_conv2d": ([P, P, P, P, P, P, P, ctypes.c_size_t, i32, P], i32),
             "dg_lut_conv2d_prepared": ([P, P, i64, P, P, P, P, P, ctypes.c_size_t, P], i32),
@@ -285,6 +286,21 @@ def lut_gemm_prepared(w: torch.Tensor, at8: torch.Tensor, M: int, N: int, K: int
     _check(lib().dg_lut_gemm_prepared(_ptr(w), w.shape[1], _ptr(at8), at8.shape[1], M, N, K, ctypes.byref(lut),
                                       _ptr(out), out.shape[1], ctypes.byref(r) if r is not None else None,
                                       _stream(stream)), "dg_lut_gemm_prepared")
+    return out
+
+
+def lut_gemm_prepared_allgather(w: torch.Tensor, at8: torch.Tensor, M: int, N: int, K: int, lut: dg_lut,
+                                out: torch.Tensor, peer_ptrs=(), stream=None):
+    """Fused GEMM + all-gather: this rank's int32 rows go to `out` (a [M][ldc] view of its rows of
+    the full C) and to every peer destination in `peer_ptrs` (raw device addresses of the other
+    ranks' C buffers, already offset to this rank's rows; same pitch)."""
+    _dev(w, torch.uint8, "w")
+    _dev(at8, torch.int8, "at8")
+    _dev(out, torch.int32, "out")
+    arr = (ctypes.c_void_p * max(1, len(peer_ptrs)))(*[int(x) for x in peer_ptrs])
+    _check(lib().dg_lut_gemm_prepared_allgather(_ptr(w), w.shape[1], _ptr(at8), at8.shape[1], M, N, K,
+                                                ctypes.byref(lut), _ptr(out), out.stride(0), arr, len(peer_ptrs),
+                                                _stream(stream)), "dg_lut_gemm_prepared_allgather")
     return out
 
 

@@ -38,6 +38,24 @@ def gather_rows(local: torch.Tensor, world: int, out: torch.Tensor | None = None
     return out
 
 
+class PeerRows:
+    """Fused all-gather destinations for config 5: every rank holds the full C in
+    symmetric memory (CUDA P2P-mapped across the node's GPUs); rank r's GEMM epilogue stores its
+    rows [r0, r1) into every peer's C directly (dg_lut_gemm_prepared_allgather), and a device-side
+    barrier on the same stream orders those stores before anyone reads C."""
+
+    def __init__(self, shape, dtype, device, rank: int, world: int, row0: int):
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm_mem
+        self.full = symm_mem.empty(*shape, dtype=dtype, device=device)
+        self.hdl = symm_mem.rendezvous(self.full, dist.group.WORLD)
+        pitch = self.full.stride(0) * self.full.element_size()
+        self.peers = [int(self.hdl.buffer_ptrs[j]) + row0 * pitch for j in range(world) if j != rank]
+
+    def barrier(self):
+        self.hdl.barrier(channel=0)
+
+
 def max_over_ranks(v: float, world: int, device="cpu") -> float:
     import torch.distributed as dist
     if world == 1:

@@ -329,6 +329,36 @@ def test_gemm_prepared_and_expand(M, N, K):
     assert np.array_equal(C, oracle.lut_gemm(W, A, oracle.build_lut16(wl, al)))
 
 
+@pytest.mark.parametrize("P,m,N,K", [(3, 200, 300, 576), (2, 128, 64, 4608), (8, 40, 130, 100)])
+def test_gemm_fused_allgather(P, m, N, K):
+    """dg_lut_gemm_prepared_allgather: P simulated ranks on one GPU, each computing its m-row block
+    and storing it into all P full-C buffers (its own + P-1 'peer' destinations at its row
+    offset).  Every buffer must end up equal to the oracle's full C (config 5's exchange step)."""
+    import synth
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    wl, al = synth.learned_levels(5, 2, synth.T_LEVELS)
+    lut = dg.build_lut(wl, al, 16)
+    g = np.random.default_rng(P * 1000 + m + N + K)
+    M = P * m
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    at8 = dg.expand_operand(gpu_pack(np.ascontiguousarray(A.T)), K, al)
+    full = [torch.full((M, N), -7, dtype=torch.int32, device=DEV) for _ in range(P)]
+    n0 = dg.kernel_launches()
+    for r in range(P):
+        w_r = gpu_pack(np.ascontiguousarray(W[r * m:(r + 1) * m]), weights=True)
+        peers = [full[j][r * m:].data_ptr() for j in range(P) if j != r]
+        n1 = dg.kernel_launches()
+        dg.lut_gemm_prepared_allgather(w_r, at8, m, N, K, lut, full[r][r * m:(r + 1) * m], peers)
+        assert dg.kernel_launches() - n1 == 1   # one fused kernel per rank, no separate collective
+    exp = oracle.lut_gemm(W, A, oracle.build_lut16(wl, al))
+    for j in range(P):
+        assert np.array_equal(host(full[j]), exp), j
+    with pytest.raises(dg.DGError, match="UNSUPPORTED"):
+        dg.lut_gemm_prepared_allgather(w_r, at8, m, N, K, lut, full[0][:m], [full[0].data_ptr()] * 8)
+
+
 @pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", CONVS)
 def test_conv_prepared_vs_oracle(B, H, W, C, Cout, k, stride, pad, pad_code):
     """dg_lut_conv2d_prepared (offline-expanded weights; direct / implicit-GEMM / im2col)."""
