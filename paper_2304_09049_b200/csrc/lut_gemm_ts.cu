@@ -704,7 +704,8 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
         }
     } else if (warp == MMA_WARP) {
-        // ---------------- MMA issuer: no mbarrier waits here (see HANDOFF_BAR)
+        // ---------------- MMA issuer: no mbarrier waits here (see HANDOFF_BAR).  The whole warp runs
+        // the loop and the *_warp helpers elect the issuing lane inside their asm (ptx::mma_i8_ts_warp).
         constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
         const uint64_t bdesc0 = ptx::desc_k_sw128(sbase + C::OFF_B);
         uint32_t g = 0, tl = 0;
@@ -718,75 +719,68 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 const int bsl = ta.bres ? tq * ta.nstages + s : (int)(g % SB);   // B smem stage
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
                 ptx::tc_fence_after();
-                if (lane == 0 && WIN) {
-                    TS_EV(14, g);
+                const int nk = (s < ta.nstages - 1) ? C::KSTEPS : ta.last_ksteps;
+                const uint64_t bd = bdesc0 + (uint64_t)((bsl * C::B_BYTES) >> 4);
+                if (lane == 0) TS_EV(14, g);
+                if (WIN) {
                     // k = tap*C + c: A = the window shifted by r*Wp + s rows (tap = 3r + s), K chunk c/16;
                     // the per-k-step start offsets come precomputed from the host (ta.koff)
                     const uint32_t wbase = sbase + C::OFF_P + (uint32_t)(2 * ta.wslot + (int)(tl % ta.nwin) * ta.wbytes);
                     const uint64_t ad = ptx::desc_k_none(wbase, (uint32_t)ta.lbo);
-                    const uint64_t bd = bdesc0 + (uint64_t)((bsl * C::B_BYTES) >> 4);
                     const int j0 = s * C::KSTEPS;
                     // all offsets into registers first: a parameter load between two tcgen05.mma
                     // (asm with a memory clobber) serialises the issue (~150 cycles per MMA measured)
                     uint32_t ko[C::KSTEPS];
 #pragma unroll
                     for (int k = 0; k < C::KSTEPS; ++k) ko[k] = ta.koff[j0 + k < 72 ? j0 + k : 71];
-                    if (s < ta.nstages - 1 || ta.last_ksteps == C::KSTEPS) {
 #pragma unroll
-                        for (int k = 0; k < C::KSTEPS; ++k)
-                            ptx::mma_i8_ss(dt, ad + ko[k], bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
-                                           idesc, (s > sb || k > 0) ? 1u : 0u);
-                    } else {
-#pragma unroll
-                        for (int k = 0; k < C::KSTEPS; ++k)
-                            if (k < ta.last_ksteps)
-                                ptx::mma_i8_ss(dt, ad + ko[k], bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
-                                               idesc, (s > sb || k > 0) ? 1u : 0u);
-                    }
-                    if (!ta.bres) ptx::mma_commit(empty_b(bsl));
+                    for (int k = 0; k < C::KSTEPS; ++k)
+                        if (k < nk)
+                            ptx::mma_i8_ss_warp(dt, ad + ko[k], bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
+                                                idesc, (s > sb || k > 0) ? 1u : 0u);
+                    if (!ta.bres) ptx::mma_commit_warp(empty_b(bsl));
                     if (s == se - 1) {
-                        ptx::mma_commit(empty_a(tl % ta.nwin));   // the window is free again
-                        ptx::mma_commit(acc_full(acc));
+                        ptx::mma_commit_warp(empty_a(tl % ta.nwin));   // the window is free again
+                        ptx::mma_commit_warp(acc_full(acc));
                     }
-                    TS_EV(15, g);
-                } else if (lane == 0 && ASM) {
+                } else if (ASM) {
                     const uint64_t ad = ptx::desc_k_none(sbase + C::OFF_A + (uint32_t)(sa * C::A_STAGE), BM * 16);
-                    const uint64_t bd = bdesc0 + (uint64_t)((bsl * C::B_BYTES) >> 4);
                     // k-step k: A K-chunks 2k, 2k+1 (+2k * BM*16 bytes), B atom k/4, +32 B per k-step inside
-                    if (s < ta.nstages - 1 || ta.last_ksteps == C::KSTEPS) {
+                    if (nk == C::KSTEPS) {
 #pragma unroll
                         for (int k = 0; k < C::KSTEPS; ++k)
-                            ptx::mma_i8_ss(dt, ad + (uint64_t)((2 * k * BM * 16) >> 4), bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
-                                           idesc, (s > sb || k > 0) ? 1u : 0u);
+                            ptx::mma_i8_ss_warp(dt, ad + (uint64_t)((2 * k * BM * 16) >> 4),
+                                                bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3), idesc,
+                                                (s > sb || k > 0) ? 1u : 0u);
                     } else {
-                        for (int k = 0; k < ta.last_ksteps; ++k)
-                            ptx::mma_i8_ss(dt, ad + (uint64_t)((2 * k * BM * 16) >> 4), bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
-                                           idesc, (s > sb || k > 0) ? 1u : 0u);
+                        for (int k = 0; k < nk; ++k)
+                            ptx::mma_i8_ss_warp(dt, ad + (uint64_t)((2 * k * BM * 16) >> 4),
+                                                bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3), idesc,
+                                                (s > sb || k > 0) ? 1u : 0u);
                     }
-                    ptx::mma_commit(empty_a(sa));
-                    if (!ta.bres) ptx::mma_commit(empty_b(bsl));
-                    if (s == se - 1) ptx::mma_commit(acc_full(acc));
-                } else if (lane == 0) {
+                    ptx::mma_commit_warp(empty_a(sa));
+                    if (!ta.bres) ptx::mma_commit_warp(empty_b(bsl));
+                    if (s == se - 1) ptx::mma_commit_warp(acc_full(acc));
+                } else {
                     const uint32_t at = tmem + C::TMEM_A0 + sa * C::ACOLS;
-                    const uint64_t bd = bdesc0 + (uint64_t)((bsl * C::B_BYTES) >> 4);
                     // k-step k: A columns 8k, B atom k/4 (+B_ATOM bytes), 32 bytes (+2) per k-step inside
-#ifdef DG_EXP_NOMMA
-                    if (false) {} else
-#endif
-                    if (s < ta.nstages - 1 || ta.last_ksteps == C::KSTEPS) {
+#ifndef DG_EXP_NOMMA
+                    if (nk == C::KSTEPS) {   // full stage: straight-line issue
 #pragma unroll
                         for (int k = 0; k < C::KSTEPS; ++k)
-                            ptx::mma_i8_ts(dt, at + 8 * k, bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3), idesc,
-                                           (s > sb || k > 0) ? 1u : 0u);
+                            ptx::mma_i8_ts_warp(dt, at + 8 * k, bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
+                                                idesc, (s > sb || k > 0) ? 1u : 0u);
                     } else {
-                        for (int k = 0; k < ta.last_ksteps; ++k)
-                            ptx::mma_i8_ts(dt, at + 8 * k, bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3), idesc,
-                                           (s > sb || k > 0) ? 1u : 0u);
+                        for (int k = 0; k < nk; ++k)
+                            ptx::mma_i8_ts_warp(dt, at + 8 * k, bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
+                                                idesc, (s > sb || k > 0) ? 1u : 0u);
                     }
-                    ptx::mma_commit(empty_a(sa));
-                    if (!ta.bres) ptx::mma_commit(empty_b(bsl));
-                    if (s == se - 1) ptx::mma_commit(acc_full(acc));
+#endif
+                    ptx::mma_commit_warp(empty_a(sa));
+                    if (!ta.bres) ptx::mma_commit_warp(empty_b(bsl));
+                    if (s == se - 1) ptx::mma_commit_warp(acc_full(acc));
                 }
+                if (lane == 0) TS_EV(15, g);
                 __syncwarp();
             }
         }
