@@ -233,6 +233,8 @@ CONVS = [  # B, H, W, C, Cout, k, stride, pad, pad_code
     (2, 9, 9, 64, 32, 3, 1, 1, 2),     # implicit-GEMM path with a non-zero pad code
     (1, 12, 12, 256, 64, 3, 2, 1, 0),  # implicit, stride 2, C/4 = 64
     (2, 10, 10, 64, 64, 1, 2, 0, 0),   # implicit 1x1 stride 2 (downsample)
+    (1, 11, 13, 64, 32, 5, 2, 2, 1),   # implicit 5x5 (25 taps: precomputed tap masks), pad 2, pad code 1
+    (1, 9, 9, 64, 16, 7, 1, 3, 0),     # implicit 7x7 (49 taps > 32: per-chunk tap arithmetic)
 ]
 
 
