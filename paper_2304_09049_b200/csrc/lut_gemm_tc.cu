@@ -235,8 +235,8 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
         }
     } else if (warp == 1) {
-        // ---------------- MMA issuer (single thread)
-        if (lane == 0) {
+        // ---------------- MMA issuer (whole warp; one lane elected inside the *_warp helpers)
+        {
             constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
             uint32_t g = 0, tl = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
@@ -256,11 +256,11 @@ lut_gemm_tc_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 #pragma unroll
                     for (int k = 0; k < KS / 32; ++k)
                         if (k < ksteps)
-                            ptx::mma_i8_ss(dt, ptx::desc_k_sw128(a + 32 * k), ptx::desc_k_sw128(b + 32 * k), idesc,
-                                           (s > 0 || k > 0) ? 1u : 0u);
-                    ptx::mma_commit(empty_u(slot));
+                            ptx::mma_i8_ss_warp(dt, ptx::desc_k_sw128(a + 32 * k), ptx::desc_k_sw128(b + 32 * k), idesc,
+                                                (s > 0 || k > 0) ? 1u : 0u);
+                    ptx::mma_commit_warp(empty_u(slot));
                 }
-                ptx::mma_commit(acc_full(acc));
+                ptx::mma_commit_warp(acc_full(acc));
             }
         }
     } else if (warp < EPI_WARP0) {

@@ -171,9 +171,13 @@ class NetRunner:
 
     # -- the user-level path: one dg_lut_conv2d per layer
     def step_conv2d(self, stream=None):
-        for p in self.plans:
-            dg.lut_conv2d(p.x, p.w, p.lut, p.params, rq=p.rq, variant=self.variant, out=p.out, ws=self.ws,
-                          stream=stream)
+        for i in range(len(self.plans)):
+            self.conv2d_layer(i, stream)
+
+    def conv2d_layer(self, i: int, stream=None):
+        """One layer through the public dg_lut_conv2d call (weights expanded inside the call)."""
+        p = self.plans[i]
+        dg.lut_conv2d(p.x, p.w, p.lut, p.params, rq=p.rq, variant=self.variant, out=p.out, ws=self.ws, stream=stream)
 
     def input_bytes(self) -> int:
         return sum(p.x.numel() for p in self.plans)
