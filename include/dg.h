@@ -192,6 +192,25 @@ DG_API int64_t dg_expand_ld(int64_t K);
 DG_API dg_status dg_expand_operand(const uint8_t *d_packed, int64_t rows, int64_t K, int64_t ld,
                             const int32_t levels[4], int8_t *d_out, int64_t ld_out, void *stream);
 
+/* Block-scaled FP4 tensor-core path (tcgen05 kind::mxf4, e2m1 x e2m1):
+ *      C[m][n] = sum_{k<K} lut.entries[(W[m][k] << 2) | A[k][n]]     (int32, exact)
+ * for product tables whose activation levels are lut->al = {0, 1, 2, 3} (the activation code is
+ * then the e2m1 encoding of al/2, so the kernel unpacks it with two nibble masks per 16 codes) and
+ * whose weight levels v have v/2 in e2m1, i.e. v in {0, +-1, +-2, +-3, +-4, +-6, +-8, +-12}
+ * (BJ configs 1-4: wl = {-2, -1, 0, 1}).  The fp32 tensor-core sums are integers below 2^22 and
+ * exact (tools/fp4_test.cu); DG_ERR_OVERFLOW if K * max|entry| >= 2^22.
+ * dg_expand_operand_f4: packed weights [rows][ld] -> e2m1 nibbles of level/2 [rows][ld_out]
+ * (ld_out >= dg_expand_f4_ld(K) = roundup(K, 256) / 2, a multiple of 128; 0 for k >= K), done
+ * once per weight tensor.  DG_ERR_UNSUPPORTED if a level is not representable.
+ * dg_lut_gemm_f4: d_w4 [M][ld4] (expanded weights, 16-byte aligned), d_at [N][lda] packed
+ * activations (K-major, lda % 16 == 0), int32 C [M][ldc] (ldc >= N), no requant.
+ * DG_ERR_UNSUPPORTED if the table does not qualify (use dg_lut_gemm / _prepared).          */
+DG_API int64_t dg_expand_f4_ld(int64_t K);
+DG_API dg_status dg_expand_operand_f4(const uint8_t *d_packed, int64_t rows, int64_t K, int64_t ld,
+                                      const int32_t levels[4], uint8_t *d_out, int64_t ld_out, void *stream);
+DG_API dg_status dg_lut_gemm_f4(const uint8_t *d_w4, int64_t ld4, const uint8_t *d_at, int64_t lda, int64_t M,
+                                int64_t N, int64_t K, const dg_lut *lut, int32_t *d_c, int64_t ldc, void *stream);
+
 /* Fused LUT GEMM + all-gather (config 5's exchange step): computes this
  * rank's row block exactly as dg_lut_gemm_prepared with int32 output and no requant,
  * and the epilogue stores every output tile to d_c AND to each of the npeers (<= 7)

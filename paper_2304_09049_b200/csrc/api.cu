@@ -160,6 +160,30 @@ dg_status dg_expand_operand(const uint8_t *d_packed, int64_t rows, int64_t K, in
     return expand_operand(d_packed, rows, K, ld, levels, d_out, ld_out, (cudaStream_t)stream);
 }
 
+int64_t dg_expand_f4_ld(int64_t K) { return K <= 0 ? 0 : expand_f4_ld(K); }
+
+dg_status dg_expand_operand_f4(const uint8_t *d_packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],
+                               uint8_t *d_out, int64_t ld_out, void *stream) {
+    if (!d_packed || !d_out || !levels) return DG_ERR_INVALID_ARG;
+    if (rows < 0 || K <= 0 || ld * 4 < K || ld % 16 || ld_out < expand_f4_ld(K) || ld_out % 128) return DG_ERR_SHAPE;
+    if (!aligned16(d_packed) || !aligned16(d_out)) return DG_ERR_INVALID_ARG;
+    if (!tc_available()) return DG_ERR_UNSUPPORTED;
+    return expand_operand_f4(d_packed, rows, K, ld, levels, d_out, ld_out, (cudaStream_t)stream);
+}
+
+dg_status dg_lut_gemm_f4(const uint8_t *d_w4, int64_t ld4, const uint8_t *d_at, int64_t lda, int64_t M, int64_t N,
+                         int64_t K, const dg_lut *lut, int32_t *d_c, int64_t ldc, void *stream) {
+    if (!d_w4 || !d_at || !lut || !d_c) return DG_ERR_INVALID_ARG;
+    if (M <= 0 || N <= 0 || K <= 0) return DG_ERR_SHAPE;
+    if (lda % 16 || lda * 4 < K || ld4 < expand_f4_ld(K) || ld4 % 128 || ldc < N) return DG_ERR_SHAPE;
+    if (!aligned16(d_w4) || !aligned16(d_at)) return DG_ERR_INVALID_ARG;
+    if (!lut->is_product || !tc_available()) return DG_ERR_UNSUPPORTED;
+    for (int c = 0; c < 4; ++c)
+        if (lut->al[c] != c || f4_nibble_half(lut->wl[c]) < 0) return DG_ERR_UNSUPPORTED;
+    if ((int64_t)K * max_abs_entry(lut->entries) >= ((int64_t)1 << 22)) return DG_ERR_OVERFLOW;
+    return lut_gemm_f4(d_at, lda, d_w4, ld4, M, N, K, d_c, ldc, (cudaStream_t)stream);
+}
+
 dg_status dg_lut_gemm_prepared(const uint8_t *d_w, int64_t ldw, const int8_t *d_at8, int64_t ld8,
                                int64_t M, int64_t N, int64_t K, const dg_lut *lut, void *d_c, int64_t ldc,
                                const dg_requant *rq, void *stream) {

@@ -214,6 +214,12 @@ int64_t expand_ld(int64_t K);
 dg_status expand_operand(const uint8_t *packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],
                          int8_t *out, int64_t ld8, cudaStream_t st);
 // implicit-GEMM convolution description for the TS kernel (P = im2col of x, gathered on chip)
+int64_t expand_f4_ld(int64_t K);
+int f4_nibble_half(int32_t v);
+dg_status expand_operand_f4(const uint8_t *packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],
+                            uint8_t *out, int64_t ld4, cudaStream_t st);
+dg_status lut_gemm_f4(const uint8_t *At, int64_t lda, const uint8_t *W4, int64_t ld4, int64_t M, int64_t N, int64_t K,
+                      int32_t *C, int64_t ldc, cudaStream_t st);
 struct TsConv {
     const uint8_t *x;
     int32_t H, W, Cb, kh, kw, stride, pad, Ho, Wo, pad_code;

@@ -79,6 +79,9 @@ def lib():
             "dg_expand_operand": ([P, i64, i64, i64, P, P, i64, P], i32),
             "dg_lut_gemm_prepared": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, P], i32),
             "dg_lut_gemm_prepared_allgather": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, i32, P], i32),
+            "dg_expand_f4_ld": ([i64], i64),
+            "dg_expand_operand_f4": ([P, i64, i64, i64, P, P, i64, P], i32),
+            "dg_lut_gemm_f4": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P], i32),
             "dg_lut_conv2d_workspace_size": ([P], ctypes.c_size_t),
             "dg_lut_conv2d": ([P, P, P, P, P, P, P, ctypes.c_size_t, i32, P], i32),
             "dg_lut_conv2d_prepared": ([P, P, i64, P, P, P, P, P, ctypes.c_size_t, P], i32),
@@ -271,6 +274,35 @@ def expand_operand(packed: torch.Tensor, K: int, levels, out: torch.Tensor | Non
     lv = (ctypes.c_int32 * 4)(*[int(x) for x in levels])
     _check(lib().dg_expand_operand(_ptr(packed), rows, K, ld, lv, _ptr(out), out.shape[1], _stream(stream)),
            "dg_expand_operand")
+    return out
+
+
+def expand_f4_ld(K: int) -> int:
+    return int(lib().dg_expand_f4_ld(K))
+
+
+def expand_operand_f4(packed: torch.Tensor, K: int, levels, out: torch.Tensor | None = None, stream=None):
+    """Packed weight codes [rows][ld] -> e2m1 nibbles of level/2 [rows][expand_f4_ld(K)] (FP4 path)."""
+    _dev(packed, torch.uint8, "packed")
+    rows, ld = packed.shape
+    if out is None:
+        out = torch.empty((rows, expand_f4_ld(K)), dtype=torch.uint8, device=packed.device)
+    lv = (ctypes.c_int32 * 4)(*[int(x) for x in levels])
+    _check(lib().dg_expand_operand_f4(_ptr(packed), rows, K, ld, lv, _ptr(out), out.shape[1], _stream(stream)),
+           "dg_expand_operand_f4")
+    return out
+
+
+def lut_gemm_f4(w4: torch.Tensor, at: torch.Tensor, M: int, N: int, K: int, lut: dg_lut,
+                out: torch.Tensor | None = None, stream=None):
+    """int32 C[M][N] on the block-scaled FP4 tensor-core path: w4 = expand_operand_f4(W, K, lut.wl),
+    at = packed activations [N][lda]; needs lut.al == (0, 1, 2, 3) and e2m1-representable wl/2."""
+    _dev(w4, torch.uint8, "w4")
+    _dev(at, torch.uint8, "at")
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.int32, device=w4.device)
+    _check(lib().dg_lut_gemm_f4(_ptr(w4), w4.shape[1], _ptr(at), at.shape[1], M, N, K, ctypes.byref(lut),
+                                _ptr(out), out.shape[1], _stream(stream)), "dg_lut_gemm_f4")
     return out
 
 

@@ -562,3 +562,64 @@ def test_conv_splitk_vs_oracle(B, H, C, Cout, k, stride):
     outr = dg.lut_conv2d_prepared(xp, w8, lut, p, rq=dg.Requant(mult=20000, shift=20, res=torch.from_numpy(res).to(DEV)), ws=ws)
     expr = oracle.requantize(e2, 20000, 20, 0, 0, 3, res=res)
     assert np.array_equal(oracle_codes_of(outr, expr.shape[0], Cout), expr)
+
+
+# ---- block-scaled FP4 path (tcgen05 kind::mxf4) -------------------------
+F4_SHAPES = [(256, 128, 256), (300, 200, 576), (64, 196, 576), (513, 129, 1000), (256, 384, 4608), (40, 7, 3)]
+
+
+@pytest.mark.parametrize("M,N,K", F4_SHAPES)
+def test_gemm_f4_vs_oracle(M, N, K):
+    """dg_expand_operand_f4 + dg_lut_gemm_f4 vs the oracle, bit-exact: ragged M / N / K (K not a
+    multiple of the 64-code MMA step or of the 256-code stage), several tiles, config-1 levels."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    lut = dg.build_lut(WL, AL, 8)
+    g = np.random.default_rng(7 * M + N + K)
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    w4 = dg.expand_operand_f4(gpu_pack(W, weights=True), K, WL)
+    C = host(dg.lut_gemm_f4(w4, gpu_pack(np.ascontiguousarray(A.T)), M, N, K, lut))
+    assert np.array_equal(C, oracle.lut_gemm(W, A, oracle.build_lut16(WL, AL)))
+
+
+@pytest.mark.parametrize("wl", [(-2, -1, 0, 1), (-12, -3, 4, 8), (0, 6, -6, 1), (3, 3, -2, 2)])
+def test_gemm_f4_levels_and_extremes(wl):
+    """Every e2m1-representable weight level set (v/2 in e2m1), all-max-magnitude rows first (the
+    adversarial order for a truncating accumulator: large partial sums, then small terms) and the
+    largest |acc| the path admits (K * max|entry| < 2^22)."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    lut = dg.build_lut(list(wl), AL, 8)
+    T = oracle.build_lut16(list(wl), AL)
+    M, N = 256, 256
+    K = min(4608, (1 << 22) // max(1, int(np.abs(T).max())) - 1)
+    g = np.random.default_rng(sum(wl) + 100)
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    big_w = int(np.argmax(np.abs(np.array(wl))))
+    W[::2, : K - 64] = big_w          # half the rows: max |level| first, random tail
+    A[: K - 64, ::2] = 3
+    w4 = dg.expand_operand_f4(gpu_pack(W, weights=True), K, list(wl))
+    C = host(dg.lut_gemm_f4(w4, gpu_pack(np.ascontiguousarray(A.T)), M, N, K, lut))
+    assert np.array_equal(C, oracle.lut_gemm(W, A, T))
+
+
+def test_gemm_f4_rejects():
+    """Tables outside the FP4 path's exact domain are refused, not approximated."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    K, M, N = 64, 8, 8
+    w = gpu_pack(np.zeros((M, K), np.uint8), weights=True)
+    at = gpu_pack(np.zeros((N, K), np.uint8))
+    with pytest.raises(dg.DGError, match="UNSUPPORTED"):
+        dg.expand_operand_f4(w, K, [-5, -1, 0, 1])          # 5/2 is not an e2m1 value
+    w4 = dg.expand_operand_f4(w, K, WL)
+    with pytest.raises(dg.DGError, match="UNSUPPORTED"):   # activation levels must be 0..3
+        dg.lut_gemm_f4(w4, at, M, N, K, dg.build_lut(WL, [0, 1, 2, 4], 8))
+    with pytest.raises(dg.DGError, match="OVERFLOW"):      # K * 12 * 3 >= 2^22
+        big = 120000
+        wb = gpu_pack(np.zeros((M, big), np.uint8), weights=True)
+        ab = gpu_pack(np.zeros((N, big), np.uint8))
+        dg.lut_gemm_f4(dg.expand_operand_f4(wb, big, [-12, 0, 1, 2]), ab, M, N, big,
+                       dg.build_lut([-12, 0, 1, 2], AL, 8))

@@ -27,6 +27,9 @@ for s in a.shapes.split(","):
             continue
         if v == "prepared":
             f = lambda: dg.lut_gemm_prepared(w, at8, M, N, ld * 4, lut, out=out)
+        elif v == "f4":   # block-scaled FP4 path: weights expanded once to e2m1
+            w4 = dg.expand_operand_f4(w, ld * 4, lut.wl)
+            f = lambda: dg.lut_gemm_f4(w4, at, M, N, ld * 4, lut, out=out)
         else:
             f = lambda: dg.lut_gemm(w, at, M, N, ld * 4, lut, variant=v, out=out, ws=ws)
         try:
