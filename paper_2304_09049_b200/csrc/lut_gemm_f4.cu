@@ -13,7 +13,7 @@
 // partial sum is an integer below 2^22, and tools/fp4_test.cu checks that the hardware
 // accumulation is exact on random and adversarial rows (profiles/r01_fp4_mxf4_test.txt).
 //
-// Tile: 128 activation rows (n) x 256 weight rows (m); D[n][m] in TMEM (fp32, one buffer), stored
+// Tile: 128 activation rows (n) x 240 weight rows (m); D[n][m] in TMEM (fp32, two buffers), stored
 // transposed into C[m][n] (each store instruction writes 32 consecutive n of one m: coalesced).
 // Persistent, warp-specialised, one CTA per SM:
 //   warps 0..3  epilogue (lane quarter = warp): TMEM -> exact int32 -> C
@@ -32,9 +32,10 @@ namespace dg {
 namespace {
 
 constexpr int F4_BM = 128;           // activation rows per tile (MMA M, TMEM lanes)
-constexpr int F4_BN = 256;           // weight rows per tile (MMA N)
+constexpr int F4_BN = 240;           // weight rows per tile (MMA N): 2 x 240 fp32 accumulator columns + 32
+                                     // block-scale columns fill the 512 TMEM columns
 constexpr int F4_KST = 256;          // codes per pipeline stage = 128 bytes of e2m1 per row = 4 MMAs
-constexpr int F4_SA = 3, F4_SB = 3, F4_SP = 3;
+constexpr int F4_SA = 3, F4_SB = 3, F4_SP = 3, F4_NACC = 2;
 constexpr int F4_A_STAGE = F4_BM * F4_KST / 2;     // 16 KB, SW128 K-major
 constexpr int F4_B_STAGE = F4_BN * F4_KST / 2;     // 32 KB, SW128 K-major
 constexpr int F4_P_SLOT = F4_BM * 128;             // 16 KB: 512 packed codes per row (2 stages)
@@ -42,13 +43,13 @@ constexpr int F4_OFF_B = 0;
 constexpr int F4_OFF_A = F4_OFF_B + F4_SB * F4_B_STAGE;
 constexpr int F4_OFF_P = F4_OFF_A + F4_SA * F4_A_STAGE;
 constexpr int F4_OFF_BAR = F4_OFF_P + F4_SP * F4_P_SLOT;
-constexpr int F4_NBAR = 2 * F4_SP + 2 * F4_SB + 2 * F4_SA + 2;
+constexpr int F4_NBAR = 2 * F4_SP + 2 * F4_SB + 2 * F4_SA + 2 * F4_NACC;
 constexpr int F4_OFF_TMEM = F4_OFF_BAR + F4_NBAR * 8;
 constexpr int F4_ALLOC = F4_OFF_TMEM + 16 + 1024;
 static_assert(F4_ALLOC <= 232448, "shared memory budget");
 constexpr int F4_EPI0 = 0, F4_UNP0 = 4, F4_PROD = 8, F4_WAIT = 9, F4_MMA = 10, F4_NT = 32 * 11;
 constexpr int F4_HANDOFF_BAR = 1;
-constexpr uint32_t F4_SF_COL = 256;  // TMEM columns [256, 288): block scales (every byte 2^1)
+constexpr uint32_t F4_SF_COL = 480;  // TMEM columns [480, 512): block scales (every byte 2^1)
 
 // instruction descriptor: kind::mxf4, e2m1 x e2m1, ue8m0 scales, K-major, dense K = 64
 __host__ __device__ constexpr uint32_t idesc_mxf4(int M, int N) {
@@ -95,8 +96,8 @@ lut_gemm_f4_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
     auto empty_b = [&](int s) { return bar0 + 8 * (2 * F4_SP + F4_SB + s); };
     auto full_a = [&](int s) { return bar0 + 8 * (2 * F4_SP + 2 * F4_SB + s); };
     auto empty_a = [&](int s) { return bar0 + 8 * (2 * F4_SP + 2 * F4_SB + F4_SA + s); };
-    const uint32_t acc_full = bar0 + 8 * (2 * F4_SP + 2 * F4_SB + 2 * F4_SA);
-    const uint32_t acc_empty = acc_full + 8;
+    auto acc_full = [&](int a) { return bar0 + 8 * (2 * F4_SP + 2 * F4_SB + 2 * F4_SA + a); };
+    auto acc_empty = [&](int a) { return bar0 + 8 * (2 * F4_SP + 2 * F4_SB + 2 * F4_SA + F4_NACC + a); };
     uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + F4_OFF_TMEM);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
 
@@ -116,8 +117,10 @@ lut_gemm_f4_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
                 ptx::mbar_init(full_a(s), 4);
                 ptx::mbar_init(empty_a(s), 1);
             }
-            ptx::mbar_init(acc_full, 1);
-            ptx::mbar_init(acc_empty, 4);
+            for (int a = 0; a < F4_NACC; ++a) {
+                ptx::mbar_init(acc_full(a), 1);
+                ptx::mbar_init(acc_empty(a), 4);
+            }
             ptx::fence_mbar_init();
         }
         __syncwarp();
@@ -167,7 +170,7 @@ lut_gemm_f4_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
     } else if (warp == F4_WAIT) {
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-            ptx::mbar_wait(acc_empty, (tl & 1u) ^ 1u);
+            ptx::mbar_wait(acc_empty(tl % F4_NACC), ((tl / F4_NACC) & 1u) ^ 1u);
             for (int s = 0; s < fa.nstages; ++s, ++g) {
                 ptx::mbar_wait(full_a(g % F4_SA), (g / F4_SA) & 1u);
                 ptx::mbar_wait(full_b(g % F4_SB), (g / F4_SB) & 1u);
@@ -177,8 +180,9 @@ lut_gemm_f4_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
     } else if (warp == F4_MMA) {
         constexpr uint32_t idesc = idesc_mxf4(F4_BM, F4_BN);
         const uint32_t sfa = tmem + F4_SF_COL, sfb = tmem + F4_SF_COL + 16;
-        uint32_t g = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        uint32_t g = 0, tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const uint32_t dt = tmem + (tl % F4_NACC) * F4_BN;
             for (int s = 0; s < fa.nstages; ++s, ++g) {
                 const int sa = (int)(g % F4_SA), bs = (int)(g % F4_SB);
                 ptx::named_bar_sync(F4_HANDOFF_BAR, 64);
@@ -187,10 +191,10 @@ lut_gemm_f4_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
                 const uint64_t bd = ptx::desc_k_sw128(sbase + F4_OFF_B + bs * F4_B_STAGE);
                 const int nk = s < fa.nstages - 1 ? 4 : fa.last_ksteps;
                 for (int k = 0; k < nk; ++k)   // k-step = 64 codes = 32 bytes of every row (+2 in 16-byte units)
-                    mma_mxf4_warp(tmem, ad + 2 * k, bd + 2 * k, idesc, (s > 0 || k > 0) ? 1u : 0u, sfa, sfb);
+                    mma_mxf4_warp(dt, ad + 2 * k, bd + 2 * k, idesc, (s > 0 || k > 0) ? 1u : 0u, sfa, sfb);
                 ptx::mma_commit_warp(empty_a(sa));
                 ptx::mma_commit_warp(empty_b(bs));
-                if (s == fa.nstages - 1) ptx::mma_commit_warp(acc_full);
+                if (s == fa.nstages - 1) ptx::mma_commit_warp(acc_full(tl % F4_NACC));
                 __syncwarp();
             }
         }
@@ -248,29 +252,31 @@ lut_gemm_f4_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
             f4_tile(fa, t, tn, tm);
             const int64_t n = (int64_t)tn * F4_BM + quarter * 32 + lane;
             const int64_t m0 = (int64_t)tm * F4_BN;
-            ptx::mbar_wait(acc_full, tl & 1u);
+            const uint32_t acc = tl % F4_NACC;
+            ptx::mbar_wait(acc_full(acc), (tl / F4_NACC) & 1u);
             ptx::tc_fence_after();
-            const uint32_t trow = tmem + ((uint32_t)(quarter * 32) << 16);
+            const uint32_t trow = tmem + acc * F4_BN + ((uint32_t)(quarter * 32) << 16);
+            constexpr int NCH = (F4_BN + 31) / 32;   // (columns >= F4_BN of the last chunk are not stored)
 #pragma unroll 1
-            for (int c = 0; c < F4_BN / 32; c += 2) {
+            for (int c = 0; c < NCH; c += 2) {
                 uint32_t r0[32], r1[32];
                 ptx::tmem_ld_32x32b_x32(trow + c * 32, r0);
                 ptx::tmem_ld_32x32b_x32(trow + c * 32 + 32, r1);
                 ptx::tmem_ld_wait();
-                if (c + 2 >= F4_BN / 32) {   // accumulator free for the next tile
+                if (c + 2 >= NCH) {   // the accumulator buffer is free again
                     ptx::tc_fence_before();
                     __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(acc_empty);
+                    if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
                 }
                 if (n < fa.N) {
-                    int32_t *cp = fa.C + m0 * fa.ldc + c * 32 * fa.ldc + n;
+                    int32_t *cp = fa.C + (m0 + c * 32) * fa.ldc + n;
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
-                        if (m0 + c * 32 + j < fa.M)
+                        if (c * 32 + j < F4_BN && m0 + c * 32 + j < fa.M)
                             cp[(int64_t)j * fa.ldc] = __float_as_int(__uint_as_float(r0[j]) + 12582912.0f) - 0x4B400000;
 #pragma unroll
                     for (int j = 0; j < 32; ++j)
-                        if (m0 + c * 32 + 32 + j < fa.M)
+                        if (c * 32 + 32 + j < F4_BN && m0 + c * 32 + 32 + j < fa.M)
                             cp[(int64_t)(32 + j) * fa.ldc] = __float_as_int(__uint_as_float(r1[j]) + 12582912.0f) - 0x4B400000;
                 }
             }
