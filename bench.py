@@ -371,8 +371,13 @@ def run_gemm(args, ws, rank, local):
     n = args.n
     r0, r1 = shard.row_shard(rank, ws, n)
     m_loc = r1 - r0
-    wl, al = synth.learned_levels(5, 0, synth.T_LEVELS)
-    lut = dg.build_lut(wl, al, 16)
+    f4 = args.variant == "f4"
+    if args.levels == "uniform" or f4:   # config-1 levels (the FP4 path needs e2m1-representable levels)
+        wl, al = list(synth.WL_UNIFORM), list(synth.AL_UNIFORM)
+        lut = dg.build_lut(wl, al, 8)
+    else:
+        wl, al = synth.learned_levels(5, 0, synth.T_LEVELS)
+        lut = dg.build_lut(wl, al, 16)
     dev = "cuda"
     ld = dg.packed_ld(n)
     # codes: W rows [rank*m_loc, (rank+1)*m_loc), A^T all n rows; counter generator (same on CPU)
@@ -385,11 +390,15 @@ def run_gemm(args, ws, rank, local):
         r1 = min(n, r0 + chunk)
         c = synth.counter_codes(r0 * n, (r1 - r0) * n, (5, n, synth.T_A), "uniform", dev).view(r1 - r0, n)
         dg.pack_codes(c, out=at[r0:r1])
-    at8 = dg.expand_operand(at, n, al)          # offline expansion of the second operand
+    if f4:   # block-scaled FP4 path: the weights are expanded once to e2m1, activations stay packed
+        w4 = dg.expand_operand_f4(w, n, wl)
+        at8 = None
+    else:
+        at8 = dg.expand_operand(at, n, al)          # offline expansion of the second operand
     # N > 1: fused GEMM + all-gather (the epilogue stores each tile into every rank's C over
     # NVLink P2P, symmetric memory) when available, else GEMM then NCCL all_gather_into_tensor
     peer = None
-    if ws > 1 and not args.nccl_gather:
+    if ws > 1 and not args.nccl_gather and not f4:
         try:
             peer = shard.PeerRows((n, n), torch.int32, dev, rank, ws, rank * m_loc)
         except Exception as e:  # (no P2P / symmetric memory on this node)
@@ -403,7 +412,9 @@ def run_gemm(args, ws, rank, local):
     ops_total = 2 * n * n * n
 
     def gemm():
-        if peer is not None:
+        if f4:
+            dg.lut_gemm_f4(w4, at, m_loc, n, n, lut, out=c_loc)
+        elif peer is not None:
             dg.lut_gemm_prepared_allgather(w, at8, m_loc, n, n, lut, c_loc, peer.peers)
         else:
             dg.lut_gemm_prepared(w, at8, m_loc, n, n, lut, out=c_loc)
@@ -468,19 +479,28 @@ def run_gemm(args, ws, rank, local):
                   "status": "bit-exact" if bad == 0 and np.array_equal(ref, C[rows]) else "MISMATCH"}
     if rank == 0:
         alg_bytes = m_loc * ld + n * ld + 4 * m_loc * n
+        peak = pk["i8_burst"] * (2 if f4 else 1)
+        peak_s = pk["i8_sustained"] * (2 if f4 else 1)
         line = {"metric": METRIC, "value": round(value, 2), "unit": "TOPS", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_all, 4), "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "int8",
-                "data": "synthetic (seeded counter-based 2-bit codes; learned-style int16 levels, Q17)",
-                "config": {"workload": f"square_gemm_n{n} (BASELINE configs[4])", "n": n,
+                "scaling": "strong", "vs_baseline": None, "dtype": "e2m1" if f4 else "int8",
+                "data": ("synthetic (seeded counter-based 2-bit codes; config-1 levels wl={-2..1}, al={0..3})"
+                         if wl == list(synth.WL_UNIFORM) else
+                         "synthetic (seeded counter-based 2-bit codes; learned-style int16 levels, Q17)"),
+                "config": {"workload": (f"square_gemm_n{n}, config-1 levels, FP4 path (SURVEY 8(f) rank 2)" if f4 else
+                                        f"square_gemm_n{n} (BASELINE configs[4])" + ("" if wl != list(synth.WL_UNIFORM) else ", config-1 levels")),
+                           "n": n,
                            "split": (f"output channels / {ws}; " + ("fused all-gather: epilogue stores every tile into all ranks' C (NVLink P2P, symmetric memory)" if peer is not None else "NCCL all_gather of int32 rows")) if ws > 1 else "none",
                            "l2": "1 GiB int32 output per step (> L2)" if flush is None else "256 MB L2 flush between steps"},
                 "compute_only": {"value": round(comp_tops, 2), "ms": round(ms_comp, 4), "per_gpu_tops": round(per_gpu, 2)},
-                "roofline": {"bound": "tensor", "kernel": "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)",
-                             "achieved": round(per_gpu, 1), "peak": round(pk["i8_burst"], 1), "unit": "TOPS",
-                             "frac": round(per_gpu / pk["i8_burst"], 4),
-                             "frac_vs_sustained_peak": round(per_gpu / pk["i8_sustained"], 4),
-                             "peak_src": pk["src"] + ": int8 = 2 x bf16 burst (kernel timed alone)",
+                "roofline": {"bound": "tensor",
+                             "kernel": ("lut_gemm_f4_kernel (tcgen05 kind::mxf4, e2m1, SS)" if f4 else
+                                        "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)"),
+                             "achieved": round(per_gpu, 1), "peak": round(peak, 1), "unit": "TOPS",
+                             "frac": round(per_gpu / peak, 4),
+                             "frac_vs_sustained_peak": round(per_gpu / peak_s, 4),
+                             "peak_src": pk["src"] + (": e2m1 dense = 4 x bf16 burst (nominal 9/2.25)" if f4 else
+                                                      ": int8 = 2 x bf16 burst (kernel timed alone)"),
                              "alg_bytes_per_launch": alg_bytes, "traffic": None},
                 "gpu_launches": launches, "clocks": clk.summary(), "parity": parity}
         print(json.dumps(line), flush=True)
@@ -527,7 +547,10 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="resnet50", choices=["resnet50", "vgg16", "gemm", "resnet18"])
     ap.add_argument("--n", type=int, default=16384, help="config 5 GEMM size (4096 / 8192 / 16384)")
-    ap.add_argument("--variant", default="auto", choices=["auto", "cc", "tc"])
+    ap.add_argument("--variant", default="auto", choices=["auto", "cc", "tc", "f4"],
+                    help="gemm workload: f4 = block-scaled FP4 path (config-1 levels)")
+    ap.add_argument("--levels", default="learned", choices=["learned", "uniform"],
+                    help="gemm workload: learned int16 levels (BJ configs[4]) or config-1 levels")
     ap.add_argument("--batch", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--oracle-budget", type=float, default=20.0)
