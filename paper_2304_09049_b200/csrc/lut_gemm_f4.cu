@@ -35,7 +35,7 @@ constexpr int F4_BM = 128;           // activation rows per tile (MMA M, TMEM la
 constexpr int F4_BN = 240;           // weight rows per tile (MMA N): 2 x 240 fp32 accumulator columns + 32
                                      // block-scale columns fill the 512 TMEM columns
 constexpr int F4_KST = 256;          // codes per pipeline stage = 128 bytes of e2m1 per row = 4 MMAs
-constexpr int F4_SA = 3, F4_SB = 3, F4_SP = 3, F4_NACC = 2;
+constexpr int F4_SA = 4, F4_SB = 4, F4_SP = 2, F4_NACC = 2;
 constexpr int F4_A_STAGE = F4_BM * F4_KST / 2;     // 16 KB, SW128 K-major
 constexpr int F4_B_STAGE = F4_BN * F4_KST / 2;     // 32 KB, SW128 K-major
 constexpr int F4_P_SLOT = F4_BM * 128;             // 16 KB: 512 packed codes per row (2 stages)
