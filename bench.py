@@ -385,7 +385,13 @@ def run_gemm(args, ws, rank, local):
     r0, r1 = shard.row_shard(rank, ws, n)
     m_loc = r1 - r0
     f4 = args.variant == "f4"
-    if args.levels == "uniform" or f4:   # config-1 levels (the FP4 path needs e2m1-representable levels)
+    onehot = args.variant == "onehot"
+    T_any = None
+    if onehot:   # an arbitrary (non-product) int8 table, seeded: the one-hot K' = 4K tensor-core path
+        T_any = np.random.default_rng(synth.MASTER_SEED + 5).integers(-127, 128, 16).astype(np.int32)
+        lut = dg.lut_from_table(T_any, 8)
+        wl = al = None
+    elif args.levels == "uniform" or f4:   # config-1 levels (the FP4 path needs e2m1-representable levels)
         wl, al = list(synth.WL_UNIFORM), list(synth.AL_UNIFORM)
         lut = dg.build_lut(wl, al, 8)
     else:
@@ -406,12 +412,16 @@ def run_gemm(args, ws, rank, local):
     if f4:   # block-scaled FP4 path: the weights are expanded once to e2m1, activations stay packed
         w4 = dg.expand_operand_f4(w, n, wl)
         at8 = None
+    elif onehot:   # both operands expanded once: one-hot weight codes, int8 table columns
+        w1h = dg.expand_onehot(w, n)
+        atc = dg.expand_tcols(at, n, lut)
+        at8 = None
     else:
         at8 = dg.expand_operand(at, n, al)          # offline expansion of the second operand
     # N > 1: fused GEMM + all-gather (the epilogue stores each tile into every rank's C over
     # NVLink P2P, symmetric memory) when available, else GEMM then NCCL all_gather_into_tensor
     peer = None
-    if ws > 1 and not args.nccl_gather and not f4:
+    if ws > 1 and not args.nccl_gather and not f4 and not onehot:
         try:
             peer = shard.PeerRows((n, n), torch.int32, dev, rank, ws, rank * m_loc)
         except Exception as e:  # (no P2P / symmetric memory on this node)
@@ -427,6 +437,8 @@ def run_gemm(args, ws, rank, local):
     def gemm():
         if f4:
             dg.lut_gemm_f4(w4, at, m_loc, n, n, lut, out=c_loc)
+        elif onehot:
+            dg.lut_gemm_onehot(w1h, atc, m_loc, n, n, lut, out=c_loc)
         elif peer is not None:
             dg.lut_gemm_prepared_allgather(w, at8, m_loc, n, n, lut, c_loc, peer.peers)
         else:
@@ -484,7 +496,7 @@ def run_gemm(args, ws, rank, local):
         C = c_loc.cpu().numpy()
         Wc = synth.counter_codes(rank * m_loc * n, m_loc * n, (5, n, synth.T_W), "uniform", "cpu").view(m_loc, n).numpy()
         Atc = synth.counter_codes(0, n * n, (5, n, synth.T_A), "uniform", "cpu").view(n, n).numpy()
-        T = oracle.build_lut16(wl, al)
+        T = T_any if onehot else oracle.build_lut16(wl, al)
         bad = oracle.freivalds_rows(Wc, Atc, C, T, trials=2)
         rows = [0, m_loc - 1]
         ref = oracle.lut_gemm(Wc[rows], np.ascontiguousarray(Atc.T), T)
@@ -492,15 +504,18 @@ def run_gemm(args, ws, rank, local):
                   "status": "bit-exact" if bad == 0 and np.array_equal(ref, C[rows]) else "MISMATCH"}
     if rank == 0:
         alg_bytes = m_loc * ld + n * ld + 4 * m_loc * n
-        peak = pk["i8_burst"] * (2 if f4 else 1)
-        peak_s = pk["i8_sustained"] * (2 if f4 else 1)
+        scale = 2.0 if f4 else (0.25 if onehot else 1.0)   # onehot: 4K MMA terms per K lookups
+        peak = pk["i8_burst"] * scale
+        peak_s = pk["i8_sustained"] * scale
         line = {"metric": METRIC, "value": round(value, 2), "unit": "TOPS", "n_gpus": ws, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": round(ms_all, 4), "higher_is_better": True,
                 "scaling": "strong", "vs_baseline": None, "dtype": "e2m1" if f4 else "int8",
-                "data": ("synthetic (seeded counter-based 2-bit codes; config-1 levels wl={-2..1}, al={0..3})"
+                "data": ("synthetic (seeded counter-based 2-bit codes; seeded random non-product int8 table)" if onehot else
+                         "synthetic (seeded counter-based 2-bit codes; config-1 levels wl={-2..1}, al={0..3})"
                          if wl == list(synth.WL_UNIFORM) else
                          "synthetic (seeded counter-based 2-bit codes; learned-style int16 levels, Q17)"),
                 "config": {"workload": (f"square_gemm_n{n}, config-1 levels, FP4 path (SURVEY 8(f) rank 2)" if f4 else
+                                        f"square_gemm_n{n}, non-product int8 table, one-hot K'=4K tensor-core path (SURVEY 8(f) rank 3)" if onehot else
                                         f"square_gemm_n{n} (BASELINE configs[4])" + ("" if wl != list(synth.WL_UNIFORM) else ", config-1 levels")),
                            "n": n,
                            "split": (f"output channels / {ws}; " + ("fused all-gather: epilogue stores every tile into all ranks' C (NVLink P2P, symmetric memory)" if peer is not None else "NCCL all_gather of int32 rows")) if ws > 1 else "none",
@@ -513,6 +528,7 @@ def run_gemm(args, ws, rank, local):
                              "frac": round(per_gpu / peak, 4),
                              "frac_vs_sustained_peak": round(per_gpu / peak_s, 4),
                              "peak_src": pk["src"] + (": e2m1 dense = 4 x bf16 burst (nominal 9/2.25)" if f4 else
+                                                      ": int8 = 2 x bf16 burst / 4 (the one-hot form runs 4K int8 MACs per K lookups)" if onehot else
                                                       ": int8 = 2 x bf16 burst (kernel timed alone)"),
                              "alg_bytes_per_launch": alg_bytes, "traffic": None},
                 "gpu_launches": launches, "clocks": clk.summary(), "parity": parity}
@@ -560,8 +576,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="resnet50", choices=["resnet50", "vgg16", "gemm", "resnet18"])
     ap.add_argument("--n", type=int, default=16384, help="config 5 GEMM size (4096 / 8192 / 16384)")
-    ap.add_argument("--variant", default="auto", choices=["auto", "cc", "tc", "f4"],
-                    help="gemm workload: f4 = block-scaled FP4 path (config-1 levels)")
+    ap.add_argument("--variant", default="auto", choices=["auto", "cc", "tc", "f4", "onehot"],
+                    help="gemm workload: f4 = block-scaled FP4 path (config-1 levels); onehot = any int8 table (K' = 4K)")
     ap.add_argument("--levels", default="learned", choices=["learned", "uniform"],
                     help="gemm workload: learned int16 levels (BJ configs[4]) or config-1 levels")
     ap.add_argument("--batch", type=int, default=0)

@@ -192,6 +192,28 @@ DG_API int64_t dg_expand_ld(int64_t K);
 DG_API dg_status dg_expand_operand(const uint8_t *d_packed, int64_t rows, int64_t K, int64_t ld,
                             const int32_t levels[4], int8_t *d_out, int64_t ld_out, void *stream);
 
+/* Non-product tables on the int8 tensor cores (the one-hot K' = 4K form).
+ * Any table splits over the weight code, T[(w<<2)|a] = sum_i [w == i] * T[(i<<2)|a] (Alg. 1's
+ * lookup), so C = P' . Q'^T over K' = 4K with
+ *      P'[m][4k+i] = [W[m][k] == i]   (packed 2-bit one-hot codes: byte k = 1 << (2 W[m][k]))
+ *      Q'[n][4k+i] = T[(i<<2) | A[k][n]]   (int8, in the tensor-core operand order of
+ *                                           dg_expand_operand; 0 for k >= K)
+ * an exact int8 dot product.  dg_expand_onehot: packed weights [rows][ld] -> [rows][ld_out]
+ * (ld_out >= dg_onehot_ld(K) = roundup(K, 16), a multiple of 16); dg_expand_tcols: packed
+ * activations [rows][ld] -> int8 [rows][ld_out] (ld_out >= dg_tcols_ld(K) = dg_expand_ld(4K), a
+ * multiple of 128, 128-byte aligned); both once per operand.  dg_lut_gemm_onehot: output and
+ * rq as dg_lut_gemm.  Requires every |entry| <= 127 (else DG_ERR_UNSUPPORTED); d_atc must have
+ * been built from the same table.  4x the MMA work of the product-table path, any table.     */
+DG_API int64_t dg_onehot_ld(int64_t K);
+DG_API int64_t dg_tcols_ld(int64_t K);
+DG_API dg_status dg_expand_onehot(const uint8_t *d_w, int64_t rows, int64_t K, int64_t ld, uint8_t *d_out,
+                                  int64_t ld_out, void *stream);
+DG_API dg_status dg_expand_tcols(const uint8_t *d_at, int64_t rows, int64_t K, int64_t ld, const dg_lut *lut,
+                                 int8_t *d_out, int64_t ld_out, void *stream);
+DG_API dg_status dg_lut_gemm_onehot(const uint8_t *d_w1h, int64_t ldw1h, const int8_t *d_atc, int64_t ldatc,
+                                    int64_t M, int64_t N, int64_t K, const dg_lut *lut, void *d_c, int64_t ldc,
+                                    const dg_requant *rq, void *stream);
+
 /* Block-scaled FP4 tensor-core path (tcgen05 kind::mxf4, e2m1 x e2m1):
  *      C[m][n] = sum_{k<K} lut.entries[(W[m][k] << 2) | A[k][n]]     (int32, exact)
  * for product tables whose activation levels are lut->al = {0, 1, 2, 3} (the activation code is

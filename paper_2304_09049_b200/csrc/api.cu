@@ -160,6 +160,47 @@ dg_status dg_expand_operand(const uint8_t *d_packed, int64_t rows, int64_t K, in
     return expand_operand(d_packed, rows, K, ld, levels, d_out, ld_out, (cudaStream_t)stream);
 }
 
+int64_t dg_onehot_ld(int64_t K) { return K <= 0 ? 0 : onehot_ld(K); }
+int64_t dg_tcols_ld(int64_t K) { return K <= 0 ? 0 : tcols_ld(K); }
+
+dg_status dg_expand_onehot(const uint8_t *d_w, int64_t rows, int64_t K, int64_t ld, uint8_t *d_out, int64_t ld_out,
+                           void *stream) {
+    if (!d_w || !d_out) return DG_ERR_INVALID_ARG;
+    if (rows < 0 || K <= 0 || ld * 4 < K || ld % 4 || ld_out < onehot_ld(K) || ld_out % 16) return DG_ERR_SHAPE;
+    if (((uintptr_t)d_w & 3) || !aligned16(d_out)) return DG_ERR_INVALID_ARG;
+    return expand_onehot(d_w, rows, K, ld, d_out, ld_out, (cudaStream_t)stream);
+}
+
+dg_status dg_expand_tcols(const uint8_t *d_at, int64_t rows, int64_t K, int64_t ld, const dg_lut *lut, int8_t *d_out,
+                          int64_t ld_out, void *stream) {
+    if (!d_at || !lut || !d_out) return DG_ERR_INVALID_ARG;
+    if (rows < 0 || K <= 0 || ld * 4 < K || ld_out < tcols_ld(K) || ld_out % 128) return DG_ERR_SHAPE;
+    if ((uintptr_t)d_out & 127) return DG_ERR_INVALID_ARG;
+    if (max_abs_entry(lut->entries) > 127) return DG_ERR_UNSUPPORTED;
+    return expand_tcols(d_at, rows, K, ld, lut->entries, d_out, ld_out, (cudaStream_t)stream);
+}
+
+dg_status dg_lut_gemm_onehot(const uint8_t *d_w1h, int64_t ldw1h, const int8_t *d_atc, int64_t ldatc, int64_t M,
+                             int64_t N, int64_t K, const dg_lut *lut, void *d_c, int64_t ldc, const dg_requant *rq,
+                             void *stream) {
+    if (!d_w1h || !d_atc || !lut || !d_c) return DG_ERR_INVALID_ARG;
+    if (M <= 0 || N <= 0 || K <= 0) return DG_ERR_SHAPE;
+    if (ldw1h % 16 || ldw1h < onehot_ld(K) || ldatc < tcols_ld(K) || ldatc % 128) return DG_ERR_SHAPE;
+    if (!aligned16(d_w1h) || ((uintptr_t)d_atc & 127)) return DG_ERR_INVALID_ARG;
+    if (rq ? (ldc * 4 < N) : (ldc < N)) return DG_ERR_SHAPE;
+    dg_status s = check_rq(rq);
+    if (s != DG_OK) return s;
+    const int64_t emax = max_abs_entry(lut->entries);
+    if (emax > 127 || !tc_available()) return DG_ERR_UNSUPPORTED;
+    if (K * emax >= ((int64_t)1 << 31)) return DG_ERR_OVERFLOW;
+    RequantArgs a{};
+    if (rq) a = to_args(rq);
+    // one-hot side: codes 0 / 1 with identity levels; the expanded side's "levels" only bound |acc|
+    const int32_t pl[4] = {0, 1, 0, 0}, ql[4] = {(int32_t)emax, 0, 0, 0};
+    return lut_gemm_ts(d_w1h, ldw1h, d_atc, ldatc, M, N, 4 * K, pl, ql, d_c, ldc, rq ? &a : nullptr,
+                       (cudaStream_t)stream);
+}
+
 int64_t dg_expand_f4_ld(int64_t K) { return K <= 0 ? 0 : expand_f4_ld(K); }
 
 dg_status dg_expand_operand_f4(const uint8_t *d_packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],

@@ -214,6 +214,12 @@ int64_t expand_ld(int64_t K);
 dg_status expand_operand(const uint8_t *packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],
                          int8_t *out, int64_t ld8, cudaStream_t st);
 // implicit-GEMM convolution description for the TS kernel (P = im2col of x, gathered on chip)
+int64_t onehot_ld(int64_t K);
+int64_t tcols_ld(int64_t K);
+dg_status expand_onehot(const uint8_t *w, int64_t rows, int64_t K, int64_t ld, uint8_t *out, int64_t ld_out,
+                        cudaStream_t st);
+dg_status expand_tcols(const uint8_t *a, int64_t rows, int64_t K, int64_t ld, const int32_t entries[16], int8_t *out,
+                       int64_t ld_out, cudaStream_t st);
 int64_t expand_f4_ld(int64_t K);
 int f4_nibble_half(int32_t v);
 dg_status expand_operand_f4(const uint8_t *packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],

@@ -79,6 +79,11 @@ def lib():
             "dg_expand_operand": ([P, i64, i64, i64, P, P, i64, P], i32),
             "dg_lut_gemm_prepared": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, P], i32),
             "dg_lut_gemm_prepared_allgather": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, i32, P], i32),
+            "dg_onehot_ld": ([i64], i64),
+            "dg_tcols_ld": ([i64], i64),
+            "dg_expand_onehot": ([P, i64, i64, i64, P, i64, P], i32),
+            "dg_expand_tcols": ([P, i64, i64, i64, P, P, i64, P], i32),
+            "dg_lut_gemm_onehot": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, P], i32),
             "dg_expand_f4_ld": ([i64], i64),
             "dg_expand_operand_f4": ([P, i64, i64, i64, P, P, i64, P], i32),
             "dg_lut_gemm_f4": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P], i32),
@@ -274,6 +279,42 @@ def expand_operand(packed: torch.Tensor, K: int, levels, out: torch.Tensor | Non
     lv = (ctypes.c_int32 * 4)(*[int(x) for x in levels])
     _check(lib().dg_expand_operand(_ptr(packed), rows, K, ld, lv, _ptr(out), out.shape[1], _stream(stream)),
            "dg_expand_operand")
+    return out
+
+
+def expand_onehot(w: torch.Tensor, K: int, out: torch.Tensor | None = None, stream=None):
+    """Packed weights [rows][ld] -> packed one-hot codes [rows][onehot_ld(K)] (K' = 4K)."""
+    _dev(w, torch.uint8, "w")
+    rows, ld = w.shape
+    if out is None:
+        out = torch.empty((rows, int(lib().dg_onehot_ld(K))), dtype=torch.uint8, device=w.device)
+    _check(lib().dg_expand_onehot(_ptr(w), rows, K, ld, _ptr(out), out.shape[1], _stream(stream)), "dg_expand_onehot")
+    return out
+
+
+def expand_tcols(at: torch.Tensor, K: int, lut: dg_lut, out: torch.Tensor | None = None, stream=None):
+    """Packed activations [rows][ld] -> int8 table columns T[(i<<2)|a] at k' = 4k+i [rows][tcols_ld(K)]."""
+    _dev(at, torch.uint8, "at")
+    rows, ld = at.shape
+    if out is None:
+        out = torch.empty((rows, int(lib().dg_tcols_ld(K))), dtype=torch.int8, device=at.device)
+    _check(lib().dg_expand_tcols(_ptr(at), rows, K, ld, ctypes.byref(lut), _ptr(out), out.shape[1], _stream(stream)),
+           "dg_expand_tcols")
+    return out
+
+
+def lut_gemm_onehot(w1h: torch.Tensor, atc: torch.Tensor, M: int, N: int, K: int, lut: dg_lut,
+                    rq: Requant | None = None, out: torch.Tensor | None = None, stream=None):
+    """Any int8 16-entry table on the tensor cores: w1h = expand_onehot(W), atc = expand_tcols(At, lut)."""
+    _dev(w1h, torch.uint8, "w1h")
+    _dev(atc, torch.int8, "atc")
+    if out is None:
+        out = (torch.empty((M, (N + 3) // 4), dtype=torch.uint8, device=w1h.device) if rq is not None
+               else torch.empty((M, N), dtype=torch.int32, device=w1h.device))
+    r = rq.c() if rq is not None else None
+    _check(lib().dg_lut_gemm_onehot(_ptr(w1h), w1h.shape[1], _ptr(atc), atc.shape[1], M, N, K, ctypes.byref(lut),
+                                    _ptr(out), out.shape[1], ctypes.byref(r) if r is not None else None,
+                                    _stream(stream)), "dg_lut_gemm_onehot")
     return out
 
 

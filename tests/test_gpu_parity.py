@@ -623,3 +623,48 @@ def test_gemm_f4_rejects():
         ab = gpu_pack(np.zeros((N, big), np.uint8))
         dg.lut_gemm_f4(dg.expand_operand_f4(wb, big, [-12, 0, 1, 2]), ab, M, N, big,
                        dg.build_lut([-12, 0, 1, 2], AL, 8))
+
+
+# ---- non-product tables on the tensor cores (one-hot K' = 4K form) ----------
+@pytest.mark.parametrize("seed", range(6))
+def test_gemm_onehot_non_product_vs_oracle(seed):
+    """Arbitrary int8 tables (not wl x al): dg_expand_onehot + dg_expand_tcols + dg_lut_gemm_onehot
+    equal the oracle's direct lookup sum bit for bit, ragged M / N / K, several tiles."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    g = np.random.default_rng(300 + seed)
+    amp = [1, 5, 60, 127, 127, 100][seed]
+    T = g.integers(-amp, amp + 1, 16).astype(np.int32)
+    M, N, K = [(31, 17, 100), (64, 130, 257), (300, 200, 576), (96, 40, 333), (256, 384, 2000), (129, 65, 7)][seed]
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    lut = dg.lut_from_table(T, 8)
+    w1h = dg.expand_onehot(gpu_pack(W, weights=True), K)
+    atc = dg.expand_tcols(gpu_pack(np.ascontiguousarray(A.T)), K, lut)
+    C = host(dg.lut_gemm_onehot(w1h, atc, M, N, K, lut))
+    assert np.array_equal(C, oracle.lut_gemm(W, A, T))
+
+
+def test_gemm_onehot_operands_and_requant():
+    """The one-hot operand is 1 << (2 * code) per original code (documented packed format); the fused
+    requant epilogue on the K' = 4K path equals the oracle's requantised codes; >127 entries refused."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    g = np.random.default_rng(77)
+    T = g.integers(-100, 101, 16).astype(np.int32)
+    M, N, K = 128, 256, 576
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    lut = dg.lut_from_table(T, 8)
+    w1h = host(dg.expand_onehot(gpu_pack(W, weights=True), K))
+    assert np.array_equal(w1h[:, :K], (1 << (2 * W.astype(np.int32))).astype(np.uint8))
+    assert not w1h[:, K:].any()
+    exp = oracle.lut_gemm(W, A, T)
+    rq = dg.Requant(20180, 20, 1, 0, 3)
+    codes = dg.lut_gemm_onehot(torch.from_numpy(w1h).to(DEV), dg.expand_tcols(gpu_pack(np.ascontiguousarray(A.T)), K, lut),
+                               M, N, K, lut, rq=rq)
+    got = oracle.unpack_codes(host(codes), M, N, codes.shape[1])
+    assert np.array_equal(got, oracle.requantize(exp, 20180, 20, 1, 0, 3))
+    big = dg.lut_from_table(np.full(16, 200, np.int32), 16)
+    with pytest.raises(dg.DGError, match="UNSUPPORTED"):
+        dg.expand_tcols(gpu_pack(np.ascontiguousarray(A.T)), K, big)

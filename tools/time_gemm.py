@@ -27,6 +27,10 @@ for s in a.shapes.split(","):
             continue
         if v == "prepared":
             f = lambda: dg.lut_gemm_prepared(w, at8, M, N, ld * 4, lut, out=out)
+        elif v == "onehot":   # any int8 table on the tensor cores (K' = 4K)
+            w1h = dg.expand_onehot(w, ld * 4)
+            atc = dg.expand_tcols(at, ld * 4, lut)
+            f = lambda: dg.lut_gemm_onehot(w1h, atc, M, N, ld * 4, lut, out=out)
         elif v == "f4":   # block-scaled FP4 path: weights expanded once to e2m1
             w4 = dg.expand_operand_f4(w, ld * 4, lut.wl)
             f = lambda: dg.lut_gemm_f4(w4, at, M, N, ld * 4, lut, out=out)
