@@ -52,6 +52,7 @@ def _load():
         lib.or_unpack_codes.argtypes = [P, i64, i64, i64, P]
         lib.or_build_lut16.argtypes = [P, P, P]
         lib.or_lut_gemm.argtypes = [P, P, i64, i64, i64, P, P]
+        lib.or_lut_gemm_bits.argtypes = [P, P, i64, i64, i64, i32, P, P]
         lib.or_lut_gemm.restype = ctypes.c_int
         lib.or_conv2d_direct.argtypes = [P, P] + [i32] * 9 + [ctypes.c_uint8, P, P]
         lib.or_conv2d_direct.restype = ctypes.c_int
@@ -100,6 +101,22 @@ def lut_gemm(W: np.ndarray, A: np.ndarray, T) -> np.ndarray:
     assert K == K2 and T.size == 16
     C = np.empty((M, N), np.int32)
     rc = lib.or_lut_gemm(Wp, Ap, M, N, K, Tp, C.ctypes.data_as(ctypes.c_void_p))
+    if rc != 0:
+        raise OverflowError("oracle: accumulator does not fit int32")
+    return C
+
+
+def lut_gemm_bits(W: np.ndarray, A: np.ndarray, T, bits: int) -> np.ndarray:
+    """C[m][n] = sum_k T[(W[m][k]<<b)|A[k][n]] for b-bit codes (Table 2)."""
+    lib = _load()
+    W, Wp = _c(W, np.uint8)
+    A, Ap = _c(A, np.uint8)
+    T, Tp = _c(T, np.int32)
+    M, K = W.shape
+    K2, N = A.shape
+    assert K == K2 and T.size == 1 << (2 * bits)
+    C = np.empty((M, N), np.int32)
+    rc = lib.or_lut_gemm_bits(Wp, Ap, M, N, K, bits, Tp, C.ctypes.data_as(ctypes.c_void_p))
     if rc != 0:
         raise OverflowError("oracle: accumulator does not fit int32")
     return C

@@ -79,6 +79,31 @@ int or_lut_gemm(const uint8_t *W, const uint8_t *A, int64_t M, int64_t N, int64_
 }
 
 /* ------------------------------------------------------------------------ */
+/* b-bit LUT GEMM (P:183-184 §"Scalability to Larger Bitwidths", Table 2 at P:164-181: for b-bit
+ * operands the index is the b-bit weight code concatenated above the b-bit activation code, a
+ * 2b-bit index into a 2^(2b)-entry table: 64 entries for 3-bit, 256 for 4-bit):
+ *     C[m][n] = sum_{k<K} T[ (W[m][k] << b) | A[k][n] ],   codes in [0, 2^b)
+ * Same loop order and int64 / int32 check as or_lut_gemm (b = 2 is that function). */
+int or_lut_gemm_bits(const uint8_t *W, const uint8_t *A, int64_t M, int64_t N, int64_t K, int32_t bits,
+                     const int32_t *T /* [1 << (2*bits)] */, int32_t *C)
+{
+    int overflow = 0;
+    const int mask = (1 << bits) - 1;
+    for (int64_t m = 0; m < M; ++m)
+        for (int64_t n = 0; n < N; ++n) {
+            int64_t acc = 0;
+            for (int64_t k = 0; k < K; ++k) {
+                int w = W[m * K + k] & mask;
+                int a = A[k * N + n] & mask;
+                acc += T[(w << bits) | a];
+            }
+            if (acc > INT32_MAX || acc < INT32_MIN) overflow = 1;
+            C[m * N + n] = (int32_t)acc;
+        }
+    return overflow ? -1 : 0;
+}
+
+/* ------------------------------------------------------------------------ */
 /* Direct 2-D convolution over codes (the layer the paper lowers to an
  * (M,N,K) GEMM, §5.1), written as the textbook 7-loop definition, NOT
  * via im2col, so that it shares no logic with the GEMM lowering:

@@ -338,3 +338,59 @@ def test_freivalds_accepts_truth_rejects_fault():
         Cb = C.copy()
         Cb[m, n] += 1
         assert oracle.freivalds_rows(W, At, Cb, T) > 0
+
+
+# ---- b-bit LUT GEMM (Table 2) -----------------------------------------
+@pytest.mark.parametrize("bits", [2, 3, 4])
+def test_gemm_bits_closed_form_fp64(bits):
+    """Product tables T[(i<<b)|j] = wl[i]*al[j] (2^(2b) entries, Table 2): C = WL @ AL in fp64
+    (exact: integer partial sums << 2^53), random shapes and level sets."""
+    g = np.random.default_rng(20 + bits)
+    L = 1 << bits
+    for it in range(60):
+        M, N, K = g.integers(1, 40, 3)
+        wl = g.integers(-40, 41, L)
+        al = g.integers(-40, 41, L)
+        T = np.outer(wl, al).reshape(-1).astype(np.int32)     # index (i << b) | j, row-major
+        W = g.integers(0, L, (M, K), dtype=np.uint8)
+        A = g.integers(0, L, (K, N), dtype=np.uint8)
+        C = oracle.lut_gemm_bits(W, A, T, bits)
+        assert np.array_equal(C, (wl[W].astype(np.float64) @ al[A].astype(np.float64)).astype(np.int64)), it
+
+
+@pytest.mark.parametrize("bits,K", [(3, 1), (3, 2), (4, 1), (4, 2)])
+def test_gemm_bits_brute_force_non_product(bits, K):
+    """Every b-bit weight vector x every b-bit activation vector (2^(bK) x 2^(bK)) for a random
+    NON-product 2^(2b)-entry table, against the pair-count decomposition
+    C[m][n] = sum_{i,j} T[i][j] #{k : W[m][k] = i, A[k][n] = j}."""
+    g = np.random.default_rng(30 + 10 * bits + K)
+    L = 1 << bits
+    T = g.integers(-1000, 1000, L * L).astype(np.int32)
+    vecs = np.array(list(itertools.product(range(L), repeat=K)), np.uint8)
+    C = oracle.lut_gemm_bits(vecs, np.ascontiguousarray(vecs.T), T, bits)
+    ohW = np.eye(L, dtype=np.int64)[vecs]
+    ohA = np.eye(L, dtype=np.int64)[np.ascontiguousarray(vecs.T)]
+    counts = np.einsum("mki,knj->mnij", ohW, ohA)
+    assert np.array_equal(C, np.einsum("mnij,ij->mn", counts, T.reshape(L, L).astype(np.int64)))
+
+
+def test_gemm_bits_index_order_and_digit_split():
+    """The weight code is the HIGH part of the index (a transposed table changes the result), and a
+    4-bit activation code a = 4 a_h + a_l with identity levels splits into two 2-bit digit GEMMs:
+    C = G2(W, A_l; wl x {0,1,2,3}) + 4 G2(W, A_h; wl x {0,1,2,3}) for 2-bit W."""
+    g = np.random.default_rng(41)
+    M, N, K = 7, 9, 33
+    T = g.integers(-50, 50, 256).astype(np.int32)
+    W = g.integers(0, 16, (M, K), dtype=np.uint8)
+    A = g.integers(0, 16, (K, N), dtype=np.uint8)
+    Tt = T.reshape(16, 16).T.reshape(-1).copy()
+    assert not np.array_equal(oracle.lut_gemm_bits(W, A, T, 4), oracle.lut_gemm_bits(W, A, Tt, 4))
+    # digit split against the independently pinned 2-bit oracle
+    wl = g.integers(-20, 20, 16)
+    W2 = g.integers(0, 4, (M, K), dtype=np.uint8)
+    wl2 = wl[:4]
+    T4 = np.outer(np.concatenate([wl2, np.zeros(12, np.int64)]), np.arange(16)).reshape(-1).astype(np.int32)
+    Tid = oracle.build_lut16(wl2, [0, 1, 2, 3])
+    lhs = oracle.lut_gemm_bits(W2, A, T4, 4)
+    rhs = oracle.lut_gemm(W2, A & 3, Tid).astype(np.int64) + 4 * oracle.lut_gemm(W2, A >> 2, Tid).astype(np.int64)
+    assert np.array_equal(lhs, rhs)
