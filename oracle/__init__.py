@@ -53,6 +53,7 @@ def _load():
         lib.or_build_lut16.argtypes = [P, P, P]
         lib.or_lut_gemm.argtypes = [P, P, i64, i64, i64, P, P]
         lib.or_lut_gemm_bits.argtypes = [P, P, i64, i64, i64, i32, P, P]
+        lib.or_conv2d_direct_bits.argtypes = [P, P] + [i32] * 9 + [ctypes.c_uint8, i32, P, P]
         lib.or_lut_gemm.restype = ctypes.c_int
         lib.or_conv2d_direct.argtypes = [P, P] + [i32] * 9 + [ctypes.c_uint8, P, P]
         lib.or_conv2d_direct.restype = ctypes.c_int
@@ -136,6 +137,26 @@ def conv2d_direct(x: np.ndarray, w: np.ndarray, T, stride: int, pad: int, pad_co
     out = np.empty((B, Ho, Wo, Cout), np.int32)
     rc = lib.or_conv2d_direct(xp, wp, B, H, Wd, C, Cout, kh, kw, stride, pad, pad_code, Tp,
                               out.ctypes.data_as(ctypes.c_void_p))
+    if rc != 0:
+        raise OverflowError("oracle: accumulator does not fit int32")
+    return out
+
+
+def conv2d_direct_bits(x: np.ndarray, w: np.ndarray, T, stride: int, pad: int, bits: int,
+                       pad_code: int = 0) -> np.ndarray:
+    """Direct NHWC conv over b-bit codes (index (w << b) | x)."""
+    lib = _load()
+    x, xp = _c(x, np.uint8)
+    w, wp = _c(w, np.uint8)
+    T, Tp = _c(T, np.int32)
+    B, H, Wd, C = x.shape
+    Cout, kh, kw, C2 = w.shape
+    assert C == C2 and T.size == 1 << (2 * bits)
+    Ho = (H + 2 * pad - kh) // stride + 1
+    Wo = (Wd + 2 * pad - kw) // stride + 1
+    out = np.empty((B, Ho, Wo, Cout), np.int32)
+    rc = lib.or_conv2d_direct_bits(xp, wp, B, H, Wd, C, Cout, kh, kw, stride, pad, pad_code, bits, Tp,
+                                   out.ctypes.data_as(ctypes.c_void_p))
     if rc != 0:
         raise OverflowError("oracle: accumulator does not fit int32")
     return out

@@ -143,6 +143,40 @@ int or_conv2d_direct(const uint8_t *x, const uint8_t *w, int32_t B, int32_t H, i
     return overflow ? -1 : 0;
 }
 
+/* b-bit direct convolution (or_conv2d_direct with the b-bit index of P:183-184 / Table 2):
+ *   out = sum_{r,s,c} T[(w << b) | x_code], out-of-image taps read pad_code. */
+int or_conv2d_direct_bits(const uint8_t *x, const uint8_t *w, int32_t B, int32_t H, int32_t Wd,
+                          int32_t C, int32_t Cout, int32_t kh, int32_t kw, int32_t stride,
+                          int32_t pad, uint8_t pad_code, int32_t bits, const int32_t *T, int32_t *out)
+{
+    int overflow = 0;
+    const int mask = (1 << bits) - 1;
+    int32_t Ho = (H + 2 * pad - kh) / stride + 1;
+    int32_t Wo = (Wd + 2 * pad - kw) / stride + 1;
+    for (int32_t b = 0; b < B; ++b)
+        for (int32_t ho = 0; ho < Ho; ++ho)
+            for (int32_t wo = 0; wo < Wo; ++wo)
+                for (int32_t co = 0; co < Cout; ++co) {
+                    int64_t acc = 0;
+                    for (int32_t r = 0; r < kh; ++r)
+                        for (int32_t s = 0; s < kw; ++s)
+                            for (int32_t c = 0; c < C; ++c) {
+                                int32_t hi = ho * stride - pad + r;
+                                int32_t wi = wo * stride - pad + s;
+                                int a;
+                                if (hi < 0 || hi >= H || wi < 0 || wi >= Wd)
+                                    a = pad_code & mask;
+                                else
+                                    a = x[(((int64_t)b * H + hi) * Wd + wi) * C + c] & mask;
+                                int wc = w[(((int64_t)co * kh + r) * kw + s) * C + c] & mask;
+                                acc += T[(wc << bits) | a];
+                            }
+                    if (acc > INT32_MAX || acc < INT32_MIN) overflow = 1;
+                    out[(((int64_t)b * Ho + ho) * Wo + wo) * Cout + co] = (int32_t)acc;
+                }
+    return overflow ? -1 : 0;
+}
+
 /* ------------------------------------------------------------------------ */
 /* Integer requantisation (Eq. 1, with s·x realised as the exact
  * rational v·mult / 2^shift, reading Q11; round half away from zero,

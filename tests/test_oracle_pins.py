@@ -394,3 +394,28 @@ def test_gemm_bits_index_order_and_digit_split():
     lhs = oracle.lut_gemm_bits(W2, A, T4, 4)
     rhs = oracle.lut_gemm(W2, A & 3, Tid).astype(np.int64) + 4 * oracle.lut_gemm(W2, A >> 2, Tid).astype(np.int64)
     assert np.array_equal(lhs, rhs)
+
+
+@pytest.mark.parametrize("bits", [2, 4])
+def test_conv_bits_against_pinned_routes(bits):
+    """The b-bit direct conv: at b = 2 it equals the pinned 2-bit direct conv (same T); at b = 4 a
+    1x1 stride-1 conv equals the pinned b-bit GEMM, and a 3x3 conv with every level 1 counts the
+    in-image taps (9 / 6 / 4 x C at interior / edge / corner pixels, pad code 0 = level 0)."""
+    g = np.random.default_rng(50 + bits)
+    L = 1 << bits
+    T = g.integers(-300, 300, L * L).astype(np.int32)
+    x = g.integers(0, L, (2, 6, 5, 3), dtype=np.uint8)
+    w = g.integers(0, L, (4, 3, 3, 3), dtype=np.uint8)
+    got = oracle.conv2d_direct_bits(x, w, T, 1, 1, bits, pad_code=1)
+    if bits == 2:
+        assert np.array_equal(got, oracle.conv2d_direct(x, w, T, 1, 1, pad_code=1))
+        return
+    w1 = g.integers(0, L, (5, 1, 1, 3), dtype=np.uint8)
+    c1 = oracle.conv2d_direct_bits(x, w1, T, 1, 0, bits).reshape(-1, 5)
+    assert np.array_equal(c1, oracle.lut_gemm_bits(w1.reshape(5, 3), np.ascontiguousarray(x.reshape(-1, 3).T), T, bits).T)
+    ones = np.zeros(256, np.int32)
+    ones[(np.arange(16)[:, None] << 4 | np.arange(1, 16)[None, :]).reshape(-1)] = 1   # level 1 unless a = 0
+    xs = g.integers(1, 16, (1, 5, 5, 2), dtype=np.uint8)
+    ws = g.integers(0, 16, (1, 3, 3, 2), dtype=np.uint8)
+    cnt = oracle.conv2d_direct_bits(xs, ws, ones, 1, 1, bits)[0, :, :, 0]
+    assert cnt[2, 2] == 18 and cnt[0, 2] == 12 and cnt[0, 0] == 8
