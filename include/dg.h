@@ -214,6 +214,29 @@ DG_API dg_status dg_lut_gemm_onehot(const uint8_t *d_w1h, int64_t ldw1h, const i
                                     int64_t M, int64_t N, int64_t K, const dg_lut *lut, void *d_c, int64_t ldc,
                                     const dg_requant *rq, void *stream);
 
+/* 4-bit operands (Table 2: b-bit LUTs with 2^(2b) entries) on the
+ * 2-bit tensor-core path, for product tables with IDENTITY activation levels (al[a] = a, a in
+ * 0..15: unsigned ReLU-style codes) and any 16 int8 weight levels with |4 wl| <= 127:
+ *      C[m][n] = sum_{k<K} wl[W[m][k]] * A[k][n]     (= sum_k T[(W << 4) | A], T = wl x {0..15})
+ * A 4-bit code is the two 2-bit digits a = a_l + 4 a_h, and a packed 4-bit row (code k in nibble
+ * k&1 of byte k>>1, low nibble first: the same bytes as the 2-bit packing of the digit sequence
+ * a_l0, a_h0, a_l1, ..., so dg_pack_codes of the digit codes packs it) is a packed 2-bit row of
+ * K' = 2K digits; the weights become Q'[2k] = wl[w_k], Q'[2k+1] = 4 wl[w_k] (dg_expand_digits4:
+ * packed 4-bit weights [rows][ld] -> int8 [rows][ld_out], ld_out >= dg_expand_ld(2K), a multiple
+ * of 128, 128-byte aligned; DG_ERR_RANGE if some |4 wl| > 127).  Out-of-image conv taps read
+ * code 0.
+ * dg_lut_gemm4_prepared: d_at4 [N][lda] packed 4-bit activations, d_w8 = dg_expand_digits4(W);
+ *      output in the activation-major orientation Ct[n][m] (the NHWC convention of the conv
+ *      calls): int32 [N][ldct], or with rq the requantised codes of C^T packed 4 m per byte.
+ * dg_lut_conv2d4_prepared: p->C = the number of 4-bit channels (x: [B][H][W][C/2] bytes),
+ *      d_w8 = dg_expand_digits4 of the packed 4-bit weights [Cout][kh*kw*C] (K order r, s, c);
+ *      p->pad_code must be 0; otherwise as dg_lut_conv2d_prepared.                            */
+DG_API dg_status dg_expand_digits4(const uint8_t *d_w4, int64_t rows, int64_t K, int64_t ld, const int32_t levels[16],
+                                   int8_t *d_out, int64_t ld_out, void *stream);
+DG_API dg_status dg_lut_gemm4_prepared(const uint8_t *d_at4, int64_t lda, const int8_t *d_w8, int64_t ld8, int64_t N,
+                                       int64_t M, int64_t K, const int32_t levels[16], void *d_ct, int64_t ldct,
+                                       const dg_requant *rq, void *stream);
+
 /* Block-scaled FP4 tensor-core path (tcgen05 kind::mxf4, e2m1 x e2m1):
  *      C[m][n] = sum_{k<K} lut.entries[(W[m][k] << 2) | A[k][n]]     (int32, exact)
  * for product tables whose activation levels are lut->al = {0, 1, 2, 3} (the activation code is
@@ -283,6 +306,12 @@ DG_API dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_
 DG_API dg_status dg_lut_conv2d_prepared(const uint8_t *d_x, const int8_t *d_w8, int64_t ld8, const dg_lut *lut,
                                  const dg_conv_params *p, const dg_requant *rq, void *d_out, void *d_ws,
                                  size_t ws_bytes, void *stream);
+
+/* 4-bit convolution (see dg_lut_gemm4_prepared above for the digit form and its requirements). */
+DG_API dg_status dg_lut_conv2d4_prepared(const uint8_t *d_x4, const int8_t *d_w8, int64_t ld8,
+                                         const int32_t levels[16], const dg_conv_params *p,
+                                         const dg_requant *rq, void *d_out, void *d_ws, size_t ws_bytes,
+                                         void *stream);
 
 #ifdef __cplusplus
 }

@@ -201,6 +201,61 @@ dg_status dg_lut_gemm_onehot(const uint8_t *d_w1h, int64_t ldw1h, const int8_t *
                        (cudaStream_t)stream);
 }
 
+// ---- 4-bit operands as 2-bit digit pairs (dg.h)
+static int32_t max_abs16(const int32_t *l) {
+    int32_t m = 0;
+    for (int i = 0; i < 16; ++i) m = (l[i] < 0 ? -l[i] : l[i]) > m ? (l[i] < 0 ? -l[i] : l[i]) : m;
+    return m;
+}
+
+dg_status dg_expand_digits4(const uint8_t *d_w4, int64_t rows, int64_t K, int64_t ld, const int32_t levels[16],
+                            int8_t *d_out, int64_t ld_out, void *stream) {
+    if (!d_w4 || !d_out || !levels) return DG_ERR_INVALID_ARG;
+    if (rows < 0 || K <= 0 || ld * 2 < K || ld_out < expand_ld(2 * K) || ld_out % 128) return DG_ERR_SHAPE;
+    if ((uintptr_t)d_out & 127) return DG_ERR_INVALID_ARG;
+    if (4 * max_abs16(levels) > 127) return DG_ERR_RANGE;
+    return expand_digits4(d_w4, rows, K, ld, levels, d_out, ld_out, (cudaStream_t)stream);
+}
+
+dg_status dg_lut_gemm4_prepared(const uint8_t *d_at4, int64_t lda, const int8_t *d_w8, int64_t ld8, int64_t N, int64_t M,
+                                int64_t K, const int32_t levels[16], void *d_ct, int64_t ldct, const dg_requant *rq,
+                                void *stream) {
+    if (!d_at4 || !d_w8 || !levels || !d_ct) return DG_ERR_INVALID_ARG;
+    if (M <= 0 || N <= 0 || K <= 0) return DG_ERR_SHAPE;
+    if (lda % 16 || lda * 2 < K || ld8 < expand_ld(2 * K) || ld8 % 128) return DG_ERR_SHAPE;
+    if (!aligned16(d_at4) || ((uintptr_t)d_w8 & 127)) return DG_ERR_INVALID_ARG;
+    if (rq ? (ldct * 4 < M) : (ldct < M)) return DG_ERR_SHAPE;
+    dg_status s = check_rq(rq);
+    if (s != DG_OK) return s;
+    const int32_t wmax = max_abs16(levels);
+    if (4 * wmax > 127) return DG_ERR_RANGE;
+    if (!tc_available()) return DG_ERR_UNSUPPORTED;
+    if (K * 15 * (int64_t)wmax >= ((int64_t)1 << 31)) return DG_ERR_OVERFLOW;
+    RequantArgs a{};
+    if (rq) a = to_args(rq);
+    // digit side: identity levels; the weights' side levels only bound |acc| (true bound 15 K wmax)
+    const int32_t pl[4] = {0, 1, 2, 3}, ql[4] = {(5 * wmax + 1) / 2, 0, 0, 0};
+    return lut_gemm_ts(d_at4, lda, d_w8, ld8, N, M, 2 * K, pl, ql, d_ct, ldct, rq ? &a : nullptr, (cudaStream_t)stream);
+}
+
+dg_status dg_lut_conv2d4_prepared(const uint8_t *d_x4, const int8_t *d_w8, int64_t ld8, const int32_t levels[16],
+                                  const dg_conv_params *p, const dg_requant *rq, void *d_out, void *d_ws, size_t ws_bytes,
+                                  void *stream) {
+    if (!d_x4 || !d_w8 || !levels || !p || !d_out) return DG_ERR_INVALID_ARG;
+    if (p->pad_code != 0) return DG_ERR_RANGE;
+    if (p->C <= 0 || p->C % 2) return DG_ERR_SHAPE;
+    const int32_t wmax = max_abs16(levels);
+    if (4 * wmax > 127) return DG_ERR_RANGE;
+    // the same conv over 2C two-bit digit channels with identity activation levels
+    dg_conv_params p2 = *p;
+    p2.C = 2 * p->C;
+    dg_lut lut{};
+    const int32_t wl[4] = {(5 * wmax + 1) / 2, 0, 0, 0}, al[4] = {0, 1, 2, 3};   // (bound: 2 x 3 x 2.5 wmax >= 15 wmax)
+    dg_status s = dg_build_lut(wl, al, 32, &lut);
+    if (s != DG_OK) return s;
+    return dg_lut_conv2d_prepared(d_x4, d_w8, ld8, &lut, &p2, rq, d_out, d_ws, ws_bytes, stream);
+}
+
 int64_t dg_expand_f4_ld(int64_t K) { return K <= 0 ? 0 : expand_f4_ld(K); }
 
 dg_status dg_expand_operand_f4(const uint8_t *d_packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],

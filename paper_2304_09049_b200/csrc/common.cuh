@@ -220,6 +220,8 @@ dg_status expand_onehot(const uint8_t *w, int64_t rows, int64_t K, int64_t ld, u
                         cudaStream_t st);
 dg_status expand_tcols(const uint8_t *a, int64_t rows, int64_t K, int64_t ld, const int32_t entries[16], int8_t *out,
                        int64_t ld_out, cudaStream_t st);
+dg_status expand_digits4(const uint8_t *w4, int64_t rows, int64_t K, int64_t ld, const int32_t levels[16], int8_t *out,
+                         int64_t ld_out, cudaStream_t st);
 int64_t expand_f4_ld(int64_t K);
 int f4_nibble_half(int32_t v);
 dg_status expand_operand_f4(const uint8_t *packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],

@@ -66,6 +66,38 @@ __global__ void expand_tcols_kernel(const uint8_t *__restrict__ a, int64_t rows,
     }
 }
 
+// 4-bit operands through the 2-bit tensor-core path (Table 2):
+// a 4-bit activation code a with identity level is the two 2-bit digits a = a_l + 4 a_h, and a
+// packed 4-bit row (code k in nibble k&1 of byte k>>1, low first) IS a packed 2-bit row of the
+// digits at k' = 2k (a_l) and 2k + 1 (a_h).  So sum_k wl[w_k] a_k = sum_{k'} digit[k'] Q'[k'] with
+// Q'[2k] = wl[w_k], Q'[2k + 1] = 4 wl[w_k]: the weights' side, built here as int8 in the
+// tensor-core operand order (unpack.cuh), 0 for k >= K.  One thread per 16 output bytes.
+struct Lev16 {
+    int8_t v[16];
+};
+__global__ void expand_digits4_kernel(const uint8_t *__restrict__ w4, int64_t rows, int64_t K, int64_t ld,
+                                      const __grid_constant__ Lev16 sl4, int8_t *__restrict__ out, int64_t ld_out) {
+    const int8_t *sl = sl4.v;
+    const int64_t groups = ld_out / 16;
+    const int64_t total = rows * groups;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / groups, g = i - r * groups;   // k' in [16g, 16g + 16): codes k = 8g .. 8g + 7
+        uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            const int kp = b < 8 ? 2 * b : 2 * (b - 8) + 1;
+            const int64_t k = 8 * g + (kp >> 1);
+            int32_t v = 0;
+            if (k < K) {
+                const uint32_t code = (w4[r * ld + (k >> 1)] >> (4 * (k & 1))) & 15u;
+                v = (kp & 1) ? 4 * sl[code] : sl[code];
+            }
+            o[b >> 2] |= ((uint32_t)v & 0xFFu) << (8 * (b & 3));
+        }
+        *reinterpret_cast<uint4 *>(out + r * ld_out + 16 * g) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
 int64_t grid_for(int64_t work) {
     int64_t blocks = (work + 255) / 256;
     const int64_t cap = (int64_t)num_sms() * 8;
@@ -73,6 +105,15 @@ int64_t grid_for(int64_t work) {
 }
 
 }  // namespace
+
+dg_status expand_digits4(const uint8_t *w4, int64_t rows, int64_t K, int64_t ld, const int32_t levels[16], int8_t *out,
+                         int64_t ld_out, cudaStream_t st) {
+    Lev16 l;   // the 16 levels travel by value in the kernel parameters
+    for (int i = 0; i < 16; ++i) l.v[i] = (int8_t)levels[i];
+    if (rows == 0) return DG_OK;
+    expand_digits4_kernel<<<(int)grid_for(rows * (ld_out / 16)), 256, 0, st>>>(w4, rows, K, ld, l, out, ld_out);
+    return launch_status();
+}
 
 int64_t onehot_ld(int64_t K) { return (K + 15) / 16 * 16; }
 int64_t tcols_ld(int64_t K) { return expand_ld(4 * K); }

@@ -84,6 +84,9 @@ def lib():
             "dg_expand_onehot": ([P, i64, i64, i64, P, i64, P], i32),
             "dg_expand_tcols": ([P, i64, i64, i64, P, P, i64, P], i32),
             "dg_lut_gemm_onehot": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, P], i32),
+            "dg_expand_digits4": ([P, i64, i64, i64, P, P, i64, P], i32),
+            "dg_lut_gemm4_prepared": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, P], i32),
+            "dg_lut_conv2d4_prepared": ([P, P, i64, P, P, P, P, P, ctypes.c_size_t, P], i32),
             "dg_expand_f4_ld": ([i64], i64),
             "dg_expand_operand_f4": ([P, i64, i64, i64, P, P, i64, P], i32),
             "dg_lut_gemm_f4": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P], i32),
@@ -315,6 +318,61 @@ def lut_gemm_onehot(w1h: torch.Tensor, atc: torch.Tensor, M: int, N: int, K: int
     _check(lib().dg_lut_gemm_onehot(_ptr(w1h), w1h.shape[1], _ptr(atc), atc.shape[1], M, N, K, ctypes.byref(lut),
                                     _ptr(out), out.shape[1], ctypes.byref(r) if r is not None else None,
                                     _stream(stream)), "dg_lut_gemm_onehot")
+    return out
+
+
+def pack_codes4(codes4: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """4-bit codes [rows][K] -> packed [rows][ld] (code k in nibble k&1 of byte k>>1, low first):
+    the 2-bit packing of the digit sequence (c & 3, c >> 2) per code (dg.h, 4-bit operands)."""
+    rows, K = codes4.shape
+    digits = torch.stack((codes4 & 3, codes4 >> 2), dim=2).reshape(rows, 2 * K).contiguous()
+    return pack_codes(digits, out=out, stream=stream)
+
+
+def expand_digits4(w4: torch.Tensor, K: int, levels, out: torch.Tensor | None = None, stream=None):
+    """Packed 4-bit weights [rows][ld] -> int8 digit-form operand [rows][expand_ld(2K)]."""
+    _dev(w4, torch.uint8, "w4")
+    rows, ld = w4.shape
+    if out is None:
+        out = torch.empty((rows, expand_ld(2 * K)), dtype=torch.int8, device=w4.device)
+    lv = (ctypes.c_int32 * 16)(*[int(x) for x in levels])
+    _check(lib().dg_expand_digits4(_ptr(w4), rows, K, ld, lv, _ptr(out), out.shape[1], _stream(stream)),
+           "dg_expand_digits4")
+    return out
+
+
+def lut_gemm4_prepared(at4: torch.Tensor, w8: torch.Tensor, N: int, M: int, K: int, levels,
+                       rq: Requant | None = None, out: torch.Tensor | None = None, stream=None):
+    """4-bit GEMM, activation-major output Ct[n][m] = sum_k levels[W[m][k]] * A[k][n]."""
+    _dev(at4, torch.uint8, "at4")
+    _dev(w8, torch.int8, "w8")
+    if out is None:
+        out = (torch.empty((N, (M + 3) // 4), dtype=torch.uint8, device=at4.device) if rq is not None
+               else torch.empty((N, M), dtype=torch.int32, device=at4.device))
+    lv = (ctypes.c_int32 * 16)(*[int(x) for x in levels])
+    r = rq.c() if rq is not None else None
+    _check(lib().dg_lut_gemm4_prepared(_ptr(at4), at4.shape[1], _ptr(w8), w8.shape[1], N, M, K, lv, _ptr(out),
+                                       out.shape[1], ctypes.byref(r) if r is not None else None, _stream(stream)),
+           "dg_lut_gemm4_prepared")
+    return out
+
+
+def lut_conv2d4_prepared(x4: torch.Tensor, w8: torch.Tensor, levels, p: dg_conv_params, rq: Requant | None = None,
+                         out: torch.Tensor | None = None, ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """4-bit NHWC conv: x4 [B*H*W][C/2] packed 4-bit codes (p.C = 4-bit channels), w8 = expand_digits4."""
+    _dev(x4, torch.uint8, "x4")
+    _dev(w8, torch.int8, "w8")
+    Ho = (p.H + 2 * p.pad - p.kh) // p.stride + 1
+    Wo = (p.W + 2 * p.pad - p.kw) // p.stride + 1
+    rows = p.B * Ho * Wo
+    if out is None:
+        out = (torch.empty((rows, p.Cout // 4), dtype=torch.uint8, device=x4.device) if rq is not None
+               else torch.empty((rows, p.Cout), dtype=torch.int32, device=x4.device))
+    lv = (ctypes.c_int32 * 16)(*[int(x) for x in levels])
+    r = rq.c() if rq is not None else None
+    _check(lib().dg_lut_conv2d4_prepared(_ptr(x4), _ptr(w8), w8.shape[1], lv, ctypes.byref(p),
+                                         ctypes.byref(r) if r is not None else None, _ptr(out), _ptr(ws),
+                                         ws.numel() if ws is not None else 0, _stream(stream)), "dg_lut_conv2d4_prepared")
     return out
 
 

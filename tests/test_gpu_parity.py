@@ -668,3 +668,67 @@ def test_gemm_onehot_operands_and_requant():
     big = dg.lut_from_table(np.full(16, 200, np.int32), 16)
     with pytest.raises(dg.DGError, match="UNSUPPORTED"):
         dg.expand_tcols(gpu_pack(np.ascontiguousarray(A.T)), K, big)
+
+
+# ---- 4-bit operands as 2-bit digit pairs (Table 2) --------------
+def _levels16(seed, amp=31):
+    return np.random.default_rng(seed).integers(-amp, amp + 1, 16).astype(np.int32)
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 196, 576), (130, 70, 300), (256, 384, 1152), (17, 9, 5)])
+def test_gemm4_vs_oracle(M, N, K):
+    """4-bit weights (16 arbitrary int8 levels) x 4-bit unsigned activations: activation-major
+    Ct[n][m] equals the b-bit oracle (256-entry product table) bit for bit; the documented packing
+    (digit sequence through dg_pack_codes) gives the nibble layout."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    g = np.random.default_rng(M * 7 + N + K)
+    wl = _levels16(M + K)
+    W = g.integers(0, 16, (M, K), dtype=np.uint8)
+    A = g.integers(0, 16, (K, N), dtype=np.uint8)
+    T = np.outer(wl, np.arange(16)).reshape(-1).astype(np.int32)
+    w4 = dg.pack_codes4(torch.from_numpy(W).to(DEV))
+    hw = host(w4)
+    assert np.array_equal(hw[:, : K // 2], (W[:, 0:K - K % 2:2] | (W[:, 1:K:2] << 4)).astype(np.uint8)[:, : K // 2])
+    at4 = dg.pack_codes4(torch.from_numpy(np.ascontiguousarray(A.T)).to(DEV))
+    w8 = dg.expand_digits4(w4, K, wl)
+    Ct = host(dg.lut_gemm4_prepared(at4, w8, N, M, K, wl))
+    assert np.array_equal(Ct, oracle.lut_gemm_bits(W, A, T, 4).T)
+
+
+@pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad", [(2, 9, 7, 32, 64, 3, 1, 1), (1, 12, 12, 64, 32, 3, 2, 1),
+                                                       (2, 6, 6, 32, 16, 1, 1, 0), (1, 8, 8, 8, 8, 3, 1, 1)])
+def test_conv4_vs_oracle(B, H, W, C, Cout, k, stride, pad):
+    """4-bit NHWC conv (implicit GEMM over 2C digit channels where C/2 bytes is a power of two >= 16,
+    direct 1x1, im2col otherwise) vs the b-bit direct-conv oracle; int32 and fused requant."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    g = np.random.default_rng(B + H + C + Cout + k)
+    wl = _levels16(C + Cout)
+    x = g.integers(0, 16, (B, H, W, C), dtype=np.uint8)
+    wc = g.integers(0, 16, (Cout, k, k, C), dtype=np.uint8)
+    T = np.outer(wl, np.arange(16)).reshape(-1).astype(np.int32)
+    exp = oracle.conv2d_direct_bits(x, wc, T, stride, pad, 4).reshape(-1, Cout)
+    # NHWC activations are contiguous C/2 bytes per pixel: pack the whole tensor as one row
+    nb = B * H * W * C // 2
+    x4 = dg.pack_codes4(torch.from_numpy(x.reshape(1, -1)).to(DEV))[0, :nb].reshape(B * H * W, C // 2).contiguous()
+    w4 = dg.pack_codes4(torch.from_numpy(wc.reshape(Cout, -1)).to(DEV))
+    w8 = dg.expand_digits4(w4, k * k * C, wl)
+    p = dg.conv_params(B, H, W, C, Cout, k, k, stride, pad, 0, ldw=w4.shape[1])
+    ws = torch.zeros(max(1, dg.conv_workspace_size(dg.conv_params(B, H, W, 2 * C, Cout, k, k, stride, pad, 0))),
+                     dtype=torch.uint8, device=DEV)
+    got = host(dg.lut_conv2d4_prepared(x4, w8, wl, p, ws=ws))
+    assert np.array_equal(got, exp)
+    rq = dg.Requant(3000, 20, 0, 0, 3, bias=torch.full((Cout,), int(-exp.mean()), dtype=torch.int32, device=DEV))
+    codes = dg.lut_conv2d4_prepared(x4, w8, wl, p, rq=rq, ws=ws)
+    gotc = oracle.unpack_codes(host(codes), exp.shape[0], Cout, codes.shape[1])
+    bias = np.full(Cout, int(-exp.mean()), np.int32)
+    assert np.array_equal(gotc, oracle.requantize(exp, 3000, 20, 0, 0, 3, bias=bias, bias_axis=0))
+
+
+def test_digits4_rejects():
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    w4 = dg.pack_codes4(torch.zeros((4, 64), dtype=torch.uint8, device=DEV))
+    with pytest.raises(dg.DGError, match="RANGE"):
+        dg.expand_digits4(w4, 64, [40] + [0] * 15)      # 4 x 40 > 127

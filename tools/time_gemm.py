@@ -31,6 +31,11 @@ for s in a.shapes.split(","):
             w1h = dg.expand_onehot(w, ld * 4)
             atc = dg.expand_tcols(at, ld * 4, lut)
             f = lambda: dg.lut_gemm_onehot(w1h, atc, M, N, ld * 4, lut, out=out)
+        elif v == "gemm4":   # 4-bit codes (the same random bytes read as 2 codes each), K4 = 2 * ld
+            lv16 = [((i * 7) % 31) - 15 for i in range(16)]
+            w8d = dg.expand_digits4(w, ld * 2, lv16)
+            out4 = torch.empty((N, M), dtype=torch.int32, device="cuda")
+            f = lambda: dg.lut_gemm4_prepared(at, w8d, N, M, ld * 2, lv16, out=out4)
         elif v == "f4":   # block-scaled FP4 path: weights expanded once to e2m1
             w4 = dg.expand_operand_f4(w, ld * 4, lut.wl)
             f = lambda: dg.lut_gemm_f4(w4, at, M, N, ld * 4, lut, out=out)
@@ -49,5 +54,5 @@ for s in a.shapes.split(","):
         e1.record()
         torch.cuda.synchronize()
         ms = e0.elapsed_time(e1) / a.iters
-        ops = 2 * M * N * ld * 4
+        ops = 2 * M * N * ld * (2 if v == "gemm4" else 4)   # (4-bit: K = 2 codes per byte)
         print(f"{s} {v}: {ms:.3f} ms  {ops / ms / 1e9:.1f} TOPS")
