@@ -51,3 +51,25 @@ def test_host_calls_without_gpu():
     assert t.is_product == 0
     assert dg.packed_ld(1) == 16 and dg.packed_ld(64) == 16 and dg.packed_ld(65) == 32
     assert dg.packed_ld(576) == 144
+
+
+def test_extension_entries_validate_on_the_host():
+    """The FP4 / one-hot / 4-bit entry points reject bad arguments before touching a device, and
+    their layout helpers follow the documented formulas (include/dg.h)."""
+    from paper_2304_09049_b200 import dg
+    L = dg.lib()
+    P = ctypes.c_void_p
+    fake = P(1 << 20)   # never dereferenced: every call below fails validation first
+    lut = dg.build_lut([-2, -1, 0, 1], [0, 1, 2, 3], 8)
+    lv16 = (ctypes.c_int32 * 16)(*range(16))
+    assert L.dg_expand_f4_ld(1) == 128 and L.dg_expand_f4_ld(256) == 128 and L.dg_expand_f4_ld(257) == 256
+    assert L.dg_onehot_ld(1) == 16 and L.dg_onehot_ld(17) == 32
+    assert L.dg_tcols_ld(32) == 128 and L.dg_tcols_ld(33) == 256
+    INVALID, SHAPE, RANGE = -1, -2, -3
+    assert L.dg_lut_gemm_f4(None, 128, fake, 16, 8, 8, 64, ctypes.byref(lut), fake, 8, None) == INVALID
+    assert L.dg_lut_gemm_f4(fake, 100, fake, 16, 8, 8, 64, ctypes.byref(lut), fake, 8, None) == SHAPE
+    assert L.dg_lut_gemm_onehot(fake, 16, fake, 256, 0, 8, 64, ctypes.byref(lut), fake, 8, None, None) == SHAPE
+    assert L.dg_expand_tcols(None, 8, 64, 16, ctypes.byref(lut), fake, 256, None) == INVALID
+    big = (ctypes.c_int32 * 16)(*([40] + [0] * 15))
+    assert L.dg_expand_digits4(fake, 8, 64, 32, big, P(1 << 21), 128, None) == RANGE
+    assert L.dg_lut_gemm4_prepared(fake, 20, P(1 << 21), 128, 8, 8, 64, lv16, fake, 8, None, None) == SHAPE
