@@ -176,6 +176,12 @@ struct TsArgs {
     uint32_t res_pair[16];    // (r[c0] & 0xFFFF) | r[c1] << 16 for the 4-bit pair index c0 | c1 << 2
 };
 
+// WIN "tile mode": C = 64 (18 k-steps of 32 codes = 9 taps x 2 chunks, stages 8 + 8 + 2) with the
+// weights resident in shared memory, so a tile needs one hand-off and one burst of 18 MMAs
+DG_DEV bool win_tile_mode(const TsArgs &ta, int ksteps) {
+    return ta.bres && ta.clog2 == 6 && ksteps == 8 && ta.nstages == 3 && ta.last_ksteps == 2 && !(ta.sk > 1);
+}
+
 // Tile t -> (row block tp, column block tq).  Tiles are walked in groups of `group` row blocks,
 // column block outer / row block inner, so that a wave of concurrent tiles touches few B tiles
 // and few A row blocks (keeps a 256 MB int8 B operand from being re-streamed from HBM).
@@ -692,6 +698,11 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             work_item<SK>(ta, t, tp, tq, sb, se);
             if (WIN) ptx::mbar_wait(full_a(tl % ta.nwin), (tl / ta.nwin) & 1u);   // the tile's window
             if (WIN && lane == 0) TS_EV(13, tl);
+            if (WIN && win_tile_mode(ta, C::KSTEPS)) {   // one hand-off per tile (B resident)
+                ptx::named_bar_sync(HANDOFF_BAR, 64);
+                g += (uint32_t)(se - sb);
+                continue;
+            }
             for (int s = sb; s < se; ++s, ++g) {
                 const int sa = g % SA;
                 if (lane == 0 && s == sb) TS_EV(3, tl);
@@ -708,36 +719,82 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         // the loop and the *_warp helpers elect the issuing lane inside their asm (ptx::mma_i8_ts_warp).
         constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
         const uint64_t bdesc0 = ptx::desc_k_sw128(sbase + C::OFF_B);
+        // WIN geometry in registers before any MMA is queued
+        const int w_slot = ta.wslot, w_nwin = ta.nwin, w_bytes = ta.wbytes;
+        const uint32_t w_lbo16 = (uint32_t)ta.lbo >> 4, w_wp = (uint32_t)ta.Wp, w_clog2 = (uint32_t)ta.clog2;
+        uint32_t w_tap[9];   // window row shift of tap (r, s) in 16-byte units: r*Wp + s
+#pragma unroll
+        for (int q = 0; q < 9; ++q) w_tap[q] = (uint32_t)(q / 3) * w_wp + (uint32_t)(q % 3);
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl % NACC;
             const uint32_t dt = tmem + acc * BN;
             int tp, tq, sb, se;
             work_item<SK>(ta, t, tp, tq, sb, se);
+            if (WIN && win_tile_mode(ta, C::KSTEPS)) {
+                // C = 64 direct 3x3 with resident weights: the tile's 18 k-steps (tap j/2, channel
+                // chunk 2(j&1)) issued after one hand-off, with compile-time B offsets and the 9 tap
+                // offsets of the window held in registers (no per-stage hand-off, no memory op)
+                const uint32_t wbase = sbase + C::OFF_P + (uint32_t)(2 * w_slot + (int)(tl % w_nwin) * w_bytes);
+                const uint64_t ad = ptx::desc_k_none(wbase, w_lbo16 << 4);
+                const uint64_t bt = bdesc0 + (uint64_t)((tq * 3 * C::B_BYTES) >> 4);
+                ptx::named_bar_sync(HANDOFF_BAR, 64);
+                ptx::tc_fence_after();
+                if (lane == 0) TS_EV(14, g);
+#pragma unroll
+                for (int j = 0; j < 18; ++j) {
+                    const int st = j >> 3, k = j & 7;
+                    ptx::mma_i8_ss_warp(dt, ad + (uint64_t)(w_tap[j >> 1] + (uint32_t)((j & 1) * 2) * w_lbo16),
+                                        bt + (uint64_t)((st * C::B_BYTES + (k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
+                                        idesc, j > 0 ? 1u : 0u);
+                }
+                ptx::mma_commit_warp(empty_a(tl % w_nwin));   // the window is free again
+                ptx::mma_commit_warp(acc_full(acc));
+                if (lane == 0) TS_EV(15, g);
+                g += (uint32_t)(se - sb);
+                __syncwarp();
+                continue;
+            }
             for (int s = sb; s < se; ++s, ++g) {
                 const int sa = g % SA;
                 const int bsl = ta.bres ? tq * ta.nstages + s : (int)(g % SB);   // B smem stage
-                ptx::named_bar_sync(HANDOFF_BAR, 64);
-                ptx::tc_fence_after();
                 const int nk = (s < ta.nstages - 1) ? C::KSTEPS : ta.last_ksteps;
                 const uint64_t bd = bdesc0 + (uint64_t)((bsl * C::B_BYTES) >> 4);
+                // WIN: k = tap*C + c: A = the window shifted by r*Wp + s rows (tap = 3r + s), K chunk
+                // c/16; the per-k-step descriptors (host-precomputed offsets ta.koff) are formed before
+                // the hand-off, so that no parameter load sits between two tcgen05.mma (a load there
+                // serialises the issue: ~150 cycles per MMA measured)
+                uint64_t wad[C::KSTEPS];
+                if (WIN) {
+                    const uint32_t wbase = sbase + C::OFF_P + (uint32_t)(2 * w_slot + (int)(tl % w_nwin) * w_bytes);
+                    const uint64_t ad = ptx::desc_k_none(wbase, w_lbo16 << 4);
+                    const int j0 = s * C::KSTEPS;
+                    // k-step j (32 codes): tap = 32j / C, channel chunk (32j mod C) / 16, tap (r, s) =
+                    // (tap / 3, tap mod 3) -> start offset chunk*lbo + (r*Wp + s)*16 bytes (the
+                    // host's ta.koff, recomputed here with ALU ops only: an indexed parameter load
+                    // in this warp waits for its queued MMAs)
+#pragma unroll
+                    for (int k = 0; k < C::KSTEPS; ++k) {
+                        const uint32_t kb = (uint32_t)(32 * (j0 + k));
+                        const uint32_t tap = kb >> w_clog2, chunk = (kb & ((1u << w_clog2) - 1u)) >> 4;
+                        const uint32_t rr = (tap * 11u) >> 5;   // tap / 3 for tap < 9
+                        wad[k] = ad + (uint64_t)(chunk * w_lbo16 + rr * w_wp + (tap - 3u * rr));
+                    }
+                }
+                ptx::named_bar_sync(HANDOFF_BAR, 64);
+                ptx::tc_fence_after();
                 if (lane == 0) TS_EV(14, g);
                 if (WIN) {
-                    // k = tap*C + c: A = the window shifted by r*Wp + s rows (tap = 3r + s), K chunk c/16;
-                    // the per-k-step start offsets come precomputed from the host (ta.koff)
-                    const uint32_t wbase = sbase + C::OFF_P + (uint32_t)(2 * ta.wslot + (int)(tl % ta.nwin) * ta.wbytes);
-                    const uint64_t ad = ptx::desc_k_none(wbase, (uint32_t)ta.lbo);
-                    const int j0 = s * C::KSTEPS;
-                    // all offsets into registers first: a parameter load between two tcgen05.mma
-                    // (asm with a memory clobber) serialises the issue (~150 cycles per MMA measured)
-                    uint32_t ko[C::KSTEPS];
+                    if (nk == C::KSTEPS) {   // full stage: straight-line issue
 #pragma unroll
-                    for (int k = 0; k < C::KSTEPS; ++k) ko[k] = ta.koff[j0 + k < 72 ? j0 + k : 71];
-#pragma unroll
-                    for (int k = 0; k < C::KSTEPS; ++k)
-                        if (k < nk)
-                            ptx::mma_i8_ss_warp(dt, ad + ko[k], bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
+                        for (int k = 0; k < C::KSTEPS; ++k)
+                            ptx::mma_i8_ss_warp(dt, wad[k], bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
                                                 idesc, (s > sb || k > 0) ? 1u : 0u);
+                    } else {
+                        for (int k = 0; k < nk; ++k)
+                            ptx::mma_i8_ss_warp(dt, wad[k], bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
+                                                idesc, (s > sb || k > 0) ? 1u : 0u);
+                    }
                     if (!ta.bres) ptx::mma_commit_warp(empty_b(bsl));
                     if (s == se - 1) {
                         ptx::mma_commit_warp(empty_a(tl % ta.nwin));   // the window is free again
@@ -794,27 +851,69 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const bool has_row = tid < ta.WR;
         const int cb = 1 << (ta.clog2 - 2), nch = cb >> 4;   // packed bytes per pixel, 16-byte chunks
         const uint32_t ring = sbase + C::OFF_P, wins = ring + WRING * ta.wslot;
+        // wide images (window > one row per thread, C = 64 only): thread tid owns rows tid + i*NUNP*32
+        constexpr int WMAXR = 3;
+        const int nrt = (ta.WR + NUNP * 32 - 1) / (NUNP * 32);
         auto fetch = [&](int t, int slot) {
-            if (has_row && t < ntiles) {
+            if (t < ntiles) {
                 int tp, tq;
                 tile_coords(ta, t, tp, tq);
-                const int64_t q = (int64_t)tp * BM - (ta.Wp + 1) + tid;   // padded pixel of this row
-                const uint8_t *src = nullptr;
-                if (q >= 0 && q < ta.nqv) {
-                    const uint32_t b = fdiv((uint32_t)q, ta.fd_hpwp);
-                    const uint32_t rem = (uint32_t)q - b * (uint32_t)((ta.H + 2) * ta.Wp);
-                    const uint32_t hp = fdiv(rem, ta.fd_wp), wp = rem - hp * (uint32_t)ta.Wp;
-                    if (hp >= 1 && hp <= (uint32_t)ta.H && wp >= 1 && wp <= (uint32_t)ta.W)
-                        src = ta.X + ((((int64_t)b * ta.H + hp - 1) * ta.W + wp - 1) << (ta.clog2 - 2));
+                for (int i = 0; i < nrt; ++i) {
+                    const int row = tid + i * NUNP * 32;
+                    if (row >= ta.WR) break;
+                    const int64_t q = (int64_t)tp * BM - (ta.Wp + 1) + row;   // padded pixel of this row
+                    const uint8_t *src = nullptr;
+                    if (q >= 0 && q < ta.nqv) {
+                        const uint32_t b = fdiv((uint32_t)q, ta.fd_hpwp);
+                        const uint32_t rem = (uint32_t)q - b * (uint32_t)((ta.H + 2) * ta.Wp);
+                        const uint32_t hp = fdiv(rem, ta.fd_wp), wp = rem - hp * (uint32_t)ta.Wp;
+                        if (hp >= 1 && hp <= (uint32_t)ta.H && wp >= 1 && wp <= (uint32_t)ta.W)
+                            src = ta.X + ((((int64_t)b * ta.H + hp - 1) * ta.W + wp - 1) << (ta.clog2 - 2));
+                    }
+                    const uint32_t dst = ring + (uint32_t)(slot * ta.wslot + row * cb);
+                    for (int c = 0; c < nch; ++c) ptx::cp_async16(dst + 16 * c, src ? src + 16 * c : ta.padsrc);
                 }
-                const uint32_t dst = ring + (uint32_t)(slot * ta.wslot + tid * cb);
-                for (int c = 0; c < nch; ++c) ptx::cp_async16(dst + 16 * c, src ? src + 16 * c : ta.padsrc);
             }
             ptx::cp_async_commit();
         };
         fetch(blockIdx.x, 0);
         fetch(blockIdx.x + gridDim.x, 1);
         uint32_t tl = 0;
+        if (nrt > 1) {   // (host guarantees C = 64: one 16-byte chunk per row)
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+                const int slot = (int)(tl & 1u), wb = (int)(tl % ta.nwin);
+                ptx::cp_async_wait<WRING - 1>();
+                uint32_t a[WMAXR][16];
+#pragma unroll
+                for (int i = 0; i < WMAXR; ++i) {
+                    const int row = tid + i * NUNP * 32;
+                    const uint4 v = (i < nrt && row < ta.WR) ? ptx::lds128(ring + (uint32_t)(slot * ta.wslot + row * cb))
+                                                             : make_uint4(0, 0, 0, 0);
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int q = 0; q < 4; ++q) {
+                        const uint4 o = unpack16_levels(w[q], ta.lp);
+                        a[i][4 * q] = o.x; a[i][4 * q + 1] = o.y; a[i][4 * q + 2] = o.z; a[i][4 * q + 3] = o.w;
+                    }
+                }
+                fetch(t + 2 * (int)gridDim.x, slot);   // the slot's bytes are consumed: refill it
+                ptx::mbar_wait(empty_a(wb), ((tl / ta.nwin) & 1u) ^ 1u);   // the window's previous tile finished
+#pragma unroll
+                for (int i = 0; i < WMAXR; ++i) {
+                    const int row = tid + i * NUNP * 32;
+                    if (i >= nrt || row >= ta.WR) break;
+                    const uint32_t wdst = wins + (uint32_t)(wb * ta.wbytes + row * 16);
+#pragma unroll
+                    for (int j = 0; j < 4; ++j)
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(wdst + (uint32_t)(j * ta.lbo)),
+                                     "r"(a[i][4 * j]), "r"(a[i][4 * j + 1]), "r"(a[i][4 * j + 2]), "r"(a[i][4 * j + 3])
+                                     : "memory");
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(full_a(wb));
+            }
+        } else
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const int slot = (int)(tl & 1u), wb = (int)(tl % ta.nwin);
             if (tid == 0) TS_EV(0, tl);
@@ -1339,7 +1438,8 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         if (ta.nqv >= ((int64_t)1 << 31)) return DG_ERR_SHAPE;
         ta.ntp = (int32_t)((ta.nqv + BM - 1) / BM);
         ta.WR = (BM + 2 * (int32_t)Wp + 2 + 7) / 8 * 8;   // multiple of 8: LBO a multiple of 128 B
-        if (ta.WR > NUNP * 32) return DG_ERR_UNSUPPORTED;   // one window row per unpack thread
+        // one window row per unpack thread, or up to 3 for C = 64 (one 16-byte chunk per row)
+        if (ta.WR > NUNP * 32 && (cv->Cb != 16 || ta.WR > 3 * NUNP * 32)) return DG_ERR_UNSUPPORTED;
         ta.lbo = ta.WR * 16;
         int lg = 0;
         while ((1 << lg) < 4 * cv->Cb) ++lg;
@@ -1536,11 +1636,15 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     g_peers = peers;
     g_npeers = peers ? npeers : 0;
     struct Reset { ~Reset() { g_peers = nullptr; g_npeers = 0; } } reset;
-    // direct 3x3 / stride 1 / pad 1 convs with C = 64, 128, 256: shifted-window kernel (DG_WIN=1; it
-    // unpacks each input pixel once per tile instead of once per tap, but measured no faster than
-    // the implicit gather on the ResNet-50 shapes)
+    // direct 3x3 / stride 1 / pad 1 convs: shifted-window kernel, which unpacks each input pixel once
+    // per tile instead of once per tap.  Default for C = 64 (the "tile mode": one hand-off and 18
+    // MMAs per tile, 3x3 64 -> 64 at 56x56 b256: 88 -> 54 us); C = 128 / 256 only with DG_WIN=1
+    // (measured no faster than the implicit gather there)
+    static const bool win_force = getenv("DG_WIN") != nullptr, win_off = getenv("DG_NO_WIN") != nullptr;
     if (cv && cv->kh == 3 && cv->kw == 3 && cv->stride == 1 && cv->pad == 1 && cv->Cb >= 16 && cv->Cb <= 64 &&
-        (cv->Cb & (cv->Cb - 1)) == 0 && getenv("DG_WIN")) {
+        (cv->Cb & (cv->Cb - 1)) == 0 && !win_off &&
+        (win_force || (cv->Cb == 16 && nq <= 128 &&
+                       (np / ((int64_t)cv->H * cv->W)) * (cv->H + 2) * (cv->W + 2) / BM >= 2 * num_sms()))) {
         const dg_status s = nq > 64 ? launch_ts<128, 4, 8, 256, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv)
                                     : launch_ts<64, 4, 8, 256, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         if (s != DG_ERR_UNSUPPORTED) return s;

@@ -443,14 +443,19 @@ WIN_CONVS = [  # B, H, W, C, Cout, pad_code: 3x3 / stride 1 / pad 1 shapes of th
     (3, 14, 14, 128, 64, 0),
     (1, 7, 11, 256, 128, 2),      # non-square, non-zero pad code
     (2, 56, 56, 64, 64, 0),       # ResNet-50 stage-1 width (window of 248 rows)
+    (2, 12, 10, 64, 128, 0),      # C = 64 tile mode with 128-wide tiles (VGG conv2_1 shape class)
+    (1, 23, 17, 64, 64, 3),       # C = 64 tile mode, ragged last tile, pad code 3
+    (1, 10, 120, 64, 64, 0),      # wide: 374-row window, 2 rows per unpack thread
+    (1, 6, 224, 64, 128, 1),      # VGG width: 582-row window, 3 rows per thread, pad code 1
 ]
 
 
 @pytest.mark.parametrize("B,H,W,C,Cout,pad_code", WIN_CONVS)
 def test_conv_window_path_vs_oracle(monkeypatch, B, H, W, C, Cout, pad_code):
-    """Direct 3x3 conv through the shifted-window kernel (DG_WIN=1: one unpacked window of padded
-    input pixels per tile, every tap an MMA on a row-shifted shared-memory descriptor) vs O-CONV,
-    int32 and fused requant."""
+    """Direct 3x3 conv through the shifted-window kernel (DG_WIN=1 forces it for C = 128 / 256; C =
+    64 takes it by default, "tile mode": one hand-off and 18 MMAs per tile): one unpacked window of
+    padded input pixels per tile, every tap an MMA on a row-shifted shared-memory descriptor, vs
+    O-CONV, int32 and fused requant."""
     if not _tc_available():
         pytest.skip("tc unavailable")
     monkeypatch.setenv("DG_WIN", "1")
