@@ -93,7 +93,8 @@ struct TsCfg {
     static constexpr int OFF_BAR = OFF_A + SA * A_STAGE;
     static constexpr int NBAR = 2 * SP_MAX + 2 * SB + 2 * SA + 2 * NACC;
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
-    static constexpr int OFF_TAB = (OFF_TMEM + 16 + 15) / 16 * 16;   // 16-bit requant offsets, one u32 per column pair
+    static constexpr int OFF_WALK = OFF_TMEM + 16;           // 32 words: the MMA warp's copy of the tile walk
+    static constexpr int OFF_TAB = (OFF_WALK + 128 + 15) / 16 * 16;   // 16-bit requant offsets, one u32 per column pair
     static constexpr int ALLOC = OFF_TAB + TAB_PAIRS * 4 + 1024;
     static_assert((ASM ? NACC * BN : TMEM_A0 + SA * ACOLS) <= TMEM_COLS && SA >= 2, "TMEM budget");
     static_assert(ALLOC <= 232448, "shared memory budget");
@@ -185,7 +186,8 @@ DG_DEV bool win_tile_mode(const TsArgs &ta, int ksteps) {
 // Tile t -> (row block tp, column block tq).  Tiles are walked in groups of `group` row blocks,
 // column block outer / row block inner, so that a wave of concurrent tiles touches few B tiles
 // and few A row blocks (keeps a 256 MB int8 B operand from being re-streamed from HBM).
-DG_DEV void tile_coords(const TsArgs &ta, int t, int &tp, int &tq) {
+template <class A>
+DG_DEV void tile_coords(const A &ta, int t, int &tp, int &tq) {
     const uint32_t grp = fdiv((uint32_t)t, ta.fd_pg);
     const uint32_t rem = (uint32_t)t - grp * (uint32_t)(ta.group * ta.ntq);
     const bool last = (int)grp == ta.last_grp;
@@ -196,8 +198,8 @@ DG_DEV void tile_coords(const TsArgs &ta, int t, int &tp, int &tq) {
 
 // Work item t -> output tile (tp, tq) and its stages [sb, se) (all stages unless split-K)
 // (SK: the kernel instance supports split-K; the others compile the plain tile walk)
-template <bool SK>
-DG_DEV void work_item(const TsArgs &ta, int t, int &tp, int &tq, int &sb, int &se) {
+template <bool SK, class A>
+DG_DEV void work_item(const A &ta, int t, int &tp, int &tq, int &sb, int &se) {
     if (SK && ta.sk > 1) {
         const int ot = (int)fdiv((uint32_t)t, ta.fd_sk), ks = t - ot * ta.sk;
         tile_coords(ta, ot, tp, tq);
@@ -208,6 +210,47 @@ DG_DEV void work_item(const TsArgs &ta, int t, int &tp, int &tq, int &sb, int &s
         sb = 0;
         se = ta.nstages;
     }
+}
+
+// The tile walk's parameters held in registers.  The MMA-issuing warp reads them through this
+// copy: a parameter-space load (LDC) issued by that warp waits behind its queued MMAs, like a
+// shared-memory load (measured on the WIN path: ~600 cycles per stage), so it must not touch
+// the parameter struct between MMAs.
+struct Walk {
+    FastDiv fd_pg, fd_grp, fd_last, fd_sk;
+    int32_t group, ntq, last_grp, last_rows, sk, nstages, bres, last_ksteps, ntiles, grid;
+};
+// The values are staged through shared memory and read back with volatile loads once, before
+// the first MMA: ptxas would otherwise rematerialise them from the parameter bank inside the loop.
+DG_DEV void put_walk(const TsArgs &ta, volatile uint32_t *d) {
+    const uint32_t v[16] = {ta.fd_pg.m, ta.fd_pg.s, ta.fd_grp.m, ta.fd_grp.s, ta.fd_last.m, ta.fd_last.s, ta.fd_sk.m,
+                            ta.fd_sk.s, (uint32_t)ta.group, (uint32_t)ta.ntq, (uint32_t)ta.last_grp,
+                            (uint32_t)ta.last_rows, (uint32_t)ta.sk, (uint32_t)ta.nstages, (uint32_t)ta.bres,
+                            (uint32_t)ta.last_ksteps};
+    for (int i = 0; i < 16; ++i) d[i] = v[i];
+    d[16] = (uint32_t)ta.nwork;
+    d[17] = gridDim.x;
+}
+DG_DEV Walk get_walk(const volatile uint32_t *d) {
+    uint32_t v[18];
+#pragma unroll
+    for (int i = 0; i < 18; ++i) v[i] = d[i];
+    Walk w;
+    w.fd_pg = FastDiv{v[0], v[1]};
+    w.fd_grp = FastDiv{v[2], v[3]};
+    w.fd_last = FastDiv{v[4], v[5]};
+    w.fd_sk = FastDiv{v[6], v[7]};
+    w.group = (int32_t)v[8];
+    w.ntq = (int32_t)v[9];
+    w.last_grp = (int32_t)v[10];
+    w.last_rows = (int32_t)v[11];
+    w.sk = (int32_t)v[12];
+    w.nstages = (int32_t)v[13];
+    w.bres = (int32_t)v[14];
+    w.last_ksteps = (int32_t)v[15];
+    w.ntiles = (int32_t)v[16];
+    w.grid = (int32_t)v[17];
+    return w;
 }
 
 // Implicit im2col gather cursor of one unpack thread (row r of its tiles): walks the thread's
@@ -610,7 +653,11 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     }
     uint32_t *f16tab = reinterpret_cast<uint32_t *>(smem + C::OFF_TAB);
     volatile uint32_t *f16_flag = reinterpret_cast<volatile uint32_t *>(smem + C::OFF_TMEM + 8);
-    if (threadIdx.x == 0) *f16_flag = 0u;
+    if (threadIdx.x == 0) {
+        *f16_flag = 0u;
+        *reinterpret_cast<volatile uint32_t *>(smem + C::OFF_TMEM + 12) = 0u;   // the MMA warp's opaque zero
+        put_walk(ta, reinterpret_cast<volatile uint32_t *>(smem + C::OFF_WALK));
+    }
     // (with __syncthreads_or here the kernel faulted with a misaligned address when launched
     // right after the tc_ss kernel, cause not determined: the flag goes through shared memory)
     ptx::tc_fence_before();
@@ -719,19 +766,27 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         // the loop and the *_warp helpers elect the issuing lane inside their asm (ptx::mma_i8_ts_warp).
         constexpr uint32_t idesc = ptx::idesc_i8(BM, BN);
         const uint64_t bdesc0 = ptx::desc_k_sw128(sbase + C::OFF_B);
+        // parameters in registers before any MMA is queued (Walk)
+        const uint32_t z0 = *reinterpret_cast<volatile uint32_t *>(smem + C::OFF_TMEM + 12);   // 0
+        auto reg_copy = [z0](uint32_t x) { return x + z0; };
         // WIN geometry in registers before any MMA is queued
-        const int w_slot = ta.wslot, w_nwin = ta.nwin, w_bytes = ta.wbytes;
-        const uint32_t w_lbo16 = (uint32_t)ta.lbo >> 4, w_wp = (uint32_t)ta.Wp, w_clog2 = (uint32_t)ta.clog2;
+        const int w_slot = (int)reg_copy((uint32_t)ta.wslot), w_nwin = (int)reg_copy((uint32_t)ta.nwin),
+                  w_bytes = (int)reg_copy((uint32_t)ta.wbytes);
+        const uint32_t w_lbo16 = reg_copy((uint32_t)ta.lbo >> 4), w_wp = reg_copy((uint32_t)ta.Wp),
+                       w_clog2 = reg_copy((uint32_t)ta.clog2);
         uint32_t w_tap[9];   // window row shift of tap (r, s) in 16-byte units: r*Wp + s
 #pragma unroll
         for (int q = 0; q < 9; ++q) w_tap[q] = (uint32_t)(q / 3) * w_wp + (uint32_t)(q % 3);
+        const Walk wk = get_walk(reinterpret_cast<volatile uint32_t *>(smem + C::OFF_WALK));
+        const bool win_mode = WIN && win_tile_mode(ta, C::KSTEPS);
+        const int ntl = wk.ntiles, grid_n = wk.grid;
         uint32_t g = 0, tl = 0;
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+        for (int t = blockIdx.x; t < ntl; t += grid_n, ++tl) {
             const uint32_t acc = tl % NACC;
             const uint32_t dt = tmem + acc * BN;
             int tp, tq, sb, se;
-            work_item<SK>(ta, t, tp, tq, sb, se);
-            if (WIN && win_tile_mode(ta, C::KSTEPS)) {
+            work_item<SK>(wk, t, tp, tq, sb, se);
+            if (WIN && win_mode) {
                 // C = 64 direct 3x3 with resident weights: the tile's 18 k-steps (tap j/2, channel
                 // chunk 2(j&1)) issued after one hand-off, with compile-time B offsets and the 9 tap
                 // offsets of the window held in registers (no per-stage hand-off, no memory op)
@@ -757,8 +812,8 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
             for (int s = sb; s < se; ++s, ++g) {
                 const int sa = g % SA;
-                const int bsl = ta.bres ? tq * ta.nstages + s : (int)(g % SB);   // B smem stage
-                const int nk = (s < ta.nstages - 1) ? C::KSTEPS : ta.last_ksteps;
+                const int bsl = wk.bres ? tq * wk.nstages + s : (int)(g % SB);   // B smem stage
+                const int nk = (s < wk.nstages - 1) ? C::KSTEPS : wk.last_ksteps;
                 const uint64_t bd = bdesc0 + (uint64_t)((bsl * C::B_BYTES) >> 4);
                 // WIN: k = tap*C + c: A = the window shifted by r*Wp + s rows (tap = 3r + s), K chunk
                 // c/16; the per-k-step descriptors (host-precomputed offsets ta.koff) are formed before
@@ -795,9 +850,9 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                             ptx::mma_i8_ss_warp(dt, wad[k], bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
                                                 idesc, (s > sb || k > 0) ? 1u : 0u);
                     }
-                    if (!ta.bres) ptx::mma_commit_warp(empty_b(bsl));
+                    if (!wk.bres) ptx::mma_commit_warp(empty_b(bsl));
                     if (s == se - 1) {
-                        ptx::mma_commit_warp(empty_a(tl % ta.nwin));   // the window is free again
+                        ptx::mma_commit_warp(empty_a(tl % w_nwin));   // the window is free again
                         ptx::mma_commit_warp(acc_full(acc));
                     }
                 } else if (ASM) {
@@ -816,7 +871,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                                                 (s > sb || k > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit_warp(empty_a(sa));
-                    if (!ta.bres) ptx::mma_commit_warp(empty_b(bsl));
+                    if (!wk.bres) ptx::mma_commit_warp(empty_b(bsl));
                     if (s == se - 1) ptx::mma_commit_warp(acc_full(acc));
                 } else {
                     const uint32_t at = tmem + C::TMEM_A0 + sa * C::ACOLS;
@@ -834,7 +889,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     }
 #endif
                     ptx::mma_commit_warp(empty_a(sa));
-                    if (!ta.bres) ptx::mma_commit_warp(empty_b(bsl));
+                    if (!wk.bres) ptx::mma_commit_warp(empty_b(bsl));
                     if (s == se - 1) ptx::mma_commit_warp(acc_full(acc));
                 }
                 if (lane == 0) TS_EV(15, g);
