@@ -81,11 +81,11 @@ struct TsCfg {
     static constexpr int SA = ASM ? 4 : ((512 - NACC * BN) / ACOLS > 8 ? 8 : (512 - NACC * BN) / ACOLS);   // A stages
     static constexpr int B_ATOM = BN * KA;                  // bytes of one 128-code B atom
     static constexpr int B_BYTES = BN * KST;
-    static constexpr int SB_RAW = (BN == 64 || WIN || ASM ? 98304 : 131072) / B_BYTES;
+    static constexpr int SB_RAW = (WIN && BN == 64 ? 49152 : (BN == 64 || WIN || ASM ? 98304 : 131072)) / B_BYTES;
     static constexpr int SB = SB_RAW > 8 ? 8 : SB_RAW;      // B (int8) smem stages
     static constexpr int TMEM_A0 = NACC * BN;               // first A column
     static constexpr int TMEM_COLS = 512;
-    static constexpr int P_REGION = WIN ? 106496 : (ASM ? 32768 : 4 * BM * PKS_MAX);   // packed P / WIN ring + windows
+    static constexpr int P_REGION = WIN ? (BN == 64 ? 155648 : 106496) : (ASM ? 32768 : 4 * BM * PKS_MAX);   // packed P / WIN ring + windows
     static constexpr int A_STAGE = ASM ? BM * KST : 0;       // ASM: one A stage, 16-byte K chunk j of row r at j*BM*16 + r*16
     static constexpr int OFF_B = 0;                          // 1024-aligned (SW128)
     static constexpr int OFF_P = OFF_B + SB * B_BYTES;
@@ -160,6 +160,7 @@ struct TsArgs {
     // WIN (direct 3x3 conv): tiles run over the padded pixel space q = (b*Hp + hp)*Wp + wp
     // (Hp = H+2, Wp = W+2); window row i of a tile = padded pixel q0 - Wp - 1 + i
     int32_t win, Wp, WR, lbo, wslot, wbytes, nwin, clog2;   // WR window rows, lbo = WR*16
+    int32_t wpair;         // WIN tile mode with 2 row blocks per work item (one window, 2 accumulators)
     int64_t nqv;           // B*Hp*Wp
     FastDiv fd_hpwp, fd_wp;
     uint16_t koff[72];     // A descriptor start offset (16-byte units) of k-step j: chunk and tap shift
@@ -740,12 +741,14 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             for (int j = 0; j < ta.ntq * ta.nstages; ++j) ptx::mbar_wait(full_b(j), 0u);
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-            ptx::mbar_wait(acc_empty(tl % NACC), ((tl / NACC) & 1u) ^ 1u);
+            const uint32_t u0 = WIN ? (tl << ta.wpair) : tl;   // accumulator use index (WIN pairs: 2 per item)
+            ptx::mbar_wait(acc_empty(u0 % NACC), ((u0 / NACC) & 1u) ^ 1u);
             int tp, tq, sb, se;
             work_item<SK>(ta, t, tp, tq, sb, se);
             if (WIN) ptx::mbar_wait(full_a(tl % ta.nwin), (tl / ta.nwin) & 1u);   // the tile's window
             if (WIN && lane == 0) TS_EV(13, tl);
             if (WIN && win_tile_mode(ta, C::KSTEPS)) {   // one hand-off per tile (B resident)
+                if (ta.wpair) ptx::mbar_wait(acc_empty((u0 + 1) % NACC), (((u0 + 1) / NACC) & 1u) ^ 1u);
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
                 g += (uint32_t)(se - sb);
                 continue;
@@ -774,6 +777,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                   w_bytes = (int)reg_copy((uint32_t)ta.wbytes);
         const uint32_t w_lbo16 = reg_copy((uint32_t)ta.lbo >> 4), w_wp = reg_copy((uint32_t)ta.Wp),
                        w_clog2 = reg_copy((uint32_t)ta.clog2);
+        const int w_pair = WIN ? (int)reg_copy((uint32_t)ta.wpair) : 0;
         uint32_t w_tap[9];   // window row shift of tap (r, s) in 16-byte units: r*Wp + s
 #pragma unroll
         for (int q = 0; q < 9; ++q) w_tap[q] = (uint32_t)(q / 3) * w_wp + (uint32_t)(q % 3);
@@ -789,22 +793,29 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             if (WIN && win_mode) {
                 // C = 64 direct 3x3 with resident weights: the tile's 18 k-steps (tap j/2, channel
                 // chunk 2(j&1)) issued after one hand-off, with compile-time B offsets and the 9 tap
-                // offsets of the window held in registers (no per-stage hand-off, no memory op)
+                // offsets of the window held in registers (no per-stage hand-off, no memory op).
+                // Pair mode: the window spans 2 row blocks; block h reads it BM rows further down
+                // and accumulates into the next accumulator buffer.
                 const uint32_t wbase = sbase + C::OFF_P + (uint32_t)(2 * w_slot + (int)(tl % w_nwin) * w_bytes);
                 const uint64_t ad = ptx::desc_k_none(wbase, w_lbo16 << 4);
                 const uint64_t bt = bdesc0 + (uint64_t)((tq * 3 * C::B_BYTES) >> 4);
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
                 ptx::tc_fence_after();
                 if (lane == 0) TS_EV(14, g);
+                for (int h = 0; h <= w_pair; ++h) {
+                    const uint32_t u = (tl << w_pair) + (uint32_t)h;
+                    const uint32_t dth = tmem + (u % NACC) * BN;
+                    const uint64_t adh = ad + (uint64_t)(h * BM);   // BM rows of 16 bytes
 #pragma unroll
-                for (int j = 0; j < 18; ++j) {
-                    const int st = j >> 3, k = j & 7;
-                    ptx::mma_i8_ss_warp(dt, ad + (uint64_t)(w_tap[j >> 1] + (uint32_t)((j & 1) * 2) * w_lbo16),
-                                        bt + (uint64_t)((st * C::B_BYTES + (k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
-                                        idesc, j > 0 ? 1u : 0u);
+                    for (int j = 0; j < 18; ++j) {
+                        const int st = j >> 3, k = j & 7;
+                        ptx::mma_i8_ss_warp(dth, adh + (uint64_t)(w_tap[j >> 1] + (uint32_t)((j & 1) * 2) * w_lbo16),
+                                            bt + (uint64_t)((st * C::B_BYTES + (k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
+                                            idesc, j > 0 ? 1u : 0u);
+                    }
+                    ptx::mma_commit_warp(acc_full(u % NACC));
                 }
                 ptx::mma_commit_warp(empty_a(tl % w_nwin));   // the window is free again
-                ptx::mma_commit_warp(acc_full(acc));
                 if (lane == 0) TS_EV(15, g);
                 g += (uint32_t)(se - sb);
                 __syncwarp();
@@ -916,7 +927,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 for (int i = 0; i < nrt; ++i) {
                     const int row = tid + i * NUNP * 32;
                     if (row >= ta.WR) break;
-                    const int64_t q = (int64_t)tp * BM - (ta.Wp + 1) + row;   // padded pixel of this row
+                    const int64_t q = ((int64_t)tp << ta.wpair) * BM - (ta.Wp + 1) + row;   // padded pixel of this row
                     const uint8_t *src = nullptr;
                     if (q >= 0 && q < ta.nqv) {
                         const uint32_t b = fdiv((uint32_t)q, ta.fd_hpwp);
@@ -1229,12 +1240,15 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const int quarter = warp & 3, eg = (warp - EPI_WARP0) >> 2, half = 0;
         const bool col_bias = rq.bias && rq.bias_axis == 0;
         uint32_t tl = 0;
+        const int wpair = WIN ? ta.wpair : 0;   // WIN pair mode: a work item = 2 row blocks (2 accumulators)
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             if (EG > 1 && (int)(tl % EG) != eg) continue;
-            const uint32_t acc = tl % NACC;
             int tp, tq;
             tile_coords(ta, t, tp, tq);
-            int64_t p = (int64_t)tp * BM + quarter * 32 + lane;
+            for (int h = 0; h <= wpair; ++h) {
+            const uint32_t u = (tl << wpair) + (uint32_t)h;   // accumulator use index
+            const uint32_t acc = u % NACC;
+            int64_t p = ((int64_t)tp << wpair) * BM + (int64_t)h * BM + quarter * 32 + lane;
             if (WIN) {   // padded pixel -> output pixel row, or np (not stored) for a padding position
                 const int64_t q = p;
                 p = ta.np;
@@ -1248,7 +1262,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
             const int64_t q0 = (int64_t)tq * BN + half * HALF;
             if (lane == 0 && quarter == 0) TS_EV(8, tl);
-            ptx::mbar_wait(acc_full(acc), (tl / NACC) & 1u);
+            ptx::mbar_wait(acc_full(acc), (u / NACC) & 1u);
             if (lane == 0 && quarter == 0) TS_EV(9, tl);
             ptx::tc_fence_after();
             const uint32_t trow = tmem + acc * BN + half * HALF + ((uint32_t)(quarter * 32) << 16);
@@ -1327,6 +1341,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
             }
             if (lane == 0 && quarter == 0) TS_EV(10, tl);
+            }   // h
         }
         }   // common modes
         if (ta.npeer) __threadfence_system();   // peer stores visible system-wide before the grid completes
@@ -1492,7 +1507,11 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         ta.nqv = B * Hp * Wp;
         if (ta.nqv >= ((int64_t)1 << 31)) return DG_ERR_SHAPE;
         ta.ntp = (int32_t)((ta.nqv + BM - 1) / BM);
-        ta.WR = (BM + 2 * (int32_t)Wp + 2 + 7) / 8 * 8;   // multiple of 8: LBO a multiple of 128 B
+        // pair mode (tile mode on 64-wide tiles: C = 64, Cout <= 64, K = 576, weights resident): one window feeds 2 row blocks, so the halo rows are filled once per 2 blocks
+        static const bool no_pair = getenv("DG_NO_WPAIR") != nullptr;
+        ta.wpair = (BN == 64 && KST == 256 && cv->Cb == 16 && K == 576 && nq <= 64 && !no_pair) ? 1 : 0;
+        if (ta.wpair) ta.ntp = (ta.ntp + 1) / 2;
+        ta.WR = ((BM << ta.wpair) + 2 * (int32_t)Wp + 2 + 7) / 8 * 8;   // multiple of 8: LBO a multiple of 128 B
         // one window row per unpack thread, or up to 3 for C = 64 (one 16-byte chunk per row)
         if (ta.WR > NUNP * 32 && (cv->Cb != 16 || ta.WR > 3 * NUNP * 32)) return DG_ERR_UNSUPPORTED;
         ta.lbo = ta.WR * 16;

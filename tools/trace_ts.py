@@ -16,7 +16,8 @@ M, N, K = (1, 1, 1) if CONV else map(int, (sys.argv[1] if len(sys.argv) > 1 else
 lut = dg.build_lut([0, 1, 2, 3], [-2, -1, 0, 1], 8)
 if CONV:
     from paper_2304_09049_b200 import netrun
-    runner = netrun.NetRunner(3, range(256), "cuda", layers=[int(sys.argv[1][4:])])
+    cfg = int(os.environ.get("DG_TRACE_CFG", "3"))   # 3: ResNet-50 b256, 4: VGG-16 b64
+    runner = netrun.NetRunner(cfg, range(256 if cfg == 3 else 64), "cuda", layers=[int(sys.argv[1][4:])])
     M, N, K = runner.plans[0].rows, runner.plans[0].layer.cout, runner.plans[0].K
 ld = dg.packed_ld(K)
 w = torch.randint(0, 256, (M, ld), dtype=torch.uint8, device="cuda")
