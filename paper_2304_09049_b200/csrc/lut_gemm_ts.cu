@@ -81,11 +81,13 @@ struct TsCfg {
     static constexpr int SA = ASM ? 4 : ((512 - NACC * BN) / ACOLS > 8 ? 8 : (512 - NACC * BN) / ACOLS);   // A stages
     static constexpr int B_ATOM = BN * KA;                  // bytes of one 128-code B atom
     static constexpr int B_BYTES = BN * KST;
-    static constexpr int SB_RAW = (WIN && BN == 64 ? 49152 : (BN == 64 || WIN || ASM ? 98304 : 131072)) / B_BYTES;
-    static constexpr int SB = SB_RAW > 8 ? 8 : SB_RAW;      // B (int8) smem stages
+    // WIN with 128-code stages = the C = 128 tile mode: all 9 weight stages (128 x 1152) resident
+    static constexpr bool WIN128 = WIN && KST == 128;
+    static constexpr int SB_RAW = (WIN128 ? 147456 : (WIN && BN == 64 ? 49152 : (BN == 64 || WIN || ASM ? 98304 : 131072))) / B_BYTES;
+    static constexpr int SB = SB_RAW > (WIN128 ? 9 : 8) ? (WIN128 ? 9 : 8) : SB_RAW;   // B (int8) smem stages
     static constexpr int TMEM_A0 = NACC * BN;               // first A column
     static constexpr int TMEM_COLS = 512;
-    static constexpr int P_REGION = WIN ? (BN == 64 ? 155648 : 106496) : (ASM ? 32768 : 4 * BM * PKS_MAX);   // packed P / WIN ring + windows
+    static constexpr int P_REGION = WIN ? (WIN128 ? 65536 : (BN == 64 ? 155648 : 106496)) : (ASM ? 32768 : 4 * BM * PKS_MAX);   // packed P / WIN ring + windows
     static constexpr int A_STAGE = ASM ? BM * KST : 0;       // ASM: one A stage, 16-byte K chunk j of row r at j*BM*16 + r*16
     static constexpr int OFF_B = 0;                          // 1024-aligned (SW128)
     static constexpr int OFF_P = OFF_B + SB * B_BYTES;
@@ -180,8 +182,11 @@ struct TsArgs {
 
 // WIN "tile mode": C = 64 (18 k-steps of 32 codes = 9 taps x 2 chunks, stages 8 + 8 + 2) with the
 // weights resident in shared memory, so a tile needs one hand-off and one burst of 18 MMAs
+// (and C = 128 with 128-code stages: 36 k-steps = 9 taps x 4 chunks, 9 stages of 4)
 DG_DEV bool win_tile_mode(const TsArgs &ta, int ksteps) {
-    return ta.bres && ta.clog2 == 6 && ksteps == 8 && ta.nstages == 3 && ta.last_ksteps == 2 && !(ta.sk > 1);
+    return ta.bres && !(ta.sk > 1) &&
+           ((ta.clog2 == 6 && ksteps == 8 && ta.nstages == 3 && ta.last_ksteps == 2) ||
+            (ta.clog2 == 7 && ksteps == 4 && ta.nstages == 9 && ta.last_ksteps == 4));
 }
 
 // Tile t -> (row block tp, column block tq).  Tiles are walked in groups of `group` row blocks,
@@ -798,7 +803,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 // and accumulates into the next accumulator buffer.
                 const uint32_t wbase = sbase + C::OFF_P + (uint32_t)(2 * w_slot + (int)(tl % w_nwin) * w_bytes);
                 const uint64_t ad = ptx::desc_k_none(wbase, w_lbo16 << 4);
-                const uint64_t bt = bdesc0 + (uint64_t)((tq * 3 * C::B_BYTES) >> 4);
+                const uint64_t bt = bdesc0 + (uint64_t)((tq * (KST == 256 ? 3 : 9) * C::B_BYTES) >> 4);
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
                 ptx::tc_fence_after();
                 if (lane == 0) TS_EV(14, g);
@@ -806,10 +811,12 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     const uint32_t u = (tl << w_pair) + (uint32_t)h;
                     const uint32_t dth = tmem + (u % NACC) * BN;
                     const uint64_t adh = ad + (uint64_t)(h * BM);   // BM rows of 16 bytes
+                    // k-step j: tap j / (C/32), channel chunk 2 (j mod C/32); B stage j / KSTEPS
+                    constexpr int CPT = KST == 256 ? 2 : 4;   // k-steps per tap (C = 64 / 128)
 #pragma unroll
-                    for (int j = 0; j < 18; ++j) {
-                        const int st = j >> 3, k = j & 7;
-                        ptx::mma_i8_ss_warp(dth, adh + (uint64_t)(w_tap[j >> 1] + (uint32_t)((j & 1) * 2) * w_lbo16),
+                    for (int j = 0; j < 9 * CPT; ++j) {
+                        const int st = j / C::KSTEPS, k = j % C::KSTEPS;
+                        ptx::mma_i8_ss_warp(dth, adh + (uint64_t)(w_tap[j / CPT] + (uint32_t)((j % CPT) * 2) * w_lbo16),
                                             bt + (uint64_t)((st * C::B_BYTES + (k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3),
                                             idesc, j > 0 ? 1u : 0u);
                     }
@@ -1715,6 +1722,13 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     // MMAs per tile, 3x3 64 -> 64 at 56x56 b256: 88 -> 54 us); C = 128 / 256 only with DG_WIN=1
     // (measured no faster than the implicit gather there)
     static const bool win_force = getenv("DG_WIN") != nullptr, win_off = getenv("DG_NO_WIN") != nullptr;
+    // C = 128, Cout <= 128 (weights 147 KB resident) when the two windows fit next to them (W <= ~30)
+    if (cv && cv->kh == 3 && cv->kw == 3 && cv->stride == 1 && cv->pad == 1 && cv->Cb == 32 && nq <= 128 && K == 1152 &&
+        !win_off && !getenv("DG_NO_WIN128") &&
+        (np / ((int64_t)cv->H * cv->W)) * (cv->H + 2) * (cv->W + 2) / BM >= 2 * num_sms()) {
+        const dg_status s = launch_ts<128, 4, 8, 128, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (s != DG_ERR_UNSUPPORTED) return s;
+    }
     if (cv && cv->kh == 3 && cv->kw == 3 && cv->stride == 1 && cv->pad == 1 && cv->Cb >= 16 && cv->Cb <= 64 &&
         (cv->Cb & (cv->Cb - 1)) == 0 && !win_off &&
         (win_force || (cv->Cb == 16 && nq <= 128 &&
