@@ -739,3 +739,31 @@ def test_digits4_rejects():
     w4 = dg.pack_codes4(torch.zeros((4, 64), dtype=torch.uint8, device=DEV))
     with pytest.raises(dg.DGError, match="RANGE"):
         dg.expand_digits4(w4, 64, [40] + [0] * 15)      # 4 x 40 > 127
+
+
+def test_conv_window_default_with_residual_and_bias():
+    """A 3x3 C = 64 conv large enough (>= 2 waves of padded-pixel tiles) to take the shifted-window
+    kernel by default (tile + pair mode) with an identity residual over packed codes and a
+    per-channel bias: the window path's general epilogue equals O-RES / O-REQ."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    lut = dg.build_lut(WL, AL, 8)
+    T = oracle.build_lut16(WL, AL)
+    g = np.random.default_rng(88)
+    B, H, C = 12, 56, 64
+    x = g.integers(0, 4, (B, H, H, C), dtype=np.uint8)
+    w = g.integers(0, 4, (C, 3, 3, C), dtype=np.uint8)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    w8 = dg.expand_operand(wp, 9 * Cp, WL)
+    p = dg.conv_params(B, H, H, C, C, 3, 3, 1, 1, 0, ldw=wp.shape[1])
+    ws = torch.empty(dg.conv_workspace_size(p), dtype=torch.uint8, device=DEV)
+    acc = oracle.conv2d_direct(x, w, T, 1, 1, 0).reshape(-1, C)
+    assert np.array_equal(host(dg.lut_conv2d_prepared(xp, w8, lut, p, ws=ws)), acc)
+    bias = g.integers(-300, 300, C).astype(np.int32)
+    rq = dg.Requant(mult=15000, shift=20, zp=0, res_codes=xp, res_mult=29, res_levels=AL,
+                    bias=torch.from_numpy(bias).to(DEV), bias_axis=0)
+    out = dg.lut_conv2d_prepared(xp, w8, lut, p, rq=rq, ws=ws)
+    r = (np.array(AL)[x.reshape(-1, C)] * 29).astype(np.int32)
+    exp = oracle.requantize(acc, 15000, 20, 0, 0, 3, res=r, bias=bias, bias_axis=0)
+    assert np.array_equal(oracle_codes_of(out, exp.shape[0], C), exp)
