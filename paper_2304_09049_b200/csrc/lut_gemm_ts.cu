@@ -76,9 +76,10 @@ struct TsCfg {
     static constexpr int HALVES = KST / KA;                 // 128-code halves (B atoms, 32-column A parts)
     // accumulator buffers (TMEM cols NACC*BN); a multiple of EG so that each buffer has one
     // epilogue group (which then waits on its barrier phases in order)
-    static constexpr int NACC = ASM ? 512 / BN : (BN == 256 ? 1 : (BN == 128 ? 2 : 4));
+    // (ASM and WIN keep A in shared memory: all 512 TMEM columns hold accumulators)
+    static constexpr int NACC = ASM ? 512 / BN : (WIN ? 4 : (BN == 256 ? 1 : (BN == 128 ? 2 : 4)));
     static_assert(NACC % EG == 0, "accumulator buffers per epilogue group");
-    static constexpr int SA = ASM ? 4 : ((512 - NACC * BN) / ACOLS > 8 ? 8 : (512 - NACC * BN) / ACOLS);   // A stages
+    static constexpr int SA = (ASM || WIN) ? 4 : ((512 - NACC * BN) / ACOLS > 8 ? 8 : (512 - NACC * BN) / ACOLS);   // A stages (WIN: windows)
     static constexpr int B_ATOM = BN * KA;                  // bytes of one 128-code B atom
     static constexpr int B_BYTES = BN * KST;
     // WIN with 128-code stages = the C = 128 tile mode: all 9 weight stages (128 x 1152) resident
@@ -98,7 +99,7 @@ struct TsCfg {
     static constexpr int OFF_WALK = OFF_TMEM + 16;           // 32 words: the MMA warp's copy of the tile walk
     static constexpr int OFF_TAB = (OFF_WALK + 128 + 15) / 16 * 16;   // 16-bit requant offsets, one u32 per column pair
     static constexpr int ALLOC = OFF_TAB + TAB_PAIRS * 4 + 1024;
-    static_assert((ASM ? NACC * BN : TMEM_A0 + SA * ACOLS) <= TMEM_COLS && SA >= 2, "TMEM budget");
+    static_assert(((ASM || WIN) ? NACC * BN : TMEM_A0 + SA * ACOLS) <= TMEM_COLS && SA >= 2, "TMEM budget");
     static_assert(ALLOC <= 232448, "shared memory budget");
 };
 
@@ -1516,7 +1517,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         ta.ntp = (int32_t)((ta.nqv + BM - 1) / BM);
         // pair mode (tile mode on 64-wide tiles: C = 64, Cout <= 64, K = 576, weights resident): one window feeds 2 row blocks, so the halo rows are filled once per 2 blocks
         static const bool no_pair = getenv("DG_NO_WPAIR") != nullptr;
-        ta.wpair = (BN == 64 && KST == 256 && cv->Cb == 16 && K == 576 && nq <= 64 && !no_pair) ? 1 : 0;
+        ta.wpair = ((BN == 64 || BN == 128) && KST == 256 && cv->Cb == 16 && K == 576 && nq <= BN && !no_pair) ? 1 : 0;
         if (ta.wpair) ta.ntp = (ta.ntp + 1) / 2;
         ta.WR = ((BM << ta.wpair) + 2 * (int32_t)Wp + 2 + 7) / 8 * 8;   // multiple of 8: LBO a multiple of 128 B
         // one window row per unpack thread, or up to 3 for C = 64 (one 16-byte chunk per row)
