@@ -88,7 +88,7 @@ struct TsCfg {
     static constexpr int SB = SB_RAW > (WIN128 ? 9 : 8) ? (WIN128 ? 9 : 8) : SB_RAW;   // B (int8) smem stages
     static constexpr int TMEM_A0 = NACC * BN;               // first A column
     static constexpr int TMEM_COLS = 512;
-    static constexpr int P_REGION = WIN ? (WIN128 ? 65536 : (BN == 64 ? 155648 : 106496)) : (ASM ? 32768 : 4 * BM * PKS_MAX);   // packed P / WIN ring + windows
+    static constexpr int P_REGION = WIN ? (WIN128 ? 70656 : (BN == 64 ? 155648 : 106496)) : (ASM ? 32768 : 4 * BM * PKS_MAX);   // packed P / WIN ring + windows
     static constexpr int A_STAGE = ASM ? BM * KST : 0;       // ASM: one A stage, 16-byte K chunk j of row r at j*BM*16 + r*16
     static constexpr int OFF_B = 0;                          // 1024-aligned (SW128)
     static constexpr int OFF_P = OFF_B + SB * B_BYTES;
@@ -953,7 +953,45 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         fetch(blockIdx.x, 0);
         fetch(blockIdx.x + gridDim.x, 1);
         uint32_t tl = 0;
-        if (nrt > 1) {   // (host guarantees C = 64: one 16-byte chunk per row)
+        if (nrt > 1 && nch == 2) {   // C = 128 (two 16-byte chunks per row), up to 2 rows per thread
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+                const int slot = (int)(tl & 1u), wb = (int)(tl % ta.nwin);
+                ptx::cp_async_wait<WRING - 1>();
+                uint32_t a[2][32];
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int row = tid + i * NUNP * 32;
+#pragma unroll
+                    for (int c = 0; c < 2; ++c) {
+                        const uint4 v = (i < nrt && row < ta.WR) ? ptx::lds128(ring + (uint32_t)(slot * ta.wslot + row * cb + 16 * c))
+                                                                 : make_uint4(0, 0, 0, 0);
+                        const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                        for (int q = 0; q < 4; ++q) {
+                            const uint4 o = unpack16_levels(w[q], ta.lp);
+                            a[i][16 * c + 4 * q] = o.x; a[i][16 * c + 4 * q + 1] = o.y;
+                            a[i][16 * c + 4 * q + 2] = o.z; a[i][16 * c + 4 * q + 3] = o.w;
+                        }
+                    }
+                }
+                fetch(t + 2 * (int)gridDim.x, slot);   // the slot's bytes are consumed: refill it
+                ptx::mbar_wait(empty_a(wb), ((tl / ta.nwin) & 1u) ^ 1u);   // the window's previous tile finished
+#pragma unroll
+                for (int i = 0; i < 2; ++i) {
+                    const int row = tid + i * NUNP * 32;
+                    if (i >= nrt || row >= ta.WR) break;
+                    const uint32_t wdst = wins + (uint32_t)(wb * ta.wbytes + row * 16);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j)
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(wdst + (uint32_t)(j * ta.lbo)),
+                                     "r"(a[i][4 * j]), "r"(a[i][4 * j + 1]), "r"(a[i][4 * j + 2]), "r"(a[i][4 * j + 3])
+                                     : "memory");
+                }
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(full_a(wb));
+            }
+        } else if (nrt > 1) {   // (host guarantees C = 64: one 16-byte chunk per row)
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
                 const int slot = (int)(tl & 1u), wb = (int)(tl % ta.nwin);
                 ptx::cp_async_wait<WRING - 1>();
@@ -1520,15 +1558,18 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         ta.wpair = ((BN == 64 || BN == 128) && KST == 256 && cv->Cb == 16 && K == 576 && nq <= BN && !no_pair) ? 1 : 0;
         if (ta.wpair) ta.ntp = (ta.ntp + 1) / 2;
         ta.WR = ((BM << ta.wpair) + 2 * (int32_t)Wp + 2 + 7) / 8 * 8;   // multiple of 8: LBO a multiple of 128 B
-        // one window row per unpack thread, or up to 3 for C = 64 (one 16-byte chunk per row)
-        if (ta.WR > NUNP * 32 && (cv->Cb != 16 || ta.WR > 3 * NUNP * 32)) return DG_ERR_UNSUPPORTED;
+        // one window row per unpack thread, or up to 3 for C = 64 / 2 for C = 128
+        if (ta.WR > NUNP * 32 && !((cv->Cb == 16 && ta.WR <= 3 * NUNP * 32) || (cv->Cb == 32 && ta.WR <= 2 * NUNP * 32)))
+            return DG_ERR_UNSUPPORTED;
         ta.lbo = ta.WR * 16;
         int lg = 0;
         while ((1 << lg) < 4 * cv->Cb) ++lg;
         ta.clog2 = lg;
         ta.wslot = (ta.WR * cv->Cb + 127) / 128 * 128;
         ta.wbytes = (cv->Cb / 4) * ta.lbo;
-        ta.nwin = (2 * ta.wslot + 3 * ta.wbytes <= C::P_REGION && C::SA >= 3) ? 3 : 2;
+        // (one window when only one fits: its fill then waits for the previous tile's MMAs)
+        ta.nwin = (2 * ta.wslot + 3 * ta.wbytes <= C::P_REGION && C::SA >= 3) ? 3
+                  : (2 * ta.wslot + 2 * ta.wbytes <= C::P_REGION ? 2 : 1);
         if (2 * ta.wslot + ta.nwin * ta.wbytes > C::P_REGION || ta.nwin > C::SA) return DG_ERR_UNSUPPORTED;
         ta.fd_hpwp = make_fastdiv((uint32_t)(Hp * Wp));
         ta.fd_wp = make_fastdiv((uint32_t)Wp);

@@ -449,6 +449,7 @@ WIN_CONVS = [  # B, H, W, C, Cout, pad_code: 3x3 / stride 1 / pad 1 shapes of th
     (1, 6, 224, 64, 128, 1),      # VGG width: 582-row window, 3 rows per thread, pad code 1
     (3, 28, 28, 128, 128, 0),     # C = 128 tile mode (weights resident), ResNet-50 stage-2 shape
     (2, 20, 13, 128, 96, 2),      # C = 128 tile mode, ragged Cout and tiles, pad code 2
+    (1, 9, 112, 128, 128, 0),     # C = 128 at VGG width: one window (2 rows per thread) beside the weights
 ]
 
 
