@@ -17,6 +17,9 @@ Parity status per function (DESIGN.md §4 lists the pins):
   requantize         pinned (exact Fraction arithmetic over all ties)
   quantize           pinned (Eq. 1 worked examples S:57-59)
   freivalds_rows     pinned (accepts the true C, rejects single-element faults)
+  conv_freivalds     pinned (accepts or_conv2d_direct's output incl. padding / stride / pad
+                     codes, rejects every single-element fault and swapped channels / pixels,
+                     equals freivalds_rows on 1x1 convs)
   resnet18_chain     parity unpinned by the paper (it prints no network outputs);
                      pinned only through its per-layer parts above.
 """
@@ -61,6 +64,8 @@ def _load():
         lib.or_quantize.argtypes = [P, i64, ctypes.c_float, ctypes.c_float, i32, i32, P]
         lib.or_freivalds_rows.argtypes = [P, P, P, i64, i64, i64, i64, P, P, P]
         lib.or_freivalds_rows.restype = i64
+        lib.or_conv_freivalds.argtypes = [P, P] + [i32] * 9 + [ctypes.c_uint8, P, P, i64, P, P]
+        lib.or_conv_freivalds.restype = i64
         _lib = lib
     return _lib
 
@@ -213,4 +218,33 @@ def freivalds_rows(W: np.ndarray, At: np.ndarray, C: np.ndarray, T, trials: int 
         bad += lib.or_freivalds_rows(Wp, Atp, C.ctypes.data_as(ctypes.c_void_p), N, M, N, K, Tp,
                                      x.ctypes.data_as(ctypes.c_void_p),
                                      H.ctypes.data_as(ctypes.c_void_p))
+    return int(bad)
+
+
+def conv_freivalds(x: np.ndarray, w: np.ndarray, T, stride: int, pad: int, pad_code: int, out: np.ndarray,
+                   trials: int = 1, seed: int = 0) -> int:
+    """Exact Freivalds check of a whole conv output (or_conv_freivalds): x [B][H][W][C] codes,
+    w [Cout][kh][kw][C] codes, out int32 [B*Ho*Wo][Cout] (or [B][Ho][Wo][Cout]).  The random
+    pixel weights are nonzero (|r| in [1, 2^15]), so any single wrong element is always caught.
+    Returns the number of inconsistent output channels summed over trials (0 = consistent)."""
+    lib = _load()
+    x, xp = _c(x, np.uint8)
+    w, wp = _c(w, np.uint8)
+    T, Tp = _c(T, np.int32)
+    B, H, Wd, C = x.shape
+    Cout, kh, kw, C2 = w.shape
+    assert C == C2 and T.size == 16
+    Ho = (H + 2 * pad - kh) // stride + 1
+    Wo = (Wd + 2 * pad - kw) // stride + 1
+    P = B * Ho * Wo
+    out = np.ascontiguousarray(out.reshape(P, -1), dtype=np.int32)
+    assert out.shape[1] >= Cout
+    rng = np.random.default_rng(seed)
+    Hs = np.empty(kh * kw * C * 4 * 16, np.uint8)   # __int128 scratch
+    bad = 0
+    for _ in range(trials):
+        r = rng.integers(1, (1 << 15) + 1, size=P, dtype=np.int64) * rng.choice(np.array([-1, 1], np.int64), size=P)
+        bad += lib.or_conv_freivalds(xp, wp, B, H, Wd, C, Cout, kh, kw, stride, pad, pad_code, Tp,
+                                     out.ctypes.data_as(ctypes.c_void_p), out.shape[1],
+                                     r.ctypes.data_as(ctypes.c_void_p), Hs.ctypes.data_as(ctypes.c_void_p))
     return int(bad)

@@ -263,3 +263,58 @@ int64_t or_freivalds_rows(const uint8_t *W, const uint8_t *At, const int32_t *C,
     }
     return bad;
 }
+
+/* ------------------------------------------------------------------------ */
+/* Freivalds check of a whole convolution output (the conv of
+ * or_conv2d_direct) when the direct loops are too slow for a full
+ * batch.  For a random weight r[p] per output pixel p = (b, ho, wo):
+ *   sum_p r[p] out[p][co]
+ *     = sum_p r[p] sum_{i,j,c} T[(w[co][i][j][c] << 2) | x_code(p, i, j, c)]
+ *     = sum_{i,j,c} sum_{a<4} T[(w[co][i][j][c] << 2) | a] * H[i][j][c][a],
+ *   H[i][j][c][a] = sum_p r[p] [x_code(p, i, j, c) == a]
+ * (x_code = pad_code outside the image, as in or_conv2d_direct).  Exact in
+ * __int128.  out is int32 NHWC [B][Ho][Wo][Cout] with row pitch ldo elements;
+ * r has B*Ho*Wo entries; H_scratch holds kh*kw*C*4 __int128.  Returns the
+ * number of output channels co where the two sides differ (0 = consistent). */
+int64_t or_conv_freivalds(const uint8_t *x, const uint8_t *w, int32_t B, int32_t H, int32_t Wd,
+                          int32_t C, int32_t Cout, int32_t kh, int32_t kw, int32_t stride,
+                          int32_t pad, uint8_t pad_code, const int32_t T[16], const int32_t *out,
+                          int64_t ldo, const int64_t *r, __int128 *H_scratch)
+{
+    int32_t Ho = (H + 2 * pad - kh) / stride + 1;
+    int32_t Wo = (Wd + 2 * pad - kw) / stride + 1;
+    int64_t ntap = (int64_t)kh * kw * C;
+    for (int64_t t = 0; t < ntap * 4; ++t) H_scratch[t] = 0;
+    for (int32_t b = 0; b < B; ++b)
+        for (int32_t ho = 0; ho < Ho; ++ho)
+            for (int32_t wo = 0; wo < Wo; ++wo) {
+                int64_t p = ((int64_t)b * Ho + ho) * Wo + wo;
+                for (int32_t i = 0; i < kh; ++i)
+                    for (int32_t j = 0; j < kw; ++j)
+                        for (int32_t c = 0; c < C; ++c) {
+                            int32_t hi = ho * stride - pad + i;
+                            int32_t wi = wo * stride - pad + j;
+                            int a;
+                            if (hi < 0 || hi >= H || wi < 0 || wi >= Wd)
+                                a = pad_code & 3;
+                            else
+                                a = x[(((int64_t)b * H + hi) * Wd + wi) * C + c] & 3;
+                            H_scratch[(((int64_t)i * kw + j) * C + c) * 4 + a] += r[p];
+                        }
+            }
+    int64_t bad = 0;
+    int64_t P = (int64_t)B * Ho * Wo;
+    for (int32_t co = 0; co < Cout; ++co) {
+        __int128 lhs = 0, rhs = 0;
+        for (int64_t p = 0; p < P; ++p) lhs += (__int128)out[p * ldo + co] * r[p];
+        for (int32_t i = 0; i < kh; ++i)
+            for (int32_t j = 0; j < kw; ++j)
+                for (int32_t c = 0; c < C; ++c) {
+                    int wc = w[(((int64_t)co * kh + i) * kw + j) * C + c] & 3;
+                    for (int a = 0; a < 4; ++a)
+                        rhs += (__int128)T[(wc << 2) | a] * H_scratch[(((int64_t)i * kw + j) * C + c) * 4 + a];
+                }
+        if (lhs != rhs) ++bad;
+    }
+    return bad;
+}

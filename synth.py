@@ -259,6 +259,36 @@ def counter_codes(start: int, count: int, key, dist: str = "uniform", device="cp
     return torch.where(r < half, torch.zeros_like(r), nz).to(torch.uint8)
 
 
+_SG = None
+
+
+def _sg_lib():
+    """synth_gen.c (the same counter generator in C + OpenMP), compiled on first use."""
+    global _SG
+    if _SG is None:
+        import ctypes
+        import os
+        import subprocess
+        here = os.path.dirname(os.path.abspath(__file__))
+        src, lib = os.path.join(here, "synth_gen.c"), os.path.join(here, "synth_gen.so")
+        if not os.path.exists(lib) or os.path.getmtime(lib) < os.path.getmtime(src):
+            tmp = lib + f".{os.getpid()}.tmp"
+            subprocess.check_call(["gcc", "-O3", "-fopenmp", "-fPIC", "-shared", src, "-o", tmp])
+            os.replace(tmp, lib)
+        L = ctypes.CDLL(lib)
+        L.sg_counter_codes.argtypes = [ctypes.c_int64, ctypes.c_int64, ctypes.c_uint64, ctypes.c_int32, ctypes.c_void_p]
+        _SG = L
+    return _SG
+
+
+def counter_codes_host(start: int, count: int, key, dist: str = "uniform") -> np.ndarray:
+    """counter_codes on the host as a numpy uint8 array (synth_gen.c; identical values)."""
+    out = np.empty(count, np.uint8)
+    _sg_lib().sg_counter_codes(start, count, _key64(key) & _M64, 0 if dist == "uniform" else 1,
+                               out.ctypes.data)
+    return out
+
+
 def counter_codes_chunked(start: int, count: int, key, dist: str = "uniform", device="cpu", chunk: int = 1 << 24):
     """counter_codes for large counts without int64 temporaries of the full size."""
     import torch

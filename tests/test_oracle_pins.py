@@ -419,3 +419,56 @@ def test_conv_bits_against_pinned_routes(bits):
     ws = g.integers(0, 16, (1, 3, 3, 2), dtype=np.uint8)
     cnt = oracle.conv2d_direct_bits(xs, ws, ones, 1, 1, bits)[0, :, :, 0]
     assert cnt[2, 2] == 18 and cnt[0, 2] == 12 and cnt[0, 0] == 8
+
+
+# ---------------------------------------------------------------- whole-output conv Freivalds
+CONV_FV = [  # B, H, W, C, Cout, k, stride, pad, pad_code
+    (2, 7, 6, 5, 4, 3, 1, 1, 0), (1, 9, 9, 8, 3, 3, 2, 1, 2), (2, 5, 7, 4, 6, 1, 2, 0, 0),
+    (1, 8, 8, 3, 5, 5, 1, 2, 3), (3, 6, 6, 4, 2, 3, 1, 1, 1), (1, 11, 10, 4, 3, 7, 2, 3, 0),
+]
+
+
+@pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", CONV_FV)
+def test_conv_freivalds_accepts_truth_rejects_every_single_fault(B, H, W, C, Cout, k, stride, pad, pad_code):
+    """or_conv_freivalds against the pinned direct conv: the true output
+    passes for any table, stride, padding and pad code; a +-1 fault at EVERY output element, a
+    swap of two channels and a swap of two pixels are each caught (r[p] is never 0)."""
+    g = np.random.default_rng(B * 100 + H * 10 + k + pad_code)
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, k, k, C), dtype=np.uint8)
+    T = g.integers(-50, 51, 16).astype(np.int32)          # non-product table
+    out = oracle.conv2d_direct(x, w, T, stride, pad, pad_code).reshape(-1, Cout)
+    assert oracle.conv_freivalds(x, w, T, stride, pad, pad_code, out, trials=2) == 0
+    for p in range(out.shape[0]):
+        for co in range(Cout):
+            bad = out.copy()
+            bad[p, co] += 1 if (p + co) % 2 else -1
+            assert oracle.conv_freivalds(x, w, T, stride, pad, pad_code, bad, seed=p) == 1, (p, co)
+    sw = out.copy()
+    sw[:, [0, 1]] = sw[:, [1, 0]]
+    if not np.array_equal(sw, out):
+        assert oracle.conv_freivalds(x, w, T, stride, pad, pad_code, sw) >= 1
+    sp = out.copy()
+    sp[[0, -1]] = sp[[-1, 0]]
+    if not np.array_equal(sp, out):
+        assert oracle.conv_freivalds(x, w, T, stride, pad, pad_code, sp) >= 1
+    # the pad code matters wherever a tap leaves the image: a wrong pad code is rejected
+    if pad > 0:
+        assert oracle.conv_freivalds(x, w, T, stride, pad, (pad_code + 1) % 4, out) >= 1
+
+
+def test_conv_freivalds_1x1_agrees_with_gemm_freivalds():
+    """A 1x1 / stride-1 conv is the GEMM C^T = LUTGEMM(W, X^T): both whole-output checks
+    accept the truth and reject the same injected fault."""
+    g = np.random.default_rng(12)
+    B, H, W, C, Cout = 2, 5, 6, 9, 7
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, 1, 1, C), dtype=np.uint8)
+    T = oracle.build_lut16([-2, -1, 0, 1], [0, 1, 2, 3])
+    out = oracle.conv2d_direct(x, w, T, 1, 0, 0).reshape(-1, Cout)
+    Wm, Xt = w.reshape(Cout, C), x.reshape(-1, C)
+    assert oracle.conv_freivalds(x, w, T, 1, 0, 0, out) == 0
+    assert oracle.freivalds_rows(Wm, Xt, np.ascontiguousarray(out.T), T) == 0
+    out[3, 4] += 7
+    assert oracle.conv_freivalds(x, w, T, 1, 0, 0, out) == 1
+    assert oracle.freivalds_rows(Wm, Xt, np.ascontiguousarray(out.T), T) >= 1
