@@ -163,6 +163,9 @@ def run_conv(args, ws, rank, local):
     from paper_2304_09049_b200 import shard
     images = list(shard.batch_shard(rank, ws, batch))         # weak scaling: disjoint shards
     torch.cuda.synchronize()
+    # weights and biases are prepared once here and synchronised: the step's kernels may read them
+    # before their programmatic-dependent-launch wait (dg.h "early_weights")
+    dg.set_option("early_weights", 1)
     runner = netrun.NetRunner(cfg, images, "cuda", variant=args.variant)
     nl = len(runner.plans)
     stream = torch.cuda.current_stream()

@@ -63,7 +63,7 @@ typedef int32_t dg_status;
 DG_API const char *dg_status_string(dg_status s);
 
 /* ABI version of this header (bumped on any signature change). */
-#define DG_ABI_VERSION 2
+#define DG_ABI_VERSION 3
 DG_API int32_t dg_abi_version(void);
 
 /* Number of CUDA kernels this library has enqueued since it was loaded (all
@@ -71,6 +71,41 @@ DG_API int32_t dg_abi_version(void);
  * capture counts once, at capture).  Process-wide, thread-safe; for the
  * benchmark's launch count (kernels per step = difference across one step). */
 DG_API uint64_t dg_kernel_launches(void);
+
+/* ---------------------------------------------------------------------------
+ * Runtime options (process-wide; every call reads them when it dispatches, so a change
+ * applies to the next call).  They select among kernel instances that compute the SAME
+ * result (ablations, tests that force an instance); none changes any output bit.
+ * Defaults are the tuned dispatch; the DG_* environment variables of DESIGN.md §6.1 set
+ * the initial values.  DG_ERR_INVALID_ARG for an unknown name.
+ *   "win"       0 auto, 1 force the shifted-window kernel for every 3x3/s1/p1 conv with
+ *               C in {64,128,256}, -1 never                                    (default 0)
+ *   "win128"    C = 128 tile mode of the window kernel in auto dispatch       (1)
+ *   "wpair"     window pair mode (one window feeds two row blocks)           (1)
+ *   "asm"       short-K wide tiles with the A operand in shared memory       (1)
+ *   "bn256"     128x256 tiles for long K                                     (1)
+ *   "bn256_k"   minimum K (codes) for the 128x256 tiles                      (512)
+ *   "kst"       codes per pipeline stage: 0 auto, 128 force 128-code stages  (0)
+ *   "bn64_short" short-K layers with Cout > 64 on 64-wide tiles              (0)
+ *   "splitk"    split-K for few-tile long-K GEMMs when workspace is given    (1)
+ *   "f16"       16-bit SIMD requant epilogue (else the 32-bit threshold path)(1)
+ *   "bres"      weight tiles resident in shared memory when they fit         (1)
+ *   "pdl"       programmatic dependent launch of the GEMM kernels            (1)
+ *   "early_weights"  the *_prepared calls may read their expanded weights and bias
+ *               BEFORE waiting for the previous kernel on the stream (programmatic
+ *               dependent launch: their prologue then overlaps that kernel's tail).
+ *               Only correct when neither was written by a kernel still in flight
+ *               on the stream (e.g. weights prepared at setup and synchronised).   (0)
+ *   "f4conv"    route qualifying product-table layers to the block-scaled FP4 kernel (1)
+ */
+DG_API dg_status dg_set_option(const char *name, int64_t value);
+DG_API dg_status dg_get_option(const char *name, int64_t *value);
+DG_API dg_status dg_reset_options(void);   /* back to the defaults (environment ignored) */
+
+/* Tag of the GEMM/conv kernel instance the CALLING THREAD launched last (static storage,
+ * never NULL, "" before the first launch), e.g. "ts bn=128 epi=4 unp=8 kst=128 win nwin=2
+ * wpair=0 ...": lets tests assert which instance computed a result. */
+DG_API const char *dg_last_kernel(void);
 
 /* ---------------------------------------------------------------------------
  * S4 — LUT build.  LUT-16 (§3.2): "The values stored in the LUT are all

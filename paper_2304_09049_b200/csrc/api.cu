@@ -1,5 +1,6 @@
 // api.cu — the C ABI of libdg (include/dg.h): host-side validation, LUT build (S4),
 // variant dispatch and the conv orchestration (im2col + LUT GEMM + fused requant).
+#include <stdlib.h>
 #include <string.h>
 
 #include "common.cuh"
@@ -9,6 +10,48 @@ using namespace dg;
 uint64_t &dg::launch_counter() {
     static uint64_t n = 0;
     return n;
+}
+
+namespace {
+
+struct OptDesc {
+    const char *name, *env;
+    int64_t def;
+    int64_t env_val;   // value an environment variable sets (its presence; DG_BN256_K: its number)
+};
+// name, initialising environment variable (ablation switches of DESIGN.md §6.1), default, env value
+const OptDesc kOpts[dg::OPT_COUNT] = {
+    {"win", "DG_WIN", 0, 1},            {"win128", "DG_NO_WIN128", 1, 0}, {"wpair", "DG_NO_WPAIR", 1, 0},
+    {"asm", "DG_NO_ASM", 1, 0},         {"bn256", "DG_TS_NO_BN256", 1, 0}, {"bn256_k", "DG_BN256_K", 512, -1},
+    {"kst", "DG_TS_K128", 0, 128},      {"bn64_short", "DG_BN64_SHORT", 0, 1}, {"splitk", "DG_NO_SPLITK", 1, 0},
+    {"f16", "DG_NO_F16", 1, 0},         {"bres", "DG_NO_BRES", 1, 0},     {"pdl", "DG_NO_PDL", 1, 0},
+    {"early_weights", "DG_EARLY_WEIGHTS", 0, 1}, {"f4conv", "DG_NO_F4CONV", 1, 0},
+};
+
+int64_t *opt_table() {
+    static int64_t v[dg::OPT_COUNT];
+    static bool init = false;   // (first touch happens on the loading thread, before any call returns)
+    if (!init) {
+        for (int i = 0; i < dg::OPT_COUNT; ++i) {
+            v[i] = kOpts[i].def;
+            const char *e = getenv(kOpts[i].env);
+            if (e) v[i] = kOpts[i].env_val >= 0 ? kOpts[i].env_val : atoll(e);
+        }
+        if (getenv("DG_NO_WIN")) v[dg::OPT_WIN] = -1;
+        init = true;
+    }
+    return v;
+}
+__attribute__((constructor)) void opt_init() { opt_table(); }
+
+thread_local char g_last_kernel[160] = "";
+
+}  // namespace
+
+int64_t dg::opt(dg::OptId id) { return __atomic_load_n(&opt_table()[id], __ATOMIC_RELAXED); }
+void dg::set_last_kernel(const char *tag) {
+    strncpy(g_last_kernel, tag, sizeof(g_last_kernel) - 1);
+    g_last_kernel[sizeof(g_last_kernel) - 1] = 0;
 }
 
 namespace {
@@ -93,6 +136,33 @@ const char *dg_status_string(dg_status s) {
 int32_t dg_abi_version(void) { return DG_ABI_VERSION; }
 
 uint64_t dg_kernel_launches(void) { return __atomic_load_n(&dg::launch_counter(), __ATOMIC_RELAXED); }
+
+dg_status dg_set_option(const char *name, int64_t value) {
+    if (!name) return DG_ERR_INVALID_ARG;
+    for (int i = 0; i < dg::OPT_COUNT; ++i)
+        if (!strcmp(name, kOpts[i].name)) {
+            __atomic_store_n(&opt_table()[i], value, __ATOMIC_RELAXED);
+            return DG_OK;
+        }
+    return DG_ERR_INVALID_ARG;
+}
+
+dg_status dg_get_option(const char *name, int64_t *value) {
+    if (!name || !value) return DG_ERR_INVALID_ARG;
+    for (int i = 0; i < dg::OPT_COUNT; ++i)
+        if (!strcmp(name, kOpts[i].name)) {
+            *value = dg::opt((dg::OptId)i);
+            return DG_OK;
+        }
+    return DG_ERR_INVALID_ARG;
+}
+
+dg_status dg_reset_options(void) {
+    for (int i = 0; i < dg::OPT_COUNT; ++i) __atomic_store_n(&opt_table()[i], kOpts[i].def, __ATOMIC_RELAXED);
+    return DG_OK;
+}
+
+const char *dg_last_kernel(void) { return g_last_kernel; }
 
 dg_status dg_build_lut(const int32_t wl[4], const int32_t al[4], int32_t entry_bits, dg_lut *out) {
     if (!wl || !al || !out) return DG_ERR_INVALID_ARG;
@@ -198,7 +268,7 @@ dg_status dg_lut_gemm_onehot(const uint8_t *d_w1h, int64_t ldw1h, const int8_t *
     // one-hot side: codes 0 / 1 with identity levels; the expanded side's "levels" only bound |acc|
     const int32_t pl[4] = {0, 1, 0, 0}, ql[4] = {(int32_t)emax, 0, 0, 0};
     return lut_gemm_ts(d_w1h, ldw1h, d_atc, ldatc, M, N, 4 * K, pl, ql, d_c, ldc, rq ? &a : nullptr,
-                       (cudaStream_t)stream);
+                       (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, true);
 }
 
 // ---- 4-bit operands as 2-bit digit pairs (dg.h)
@@ -235,7 +305,8 @@ dg_status dg_lut_gemm4_prepared(const uint8_t *d_at4, int64_t lda, const int8_t 
     if (rq) a = to_args(rq);
     // digit side: identity levels; the weights' side levels only bound |acc| (true bound 15 K wmax)
     const int32_t pl[4] = {0, 1, 2, 3}, ql[4] = {(5 * wmax + 1) / 2, 0, 0, 0};
-    return lut_gemm_ts(d_at4, lda, d_w8, ld8, N, M, 2 * K, pl, ql, d_ct, ldct, rq ? &a : nullptr, (cudaStream_t)stream);
+    return lut_gemm_ts(d_at4, lda, d_w8, ld8, N, M, 2 * K, pl, ql, d_ct, ldct, rq ? &a : nullptr, (cudaStream_t)stream,
+                       nullptr, nullptr, 0, nullptr, 0, true);
 }
 
 dg_status dg_lut_conv2d4_prepared(const uint8_t *d_x4, const int8_t *d_w8, int64_t ld8, const int32_t levels[16],
@@ -296,7 +367,7 @@ dg_status dg_lut_gemm_prepared(const uint8_t *d_w, int64_t ldw, const int8_t *d_
     RequantArgs a{};
     if (rq) a = to_args(rq);
     return lut_gemm_ts(d_w, ldw, d_at8, ld8, M, N, K, lut->wl, lut->al, d_c, ldc, rq ? &a : nullptr,
-                       (cudaStream_t)stream);
+                       (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, true);
 }
 
 dg_status dg_lut_gemm_prepared_allgather(const uint8_t *d_w, int64_t ldw, const int8_t *d_at8, int64_t ld8,
@@ -313,7 +384,7 @@ dg_status dg_lut_gemm_prepared_allgather(const uint8_t *d_w, int64_t ldw, const 
         return DG_ERR_UNSUPPORTED;
     if ((int64_t)K * max_abs_entry(lut->entries) >= ((int64_t)1 << 31)) return DG_ERR_OVERFLOW;
     return lut_gemm_ts(d_w, ldw, d_at8, ld8, M, N, K, lut->wl, lut->al, d_c, ldc, nullptr, (cudaStream_t)stream,
-                       nullptr, nullptr, 0, d_c_peers, npeers);
+                       nullptr, nullptr, 0, d_c_peers, npeers, true);
 }
 
 static bool conv_implicit_ok(const dg_conv_params *p, const uint8_t *d_x) {
@@ -452,11 +523,11 @@ dg_status dg_lut_conv2d_prepared(const uint8_t *d_x, const int8_t *d_w8, int64_t
     }
     if (conv_is_direct(p) && aligned16(d_x))
         return lut_gemm_ts(d_x, p->C / 4, d_w8, ld8, rows, p->Cout, K, lut->al, lut->wl, d_out, ldd, rq ? &ra : nullptr, st,
-                           nullptr, skws, (size_t)skb);
+                           nullptr, skws, (size_t)skb, nullptr, 0, true);
     if (conv_implicit_ok(p, d_x)) {
         TsConv cv{d_x, p->H, p->W, p->C / 4, p->kh, p->kw, p->stride, p->pad, (int32_t)Ho, (int32_t)Wo, p->pad_code};
         return lut_gemm_ts(nullptr, 0, d_w8, ld8, rows, p->Cout, K, lut->al, lut->wl, d_out, ldd, rq ? &ra : nullptr, st,
-                           &cv, skws, (size_t)skb);
+                           &cv, skws, (size_t)skb, nullptr, 0, true);
     }
     // explicit im2col fallback (e.g. VGG conv1_1 with C = 4 padded channels)
     const int64_t ld = dg_packed_ld(K);
@@ -464,7 +535,8 @@ dg_status dg_lut_conv2d_prepared(const uint8_t *d_x, const int8_t *d_w8, int64_t
     if (!d_ws || (int64_t)ws_bytes - (int64_t)(cols - (uint8_t *)d_ws) < rows * ld) return DG_ERR_WORKSPACE;
     s = dg_im2col(d_x, p->B, p->H, p->W, p->C, p->kh, p->kw, p->stride, p->pad, (uint8_t)p->pad_code, cols, ld, stream);
     if (s != DG_OK) return s;
-    return lut_gemm_ts(cols, ld, d_w8, ld8, rows, p->Cout, K, lut->al, lut->wl, d_out, ldd, rq ? &ra : nullptr, st);
+    return lut_gemm_ts(cols, ld, d_w8, ld8, rows, p->Cout, K, lut->al, lut->wl, d_out, ldd, rq ? &ra : nullptr, st,
+                       nullptr, nullptr, 0, nullptr, 0, true);
 }
 
 }  // extern "C"

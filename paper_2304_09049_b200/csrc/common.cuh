@@ -181,6 +181,29 @@ inline RequantArgs to_args(const dg_requant *rq) {
 
 // process-wide count of kernels enqueued by the library (dg_kernel_launches)
 uint64_t &launch_counter();
+
+// Runtime options (dg_set_option; read on every call, never cached in a static).  Defaults are
+// the tuned dispatch; DG_* environment variables set the initial values (ablations).
+enum OptId {
+    OPT_WIN,            // 3x3 s1 shifted-window kernel: 0 auto, 1 force for C = 64..256, -1 never
+    OPT_WIN128,         // C = 128 tile mode of the window kernel (auto): 1 on, 0 off
+    OPT_WPAIR,          // window pair mode (2 row blocks per window): 1 on, 0 off
+    OPT_ASM,            // short-K wide tiles with A in shared memory: 1 on, 0 off
+    OPT_BN256,          // 128x256 tiles for long K: 1 on, 0 off
+    OPT_BN256_K,        // minimum K (codes) for the 128x256 tiles
+    OPT_KST,            // codes per pipeline stage: 0 auto, 128 force 128
+    OPT_BN64_SHORT,     // short K with Cout > 64 on 64-wide tiles: 0 off, 1 on
+    OPT_SPLITK,         // split-K for few-tile long-K GEMMs (workspace given): 1 on, 0 off
+    OPT_F16,            // 16-bit SIMD requant epilogue: 1 on, 0 off (32-bit thresholds)
+    OPT_BRES,           // resident weight tiles when they fit shared memory: 1 on, 0 off
+    OPT_PDL,            // programmatic dependent launch of the TS kernel: 1 on, 0 off
+    OPT_EARLY_WEIGHTS,  // *_prepared: load resident weights / bias before griddepcontrol.wait (0 off)
+    OPT_F4CONV,         // FP4 (kind::mxf4) kernel for qualifying product-table GEMM/conv layers: 0 off, 1 auto
+    OPT_COUNT
+};
+int64_t opt(OptId id);
+// tag of the GEMM kernel instance this thread launched last (dg_last_kernel)
+void set_last_kernel(const char *tag);
 inline dg_status launch_status(int nlaunched = 1) {
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) __atomic_fetch_add(&launch_counter(), (uint64_t)nlaunched, __ATOMIC_RELAXED);
@@ -235,5 +258,5 @@ struct TsConv {
 dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                       const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                       cudaStream_t st, const TsConv *cv = nullptr, void *skws = nullptr, size_t skws_bytes = 0,
-                      int32_t *const *peers = nullptr, int32_t npeers = 0);
+                      int32_t *const *peers = nullptr, int32_t npeers = 0, bool b_prepared = false);
 }  // namespace dg

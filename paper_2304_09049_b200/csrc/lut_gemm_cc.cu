@@ -226,6 +226,7 @@ dg_status lut_gemm_cc(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t l
         DG_CC_LAUNCH(4, 1);
     }
 #undef DG_CC_LAUNCH
+    set_last_kernel(nch == 1 ? "cc nch=1" : nch == 2 ? "cc nch=2" : nch == 3 ? "cc nch=3" : "cc nch=4");
     return launch_status();
 }
 

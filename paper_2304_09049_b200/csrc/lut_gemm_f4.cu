@@ -397,6 +397,7 @@ dg_status lut_gemm_f4(const uint8_t *At, int64_t lda, const uint8_t *W4, int64_t
     }
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
     lut_gemm_f4_kernel<<<grid, F4_NT, F4_ALLOC, st>>>(ma, mb, fa);
+    set_last_kernel("f4 gemm");
     return launch_status();
 }
 

@@ -513,6 +513,7 @@ dg_status launch(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t ldq, i
     if (ntiles > INT32_MAX) return DG_ERR_SHAPE;
     const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
     lut_gemm_tc_kernel<BN><<<grid, NT, Cfg<BN>::ALLOC, st>>>(mp, mq, ta, rq ? *rq : dummy);
+    set_last_kernel(BN == 256 ? "tc_ss bn=256" : BN == 128 ? "tc_ss bn=128" : "tc_ss bn=64");
     return launch_status();
 }
 

@@ -19,6 +19,7 @@
 //   warp 13       waiter: waits on the MMA-side mbarriers, hands stages to warp 14 by bar.sync
 //   warp 14       MMA issuer (one thread): tcgen05.mma [D], [A_tmem], B_desc, 4 k-steps/stage
 #include <cuda.h>
+#include <stdio.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -147,6 +148,7 @@ struct TsArgs {
     int64_t ldp;
     int32_t sp;            // packed P slots (SP_MAX max)
     int32_t bres;          // 1: all ntq x nstages B tiles resident in smem (loaded once)
+    int32_t early_b;       // 1: resident B tiles and the bias table are loaded before griddepcontrol.wait
     uint32_t lp;           // int8 levels of P codes
     void *D;
     int64_t ldd;
@@ -680,7 +682,9 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         // ---------------- producer.  The whole warp runs the loop (a lone lane 0 with 31 lanes
         // parked at the final __syncthreads ran the loop several times slower); lane 0 issues.
         uint32_t gb = 0, pslot_i = 0, pphase = 0;
-        if (!ta.bres) ptx::griddep_wait();
+        // (the B operand may have been written by the previous kernel on the stream, e.g. the weight
+        // expansion of dg_lut_conv2d: only the early_weights contract lets it be read before the wait)
+        if (!ta.bres || !ta.early_b) ptx::griddep_wait();
         if (ta.bres) {   // every B tile once: slot tq * nstages + s
             for (int tq = 0; tq < ta.ntq; ++tq)
                 for (int s = 0; s < ta.nstages; ++s) {
@@ -694,7 +698,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     }
                 }
             __syncwarp();
-            ptx::griddep_wait();
+            if (ta.early_b) ptx::griddep_wait();
         }
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             int tp, tq, sb, se;
@@ -1264,6 +1268,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         static_assert(NCH % 2 == 0, "epilogue loads 64 columns at a time");
         // 16-bit requant offsets per column pair (bias_axis 0): negA = bias - (thr0 - 1), checked
         // against int16 overflow of acc + negA; any failure sends every tile to the 32-bit path
+        if (!ta.early_b) ptx::griddep_wait();   // (the bias may come from the previous kernel)
         if (ta.f16 && ta.f16_res == 1 && threadIdx.x - EPI_WARP0 * 32 < 16)   // residual pair table (smem)
             f16tab[TAB_PAIRS - 16 + threadIdx.x - EPI_WARP0 * 32] = ta.res_pair[threadIdx.x - EPI_WARP0 * 32];
         if (ta.f16 && ta.f16_tab) {
@@ -1526,6 +1531,7 @@ bool f16_params(int64_t t0, int64_t t1, int64_t t2, uint32_t &m_out, uint32_t &c
 // extra all-gather destinations of the current lut_gemm_ts call (set there, read by launch_ts)
 thread_local int32_t *const *g_peers = nullptr;
 thread_local int32_t g_npeers = 0;
+thread_local bool g_b_prepared = false;   // the B operand / bias are caller-prepared set-up data
 
 template <int BN, int NEPI, int NUNP, int KST, bool WIN = false, bool ASM = false, bool SK = false>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
@@ -1554,8 +1560,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         if (ta.nqv >= ((int64_t)1 << 31)) return DG_ERR_SHAPE;
         ta.ntp = (int32_t)((ta.nqv + BM - 1) / BM);
         // pair mode (tile mode on 64-wide tiles: C = 64, Cout <= 64, K = 576, weights resident): one window feeds 2 row blocks, so the halo rows are filled once per 2 blocks
-        static const bool no_pair = getenv("DG_NO_WPAIR") != nullptr;
-        ta.wpair = ((BN == 64 || BN == 128) && KST == 256 && cv->Cb == 16 && K == 576 && nq <= BN && !no_pair) ? 1 : 0;
+        ta.wpair = ((BN == 64 || BN == 128) && KST == 256 && cv->Cb == 16 && K == 576 && nq <= BN && opt(OPT_WPAIR)) ? 1 : 0;
         if (ta.wpair) ta.ntp = (ta.ntp + 1) / 2;
         ta.WR = ((BM << ta.wpair) + 2 * (int32_t)Wp + 2 + 7) / 8 * 8;   // multiple of 8: LBO a multiple of 128 B
         // one window row per unpack thread, or up to 3 for C = 64 / 2 for C = 128
@@ -1595,7 +1600,9 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     ta.ldp = ldp;
     ta.sp = C::P_REGION / (BM * ta.pks);
     if (ta.sp > SP_MAX) ta.sp = SP_MAX;
-    ta.bres = ((int64_t)ta.ntq * ta.nstages <= C::SB && !getenv("DG_NO_BRES")) ? 1 : 0;
+    ta.bres = ((int64_t)ta.ntq * ta.nstages <= C::SB && opt(OPT_BRES)) ? 1 : 0;
+    // weights (and bias) read before griddepcontrol.wait only when the caller declared them set-up data
+    ta.early_b = (g_b_prepared && opt(OPT_EARLY_WEIGHTS)) ? 1 : 0;
     ta.lp = pack_levels_i8(pl);
     ta.D = D;
     ta.ldd = ldd;
@@ -1637,7 +1644,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
                             (rq->res && !rq->res_codes && (rq->ld_res & 3) == 0 && (((uintptr_t)rq->res) & 15) == 0);
         if (rq->res && !rq->res_codes) res_bound = 16384;   // int32 residuals: |r| < 2^14 checked per chunk
         if (rq->dir > 0 && acc_bound + res_bound <= 32767 && t[0] > -((int64_t)1 << 30) && t[2] < ((int64_t)1 << 30) &&
-            res_ok && (nq >> 1) <= TAB_PAIRS - 16 && !getenv("DG_NO_F16") && f16_params(t[0], t[1], t[2], m16, c16)) {
+            res_ok && (nq >> 1) <= TAB_PAIRS - 16 && opt(OPT_F16) && f16_params(t[0], t[1], t[2], m16, c16)) {
             const int64_t thr0m1 = t[0] - 1;
             ta.f16_m = m16;
             ta.f16_c2 = c16 * 0x10001u;
@@ -1717,7 +1724,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     lc.stream = st;
     cudaLaunchAttribute la[1];
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    la[0].val.programmaticStreamSerializationAllowed = getenv("DG_NO_PDL") ? 0 : 1;
+    la[0].val.programmaticStreamSerializationAllowed = opt(OPT_PDL) ? 1 : 0;
     lc.attrs = la;
     lc.numAttrs = 1;
     if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK>, mp, mb, ta, rqv) != cudaSuccess)
@@ -1733,6 +1740,11 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
                                (int32_t)(rq != nullptr), rqv) != cudaSuccess)
             return DG_ERR_CUDA;
     }
+    char tag[160];
+    snprintf(tag, sizeof(tag), "ts bn=%d epi=%d unp=%d kst=%d%s%s%s nwin=%d wpair=%d sk=%d bres=%d f16=%d implicit=%d bulk=%d early=%d",
+             BN, NEPI, NUNP, KST, WIN ? " win" : "", ASM ? " asm" : "", SK ? " skinst" : "", ta.nwin, ta.wpair, ta.sk,
+             ta.bres, ta.f16, ta.implicit, ta.bulk, ta.early_b);
+    set_last_kernel(tag);
     return launch_status(ta.sk > 1 ? 2 : 1);
 }
 
@@ -1754,27 +1766,26 @@ dg_status expand_operand(const uint8_t *packed, int64_t rows, int64_t K, int64_t
 dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                       const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                       cudaStream_t st, const TsConv *cv, void *skws, size_t skws_bytes, int32_t *const *peers,
-                      int32_t npeers) {
+                      int32_t npeers, bool b_prepared) {
     if (np > ((int64_t)1 << 31) - 1 || nq > ((int64_t)1 << 31) - 1) return DG_ERR_SHAPE;
     g_peers = peers;
     g_npeers = peers ? npeers : 0;
-    struct Reset { ~Reset() { g_peers = nullptr; g_npeers = 0; } } reset;
+    g_b_prepared = b_prepared;
+    struct Reset { ~Reset() { g_peers = nullptr; g_npeers = 0; g_b_prepared = false; } } reset;
+    // (every switch below is read per call: dg_set_option, include/dg.h)
+    const int64_t o_win = opt(OPT_WIN);
     // direct 3x3 / stride 1 / pad 1 convs: shifted-window kernel, which unpacks each input pixel once
     // per tile instead of once per tap.  Default for C = 64 (the "tile mode": one hand-off and 18
-    // MMAs per tile, 3x3 64 -> 64 at 56x56 b256: 88 -> 54 us); C = 128 / 256 only with DG_WIN=1
-    // (measured no faster than the implicit gather there)
-    static const bool win_force = getenv("DG_WIN") != nullptr, win_off = getenv("DG_NO_WIN") != nullptr;
-    // C = 128, Cout <= 128 (weights 147 KB resident) when the two windows fit next to them (W <= ~30)
-    if (cv && cv->kh == 3 && cv->kw == 3 && cv->stride == 1 && cv->pad == 1 && cv->Cb == 32 && nq <= 128 && K == 1152 &&
-        !win_off && !getenv("DG_NO_WIN128") &&
-        (np / ((int64_t)cv->H * cv->W)) * (cv->H + 2) * (cv->W + 2) / BM >= 2 * num_sms()) {
+    // MMAs per tile, 3x3 64 -> 64 at 56x56 b256: 88 -> 54 us) and C = 128 with Cout <= 128 (weights
+    // resident); C = 128 / 256 otherwise only when forced (measured no faster than the implicit gather)
+    const bool win_shape = cv && cv->kh == 3 && cv->kw == 3 && cv->stride == 1 && cv->pad == 1;
+    const bool two_waves = win_shape && (np / ((int64_t)cv->H * cv->W)) * (cv->H + 2) * (cv->W + 2) / BM >= 2 * num_sms();
+    if (win_shape && cv->Cb == 32 && nq <= 128 && K == 1152 && o_win >= 0 && opt(OPT_WIN128) && (two_waves || o_win > 0)) {
         const dg_status s = launch_ts<128, 4, 8, 128, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         if (s != DG_ERR_UNSUPPORTED) return s;
     }
-    if (cv && cv->kh == 3 && cv->kw == 3 && cv->stride == 1 && cv->pad == 1 && cv->Cb >= 16 && cv->Cb <= 64 &&
-        (cv->Cb & (cv->Cb - 1)) == 0 && !win_off &&
-        (win_force || (cv->Cb == 16 && nq <= 128 &&
-                       (np / ((int64_t)cv->H * cv->W)) * (cv->H + 2) * (cv->W + 2) / BM >= 2 * num_sms()))) {
+    if (win_shape && cv->Cb >= 16 && cv->Cb <= 64 && (cv->Cb & (cv->Cb - 1)) == 0 && o_win >= 0 &&
+        (o_win > 0 || (cv->Cb == 16 && nq <= 128 && two_waves))) {
         const dg_status s = nq > 64 ? launch_ts<128, 4, 8, 256, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv)
                                     : launch_ts<64, 4, 8, 256, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         if (s != DG_ERR_UNSUPPORTED) return s;
@@ -1784,26 +1795,26 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     // stages already carry 512 MMA cycles).
     const bool short_k = K <= 2 * KA;
     // split-K candidates (few output tiles, K of >= 4 stages, workspace given): the SK instances
-    static const bool no_sk = getenv("DG_NO_SPLITK") != nullptr;
+    const bool sk_on = opt(OPT_SPLITK) != 0;
     auto few = [&](int64_t bn) {
-        return skws && !no_sk && !short_k && ((np + BM - 1) / BM) * ((nq + bn - 1) / bn) * 2 <= num_sms();
+        return skws && sk_on && !short_k && ((np + BM - 1) / BM) * ((nq + bn - 1) / bn) * 2 <= num_sms();
     };
-    const bool k256 = K > KA && !getenv("DG_TS_K128");
+    const bool k256 = K > KA && opt(OPT_KST) != 128;
     // short K, wide output: 128x256 tiles with the A operand in shared memory and two TMEM accumulators
     // (measured: narrower ASM tiles with 128-code stages lose to the TMEM-A kernel at K = 256)
-    if (short_k && nq >= 256 && !getenv("DG_NO_ASM"))
+    if (short_k && nq >= 256 && opt(OPT_ASM))
         return launch_ts<256, 8, 4, 128, false, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     // 128x256 tiles halve the shared-memory bytes of B per MAC (measured: 8192^3 1666 -> 2323
     // TOPS); their single TMEM accumulator buffer cannot overlap the epilogue with the next tile,
     // so they are used only when the K loop is long (>= 24 x 128 codes).
     // 128x256 tiles for K >= 512 (measured: ResNet-50 stage-3 3x3 46 -> 35 us, downsamples -10%)
-    static const int64_t bn256_k = getenv("DG_BN256_K") ? atoll(getenv("DG_BN256_K")) : 4 * KA;
+    const int64_t bn256_k = opt(OPT_BN256_K);
     const int64_t tiles256 = ((np + BM - 1) / BM) * ((nq + 255) / 256);
-    if (nq >= 256 && K >= bn256_k && (tiles256 >= num_sms() || K >= 24 * KA) && !getenv("DG_TS_NO_BN256"))
+    if (nq >= 256 && K >= bn256_k && (tiles256 >= num_sms() || K >= 24 * KA) && opt(OPT_BN256))
         return few(256) ? launch_ts<256, 4, 8, 128, false, false, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv, skws, skws_bytes)
                         : launch_ts<256, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 
-    if (nq > 64 && !(short_k && getenv("DG_BN64_SHORT"))) {
+    if (nq > 64 && !(short_k && opt(OPT_BN64_SHORT))) {
         if (short_k && !k256) return launch_ts<128, 8, 4, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         if (short_k) return launch_ts<128, 8, 4, 256>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         if (few(128))

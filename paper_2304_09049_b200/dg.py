@@ -63,6 +63,10 @@ def lib():
             "dg_status_string": ([i32], ctypes.c_char_p),
             "dg_abi_version": ([], i32),
             "dg_kernel_launches": ([], ctypes.c_uint64),
+            "dg_set_option": ([ctypes.c_char_p, i64], i32),
+            "dg_get_option": ([ctypes.c_char_p, P], i32),
+            "dg_reset_options": ([], i32),
+            "dg_last_kernel": ([], ctypes.c_char_p),
             "dg_build_lut": ([P, P, i32, P], i32),
             "dg_lut_from_table": ([P, i32, P], i32),
             "dg_packed_ld": ([i64], i64),
@@ -105,6 +109,44 @@ def lib():
 def kernel_launches() -> int:
     """Kernels enqueued by libdg so far (dg_kernel_launches; graph capture counts each once)."""
     return int(lib().dg_kernel_launches())
+
+
+def set_option(name: str, value: int) -> None:
+    """dg_set_option: select among kernel instances computing the same result (include/dg.h)."""
+    _check(lib().dg_set_option(name.encode(), int(value)), f"dg_set_option({name})")
+
+
+def get_option(name: str) -> int:
+    v = ctypes.c_int64()
+    _check(lib().dg_get_option(name.encode(), ctypes.byref(v)), f"dg_get_option({name})")
+    return int(v.value)
+
+
+def reset_options() -> None:
+    _check(lib().dg_reset_options(), "dg_reset_options")
+
+
+class options:
+    """Context manager: ``with dg.options(win=1, splitk=0): ...`` restores the previous values."""
+
+    def __init__(self, **kw):
+        self.kw = kw
+        self.old = {}
+
+    def __enter__(self):
+        for k, v in self.kw.items():
+            self.old[k] = get_option(k)
+            set_option(k, v)
+        return self
+
+    def __exit__(self, *a):
+        for k, v in self.old.items():
+            set_option(k, v)
+
+
+def last_kernel() -> str:
+    """Tag of the GEMM kernel instance this thread launched last (dg_last_kernel)."""
+    return lib().dg_last_kernel().decode()
 
 
 def _check(status: int, what: str):

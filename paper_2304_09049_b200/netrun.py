@@ -40,6 +40,7 @@ class LayerPlan:
     K: int                 # computed reduction length (padded channels)
     direct: bool           # 1x1 / stride 1 / unpadded: the input is its own im2col matrix
     ops: int               # algorithmic 2*M*N*K with the unpadded K
+    kernel: str = ""       # dg_last_kernel() tag of the GEMM instance the layer ran (last step)
 
     @property
     def cols_ld(self) -> int:
@@ -134,7 +135,9 @@ class NetRunner:
         self.total_ops = sum(p.ops for p in self.plans)
 
     # -- the step, split into C-ABI calls so the GEMM launches can be bracketed by events
-    def step(self, gemm_events=None, stream=None):
+    def step(self, gemm_events=None, stream=None, int32_out=None):
+        """One step: every layer, requantised codes into plan.out, or (int32_out = one int32
+        [rows][Cout] buffer per layer) the raw accumulators of the same kernel instances."""
         n = 0
         for i, p in enumerate(self.plans):
             L = p.layer
@@ -142,7 +145,9 @@ class NetRunner:
                 # tensor-core path without an im2col matrix (direct 1x1 or implicit GEMM)
                 if gemm_events is not None:
                     gemm_events[i][0].record()
-                dg.lut_conv2d_prepared(p.x, p.w8, p.lut, p.params, rq=p.rq, out=p.out, stream=stream)
+                dg.lut_conv2d_prepared(p.x, p.w8, p.lut, p.params, rq=None if int32_out else p.rq,
+                                       out=int32_out[i] if int32_out else p.out, ws=self.ws, stream=stream)
+                p.kernel = dg.last_kernel()
                 if gemm_events is not None:
                     gemm_events[i][1].record()
                 n += 1
@@ -160,7 +165,9 @@ class NetRunner:
             if gemm_events is not None:
                 gemm_events[i][0].record()
             if p.w8 is not None:   # tensor-core path with the offline-expanded weights
-                dg.lut_gemm_prepared(P, p.w8, p.rows, L.cout, p.K, p.lut_t, rq=p.rq, out=p.out, stream=stream)
+                dg.lut_gemm_prepared(P, p.w8, p.rows, L.cout, p.K, p.lut_t, rq=None if int32_out else p.rq,
+                                     out=int32_out[i] if int32_out else p.out, stream=stream)
+                p.kernel = dg.last_kernel()
             else:
                 dg.lut_gemm(P, p.w, p.rows, L.cout, p.K, p.lut_t, rq=p.rq, variant=self.variant, out=p.out,
                             ws=self.ws_gemm, stream=stream)
@@ -178,6 +185,9 @@ class NetRunner:
         """One layer through the public dg_lut_conv2d call (weights expanded inside the call)."""
         p = self.plans[i]
         dg.lut_conv2d(p.x, p.w, p.lut, p.params, rq=p.rq, variant=self.variant, out=p.out, ws=self.ws, stream=stream)
+
+    def int32_buffers(self):
+        return [torch.empty((p.rows, p.layer.cout), dtype=torch.int32, device=self.device) for p in self.plans]
 
     def input_bytes(self) -> int:
         return sum(p.x.numel() for p in self.plans)

@@ -36,7 +36,7 @@ def test_every_declared_symbol_is_exported(lib):
 def test_host_calls_without_gpu():
     from paper_2304_09049_b200 import dg
     L = dg.lib()
-    assert L.dg_abi_version() == 2
+    assert L.dg_abi_version() == 3
     assert isinstance(dg.kernel_launches(), int) and dg.kernel_launches() >= 0
     assert L.dg_status_string(-4) == b"DG_ERR_OVERFLOW"
     lut = dg.build_lut([-2, -1, 0, 1], [0, 1, 2, 3], 8)
@@ -73,3 +73,25 @@ def test_extension_entries_validate_on_the_host():
     big = (ctypes.c_int32 * 16)(*([40] + [0] * 15))
     assert L.dg_expand_digits4(fake, 8, 64, 32, big, P(1 << 21), 128, None) == RANGE
     assert L.dg_lut_gemm4_prepared(fake, 20, P(1 << 21), 128, 8, 8, 64, lv16, fake, 8, None, None) == SHAPE
+
+
+def test_runtime_options_host():
+    """dg_set_option / dg_get_option / dg_reset_options: every documented name is accepted, values
+    are read back, unknown names are rejected, reset restores the defaults; dg_last_kernel is a
+    (possibly empty) string before any launch on this thread."""
+    from paper_2304_09049_b200 import dg
+    src = open(os.path.join(ROOT, "include", "dg.h")).read()
+    names = re.findall(r'^ \*   "(\w+)"', src, re.M)
+    assert {"win", "win128", "wpair", "asm", "bn256", "splitk", "f16", "pdl", "early_weights"} <= set(names)
+    dg.reset_options()
+    defaults = {n: dg.get_option(n) for n in names}
+    assert defaults["early_weights"] == 0 and defaults["win"] == 0 and defaults["pdl"] == 1
+    with dg.options(win=1, splitk=0):
+        assert dg.get_option("win") == 1 and dg.get_option("splitk") == 0
+    assert dg.get_option("win") == 0 and dg.get_option("splitk") == 1
+    dg.set_option("bn256_k", 1024)
+    dg.reset_options()
+    assert {n: dg.get_option(n) for n in names} == defaults
+    with pytest.raises(dg.DGError, match="INVALID"):
+        dg.set_option("no_such_option", 1)
+    assert isinstance(dg.last_kernel(), str)

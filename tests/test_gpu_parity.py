@@ -453,15 +453,9 @@ WIN_CONVS = [  # B, H, W, C, Cout, pad_code: 3x3 / stride 1 / pad 1 shapes of th
 ]
 
 
-@pytest.mark.parametrize("B,H,W,C,Cout,pad_code", WIN_CONVS)
-def test_conv_window_path_vs_oracle(monkeypatch, B, H, W, C, Cout, pad_code):
-    """Direct 3x3 conv through the shifted-window kernel (DG_WIN=1 forces it for C = 128 / 256; C =
-    64 takes it by default, "tile mode": one hand-off and 18 MMAs per tile): one unpacked window of
-    padded input pixels per tile, every tap an MMA on a row-shifted shared-memory descriptor, vs
-    O-CONV, int32 and fused requant."""
-    if not _tc_available():
-        pytest.skip("tc unavailable")
-    monkeypatch.setenv("DG_WIN", "1")
+def _win_check(B, H, W, C, Cout, pad_code, expect, exact_images=None):
+    """Window-kernel conv vs the oracle: int32 output (element by element) and fused requant with a
+    per-channel bias; asserts that the instance which ran carries every tag in `expect`."""
     lut = dg.build_lut(WL, AL, 8)
     g = np.random.default_rng(B + H + W + C + Cout + pad_code)
     x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
@@ -473,12 +467,51 @@ def test_conv_window_path_vs_oracle(monkeypatch, B, H, W, C, Cout, pad_code):
     p = dg.conv_params(B, H, W, Cp, Cout, 3, 3, 1, 1, pad_code, ldw=wp.shape[1])
     ws = torch.empty(dg.conv_workspace_size(p), dtype=torch.uint8, device=DEV)
     out = dg.lut_conv2d_prepared(xp, w8, lut, p, ws=ws)
+    tag = dg.last_kernel()
+    for e in expect:
+        assert e in tag, (e, tag)
     assert np.array_equal(host(out).reshape(exp.shape), exp)
     bias = g.integers(-50, 50, Cout).astype(np.int32)
     rq = dg.Requant(mult=30000, shift=20, zp=1, bias=torch.from_numpy(bias).to(DEV), bias_axis=0)
     outc = dg.lut_conv2d_prepared(xp, w8, lut, p, rq=rq, ws=ws)
+    assert dg.last_kernel() == tag
     expc = oracle.requantize(exp.reshape(-1, Cout), 30000, 20, 1, 0, 3, bias=bias, bias_axis=0)
     assert np.array_equal(oracle_codes_of(outc, expc.shape[0], Cout), expc)
+
+
+@pytest.mark.parametrize("win128", [0, 1])
+@pytest.mark.parametrize("B,H,W,C,Cout,pad_code", WIN_CONVS)
+def test_conv_window_path_vs_oracle(win128, B, H, W, C, Cout, pad_code):
+    """Direct 3x3 conv through the shifted-window kernel, FORCED (dg_set_option win=1) on shapes
+    below its two-wave auto threshold: one unpacked window of padded input pixels per tile, every
+    tap an MMA on a row-shifted shared-memory descriptor, vs O-CONV, int32 and fused requant.
+    C = 128 / Cout <= 128 runs the C = 128 tile mode (win128=1) or the 256-code stage form."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    if win128 and not (C == 128 and Cout <= 128):
+        pytest.skip("win128 applies to C = 128, Cout <= 128")
+    expect = [" win "] + (["kst=128"] if win128 else ["kst=256"])
+    with dg.options(win=1, win128=win128):
+        _win_check(B, H, W, C, Cout, pad_code, expect)
+
+
+DEFAULT_WIN = [  # shapes that select each default window instance with NO option forced (>= 2 waves)
+    (48, 28, 28, 128, 128, 0, ["kst=128", "nwin=2"]),           # C = 128 tile mode, 2 windows (R-50 stage 2)
+    (3, 112, 112, 128, 128, 2, ["kst=128", "nwin=1"]),          # C = 128 at 112 wide: 1 window (VGG conv2_2)
+    (3, 112, 112, 64, 128, 0, ["bn=128", "kst=256", "wpair=1"]),   # 64 -> 128 pair mode (VGG conv2_1)
+    (12, 56, 56, 64, 64, 1, ["bn=64", "kst=256", "wpair=1"]),      # 64 -> 64 pair mode (R-50 stage 1)
+    (2, 224, 224, 64, 64, 0, ["bn=64", "wpair=1"]),              # VGG width: 3 window rows per thread
+]
+
+
+@pytest.mark.parametrize("B,H,W,C,Cout,pad_code,expect", DEFAULT_WIN)
+def test_conv_window_default_instances_vs_oracle(B, H, W, C, Cout, pad_code, expect):
+    """Every window instance the auto dispatch picks for the bench's layers, at a size that picks it
+    by default (checked through dg_last_kernel), bit-exact against the oracle's direct conv."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    dg.reset_options()
+    _win_check(B, H, W, C, Cout, pad_code, [" win "] + expect)
 
 
 @pytest.mark.parametrize("C2,res_mult", [(64, 37), (128, 900), (64, 20000)])
@@ -557,6 +590,7 @@ def test_conv_splitk_vs_oracle(B, H, C, Cout, k, stride):
     out = dg.lut_conv2d_prepared(xp, w8, lut, p, ws=ws)
     if k == 3:   # implicit GEMM split over K + the reduce kernel
         assert dg.kernel_launches() - n0 == 2
+        assert "skinst" in dg.last_kernel() and "sk=1 " not in dg.last_kernel(), dg.last_kernel()
     assert np.array_equal(host(out).reshape(exp.shape), exp)
     if Cout % 4:
         return
@@ -593,15 +627,17 @@ def test_gemm_f4_vs_oracle(M, N, K):
 
 @pytest.mark.parametrize("wl", [(-2, -1, 0, 1), (-12, -3, 4, 8), (0, 6, -6, 1), (3, 3, -2, 2)])
 def test_gemm_f4_levels_and_extremes(wl):
-    """Every e2m1-representable weight level set (v/2 in e2m1), all-max-magnitude rows first (the
-    adversarial order for a truncating accumulator: large partial sums, then small terms) and the
-    largest |acc| the path admits (K * max|entry| < 2^22)."""
+    """Every e2m1-representable weight level set (v/2 in e2m1) at the LARGEST K the API admits
+    (K * max|entry| just below 2^22, api.cu) in the adversarial order for an fp32 accumulator that
+    might truncate: half the rows / columns carry the max-magnitude product on every k < K - 64
+    (|partial sum| climbing to ~2^22), then 64 random small terms that must still land exactly;
+    the other half random.  Bit-exact against the oracle."""
     if not _tc_available():
         pytest.skip("tc unavailable")
     lut = dg.build_lut(list(wl), AL, 8)
     T = oracle.build_lut16(list(wl), AL)
-    M, N = 256, 256
-    K = min(4608, (1 << 22) // max(1, int(np.abs(T).max())) - 1)
+    M, N = 48, 40
+    K = ((1 << 22) - 1) // int(np.abs(T).max())
     g = np.random.default_rng(sum(wl) + 100)
     W = g.integers(0, 4, (M, K), dtype=np.uint8)
     A = g.integers(0, 4, (K, N), dtype=np.uint8)
@@ -610,7 +646,12 @@ def test_gemm_f4_levels_and_extremes(wl):
     A[: K - 64, ::2] = 3
     w4 = dg.expand_operand_f4(gpu_pack(W, weights=True), K, list(wl))
     C = host(dg.lut_gemm_f4(w4, gpu_pack(np.ascontiguousarray(A.T)), M, N, K, lut))
-    assert np.array_equal(C, oracle.lut_gemm(W, A, T))
+    exp = oracle.lut_gemm(W, A, T)
+    assert np.abs(exp).max() >= (1 << 21) + (1 << 20)   # the admitted bound is really reached
+    assert np.array_equal(C, exp)
+    with pytest.raises(dg.DGError, match="OVERFLOW"):   # one more code and the API refuses
+        dg.lut_gemm_f4(dg.expand_operand_f4(gpu_pack(W[:8, :1].repeat(K + 1, 1), weights=True), K + 1, list(wl)),
+                       gpu_pack(np.zeros((8, K + 1), np.uint8)), 8, 8, K + 1, lut)
 
 
 def test_gemm_f4_rejects():
@@ -768,3 +809,52 @@ def test_conv_window_default_with_residual_and_bias():
     r = (np.array(AL)[x.reshape(-1, C)] * 29).astype(np.int32)
     exp = oracle.requantize(acc, 15000, 20, 0, 0, 3, res=r, bias=bias, bias_axis=0)
     assert np.array_equal(oracle_codes_of(out, exp.shape[0], C), exp)
+
+
+# ---- every TS-kernel instance of the auto dispatch (and the forced ablation forms), tag-checked ----
+INSTANCES = [  # np (pixels), nq (channels), K, options, tags the instance must carry
+    (300, 64, 64, {}, ["bn=64 epi=8 unp=8 kst=128"]),
+    (300, 64, 256, {}, ["bn=64 epi=8 unp=8 kst=256"]),
+    (300, 128, 128, {}, ["bn=128 epi=8 unp=4 kst=128"]),
+    (300, 128, 256, {}, ["bn=128 epi=8 unp=4 kst=256"]),
+    (300, 256, 64, {}, ["bn=256 epi=8 unp=4 kst=128 asm"]),
+    (260, 512, 256, {}, ["bn=256 epi=8 unp=4 kst=128 asm"]),
+    (300, 256, 3200, {}, ["bn=256 epi=4 unp=8 kst=128", "sk=1"]),
+    (300, 128, 1152, {}, ["bn=128 epi=4 unp=8 kst=256"]),
+    (300, 64, 1152, {}, ["bn=64 epi=4 unp=8 kst=256"]),
+    (300, 96, 1152, {"kst": 128}, ["bn=128 epi=4 unp=8 kst=128"]),
+    (300, 64, 1000, {"kst": 128}, ["bn=64 epi=4 unp=8 kst=128"]),
+    (300, 100, 256, {"bn64_short": 1}, ["bn=64 epi=8 unp=8 kst=256"]),
+    (300, 256, 3200, {"bn256": 0}, ["bn=128 epi=4 unp=8 kst=256"]),
+    (300, 256, 64, {"asm": 0}, ["bn=128 epi=8 unp=4 kst=128"]),
+    (300, 128, 1152, {"f16": 0}, ["f16=0"]),
+    (300, 128, 1152, {"bres": 0}, ["bres=0"]),
+    (300, 128, 576, {"pdl": 0, "early_weights": 1}, ["early=1"]),
+]
+
+
+@pytest.mark.parametrize("np_,nq,K,opts,tags", INSTANCES)
+def test_dispatch_instances_vs_oracle(np_, nq, K, opts, tags):
+    """Each TS-kernel instance (template / runtime mode named by dg_last_kernel), int32 and fused
+    requant (per-column bias) in the conv orientation, bit-exact against the oracle; ragged rows."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    g = np.random.default_rng(np_ + 7 * nq + K)
+    A = g.integers(0, 4, (np_, K), dtype=np.uint8)      # activations (pixels), K-major
+    Wt = g.integers(0, 4, (nq, K), dtype=np.uint8)      # weights [channel][K]
+    acc = oracle.lut_gemm(Wt, np.ascontiguousarray(A.T), oracle.build_lut16(WL, AL)).T
+    a_p, w8 = gpu_pack(A), dg.expand_operand(gpu_pack(Wt, weights=True), K, WL)
+    lut_t = dg.build_lut(AL, WL, 8)
+    bias = (-int(np.round(acc.mean())) + g.integers(-30, 30, nq)).astype(np.int32)
+    rq = dg.Requant(20000 if K < 1024 else 9000, 20, 1, 0, 3, bias=torch.from_numpy(bias).to(DEV), bias_axis=0)
+    dg.reset_options()
+    with dg.options(**opts):
+        C = dg.lut_gemm_prepared(a_p, w8, np_, nq, K, lut_t)
+        tag = dg.last_kernel()
+        codes = dg.lut_gemm_prepared(a_p, w8, np_, nq, K, lut_t, rq=rq)
+        assert dg.last_kernel() == tag
+    for t in tags:
+        assert t in tag, (t, tag)
+    assert np.array_equal(host(C), acc)
+    exp = oracle.requantize(np.ascontiguousarray(acc), rq.mult, 20, 1, 0, 3, bias=bias, bias_axis=0)
+    assert np.array_equal(oracle_codes_of(codes, np_, nq), exp)
