@@ -84,7 +84,7 @@ class ClockSampler:
                         self.reasons.add(name)
             except Exception:
                 pass
-            time.sleep(0.02)
+            time.sleep(0.005)
 
     def __enter__(self):
         if self.nv:
@@ -120,6 +120,30 @@ def barrier(ws):
         dist.barrier()
 
 
+def cpu_info():
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except AttributeError:  # pragma: no cover
+        cores = os.cpu_count() or 1
+    return model, cores
+
+
+def i8_mma_ceiling(sm_mhz):
+    """The kind::i8 instruction's own rate: one 128x128x32 MMA per 64 SM cycles (tools/mma_bench.cu,
+    profiles/r01_mma_issue_bench.txt: 4418 TOPS measured chip-wide) = 16384 ops/clk/SM, at the SM
+    clock observed during the timed region."""
+    return 16384 * 148 * (sm_mhz or 1965.0) * 1e6 / 1e12
+
+
 # ---------------------------------------------------------------- oracle (CPU) legs
 def oracle_conv_sample(cfg, runner_layers, image, budget_s=25.0, check=None):
     """Run the plain CPU oracle on one image through the given layers (cpu_baseline leg;
@@ -128,15 +152,16 @@ def oracle_conv_sample(cfg, runner_layers, image, budget_s=25.0, check=None):
     Returns (ops, seconds, layers_done, mismatches)."""
     import oracle
     import synth
-    from paper_2304_09049_b200 import netrun
     T = oracle.build_lut16(synth.WL_UNIFORM, synth.AL_UNIFORM)
     ops = 0
     secs = 0.0
     done = 0
     bad = 0
     for li, L in runner_layers:
-        x = netrun.input_codes(cfg, li, L, [image], "cpu").numpy()
-        w = netrun.weight_codes(cfg, li, L, "cpu").numpy()
+        per = L.h * L.h * L.cin
+        x = synth.counter_codes_host(image * per, per, (cfg, li, synth.T_X), "relu").reshape(1, L.h, L.h, L.cin)
+        w = synth.counter_codes_host(0, L.cout * L.k * L.k * L.cin, (cfg, li, synth.T_W),
+                                     "uniform").reshape(L.cout, L.k, L.k, L.cin)
         t0 = time.perf_counter()
         acc = oracle.conv2d_direct(x, w, T, L.stride, L.pad, 0)
         r = synth.conv_requant(L)
@@ -152,6 +177,29 @@ def oracle_conv_sample(cfg, runner_layers, image, budget_s=25.0, check=None):
         if secs > budget_s:
             break
     return ops, secs, done, bad
+
+
+def oracle_all_cores(cfg, runner_layers, images, check):
+    """The same oracle (unchanged, single-threaded C) run on every host core at once: one image per
+    thread (ctypes releases the GIL), all layers; also compares each image with the GPU codes in
+    `check` (layer index -> host codes of the whole local batch, rows image-major).
+    Returns (ops, wall seconds, threads, mismatched codes)."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    def one(slot_image):
+        slot, image = slot_image
+        sub = {}
+        for li, L in runner_layers:
+            rows = L.ho * L.ho
+            sub[li] = check[li][slot * rows:(slot + 1) * rows]
+        o, _, _, bad = oracle_conv_sample(cfg, runner_layers, image, budget_s=1e9, check=sub)
+        return o, bad
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(max_workers=len(images)) as ex:
+        res = list(ex.map(one, images))
+    wall = time.perf_counter() - t0
+    return sum(r[0] for r in res), wall, len(images), sum(r[1] for r in res)
 
 
 # ---------------------------------------------------------------- conv workloads
@@ -204,10 +252,13 @@ def run_conv(args, ws, rank, local):
         torch.cuda.synchronize()
     barrier(ws)
     ms = e0.elapsed_time(e1) / args.steps
+    # the outputs the TIMED graph replays wrote, kept before anything else rewrites them (parity leg)
+    snap = [p.out.clone() for p in runner.plans]
     # per-layer GEMM times: one instrumented replay after the timed region (layers run unoverlapped)
     graph_ev.replay()
     torch.cuda.synchronize()
     gemm_ms = [a.elapsed_time(b) for a, b in gev]
+    replay_equal = all(torch.equal(a, p.out) for a, p in zip(snap, runner.plans))
     ms_max = max_over_ranks(ms, ws)
     ops_step = runner.total_ops
     value = ops_step * ws / (ms_max * 1e-3) / 1e12
@@ -240,6 +291,7 @@ def run_conv(args, ws, rank, local):
             "achieved_src": "sum of the step's GEMM ops / step time over the timed region (CUDA events on the launching stream; the step is only lut_gemm_ts_kernel launches)",
             "instrumented_gemm_ms_sum": round(gemm_total_ms, 4),
             "frac_vs_layer_roofline": round(frac_layer, 4),
+            "i8_mma_ceiling": None, "frac_vs_i8_mma_ceiling": None,
             "layer_roofline_ms": round(t_roof * 1e3, 4),
             "traffic": tr, "alg_bytes_per_launch": round(alg_bytes),
             "traffic_src": "profiles/traffic.json (ncu dram__bytes_read+write, mean per GEMM launch)"}
@@ -297,25 +349,45 @@ def run_conv(args, ws, rank, local):
                "d2h_bytes_per_step": runner.output_bytes(),
                "api": "dg_lut_conv2d (pinned host buffers; per-layer H2D / conv / D2H on three streams)"}
 
-    # ---- parity on a sampled image + the CPU oracle baseline (rank 0, N=1 only)
+    # ---- parity of the TIMED outputs (snapshot) on sampled images + the CPU oracle baseline
     cpu = None
     parity = None
     if rank == 0 and not args.no_oracle:
         all_layers = synth.CONFIG_LAYERS[cfg]()
-        check = {}
-        for p, li in zip(runner.plans, runner.layer_ids):
-            L = p.layer
-            rows = L.ho * L.ho
-            check[li] = p.out[:rows].cpu().numpy()     # image images[0] = rows [0, Ho*Wo)
+        check = {li: t.cpu().numpy() for t, li in zip(snap, runner.layer_ids)}
+        del snap
         sel = [(li, all_layers[li]) for li in runner.layer_ids]
-        o_ops, o_s, done, bad = oracle_conv_sample(cfg, sel, images[0], budget_s=args.oracle_budget, check=check)
-        parity = {"image": images[0], "layers_checked": done, "mismatched_codes": bad,
-                  "status": "bit-exact" if bad == 0 else "MISMATCH"}
+        model, ncores = cpu_info()
+        # (1) the oracle as it stands, one thread, first local image, every layer
+        o_ops, o_s, done, bad1 = oracle_conv_sample(cfg, sel, images[0], budget_s=args.oracle_budget,
+                                                    check={li: c[:all_layers[li].ho ** 2] for li, c in check.items()})
+        # (2) the same oracle on every host core: one image per core, spread over the local batch
+        nimg = max(2, min(ncores, len(images), args.oracle_images))
+        slots = sorted(set(int(round(i * (len(images) - 1) / (nimg - 1))) for i in range(nimg)))
+        a_ops, a_s, a_thr, bad2 = oracle_all_cores(cfg, sel, [(s_, images[s_]) for s_ in slots], check)
+        parity = {"of": "outputs of the timed graph replays (snapshot before any other replay)",
+                  "images": [images[s_] for s_ in slots], "layers_checked": len(sel),
+                  "mismatched_codes": bad1 + bad2, "instrumented_replay_equal": replay_equal,
+                  "status": "bit-exact" if bad1 + bad2 == 0 and replay_equal else "MISMATCH"}
         if ws == 1:
             cpu = {"value": o_ops / o_s / 1e12, "unit": "TOPS", "cores": 1, "kind": "oracle",
+                   "cpu_model": model, "host_cores": ncores,
                    "sample": f"oracle/oracle.c conv2d_direct+requantize, image {images[0]}, first {done} of {nl} "
-                             f"layers ({o_ops / 1e9:.2f} GOP in {o_s:.1f} s), single thread"}
+                             f"layers ({o_ops / 1e9:.2f} GOP in {o_s:.1f} s), single thread",
+                   "all_cores": {"value": a_ops / a_s / 1e12, "unit": "TOPS", "cores": a_thr,
+                                 "sample": f"the same oracle on {a_thr} threads, one image each (images "
+                                           f"{[images[s_] for s_ in slots][:4]}...), all {nl} layers: "
+                                           f"{a_ops / 1e9:.1f} GOP in {a_s:.1f} s wall"}}
 
+    clocks = clk.summary()
+    ceil = i8_mma_ceiling(clocks["sm_mhz"])
+    roof["i8_mma_ceiling"] = round(ceil, 1)
+    roof["frac_vs_i8_mma_ceiling"] = round(achieved / ceil, 4)
+    roof["i8_mma_ceiling_src"] = ("tools/mma_bench.cu: 64 SM cycles per 128x128x32 kind::i8 MMA (16384 ops/clk/SM) "
+                                  "x 148 SMs x the median SM clock of the timed region")
+    gemm_big = None
+    if args.gemm_n > 0:   # config 5 (BJ configs[4]) in the same process: the headline GEMM
+        gemm_big = gemm_line(args, ws, rank, local, args.gemm_n, levels="learned", variant="auto")
     if rank == 0:
         line = {"metric": METRIC, "value": round(value, 2), "unit": "TOPS", "n_gpus": ws,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_max, 4),
@@ -328,8 +400,11 @@ def run_conv(args, ws, rank, local):
                                  "independent packed inputs per step per GPU (126 MB L2)",
                            "parallelism": f"dp{ws} (batch shards, no collective in the step)"},
                 "roofline": roof, "cpu_baseline": cpu, "e2e": e2e,
-                "gpu_launches": launches_per_step * args.steps, "clocks": clk.summary(),
-                "parity": parity, "gemm_ms_per_layer": [round(x, 4) for x in gemm_ms]}
+                "gpu_launches": launches_per_step * args.steps, "clocks": clocks,
+                "parity": parity, "gemm_ms_per_layer": [round(x, 4) for x in gemm_ms],
+                "kernel_per_layer": [p.kernel for p in runner.plans]}
+        if gemm_big is not None:
+            line[f"gemm{args.gemm_n}"] = gemm_big
         print(json.dumps(line), flush=True)
 
 
@@ -378,23 +453,25 @@ def run_resnet18(args, ws, rank, local):
 
 
 # ---------------------------------------------------------------- config 5: square LUT-GEMM
-def run_gemm(args, ws, rank, local):
+def gemm_line(args, ws, rank, local, n, levels="learned", variant="auto"):
     """BJ configs[4]: C[n][n] = sum_k T[(W<<2)|A] with learned-style int16 levels (Q17), int32 out.
     Output channels (rows of W / C) are split across ranks; the int32 row blocks are all-gathered
-    over NCCL so every rank holds C.  Reports compute-only and end-to-end TOPS."""
+    over NCCL so every rank holds C; --fused-gather stores every tile into all
+    ranks' C from the GEMM epilogue instead (P2P, symmetric memory).  Returns rank 0's JSON dict
+    (None elsewhere): compute-only and end-to-end TOPS, roofline, clocks, exact parity of the
+    WHOLE gathered C (Freivalds) + sampled rows from every rank's block."""
     import synth
     from paper_2304_09049_b200 import dg, shard
-    n = args.n
     r0, r1 = shard.row_shard(rank, ws, n)
     m_loc = r1 - r0
-    f4 = args.variant == "f4"
-    onehot = args.variant == "onehot"
+    f4 = variant == "f4"
+    onehot = variant == "onehot"
     T_any = None
     if onehot:   # an arbitrary (non-product) int8 table, seeded: the one-hot K' = 4K tensor-core path
         T_any = np.random.default_rng(synth.MASTER_SEED + 5).integers(-127, 128, 16).astype(np.int32)
         lut = dg.lut_from_table(T_any, 8)
         wl = al = None
-    elif args.levels == "uniform" or f4:   # config-1 levels (the FP4 path needs e2m1-representable levels)
+    elif levels == "uniform" or f4:   # config-1 levels (the FP4 path needs e2m1-representable levels)
         wl, al = list(synth.WL_UNIFORM), list(synth.AL_UNIFORM)
         lut = dg.build_lut(wl, al, 8)
     else:
@@ -408,10 +485,10 @@ def run_gemm(args, ws, rank, local):
     del w_codes
     at = torch.empty((n, ld), dtype=torch.uint8, device=dev)
     chunk = max(1, (1 << 26) // n)
-    for r0 in range(0, n, chunk):
-        r1 = min(n, r0 + chunk)
-        c = synth.counter_codes(r0 * n, (r1 - r0) * n, (5, n, synth.T_A), "uniform", dev).view(r1 - r0, n)
-        dg.pack_codes(c, out=at[r0:r1])
+    for q0 in range(0, n, chunk):
+        q1 = min(n, q0 + chunk)
+        c = synth.counter_codes(q0 * n, (q1 - q0) * n, (5, n, synth.T_A), "uniform", dev).view(q1 - q0, n)
+        dg.pack_codes(c, out=at[q0:q1])
     if f4:   # block-scaled FP4 path: the weights are expanded once to e2m1, activations stay packed
         w4 = dg.expand_operand_f4(w, n, wl)
         at8 = None
@@ -421,10 +498,8 @@ def run_gemm(args, ws, rank, local):
         at8 = None
     else:
         at8 = dg.expand_operand(at, n, al)          # offline expansion of the second operand
-    # N > 1: fused GEMM + all-gather (the epilogue stores each tile into every rank's C over
-    # NVLink P2P, symmetric memory) when available, else GEMM then NCCL all_gather_into_tensor
     peer = None
-    if ws > 1 and not args.nccl_gather and not f4 and not onehot:
+    if ws > 1 and args.fused_gather and not f4 and not onehot:
         try:
             peer = shard.PeerRows((n, n), torch.int32, dev, rank, ws, rank * m_loc)
         except Exception as e:  # (no P2P / symmetric memory on this node)
@@ -453,26 +528,24 @@ def run_gemm(args, ws, rank, local):
         elif ws > 1:
             shard.gather_rows(c_loc, ws, out=c_full)
 
-    def step(gather_too=True):
+    for _ in range(max(3, args.warmup)):
         gemm()
-        if gather_too:
-            gather()
-
-    for _ in range(args.warmup):
-        step()
+        gather()
     torch.cuda.synchronize()
+    kernel = dg.last_kernel()
     # L2 is flushed between steps by the 1 GiB int32 output of n=16384 itself; for smaller n a
     # 256 MB scratch write is issued between steps (outside the events).
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev) if n < 16384 else None
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    g1 = torch.cuda.Event(enable_timing=True)
     t_comp = 0.0
     t_all = 0.0
+    steps = max(3, args.gemm_steps if args.workload != "gemm" else args.steps)
     barrier(ws)
     torch.cuda.synchronize()
     n0 = dg.kernel_launches()
     with ClockSampler(local) as clk:
-        for _ in range(args.steps):
+        for _ in range(steps):
             if flush is not None:
                 flush.zero_()
             barrier(ws)
@@ -486,55 +559,68 @@ def run_gemm(args, ws, rank, local):
             t_all += e0.elapsed_time(g1)
     launches = dg.kernel_launches() - n0
     barrier(ws)
-    ms_comp = max_over_ranks(t_comp / args.steps, ws)
-    ms_all = max_over_ranks(t_all / args.steps, ws)
+    ms_comp = max_over_ranks(t_comp / steps, ws)
+    ms_all = max_over_ranks(t_all / steps, ws)
     pk = peaks()
     value = ops_total / (ms_all * 1e-3) / 1e12
     comp_tops = ops_total / (ms_comp * 1e-3) / 1e12
-    per_gpu = (2 * m_loc * n * n) / (t_comp / args.steps * 1e-3) / 1e12
-    # parity: exact Freivalds check of this rank's rows (4 trials) + 2 sampled rows vs the oracle
+    per_gpu = (2 * m_loc * n * n) / (t_comp / steps * 1e-3) / 1e12
+    # parity (rank 0): exact Freivalds over the WHOLE gathered C (every rank's rows) + the first and
+    # last row of every rank's block against the oracle
     parity = None
     if not args.no_oracle and rank == 0:
         import oracle
-        C = c_loc.cpu().numpy()
-        Wc = synth.counter_codes(rank * m_loc * n, m_loc * n, (5, n, synth.T_W), "uniform", "cpu").view(m_loc, n).numpy()
-        Atc = synth.counter_codes(0, n * n, (5, n, synth.T_A), "uniform", "cpu").view(n, n).numpy()
+        C = c_full.cpu().numpy()
+        Wc = synth.counter_codes_host(0, n * n, (5, n, synth.T_W), "uniform").reshape(n, n)
+        Atc = synth.counter_codes_host(0, n * n, (5, n, synth.T_A), "uniform").reshape(n, n)
         T = T_any if onehot else oracle.build_lut16(wl, al)
-        bad = oracle.freivalds_rows(Wc, Atc, C, T, trials=2)
-        rows = [0, m_loc - 1]
+        t0 = time.perf_counter()
+        bad = oracle.freivalds_rows(Wc, Atc, C, T, trials=1)
+        rows = sorted(set([r_ * m_loc for r_ in range(ws)] + [r_ * m_loc + m_loc - 1 for r_ in range(ws)]))
         ref = oracle.lut_gemm(Wc[rows], np.ascontiguousarray(Atc.T), T)
-        parity = {"freivalds_bad_rows": bad, "sampled_rows_equal": bool(np.array_equal(ref, C[rows])),
-                  "status": "bit-exact" if bad == 0 and np.array_equal(ref, C[rows]) else "MISMATCH"}
-    if rank == 0:
-        alg_bytes = m_loc * ld + n * ld + 4 * m_loc * n
-        scale = 2.0 if f4 else (0.25 if onehot else 1.0)   # onehot: 4K MMA terms per K lookups
-        peak = pk["i8_burst"] * scale
-        peak_s = pk["i8_sustained"] * scale
-        line = {"metric": METRIC, "value": round(value, 2), "unit": "TOPS", "n_gpus": ws, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": round(ms_all, 4), "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": "e2m1" if f4 else "int8",
-                "data": ("synthetic (seeded counter-based 2-bit codes; seeded random non-product int8 table)" if onehot else
-                         "synthetic (seeded counter-based 2-bit codes; config-1 levels wl={-2..1}, al={0..3})"
-                         if wl == list(synth.WL_UNIFORM) else
-                         "synthetic (seeded counter-based 2-bit codes; learned-style int16 levels, Q17)"),
-                "config": {"workload": (f"square_gemm_n{n}, config-1 levels, FP4 path (SURVEY 8(f) rank 2)" if f4 else
-                                        f"square_gemm_n{n}, non-product int8 table, one-hot K'=4K tensor-core path (SURVEY 8(f) rank 3)" if onehot else
-                                        f"square_gemm_n{n} (BASELINE configs[4])" + ("" if wl != list(synth.WL_UNIFORM) else ", config-1 levels")),
-                           "n": n,
-                           "split": (f"output channels / {ws}; " + ("fused all-gather: epilogue stores every tile into all ranks' C (NVLink P2P, symmetric memory)" if peer is not None else "NCCL all_gather of int32 rows")) if ws > 1 else "none",
-                           "l2": "1 GiB int32 output per step (> L2)" if flush is None else "256 MB L2 flush between steps"},
-                "compute_only": {"value": round(comp_tops, 2), "ms": round(ms_comp, 4), "per_gpu_tops": round(per_gpu, 2)},
-                "roofline": {"bound": "tensor",
-                             "kernel": ("lut_gemm_f4_kernel (tcgen05 kind::mxf4, e2m1, SS)" if f4 else
-                                        "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)"),
-                             "achieved": round(per_gpu, 1), "peak": round(peak, 1), "unit": "TOPS",
-                             "frac": round(per_gpu / peak, 4),
-                             "frac_vs_sustained_peak": round(per_gpu / peak_s, 4),
-                             "peak_src": pk["src"] + (": e2m1 dense = 4 x bf16 burst (nominal 9/2.25)" if f4 else
-                                                      ": int8 = 2 x bf16 burst / 4 (the one-hot form runs 4K int8 MACs per K lookups)" if onehot else
-                                                      ": int8 = 2 x bf16 burst (kernel timed alone)"),
-                             "alg_bytes_per_launch": alg_bytes, "traffic": None},
-                "gpu_launches": launches, "clocks": clk.summary(), "parity": parity}
+        parity = {"of": f"the whole gathered C ({ws} rank block(s))", "freivalds_bad_rows": bad,
+                  "sampled_rows": rows[:16], "sampled_rows_equal": bool(np.array_equal(ref, C[rows])),
+                  "status": "bit-exact" if bad == 0 and np.array_equal(ref, C[rows]) else "MISMATCH",
+                  "oracle_s": round(time.perf_counter() - t0, 1)}
+    if rank != 0:
+        return None
+    clocks = clk.summary()
+    alg_bytes = m_loc * ld + n * ld + 4 * m_loc * n
+    scale = 2.0 if f4 else (0.25 if onehot else 1.0)   # onehot: 4K MMA terms per K lookups
+    peak = pk["i8_burst"] * scale
+    peak_s = pk["i8_sustained"] * scale
+    ceil = i8_mma_ceiling(clocks["sm_mhz"]) * scale
+    uni = wl is not None and list(wl) == list(synth.WL_UNIFORM)
+    return {"metric": METRIC, "value": round(value, 2), "unit": "TOPS", "n_gpus": ws, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": round(ms_all, 4), "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "e2m1" if f4 else "int8",
+            "data": ("synthetic (seeded counter-based 2-bit codes; seeded random non-product int8 table)" if onehot else
+                     "synthetic (seeded counter-based 2-bit codes; config-1 levels wl={-2..1}, al={0..3})" if uni else
+                     "synthetic (seeded counter-based 2-bit codes; learned-style int16 levels, Q17)"),
+            "config": {"workload": (f"square_gemm_n{n}, config-1 levels, FP4 path (SURVEY 8(f) rank 2)" if f4 else
+                                    f"square_gemm_n{n}, non-product int8 table, one-hot K'=4K tensor-core path (SURVEY 8(f) rank 3)" if onehot else
+                                    f"square_gemm_n{n} (BASELINE configs[4])" + (", config-1 levels" if uni else "")),
+                       "n": n, "kernel": kernel,
+                       "split": (f"output channels / {ws}; " + ("fused all-gather: epilogue stores every tile into all ranks' C (NVLink P2P, symmetric memory)" if peer is not None else "NCCL all_gather_into_tensor of int32 rows")) if ws > 1 else "none",
+                       "l2": "1 GiB int32 output per step (> L2)" if flush is None else "256 MB L2 flush between steps"},
+            "compute_only": {"value": round(comp_tops, 2), "ms": round(ms_comp, 4), "per_gpu_tops": round(per_gpu, 2)},
+            "roofline": {"bound": "tensor",
+                         "kernel": ("lut_gemm_f4_kernel (tcgen05 kind::mxf4, e2m1, SS)" if f4 else
+                                    "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)"),
+                         "achieved": round(per_gpu, 1), "peak": round(peak, 1), "unit": "TOPS",
+                         "frac": round(per_gpu / peak, 4),
+                         "frac_vs_sustained_peak": round(per_gpu / peak_s, 4),
+                         "i8_mma_ceiling": round(ceil, 1), "frac_vs_i8_mma_ceiling": round(per_gpu / ceil, 4),
+                         "peak_src": pk["src"] + (": e2m1 dense = 4 x bf16 burst (nominal 9/2.25)" if f4 else
+                                                  ": int8 = 2 x bf16 burst / 4 (the one-hot form runs 4K int8 MACs per K lookups)" if onehot else
+                                                  ": int8 = 2 x bf16 burst (kernel timed alone)"),
+                         "alg_bytes_per_launch": alg_bytes, "traffic": None},
+            "gpu_launches": launches, "clocks": clocks, "parity": parity}
+
+
+def run_gemm(args, ws, rank, local):
+    line = gemm_line(args, ws, rank, local, args.n, levels=args.levels, variant=args.variant)
+    if line is not None:
         print(json.dumps(line), flush=True)
 
 
@@ -587,7 +673,12 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--oracle-budget", type=float, default=20.0)
     ap.add_argument("--no-oracle", action="store_true")
-    ap.add_argument("--nccl-gather", action="store_true", help="config 5 at N > 1: GEMM then NCCL all_gather (baseline)")
+    ap.add_argument("--fused-gather", action="store_true",
+                    help="config 5 at N > 1: all-gather fused into the GEMM epilogue over P2P (default: NCCL all_gather)")
+    ap.add_argument("--gemm-n", type=int, default=16384,
+                    help="conv workloads: also time config 5 at this n in the same run (0 = skip)")
+    ap.add_argument("--gemm-steps", type=int, default=10)
+    ap.add_argument("--oracle-images", type=int, default=64, help="images checked by the all-core oracle leg")
     args = ap.parse_args()
     ws, rank, local = dist_env()
     if args.impl == "reference":
