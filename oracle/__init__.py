@@ -17,6 +17,8 @@ Parity status per function (DESIGN.md §4 lists the pins):
   requantize         pinned (exact Fraction arithmetic over all ties)
   quantize           pinned (Eq. 1 worked examples S:57-59)
   freivalds_rows     pinned (accepts the true C, rejects single-element faults)
+  lut_gemm_f64       pinned (fp64 BLAS closed form for float product tables, integer-valued
+                     tables equal lut_gemm exactly, brute force via pair counts, linearity)
   conv_freivalds     pinned (accepts or_conv2d_direct's output incl. padding / stride / pad
                      codes, rejects every single-element fault and swapped channels / pixels,
                      equals freivalds_rows on 1x1 convs)
@@ -64,6 +66,7 @@ def _load():
         lib.or_quantize.argtypes = [P, i64, ctypes.c_float, ctypes.c_float, i32, i32, P]
         lib.or_freivalds_rows.argtypes = [P, P, P, i64, i64, i64, i64, P, P, P]
         lib.or_freivalds_rows.restype = i64
+        lib.or_lut_gemm_f64.argtypes = [P, P, i64, i64, i64, P, P]
         lib.or_conv_freivalds.argtypes = [P, P] + [i32] * 9 + [ctypes.c_uint8, P, P, i64, P, P]
         lib.or_conv_freivalds.restype = i64
         _lib = lib
@@ -248,3 +251,17 @@ def conv_freivalds(x: np.ndarray, w: np.ndarray, T, stride: int, pad: int, pad_c
                                      out.ctypes.data_as(ctypes.c_void_p), out.shape[1],
                                      r.ctypes.data_as(ctypes.c_void_p), Hs.ctypes.data_as(ctypes.c_void_p))
     return int(bad)
+
+
+def lut_gemm_f64(W: np.ndarray, A: np.ndarray, T) -> np.ndarray:
+    """C[m][n] = sum_k T[(W[m][k]<<2)|A[k][n]] for a float-valued table, summed in fp64."""
+    lib = _load()
+    W, Wp = _c(W, np.uint8)
+    A, Ap = _c(A, np.uint8)
+    T, Tp = _c(T, np.float64)
+    M, K = W.shape
+    K2, N = A.shape
+    assert K == K2 and T.size == 16
+    C = np.empty((M, N), np.float64)
+    lib.or_lut_gemm_f64(Wp, Ap, M, N, K, Tp, C.ctypes.data_as(ctypes.c_void_p))
+    return C

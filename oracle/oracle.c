@@ -318,3 +318,24 @@ int64_t or_conv_freivalds(const uint8_t *x, const uint8_t *w, int32_t B, int32_t
     }
     return bad;
 }
+
+/* ------------------------------------------------------------------------ */
+/* LUT GEMM over a FLOAT-valued table (§5.3: "The LUT can store either integer or
+ * floating-point values", e.g. the products of a non-uniform quantiser's levels):
+ *     C[m][n] = sum_{k<K} T[(W[m][k] << 2) | A[k][n]]        (T double, summed in double)
+ * Same loops and index as or_lut_gemm (Alg. 1); the sum is carried in fp64 in k
+ * order, so it is the exact value up to K * 2^-53 * sum|T| (reading Q24). */
+void or_lut_gemm_f64(const uint8_t *W, const uint8_t *A, int64_t M, int64_t N, int64_t K,
+                     const double T[16], double *C)
+{
+    for (int64_t m = 0; m < M; ++m)
+        for (int64_t n = 0; n < N; ++n) {
+            double acc = 0.0;
+            for (int64_t k = 0; k < K; ++k) {
+                int w = W[m * K + k] & 3;
+                int a = A[k * N + n] & 3;
+                acc += T[(w << 2) | a];
+            }
+            C[m * N + n] = acc;
+        }
+}

@@ -472,3 +472,38 @@ def test_conv_freivalds_1x1_agrees_with_gemm_freivalds():
     out[3, 4] += 7
     assert oracle.conv_freivalds(x, w, T, 1, 0, 0, out) == 1
     assert oracle.freivalds_rows(Wm, Xt, np.ascontiguousarray(out.T), T) >= 1
+
+
+# ---------------------------------------------------------------- float-valued tables
+def test_gemm_f64_float_product_table_closed_form():
+    """A float PRODUCT table T = wl (x) al (non-uniform quantiser levels) makes the LUT
+    sum the dense product of the level matrices: equal to fp64 BLAS within its rounding."""
+    g = np.random.default_rng(31)
+    for M, N, K in [(7, 5, 33), (16, 40, 300), (3, 64, 1000)]:
+        wl, al = g.normal(size=4), np.abs(g.normal(size=4))
+        T = np.outer(wl, al).reshape(-1)          # index (i << 2) | j
+        W = g.integers(0, 4, (M, K), dtype=np.uint8)
+        A = g.integers(0, 4, (K, N), dtype=np.uint8)
+        C = oracle.lut_gemm_f64(W, A, T)
+        ref = wl[W] @ al[A]
+        assert np.allclose(C, ref, rtol=0, atol=K * 4e-15 * np.abs(T).max())
+        # the transposed index (a << 2 | w) would give a different result for asymmetric levels
+        Tt = np.outer(wl, al).T.reshape(-1)
+        assert not np.allclose(oracle.lut_gemm_f64(W, A, Tt), ref)
+
+
+def test_gemm_f64_integer_table_equals_integer_oracle_and_pair_counts():
+    """Integer-valued float tables reproduce the pinned integer oracle exactly; any table equals the
+    pair-count form sum_{i,j} T[(i<<2)|j] * #{k : W=i, A=j} (brute force over the counts)."""
+    g = np.random.default_rng(32)
+    M, N, K = 9, 11, 257
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    Ti = g.integers(-1000, 1000, 16).astype(np.int32)
+    assert np.array_equal(oracle.lut_gemm_f64(W, A, Ti.astype(np.float64)), oracle.lut_gemm(W, A, Ti).astype(np.float64))
+    Tf = g.normal(size=16) * 10.0 ** g.integers(-3, 4, 16)
+    cnt = np.zeros((M, N, 16))
+    for i in range(4):
+        for j in range(4):
+            cnt[:, :, (i << 2) | j] = (W == i).astype(np.float64) @ (A == j).astype(np.float64)
+    assert np.allclose(oracle.lut_gemm_f64(W, A, Tf), cnt @ Tf, rtol=1e-12, atol=1e-9)
