@@ -681,6 +681,11 @@ def main():
     ap.add_argument("--oracle-images", type=int, default=64, help="images checked by the all-core oracle leg")
     args = ap.parse_args()
     ws, rank, local = dist_env()
+    if os.environ.get("DG_OPTS"):   # ablation hook: "name=value,name=value" (dg_set_option)
+        from paper_2304_09049_b200 import dg
+        for kv in os.environ["DG_OPTS"].split(","):
+            k, v = kv.split("=")
+            dg.set_option(k, int(v))
     if args.impl == "reference":
         return run_reference(args, ws, rank)
     torch.cuda.set_device(local)

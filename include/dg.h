@@ -63,7 +63,7 @@ typedef int32_t dg_status;
 DG_API const char *dg_status_string(dg_status s);
 
 /* ABI version of this header (bumped on any signature change). */
-#define DG_ABI_VERSION 3
+#define DG_ABI_VERSION 4
 DG_API int32_t dg_abi_version(void);
 
 /* Number of CUDA kernels this library has enqueued since it was loaded (all
@@ -97,6 +97,11 @@ DG_API uint64_t dg_kernel_launches(void);
  *               Only correct when neither was written by a kernel still in flight
  *               on the stream (e.g. weights prepared at setup and synchronised).   (0)
  *   "f4conv"    route qualifying product-table layers to the block-scaled FP4 kernel (1)
+ *   "em"        epilogue arrangement of the short-K wide kernel: 0 groups own alternate tiles,
+ *               1 groups split each tile's columns, 2 epilogue warps first in scheduling
+ *               priority, 3 both                                            (0)
+ *   "tma_store" int32 output tiles through the TMA tensor store (staging in shared memory)
+ *               instead of per-lane row stores, where the instance has room (1)
  */
 DG_API dg_status dg_set_option(const char *name, int64_t value);
 DG_API dg_status dg_get_option(const char *name, int64_t *value);
@@ -206,13 +211,16 @@ DG_API dg_status dg_requantize(const int32_t *d_acc, int64_t rows, int64_t cols,
  *         rq != NULL -> requantised codes (S7 fused), packed 4 columns (n) per
  *                       byte: d_c is uint8 [M][ldc bytes].
  * variant: 0 auto, 1 cc (CUDA-core PRMT lookups, any table),
- *          2 tc (tcgen05 kind::i8, A operand unpacked into tensor memory; needs
- *            lut->is_product with int8 levels, else DG_ERR_UNSUPPORTED; uses
- *            d_ws for the int8 expansion of At: dg_lut_gemm_workspace_size bytes),
+ *          2 tc (tcgen05 kind::i8, A operand unpacked into tensor memory): product tables with
+ *            int8 levels use d_ws for the int8 expansion of At; NON-product tables with every
+ *            |entry| <= 127 run the one-hot K' = 4K form (see dg_lut_gemm_onehot) with both
+ *            expanded operands in d_ws; others DG_ERR_UNSUPPORTED;
+ *            dg_lut_gemm_workspace_size(M, N, K) bytes cover either form,
  *          3 tc_ss (earlier tcgen05 variant: both operands unpacked to shared memory).
+ * auto = tc where it applies, else cc (non-product tables with |entry| > 127).
  * DG_ERR_OVERFLOW if K * max|entry| >= 2^31.  With rq, |acc + bias| < 2^30 is
  * required for the fused fast path's int32 threshold compare (else exact int64). */
-DG_API size_t dg_lut_gemm_workspace_size(int64_t N, int64_t K);
+DG_API size_t dg_lut_gemm_workspace_size(int64_t M, int64_t N, int64_t K);
 DG_API dg_status dg_lut_gemm(const uint8_t *d_w, int64_t ldw, const uint8_t *d_at, int64_t lda, int64_t M,
                       int64_t N, int64_t K, const dg_lut *lut, void *d_c, int64_t ldc,
                       const dg_requant *rq, void *d_ws, size_t ws_bytes, int32_t variant, void *stream);

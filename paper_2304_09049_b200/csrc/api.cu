@@ -25,7 +25,8 @@ const OptDesc kOpts[dg::OPT_COUNT] = {
     {"asm", "DG_NO_ASM", 1, 0},         {"bn256", "DG_TS_NO_BN256", 1, 0}, {"bn256_k", "DG_BN256_K", 512, -1},
     {"kst", "DG_TS_K128", 0, 128},      {"bn64_short", "DG_BN64_SHORT", 0, 1}, {"splitk", "DG_NO_SPLITK", 1, 0},
     {"f16", "DG_NO_F16", 1, 0},         {"bres", "DG_NO_BRES", 1, 0},     {"pdl", "DG_NO_PDL", 1, 0},
-    {"early_weights", "DG_EARLY_WEIGHTS", 0, 1}, {"f4conv", "DG_NO_F4CONV", 1, 0},
+    {"early_weights", "DG_EARLY_WEIGHTS", 0, 1}, {"f4conv", "DG_NO_F4CONV", 1, 0}, {"em", "DG_EM", 0, -1},
+    {"tma_store", "DG_NO_TMA_STORE", 1, 0},
 };
 
 int64_t *opt_table() {
@@ -102,7 +103,26 @@ dg_status gemm_dispatch(const uint8_t *P, int64_t ldp, const uint8_t *Q, int64_t
     const RequantArgs *ap = nullptr;
     if (rq) { a = to_args(rq); ap = &a; }
     const bool tc_ok = is_product && levels_fit_i8(pl) && levels_fit_i8(ql) && tc_available();
-    if ((variant == 2 || variant == 3) && !tc_ok) return DG_ERR_UNSUPPORTED;
+    // non-product table with int8 entries: the one-hot K' = 4K form on the tensor cores (dg.h)
+    const bool oh_ok = !is_product && max_abs_entry(Tt) <= 127 && tc_available() && (ldp % 4) == 0 &&
+                       (((uintptr_t)P) & 3) == 0;
+    if (variant == 3 && !tc_ok) return DG_ERR_UNSUPPORTED;
+    if (variant == 2 && !tc_ok && !oh_ok) return DG_ERR_UNSUPPORTED;
+    if ((variant == 0 || variant == 2) && !tc_ok && oh_ok) {
+        // P' = one-hot(P) [np][onehot_ld(K)], Q' = table columns of Q [nq][tcols_ld(K)]:
+        // D[p][q] = sum_k sum_i [P[p][k] == i] * Tt[(i << 2) | Q[q][k]]
+        const int64_t l1 = onehot_ld(K), lt = tcols_ld(K);
+        uint8_t *p1 = (uint8_t *)(((uintptr_t)ws + 127) & ~(uintptr_t)127);
+        int8_t *qt = (int8_t *)(((uintptr_t)(p1 + np * l1) + 127) & ~(uintptr_t)127);
+        if (!ws || (uint8_t *)(qt + nq * lt) > (uint8_t *)ws + ws_bytes) return DG_ERR_WORKSPACE;
+        dg_status s = expand_onehot(P, np, K, ldp, p1, l1, st);
+        if (s != DG_OK) return s;
+        s = expand_tcols(Q, nq, K, ldq, Tt, qt, lt, st);
+        if (s != DG_OK) return s;
+        const int32_t emax = (int32_t)max_abs_entry(Tt);
+        const int32_t pl1[4] = {0, 1, 0, 0}, ql1[4] = {emax, 0, 0, 0};   // (ql1 only bounds |acc|)
+        return lut_gemm_ts(p1, l1, qt, lt, np, nq, 4 * K, pl1, ql1, D, ldd, ap, st);
+    }
     if (variant == 3) return lut_gemm_tc(P, ldp, Q, ldq, np, nq, K, pl, ql, D, ldd, ap, st);
     if (variant == 2 || (variant == 0 && tc_ok)) {
         const int64_t ld8 = expand_ld(K);
@@ -197,9 +217,11 @@ dg_status dg_lut_from_table(const int32_t entries[16], int32_t entry_bits, dg_lu
     return DG_OK;
 }
 
-size_t dg_lut_gemm_workspace_size(int64_t N, int64_t K) {
-    if (N <= 0 || K <= 0) return 0;
-    return (size_t)(N * expand_ld(K) + 128);
+size_t dg_lut_gemm_workspace_size(int64_t M, int64_t N, int64_t K) {
+    if (M <= 0 || N <= 0 || K <= 0) return 0;
+    const int64_t product = N * expand_ld(K) + 128;
+    const int64_t onehot = M * onehot_ld(K) + 128 + N * tcols_ld(K) + 128;   // non-product int8 tables
+    return (size_t)(product > onehot ? product : onehot);
 }
 
 dg_status dg_lut_gemm(const uint8_t *d_w, int64_t ldw, const uint8_t *d_at, int64_t lda, int64_t M,
@@ -417,9 +439,12 @@ size_t dg_lut_conv2d_workspace_size(const dg_conv_params *p) {
     const int64_t Ho = (p->H + 2 * p->pad - p->kh) / p->stride + 1;
     const int64_t Wo = (p->W + 2 * p->pad - p->kw) / p->stride + 1;
     const int64_t K = (int64_t)p->kh * p->kw * p->C;
-    const int64_t cols = conv_is_direct(p) ? 0 : (int64_t)p->B * Ho * Wo * dg_packed_ld(K);   // upper bound
+    const int64_t rows = (int64_t)p->B * Ho * Wo;
+    const int64_t cols = conv_is_direct(p) ? 0 : rows * dg_packed_ld(K);   // upper bound
     const int64_t a = (cols + 127) / 128 * 128 + (int64_t)p->Cout * expand_ld(K) + 256;
-    return (size_t)(a + splitk_bytes(p));
+    // non-product int8 tables: one-hot activations + weight table columns after the im2col matrix
+    const int64_t b = (cols + 127) / 128 * 128 + rows * onehot_ld(K) + 128 + (int64_t)p->Cout * tcols_ld(K) + 384;
+    return (size_t)((a > b ? a : b) + splitk_bytes(p));
 }
 
 dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_lut *lut,
@@ -478,7 +503,7 @@ dg_status dg_lut_conv2d(const uint8_t *d_x, const uint8_t *d_w, const dg_lut *lu
     for (int a = 0; a < 4; ++a)
         for (int w = 0; w < 4; ++w) Tt[(a << 2) | w] = lut->entries[(w << 2) | a];
     const int64_t ldd = rq ? p->Cout / 4 : p->Cout;
-    // the rest of the workspace (after the im2col matrix) holds the expanded weights
+    // the rest of the workspace (after the im2col matrix) holds the expanded operands
     uint8_t *ws_rest = (uint8_t *)d_ws;
     size_t rest = ws_bytes;
     if (P != d_x) {

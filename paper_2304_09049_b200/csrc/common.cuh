@@ -199,6 +199,8 @@ enum OptId {
     OPT_PDL,            // programmatic dependent launch of the TS kernel: 1 on, 0 off
     OPT_EARLY_WEIGHTS,  // *_prepared: load resident weights / bias before griddepcontrol.wait (0 off)
     OPT_F4CONV,         // FP4 (kind::mxf4) kernel for qualifying product-table GEMM/conv layers: 0 off, 1 auto
+    OPT_EM,             // epilogue mode of the short-K wide kernel: 0 alternate tiles, 1 column split, 2 high priority, 3 both
+    OPT_TMA_STORE,      // int32 output tiles through the TMA tensor store where the instance has staging: 1 on, 0 off
     OPT_COUNT
 };
 int64_t opt(OptId id);

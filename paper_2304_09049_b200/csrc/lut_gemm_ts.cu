@@ -42,12 +42,17 @@ constexpr int SP_MAX = 32;       // packed P slots (narrow rows -> many slots in
 // BN columns) owns every EG-th tile, so EG = 2 keeps two tiles' epilogues in flight (short-K
 // tiles, where the epilogue dominates).
 // NUNP (template) unpack warps: 4 (one stage group) or 8 (two groups owning alternate stages).
-template <int NEPI, int NUNP>
+// EM (epilogue mode, template bits): EM_CSPLIT = every epilogue group works on every tile, group g on
+// column block g (the accumulator is released as soon as each warp has loaded its columns) instead
+// of groups owning alternate tiles; EM_HIGH = epilogue warps above the unpack warps in warp-id order
+// (scheduler priority) for layers whose cost is the epilogue.
+constexpr int EM_CSPLIT = 1, EM_HIGH = 2;
+template <int NEPI, int NUNP, int EM = 0>
 struct Roles {
     static constexpr int NUM_UGROUPS = NUNP / 4;
-    static constexpr int EPI_WARP0 = 0;                                   // lane quarter = warp % 4
-    static constexpr int UNPACK_WARP0 = EPI_WARP0 + NEPI;                 // lane quarter = warp % 4
-    static constexpr int PRODUCER_WARP = UNPACK_WARP0 + NUNP;
+    static constexpr int EPI_WARP0 = (EM & EM_HIGH) ? NUNP : 0;          // lane quarter = warp % 4
+    static constexpr int UNPACK_WARP0 = (EM & EM_HIGH) ? 0 : NEPI;        // lane quarter = warp % 4
+    static constexpr int PRODUCER_WARP = NEPI + NUNP;
     static constexpr int WAITER_WARP = PRODUCER_WARP + 1;
     static constexpr int MMA_WARP = WAITER_WARP + 1;
     static constexpr int NT = 32 * (MMA_WARP + 1);
@@ -99,7 +104,11 @@ struct TsCfg {
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr int OFF_WALK = OFF_TMEM + 16;           // 32 words: the MMA warp's copy of the tile walk
     static constexpr int OFF_TAB = (OFF_WALK + 128 + 15) / 16 * 16;   // 16-bit requant offsets, one u32 per column pair
-    static constexpr int ALLOC = OFF_TAB + TAB_PAIRS * 4 + 1024;
+    // int32-output staging for the TMA tensor store (4 epilogue warps x one 32 x 32 int32 chunk,
+    // 128-byte swizzle, 1024-aligned) in the instances with one epilogue group and room for it
+    static constexpr int STG_BYTES = (EG == 1 && !WIN && !ASM) ? 4 * 4096 : 0;
+    static constexpr int OFF_STG = (OFF_TAB + TAB_PAIRS * 4 + 1023) / 1024 * 1024;
+    static constexpr int ALLOC = OFF_STG + STG_BYTES + 1024;
     static_assert(((ASM || WIN) ? NACC * BN : TMEM_A0 + SA * ACOLS) <= TMEM_COLS && SA >= 2, "TMEM budget");
     static_assert(ALLOC <= 232448, "shared memory budget");
 };
@@ -107,8 +116,9 @@ struct TsCfg {
 #ifdef DG_TRACE
 // CTA 0 event timeline (tools/trace_ts.py): [event][stage or tile index] = clock(), recorded
 // in shared memory (a global store per event perturbs the pipeline) and copied out at the end
-constexpr int TL_N = 96;
-__device__ long long g_ts_tl[16][TL_N];
+constexpr int TL_N = 96, TL_E = 24;
+__device__ long long g_ts_tl[TL_E][TL_N];
+__shared__ uint32_t s_tl[TL_E][TL_N];
 #define TS_EV(e, i) do { if ((int)(i) < TL_N) s_tl[e][i] = (uint32_t)clock(); } while (0)
 #else
 #define TS_EV(e, i) do { } while (0)
@@ -149,6 +159,7 @@ struct TsArgs {
     int32_t sp;            // packed P slots (SP_MAX max)
     int32_t bres;          // 1: all ntq x nstages B tiles resident in smem (loaded once)
     int32_t early_b;       // 1: resident B tiles and the bias table are loaded before griddepcontrol.wait
+    int32_t tma_d;         // 1: int32 output tiles leave through the TMA tensor store (tm_d, staging smem)
     uint32_t lp;           // int8 levels of P codes
     void *D;
     int64_t ldd;
@@ -477,7 +488,7 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const int32_t *__res
 // 32 columns (measured 8% of the K = 64 layers' instructions).
 template <int BN, int RES, bool TAB>
 __device__ __forceinline__ void epi16_tile(const TsArgs &ta, const RequantArgs &rq, uint32_t trow, int64_t p, int64_t q0,
-                                           uint32_t na_row, uint32_t tab, int lane, uint32_t acc_bar) {
+                                           uint32_t na_row, uint32_t tab, int lane, uint32_t acc_bar, uint32_t tl_ev = 0) {
     constexpr int NCH = BN / 32;
     // all of the tile's accumulators (up to 128 columns as 16-bit pairs) are loaded
     // before any requant work, so the TMEM buffer goes back to the MMA as early as
@@ -489,16 +500,24 @@ __device__ __forceinline__ void epi16_tile(const TsArgs &ta, const RequantArgs &
 #pragma unroll
         for (int l = 0; l < NLD; ++l) ptx::tmem_ld_32x32b_x32_pack16(trow + (c0 + 2 * l) * 32, r16[l]);
         ptx::tmem_ld_wait();
+        if (lane == 0 && threadIdx.x < 32) TS_EV(c0 == 0 ? 16 : 18, tl_ev);
         if (c0 + 2 * NLD >= NCH && RES != 2) {   // (int32 residual: kept for an exact redo)
             ptx::tc_fence_before();
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(acc_bar);
         }
+#ifdef DG_EXP_LDONLY
+        if (r16[0][5] != 0x12345u) continue;
+#endif
 #pragma unroll
         for (int hh = 0; hh < 2 * NLD; ++hh) {
             const int64_t qc = q0 + (c0 + hh) * 32;
             uint32_t na[16];
+#ifdef DG_EXP_NOLDS
+            if (false) {
+#else
             if constexpr (TAB) {
+#endif
                 const uint32_t ta4 = tab + (uint32_t)(qc >> 1) * 4u;
 #pragma unroll
                 for (int j = 0; j < 4; ++j) {
@@ -542,9 +561,13 @@ __device__ __forceinline__ void epi16_tile(const TsArgs &ta, const RequantArgs &
             if (p >= ta.np) continue;
             const uint2 o = requant16_32(rr, na, ta.f16_w2, ta.f16_m, ta.f16_c2);
             uint8_t *dp = reinterpret_cast<uint8_t *>(ta.D) + p * ta.ldd + (qc >> 2);
+#ifdef DG_EXP_NOSTORE
+            if (o.x == 0x12345678u && o.y == 0x9abcdef0u)
+#endif
             if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = o;
             else store_codes32_ts(dp, o.x, o.y, 8);
         }
+        if (lane == 0 && threadIdx.x < 32) TS_EV(c0 == 0 ? 17 : 19, tl_ev);
     }
     if constexpr (RES == 2) {
         ptx::tc_fence_before();
@@ -556,29 +579,30 @@ __device__ __forceinline__ void epi16_tile(const TsArgs &ta, const RequantArgs &
 // Epilogue tile loop for the launch-uniform rare modes — split-K partial tiles, and 16-bit
 // requant with a residual — kept out of line: inlined, their code raised register pressure in the
 // common loop past the 128-register cap and its spills cost ~40% on short-K layers (measured).
-template <int BN, int NACC, int EG, bool WIN>
+template <int BN, int NACC, int EG, bool WIN, bool CS>
 __device__ __noinline__ void epilogue_loop_rare(const TsArgs &ta, const RequantArgs &rq, uint32_t tmem, uint32_t tab,
                                                 uint32_t acc_bar0, int ntiles, int warp, int lane, bool f16_ok) {
-    constexpr int NCH = BN / 32;
+    // CS: group eg takes columns [eg * BN / EG, (eg + 1) * BN / EG) of every tile
+    constexpr int CW = CS ? BN / EG : BN, NCH = CW / 32;
     const int quarter = warp & 3, eg = warp >> 2;
     uint32_t tl = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-        if (EG > 1 && (int)(tl % EG) != eg) continue;
+        if (!CS && EG > 1 && (int)(tl % EG) != eg) continue;
         const uint32_t acc = tl % NACC;
         const uint32_t acc_full = acc_bar0 + 8 * acc, acc_empty = acc_bar0 + 8 * (NACC + acc);
         int tp, tq, sb_, se_;
         work_item<true>(ta, t, tp, tq, sb_, se_);
         const int64_t p = (int64_t)tp * BM + quarter * 32 + lane;
-        const int64_t q0 = (int64_t)tq * BN;
+        const int64_t q0 = (int64_t)tq * BN + (CS ? eg * CW : 0);
         ptx::mbar_wait(acc_full, (tl / NACC) & 1u);
         ptx::tc_fence_after();
-        const uint32_t trow = tmem + acc * BN + ((uint32_t)(quarter * 32) << 16);
+        const uint32_t trow = tmem + acc * BN + (CS ? eg * CW : 0) + ((uint32_t)(quarter * 32) << 16);
         if (ta.sk > 1) {
             ts_epilogue_splitk(ta, trow, NCH, p, q0, (int)(t - (int)fdiv((uint32_t)t, ta.fd_sk) * ta.sk), lane, acc_empty);
             continue;
         }
         // residual in the 16-bit path (every lane's row offset must fit int16 for bias_axis 1)
-        bool use16 = f16_ok && q0 + BN <= ta.nq;
+        bool use16 = f16_ok && q0 + CW <= ta.nq;
         uint32_t na_row = ta.f16_na2;
         if (use16 && !ta.f16_tab && rq.bias && rq.bias_axis == 1) {
             const int64_t n = (int64_t)(p < ta.np ? __ldg(rq.bias + p) : 0) - ta.f16_thr0m1;
@@ -586,11 +610,11 @@ __device__ __noinline__ void epilogue_loop_rare(const TsArgs &ta, const RequantA
             use16 = __all_sync(0xFFFFFFFFu, (n < 0 ? -n : n) + ta.f16_accmax <= 32767);
         }
         if (use16 && ta.f16_res == 1) {
-            if (ta.f16_tab) epi16_tile<BN, 1, true>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
-            else epi16_tile<BN, 1, false>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
+            if (ta.f16_tab) epi16_tile<CW, 1, true>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
+            else epi16_tile<CW, 1, false>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
         } else if (use16 && ta.f16_res == 2) {
-            if (ta.f16_tab) epi16_tile<BN, 2, true>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
-            else epi16_tile<BN, 2, false>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
+            if (ta.f16_tab) epi16_tile<CW, 2, true>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
+            else epi16_tile<CW, 2, false>(ta, rq, trow, p, q0, na_row, tab, lane, acc_empty);
         } else {
 #pragma unroll 1
             for (int c = 0; c < NCH; ++c) ts_epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
@@ -601,12 +625,14 @@ __device__ __noinline__ void epilogue_loop_rare(const TsArgs &ta, const RequantA
     }
 }
 
-template <int BN, int NEPI, int NUNP, int KST, bool WIN, bool ASM, bool SK>
-__global__ void __launch_bounds__(Roles<NEPI, NUNP>::NT, 1)
+template <int BN, int NEPI, int NUNP, int KST, bool WIN, bool ASM, bool SK, int EM>
+__global__ void __launch_bounds__(Roles<NEPI, NUNP, EM>::NT, 1)
 lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
-                   const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
-    using C = TsCfg<BN, NEPI / 4, KST, WIN, ASM>;
-    using R = Roles<NEPI, NUNP>;
+                   const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ TsArgs ta,
+                   const __grid_constant__ RequantArgs rq) {
+    using C = TsCfg<BN, (EM & EM_CSPLIT) ? 1 : NEPI / 4, KST, WIN, ASM>;
+    using R = Roles<NEPI, NUNP, EM>;
+    constexpr bool CS = (EM & EM_CSPLIT) != 0;
     constexpr int SB = C::SB, SA = C::SA, NACC = C::NACC, SP = SP_MAX;
     const int nsp = ta.sp;
     const uint32_t pslot = (uint32_t)(BM * ta.pks);
@@ -615,8 +641,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                   NUM_UGROUPS = R::NUM_UGROUPS;
     extern __shared__ uint8_t smem_raw[];
 #ifdef DG_TRACE
-    __shared__ uint32_t s_tl[16][TL_N];
-    for (int i = threadIdx.x; i < 16 * TL_N; i += blockDim.x) (&s_tl[0][0])[i] = 0u;
+    for (int i = threadIdx.x; i < TL_E * TL_N; i += blockDim.x) (&s_tl[0][0])[i] = 0u;
 #endif
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = ptx::smem_u32(smem);
@@ -653,7 +678,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
             for (int a = 0; a < NACC; ++a) {
                 ptx::mbar_init(acc_full(a), 1);
-                ptx::mbar_init(acc_empty(a), 4);   // the 4 warps of the owning group
+                ptx::mbar_init(acc_empty(a), CS ? NEPI : 4);   // the 4 warps of the owning group (CS: all)
             }
             ptx::fence_mbar_init();
         }
@@ -919,7 +944,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 __syncwarp();
             }
         }
-    } else if (warp >= UNPACK_WARP0 && WIN) {
+    } else if (warp >= UNPACK_WARP0 && warp < UNPACK_WARP0 + NUNP && WIN) {
         // ---------------- WIN: fill each tile's window of padded input pixels.  Thread = window row:
         // its packed pixel (C/4 bytes) arrives by cp.async two tiles ahead (ring of 2 slots), is
         // unpacked to int8 levels and stored as C/16 16-byte K chunks (chunk j at j*lbo + row*16).
@@ -1067,7 +1092,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             if (lane == 0) ptx::mbar_arrive(full_a(wb));
             if (tid == 0) TS_EV(2, tl);
         }
-    } else if (warp >= UNPACK_WARP0) {
+    } else if (warp >= UNPACK_WARP0 && warp < UNPACK_WARP0 + NUNP) {
         // ---------------- unpackers: thread = row; packed smem -> int8 levels -> TMEM (A operand).
         // Groups of 4 warps (one per TMEM lane quarter) take alternate stages.
         ptx::griddep_wait();
@@ -1179,7 +1204,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 } else {
                     ++sub;
                 }
-                if ((int)(g & (NUM_UGROUPS - 1)) != grp) continue;
+                if ((int)(g % NUM_UGROUPS) != grp) continue;
                 const int sa = g % SA;
                 // 16-byte chunks (64 codes, 2 k-steps) of this stage that the MMA reads
                 const int nchunk = (s != ta.nstages - 1) ? 2 * C::HALVES : (ta.last_ksteps + 1) / 2;
@@ -1264,7 +1289,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         }   // general stages
     } else {
         // ---------------- epilogue (lane quarter = warp % 4, tile group = warp / 4)
-        constexpr int EG = NEPI / 4, HALF = BN, NCH = BN / 32;
+        constexpr int EG = NEPI / 4, HALF = CS ? BN / EG : BN, NCH = HALF / 32;
         static_assert(NCH % 2 == 0, "epilogue loads 64 columns at a time");
         // 16-bit requant offsets per column pair (bias_axis 0): negA = bias - (thr0 - 1), checked
         // against int16 overflow of acc + negA; any failure sends every tile to the 32-bit path
@@ -1285,15 +1310,15 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const bool f16_ok = ta.f16 && *f16_flag == 0u;
         ptx::griddep_wait();
         if (!WIN && ((SK && ta.sk > 1) || ta.f16_res)) {
-            epilogue_loop_rare<BN, NACC, EG, WIN>(ta, rq, tmem, sbase + C::OFF_TAB, acc_full(0), ntiles, warp - EPI_WARP0,
+            epilogue_loop_rare<BN, NACC, EG, WIN, CS>(ta, rq, tmem, sbase + C::OFF_TAB, acc_full(0), ntiles, warp - EPI_WARP0,
                                                   lane, f16_ok);
         } else {
-        const int quarter = warp & 3, eg = (warp - EPI_WARP0) >> 2, half = 0;
+        const int quarter = warp & 3, eg = (warp - EPI_WARP0) >> 2, half = CS ? eg : 0;
         const bool col_bias = rq.bias && rq.bias_axis == 0;
         uint32_t tl = 0;
         const int wpair = WIN ? ta.wpair : 0;   // WIN pair mode: a work item = 2 row blocks (2 accumulators)
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-            if (EG > 1 && (int)(tl % EG) != eg) continue;
+            if (!CS && EG > 1 && (int)(tl % EG) != eg) continue;
             int tp, tq;
             tile_coords(ta, t, tp, tq);
             for (int h = 0; h <= wpair; ++h) {
@@ -1336,8 +1361,40 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 use16 = __all_sync(0xFFFFFFFFu, (n < 0 ? -n : n) + ta.f16_accmax <= 32767);
             }
             if (use16) {
-                if (ta.f16_tab) epi16_tile<BN, 0, true>(ta, rq, trow, p, q0, na_row, sbase + C::OFF_TAB, lane, acc_empty(acc));
-                else epi16_tile<BN, 0, false>(ta, rq, trow, p, q0, na_row, sbase + C::OFF_TAB, lane, acc_empty(acc));
+                if (ta.f16_tab) epi16_tile<HALF, 0, true>(ta, rq, trow, p, q0, na_row, sbase + C::OFF_TAB, lane, acc_empty(acc), tl);
+                else epi16_tile<HALF, 0, false>(ta, rq, trow, p, q0, na_row, sbase + C::OFF_TAB, lane, acc_empty(acc), tl);
+            } else if (C::STG_BYTES > 0 && ta.tma_d && !ta.has_rq && q0 + HALF <= ta.nq) {
+                // int32 tile through the TMA tensor store: per 32-column chunk the warp's 32 rows x
+                // 128 bytes go to its staging buffer (128-byte swizzle: 16-byte unit u of row r at
+                // u ^ (r & 7), conflict-free STS.128) and one bulk tensor store writes them out; the
+                // scattered per-lane row stores cost a wavefront per row (measured 21k cycles per
+                // 128 x 256 int32 tile on the 16384^3 GEMM, with the single accumulator idle)
+                const uint32_t stg = sbase + (uint32_t)C::OFF_STG + (uint32_t)(quarter * 4096);
+                const int32_t row0 = (int32_t)(((int64_t)tp << wpair) * BM + quarter * 32);
+#pragma unroll 1
+                for (int c = 0; c < NCH; ++c) {
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(trow + c * 32, v);
+                    ptx::tmem_ld_wait();
+                    if (c == NCH - 1) {
+                        ptx::tc_fence_before();
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
+                    }
+                    if (lane == 0) ptx::bulk_wait_read<0>();   // the previous chunk's store has read the buffer
+                    __syncwarp();
+#pragma unroll
+                    for (int u = 0; u < 8; ++u)
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(stg + (uint32_t)lane * 128u +
+                                                                                   ((uint32_t)(u ^ (lane & 7)) << 4)),
+                                     "r"(v[4 * u]), "r"(v[4 * u + 1]), "r"(v[4 * u + 2]), "r"(v[4 * u + 3]) : "memory");
+                    ptx::fence_proxy_async_smem();
+                    __syncwarp();
+                    if (lane == 0) {
+                        ptx::tma_store_2d(&tm_d, stg, (int32_t)(q0 + c * 32), row0);
+                        ptx::bulk_commit();
+                    }
+                }
             } else if (!fast) {
 #pragma unroll 1
                 for (int c = 0; c < NCH; ++c) ts_epilogue_general(ta, rq, trow + c * 32, p, q0 + c * 32);
@@ -1395,6 +1452,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }   // h
         }
         }   // common modes
+        if (C::STG_BYTES > 0 && ta.tma_d && lane == 0) ptx::bulk_wait<0>();   // TMA stores complete before exit
         if (ta.npeer) __threadfence_system();   // peer stores visible system-wide before the grid completes
     }
 
@@ -1402,7 +1460,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     __syncthreads();
 #ifdef DG_TRACE
     if (blockIdx.x == 0)
-        for (int i = threadIdx.x; i < 16 * TL_N; i += blockDim.x) (&g_ts_tl[0][0])[i] = (&s_tl[0][0])[i];
+        for (int i = threadIdx.x; i < TL_E * TL_N; i += blockDim.x) (&g_ts_tl[0][0])[i] = (&s_tl[0][0])[i];
 #endif
     if (warp == PRODUCER_WARP) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
 }
@@ -1478,10 +1536,10 @@ EncodeTiledFn encode_fn_ts() {
 #ifdef DG_TRACE
 extern "C" __attribute__((visibility("default"))) int dg_debug_ts_timeline(long long *host, int reset) {
     if (reset) {
-        static long long z[16 * TL_N];
+        static long long z[TL_E * TL_N];
         return cudaMemcpyToSymbol(g_ts_tl, z, sizeof(z)) == cudaSuccess ? 0 : -1;
     }
-    return cudaMemcpyFromSymbol(host, g_ts_tl, sizeof(long long) * 16 * TL_N) == cudaSuccess ? 0 : -1;
+    return cudaMemcpyFromSymbol(host, g_ts_tl, sizeof(long long) * TL_E * TL_N) == cudaSuccess ? 0 : -1;
 }
 #endif
 
@@ -1533,11 +1591,11 @@ thread_local int32_t *const *g_peers = nullptr;
 thread_local int32_t g_npeers = 0;
 thread_local bool g_b_prepared = false;   // the B operand / bias are caller-prepared set-up data
 
-template <int BN, int NEPI, int NUNP, int KST, bool WIN = false, bool ASM = false, bool SK = false>
+template <int BN, int NEPI, int NUNP, int KST, bool WIN = false, bool ASM = false, bool SK = false, int EM = 0>
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                     cudaStream_t st, const TsConv *cv, void *skws = nullptr, size_t skws_bytes = 0) {
-    using C = TsCfg<BN, NEPI / 4, KST, WIN, ASM>;
+    using C = TsCfg<BN, (EM & EM_CSPLIT) ? 1 : NEPI / 4, KST, WIN, ASM>;
     int64_t acc_bound = 0;   // K * max |pl[a] * ql[b]|
     for (int a = 0; a < 4; ++a)
         for (int b = 0; b < 4; ++b) {
@@ -1686,13 +1744,26 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         ta.fd_ho = make_fastdiv((uint32_t)cv->Ho);
         if (np >= ((int64_t)1 << 31)) return DG_ERR_SHAPE;
     }
-    CUtensorMap mp, mb;
+    CUtensorMap mp, mb, md;
     memset(&mp, 0, sizeof(mp));
+    memset(&md, 0, sizeof(md));
+    ta.tma_d = 0;
+    if (C::STG_BYTES > 0 && !rq && ta.npeer == 0 && ((uintptr_t)D & 15) == 0 && (ldd * 4) % 16 == 0 && nq >= 32 &&
+        opt(OPT_TMA_STORE)) {
+        EncodeTiledFn fn = encode_fn_ts();
+        cuuint64_t dims[2] = {(cuuint64_t)nq, (cuuint64_t)np};
+        cuuint64_t strides[1] = {(cuuint64_t)(ldd * 4)};
+        cuuint32_t box[2] = {32, 32}, estr[2] = {1, 1};
+        if (fn && fn(&md, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, D, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
+            ta.tma_d = 1;
+    }
     if (!cv && !ta.bulk && !make_map_sw128(&mp, P, ldp, np, BM, ta.pks)) return DG_ERR_CUDA;
     if (!make_map_sw128(&mb, Q8, ld8, nq, BN, 128)) return DG_ERR_CUDA;
     static bool attr_set = false;
     if (!attr_set) {
-        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
+        if (cudaFuncSetAttribute(lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK, EM>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::ALLOC) !=
             cudaSuccess)
             return DG_ERR_CUDA;
         attr_set = true;
@@ -1719,7 +1790,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     const RequantArgs rqv = rq ? *rq : dummy;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)grid);
-    lc.blockDim = dim3((unsigned)Roles<NEPI, NUNP>::NT);
+    lc.blockDim = dim3((unsigned)Roles<NEPI, NUNP, EM>::NT);
     lc.dynamicSmemBytes = C::ALLOC;
     lc.stream = st;
     cudaLaunchAttribute la[1];
@@ -1727,7 +1798,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     la[0].val.programmaticStreamSerializationAllowed = opt(OPT_PDL) ? 1 : 0;
     lc.attrs = la;
     lc.numAttrs = 1;
-    if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK>, mp, mb, ta, rqv) != cudaSuccess)
+    if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK, EM>, mp, mb, md, ta, rqv) != cudaSuccess)
         return DG_ERR_CUDA;
     if (ta.sk > 1) {
         const int64_t thr = np * ((nq + 3) >> 2);
@@ -1741,9 +1812,9 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
             return DG_ERR_CUDA;
     }
     char tag[160];
-    snprintf(tag, sizeof(tag), "ts bn=%d epi=%d unp=%d kst=%d%s%s%s nwin=%d wpair=%d sk=%d bres=%d f16=%d implicit=%d bulk=%d early=%d",
-             BN, NEPI, NUNP, KST, WIN ? " win" : "", ASM ? " asm" : "", SK ? " skinst" : "", ta.nwin, ta.wpair, ta.sk,
-             ta.bres, ta.f16, ta.implicit, ta.bulk, ta.early_b);
+    snprintf(tag, sizeof(tag), "ts bn=%d epi=%d unp=%d kst=%d%s%s%s em=%d nwin=%d wpair=%d sk=%d bres=%d f16=%d implicit=%d bulk=%d early=%d tmad=%d",
+             BN, NEPI, NUNP, KST, WIN ? " win" : "", ASM ? " asm" : "", SK ? " skinst" : "", EM, ta.nwin, ta.wpair, ta.sk,
+             ta.bres, ta.f16, ta.implicit, ta.bulk, ta.early_b, ta.tma_d);
     set_last_kernel(tag);
     return launch_status(ta.sk > 1 ? 2 : 1);
 }
@@ -1802,8 +1873,13 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     const bool k256 = K > KA && opt(OPT_KST) != 128;
     // short K, wide output: 128x256 tiles with the A operand in shared memory and two TMEM accumulators
     // (measured: narrower ASM tiles with 128-code stages lose to the TMEM-A kernel at K = 256)
-    if (short_k && nq >= 256 && opt(OPT_ASM))
+    if (short_k && nq >= 256 && opt(OPT_ASM)) {
+        const int64_t em = opt(OPT_EM);
+        if (em == 1) return launch_ts<256, 8, 4, 128, false, true, false, EM_CSPLIT>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (em == 2) return launch_ts<256, 8, 4, 128, false, true, false, EM_HIGH>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (em == 3) return launch_ts<256, 8, 4, 128, false, true, false, EM_CSPLIT | EM_HIGH>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         return launch_ts<256, 8, 4, 128, false, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+    }
     // 128x256 tiles halve the shared-memory bytes of B per MAC (measured: 8192^3 1666 -> 2323
     // TOPS); their single TMEM accumulator buffer cannot overlap the epilogue with the next tile,
     // so they are used only when the K loop is long (>= 24 x 128 codes).

@@ -90,6 +90,25 @@ DG_DEV void tma_load_2d(uint32_t dst, const CUtensorMap *m, uint32_t bar, int32_
 }
 
 // 1-D bulk copy global -> shared (contiguous bytes, multiple of 16), completes on an mbarrier
+// TMA tensor store shared -> global (bulk-group completion): box at {x (innermost), y}; the smem
+// source must be laid out as the map's box with its swizzle.  Commit / wait: the store has finished
+// READING shared memory after wait_group.read (the buffer may be rewritten), and is complete after
+// wait_group.
+DG_DEV void tma_store_2d(const CUtensorMap *m, uint32_t src, int32_t x, int32_t y) {
+    asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%2, %3}], [%1];" ::"l"(
+                     reinterpret_cast<uint64_t>(m)),
+                 "r"(src), "r"(x), "r"(y)
+                 : "memory");
+}
+DG_DEV void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+template <int N>
+DG_DEV void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory"); }
+template <int N>
+DG_DEV void bulk_wait() { asm volatile("cp.async.bulk.wait_group %0;" ::"n"(N) : "memory"); }
+DG_DEV void sts64(uint32_t saddr, uint32_t a, uint32_t b) {
+    asm volatile("st.shared.v2.u32 [%0], {%1, %2};" ::"r"(saddr), "r"(a), "r"(b) : "memory");
+}
+
 DG_DEV void bulk_load(uint32_t dst, const void *src, uint32_t bytes, uint32_t bar) {
     asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                  "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)

@@ -77,7 +77,7 @@ def lib():
                                               P, i64, P], i32),
             "dg_im2col": ([P, i32, i32, i32, i32, i32, i32, i32, i32, u8, P, i64, P], i32),
             "dg_requantize": ([P, i64, i64, i64, P, P, i64, P], i32),
-            "dg_lut_gemm_workspace_size": ([i64, i64], ctypes.c_size_t),
+            "dg_lut_gemm_workspace_size": ([i64, i64, i64], ctypes.c_size_t),
             "dg_lut_gemm": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, P, ctypes.c_size_t, i32, P], i32),
             "dg_expand_ld": ([i64], i64),
             "dg_expand_operand": ([P, i64, i64, i64, P, P, i64, P], i32),
@@ -288,8 +288,8 @@ def requantize(acc: torch.Tensor, rq: Requant, out: torch.Tensor | None = None, 
 
 
 # ---------------------------------------------------------------- GEMM / conv
-def gemm_workspace_size(N: int, K: int) -> int:
-    return int(lib().dg_lut_gemm_workspace_size(N, K))
+def gemm_workspace_size(M: int, N: int, K: int) -> int:
+    return int(lib().dg_lut_gemm_workspace_size(M, N, K))
 
 
 def lut_gemm(w: torch.Tensor, at: torch.Tensor, M: int, N: int, K: int, lut: dg_lut,
@@ -303,7 +303,7 @@ def lut_gemm(w: torch.Tensor, at: torch.Tensor, M: int, N: int, K: int, lut: dg_
         out = (torch.empty((M, (N + 3) // 4), dtype=torch.uint8, device=w.device) if rq is not None
                else torch.empty((M, N), dtype=torch.int32, device=w.device))
     if ws is None:
-        ws = torch.empty(gemm_workspace_size(N, K), dtype=torch.uint8, device=w.device)
+        ws = torch.empty(gemm_workspace_size(M, N, K), dtype=torch.uint8, device=w.device)
     r = rq.c() if rq is not None else None
     _check(lib().dg_lut_gemm(_ptr(w), w.shape[1], _ptr(at), at.shape[1], M, N, K, ctypes.byref(lut),
                              _ptr(out), out.shape[1], ctypes.byref(r) if r is not None else None,

@@ -128,7 +128,7 @@ class NetRunner:
             plan = LayerPlan(L.name, L, params, lut, lut_t, rq, wq, w8, xq, out, rows, K, direct,
                              2 * L.cout * rows * L.k * L.k * L.cin)
             ws_need = max(ws_need, dg.conv_workspace_size(params), (0 if direct else rows * plan.cols_ld),
-                          dg.gemm_workspace_size(L.cout, K))
+                          dg.gemm_workspace_size(rows, L.cout, K))
             self.plans.append(plan)
         self.ws = torch.zeros(max(ws_need, 16), dtype=torch.uint8, device=device)
         self.ws_gemm = self.ws

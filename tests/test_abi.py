@@ -36,7 +36,7 @@ def test_every_declared_symbol_is_exported(lib):
 def test_host_calls_without_gpu():
     from paper_2304_09049_b200 import dg
     L = dg.lib()
-    assert L.dg_abi_version() == 3
+    assert L.dg_abi_version() == 4
     assert isinstance(dg.kernel_launches(), int) and dg.kernel_launches() >= 0
     assert L.dg_status_string(-4) == b"DG_ERR_OVERFLOW"
     lut = dg.build_lut([-2, -1, 0, 1], [0, 1, 2, 3], 8)

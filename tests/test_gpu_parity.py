@@ -171,10 +171,20 @@ def test_gemm_non_product_tables_cc(seed):
     W = g.integers(0, 4, (M, K), dtype=np.uint8)
     A = g.integers(0, 4, (K, N), dtype=np.uint8)
     lut = dg.lut_from_table(T, 32)
-    assert np.array_equal(host(run_gemm(W, A, lut, "cc")), oracle.lut_gemm(W, A, T))
-    for v in ("tc", "tc_ss"):
+    exp = oracle.lut_gemm(W, A, T)
+    assert np.array_equal(host(run_gemm(W, A, lut, "cc")), exp)
+    assert dg.last_kernel().startswith("cc")
+    with pytest.raises(dg.DGError, match="UNSUPPORTED"):
+        run_gemm(W, A, lut, "tc_ss")
+    if amp <= 127:   # int8 entries: the public call runs the one-hot K' = 4K tensor-core form (auto and tc)
+        for v in ("auto", "tc"):
+            assert np.array_equal(host(run_gemm(W, A, lut, v)), exp)
+            assert dg.last_kernel().startswith("ts ")
+    else:
         with pytest.raises(dg.DGError, match="UNSUPPORTED"):
-            run_gemm(W, A, lut, v)
+            run_gemm(W, A, lut, "tc")
+        assert np.array_equal(host(run_gemm(W, A, lut, "auto")), exp)   # auto falls back to the cc kernel
+        assert dg.last_kernel().startswith("cc")
 
 
 @pytest.mark.parametrize("variant", VARIANTS)
@@ -692,6 +702,34 @@ def test_gemm_onehot_non_product_vs_oracle(seed):
     atc = dg.expand_tcols(gpu_pack(np.ascontiguousarray(A.T)), K, lut)
     C = host(dg.lut_gemm_onehot(w1h, atc, M, N, K, lut))
     assert np.array_equal(C, oracle.lut_gemm(W, A, T))
+
+
+@pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", [(2, 9, 7, 64, 32, 3, 1, 1, 2), (1, 10, 10, 12, 20, 3, 2, 1, 1),
+                                                                   (2, 6, 6, 64, 64, 1, 1, 0, 0), (1, 9, 9, 8, 16, 5, 1, 2, 3)])
+def test_conv_non_product_table_public_call(B, H, W, C, Cout, k, stride, pad, pad_code):
+    """dg_lut_conv2d with a NON-product int8 table (any 16 entries): im2col + one-hot
+    activations + weight table columns on the tensor cores, int32 and fused requant, vs O-CONV."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    g = np.random.default_rng(B + H + C + Cout + k + pad_code)
+    T = g.integers(-127, 128, 16).astype(np.int32)
+    lut = dg.lut_from_table(T, 8)
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, k, k, C), dtype=np.uint8)
+    exp = oracle.conv2d_direct(x, w, T, stride, pad, pad_code)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp, wpad=0)
+    if Cp != C:   # padded channels must contribute nothing: pad weights and activations with codes whose entry is 0
+        pytest.skip("non-product tables need C % 4 == 0 (no neutral pad code in general)")
+    p = dg.conv_params(B, H, W, Cp, Cout, k, k, stride, pad, pad_code, ldw=wp.shape[1])
+    out = dg.lut_conv2d(xp, wp, lut, p)
+    assert dg.last_kernel().startswith("ts "), dg.last_kernel()
+    assert np.array_equal(host(out).reshape(exp.shape), exp)
+    mu = int(np.round(exp.mean()))
+    rq = dg.Requant(mult=15000, shift=20, zp=1, bias=torch.full((Cout,), -mu, dtype=torch.int32, device=DEV))
+    outc = dg.lut_conv2d(xp, wp, lut, p, rq=rq)
+    expc = oracle.requantize(exp.reshape(-1, Cout), 15000, 20, 1, 0, 3, bias=np.full(Cout, -mu, np.int32), bias_axis=0)
+    assert np.array_equal(oracle_codes_of(outc, expc.shape[0], Cout), expc)
 
 
 def test_gemm_onehot_operands_and_requant():

@@ -20,7 +20,7 @@ for s in a.shapes.split(","):
     w = torch.randint(0, 256, (M, ld), dtype=torch.uint8, device="cuda")
     at = torch.randint(0, 256, (N, ld), dtype=torch.uint8, device="cuda")
     out = torch.empty((M, N), dtype=torch.int32, device="cuda")
-    ws = torch.empty(dg.gemm_workspace_size(N, ld * 4), dtype=torch.uint8, device="cuda")
+    ws = torch.empty(dg.gemm_workspace_size(M, N, ld * 4), dtype=torch.uint8, device="cuda")
     at8 = dg.expand_operand(at, ld * 4, lut.al)
     for v in a.variants.split(","):
         if v == "cc" and M * N * K > 2 ** 36:

@@ -31,7 +31,8 @@ else:
     rq = None
 L = dg.lib()
 TLN = 96
-buf = (ctypes.c_longlong * (16 * TLN))()
+TLE = 24
+buf = (ctypes.c_longlong * (TLE * TLN))()
 for it in range(2):
     L.dg_debug_ts_timeline(buf, 1)
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -42,14 +43,14 @@ for it in range(2):
         dg.lut_gemm_prepared(w, at8, M, N, K, lut, rq=rq, out=out)
     e1.record(); torch.cuda.synchronize()
 L.dg_debug_ts_timeline(buf, 0)
-a = np.frombuffer(buf, dtype=np.int64).reshape(16, TLN).astype(np.int64)
+a = np.frombuffer(buf, dtype=np.int64).reshape(TLE, TLN).astype(np.int64)
 print(f"{M}x{N}x{K}: {e0.elapsed_time(e1):.3f} ms")
 t0 = a[a > 0].min()
 a = np.where(a > 0, a - t0, -1)
 nst = (K + 127) // 128
 names = {13: "P_loop", 14: "P_slot", 12: "P_tma", 0: "unp0", 1: "unp_rdy", 11: "emptyA", 2: "fullA", 4: "w_fullA", 5: "w_fullB", 6: "handoff"}
 print("stage " + " ".join(f"{v:>8s}" for v in names.values()))
-for g in list(range(0, 40)):
+for g in list(range(0, int(os.environ.get('TRACE_STAGES', '40')))):
     print(f"{g:5d} " + " ".join(f"{a[e][g]:8d}" for e in names))
 if len(sys.argv) > 2 and sys.argv[2] == "--short":
     print("tile  P_loop P_tma unp0 unp_done w_start w_fullA handoff epi0 epi_accfull epi_done")
@@ -62,6 +63,6 @@ if len(sys.argv) > 2 and sys.argv[2] == "--win":
     print("tile unp0 cpa_ok unp_done emptyW fullW_arr waiter_fullW  w_start epi0 epi_accfull epi_done")
     for t in range(0, 40):
         print(f"{t:4d} " + " ".join(f"{a[e][t]:8d}" for e in (0, 12, 1, 11, 2, 13, 3, 8, 9, 10)))
-print("tile  w_start  epi0   epi_accfull  epi_done")
+print("tile  w_start  epi0   epi_accfull  ld0_ok  r0_done  ld1_ok  r1_done  epi_done   (warp 0: even tiles)")
 for t in list(range(0, 16)) + list(range(38, 43)):
-    print(f"{t:4d} {a[3][t]:8d} {a[8][t]:8d} {a[9][t]:8d} {a[10][t]:8d}")
+    print(f"{t:4d} " + " ".join(f"{a[e][t]:8d}" for e in (3, 8, 9, 16, 17, 18, 19, 10)))
