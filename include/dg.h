@@ -350,6 +350,19 @@ DG_API dg_status dg_lut_conv2d_prepared(const uint8_t *d_x, const int8_t *d_w8, 
                                  const dg_conv_params *p, const dg_requant *rq, void *d_out, void *d_ws,
                                  size_t ws_bytes, void *stream);
 
+/* Convolution on the block-scaled FP4 tensor-core path (tcgen05 kind::mxf4):
+ * the same result as dg_lut_conv2d_prepared for product tables whose activation levels are
+ * lut->al = {0, 1, 2, 3} and whose weight levels v have v/2 in e2m1 (see dg_lut_gemm_f4), with
+ * K * max|entry| < 2^22 (else DG_ERR_OVERFLOW).  d_w4 = dg_expand_operand_f4(weights [Cout][K],
+ * levels = lut->wl) [Cout][ld4], K order (r, s, c).  The activation codes are unpacked on chip into
+ * e2m1 nibbles; 1x1 / stride-1 convs read x directly, others gather their taps (C/4 a power of
+ * two >= 16).  Output as dg_lut_conv2d_prepared.  DG_ERR_UNSUPPORTED (use the int8 path) for:
+ * residuals in rq, bias per row, requant parameters without a 16-bit form, other channel counts,
+ * Cout > 2048.  The expanded weights / bias are read before the programmatic-dependent-launch wait
+ * only under the "early_weights" option.                                                        */
+DG_API dg_status dg_lut_conv2d_f4_prepared(const uint8_t *d_x, const uint8_t *d_w4, int64_t ld4, const dg_lut *lut,
+                                           const dg_conv_params *p, const dg_requant *rq, void *d_out, void *stream);
+
 /* 4-bit convolution (see dg_lut_gemm4_prepared above for the digit form and its requirements). */
 DG_API dg_status dg_lut_conv2d4_prepared(const uint8_t *d_x4, const int8_t *d_w8, int64_t ld8,
                                          const int32_t levels[16], const dg_conv_params *p,

@@ -26,7 +26,7 @@ const OptDesc kOpts[dg::OPT_COUNT] = {
     {"kst", "DG_TS_K128", 0, 128},      {"bn64_short", "DG_BN64_SHORT", 0, 1}, {"splitk", "DG_NO_SPLITK", 1, 0},
     {"f16", "DG_NO_F16", 1, 0},         {"bres", "DG_NO_BRES", 1, 0},     {"pdl", "DG_NO_PDL", 1, 0},
     {"early_weights", "DG_EARLY_WEIGHTS", 0, 1}, {"f4conv", "DG_NO_F4CONV", 1, 0}, {"em", "DG_EM", 0, -1},
-    {"tma_store", "DG_NO_TMA_STORE", 1, 0},
+    {"tma_store", "DG_NO_TMA_STORE", 1, 0},      {"unp", "DG_UNP", 8, -1},
 };
 
 int64_t *opt_table() {
@@ -329,6 +329,34 @@ dg_status dg_lut_gemm4_prepared(const uint8_t *d_at4, int64_t lda, const int8_t 
     const int32_t pl[4] = {0, 1, 2, 3}, ql[4] = {(5 * wmax + 1) / 2, 0, 0, 0};
     return lut_gemm_ts(d_at4, lda, d_w8, ld8, N, M, 2 * K, pl, ql, d_ct, ldct, rq ? &a : nullptr, (cudaStream_t)stream,
                        nullptr, nullptr, 0, nullptr, 0, true);
+}
+
+dg_status dg_lut_conv2d_f4_prepared(const uint8_t *d_x, const uint8_t *d_w4, int64_t ld4, const dg_lut *lut,
+                                    const dg_conv_params *p, const dg_requant *rq, void *d_out, void *stream) {
+    if (!d_x || !d_w4 || !lut || !p || !d_out) return DG_ERR_INVALID_ARG;
+    if (p->B <= 0 || p->H <= 0 || p->W <= 0 || p->C <= 0 || p->Cout <= 0 || p->kh <= 0 || p->kw <= 0 ||
+        p->stride <= 0 || p->pad < 0)
+        return DG_ERR_SHAPE;
+    if (p->C % 4 || p->pad_code < 0 || p->pad_code > 3) return DG_ERR_RANGE;
+    if (rq && p->Cout % 4) return DG_ERR_SHAPE;
+    const int64_t Ho = (p->H + 2 * p->pad - p->kh) / p->stride + 1;
+    const int64_t Wo = (p->W + 2 * p->pad - p->kw) / p->stride + 1;
+    if (Ho <= 0 || Wo <= 0) return DG_ERR_SHAPE;
+    const int64_t K = (int64_t)p->kh * p->kw * p->C;
+    if (ld4 < expand_f4_ld(K) || ld4 % 128 || !aligned16(d_w4) || !aligned16(d_x)) return DG_ERR_SHAPE;
+    dg_status s = check_rq(rq);
+    if (s != DG_OK) return s;
+    if (!lut->is_product || !tc_available()) return DG_ERR_UNSUPPORTED;
+    for (int c = 0; c < 4; ++c)
+        if (lut->al[c] != c || f4_nibble_half(lut->wl[c]) < 0) return DG_ERR_UNSUPPORTED;
+    const int64_t acc_bound = K * max_abs_entry(lut->entries);
+    if (acc_bound >= ((int64_t)1 << 22)) return DG_ERR_OVERFLOW;
+    // the pad code's level must be exact in e2m1 too: codes are e2m1 already, nothing to check
+    RequantArgs ra{};
+    if (rq) ra = to_args(rq);
+    TsConv cv{d_x, p->H, p->W, p->C / 4, p->kh, p->kw, p->stride, p->pad, (int32_t)Ho, (int32_t)Wo, p->pad_code};
+    return lut_conv_f4(d_x, d_w4, ld4, cv, (int64_t)p->B * Ho * Wo, p->Cout, K, acc_bound, d_out,
+                       rq ? p->Cout / 4 : p->Cout, rq ? &ra : nullptr, (cudaStream_t)stream, true);
 }
 
 dg_status dg_lut_conv2d4_prepared(const uint8_t *d_x4, const int8_t *d_w8, int64_t ld8, const int32_t levels[16],

@@ -201,11 +201,14 @@ enum OptId {
     OPT_F4CONV,         // FP4 (kind::mxf4) kernel for qualifying product-table GEMM/conv layers: 0 off, 1 auto
     OPT_EM,             // epilogue mode of the short-K wide kernel: 0 alternate tiles, 1 column split, 2 high priority, 3 both
     OPT_TMA_STORE,      // int32 output tiles through the TMA tensor store where the instance has staging: 1 on, 0 off
+    OPT_UNP,            // unpack warps of the 128x256 long-K instance: 8 (default), 12 or 16
     OPT_COUNT
 };
 int64_t opt(OptId id);
 // tag of the GEMM kernel instance this thread launched last (dg_last_kernel)
 void set_last_kernel(const char *tag);
+// 16-bit SIMD requant constants (m, c) for thresholds t0 <= t1 <= t2, verified for every x (lut_gemm_ts.cu)
+bool f16_params(int64_t t0, int64_t t1, int64_t t2, uint32_t &m_out, uint32_t &c_out);
 inline dg_status launch_status(int nlaunched = 1) {
     cudaError_t e = cudaGetLastError();
     if (e == cudaSuccess) __atomic_fetch_add(&launch_counter(), (uint64_t)nlaunched, __ATOMIC_RELAXED);
@@ -257,6 +260,9 @@ struct TsConv {
     const uint8_t *x;
     int32_t H, W, Cb, kh, kw, stride, pad, Ho, Wo, pad_code;
 };
+dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const TsConv &cv, int64_t rows, int64_t cout,
+                      int64_t K, int64_t acc_bound, void *out, int64_t ldd, const RequantArgs *rq, cudaStream_t st,
+                      bool b_prepared);
 dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                       const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                       cudaStream_t st, const TsConv *cv = nullptr, void *skws = nullptr, size_t skws_bytes = 0,

@@ -1,0 +1,571 @@
+// lut_conv_f4.cu — the LUT-16 convolution on the block-scaled FP4 tensor-core path (tcgen05
+// kind::mxf4, e2m1 x e2m1; SURVEY §8(f) rank 2 on the conv workloads), in the conv orientation
+//
+//   out[pixel][co] = sum_{k<K} T[(w[co][k] << 2) | x_col[pixel][k]] = sum_k wl[w] * al[x]
+//
+// with the activation codes unpacked on chip (Alg. 1 line 9) into e2m1 nibbles (for activation
+// levels al = {0,1,2,3} the 2-bit code c IS the e2m1 encoding of c/2: two nibble masks per 16
+// codes), weights expanded offline to e2m1 nibbles of wl/2 (dg_expand_operand_f4), unit block
+// scales 2 x 2, so the fp32 tensor-core sum is sum(wl*al) exactly (every partial sum is an integer
+// below 2^22; the accumulators start at 1.5*2^23 so that the low 16 bits of an fp32 accumulator ARE
+// the int16 of its integer value: the 16-bit SIMD requant of the int8 kernel reads them unchanged).
+//
+// Tile 128 pixels x 128 output channels, three fp32 accumulator buffers (384 TMEM columns) + 32
+// block-scale columns.  Persistent, warp-specialised, one CTA per SM:
+//   warps 0..3   epilogue (lane quarter = warp): TMEM -> requant (S7) or int32 -> NHWC output
+//   warps 4..7   unpack: thread = output pixel; 1x1 convs read TMA slots of the NHWC tensor,
+//                others gather their pixel's taps (implicit im2col, cp.async ring); -> e2m1 A stage
+//   warp 8       producer: TMA of the e2m1 weight stages (and of the packed slots of direct convs)
+//   warp 9       waiter: mbarrier waits, hands each stage to the MMA warp through a named barrier
+//   warp 10      MMA issuer (whole warp, one lane elected inside the asm)
+#include <cuda.h>
+#include <stdio.h>
+#include <string.h>
+
+#include "common.cuh"
+#include "requant16.cuh"
+#include "tc_ptx.cuh"
+
+namespace dg {
+namespace {
+
+constexpr int CF_BM = 128, CF_BN = 128;
+constexpr int CF_KST = 256;                        // codes per stage: 128 bytes of e2m1 per row = 4 MMAs (K = 64)
+constexpr int CF_NACC = 3, CF_SA = 4, CF_SB = 6, CF_SP = 3, CF_IG = 6;
+constexpr int CF_A_STAGE = CF_BM * CF_KST / 2;     // 16 KB, SW128 K-major
+constexpr int CF_B_STAGE = CF_BN * CF_KST / 2;     // 16 KB, SW128 K-major
+constexpr int CF_P_SLOT = CF_BM * 128;             // 16 KB: 512 packed codes of every row (2 stages)
+constexpr int CF_RING = CF_BM * 64;                // 8 KB: one stage (64 packed bytes) of every row
+constexpr int CF_P_REGION = CF_SP * CF_P_SLOT > CF_IG * CF_RING ? CF_SP * CF_P_SLOT : CF_IG * CF_RING;
+constexpr int CF_TAB_PAIRS = 1024;                 // per-column requant offsets: Cout <= 2048
+constexpr int CF_OFF_B = 0;
+constexpr int CF_OFF_A = CF_OFF_B + CF_SB * CF_B_STAGE;
+constexpr int CF_OFF_P = CF_OFF_A + CF_SA * CF_A_STAGE;
+constexpr int CF_OFF_BAR = CF_OFF_P + CF_P_REGION;
+constexpr int CF_NBAR = 2 * CF_SP + 2 * CF_SB + 2 * CF_SA + 2 * CF_NACC;
+constexpr int CF_OFF_TMEM = CF_OFF_BAR + CF_NBAR * 8;
+constexpr int CF_OFF_TAB = (CF_OFF_TMEM + 16 + 15) / 16 * 16;
+constexpr int CF_ALLOC = CF_OFF_TAB + CF_TAB_PAIRS * 4 + 1024;
+static_assert(CF_ALLOC <= 232448, "shared memory budget");
+constexpr int CF_UNP0 = 4, CF_PROD = 8, CF_WAIT = 9, CF_MMA = 10, CF_NT = 32 * 11;
+constexpr int CF_HANDOFF_BAR = 1, CF_EPI_BAR = 2;
+constexpr uint32_t CF_SF_COL = 480;                // TMEM columns [480, 512): block scales (every byte 2^1)
+constexpr uint32_t CF_ACC0 = 0x4B400000u;          // fp32 1.5 * 2^23: the accumulators' integer origin
+
+__host__ __device__ constexpr uint32_t cf_idesc(int M, int N) {   // kind::mxf4, e2m1 x e2m1, ue8m0, K-major
+    return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+
+DG_DEV void cf_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t sfa, uint32_t sfb) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], %1, %2, %3, [%4], [%5], 1;\n\t}" ::"r"(d),
+        "l"(a), "l"(b), "r"(idesc), "r"(sfa), "r"(sfb)
+        : "memory");
+}
+
+struct CfDiv {
+    uint32_t m, s;
+};
+inline CfDiv cf_div(uint32_t d) {
+    uint32_t s = 0;
+    while ((1ull << s) < d) ++s;
+    return CfDiv{(uint32_t)((((1ull << s) - d) << 32) / d + 1), s};
+}
+DG_DEV uint32_t cf_fdiv(uint32_t n, CfDiv f) { return (__umulhi(n, f.m) + n) >> f.s; }
+
+struct CfArgs {
+    int64_t np, nq;              // output pixels (rows), output channels (columns)
+    int32_t nstages, last_ksteps, ntp, ntq, ntiles;
+    int32_t direct;              // 1: 1x1 / stride 1: the NHWC tensor is the im2col matrix (TMA slots)
+    // implicit im2col (direct == 0): x [B][H][W][Cb] packed, Cb = C/4 a power of two >= 16
+    const uint8_t *X;
+    int32_t H, W, Cb_log2, kw, kw_recip, stride, pad, Ho, Wo, kb;
+    const uint8_t *padsrc;       // 16 bytes of the pad code, then 16 zero bytes (beyond K)
+    CfDiv fd_wo, fd_ho;
+    void *D;
+    int64_t ldd;
+    int32_t has_rq, early_b;
+    // 16-bit SIMD requant (host-verified, f16_params): x = clamp(acc + negA, 0, W), code = (x m + c) >> 14
+    uint32_t f16_m, f16_c2, f16_w2, f16_na2;
+    int32_t f16_tab, f16_thr0m1, f16_accmax;
+};
+
+__device__ __align__(16) uint8_t g_cf_pad[4][32];
+
+__global__ void __launch_bounds__(CF_NT, 1)
+lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
+                   const __grid_constant__ CfArgs fa, const __grid_constant__ RequantArgs rq) {
+    extern __shared__ uint8_t smem_raw[];
+    uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+    const uint32_t sbase = ptx::smem_u32(smem);
+    const uint32_t bar0 = sbase + CF_OFF_BAR;
+    auto full_p = [&](int s) { return bar0 + 8 * s; };
+    auto empty_p = [&](int s) { return bar0 + 8 * (CF_SP + s); };
+    auto full_b = [&](int s) { return bar0 + 8 * (2 * CF_SP + s); };
+    auto empty_b = [&](int s) { return bar0 + 8 * (2 * CF_SP + CF_SB + s); };
+    auto full_a = [&](int s) { return bar0 + 8 * (2 * CF_SP + 2 * CF_SB + s); };
+    auto empty_a = [&](int s) { return bar0 + 8 * (2 * CF_SP + 2 * CF_SB + CF_SA + s); };
+    auto acc_full = [&](int a) { return bar0 + 8 * (2 * CF_SP + 2 * CF_SB + 2 * CF_SA + a); };
+    auto acc_empty = [&](int a) { return bar0 + 8 * (2 * CF_SP + 2 * CF_SB + 2 * CF_SA + CF_NACC + a); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + CF_OFF_TMEM);
+    uint32_t *tab = reinterpret_cast<uint32_t *>(smem + CF_OFF_TAB);
+    volatile uint32_t *f16_bad = reinterpret_cast<volatile uint32_t *>(smem + CF_OFF_TMEM + 8);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int ntiles = fa.ntiles;
+    if (threadIdx.x == 0) *f16_bad = 0u;
+
+    if (warp == CF_PROD) {
+        if (lane == 0) {
+            if (fa.direct) ptx::tma_prefetch(&tm_p);
+            ptx::tma_prefetch(&tm_b);
+            for (int s = 0; s < CF_SP; ++s) {
+                ptx::mbar_init(full_p(s), 1);
+                ptx::mbar_init(empty_p(s), 4);   // the 4 unpack warps, once per slot
+            }
+            for (int s = 0; s < CF_SB; ++s) {
+                ptx::mbar_init(full_b(s), 1);
+                ptx::mbar_init(empty_b(s), 1);
+            }
+            for (int s = 0; s < CF_SA; ++s) {
+                ptx::mbar_init(full_a(s), 4);
+                ptx::mbar_init(empty_a(s), 1);
+            }
+            for (int a = 0; a < CF_NACC; ++a) {
+                ptx::mbar_init(acc_full(a), 1);
+                ptx::mbar_init(acc_empty(a), 4);
+            }
+            ptx::fence_mbar_init();
+        }
+        __syncwarp();
+        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+    if (warp < 4) {
+        // block scales (every byte 2^1: D = sum (a/2 * 2)(v/2 * 2)) and the accumulators' origin
+        const uint32_t lanes = (uint32_t)(warp * 32) << 16;
+        uint32_t r[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = 0x80808080u;
+        ptx::tmem_st_32x32b_x32(tmem + CF_SF_COL + lanes, r);
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = CF_ACC0;
+#pragma unroll
+        for (int c = 0; c < CF_NACC * CF_BN / 32; ++c) ptx::tmem_st_32x32b_x32(tmem + (uint32_t)(c * 32) + lanes, r);
+        ptx::tmem_st_wait();
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+    if (threadIdx.x == 0) ptx::griddep_launch_dependents();
+
+    if (warp == CF_PROD) {
+        // (weights are read before the programmatic-dependent-launch wait only under early_weights)
+        if (!fa.early_b || fa.direct) ptx::griddep_wait();
+        uint32_t gp = 0, gb = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            const int tq = t % fa.ntq, tp = t / fa.ntq;
+            for (int s = 0; s < fa.nstages; ++s, ++gb) {
+                if (fa.direct && (s & 1) == 0) {   // a packed slot = 2 stages of every pixel row
+                    const int ps = (int)(gp % CF_SP);
+                    ptx::mbar_wait(empty_p(ps), ((gp / CF_SP) & 1u) ^ 1u);
+                    if (lane == 0) {
+                        ptx::mbar_arrive_expect_tx(full_p(ps), (uint32_t)CF_P_SLOT);
+                        ptx::tma_load_2d(sbase + CF_OFF_P + ps * CF_P_SLOT, &tm_p, full_p(ps), s * (CF_KST / 4), tp * CF_BM);
+                    }
+                    __syncwarp();
+                    ++gp;
+                }
+                const int bs = (int)(gb % CF_SB);
+                ptx::mbar_wait(empty_b(bs), ((gb / CF_SB) & 1u) ^ 1u);
+                if (lane == 0) {
+                    ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)CF_B_STAGE);
+                    ptx::tma_load_2d(sbase + CF_OFF_B + bs * CF_B_STAGE, &tm_b, full_b(bs), s * (CF_KST / 2), tq * CF_BN);
+                }
+                __syncwarp();
+            }
+        }
+    } else if (warp == CF_WAIT) {
+        uint32_t g = 0, tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            ptx::mbar_wait(acc_empty(tl % CF_NACC), ((tl / CF_NACC) & 1u) ^ 1u);
+            for (int s = 0; s < fa.nstages; ++s, ++g) {
+                ptx::mbar_wait(full_a(g % CF_SA), (g / CF_SA) & 1u);
+                ptx::mbar_wait(full_b(g % CF_SB), (g / CF_SB) & 1u);
+                ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
+            }
+        }
+    } else if (warp == CF_MMA) {
+        constexpr uint32_t idesc = cf_idesc(CF_BM, CF_BN);
+        const uint32_t sfa = tmem + CF_SF_COL, sfb = tmem + CF_SF_COL + 16;
+        const int nst = fa.nstages, lastk = fa.last_ksteps;   // (in registers before any MMA is queued)
+        uint32_t g = 0, tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const uint32_t acc = tl % CF_NACC;
+            const uint32_t dt = tmem + acc * CF_BN;
+            for (int s = 0; s < nst; ++s, ++g) {
+                const int sa = (int)(g % CF_SA), bs = (int)(g % CF_SB);
+                ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
+                ptx::tc_fence_after();
+                const uint64_t ad = ptx::desc_k_sw128(sbase + CF_OFF_A + sa * CF_A_STAGE);
+                const uint64_t bd = ptx::desc_k_sw128(sbase + CF_OFF_B + bs * CF_B_STAGE);
+                if (s < nst - 1) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) cf_mma(dt, ad + 2 * k, bd + 2 * k, idesc, sfa, sfb);
+                } else {
+                    for (int k = 0; k < lastk; ++k) cf_mma(dt, ad + 2 * k, bd + 2 * k, idesc, sfa, sfb);
+                }
+                ptx::mma_commit_warp(empty_a(sa));
+                ptx::mma_commit_warp(empty_b(bs));
+                if (s == nst - 1) ptx::mma_commit_warp(acc_full(acc));
+                __syncwarp();
+            }
+        }
+    } else if (warp >= CF_UNP0) {
+        // thread = pixel row r of the tile: 64 packed bytes (256 codes) per stage -> 32 words of e2m1
+        // nibbles (x & 0x33333333, (x >> 2) & 0x33333333 per packed word) -> SW128 K-major A stage
+        ptx::griddep_wait();
+        const int r = (warp - CF_UNP0) * 32 + lane;
+        uint32_t g = 0, gp = 0;
+        // implicit gather cursor: work item gt, stage gs of the next fetch; this row's pixel
+        int gt = blockIdx.x, gs = 0;
+        const uint8_t *img = fa.X;
+        int32_t h0 = 0, w0 = 0;
+        auto pixel = [&]() {
+            const int64_t p = (int64_t)(gt / fa.ntq) * CF_BM + r;
+            const uint32_t pp = (uint32_t)(p < fa.np ? p : fa.np - 1);
+            const uint32_t tt = cf_fdiv(pp, fa.fd_wo), b = cf_fdiv(tt, fa.fd_ho);
+            img = fa.X + (((int64_t)b * fa.H * fa.W) << fa.Cb_log2);
+            h0 = (int32_t)(tt - b * (uint32_t)fa.Ho) * fa.stride - fa.pad;
+            w0 = (int32_t)(pp - tt * (uint32_t)fa.Wo) * fa.stride - fa.pad;
+        };
+        const uint32_t ring = sbase + CF_OFF_P + (uint32_t)(r * 64);
+        auto fetch = [&](int slot) {   // the cursor's stage -> ring slot; advance the cursor
+            if (gt < ntiles) {
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const int32_t byte = gs * 64 + 16 * c;
+                    const int32_t tap = byte >> fa.Cb_log2, off = byte & ((1 << fa.Cb_log2) - 1);
+                    const int32_t rr = (tap * fa.kw_recip) >> 16, ss = tap - rr * fa.kw;
+                    const int32_t hi = h0 + rr, wi = w0 + ss;
+                    const uint8_t *src = byte >= fa.kb ? fa.padsrc + 16
+                                         : ((uint32_t)hi < (uint32_t)fa.H && (uint32_t)wi < (uint32_t)fa.W)
+                                               ? img + ((((int64_t)hi * fa.W + wi) << fa.Cb_log2) + off)
+                                               : fa.padsrc;
+                    ptx::cp_async16(ring + (uint32_t)(slot * CF_RING) + ((c ^ ((r >> 1) & 3)) << 4), src);
+                }
+                if (++gs == fa.nstages) {
+                    gs = 0;
+                    gt += gridDim.x;
+                    if (gt < ntiles) pixel();
+                }
+            }
+            ptx::cp_async_commit();
+        };
+        if (!fa.direct) {
+            if (gt < ntiles) pixel();
+            for (int i = 0; i < CF_IG; ++i) fetch(i);
+        }
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+            for (int s = 0; s < fa.nstages; ++s, ++g) {
+                uint4 v[4];
+                if (fa.direct) {
+                    const int ps = (int)(gp % CF_SP), sub = s & 1;
+                    if (sub == 0) ptx::mbar_wait(full_p(ps), (gp / CF_SP) & 1u);
+                    const uint32_t pbase = sbase + CF_OFF_P + ps * CF_P_SLOT;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {   // SW128 slot: 16-byte unit XOR row bits
+                        const uint32_t lin = (uint32_t)(r * 128 + sub * 64 + 16 * c);
+                        v[c] = ptx::lds128(pbase + (lin ^ (((lin >> 7) & 7u) << 4)));
+                    }
+                    if (sub == 1 || s == fa.nstages - 1) {   // this warp is done with the slot
+                        __syncwarp();
+                        if (lane == 0) ptx::mbar_arrive(empty_p(ps));
+                        ++gp;
+                    }
+                } else {
+                    ptx::cp_async_wait<CF_IG - 1>();   // this stage's copies (the oldest group) landed
+                    const int slot = (int)(g % CF_IG);
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        v[c] = ptx::lds128(ring + (uint32_t)(slot * CF_RING) + ((c ^ ((r >> 1) & 3)) << 4));
+                    fetch(slot);   // values are in registers: refill the slot CF_IG stages ahead
+                }
+                uint32_t e[32];
+#pragma unroll
+                for (int c = 0; c < 4; ++c) {
+                    const uint32_t w[4] = {v[c].x, v[c].y, v[c].z, v[c].w};
+#pragma unroll
+                    for (int i = 0; i < 4; ++i) {
+                        e[8 * c + 2 * i] = w[i] & 0x33333333u;
+                        e[8 * c + 2 * i + 1] = (w[i] >> 2) & 0x33333333u;
+                    }
+                }
+                const int sa = (int)(g % CF_SA);
+                ptx::mbar_wait(empty_a(sa), ((g / CF_SA) & 1u) ^ 1u);
+                // SW128 K-major A stage: row r at (r/8)*1024 + (r%8)*128, 16-byte chunk j at (j ^ (r%8))*16
+                const uint32_t row = sbase + CF_OFF_A + sa * CF_A_STAGE + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+#pragma unroll
+                for (int j = 0; j < 8; ++j)
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row + (uint32_t)(((j ^ (r & 7)) << 4))),
+                                 "r"(e[4 * j]), "r"(e[4 * j + 1]), "r"(e[4 * j + 2]), "r"(e[4 * j + 3])
+                                 : "memory");
+                ptx::fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(full_a(sa));
+            }
+        }
+    } else {
+        // ---------------- epilogue (lane quarter = warp)
+        const int quarter = warp;
+        if (!fa.early_b) ptx::griddep_wait();   // (the bias may come from the previous kernel)
+        if (fa.has_rq && fa.f16_tab) {   // per-column 16-bit offsets: negA = bias - (thr0 - 1)
+            uint32_t bad = 0;
+            for (int i = threadIdx.x; i < (int)(fa.nq >> 1); i += 128) {
+                const int64_t n0 = (int64_t)__ldg(rq.bias + 2 * i) - fa.f16_thr0m1;
+                const int64_t n1 = (int64_t)__ldg(rq.bias + 2 * i + 1) - fa.f16_thr0m1;
+                if ((n0 < 0 ? -n0 : n0) + fa.f16_accmax > 32767 || (n1 < 0 ? -n1 : n1) + fa.f16_accmax > 32767) bad = 1;
+                tab[i] = ((uint32_t)n0 & 0xFFFFu) | ((uint32_t)n1 << 16);
+            }
+            if (bad) *f16_bad = 1u;   // some offset overflows int16: every tile takes the exact path
+            ptx::named_bar_sync(CF_EPI_BAR, 128);
+        }
+        const bool f16_ok = fa.has_rq && *f16_bad == 0u;
+        ptx::griddep_wait();
+        const uint32_t tabs = sbase + CF_OFF_TAB;
+        uint32_t origin[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) origin[j] = CF_ACC0;
+        uint32_t tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const int tq = t % fa.ntq, tp = t / fa.ntq;
+            const int64_t p = (int64_t)tp * CF_BM + quarter * 32 + lane;
+            const int64_t q0 = (int64_t)tq * CF_BN;
+            const uint32_t acc = tl % CF_NACC;
+            ptx::mbar_wait(acc_full(acc), (tl / CF_NACC) & 1u);
+            ptx::tc_fence_after();
+            const uint32_t trow = tmem + acc * CF_BN + ((uint32_t)(quarter * 32) << 16);
+            if (f16_ok && q0 + CF_BN <= fa.nq) {
+                uint32_t r16[2][32];   // all 128 columns as 16-bit pairs (low halves = the integer values)
+                ptx::tmem_ld_32x32b_x32_pack16(trow, r16[0]);
+                ptx::tmem_ld_32x32b_x32_pack16(trow + 64, r16[1]);
+                ptx::tmem_ld_wait();
+#pragma unroll
+                for (int c = 0; c < 4; ++c) ptx::tmem_st_32x32b_x32(trow + 32 * c, origin);   // reset to the origin
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
+                if (p < fa.np) {
+#pragma unroll
+                    for (int hh = 0; hh < 4; ++hh) {
+                        const int64_t qc = q0 + hh * 32;
+                        uint32_t na[16];
+                        if (fa.f16_tab) {
+#pragma unroll
+                            for (int j = 0; j < 4; ++j) {
+                                const uint4 t4 = ptx::lds128(tabs + (uint32_t)(qc >> 1) * 4u + 16 * j);
+                                na[4 * j] = t4.x; na[4 * j + 1] = t4.y; na[4 * j + 2] = t4.z; na[4 * j + 3] = t4.w;
+                            }
+                        } else {
+#pragma unroll
+                            for (int j = 0; j < 16; ++j) na[j] = fa.f16_na2;
+                        }
+                        uint32_t rr[16];
+#pragma unroll
+                        for (int j = 0; j < 16; ++j) rr[j] = r16[hh >> 1][16 * (hh & 1) + j];
+                        const uint2 o = requant16_32(rr, na, fa.f16_w2, fa.f16_m, fa.f16_c2);
+                        uint8_t *dp = reinterpret_cast<uint8_t *>(fa.D) + p * fa.ldd + (qc >> 2);
+                        if ((reinterpret_cast<uintptr_t>(dp) & 7) == 0) *reinterpret_cast<uint2 *>(dp) = o;
+                        else store_codes32_ts(dp, o.x, o.y, 8);
+                    }
+                }
+            } else {   // int32 output, or the ragged last column tile with requant (exact 64-bit path)
+#pragma unroll 1
+                for (int c = 0; c < CF_BN / 32; ++c) {
+                    uint32_t v[32];
+                    ptx::tmem_ld_32x32b_x32(trow + 32 * c, v);
+                    ptx::tmem_ld_wait();
+                    ptx::tmem_st_32x32b_x32(trow + 32 * c, origin);
+                    const int64_t qc = q0 + c * 32;
+                    if (p >= fa.np || qc >= fa.nq) continue;
+                    int32_t a[32];
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) a[j] = (int32_t)(v[j] - CF_ACC0);
+                    if (!fa.has_rq) {
+                        int32_t *dp = reinterpret_cast<int32_t *>(fa.D) + p * fa.ldd + qc;
+                        if (qc + 32 <= fa.nq && (reinterpret_cast<uintptr_t>(dp) & 15) == 0) {
+#pragma unroll
+                            for (int j = 0; j < 32; j += 4) *reinterpret_cast<int4 *>(dp + j) = make_int4(a[j], a[j + 1], a[j + 2], a[j + 3]);
+                        } else {
+                            for (int j = 0; j < 32; ++j)
+                                if (qc + j < fa.nq) dp[j] = a[j];
+                        }
+                    } else {
+                        uint32_t o0 = 0, o1 = 0;
+#pragma unroll
+                        for (int j = 0; j < 32; ++j)
+                            if (qc + j < fa.nq) {
+                                const uint32_t cd = requant_one(rq, a[j], p, qc + j);
+                                if (j < 16) o0 |= cd << (2 * j);
+                                else o1 |= cd << (2 * (j - 16));
+                            }
+                        store_codes32_ts(reinterpret_cast<uint8_t *>(fa.D) + p * fa.ldd + (qc >> 2), o0, o1,
+                                         (int)((fa.nq - qc + 3) / 4 < 8 ? (fa.nq - qc + 3) / 4 : 8));
+                    }
+                }
+                ptx::tmem_st_wait();
+                ptx::tc_fence_before();
+                __syncwarp();
+                if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
+            }
+        }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();
+    if (warp == CF_PROD) ptx::tmem_dealloc(tmem, 512);
+}
+
+typedef CUresult (*CfEncode)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                             const cuuint64_t *, const cuuint32_t *, const cuuint32_t *, CUtensorMapInterleave,
+                             CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+bool cf_map(CUtensorMap *m, const void *base, int64_t row_bytes, int64_t ld, int64_t rows, int box_rows) {
+    static CfEncode fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<CfEncode>(p);
+    }
+    if (!fn) return false;
+    cuuint64_t dims[2] = {(cuuint64_t)row_bytes, (cuuint64_t)rows};
+    cuuint64_t strides[1] = {(cuuint64_t)ld};
+    cuuint32_t box[2] = {128, (cuuint32_t)box_rows}, estr[2] = {1, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<void *>(base), dims, strides, box, estr,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+const uint8_t *cf_pad_source(int pad_code) {
+    static const uint8_t *base = nullptr;
+    if (!base) {
+        uint8_t h[4][32] = {};
+        for (int c = 0; c < 4; ++c)
+            for (int i = 0; i < 16; ++i) h[c][i] = (uint8_t)(c | (c << 2) | (c << 4) | (c << 6));
+        if (cudaMemcpyToSymbol(g_cf_pad, h, sizeof(h)) != cudaSuccess) return nullptr;
+        void *p = nullptr;
+        if (cudaGetSymbolAddress(&p, g_cf_pad) != cudaSuccess) return nullptr;
+        base = reinterpret_cast<const uint8_t *>(p);
+    }
+    return base + 32 * (pad_code & 3);
+}
+
+}  // namespace
+
+// Conv (or a 1x1 conv = GEMM in the conv orientation) on the FP4 path.  x: NHWC packed [B][H][W][C/4];
+// w4: e2m1 weights [Cout][ld4] (dg_expand_operand_f4 of the packed weights, K order (r, s, c));
+// out: int32 [pixels][Cout] or, with rq, packed codes [pixels][Cout/4].  Returns DG_ERR_UNSUPPORTED
+// for what this kernel does not cover (the caller then runs the int8 tensor-core path):
+// residuals, bias per row, requant parameters without a 16-bit form, channel counts whose taps are
+// not 16-byte power-of-two chunks.
+dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const TsConv &cv, int64_t rows, int64_t cout,
+                      int64_t K, int64_t acc_bound, void *out, int64_t ldd, const RequantArgs *rq, cudaStream_t st,
+                      bool b_prepared) {
+    if (rq && (rq->res || rq->res_codes || (rq->bias && rq->bias_axis != 0) || rq->dir <= 0)) return DG_ERR_UNSUPPORTED;
+    if (cout > 2 * CF_TAB_PAIRS || rows >= ((int64_t)1 << 31)) return DG_ERR_UNSUPPORTED;
+    const bool direct = cv.kh == 1 && cv.kw == 1 && cv.stride == 1 && cv.pad == 0;
+    const int32_t cb = cv.Cb;
+    if (!direct && !(cb >= 16 && (cb & (cb - 1)) == 0 && cv.kh * cv.kw <= 64)) return DG_ERR_UNSUPPORTED;
+    if (direct && (cb % 16 || ((uintptr_t)x & 15))) return DG_ERR_UNSUPPORTED;
+    CfArgs fa{};
+    fa.np = rows;
+    fa.nq = cout;
+    fa.nstages = (int32_t)((K + CF_KST - 1) / CF_KST);
+    fa.last_ksteps = (int32_t)(((K - (int64_t)(fa.nstages - 1) * CF_KST) + 63) / 64);
+    fa.ntp = (int32_t)((rows + CF_BM - 1) / CF_BM);
+    fa.ntq = (int32_t)((cout + CF_BN - 1) / CF_BN);
+    const int64_t nt = (int64_t)fa.ntp * fa.ntq;
+    if (nt > INT32_MAX) return DG_ERR_SHAPE;
+    fa.ntiles = (int32_t)nt;
+    fa.direct = direct ? 1 : 0;
+    fa.X = x;
+    fa.H = cv.H;
+    fa.W = cv.W;
+    int lg = 0;
+    while ((1 << lg) < cb) ++lg;
+    fa.Cb_log2 = lg;
+    fa.kw = cv.kw;
+    fa.kw_recip = (65536 + cv.kw - 1) / cv.kw;
+    fa.stride = cv.stride;
+    fa.pad = cv.pad;
+    fa.Ho = cv.Ho;
+    fa.Wo = cv.Wo;
+    fa.kb = cv.kh * cv.kw * cb;
+    fa.padsrc = cf_pad_source(cv.pad_code);
+    if (!fa.padsrc) return DG_ERR_CUDA;
+    fa.fd_wo = cf_div((uint32_t)cv.Wo);
+    fa.fd_ho = cf_div((uint32_t)cv.Ho);
+    fa.D = out;
+    fa.ldd = ldd;
+    fa.has_rq = rq ? 1 : 0;
+    fa.early_b = (b_prepared && opt(OPT_EARLY_WEIGHTS)) ? 1 : 0;
+    if (rq) {   // the 16-bit SIMD requant (reading Q23) is the only requant form of this kernel
+        const int64_t *t = rq->thr;
+        uint32_t m16 = 0, c16 = 0;
+        if (!(acc_bound <= 32767 && t[0] > -((int64_t)1 << 30) && t[2] < ((int64_t)1 << 30) && (cout >> 1) <= CF_TAB_PAIRS &&
+              opt(OPT_F16) && f16_params(t[0], t[1], t[2], m16, c16)))
+            return DG_ERR_UNSUPPORTED;
+        const int64_t thr0m1 = t[0] - 1;
+        fa.f16_accmax = (int32_t)acc_bound;
+        if (rq->bias) {   // per-column offsets, range-checked by the kernel when it builds their table
+            fa.f16_tab = 1;
+        } else {
+            const int64_t n = -thr0m1;
+            if ((n < 0 ? -n : n) + acc_bound > 32767) return DG_ERR_UNSUPPORTED;
+            fa.f16_na2 = ((uint32_t)n & 0xFFFFu) * 0x10001u;
+        }
+        fa.f16_m = m16;
+        fa.f16_c2 = c16 * 0x10001u;
+        fa.f16_w2 = (uint32_t)(t[2] - t[0] + 1) * 0x10001u;
+        fa.f16_thr0m1 = (int32_t)thr0m1;
+    }
+    CUtensorMap mp, mb;
+    memset(&mp, 0, sizeof(mp));
+    if (direct && !cf_map(&mp, x, cb, cb, rows, CF_BM)) return DG_ERR_CUDA;
+    if (!cf_map(&mb, w4, ld4, ld4, cout, CF_BN)) return DG_ERR_CUDA;
+    static bool attr = false;
+    if (!attr) {
+        if (cudaFuncSetAttribute(lut_conv_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CF_ALLOC) != cudaSuccess)
+            return DG_ERR_CUDA;
+        attr = true;
+    }
+    RequantArgs dummy{};
+    const RequantArgs rqv = rq ? *rq : dummy;
+    const int grid = (int)(nt < num_sms() ? nt : num_sms());
+    cudaLaunchConfig_t lc = {};
+    lc.gridDim = dim3((unsigned)grid);
+    lc.blockDim = dim3((unsigned)CF_NT);
+    lc.dynamicSmemBytes = CF_ALLOC;
+    lc.stream = st;
+    cudaLaunchAttribute la[1];
+    la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    la[0].val.programmaticStreamSerializationAllowed = opt(OPT_PDL) ? 1 : 0;
+    lc.attrs = la;
+    lc.numAttrs = 1;
+    if (cudaLaunchKernelEx(&lc, lut_conv_f4_kernel, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
+    char tag[96];
+    snprintf(tag, sizeof(tag), "f4conv bn=128 nacc=3 direct=%d rq=%d tab=%d early=%d", fa.direct, fa.has_rq, fa.f16_tab,
+             fa.early_b);
+    set_last_kernel(tag);
+    return launch_status();
+}
+
+}  // namespace dg

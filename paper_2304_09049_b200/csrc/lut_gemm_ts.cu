@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "tc_ptx.cuh"
+#include "requant16.cuh"
 #include "unpack.cuh"
 
 namespace dg {
@@ -333,30 +334,6 @@ struct GatherCursor {
         ptx::cp_async_commit();
     }
 };
-
-DG_DEV void store_codes32_ts(uint8_t *dp, uint32_t o0, uint32_t o1, int nbytes) {
-#pragma unroll
-    for (int b = 0; b < 8; ++b)
-        if (b < nbytes) dp[b] = (uint8_t)((b < 4 ? o0 : o1) >> (8 * (b & 3)));
-}
-
-// 16-bit SIMD requant of 32 columns (S7; the exact threshold map of reading Q23 written as one
-// clamp + one multiply-add per column PAIR).  r[i] = columns 2i | 2i+1 (tcgen05.ld pack::16b),
-// na[i] = their offsets.  The code of lane j ends in bits [14,16) of that lane; PRMT gathers the
-// four codes of 4 consecutive columns into the top bits of 4 bytes, a masked multiply by
-// 2^18+2^12+2^6+1 moves them into the top byte in LSB-first order (the cross terms land below
-// bit 24 without overlapping, or above bit 31), and two PRMT levels assemble 16 columns per word.
-DG_DEV uint2 requant16_32(const uint32_t (&r)[16], const uint32_t (&na)[16], uint32_t w2, uint32_t m, uint32_t c2) {
-    uint32_t y[16];
-#pragma unroll
-    for (int i = 0; i < 16; ++i) y[i] = __viaddmin_s16x2_relu(r[i], na[i], w2) * m + c2;
-    uint32_t u[8];
-#pragma unroll
-    for (int b = 0; b < 8; ++b) u[b] = (prmt_b32(y[2 * b], y[2 * b + 1], 0x7531u) & 0xC0C0C0C0u) * 0x41041u;
-    const uint32_t lo = prmt_b32(prmt_b32(u[0], u[1], 0x0073u), prmt_b32(u[2], u[3], 0x0073u), 0x5410u);
-    const uint32_t hi = prmt_b32(prmt_b32(u[4], u[5], 0x0073u), prmt_b32(u[6], u[7], 0x0073u), 0x5410u);
-    return make_uint2(lo, hi);
-}
 
 // int32 output / residual requant / ragged tail for one 32-column chunk of accumulator values
 __device__ __forceinline__ void ts_epilogue_values(const TsArgs &ta, const RequantArgs &rq, const int32_t (&v)[32], int64_t p,
@@ -1559,33 +1536,6 @@ bool make_map_sw128(CUtensorMap *m, const void *base, int64_t ld, int64_t rows, 
               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// 16-bit SIMD requant parameters.  With x = clamp(acc + bias - (t0 - 1), 0, W), W = t2 - t0 + 1,
-// the exact code is [x >= 1] + [x >= t1 - t0 + 1] + [x >= W]; find integers m, c with
-// floor((x*m + c) / 2^14) equal to it.  x*m + c is monotone in x, so matching at the threshold
-// boundaries suffices; the result is re-verified for every x in [0, W].
-bool f16_params(int64_t t0, int64_t t1, int64_t t2, uint32_t &m_out, uint32_t &c_out) {
-    const int64_t W = t2 - t0 + 1, X2 = t1 - t0 + 1;
-    if (W < 1 || W > 16383 || X2 < 1 || X2 > W) return false;
-    auto code = [&](int64_t x) { return (int64_t)(x >= 1) + (int64_t)(x >= X2) + (int64_t)(x >= W); };
-    const int64_t pts[7] = {0, 0, 1, X2 - 1, X2, W - 1, W};
-    for (int64_t m = 1; m * W < 65536; ++m) {
-        int64_t lo = 0, hi = 65535;
-        for (int i = 0; i < 7; ++i) {
-            const int64_t x = pts[i], k = code(x);
-            lo = lo > k * 16384 - x * m ? lo : k * 16384 - x * m;
-            hi = hi < (k + 1) * 16384 - 1 - x * m ? hi : (k + 1) * 16384 - 1 - x * m;
-        }
-        if (lo > hi) continue;
-        bool ok = true;
-        for (int64_t x = 0; x <= W && ok; ++x) ok = (x * m + lo) >> 14 == code(x) && x * m + lo < 65536;
-        if (!ok) continue;
-        m_out = (uint32_t)m;
-        c_out = (uint32_t)lo;
-        return true;
-    }
-    return false;
-}
-
 // extra all-gather destinations of the current lut_gemm_ts call (set there, read by launch_ts)
 thread_local int32_t *const *g_peers = nullptr;
 thread_local int32_t g_npeers = 0;
@@ -1821,6 +1771,33 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
 
 }  // namespace
 
+// 16-bit SIMD requant parameters.  With x = clamp(acc + bias - (t0 - 1), 0, W), W = t2 - t0 + 1,
+// the exact code is [x >= 1] + [x >= t1 - t0 + 1] + [x >= W]; find integers m, c with
+// floor((x*m + c) / 2^14) equal to it.  x*m + c is monotone in x, so matching at the threshold
+// boundaries suffices; the result is re-verified for every x in [0, W].
+bool f16_params(int64_t t0, int64_t t1, int64_t t2, uint32_t &m_out, uint32_t &c_out) {
+    const int64_t W = t2 - t0 + 1, X2 = t1 - t0 + 1;
+    if (W < 1 || W > 16383 || X2 < 1 || X2 > W) return false;
+    auto code = [&](int64_t x) { return (int64_t)(x >= 1) + (int64_t)(x >= X2) + (int64_t)(x >= W); };
+    const int64_t pts[7] = {0, 0, 1, X2 - 1, X2, W - 1, W};
+    for (int64_t m = 1; m * W < 65536; ++m) {
+        int64_t lo = 0, hi = 65535;
+        for (int i = 0; i < 7; ++i) {
+            const int64_t x = pts[i], k = code(x);
+            lo = lo > k * 16384 - x * m ? lo : k * 16384 - x * m;
+            hi = hi < (k + 1) * 16384 - 1 - x * m ? hi : (k + 1) * 16384 - 1 - x * m;
+        }
+        if (lo > hi) continue;
+        bool ok = true;
+        for (int64_t x = 0; x <= W && ok; ++x) ok = (x * m + lo) >> 14 == code(x) && x * m + lo < 65536;
+        if (!ok) continue;
+        m_out = (uint32_t)m;
+        c_out = (uint32_t)lo;
+        return true;
+    }
+    return false;
+}
+
 int64_t expand_ld(int64_t K) { return (K + KA - 1) / KA * KA; }
 
 dg_status expand_operand(const uint8_t *packed, int64_t rows, int64_t K, int64_t ld, const int32_t levels[4],
@@ -1888,7 +1865,9 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
     const int64_t tiles256 = ((np + BM - 1) / BM) * ((nq + 255) / 256);
     if (nq >= 256 && K >= bn256_k && (tiles256 >= num_sms() || K >= 24 * KA) && opt(OPT_BN256))
         return few(256) ? launch_ts<256, 4, 8, 128, false, false, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv, skws, skws_bytes)
-                        : launch_ts<256, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+               : opt(OPT_UNP) == 12 ? launch_ts<256, 4, 12, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv)
+               : opt(OPT_UNP) == 16 ? launch_ts<256, 4, 16, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv)
+                                    : launch_ts<256, 4, 8, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
 
     if (nq > 64 && !(short_k && opt(OPT_BN64_SHORT))) {
         if (short_k && !k256) return launch_ts<128, 8, 4, 128>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);

@@ -97,6 +97,7 @@ def lib():
             "dg_lut_conv2d_workspace_size": ([P], ctypes.c_size_t),
             "dg_lut_conv2d": ([P, P, P, P, P, P, P, ctypes.c_size_t, i32, P], i32),
             "dg_lut_conv2d_prepared": ([P, P, i64, P, P, P, P, P, ctypes.c_size_t, P], i32),
+            "dg_lut_conv2d_f4_prepared": ([P, P, i64, P, P, P, P, P], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -528,4 +529,22 @@ def lut_conv2d_prepared(x: torch.Tensor, w8: torch.Tensor, lut: dg_lut, p: dg_co
     _check(lib().dg_lut_conv2d_prepared(_ptr(x), _ptr(w8), w8.shape[1], ctypes.byref(lut), ctypes.byref(p),
                                         ctypes.byref(r) if r is not None else None, _ptr(out), _ptr(ws),
                                         ws.numel() if ws is not None else 0, _stream(stream)), "dg_lut_conv2d_prepared")
+    return out
+
+
+def lut_conv2d_f4_prepared(x: torch.Tensor, w4: torch.Tensor, lut: dg_lut, p: dg_conv_params,
+                           rq: Requant | None = None, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Conv on the FP4 (kind::mxf4) path with weights pre-expanded by expand_operand_f4(w, K, lut.wl)."""
+    _dev(x, torch.uint8, "x")
+    _dev(w4, torch.uint8, "w4")
+    Ho = (p.H + 2 * p.pad - p.kh) // p.stride + 1
+    Wo = (p.W + 2 * p.pad - p.kw) // p.stride + 1
+    rows = p.B * Ho * Wo
+    if out is None:
+        out = (torch.empty((rows, p.Cout // 4), dtype=torch.uint8, device=x.device) if rq is not None
+               else torch.empty((rows, p.Cout), dtype=torch.int32, device=x.device))
+    r = rq.c() if rq is not None else None
+    _check(lib().dg_lut_conv2d_f4_prepared(_ptr(x), _ptr(w4), w4.shape[1], ctypes.byref(lut), ctypes.byref(p),
+                                           ctypes.byref(r) if r is not None else None, _ptr(out), _stream(stream)),
+           "dg_lut_conv2d_f4_prepared")
     return out

@@ -41,6 +41,7 @@ class LayerPlan:
     direct: bool           # 1x1 / stride 1 / unpadded: the input is its own im2col matrix
     ops: int               # algorithmic 2*M*N*K with the unpadded K
     kernel: str = ""       # dg_last_kernel() tag of the GEMM instance the layer ran (last step)
+    w4: torch.Tensor | None = None   # e2m1 expansion of w (FP4 conv kernel), dg_expand_operand_f4
 
     @property
     def cols_ld(self) -> int:
@@ -51,6 +52,12 @@ class LayerPlan:
         """tc path gathers im2col rows on chip (dg_lut_conv2d_prepared): C/4 a power of two >= 16."""
         cb = self.params.C // 4
         return (not self.direct) and cb >= 16 and (cb & (cb - 1)) == 0 and self.layer.k * self.layer.k <= 64
+
+
+def f4_default(layer, Cp: int) -> bool:
+    """Layers the block-scaled FP4 conv kernel takes by default (measured per layer class,
+    DESIGN.md §6.4): none until measured."""
+    return False
 
 
 def input_codes(cfg: int, li: int, layer, images, device):
@@ -97,7 +104,9 @@ def pack_conv_weights(w: torch.Tensor, wpad_code: int = 2) -> torch.Tensor:
 
 
 class NetRunner:
-    def __init__(self, cfg: int, images, device="cuda", variant="auto", layers=None):
+    def __init__(self, cfg: int, images, device="cuda", variant="auto", layers=None, f4=None):
+        """f4: layer ids to run on the block-scaled FP4 conv kernel (dg_lut_conv2d_f4_prepared), or
+        None for the default selection f4_default(layer)."""
         s = _synth()
         self.cfg = cfg
         self.images = list(images)
@@ -127,6 +136,9 @@ class NetRunner:
             w8 = dg.expand_operand(wq, K, wl) if variant in ("auto", "tc") else None
             plan = LayerPlan(L.name, L, params, lut, lut_t, rq, wq, w8, xq, out, rows, K, direct,
                              2 * L.cout * rows * L.k * L.k * L.cin)
+            use_f4 = (li in f4) if f4 is not None else (variant == "auto" and f4_default(L, Cp))
+            if use_f4:
+                plan.w4 = dg.expand_operand_f4(wq, K, wl)
             ws_need = max(ws_need, dg.conv_workspace_size(params), (0 if direct else rows * plan.cols_ld),
                           dg.gemm_workspace_size(rows, L.cout, K))
             self.plans.append(plan)
@@ -139,8 +151,18 @@ class NetRunner:
         """One step: every layer, requantised codes into plan.out, or (int32_out = one int32
         [rows][Cout] buffer per layer) the raw accumulators of the same kernel instances."""
         n = 0
-        for i, p in enumerate(self.plans):
+            for i, p in enumerate(self.plans):
             L = p.layer
+            if p.w4 is not None:   # block-scaled FP4 conv kernel
+                if gemm_events is not None:
+                    gemm_events[i][0].record()
+                dg.lut_conv2d_f4_prepared(p.x, p.w4, p.lut, p.params, rq=None if int32_out else p.rq,
+                                          out=int32_out[i] if int32_out else p.out, stream=stream)
+                p.kernel = dg.last_kernel()
+                if gemm_events is not None:
+                    gemm_events[i][1].record()
+                n += 1
+                continue
             if p.w8 is not None and (p.direct or p.implicit):
                 # tensor-core path without an im2col matrix (direct 1x1 or implicit GEMM)
                 if gemm_events is not None:

@@ -898,3 +898,84 @@ def test_dispatch_instances_vs_oracle(np_, nq, K, opts, tags):
     assert np.array_equal(host(C), acc)
     exp = oracle.requantize(np.ascontiguousarray(acc), rq.mult, 20, 1, 0, 3, bias=bias, bias_axis=0)
     assert np.array_equal(oracle_codes_of(codes, np_, nq), exp)
+
+
+# ---- convolution on the block-scaled FP4 path (dg_lut_conv2d_f4_prepared) ----
+F4_CONVS = [  # B, H, W, C, Cout, k, stride, pad, pad_code
+    (2, 9, 9, 64, 128, 1, 1, 0, 0),      # direct 1x1 (TMA slots of the NHWC tensor), 64 channels
+    (3, 7, 7, 256, 256, 1, 1, 0, 0),     # direct, 2 column tiles
+    (1, 6, 5, 512, 200, 1, 1, 0, 0),     # direct, ragged Cout and rows
+    (2, 10, 10, 64, 128, 3, 1, 1, 0),    # implicit 3x3 gather, 4 taps per stage
+    (2, 9, 11, 128, 128, 3, 2, 1, 2),    # implicit stride 2, pad code 2
+    (1, 8, 8, 256, 384, 3, 1, 1, 1),     # implicit, 1 tap per stage, 3 column tiles, pad code 1
+    (2, 12, 12, 256, 128, 1, 2, 0, 0),   # implicit 1x1 stride 2 (downsample)
+    (1, 7, 7, 512, 136, 3, 1, 1, 3),     # ragged Cout, K = 4608
+]
+
+
+@pytest.mark.parametrize("wl", [(-2, -1, 0, 1), (-12, -3, 4, 8)])
+@pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", F4_CONVS)
+def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code):
+    """FP4 conv kernel vs O-CONV: int32 output, fused 16-bit requant with a per-channel bias, a
+    uniform-offset requant without bias, and a bias whose 16-bit offsets overflow (exact path)."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    wl = list(wl)
+    lut = dg.build_lut(wl, AL, 8)
+    T = oracle.build_lut16(wl, AL)
+    g = np.random.default_rng(B + H + W + C + Cout + k + pad_code + wl[0])
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, k, k, C), dtype=np.uint8)
+    exp = oracle.conv2d_direct(x, w, T, stride, pad, pad_code).reshape(-1, Cout)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    w4 = dg.expand_operand_f4(wp, k * k * Cp, wl)
+    p = dg.conv_params(B, H, W, Cp, Cout, k, k, stride, pad, pad_code, ldw=wp.shape[1])
+    out = dg.lut_conv2d_f4_prepared(xp, w4, lut, p)
+    assert dg.last_kernel().startswith("f4conv"), dg.last_kernel()
+    assert np.array_equal(host(out), exp)
+    if Cout % 4:
+        return
+    mu = int(np.round(exp.mean()))
+    bias = (-mu + g.integers(-40, 40, Cout)).astype(np.int32)
+    mult = max(1, int(round((1 << 20) * 1.2 / max(1.0, float(exp.std())))))
+    for b in (bias, None, np.full(Cout, 30000, np.int32)):
+        rq = dg.Requant(mult, 20, 1, 0, 3, bias=None if b is None else torch.from_numpy(b).to(DEV), bias_axis=0)
+        try:
+            codes = dg.lut_conv2d_f4_prepared(xp, w4, lut, p, rq=rq)
+        except dg.DGError as e:   # (no 16-bit form of these parameters: the caller takes the int8 path)
+            assert "UNSUPPORTED" in str(e)
+            continue
+        expc = oracle.requantize(exp, mult, 20, 1, 0, 3, bias=b, bias_axis=0)
+        assert np.array_equal(oracle_codes_of(codes, exp.shape[0], Cout), expc)
+
+
+def test_conv_f4_accumulator_origin_at_the_bound():
+    """The FP4 conv accumulates from 1.5 * 2^23: at the largest K the API admits (K * 36 < 2^22 for
+    weight level -12 and activation level 3), all-max products first then a random tail, positive and
+    negative sums must stay exact; one code more is refused."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    wl = [-12, -3, 4, 8]
+    lut = dg.build_lut(wl, AL, 8)
+    T = oracle.build_lut16(wl, AL)
+    K = ((1 << 22) - 1) // 36 // 64 * 64          # 1x1 conv over K channels
+    B, H, W, Cout = 1, 1, 5, 128
+    g = np.random.default_rng(9)
+    x = g.integers(0, 4, (B, H, W, K), dtype=np.uint8)
+    x[0, 0, :3, : K - 64] = 3
+    w = g.integers(0, 4, (Cout, 1, 1, K), dtype=np.uint8)
+    w[::2, 0, 0, : K - 64] = 0                    # level -12 (negative extreme)
+    w[1::4, 0, 0, : K - 64] = 3                   # level 8
+    exp = oracle.conv2d_direct(x, w, T, 1, 0, 0).reshape(-1, Cout)
+    assert exp.min() < -(1 << 21) and exp.max() > (1 << 20)
+    xp, _ = nhwc_pack(x)
+    wp = conv_weights_pack(w, K)
+    w4 = dg.expand_operand_f4(wp, K, wl)
+    p = dg.conv_params(B, H, W, K, Cout, 1, 1, 1, 0, 0, ldw=wp.shape[1])
+    assert np.array_equal(host(dg.lut_conv2d_f4_prepared(xp, w4, lut, p)), exp)
+    K2 = K + 64 * 60
+    p2 = dg.conv_params(1, 1, 1, K2, 8, 1, 1, 1, 0, 0)
+    w2 = dg.expand_operand_f4(gpu_pack(np.zeros((8, K2), np.uint8), weights=True), K2, wl)
+    with pytest.raises(dg.DGError, match="OVERFLOW"):
+        dg.lut_conv2d_f4_prepared(gpu_pack(np.zeros((1, K2), np.uint8))[:, : K2 // 4].contiguous(), w2, lut, p2)

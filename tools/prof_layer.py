@@ -23,13 +23,15 @@ ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--reps", type=int, default=8)
 ap.add_argument("--opt", action="append", default=[])
 ap.add_argument("--sweep", default="")
+ap.add_argument("--f4", default="", help="comma-separated layer ids on the FP4 conv kernel ('all' = every layer given)")
 a = ap.parse_args()
 for o in a.opt:
     k, v = o.split("=")
     dg.set_option(k, int(v))
 batch = a.batch or (256 if a.cfg == 3 else 64)
 layers = [int(x) for x in a.layers.split(",")]
-r = netrun.NetRunner(a.cfg, range(batch), "cuda", layers=layers)
+f4 = None if not a.f4 else (set(layers) if a.f4 == "all" else {int(x) for x in a.f4.split(",")})
+r = netrun.NetRunner(a.cfg, range(batch), "cuda", layers=layers, f4=f4 if f4 is not None else set())
 sweep = [("", [None])]
 if a.sweep:
     k, vs = a.sweep.split("=")
