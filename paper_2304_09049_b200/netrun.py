@@ -151,7 +151,7 @@ class NetRunner:
         """One step: every layer, requantised codes into plan.out, or (int32_out = one int32
         [rows][Cout] buffer per layer) the raw accumulators of the same kernel instances."""
         n = 0
-            for i, p in enumerate(self.plans):
+        for i, p in enumerate(self.plans):
             L = p.layer
             if p.w4 is not None:   # block-scaled FP4 conv kernel
                 if gemm_events is not None:
