@@ -31,7 +31,7 @@ namespace {
 
 constexpr int CF_BM = 128, CF_BN = 128;
 constexpr int CF_KST = 256;                        // codes per stage: 128 bytes of e2m1 per row = 4 MMAs (K = 64)
-constexpr int CF_NACC = 3, CF_SA = 4, CF_SB = 6, CF_SP = 3, CF_IG = 6;
+constexpr int CF_NACC_MAX = 3, CF_SA_MAX = 6, CF_SB = 6, CF_SP = 3, CF_IG = 6;
 constexpr int CF_A_STAGE = CF_BM * CF_KST / 2;     // 16 KB, SW128 K-major
 constexpr int CF_B_STAGE = CF_BN * CF_KST / 2;     // 16 KB, SW128 K-major
 constexpr int CF_P_SLOT = CF_BM * 128;             // 16 KB: 512 packed codes of every row (2 stages)
@@ -40,9 +40,9 @@ constexpr int CF_P_REGION = CF_SP * CF_P_SLOT > CF_IG * CF_RING ? CF_SP * CF_P_S
 constexpr int CF_TAB_PAIRS = 1024;                 // per-column requant offsets: Cout <= 2048
 constexpr int CF_OFF_B = 0;
 constexpr int CF_OFF_A = CF_OFF_B + CF_SB * CF_B_STAGE;
-constexpr int CF_OFF_P = CF_OFF_A + CF_SA * CF_A_STAGE;
+constexpr int CF_OFF_P = CF_OFF_A + 4 * CF_A_STAGE;   // (shared-memory A: 4 stages)
 constexpr int CF_OFF_BAR = CF_OFF_P + CF_P_REGION;
-constexpr int CF_NBAR = 2 * CF_SP + 2 * CF_SB + 2 * CF_SA + 2 * CF_NACC;
+constexpr int CF_NBAR = 2 * CF_SP + 2 * CF_SB + 2 * CF_SA_MAX + 2 * CF_NACC_MAX;
 constexpr int CF_OFF_TMEM = CF_OFF_BAR + CF_NBAR * 8;
 constexpr int CF_OFF_TAB = (CF_OFF_TMEM + 16 + 15) / 16 * 16;
 constexpr int CF_ALLOC = CF_OFF_TAB + CF_TAB_PAIRS * 4 + 1024;
@@ -54,6 +54,17 @@ constexpr uint32_t CF_ACC0 = 0x4B400000u;          // fp32 1.5 * 2^23: the accum
 
 __host__ __device__ constexpr uint32_t cf_idesc(int M, int N) {   // kind::mxf4, e2m1 x e2m1, ue8m0, K-major
     return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+
+// A operand in tensor memory (TA): the unpacked e2m1 stage is written with tcgen05.st, 8 columns
+// (32 bytes = 64 nibbles of every row) per K = 64 step
+DG_DEV void cf_mma_ts(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t sfa, uint32_t sfb) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%4], [%5], 1;\n\t}" ::"r"(d),
+        "r"(a), "l"(b), "r"(idesc), "r"(sfa), "r"(sfb)
+        : "memory");
 }
 
 DG_DEV void cf_mma(uint32_t d, uint64_t a, uint64_t b, uint32_t idesc, uint32_t sfa, uint32_t sfb) {
@@ -94,9 +105,14 @@ struct CfArgs {
 
 __device__ __align__(16) uint8_t g_cf_pad[4][32];
 
+// TA: A stages in tensor memory (two accumulators, six 32-column A stages) instead of shared memory
+// (three accumulators, four 16 KB SW128 stages written with st.shared)
+template <bool TA>
 __global__ void __launch_bounds__(CF_NT, 1)
 lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CfArgs fa, const __grid_constant__ RequantArgs rq) {
+    constexpr int CF_NACC = TA ? 2 : 3, CF_SA = TA ? 6 : 4;
+    constexpr uint32_t TA0 = CF_NACC * CF_BN;   // first tensor-memory A column (TA)
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = ptx::smem_u32(smem);
@@ -213,11 +229,18 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 ptx::tc_fence_after();
                 const uint64_t ad = ptx::desc_k_sw128(sbase + CF_OFF_A + sa * CF_A_STAGE);
                 const uint64_t bd = ptx::desc_k_sw128(sbase + CF_OFF_B + bs * CF_B_STAGE);
+                const uint32_t at = tmem + TA0 + (uint32_t)(sa * 32);
                 if (s < nst - 1) {
 #pragma unroll
-                    for (int k = 0; k < 4; ++k) cf_mma(dt, ad + 2 * k, bd + 2 * k, idesc, sfa, sfb);
+                    for (int k = 0; k < 4; ++k) {
+                        if constexpr (TA) cf_mma_ts(dt, at + 8 * k, bd + 2 * k, idesc, sfa, sfb);
+                        else cf_mma(dt, ad + 2 * k, bd + 2 * k, idesc, sfa, sfb);
+                    }
                 } else {
-                    for (int k = 0; k < lastk; ++k) cf_mma(dt, ad + 2 * k, bd + 2 * k, idesc, sfa, sfb);
+                    for (int k = 0; k < lastk; ++k) {
+                        if constexpr (TA) cf_mma_ts(dt, at + 8 * k, bd + 2 * k, idesc, sfa, sfb);
+                        else cf_mma(dt, ad + 2 * k, bd + 2 * k, idesc, sfa, sfb);
+                    }
                 }
                 ptx::mma_commit_warp(empty_a(sa));
                 ptx::mma_commit_warp(empty_b(bs));
@@ -307,14 +330,21 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
                 const int sa = (int)(g % CF_SA);
                 ptx::mbar_wait(empty_a(sa), ((g / CF_SA) & 1u) ^ 1u);
-                // SW128 K-major A stage: row r at (r/8)*1024 + (r%8)*128, 16-byte chunk j at (j ^ (r%8))*16
-                const uint32_t row = sbase + CF_OFF_A + sa * CF_A_STAGE + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
+                if constexpr (TA) {   // row r = lane quarter (warp & 3) x 32 + lane: 32 columns of this stage
+                    ptx::tc_fence_after();
+                    ptx::tmem_st_32x32b_x32(tmem + TA0 + (uint32_t)(sa * 32) + ((uint32_t)((warp & 3) * 32) << 16), e);
+                    ptx::tmem_st_wait();
+                    ptx::tc_fence_before();
+                } else {
+                    // SW128 K-major A stage: row r at (r/8)*1024 + (r%8)*128, 16-byte chunk j at (j ^ (r%8))*16
+                    const uint32_t row = sbase + CF_OFF_A + sa * CF_A_STAGE + (uint32_t)((r >> 3) * 1024 + (r & 7) * 128);
 #pragma unroll
-                for (int j = 0; j < 8; ++j)
-                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row + (uint32_t)(((j ^ (r & 7)) << 4))),
-                                 "r"(e[4 * j]), "r"(e[4 * j + 1]), "r"(e[4 * j + 2]), "r"(e[4 * j + 3])
-                                 : "memory");
-                ptx::fence_proxy_async_smem();
+                    for (int j = 0; j < 8; ++j)
+                        asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(row + (uint32_t)(((j ^ (r & 7)) << 4))),
+                                     "r"(e[4 * j]), "r"(e[4 * j + 1]), "r"(e[4 * j + 2]), "r"(e[4 * j + 3])
+                                     : "memory");
+                    ptx::fence_proxy_async_smem();
+                }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(full_a(sa));
             }
@@ -541,11 +571,13 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     memset(&mp, 0, sizeof(mp));
     if (direct && !cf_map(&mp, x, cb, cb, rows, CF_BM)) return DG_ERR_CUDA;
     if (!cf_map(&mb, w4, ld4, ld4, cout, CF_BN)) return DG_ERR_CUDA;
-    static bool attr = false;
-    if (!attr) {
-        if (cudaFuncSetAttribute(lut_conv_f4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, CF_ALLOC) != cudaSuccess)
+    const bool ta = opt(OPT_F4_TA) != 0;
+    static bool attr[2] = {false, false};
+    if (!attr[ta]) {
+        if (cudaFuncSetAttribute(ta ? lut_conv_f4_kernel<true> : lut_conv_f4_kernel<false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, CF_ALLOC) != cudaSuccess)
             return DG_ERR_CUDA;
-        attr = true;
+        attr[ta] = true;
     }
     RequantArgs dummy{};
     const RequantArgs rqv = rq ? *rq : dummy;
@@ -560,10 +592,11 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     la[0].val.programmaticStreamSerializationAllowed = opt(OPT_PDL) ? 1 : 0;
     lc.attrs = la;
     lc.numAttrs = 1;
-    if (cudaLaunchKernelEx(&lc, lut_conv_f4_kernel, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
+    if (cudaLaunchKernelEx(&lc, ta ? lut_conv_f4_kernel<true> : lut_conv_f4_kernel<false>, mp, mb, fa, rqv) != cudaSuccess)
+        return DG_ERR_CUDA;
     char tag[96];
-    snprintf(tag, sizeof(tag), "f4conv bn=128 nacc=3 direct=%d rq=%d tab=%d early=%d", fa.direct, fa.has_rq, fa.f16_tab,
-             fa.early_b);
+    snprintf(tag, sizeof(tag), "f4conv bn=128 %s direct=%d rq=%d tab=%d early=%d", ta ? "ta nacc=2" : "sa nacc=3", fa.direct,
+             fa.has_rq, fa.f16_tab, fa.early_b);
     set_last_kernel(tag);
     return launch_status();
 }
