@@ -305,11 +305,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         const uint32_t lin = (uint32_t)(r * 128 + sub * 64 + 16 * c);
                         v[c] = ptx::lds128(pbase + (lin ^ (((lin >> 7) & 7u) << 4)));
                     }
-                    if (sub == 1 || s == fa.nstages - 1) {   // this warp is done with the slot
-                        __syncwarp();
-                        if (lane == 0) ptx::mbar_arrive(empty_p(ps));
-                        ++gp;
-                    }
+
                 } else {
                     ptx::cp_async_wait<CF_IG - 1>();   // this stage's copies (the oldest group) landed
                     const int slot = (int)(g % CF_IG);
@@ -327,6 +323,12 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         e[8 * c + 2 * i] = w[i] & 0x33333333u;
                         e[8 * c + 2 * i + 1] = (w[i] >> 2) & 0x33333333u;
                     }
+                }
+                // this warp is done with the slot once its loads have landed (release_after_loads: the
+                // TMA that refills the slot raced with outstanding loads, measured nondeterministic rows)
+                if (fa.direct && ((s & 1) == 1 || s == fa.nstages - 1)) {
+                    ptx::release_after_loads(empty_p((int)(gp % CF_SP)), 1u, v[0].x ^ v[1].x ^ v[2].x ^ v[3].x);
+                    ++gp;
                 }
                 const int sa = (int)(g % CF_SA);
                 ptx::mbar_wait(empty_a(sa), ((g / CF_SA) & 1u) ^ 1u);

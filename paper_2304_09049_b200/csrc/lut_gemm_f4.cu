@@ -214,11 +214,6 @@ lut_gemm_f4_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
                     const uint32_t lin = (uint32_t)(r * 128 + sub * 64 + 16 * c);
                     v[c] = ptx::lds128(pbase + (lin ^ (((lin >> 7) & 7u) << 4)));
                 }
-                if (sub == 1 || s == fa.nstages - 1) {   // this warp is done with the slot
-                    __syncwarp();
-                    if (lane == 0) ptx::mbar_arrive(empty_p(ps));
-                    ++gp;
-                }
                 uint32_t e[32];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -228,6 +223,12 @@ lut_gemm_f4_kernel(const __grid_constant__ CUtensorMap tm_a, const __grid_consta
                         e[8 * c + 2 * i] = w[i] & 0x33333333u;
                         e[8 * c + 2 * i + 1] = (w[i] >> 2) & 0x33333333u;
                     }
+                }
+                // release the slot only after its loaded values are used (an mbarrier arrive does not
+                // wait for outstanding shared-memory loads; the refilling TMA could overtake them)
+                if (sub == 1 || s == fa.nstages - 1) {
+                    ptx::release_after_loads(empty_p(ps), 1u, v[0].x ^ v[1].x ^ v[2].x ^ v[3].x);
+                    ++gp;
                 }
                 const int sa = (int)(g % F4_SA);
                 ptx::mbar_wait(empty_a(sa), ((g / F4_SA) & 1u) ^ 1u);

@@ -1104,11 +1104,6 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     v[b][0] = ptx::lds128(pbase + (lin ^ (((lin >> 7) & msk) << 4)));
                     v[b][1] = nch > 1 ? ptx::lds128(pbase + ((lin + 16) ^ ((((lin + 16) >> 7) & msk) << 4))) : make_uint4(0, 0, 0, 0);
                 }
-                __syncwarp();
-                if (lane == 0) {
-                    ptx::mbar_arrive_cnt(empty_p((int)(tl0 % (uint32_t)nsp)), (uint32_t)nsub);
-                    if (has1) ptx::mbar_arrive_cnt(empty_p((int)(tl1 % (uint32_t)nsp)), (uint32_t)nsub);
-                }
                 uint32_t a[2][32];
 #pragma unroll
                 for (int b = 0; b < 2; ++b)
@@ -1123,6 +1118,14 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                             a[b][16 * c + 4 * i + 3] = o.w;
                         }
                     }
+                // the slots are released only once their loaded values are USED: an mbarrier arrive
+                // does not wait for outstanding shared-memory loads, and the TMA / bulk copy that
+                // refills a slot after the arrive can overtake them (measured on the FP4 conv kernel)
+                {
+                    const uint32_t dep = v[0][0].x ^ v[0][1].x ^ v[1][0].x ^ v[1][1].x;
+                    ptx::release_after_loads(empty_p((int)(tl0 % (uint32_t)nsp)), (uint32_t)nsub, dep);
+                    if (has1) ptx::release_after_loads(empty_p((int)(tl1 % (uint32_t)nsp)), (uint32_t)nsub, dep);
+                }
 #pragma unroll
                 for (int b = 0; b < 2; ++b) {
                     const uint32_t tl = b ? tl1 : tl0;
@@ -1204,9 +1207,6 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         const uint32_t lin = lin0 + 16 * c;
                         v[c] = c < nchunk ? ptx::lds128(pbase + (lin ^ (((lin >> 7) & msk) << 4))) : make_uint4(0, 0, 0, 0);
                     }
-                    __syncwarp();
-                    if (lane == 0)   // this warp's share of the slot is consumed (+ the slot's unused stages)
-                        ptx::mbar_arrive_cnt(empty_p(slot), 1u + (s == se - 1 ? (uint32_t)(nsub - 1 - sub_) : 0u));
                 }
                 // unpack the whole stage into registers before waiting for the A buffer, so that the
                 // wait overlaps the ALU work (a[32 h + j]: 32-column half h)
@@ -1226,6 +1226,12 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     gc.issue<2 * C::HALVES>(ta, ring + (uint32_t)((consumed % IG_DEPTH) * BM * 64), r, ntiles, KST / 4);
                     gc.advance(ta, NUM_UGROUPS, r, ntiles);
                     ++consumed;
+                } else {   // this warp's share of the slot is consumed (+ the slot's unused stages); released
+                           // only after the values are used (see the one-stage path above)
+                    uint32_t dep = 0;
+#pragma unroll
+                    for (int c = 0; c < 2 * C::HALVES; ++c) dep ^= v[c].x;
+                    ptx::release_after_loads(empty_p(slot), 1u + (s == se - 1 ? (uint32_t)(nsub - 1 - sub_) : 0u), dep);
                 }
                 if (lane == 0 && quarter == 0) TS_EV(1, g);
                 ptx::mbar_wait(empty_a(sa), ((g / SA) & 1u) ^ 1u);   // MMA(g - SA) completed

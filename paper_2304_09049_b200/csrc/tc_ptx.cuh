@@ -29,6 +29,19 @@ DG_DEV void mbar_arrive(uint32_t bar) {
 DG_DEV void mbar_arrive_cnt(uint32_t bar, uint32_t count) {
     asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(count) : "memory");
 }
+// Release of a shared-memory buffer whose contents this WARP loaded into registers: an mbarrier
+// arrive does not wait for outstanding ld.shared (the scoreboard), and neither does __syncwarp, so
+// the TMA / bulk copy that refills the buffer after the arrive could overtake the loads (measured:
+// nondeterministic rows).  `dep` must be computed from the loaded registers (one word per load
+// instruction): every lane stores it to a scratch word, which cannot issue before its loads have
+// landed, and the warp barrier orders those stores before lane 0's (release) arrive.  (A register
+// dependency alone is removed by ptxas when its value is otherwise unused.)
+DG_DEV void release_after_loads(uint32_t bar, uint32_t count, uint32_t dep) {
+    __shared__ uint32_t s_dep_sink[32];
+    asm volatile("st.shared.u32 [%0], %1;" ::"r"(smem_u32(&s_dep_sink[(threadIdx.x >> 5) & 31])), "r"(dep) : "memory");
+    __syncwarp();
+    if ((threadIdx.x & 31) == 0) asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(count) : "memory");
+}
 DG_DEV void mbar_arrive_expect_tx(uint32_t bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
 }

@@ -61,14 +61,21 @@ def run_graphs(r):
         r.step()
     with torch.cuda.graph(g_acc):
         r.step(int32_out=acc)
-    for p in r.plans:
-        p.out.fill_(0xA5)
-    for a in acc:
-        a.fill_(-12345)
-    for _ in range(2):
+    first = None
+    for rep in range(3):   # every replay must reproduce the first bit for bit (a launch race would not)
+        for p in r.plans:
+            p.out.fill_(0xA5)
+        for a in acc:
+            a.fill_(-12345)
         g_codes.replay()
         g_acc.replay()
-    torch.cuda.synchronize()
+        torch.cuda.synchronize()
+        if first is None:
+            first = [p.out.clone() for p in r.plans] + [a.clone() for a in acc]
+        else:
+            now = [p.out for p in r.plans] + list(acc)
+            diff = [i for i, (x, y) in enumerate(zip(first, now)) if not torch.equal(x, y)]
+            assert not diff, ("replay differs", rep, [r.plans[i % len(r.plans)].kernel for i in diff])
     return acc
 
 
