@@ -280,6 +280,25 @@ DG_API dg_status dg_lut_gemm4_prepared(const uint8_t *d_at4, int64_t lda, const 
                                        int64_t M, int64_t K, const int32_t levels[16], void *d_ct, int64_t ldct,
                                        const dg_requant *rq, void *stream);
 
+/* FLOAT-valued tables (§5.3: "The LUT can store either integer or floating-point values";
+ * e.g. the products of a non-uniform quantiser's levels):
+ *      C[m][n] = sum_{k<K} table[(W[m][k] << 2) | A[k][n]]          (fp32 output C [M][ldc])
+ * on the int8 tensor cores: the table is written in fixed point, Ti = rne(table * 2^s) with the
+ * largest s keeping max|Ti| <= Q = 127 (2^16 + 2^8 + 1), split into three balanced int8 digits
+ * Ti = d2 2^16 + d1 2^8 + d0; the three digit LUT sums are exact int8 dot products in the one-hot
+ * form (dg_lut_gemm_onehot), and (acc2 2^16 + acc1 2^8 + acc0) 2^-s is formed exactly in fp64
+ * before one rounding to fp32.  Error bound (reading Q24), tested against the fp64 oracle:
+ *      |C - sum_k table[...]| <= K max|table| / Q + 2^-24 |sum_k table[...]|
+ * (exact up to the final rounding when every entry is a multiple of 2^-s).  d_ws:
+ * dg_lut_gemm_f32_workspace_size(M, N, K) bytes.  DG_ERR_RANGE for a non-finite entry,
+ * DG_ERR_OVERFLOW for K >= 2^22.  dg_float_table_fixed (host) returns s and the digits
+ * (digits[16 j + e] = d_j of entry e) for inspection.                                           */
+DG_API dg_status dg_float_table_fixed(const float table[16], int32_t digits[48], int32_t *shift);
+DG_API size_t dg_lut_gemm_f32_workspace_size(int64_t M, int64_t N, int64_t K);
+DG_API dg_status dg_lut_gemm_f32(const uint8_t *d_w, int64_t ldw, const uint8_t *d_at, int64_t lda, int64_t M, int64_t N,
+                                 int64_t K, const float table[16], float *d_c, int64_t ldc, void *d_ws, size_t ws_bytes,
+                                 void *stream);
+
 /* Block-scaled FP4 tensor-core path (tcgen05 kind::mxf4, e2m1 x e2m1):
  *      C[m][n] = sum_{k<K} lut.entries[(W[m][k] << 2) | A[k][n]]     (int32, exact)
  * for product tables whose activation levels are lut->al = {0, 1, 2, 3} (the activation code is

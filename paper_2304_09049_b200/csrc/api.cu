@@ -1,5 +1,6 @@
 // api.cu — the C ABI of libdg (include/dg.h): host-side validation, LUT build (S4),
 // variant dispatch and the conv orchestration (im2col + LUT GEMM + fused requant).
+#include <math.h>
 #include <stdlib.h>
 #include <string.h>
 
@@ -330,6 +331,37 @@ dg_status dg_lut_gemm4_prepared(const uint8_t *d_at4, int64_t lda, const int8_t 
     const int32_t pl[4] = {0, 1, 2, 3}, ql[4] = {(5 * wmax + 1) / 2, 0, 0, 0};
     return lut_gemm_ts(d_at4, lda, d_w8, ld8, N, M, 2 * K, pl, ql, d_ct, ldct, rq ? &a : nullptr, (cudaStream_t)stream,
                        nullptr, nullptr, 0, nullptr, 0, true);
+}
+
+dg_status dg_float_table_fixed(const float table[16], int32_t digits[48], int32_t *shift) {
+    if (!table || !digits || !shift) return DG_ERR_INVALID_ARG;
+    for (int e = 0; e < 16; ++e)
+        if (!isfinite(table[e])) return DG_ERR_RANGE;
+    int32_t d[3][16];
+    float_table_digits(table, d, shift);
+    for (int j = 0; j < 3; ++j)
+        for (int e = 0; e < 16; ++e) digits[16 * j + e] = d[j][e];
+    return DG_OK;
+}
+
+size_t dg_lut_gemm_f32_workspace_size(int64_t M, int64_t N, int64_t K) {
+    if (M <= 0 || N <= 0 || K <= 0) return 0;
+    return (size_t)lut_gemm_f32_workspace(M, N, K);
+}
+
+dg_status dg_lut_gemm_f32(const uint8_t *d_w, int64_t ldw, const uint8_t *d_at, int64_t lda, int64_t M, int64_t N,
+                          int64_t K, const float table[16], float *d_c, int64_t ldc, void *d_ws, size_t ws_bytes,
+                          void *stream) {
+    if (!d_w || !d_at || !table || !d_c || !d_ws) return DG_ERR_INVALID_ARG;
+    if (M <= 0 || N <= 0 || K <= 0) return DG_ERR_SHAPE;
+    if (ldw % 16 || lda % 16 || ldw * 4 < K || lda * 4 < K || ldc < N) return DG_ERR_SHAPE;
+    if (!aligned16(d_w) || !aligned16(d_at)) return DG_ERR_INVALID_ARG;
+    for (int e = 0; e < 16; ++e)
+        if (!isfinite(table[e])) return DG_ERR_RANGE;
+    if (K >= ((int64_t)1 << 22)) return DG_ERR_OVERFLOW;   // digit sums K * 4 * 128 < 2^31
+    if (!tc_available()) return DG_ERR_UNSUPPORTED;
+    if (ws_bytes < (size_t)lut_gemm_f32_workspace(M, N, K)) return DG_ERR_WORKSPACE;
+    return lut_gemm_f32(d_w, ldw, d_at, lda, M, N, K, table, d_c, ldc, d_ws, ws_bytes, (cudaStream_t)stream);
 }
 
 dg_status dg_lut_conv2d_f4_prepared(const uint8_t *d_x, const uint8_t *d_w4, int64_t ld4, const dg_lut *lut,

@@ -261,6 +261,10 @@ struct TsConv {
     const uint8_t *x;
     int32_t H, W, Cb, kh, kw, stride, pad, Ho, Wo, pad_code;
 };
+bool float_table_digits(const float T[16], int32_t digits[3][16], int32_t *s_out);
+int64_t lut_gemm_f32_workspace(int64_t M, int64_t N, int64_t K);
+dg_status lut_gemm_f32(const uint8_t *W, int64_t ldw, const uint8_t *At, int64_t lda, int64_t M, int64_t N, int64_t K,
+                       const float T[16], float *C, int64_t ldc, void *ws, size_t ws_bytes, cudaStream_t st);
 dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const TsConv &cv, int64_t rows, int64_t cout,
                       int64_t K, int64_t acc_bound, void *out, int64_t ldd, const RequantArgs *rq, cudaStream_t st,
                       bool b_prepared);

@@ -98,6 +98,9 @@ def lib():
             "dg_lut_conv2d": ([P, P, P, P, P, P, P, ctypes.c_size_t, i32, P], i32),
             "dg_lut_conv2d_prepared": ([P, P, i64, P, P, P, P, P, ctypes.c_size_t, P], i32),
             "dg_lut_conv2d_f4_prepared": ([P, P, i64, P, P, P, P, P], i32),
+            "dg_float_table_fixed": ([P, P, P], i32),
+            "dg_lut_gemm_f32_workspace_size": ([i64, i64, i64], ctypes.c_size_t),
+            "dg_lut_gemm_f32": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, ctypes.c_size_t, P], i32),
         }
         for name, (args, res) in sig.items():
             f = getattr(L, name)
@@ -547,4 +550,28 @@ def lut_conv2d_f4_prepared(x: torch.Tensor, w4: torch.Tensor, lut: dg_lut, p: dg
     _check(lib().dg_lut_conv2d_f4_prepared(_ptr(x), _ptr(w4), w4.shape[1], ctypes.byref(lut), ctypes.byref(p),
                                            ctypes.byref(r) if r is not None else None, _ptr(out), _stream(stream)),
            "dg_lut_conv2d_f4_prepared")
+    return out
+
+
+def float_table_fixed(table):
+    """Host: (shift s, digits [3][16]) of the fixed-point form of a float table (dg_float_table_fixed)."""
+    t = (ctypes.c_float * 16)(*[float(v) for v in table])
+    d = (ctypes.c_int32 * 48)()
+    sh = ctypes.c_int32()
+    _check(lib().dg_float_table_fixed(t, d, ctypes.byref(sh)), "dg_float_table_fixed")
+    return int(sh.value), [list(d[16 * j:16 * j + 16]) for j in range(3)]
+
+
+def lut_gemm_f32(w: torch.Tensor, at: torch.Tensor, M: int, N: int, K: int, table, out: torch.Tensor | None = None,
+                 ws: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """fp32 C[m][n] = sum_k table[(W[m][k]<<2)|A[k][n]] for a float-valued table."""
+    _dev(w, torch.uint8, "w")
+    _dev(at, torch.uint8, "at")
+    if out is None:
+        out = torch.empty((M, N), dtype=torch.float32, device=w.device)
+    if ws is None:
+        ws = torch.empty(int(lib().dg_lut_gemm_f32_workspace_size(M, N, K)), dtype=torch.uint8, device=w.device)
+    t = (ctypes.c_float * 16)(*[float(v) for v in table])
+    _check(lib().dg_lut_gemm_f32(_ptr(w), w.shape[1], _ptr(at), at.shape[1], M, N, K, t, _ptr(out), out.stride(0),
+                                 _ptr(ws), ws.numel(), _stream(stream)), "dg_lut_gemm_f32")
     return out

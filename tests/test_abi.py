@@ -95,3 +95,28 @@ def test_runtime_options_host():
     with pytest.raises(dg.DGError, match="INVALID"):
         dg.set_option("no_such_option", 1)
     assert isinstance(dg.last_kernel(), str)
+
+
+def test_float_table_fixed_point_digits_host():
+    """dg_float_table_fixed (host part of the float-table path, include/dg.h): the three balanced
+    int8 digits rebuild rne(table * 2^s) exactly, |digit| <= 128, max|Ti| <= Q and s is maximal
+    (one more bit would exceed Q), so every entry is within max|table| / Q of its fixed-point value."""
+    import numpy as np
+    from paper_2304_09049_b200 import dg
+    Q = 127 * (65536 + 256 + 1)
+    g = np.random.default_rng(11)
+    tables = [g.normal(size=16) * 10.0 ** g.integers(-3, 4, 16), np.linspace(-1, 1, 16), np.full(16, 3.5e-20),
+              np.array([1e6] + [0.0] * 15), -np.abs(g.normal(size=16)) * 1e-5]
+    for t in tables:
+        t32 = t.astype(np.float32).astype(np.float64)
+        s, d = dg.float_table_fixed(t)
+        d = np.array(d, np.int64)
+        Ti = d[2] * 65536 + d[1] * 256 + d[0]
+        assert np.array_equal(Ti, np.rint(np.ldexp(t32, s)).astype(np.int64))
+        assert np.abs(d).max() <= 128 and np.abs(Ti).max() <= Q
+        assert 2 * np.abs(np.ldexp(t32, s)).max() > Q
+        assert np.all(np.abs(t32 - np.ldexp(Ti.astype(np.float64), -s)) <= np.abs(t32).max() / Q)
+    s, d = dg.float_table_fixed(np.zeros(16))
+    assert not np.any(d)
+    with pytest.raises(dg.DGError, match="RANGE"):
+        dg.float_table_fixed([float("nan")] + [0.0] * 15)

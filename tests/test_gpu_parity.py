@@ -979,3 +979,36 @@ def test_conv_f4_accumulator_origin_at_the_bound():
     w2 = dg.expand_operand_f4(gpu_pack(np.zeros((8, K2), np.uint8), weights=True), K2, wl)
     with pytest.raises(dg.DGError, match="OVERFLOW"):
         dg.lut_conv2d_f4_prepared(gpu_pack(np.zeros((1, K2), np.uint8))[:, : K2 // 4].contiguous(), w2, lut, p2)
+
+
+# ---- float-valued tables (dg_lut_gemm_f32, fixed-point digits on the one-hot tensor-core form) ----
+F32_Q = 127 * (65536 + 256 + 1)
+
+
+@pytest.mark.parametrize("kind", ["random", "product", "dyadic", "tiny"])
+@pytest.mark.parametrize("M,N,K", [(64, 196, 576), (130, 70, 1000), (7, 300, 33)])
+def test_gemm_float_table_vs_fp64_oracle(kind, M, N, K):
+    """fp32 result within the stated bound of the fp64 oracle (Q24):
+    |C - C64| <= K max|T| / Q + 2^-24 |C64|; exact (up to the fp32 rounding) for dyadic entries."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    g = np.random.default_rng(M + N + K + len(kind))
+    if kind == "random":
+        T = g.normal(size=16) * 10.0 ** g.integers(-2, 3, 16)
+    elif kind == "product":    # non-uniform quantiser levels (P:102-103): T = wl (x) al
+        wl, al = np.sort(g.normal(size=4)), np.sort(np.abs(g.normal(size=4)))
+        T = np.outer(wl, al).reshape(-1)
+    elif kind == "dyadic":     # multiples of 2^-6 below 2^13: exactly representable in the fixed point
+        T = g.integers(-2 ** 19, 2 ** 19, 16) / 64.0
+    else:
+        T = g.normal(size=16) * 1e-30
+    T32 = T.astype(np.float32).astype(np.float64)
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    C = host(dg.lut_gemm_f32(gpu_pack(W, weights=True), gpu_pack(np.ascontiguousarray(A.T)), M, N, K, T32)).astype(np.float64)
+    assert dg.last_kernel().startswith("f32 table")
+    C64 = oracle.lut_gemm_f64(W, A, T32)
+    tol = K * np.abs(T32).max() / F32_Q + 2.0 ** -24 * np.abs(C64)
+    if kind == "dyadic":
+        tol = 2.0 ** -24 * np.abs(C64)
+    assert np.all(np.abs(C - C64) <= tol), np.max(np.abs(C - C64) - tol)
