@@ -1012,3 +1012,22 @@ def test_gemm_float_table_vs_fp64_oracle(kind, M, N, K):
     if kind == "dyadic":
         tol = 2.0 ** -24 * np.abs(C64)
     assert np.all(np.abs(C - C64) <= tol), np.max(np.abs(C - C64) - tol)
+
+
+@pytest.mark.parametrize("M,N,K", [(64, 196, 576), (33, 70, 301)])
+def test_gemm3_bit_codes_in_4bit_storage(M, N, K):
+    """3-bit operands (Table 2: a 6-bit index into a 64-entry table) on the 4-bit path:
+    3-bit codes are 4-bit codes 0..7 (levels 8..15 unused); product table wl (x) {0..7}, vs the
+    b-bit oracle with bits = 3."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    g = np.random.default_rng(M + N + K + 3)
+    wl8 = g.integers(-31, 32, 8).astype(np.int32)
+    wl16 = np.concatenate([wl8, np.zeros(8, np.int32)])
+    W = g.integers(0, 8, (M, K), dtype=np.uint8)
+    A = g.integers(0, 8, (K, N), dtype=np.uint8)
+    T3 = np.outer(wl8, np.arange(8)).reshape(-1).astype(np.int32)   # index (w << 3) | a
+    w4 = dg.pack_codes4(torch.from_numpy(W).to(DEV))
+    at4 = dg.pack_codes4(torch.from_numpy(np.ascontiguousarray(A.T)).to(DEV))
+    Ct = host(dg.lut_gemm4_prepared(at4, dg.expand_digits4(w4, K, wl16), N, M, K, wl16))
+    assert np.array_equal(Ct, oracle.lut_gemm_bits(W, A, T3, 3).T)
