@@ -323,7 +323,9 @@ DG_API dg_status dg_lut_gemm_f4(const uint8_t *d_w4, int64_t ld4, const uint8_t 
  * and the epilogue stores every output tile to d_c AND to each of the npeers (<= 7)
  * extra destinations d_c_peers[i] (host array of device pointers: the other ranks'
  * C buffers mapped peer-to-peer, e.g. CUDA IPC / symmetric memory), all with the
- * same row pitch ldc and already offset to this rank's first row.  The exchange thus
+ * same row pitch ldc and already offset to this rank's first row.  Where the instance
+ * stages int32 tiles for the TMA store, each 32 x 32 chunk leaves the staging buffer once
+ * per destination as one bulk tensor store (whole boxes over NVLink, not per-lane stores).  The exchange thus
  * overlaps the math tile by tile instead of following it as a separate collective.
  * Every destination must have the 16-byte alignment of d_c.  The caller orders
  * completion before peers read (e.g. a barrier on the same stream after the call);

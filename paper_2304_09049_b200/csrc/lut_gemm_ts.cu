@@ -137,6 +137,13 @@ inline FastDiv make_fastdiv(uint32_t d) {
 }
 DG_DEV uint32_t fdiv(uint32_t n, FastDiv f) { return (__umulhi(n, f.m) + n) >> f.s; }
 
+// tensor maps of the fused all-gather destinations (peer GPUs' C, P2P-mapped): the TMA-store
+// epilogue writes every staged int32 chunk to its own C and, from the same shared-memory bytes,
+// to each peer (whole 32 x 32 boxes per request instead of per-lane 16-byte stores)
+struct PeerMaps {
+    CUtensorMap m[7];
+};
+
 struct TsArgs {
     int64_t np, nq;
     int32_t nstages, last_ksteps, ntp, ntq;
@@ -605,8 +612,8 @@ __device__ __noinline__ void epilogue_loop_rare(const TsArgs &ta, const RequantA
 template <int BN, int NEPI, int NUNP, int KST, bool WIN, bool ASM, bool SK, int EM>
 __global__ void __launch_bounds__(Roles<NEPI, NUNP, EM>::NT, 1)
 lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
-                   const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ TsArgs ta,
-                   const __grid_constant__ RequantArgs rq) {
+                   const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ PeerMaps pm,
+                   const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
     using C = TsCfg<BN, (EM & EM_CSPLIT) ? 1 : NEPI / 4, KST, WIN, ASM>;
     using R = Roles<NEPI, NUNP, EM>;
     constexpr bool CS = (EM & EM_CSPLIT) != 0;
@@ -1375,6 +1382,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     __syncwarp();
                     if (lane == 0) {
                         ptx::tma_store_2d(&tm_d, stg, (int32_t)(q0 + c * 32), row0);
+                        for (int d = 0; d < ta.npeer; ++d) ptx::tma_store_2d(&pm.m[d], stg, (int32_t)(q0 + c * 32), row0);
                         ptx::bulk_commit();
                     }
                 }
@@ -1704,16 +1712,21 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     memset(&mp, 0, sizeof(mp));
     memset(&md, 0, sizeof(md));
     ta.tma_d = 0;
-    if (C::STG_BYTES > 0 && !rq && ta.npeer == 0 && ((uintptr_t)D & 15) == 0 && (ldd * 4) % 16 == 0 && nq >= 32 &&
-        opt(OPT_TMA_STORE)) {
+    PeerMaps pmaps;
+    memset(&pmaps, 0, sizeof(pmaps));
+    if (C::STG_BYTES > 0 && !rq && ((uintptr_t)D & 15) == 0 && (ldd * 4) % 16 == 0 && nq >= 32 && opt(OPT_TMA_STORE)) {
         EncodeTiledFn fn = encode_fn_ts();
         cuuint64_t dims[2] = {(cuuint64_t)nq, (cuuint64_t)np};
         cuuint64_t strides[1] = {(cuuint64_t)(ldd * 4)};
         cuuint32_t box[2] = {32, 32}, estr[2] = {1, 1};
-        if (fn && fn(&md, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, D, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                     CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
-                     CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS)
-            ta.tma_d = 1;
+        auto enc = [&](CUtensorMap *m, void *base) {
+            return fn && fn(m, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, base, dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                            CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_NONE,
+                            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+        };
+        bool ok = enc(&md, D);
+        for (int i = 0; i < ta.npeer && ok; ++i) ok = enc(&pmaps.m[i], ta.peer[i]);
+        ta.tma_d = ok ? 1 : 0;
     }
     if (!cv && !ta.bulk && !make_map_sw128(&mp, P, ldp, np, BM, ta.pks)) return DG_ERR_CUDA;
     if (!make_map_sw128(&mb, Q8, ld8, nq, BN, 128)) return DG_ERR_CUDA;
@@ -1754,7 +1767,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     la[0].val.programmaticStreamSerializationAllowed = opt(OPT_PDL) ? 1 : 0;
     lc.attrs = la;
     lc.numAttrs = 1;
-    if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK, EM>, mp, mb, md, ta, rqv) != cudaSuccess)
+    if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK, EM>, mp, mb, md, pmaps, ta, rqv) != cudaSuccess)
         return DG_ERR_CUDA;
     if (ta.sk > 1) {
         const int64_t thr = np * ((nq + 3) >> 2);
