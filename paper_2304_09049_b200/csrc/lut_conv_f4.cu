@@ -47,7 +47,7 @@ constexpr int CF_OFF_TMEM = CF_OFF_BAR + CF_NBAR * 8;
 constexpr int CF_OFF_TAB = (CF_OFF_TMEM + 16 + 15) / 16 * 16;
 constexpr int CF_ALLOC = CF_OFF_TAB + CF_TAB_PAIRS * 4 + 1024;
 static_assert(CF_ALLOC <= 232448, "shared memory budget");
-constexpr int CF_UNP0 = 4, CF_PROD = 8, CF_WAIT = 9, CF_MMA = 10, CF_NT = 32 * 11;
+constexpr int CF_UNP0 = 4;   // unpack warps 4 .. 4 + NUNP - 1, then producer, waiter, MMA issuer
 constexpr int CF_HANDOFF_BAR = 1, CF_EPI_BAR = 2;
 constexpr uint32_t CF_SF_COL = 480;                // TMEM columns [480, 512): block scales (every byte 2^1)
 constexpr uint32_t CF_ACC0 = 0x4B400000u;          // fp32 1.5 * 2^23: the accumulators' integer origin
@@ -107,12 +107,16 @@ __device__ __align__(16) uint8_t g_cf_pad[4][32];
 
 // TA: A stages in tensor memory (two accumulators, six 32-column A stages) instead of shared memory
 // (three accumulators, four 16 KB SW128 stages written with st.shared)
-template <bool TA>
-__global__ void __launch_bounds__(CF_NT, 1)
+// NUNP: unpack warps, 4 (one group) or 8 (two groups of 4 owning alternate stages, each with its
+// own gather ring: more gathers in flight for the implicit convolutions)
+template <bool TA, int NUNP>
+__global__ void __launch_bounds__(32 * (7 + NUNP), 1)
 lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CfArgs fa, const __grid_constant__ RequantArgs rq) {
     constexpr int CF_NACC = TA ? 2 : 3, CF_SA = TA ? 6 : 4;
     constexpr uint32_t TA0 = CF_NACC * CF_BN;   // first tensor-memory A column (TA)
+    constexpr int CF_PROD = CF_UNP0 + NUNP, CF_WAIT = CF_PROD + 1, CF_MMA = CF_PROD + 2, NG = NUNP / 4;
+    constexpr int IGG = CF_IG / NG;             // gather ring stages per unpack group
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = ptx::smem_u32(smem);
@@ -138,7 +142,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             ptx::tma_prefetch(&tm_b);
             for (int s = 0; s < CF_SP; ++s) {
                 ptx::mbar_init(full_p(s), 1);
-                ptx::mbar_init(empty_p(s), 4);   // the 4 unpack warps, once per slot
+                ptx::mbar_init(empty_p(s), 8);   // 4 unpack warps x 2 stages per slot (count 2 for a lone stage)
             }
             for (int s = 0; s < CF_SB; ++s) {
                 ptx::mbar_init(full_b(s), 1);
@@ -250,12 +254,14 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         }
     } else if (warp >= CF_UNP0) {
         // thread = pixel row r of the tile: 64 packed bytes (256 codes) per stage -> 32 words of e2m1
-        // nibbles (x & 0x33333333, (x >> 2) & 0x33333333 per packed word) -> SW128 K-major A stage
+        // nibbles (x & 0x33333333, (x >> 2) & 0x33333333 per packed word) -> A stage.  Group grp owns
+        // the stages g with g % NG == grp.
         ptx::griddep_wait();
-        const int r = (warp - CF_UNP0) * 32 + lane;
-        uint32_t g = 0, gp = 0;
-        // implicit gather cursor: work item gt, stage gs of the next fetch; this row's pixel
-        int gt = blockIdx.x, gs = 0;
+        const int grp = (warp - CF_UNP0) >> 2;
+        const int r = (warp & 3) * 32 + lane;
+        uint32_t g = 0, gp = 0, own = 0;
+        // implicit gather cursor of this group: work item gt, stage gs of the next fetch; this row's pixel
+        int gt = blockIdx.x, gs = grp;
         const uint8_t *img = fa.X;
         int32_t h0 = 0, w0 = 0;
         auto pixel = [&]() {
@@ -266,8 +272,13 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             h0 = (int32_t)(tt - b * (uint32_t)fa.Ho) * fa.stride - fa.pad;
             w0 = (int32_t)(pp - tt * (uint32_t)fa.Wo) * fa.stride - fa.pad;
         };
-        const uint32_t ring = sbase + CF_OFF_P + (uint32_t)(r * 64);
-        auto fetch = [&](int slot) {   // the cursor's stage -> ring slot; advance the cursor
+        auto settle = [&]() {   // move (gt, gs) into the work item that holds stage gs
+            bool moved = false;
+            while (gs >= fa.nstages && gt < ntiles) { gs -= fa.nstages; gt += gridDim.x; moved = true; }
+            if (moved && gt < ntiles) pixel();
+        };
+        const uint32_t ring = sbase + CF_OFF_P + (uint32_t)(grp * IGG * CF_RING) + (uint32_t)(r * 64);
+        auto fetch = [&](int slot) {   // the cursor's stage -> ring slot; advance the cursor by NG stages
             if (gt < ntiles) {
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -281,39 +292,48 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                                                : fa.padsrc;
                     ptx::cp_async16(ring + (uint32_t)(slot * CF_RING) + ((c ^ ((r >> 1) & 3)) << 4), src);
                 }
-                if (++gs == fa.nstages) {
-                    gs = 0;
-                    gt += gridDim.x;
-                    if (gt < ntiles) pixel();
-                }
+                gs += NG;
+                settle();
             }
             ptx::cp_async_commit();
         };
         if (!fa.direct) {
             if (gt < ntiles) pixel();
-            for (int i = 0; i < CF_IG; ++i) fetch(i);
+            settle();
+            for (int i = 0; i < IGG; ++i) fetch(i);
         }
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             for (int s = 0; s < fa.nstages; ++s, ++g) {
+                const bool slot_end = (s & 1) == 1 || s == fa.nstages - 1;   // last stage of a packed slot
+                if (NG > 1 && (int)(g % NG) != grp) {   // another group's stage: slot bookkeeping only
+                    if (fa.direct && slot_end) ++gp;
+                    continue;
+                }
                 uint4 v[4];
                 if (fa.direct) {
                     const int ps = (int)(gp % CF_SP), sub = s & 1;
-                    if (sub == 0) ptx::mbar_wait(full_p(ps), (gp / CF_SP) & 1u);
+                    ptx::mbar_wait(full_p(ps), (gp / CF_SP) & 1u);
                     const uint32_t pbase = sbase + CF_OFF_P + ps * CF_P_SLOT;
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {   // SW128 slot: 16-byte unit XOR row bits
                         const uint32_t lin = (uint32_t)(r * 128 + sub * 64 + 16 * c);
                         v[c] = ptx::lds128(pbase + (lin ^ (((lin >> 7) & 7u) << 4)));
                     }
-
+                    // this stage's share of the slot is released once its loads have landed
+                    // (release_after_loads: the refilling TMA raced with outstanding loads, measured
+                    // nondeterministic rows); a slot's lone last stage counts twice
+                    ptx::release_after_loads(empty_p(ps), (s & 1) == 0 && s == fa.nstages - 1 ? 2u : 1u,
+                                             v[0].x ^ v[1].x ^ v[2].x ^ v[3].x);
+                    if (slot_end) ++gp;
                 } else {
-                    ptx::cp_async_wait<CF_IG - 1>();   // this stage's copies (the oldest group) landed
-                    const int slot = (int)(g % CF_IG);
+                    ptx::cp_async_wait<IGG - 1>();   // this stage's copies (the oldest group) landed
+                    const int slot = (int)(own % IGG);
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
                         v[c] = ptx::lds128(ring + (uint32_t)(slot * CF_RING) + ((c ^ ((r >> 1) & 3)) << 4));
-                    fetch(slot);   // values are in registers: refill the slot CF_IG stages ahead
+                    fetch(slot);   // values are in registers: refill the slot IGG own stages ahead
                 }
+                ++own;
                 uint32_t e[32];
 #pragma unroll
                 for (int c = 0; c < 4; ++c) {
@@ -323,12 +343,6 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         e[8 * c + 2 * i] = w[i] & 0x33333333u;
                         e[8 * c + 2 * i + 1] = (w[i] >> 2) & 0x33333333u;
                     }
-                }
-                // this warp is done with the slot once its loads have landed (release_after_loads: the
-                // TMA that refills the slot raced with outstanding loads, measured nondeterministic rows)
-                if (fa.direct && ((s & 1) == 1 || s == fa.nstages - 1)) {
-                    ptx::release_after_loads(empty_p((int)(gp % CF_SP)), 1u, v[0].x ^ v[1].x ^ v[2].x ^ v[3].x);
-                    ++gp;
                 }
                 const int sa = (int)(g % CF_SA);
                 ptx::mbar_wait(empty_a(sa), ((g / CF_SA) & 1u) ^ 1u);
@@ -574,19 +588,23 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     if (direct && !cf_map(&mp, x, cb, cb, rows, CF_BM)) return DG_ERR_CUDA;
     if (!cf_map(&mb, w4, ld4, ld4, cout, CF_BN)) return DG_ERR_CUDA;
     const bool ta = opt(OPT_F4_TA) != 0;
-    static bool attr[2] = {false, false};
-    if (!attr[ta]) {
-        if (cudaFuncSetAttribute(ta ? lut_conv_f4_kernel<true> : lut_conv_f4_kernel<false>,
-                                 cudaFuncAttributeMaxDynamicSharedMemorySize, CF_ALLOC) != cudaSuccess)
+    const int nunp = (int)opt(OPT_F4_UNP) == 4 ? 4 : ((int)opt(OPT_F4_UNP) == 8 ? 8 : (direct ? 4 : 8));
+    void (*kern)(const CUtensorMap, const CUtensorMap, const CfArgs, const RequantArgs) =
+        ta ? (nunp == 8 ? lut_conv_f4_kernel<true, 8> : lut_conv_f4_kernel<true, 4>)
+           : (nunp == 8 ? lut_conv_f4_kernel<false, 8> : lut_conv_f4_kernel<false, 4>);
+    static bool attr[4] = {false, false, false, false};
+    const int ai = (ta ? 2 : 0) + (nunp == 8 ? 1 : 0);
+    if (!attr[ai]) {
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF_ALLOC) != cudaSuccess)
             return DG_ERR_CUDA;
-        attr[ta] = true;
+        attr[ai] = true;
     }
     RequantArgs dummy{};
     const RequantArgs rqv = rq ? *rq : dummy;
     const int grid = (int)(nt < num_sms() ? nt : num_sms());
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)grid);
-    lc.blockDim = dim3((unsigned)CF_NT);
+    lc.blockDim = dim3((unsigned)(32 * (7 + nunp)));
     lc.dynamicSmemBytes = CF_ALLOC;
     lc.stream = st;
     cudaLaunchAttribute la[1];
@@ -594,11 +612,10 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     la[0].val.programmaticStreamSerializationAllowed = opt(OPT_PDL) ? 1 : 0;
     lc.attrs = la;
     lc.numAttrs = 1;
-    if (cudaLaunchKernelEx(&lc, ta ? lut_conv_f4_kernel<true> : lut_conv_f4_kernel<false>, mp, mb, fa, rqv) != cudaSuccess)
-        return DG_ERR_CUDA;
+    if (cudaLaunchKernelEx(&lc, kern, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
     char tag[96];
-    snprintf(tag, sizeof(tag), "f4conv bn=128 %s direct=%d rq=%d tab=%d early=%d", ta ? "ta nacc=2" : "sa nacc=3", fa.direct,
-             fa.has_rq, fa.f16_tab, fa.early_b);
+    snprintf(tag, sizeof(tag), "f4conv bn=128 %s unp=%d direct=%d rq=%d tab=%d early=%d", ta ? "ta nacc=2" : "sa nacc=3", nunp,
+             fa.direct, fa.has_rq, fa.f16_tab, fa.early_b);
     set_last_kernel(tag);
     return launch_status();
 }
