@@ -299,6 +299,26 @@ DG_API dg_status dg_lut_gemm_f32(const uint8_t *d_w, int64_t ldw, const uint8_t 
                                  int64_t K, const float table[16], float *d_c, int64_t ldc, void *d_ws, size_t ws_bytes,
                                  void *stream);
 
+/* General 4-bit tables (Table 2: 4-bit codes, an 8-bit index (w << 4) | a into a
+ * 256-entry table; 3-bit tables are 4-bit tables over codes 0..7): any int8 table (|entry| <= 127,
+ * e.g. non-affine activation levels or non-product entries) in the one-hot form over the 16
+ * weight codes, K' = 16K, on the int8 tensor cores:
+ *      C[m][n] = sum_{k<K} table[(W[m][k] << 4) | A[k][n]]
+ * dg_expand_onehot4: packed 4-bit weights [rows][ld] (code k in nibble k&1 of byte k>>1) ->
+ *   packed 2-bit one-hot codes [rows][ld_out >= dg_onehot4_ld(K)] (the word 1 << (2 code) per code);
+ * dg_expand_tcols4: packed 4-bit activations -> int8 [rows][ld_out >= dg_tcols4_ld(K)] (128-byte
+ *   aligned) of table[(i << 4) | a] at k' = 16k + i in the tensor-core operand order;
+ * dg_lut_gemm4_onehot: output and rq as dg_lut_gemm.  DG_ERR_UNSUPPORTED if some |entry| > 127.  */
+DG_API int64_t dg_onehot4_ld(int64_t K);
+DG_API int64_t dg_tcols4_ld(int64_t K);
+DG_API dg_status dg_expand_onehot4(const uint8_t *d_w4, int64_t rows, int64_t K, int64_t ld, uint8_t *d_out,
+                                   int64_t ld_out, void *stream);
+DG_API dg_status dg_expand_tcols4(const uint8_t *d_at4, int64_t rows, int64_t K, int64_t ld, const int32_t table[256],
+                                  int8_t *d_out, int64_t ld_out, void *stream);
+DG_API dg_status dg_lut_gemm4_onehot(const uint8_t *d_w1h, int64_t ldw1h, const int8_t *d_atc, int64_t ldatc, int64_t M,
+                                     int64_t N, int64_t K, const int32_t table[256], void *d_c, int64_t ldc,
+                                     const dg_requant *rq, void *stream);
+
 /* Block-scaled FP4 tensor-core path (tcgen05 kind::mxf4, e2m1 x e2m1):
  *      C[m][n] = sum_{k<K} lut.entries[(W[m][k] << 2) | A[k][n]]     (int32, exact)
  * for product tables whose activation levels are lut->al = {0, 1, 2, 3} (the activation code is

@@ -295,6 +295,53 @@ dg_status dg_lut_gemm_onehot(const uint8_t *d_w1h, int64_t ldw1h, const int8_t *
                        (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, true);
 }
 
+// ---- general 4-bit (and 3-bit) tables: one-hot over the 16 weight codes, K' = 16K (dg.h)
+static int64_t max_abs256(const int32_t *t) {
+    int64_t m = 0;
+    for (int e = 0; e < 256; ++e) m = (t[e] < 0 ? -(int64_t)t[e] : t[e]) > m ? (t[e] < 0 ? -(int64_t)t[e] : t[e]) : m;
+    return m;
+}
+
+int64_t dg_onehot4_ld(int64_t K) { return K <= 0 ? 0 : onehot4_ld(K); }
+int64_t dg_tcols4_ld(int64_t K) { return K <= 0 ? 0 : tcols4_ld(K); }
+
+dg_status dg_expand_onehot4(const uint8_t *d_w4, int64_t rows, int64_t K, int64_t ld, uint8_t *d_out, int64_t ld_out,
+                            void *stream) {
+    if (!d_w4 || !d_out) return DG_ERR_INVALID_ARG;
+    if (rows < 0 || K <= 0 || ld * 2 < K || ld_out < onehot4_ld(K) || ld_out % 16) return DG_ERR_SHAPE;
+    if (!aligned16(d_out)) return DG_ERR_INVALID_ARG;
+    return expand_onehot4(d_w4, rows, K, ld, d_out, ld_out, (cudaStream_t)stream);
+}
+
+dg_status dg_expand_tcols4(const uint8_t *d_at4, int64_t rows, int64_t K, int64_t ld, const int32_t table[256],
+                           int8_t *d_out, int64_t ld_out, void *stream) {
+    if (!d_at4 || !table || !d_out) return DG_ERR_INVALID_ARG;
+    if (rows < 0 || K <= 0 || ld * 2 < K || ld_out < tcols4_ld(K) || ld_out % 128) return DG_ERR_SHAPE;
+    if ((uintptr_t)d_out & 127) return DG_ERR_INVALID_ARG;
+    if (max_abs256(table) > 127) return DG_ERR_UNSUPPORTED;
+    return expand_tcols4(d_at4, rows, K, ld, table, d_out, ld_out, (cudaStream_t)stream);
+}
+
+dg_status dg_lut_gemm4_onehot(const uint8_t *d_w1h, int64_t ldw1h, const int8_t *d_atc, int64_t ldatc, int64_t M, int64_t N,
+                              int64_t K, const int32_t table[256], void *d_c, int64_t ldc, const dg_requant *rq,
+                              void *stream) {
+    if (!d_w1h || !d_atc || !table || !d_c) return DG_ERR_INVALID_ARG;
+    if (M <= 0 || N <= 0 || K <= 0) return DG_ERR_SHAPE;
+    if (ldw1h % 16 || ldw1h < onehot4_ld(K) || ldatc < tcols4_ld(K) || ldatc % 128) return DG_ERR_SHAPE;
+    if (!aligned16(d_w1h) || ((uintptr_t)d_atc & 127)) return DG_ERR_INVALID_ARG;
+    if (rq ? (ldc * 4 < N) : (ldc < N)) return DG_ERR_SHAPE;
+    dg_status s = check_rq(rq);
+    if (s != DG_OK) return s;
+    const int64_t emax = max_abs256(table);
+    if (emax > 127 || !tc_available()) return DG_ERR_UNSUPPORTED;
+    if (K * emax >= ((int64_t)1 << 31)) return DG_ERR_OVERFLOW;
+    RequantArgs a{};
+    if (rq) a = to_args(rq);
+    const int32_t pl[4] = {0, 1, 0, 0}, ql[4] = {(int32_t)emax, 0, 0, 0};   // (ql only bounds |acc|)
+    return lut_gemm_ts(d_w1h, ldw1h, d_atc, ldatc, M, N, 16 * K, pl, ql, d_c, ldc, rq ? &a : nullptr,
+                       (cudaStream_t)stream, nullptr, nullptr, 0, nullptr, 0, true);
+}
+
 // ---- 4-bit operands as 2-bit digit pairs (dg.h)
 static int32_t max_abs16(const int32_t *l) {
     int32_t m = 0;

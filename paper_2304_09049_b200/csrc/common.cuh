@@ -245,6 +245,12 @@ dg_status expand_operand(const uint8_t *packed, int64_t rows, int64_t K, int64_t
                          int8_t *out, int64_t ld8, cudaStream_t st);
 // implicit-GEMM convolution description for the TS kernel (P = im2col of x, gathered on chip)
 int64_t onehot_ld(int64_t K);
+int64_t onehot4_ld(int64_t K);
+int64_t tcols4_ld(int64_t K);
+dg_status expand_onehot4(const uint8_t *w4, int64_t rows, int64_t K, int64_t ld, uint8_t *out, int64_t ld_out,
+                         cudaStream_t st);
+dg_status expand_tcols4(const uint8_t *a4, int64_t rows, int64_t K, int64_t ld, const int32_t table[256], int8_t *out,
+                        int64_t ld_out, cudaStream_t st);
 int64_t tcols_ld(int64_t K);
 dg_status expand_onehot(const uint8_t *w, int64_t rows, int64_t K, int64_t ld, uint8_t *out, int64_t ld_out,
                         cudaStream_t st);

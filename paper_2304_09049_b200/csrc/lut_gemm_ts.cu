@@ -47,7 +47,7 @@ constexpr int SP_MAX = 32;       // packed P slots (narrow rows -> many slots in
 // column block g (the accumulator is released as soon as each warp has loaded its columns) instead
 // of groups owning alternate tiles; EM_HIGH = epilogue warps above the unpack warps in warp-id order
 // (scheduler priority) for layers whose cost is the epilogue.
-constexpr int EM_CSPLIT = 1, EM_HIGH = 2;
+constexpr int EM_CSPLIT = 1, EM_HIGH = 2, EM_A6 = 4;
 template <int NEPI, int NUNP, int EM = 0>
 struct Roles {
     static constexpr int NUM_UGROUPS = NUNP / 4;
@@ -76,7 +76,7 @@ constexpr int EPI_BAR = 2;       // epilogue warps only (requant table build)
 // ASM (template): the A operand in SHARED memory (no-swizzle K-major stages written by the unpack
 // warps, SS MMA) instead of tensor memory, which leaves all 512 TMEM columns to two 128x256
 // accumulators: short-K, wide-output layers, whose cost is a fixed chain of hand-offs per tile.
-template <int BN, int EG, int KST, bool WIN = false, bool ASM = false>
+template <int BN, int EG, int KST, bool WIN = false, bool ASM = false, bool A6 = false>
 struct TsCfg {
     static constexpr int KSTEPS = KST / 32;                 // MMAs (K = 32) per stage
     static constexpr int ACOLS = KST / 4;                   // TMEM columns of one A stage
@@ -86,13 +86,15 @@ struct TsCfg {
     // (ASM and WIN keep A in shared memory: all 512 TMEM columns hold accumulators)
     static constexpr int NACC = ASM ? 512 / BN : (WIN ? 4 : (BN == 256 ? 1 : (BN == 128 ? 2 : 4)));
     static_assert(NACC % EG == 0, "accumulator buffers per epilogue group");
-    static constexpr int SA = (ASM || WIN) ? 4 : ((512 - NACC * BN) / ACOLS > 8 ? 8 : (512 - NACC * BN) / ACOLS);   // A stages (WIN: windows)
+    // (A6: the short-K shared-memory-A kernel with six A stages and at most two weight stages)
+    static constexpr int SA = (ASM && A6) ? 6 : ((ASM || WIN) ? 4 : ((512 - NACC * BN) / ACOLS > 8 ? 8 : (512 - NACC * BN) / ACOLS));   // A stages (WIN: windows)
     static constexpr int B_ATOM = BN * KA;                  // bytes of one 128-code B atom
     static constexpr int B_BYTES = BN * KST;
     // WIN with 128-code stages = the C = 128 tile mode: all 9 weight stages (128 x 1152) resident
     static constexpr bool WIN128 = WIN && KST == 128;
     static constexpr int SB_RAW = (WIN128 ? 147456 : (WIN && BN == 64 ? 49152 : (BN == 64 || WIN || ASM ? 98304 : 131072))) / B_BYTES;
-    static constexpr int SB = SB_RAW > (WIN128 ? 9 : 8) ? (WIN128 ? 9 : 8) : SB_RAW;   // B (int8) smem stages
+    static constexpr int SB_CAP = (ASM && A6) ? 2 : (WIN128 ? 9 : 8);
+    static constexpr int SB = SB_RAW > SB_CAP ? SB_CAP : SB_RAW;   // B (int8) smem stages
     static constexpr int TMEM_A0 = NACC * BN;               // first A column
     static constexpr int TMEM_COLS = 512;
     static constexpr int P_REGION = WIN ? (WIN128 ? 70656 : (BN == 64 ? 155648 : 106496)) : (ASM ? 32768 : 4 * BM * PKS_MAX);   // packed P / WIN ring + windows
@@ -614,7 +616,7 @@ __global__ void __launch_bounds__(Roles<NEPI, NUNP, EM>::NT, 1)
 lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ PeerMaps pm,
                    const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
-    using C = TsCfg<BN, (EM & EM_CSPLIT) ? 1 : NEPI / 4, KST, WIN, ASM>;
+    using C = TsCfg<BN, (EM & EM_CSPLIT) ? 1 : NEPI / 4, KST, WIN, ASM, (EM & EM_A6) != 0>;
     using R = Roles<NEPI, NUNP, EM>;
     constexpr bool CS = (EM & EM_CSPLIT) != 0;
     constexpr int SB = C::SB, SA = C::SA, NACC = C::NACC, SP = SP_MAX;
@@ -1559,7 +1561,7 @@ template <int BN, int NEPI, int NUNP, int KST, bool WIN = false, bool ASM = fals
 dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8, int64_t np, int64_t nq, int64_t K,
                     const int32_t pl[4], const int32_t ql[4], void *D, int64_t ldd, const RequantArgs *rq,
                     cudaStream_t st, const TsConv *cv, void *skws = nullptr, size_t skws_bytes = 0) {
-    using C = TsCfg<BN, (EM & EM_CSPLIT) ? 1 : NEPI / 4, KST, WIN, ASM>;
+    using C = TsCfg<BN, (EM & EM_CSPLIT) ? 1 : NEPI / 4, KST, WIN, ASM, (EM & EM_A6) != 0>;
     int64_t acc_bound = 0;   // K * max |pl[a] * ql[b]|
     for (int a = 0; a < 4; ++a)
         for (int b = 0; b < 4; ++b) {
@@ -1874,6 +1876,8 @@ dg_status lut_gemm_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t l
         if (em == 1) return launch_ts<256, 8, 4, 128, false, true, false, EM_CSPLIT>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         if (em == 2) return launch_ts<256, 8, 4, 128, false, true, false, EM_HIGH>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         if (em == 3) return launch_ts<256, 8, 4, 128, false, true, false, EM_CSPLIT | EM_HIGH>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (em == 4) return launch_ts<256, 8, 4, 128, false, true, false, EM_A6>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
+        if (em == 5) return launch_ts<256, 8, 4, 128, false, true, false, EM_A6 | EM_CSPLIT>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
         return launch_ts<256, 8, 4, 128, false, true>(P, ldp, Q8, ld8, np, nq, K, pl, ql, D, ldd, rq, st, cv);
     }
     // 128x256 tiles halve the shared-memory bytes of B per MAC (measured: 8192^3 1666 -> 2323

@@ -98,6 +98,52 @@ __global__ void expand_digits4_kernel(const uint8_t *__restrict__ w4, int64_t ro
     }
 }
 
+// 4-bit codes, any 256-entry table (Table 2: the 2b-bit index into a 2^(2b)-entry
+// LUT; 3-bit tables are 4-bit tables over codes 0..7): the one-hot split over the 16 weight codes,
+//     P'[m][16k + i] = [W[m][k] == i],   Q'[n][16k + i] = T[(i << 4) | A[k][n]],   K' = 16K.
+// P': packed 4-bit weights [rows][ld] -> packed 2-bit one-hot codes, 4 bytes per original code
+// (the 32-bit word 1 << (2 code)); one thread per 4 original codes (16 output bytes).
+__global__ void expand_onehot4_kernel(const uint8_t *__restrict__ w4, int64_t rows, int64_t K, int64_t ld,
+                                      uint8_t *__restrict__ out, int64_t ld_out) {
+    const int64_t groups = ld_out / 16;
+    const int64_t total = rows * groups;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / groups, g = i - r * groups;   // original codes k = 4g .. 4g + 3
+        uint32_t o[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t k = 4 * g + q;
+            const uint32_t c = k < K ? (w4[r * ld + (k >> 1)] >> (4 * (k & 1))) & 15u : 0u;
+            o[q] = k < K ? 1u << (2 * c) : 0u;
+        }
+        *reinterpret_cast<uint4 *>(out + r * ld_out + 16 * g) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
+// Q': packed 4-bit activations [rows][ld] -> int8 [rows][ld_out] of T[(i << 4) | a] at k' = 16k + i,
+// in the TS kernel's unpack order (the 16 k' of original code k as 0,2,..,14,1,3,..,15), 0 for
+// k >= K.  One thread per original code (16 output bytes).
+struct Tab256 {
+    int8_t v[256];
+};
+__global__ void expand_tcols4_kernel(const uint8_t *__restrict__ a4, int64_t rows, int64_t K, int64_t ld,
+                                     const __grid_constant__ Tab256 tab, int8_t *__restrict__ out, int64_t ld_out) {
+    const int64_t groups = ld_out / 16;
+    const int64_t total = rows * groups;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / groups, k = i - r * groups;
+        const uint32_t x = k < K ? (a4[r * ld + (k >> 1)] >> (4 * (k & 1))) & 15u : 0u;
+        uint32_t o[4] = {0, 0, 0, 0};
+#pragma unroll
+        for (int b = 0; b < 16; ++b) {
+            const int ii = b < 8 ? 2 * b : 2 * (b - 8) + 1;   // weight code i stored at byte b
+            const uint32_t v = k < K ? (uint32_t)(uint8_t)tab.v[(ii << 4) | x] : 0u;
+            o[b >> 2] |= v << (8 * (b & 3));
+        }
+        *reinterpret_cast<uint4 *>(out + r * ld_out + 16 * k) = make_uint4(o[0], o[1], o[2], o[3]);
+    }
+}
+
 int64_t grid_for(int64_t work) {
     int64_t blocks = (work + 255) / 256;
     const int64_t cap = (int64_t)num_sms() * 8;
@@ -116,6 +162,24 @@ dg_status expand_digits4(const uint8_t *w4, int64_t rows, int64_t K, int64_t ld,
 }
 
 int64_t onehot_ld(int64_t K) { return (K + 15) / 16 * 16; }
+int64_t onehot4_ld(int64_t K) { return (4 * K + 15) / 16 * 16; }
+int64_t tcols4_ld(int64_t K) { return expand_ld(16 * K); }
+
+dg_status expand_onehot4(const uint8_t *w4, int64_t rows, int64_t K, int64_t ld, uint8_t *out, int64_t ld_out,
+                         cudaStream_t st) {
+    if (rows == 0) return DG_OK;
+    expand_onehot4_kernel<<<(int)grid_for(rows * (ld_out / 16)), 256, 0, st>>>(w4, rows, K, ld, out, ld_out);
+    return launch_status();
+}
+
+dg_status expand_tcols4(const uint8_t *a4, int64_t rows, int64_t K, int64_t ld, const int32_t table[256], int8_t *out,
+                        int64_t ld_out, cudaStream_t st) {
+    Tab256 t;   // the table travels by value in the kernel parameters
+    for (int e = 0; e < 256; ++e) t.v[e] = (int8_t)table[e];
+    if (rows == 0) return DG_OK;
+    expand_tcols4_kernel<<<(int)grid_for(rows * (ld_out / 16)), 256, 0, st>>>(a4, rows, K, ld, t, out, ld_out);
+    return launch_status();
+}
 int64_t tcols_ld(int64_t K) { return expand_ld(4 * K); }
 
 dg_status expand_onehot(const uint8_t *w, int64_t rows, int64_t K, int64_t ld, uint8_t *out, int64_t ld_out,

@@ -99,6 +99,11 @@ def lib():
             "dg_lut_conv2d_prepared": ([P, P, i64, P, P, P, P, P, ctypes.c_size_t, P], i32),
             "dg_lut_conv2d_f4_prepared": ([P, P, i64, P, P, P, P, P], i32),
             "dg_float_table_fixed": ([P, P, P], i32),
+            "dg_onehot4_ld": ([i64], i64),
+            "dg_tcols4_ld": ([i64], i64),
+            "dg_expand_onehot4": ([P, i64, i64, i64, P, i64, P], i32),
+            "dg_expand_tcols4": ([P, i64, i64, i64, P, P, i64, P], i32),
+            "dg_lut_gemm4_onehot": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, P], i32),
             "dg_lut_gemm_f32_workspace_size": ([i64, i64, i64], ctypes.c_size_t),
             "dg_lut_gemm_f32": ([P, i64, P, i64, i64, i64, i64, P, P, i64, P, ctypes.c_size_t, P], i32),
         }
@@ -574,4 +579,27 @@ def lut_gemm_f32(w: torch.Tensor, at: torch.Tensor, M: int, N: int, K: int, tabl
     t = (ctypes.c_float * 16)(*[float(v) for v in table])
     _check(lib().dg_lut_gemm_f32(_ptr(w), w.shape[1], _ptr(at), at.shape[1], M, N, K, t, _ptr(out), out.stride(0),
                                  _ptr(ws), ws.numel(), _stream(stream)), "dg_lut_gemm_f32")
+    return out
+
+
+def lut_gemm4_table(w4: torch.Tensor, at4: torch.Tensor, M: int, N: int, K: int, table, rq: Requant | None = None,
+                    out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """Any 256-entry int8 table over 4-bit codes (Table 2): C[m][n] = sum_k table[(W<<4)|A]
+    via dg_expand_onehot4 + dg_expand_tcols4 + dg_lut_gemm4_onehot (K' = 16K)."""
+    _dev(w4, torch.uint8, "w4")
+    _dev(at4, torch.uint8, "at4")
+    t = (ctypes.c_int32 * 256)(*[int(v) for v in table])
+    w1h = torch.empty((M, int(lib().dg_onehot4_ld(K))), dtype=torch.uint8, device=w4.device)
+    _check(lib().dg_expand_onehot4(_ptr(w4), M, K, w4.shape[1], _ptr(w1h), w1h.shape[1], _stream(stream)),
+           "dg_expand_onehot4")
+    atc = torch.empty((N, int(lib().dg_tcols4_ld(K))), dtype=torch.int8, device=w4.device)
+    _check(lib().dg_expand_tcols4(_ptr(at4), N, K, at4.shape[1], t, _ptr(atc), atc.shape[1], _stream(stream)),
+           "dg_expand_tcols4")
+    if out is None:
+        out = (torch.empty((M, (N + 3) // 4), dtype=torch.uint8, device=w4.device) if rq is not None
+               else torch.empty((M, N), dtype=torch.int32, device=w4.device))
+    r = rq.c() if rq is not None else None
+    _check(lib().dg_lut_gemm4_onehot(_ptr(w1h), w1h.shape[1], _ptr(atc), atc.shape[1], M, N, K, t, _ptr(out),
+                                     out.shape[1], ctypes.byref(r) if r is not None else None, _stream(stream)),
+           "dg_lut_gemm4_onehot")
     return out

@@ -1031,3 +1031,45 @@ def test_gemm3_bit_codes_in_4bit_storage(M, N, K):
     at4 = dg.pack_codes4(torch.from_numpy(np.ascontiguousarray(A.T)).to(DEV))
     Ct = host(dg.lut_gemm4_prepared(at4, dg.expand_digits4(w4, K, wl16), N, M, K, wl16))
     assert np.array_equal(Ct, oracle.lut_gemm_bits(W, A, T3, 3).T)
+
+
+@pytest.mark.parametrize("kind", ["random", "nonaffine_product", "three_bit"])
+@pytest.mark.parametrize("M,N,K", [(64, 196, 576), (33, 70, 301)])
+def test_gemm4_general_table_onehot(kind, M, N, K):
+    """Any 256-entry int8 table over 4-bit codes (Table 2) on the one-hot K' = 16K path, vs the
+    b-bit oracle: random non-product tables, products with NON-affine activation levels (which the
+    digit path cannot take) and 3-bit tables embedded in 4-bit codes; int32 and fused requant."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    g = np.random.default_rng(M + N + K + len(kind))
+    if kind == "random":
+        T = g.integers(-127, 128, 256).astype(np.int32)
+        W = g.integers(0, 16, (M, K), dtype=np.uint8)
+        A = g.integers(0, 16, (K, N), dtype=np.uint8)
+        exp = oracle.lut_gemm_bits(W, A, T, 4)
+    elif kind == "nonaffine_product":
+        wl = g.integers(-11, 12, 16)
+        al = np.sort(g.integers(0, 12, 16))                  # non-uniform activation levels
+        T = np.outer(wl, al).reshape(-1).astype(np.int32)
+        W = g.integers(0, 16, (M, K), dtype=np.uint8)
+        A = g.integers(0, 16, (K, N), dtype=np.uint8)
+        exp = oracle.lut_gemm_bits(W, A, T, 4)
+    else:
+        T3 = g.integers(-127, 128, 64).astype(np.int32)    # 3-bit: 6-bit index (w << 3) | a
+        T = np.zeros(256, np.int32)
+        for w in range(8):
+            for a in range(8):
+                T[(w << 4) | a] = T3[(w << 3) | a]
+        W = g.integers(0, 8, (M, K), dtype=np.uint8)
+        A = g.integers(0, 8, (K, N), dtype=np.uint8)
+        exp = oracle.lut_gemm_bits(W, A, T3, 3)
+    w4 = dg.pack_codes4(torch.from_numpy(W).to(DEV))
+    at4 = dg.pack_codes4(torch.from_numpy(np.ascontiguousarray(A.T)).to(DEV))
+    C = host(dg.lut_gemm4_table(w4, at4, M, N, K, T))
+    assert np.array_equal(C, exp)
+    mu = int(np.round(exp.mean()))
+    rq = dg.Requant(max(1, int((1 << 20) / max(1.0, exp.std()))), 20, 1, 0, 3,
+                    bias=torch.full((N,), -mu, dtype=torch.int32, device=DEV), bias_axis=0)
+    codes = dg.lut_gemm4_table(w4, at4, M, N, K, T, rq=rq)
+    expc = oracle.requantize(exp, rq.mult, 20, 1, 0, 3, bias=np.full(N, -mu, np.int32), bias_axis=0)
+    assert np.array_equal(oracle_codes_of(codes, M, N), expc)
