@@ -279,16 +279,21 @@ def run_conv(args, ws, rank, local):
     # per-layer roofline t_roof = max(ops / int8 peak, algorithmic bytes / HBM): the fraction of it
     # the measured GEMM times reach (HBM-bound 1x1 layers count against bandwidth)
     t_roof = 0.0
-    for p_ in runner.plans:
+    for p_ in runner.plans:   # (layers on the FP4 conv kernel against the e2m1 peak, 2 x int8)
         lb = p_.x.numel() + p_.w.numel() + p_.out.numel()
-        t_roof += max(p_.ops / (pk["i8_burst"] * 1e12), lb / (pk["hbm_gbs"] * 1e9))
+        peak_l = pk["i8_burst"] * (2.0 if p_.w4 is not None else 1.0)
+        t_roof += max(p_.ops / (peak_l * 1e12), lb / (pk["hbm_gbs"] * 1e9))
+    n_f4 = sum(1 for p_ in runner.plans if p_.w4 is not None)
     frac_layer = t_roof / (ms * 1e-3)
-    roof = {"bound": "tensor", "kernel": "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)",
+    roof = {"bound": "tensor",
+            "kernel": "lut_gemm_ts_kernel (tcgen05 kind::i8, A in TMEM)" + (
+                f" + lut_conv_f4_kernel (kind::mxf4) on {n_f4} of {nl} layers" if n_f4 else ""),
             "achieved": round(achieved, 1), "peak": round(pk["i8_burst"], 1), "unit": "TOPS",
             "frac": round(achieved / pk["i8_burst"], 4),
             "frac_vs_sustained_peak": round(achieved / pk["i8_sustained"], 4),
-            "peak_src": pk["src"] + ": int8 = 2 x bf16 burst (nominal 4.5/2.25); conservative vs the sustained figure",
-            "achieved_src": "sum of the step's GEMM ops / step time over the timed region (CUDA events on the launching stream; the step is only lut_gemm_ts_kernel launches)",
+            "peak_src": pk["src"] + ": int8 = 2 x bf16 burst (nominal 4.5/2.25); conservative vs the sustained figure"
+                        " (and vs the e2m1 peak of the FP4 layers: frac_vs_layer_roofline uses 2 x int8 for them)",
+            "achieved_src": "sum of the step's GEMM ops / step time over the timed region (CUDA events on the launching stream; the step is only the layers' GEMM kernel launches)",
             "instrumented_gemm_ms_sum": round(gemm_total_ms, 4),
             "frac_vs_layer_roofline": round(frac_layer, 4),
             "i8_mma_ceiling": None, "frac_vs_i8_mma_ceiling": None,
