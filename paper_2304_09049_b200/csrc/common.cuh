@@ -202,7 +202,6 @@ enum OptId {
     OPT_EM,             // epilogue mode of the short-K wide kernel: 0 alternate tiles, 1 column split, 2 high priority, 3 both
     OPT_TMA_STORE,      // int32 output tiles through the TMA tensor store where the instance has staging: 1 on, 0 off
     OPT_UNP,            // unpack warps of the 128x256 long-K instance: 8 (default), 12 or 16
-    OPT_F4_TA,          // FP4 conv kernel: A operand in tensor memory (1) or shared memory (0)
     OPT_F4_UNP,         // FP4 conv kernel unpack warps: 0 auto (4 direct, 8 gathered), 4 or 8
     OPT_COUNT
 };

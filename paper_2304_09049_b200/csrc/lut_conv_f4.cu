@@ -105,11 +105,53 @@ struct CfArgs {
 
 __device__ __align__(16) uint8_t g_cf_pad[4][32];
 
+
+// int32 output, or a ragged last column tile with requant (exact 64-bit path): out of line, so that
+// the common 16-bit loop stays compact (instruction-cache misses were a top stall of this kernel)
+__device__ __noinline__ void cf_epilogue_general(const CfArgs &fa, const RequantArgs &rq, uint32_t trow, int64_t p,
+                                                 int64_t q0) {
+    uint32_t origin[32];
+#pragma unroll
+    for (int j = 0; j < 32; ++j) origin[j] = CF_ACC0;
+#pragma unroll 1
+    for (int c = 0; c < CF_BN / 32; ++c) {
+        uint32_t v[32];
+        ptx::tmem_ld_32x32b_x32(trow + 32 * c, v);
+        ptx::tmem_ld_wait();
+        ptx::tmem_st_32x32b_x32(trow + 32 * c, origin);
+        const int64_t qc = q0 + c * 32;
+        if (p >= fa.np || qc >= fa.nq) continue;
+        int32_t a[32];
+#pragma unroll
+        for (int j = 0; j < 32; ++j) a[j] = (int32_t)(v[j] - CF_ACC0);
+        if (!fa.has_rq) {
+            int32_t *dp = reinterpret_cast<int32_t *>(fa.D) + p * fa.ldd + qc;
+            if (qc + 32 <= fa.nq && (reinterpret_cast<uintptr_t>(dp) & 15) == 0) {
+#pragma unroll
+                for (int j = 0; j < 32; j += 4) *reinterpret_cast<int4 *>(dp + j) = make_int4(a[j], a[j + 1], a[j + 2], a[j + 3]);
+            } else {
+                for (int j = 0; j < 32; ++j)
+                    if (qc + j < fa.nq) dp[j] = a[j];
+            }
+        } else {
+            uint32_t o0 = 0, o1 = 0;
+            for (int j = 0; j < 32; ++j)
+                if (qc + j < fa.nq) {
+                    const uint32_t cd = requant_one(rq, a[j], p, qc + j);
+                    if (j < 16) o0 |= cd << (2 * j);
+                    else o1 |= cd << (2 * (j - 16));
+                }
+            store_codes32_ts(reinterpret_cast<uint8_t *>(fa.D) + p * fa.ldd + (qc >> 2), o0, o1,
+                             (int)((fa.nq - qc + 3) / 4 < 8 ? (fa.nq - qc + 3) / 4 : 8));
+        }
+    }
+}
+
 // TA: A stages in tensor memory (two accumulators, six 32-column A stages) instead of shared memory
 // (three accumulators, four 16 KB SW128 stages written with st.shared)
 // NUNP: unpack warps, 4 (one group) or 8 (two groups of 4 owning alternate stages, each with its
 // own gather ring: more gathers in flight for the implicit convolutions)
-template <bool TA, int NUNP>
+template <bool TA, int NUNP, bool DIRECT>
 __global__ void __launch_bounds__(32 * (7 + NUNP), 1)
 lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CfArgs fa, const __grid_constant__ RequantArgs rq) {
@@ -138,7 +180,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 
     if (warp == CF_PROD) {
         if (lane == 0) {
-            if (fa.direct) ptx::tma_prefetch(&tm_p);
+            if (DIRECT) ptx::tma_prefetch(&tm_p);
             ptx::tma_prefetch(&tm_b);
             for (int s = 0; s < CF_SP; ++s) {
                 ptx::mbar_init(full_p(s), 1);
@@ -185,12 +227,12 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 
     if (warp == CF_PROD) {
         // (weights are read before the programmatic-dependent-launch wait only under early_weights)
-        if (!fa.early_b || fa.direct) ptx::griddep_wait();
+        if (!fa.early_b || DIRECT) ptx::griddep_wait();
         uint32_t gp = 0, gb = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int tq = t % fa.ntq, tp = t / fa.ntq;
             for (int s = 0; s < fa.nstages; ++s, ++gb) {
-                if (fa.direct && (s & 1) == 0) {   // a packed slot = 2 stages of every pixel row
+                if (DIRECT && (s & 1) == 0) {   // a packed slot = 2 stages of every pixel row
                     const int ps = (int)(gp % CF_SP);
                     ptx::mbar_wait(empty_p(ps), ((gp / CF_SP) & 1u) ^ 1u);
                     if (lane == 0) {
@@ -297,7 +339,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
             ptx::cp_async_commit();
         };
-        if (!fa.direct) {
+        if (!DIRECT) {
             if (gt < ntiles) pixel();
             settle();
             for (int i = 0; i < IGG; ++i) fetch(i);
@@ -306,11 +348,11 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             for (int s = 0; s < fa.nstages; ++s, ++g) {
                 const bool slot_end = (s & 1) == 1 || s == fa.nstages - 1;   // last stage of a packed slot
                 if (NG > 1 && (int)(g % NG) != grp) {   // another group's stage: slot bookkeeping only
-                    if (fa.direct && slot_end) ++gp;
+                    if (DIRECT && slot_end) ++gp;
                     continue;
                 }
                 uint4 v[4];
-                if (fa.direct) {
+                if (DIRECT) {
                     const int ps = (int)(gp % CF_SP), sub = s & 1;
                     ptx::mbar_wait(full_p(ps), (gp / CF_SP) & 1u);
                     const uint32_t pbase = sbase + CF_OFF_P + ps * CF_P_SLOT;
@@ -431,39 +473,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     }
                 }
             } else {   // int32 output, or the ragged last column tile with requant (exact 64-bit path)
-#pragma unroll 1
-                for (int c = 0; c < CF_BN / 32; ++c) {
-                    uint32_t v[32];
-                    ptx::tmem_ld_32x32b_x32(trow + 32 * c, v);
-                    ptx::tmem_ld_wait();
-                    ptx::tmem_st_32x32b_x32(trow + 32 * c, origin);
-                    const int64_t qc = q0 + c * 32;
-                    if (p >= fa.np || qc >= fa.nq) continue;
-                    int32_t a[32];
-#pragma unroll
-                    for (int j = 0; j < 32; ++j) a[j] = (int32_t)(v[j] - CF_ACC0);
-                    if (!fa.has_rq) {
-                        int32_t *dp = reinterpret_cast<int32_t *>(fa.D) + p * fa.ldd + qc;
-                        if (qc + 32 <= fa.nq && (reinterpret_cast<uintptr_t>(dp) & 15) == 0) {
-#pragma unroll
-                            for (int j = 0; j < 32; j += 4) *reinterpret_cast<int4 *>(dp + j) = make_int4(a[j], a[j + 1], a[j + 2], a[j + 3]);
-                        } else {
-                            for (int j = 0; j < 32; ++j)
-                                if (qc + j < fa.nq) dp[j] = a[j];
-                        }
-                    } else {
-                        uint32_t o0 = 0, o1 = 0;
-#pragma unroll
-                        for (int j = 0; j < 32; ++j)
-                            if (qc + j < fa.nq) {
-                                const uint32_t cd = requant_one(rq, a[j], p, qc + j);
-                                if (j < 16) o0 |= cd << (2 * j);
-                                else o1 |= cd << (2 * (j - 16));
-                            }
-                        store_codes32_ts(reinterpret_cast<uint8_t *>(fa.D) + p * fa.ldd + (qc >> 2), o0, o1,
-                                         (int)((fa.nq - qc + 3) / 4 < 8 ? (fa.nq - qc + 3) / 4 : 8));
-                    }
-                }
+                cf_epilogue_general(fa, rq, trow, p, q0);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -587,13 +597,14 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     memset(&mp, 0, sizeof(mp));
     if (direct && !cf_map(&mp, x, cb, cb, rows, CF_BM)) return DG_ERR_CUDA;
     if (!cf_map(&mb, w4, ld4, ld4, cout, CF_BN)) return DG_ERR_CUDA;
-    const bool ta = opt(OPT_F4_TA) != 0;
+    // (the shared-memory-A form, TA = false, measured 5-20 % slower: kept in the source, not built)
+    const bool ta = true;
     const int nunp = (int)opt(OPT_F4_UNP) == 4 ? 4 : ((int)opt(OPT_F4_UNP) == 8 ? 8 : (direct ? 4 : 8));
     void (*kern)(const CUtensorMap, const CUtensorMap, const CfArgs, const RequantArgs) =
-        ta ? (nunp == 8 ? lut_conv_f4_kernel<true, 8> : lut_conv_f4_kernel<true, 4>)
-           : (nunp == 8 ? lut_conv_f4_kernel<false, 8> : lut_conv_f4_kernel<false, 4>);
+        direct ? (nunp == 8 ? lut_conv_f4_kernel<true, 8, true> : lut_conv_f4_kernel<true, 4, true>)
+               : (nunp == 8 ? lut_conv_f4_kernel<true, 8, false> : lut_conv_f4_kernel<true, 4, false>);
     static bool attr[4] = {false, false, false, false};
-    const int ai = (ta ? 2 : 0) + (nunp == 8 ? 1 : 0);
+    const int ai = (direct ? 2 : 0) + (nunp == 8 ? 1 : 0);
     if (!attr[ai]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF_ALLOC) != cudaSuccess)
             return DG_ERR_CUDA;

@@ -18,7 +18,7 @@ L = synth.resnet50_layers()[li]
 T = oracle.build_lut16(synth.WL_UNIFORM, synth.AL_UNIFORM)
 x = synth.counter_codes_host(0, 256 * L.h * L.h * L.cin, (3, li, synth.T_X), "relu").reshape(256, L.h, L.h, L.cin)
 w = synth.counter_codes_host(0, L.cout * L.k * L.k * L.cin, (3, li, synth.T_W), "uniform").reshape(L.cout, L.k, L.k, L.cin)
-for opts in [dict(), dict(f4_ta=0)][: int(os.environ.get('NOPTS', '2'))]:
+for opts in [dict(), dict(f4_unp=8)][: int(os.environ.get('NOPTS', '2'))]:
     dg.reset_options()
     for k, v in opts.items():
         dg.set_option(k, v)
