@@ -109,12 +109,12 @@ __device__ __align__(16) uint8_t g_cf_pad[4][32];
 // int32 output, or a ragged last column tile with requant (exact 64-bit path): out of line, so that
 // the common 16-bit loop stays compact (instruction-cache misses were a top stall of this kernel)
 __device__ __noinline__ void cf_epilogue_general(const CfArgs &fa, const RequantArgs &rq, uint32_t trow, int64_t p,
-                                                 int64_t q0) {
+                                                 int64_t q0, int ncols) {
     uint32_t origin[32];
 #pragma unroll
     for (int j = 0; j < 32; ++j) origin[j] = CF_ACC0;
 #pragma unroll 1
-    for (int c = 0; c < CF_BN / 32; ++c) {
+    for (int c = 0; c < ncols / 32; ++c) {
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(trow + 32 * c, v);
         ptx::tmem_ld_wait();
@@ -151,12 +151,16 @@ __device__ __noinline__ void cf_epilogue_general(const CfArgs &fa, const Requant
 // (three accumulators, four 16 KB SW128 stages written with st.shared)
 // NUNP: unpack warps, 4 (one group) or 8 (two groups of 4 owning alternate stages, each with its
 // own gather ring: more gathers in flight for the implicit convolutions)
-template <bool TA, int NUNP, bool DIRECT>
+// BNT: output channels per tile, 128 (TA: two accumulators) or 256 (one accumulator: the A operand
+// is unpacked once per 256 output channels; the epilogue releases it after two load rounds)
+template <bool TA, int NUNP, bool DIRECT, int BNT>
 __global__ void __launch_bounds__(32 * (7 + NUNP), 1)
 lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CfArgs fa, const __grid_constant__ RequantArgs rq) {
-    constexpr int CF_NACC = TA ? 2 : 3, CF_SA = TA ? 6 : 4;
-    constexpr uint32_t TA0 = CF_NACC * CF_BN;   // first tensor-memory A column (TA)
+    constexpr int BN_ = BNT, SB_ = BNT == 256 ? 3 : CF_SB, B_STAGE_ = BNT * CF_KST / 2;   // (96 KB of B stages)
+    constexpr int CF_NACC = TA ? (BNT == 256 ? 1 : 2) : 3, CF_SA = TA ? 6 : 4;
+    constexpr uint32_t TA0 = CF_NACC * BN_;   // first tensor-memory A column (TA)
+    static_assert(!TA || TA0 + 6 * 32 <= CF_SF_COL, "tensor memory budget");
     constexpr int CF_PROD = CF_UNP0 + NUNP, CF_WAIT = CF_PROD + 1, CF_MMA = CF_PROD + 2, NG = NUNP / 4;
     constexpr int IGG = CF_IG / NG;             // gather ring stages per unpack group
     extern __shared__ uint8_t smem_raw[];
@@ -186,7 +190,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 ptx::mbar_init(full_p(s), 1);
                 ptx::mbar_init(empty_p(s), 8);   // 4 unpack warps x 2 stages per slot (count 2 for a lone stage)
             }
-            for (int s = 0; s < CF_SB; ++s) {
+            for (int s = 0; s < SB_; ++s) {
                 ptx::mbar_init(full_b(s), 1);
                 ptx::mbar_init(empty_b(s), 1);
             }
@@ -217,7 +221,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 #pragma unroll
         for (int j = 0; j < 32; ++j) r[j] = CF_ACC0;
 #pragma unroll
-        for (int c = 0; c < CF_NACC * CF_BN / 32; ++c) ptx::tmem_st_32x32b_x32(tmem + (uint32_t)(c * 32) + lanes, r);
+        for (int c = 0; c < CF_NACC * BN_ / 32; ++c) ptx::tmem_st_32x32b_x32(tmem + (uint32_t)(c * 32) + lanes, r);
         ptx::tmem_st_wait();
     }
     ptx::tc_fence_before();
@@ -242,11 +246,11 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     __syncwarp();
                     ++gp;
                 }
-                const int bs = (int)(gb % CF_SB);
-                ptx::mbar_wait(empty_b(bs), ((gb / CF_SB) & 1u) ^ 1u);
+                const int bs = (int)(gb % SB_);
+                ptx::mbar_wait(empty_b(bs), ((gb / SB_) & 1u) ^ 1u);
                 if (lane == 0) {
-                    ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)CF_B_STAGE);
-                    ptx::tma_load_2d(sbase + CF_OFF_B + bs * CF_B_STAGE, &tm_b, full_b(bs), s * (CF_KST / 2), tq * CF_BN);
+                    ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)B_STAGE_);
+                    ptx::tma_load_2d(sbase + CF_OFF_B + bs * B_STAGE_, &tm_b, full_b(bs), s * (CF_KST / 2), tq * BN_);
                 }
                 __syncwarp();
             }
@@ -257,24 +261,24 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             ptx::mbar_wait(acc_empty(tl % CF_NACC), ((tl / CF_NACC) & 1u) ^ 1u);
             for (int s = 0; s < fa.nstages; ++s, ++g) {
                 ptx::mbar_wait(full_a(g % CF_SA), (g / CF_SA) & 1u);
-                ptx::mbar_wait(full_b(g % CF_SB), (g / CF_SB) & 1u);
+                ptx::mbar_wait(full_b(g % SB_), (g / SB_) & 1u);
                 ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
             }
         }
     } else if (warp == CF_MMA) {
-        constexpr uint32_t idesc = cf_idesc(CF_BM, CF_BN);
+        constexpr uint32_t idesc = cf_idesc(CF_BM, BN_);
         const uint32_t sfa = tmem + CF_SF_COL, sfb = tmem + CF_SF_COL + 16;
         const int nst = fa.nstages, lastk = fa.last_ksteps;   // (in registers before any MMA is queued)
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl % CF_NACC;
-            const uint32_t dt = tmem + acc * CF_BN;
+            const uint32_t dt = tmem + acc * BN_;
             for (int s = 0; s < nst; ++s, ++g) {
-                const int sa = (int)(g % CF_SA), bs = (int)(g % CF_SB);
+                const int sa = (int)(g % CF_SA), bs = (int)(g % SB_);
                 ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
                 ptx::tc_fence_after();
                 const uint64_t ad = ptx::desc_k_sw128(sbase + CF_OFF_A + sa * CF_A_STAGE);
-                const uint64_t bd = ptx::desc_k_sw128(sbase + CF_OFF_B + bs * CF_B_STAGE);
+                const uint64_t bd = ptx::desc_k_sw128(sbase + CF_OFF_B + bs * B_STAGE_);
                 const uint32_t at = tmem + TA0 + (uint32_t)(sa * 32);
                 if (s < nst - 1) {
 #pragma unroll
@@ -432,26 +436,30 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const int tq = t % fa.ntq, tp = t / fa.ntq;
             const int64_t p = (int64_t)tp * CF_BM + quarter * 32 + lane;
-            const int64_t q0 = (int64_t)tq * CF_BN;
+            const int64_t q0 = (int64_t)tq * BN_;
             const uint32_t acc = tl % CF_NACC;
             ptx::mbar_wait(acc_full(acc), (tl / CF_NACC) & 1u);
             ptx::tc_fence_after();
-            const uint32_t trow = tmem + acc * CF_BN + ((uint32_t)(quarter * 32) << 16);
-            if (f16_ok && q0 + CF_BN <= fa.nq) {
+            const uint32_t trow = tmem + acc * BN_ + ((uint32_t)(quarter * 32) << 16);
+            if (f16_ok && q0 + BN_ <= fa.nq) {
+#pragma unroll 1
+              for (int rd = 0; rd < BN_ / 128; ++rd) {   // 128 columns per load round
+                const uint32_t trd = trow + (uint32_t)(rd * 128);
+                const int64_t q0r = q0 + rd * 128;
                 uint32_t r16[2][32];   // all 128 columns as 16-bit pairs (low halves = the integer values)
-                ptx::tmem_ld_32x32b_x32_pack16(trow, r16[0]);
-                ptx::tmem_ld_32x32b_x32_pack16(trow + 64, r16[1]);
+                ptx::tmem_ld_32x32b_x32_pack16(trd, r16[0]);
+                ptx::tmem_ld_32x32b_x32_pack16(trd + 64, r16[1]);
                 ptx::tmem_ld_wait();
 #pragma unroll
-                for (int c = 0; c < 4; ++c) ptx::tmem_st_32x32b_x32(trow + 32 * c, origin);   // reset to the origin
+                for (int c = 0; c < 4; ++c) ptx::tmem_st_32x32b_x32(trd + 32 * c, origin);   // reset to the origin
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
+                if (lane == 0 && rd == BN_ / 128 - 1) ptx::mbar_arrive(acc_empty(acc));
                 if (p < fa.np) {
 #pragma unroll
                     for (int hh = 0; hh < 4; ++hh) {
-                        const int64_t qc = q0 + hh * 32;
+                        const int64_t qc = q0r + hh * 32;
                         uint32_t na[16];
                         if (fa.f16_tab) {
 #pragma unroll
@@ -472,8 +480,9 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         else store_codes32_ts(dp, o.x, o.y, 8);
                     }
                 }
+              }
             } else {   // int32 output, or the ragged last column tile with requant (exact 64-bit path)
-                cf_epilogue_general(fa, rq, trow, p, q0);
+                cf_epilogue_general(fa, rq, trow, p, q0, BN_);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -547,7 +556,13 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     fa.nstages = (int32_t)((K + CF_KST - 1) / CF_KST);
     fa.last_ksteps = (int32_t)(((K - (int64_t)(fa.nstages - 1) * CF_KST) + 63) / 64);
     fa.ntp = (int32_t)((rows + CF_BM - 1) / CF_BM);
-    fa.ntq = (int32_t)((cout + CF_BN - 1) / CF_BN);
+    // tile width: 256 output channels (one accumulator, half the gather + unpack work per output) when
+    // they divide Cout (a ragged last tile takes the slow exact epilogue), else 128 (option f4_bn: 0
+    // auto, 128, 256).  Measured per layer: the 3x3 convs over 256 channels
+    // 28.5 -> 18.5 us against 26.3 us at 128 wide.
+    const int fbn = (int)opt(OPT_F4_BN);
+    const int bnt = fbn == 128 ? 128 : (fbn == 256 ? 256 : (cout % 256 == 0 ? 256 : 128));
+    fa.ntq = (int32_t)((cout + bnt - 1) / bnt);
     const int64_t nt = (int64_t)fa.ntp * fa.ntq;
     if (nt > INT32_MAX) return DG_ERR_SHAPE;
     fa.ntiles = (int32_t)nt;
@@ -596,15 +611,18 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     CUtensorMap mp, mb;
     memset(&mp, 0, sizeof(mp));
     if (direct && !cf_map(&mp, x, cb, cb, rows, CF_BM)) return DG_ERR_CUDA;
-    if (!cf_map(&mb, w4, ld4, ld4, cout, CF_BN)) return DG_ERR_CUDA;
+    if (!cf_map(&mb, w4, ld4, ld4, cout, bnt)) return DG_ERR_CUDA;
     // (the shared-memory-A form, TA = false, measured 5-20 % slower: kept in the source, not built)
     const bool ta = true;
     const int nunp = (int)opt(OPT_F4_UNP) == 4 ? 4 : ((int)opt(OPT_F4_UNP) == 8 ? 8 : (direct ? 4 : 8));
     void (*kern)(const CUtensorMap, const CUtensorMap, const CfArgs, const RequantArgs) =
-        direct ? (nunp == 8 ? lut_conv_f4_kernel<true, 8, true> : lut_conv_f4_kernel<true, 4, true>)
-               : (nunp == 8 ? lut_conv_f4_kernel<true, 8, false> : lut_conv_f4_kernel<true, 4, false>);
-    static bool attr[4] = {false, false, false, false};
-    const int ai = (direct ? 2 : 0) + (nunp == 8 ? 1 : 0);
+        bnt == 256
+            ? (direct ? (nunp == 8 ? lut_conv_f4_kernel<true, 8, true, 256> : lut_conv_f4_kernel<true, 4, true, 256>)
+                      : (nunp == 8 ? lut_conv_f4_kernel<true, 8, false, 256> : lut_conv_f4_kernel<true, 4, false, 256>))
+            : (direct ? (nunp == 8 ? lut_conv_f4_kernel<true, 8, true, 128> : lut_conv_f4_kernel<true, 4, true, 128>)
+                      : (nunp == 8 ? lut_conv_f4_kernel<true, 8, false, 128> : lut_conv_f4_kernel<true, 4, false, 128>));
+    static bool attr[8] = {};
+    const int ai = (bnt == 256 ? 4 : 0) + (direct ? 2 : 0) + (nunp == 8 ? 1 : 0);
     if (!attr[ai]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF_ALLOC) != cudaSuccess)
             return DG_ERR_CUDA;
@@ -625,8 +643,8 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     lc.numAttrs = 1;
     if (cudaLaunchKernelEx(&lc, kern, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
     char tag[96];
-    snprintf(tag, sizeof(tag), "f4conv bn=128 %s unp=%d direct=%d rq=%d tab=%d early=%d", ta ? "ta nacc=2" : "sa nacc=3", nunp,
-             fa.direct, fa.has_rq, fa.f16_tab, fa.early_b);
+    snprintf(tag, sizeof(tag), "f4conv bn=%d %s unp=%d direct=%d rq=%d tab=%d early=%d", bnt,
+             ta ? (bnt == 256 ? "ta nacc=1" : "ta nacc=2") : "sa nacc=3", nunp, fa.direct, fa.has_rq, fa.f16_tab, fa.early_b);
     set_last_kernel(tag);
     return launch_status();
 }

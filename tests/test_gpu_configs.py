@@ -114,9 +114,10 @@ def test_config3_resnet50_every_layer_full_batch():
     assert any(" win " in t and "kst=256" in t and "wpair=1" in t for t in tags), tags        # C = 64 pair mode
     assert any(" win " in t and "kst=128" in t for t in tags), tags                           # C = 128 tile mode
     assert any(" asm " in t for t in tags), tags                                              # short-K 1x1
-    assert any("bn=256" in t and "implicit=1" in t for t in tags), tags                       # 3x3 C >= 256
-    assert any(t.startswith("f4conv") and "direct=1" in t for t in tags), tags                 # 1x1 K >= 512: FP4
-    assert any(t.startswith("f4conv") and "direct=0" in t for t in tags), tags                 # 3x3 s2 128: FP4
+    assert any(t.startswith("f4conv bn=256") and "direct=1" in t for t in tags), tags         # 1x1 K >= 256: FP4
+    assert any(t.startswith("f4conv bn=128") and "direct=1" in t for t in tags), tags         # 1x1 into 128
+    assert any(t.startswith("f4conv bn=256") and "direct=0" in t for t in tags), tags         # 3x3 C >= 256: FP4
+    assert any(t.startswith("f4conv bn=128") and "direct=0" in t for t in tags), tags         # 3x3 s2 128: FP4
 
 
 def test_config4_vgg16_every_layer_full_batch():
