@@ -104,6 +104,7 @@ DG_API uint64_t dg_kernel_launches(void);
  *               instead of per-lane row stores, where the instance has room (1)
  *   "unp"       unpack warps of the 128x256 long-K int8 instance: 8, 12 or 16 (8)
  *   "f4_unp"    unpack warps of the FP4 conv kernel: 0 auto, 4 or 8         (0)
+ *   "f4_epi"    epilogue warps of the FP4 conv kernel: 0 auto, 4 or 8       (0)
  *   "f4_bn"     FP4 conv tile width: 0 auto (256 when it divides Cout), 128, 256 (0)
  */
 DG_API dg_status dg_set_option(const char *name, int64_t value);

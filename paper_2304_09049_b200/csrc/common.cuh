@@ -203,6 +203,7 @@ enum OptId {
     OPT_TMA_STORE,      // int32 output tiles through the TMA tensor store where the instance has staging: 1 on, 0 off
     OPT_UNP,            // unpack warps of the 128x256 long-K instance: 8 (default), 12 or 16
     OPT_F4_UNP,         // FP4 conv kernel unpack warps: 0 auto (4 direct, 8 gathered), 4 or 8
+    OPT_F4_EPI,         // FP4 conv kernel epilogue warps: 0 auto, 4 or 8
     OPT_F4_BN,          // FP4 conv tile width: 0 auto (256 when 256 | Cout), 128 or 256
     OPT_COUNT
 };

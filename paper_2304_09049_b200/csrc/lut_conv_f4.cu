@@ -47,7 +47,7 @@ constexpr int CF_OFF_TMEM = CF_OFF_BAR + CF_NBAR * 8;
 constexpr int CF_OFF_TAB = (CF_OFF_TMEM + 16 + 15) / 16 * 16;
 constexpr int CF_ALLOC = CF_OFF_TAB + CF_TAB_PAIRS * 4 + 1024;
 static_assert(CF_ALLOC <= 232448, "shared memory budget");
-constexpr int CF_UNP0 = 4;   // unpack warps 4 .. 4 + NUNP - 1, then producer, waiter, MMA issuer
+// warps: NEPI epilogue warps, then the unpack warps NEPI .. NEPI + NUNP - 1, then producer, waiter, MMA issuer
 constexpr int CF_HANDOFF_BAR = 1, CF_EPI_BAR = 2;
 constexpr uint32_t CF_SF_COL = 480;                // TMEM columns [480, 512): block scales (every byte 2^1)
 constexpr uint32_t CF_ACC0 = 0x4B400000u;          // fp32 1.5 * 2^23: the accumulators' integer origin
@@ -153,14 +153,19 @@ __device__ __noinline__ void cf_epilogue_general(const CfArgs &fa, const Requant
 // own gather ring: more gathers in flight for the implicit convolutions)
 // BNT: output channels per tile, 128 (TA: two accumulators) or 256 (one accumulator: the A operand
 // is unpacked once per 256 output channels; the epilogue releases it after two load rounds)
-template <bool TA, int NUNP, bool DIRECT, int BNT>
-__global__ void __launch_bounds__(32 * (7 + NUNP), 1)
+// NEPI: epilogue warps, 4 (one per lane quarter) or 8: two groups, which split each 256-wide tile's
+// columns (each group loads its 128 columns and releases them: the single accumulator is free after
+// one load round) or own alternate tiles of the 128-wide kernel's two accumulators
+template <bool TA, int NUNP, bool DIRECT, int BNT, int NEPI>
+__global__ void __launch_bounds__(32 * (3 + NEPI + NUNP), 1)
 lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CfArgs fa, const __grid_constant__ RequantArgs rq) {
     constexpr int BN_ = BNT, SB_ = BNT == 256 ? 3 : CF_SB, B_STAGE_ = BNT * CF_KST / 2;   // (96 KB of B stages)
     constexpr int CF_NACC = TA ? (BNT == 256 ? 1 : 2) : 3, CF_SA = TA ? 6 : 4;
     constexpr uint32_t TA0 = CF_NACC * BN_;   // first tensor-memory A column (TA)
     static_assert(!TA || TA0 + 6 * 32 <= CF_SF_COL, "tensor memory budget");
+    constexpr int CF_UNP0 = NEPI;
+    constexpr bool CSPLIT = NEPI == 8 && BNT == 256;   // the two epilogue groups split every tile's columns
     constexpr int CF_PROD = CF_UNP0 + NUNP, CF_WAIT = CF_PROD + 1, CF_MMA = CF_PROD + 2, NG = NUNP / 4;
     constexpr int IGG = CF_IG / NG;             // gather ring stages per unpack group
     extern __shared__ uint8_t smem_raw[];
@@ -200,7 +205,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
             for (int a = 0; a < CF_NACC; ++a) {
                 ptx::mbar_init(acc_full(a), 1);
-                ptx::mbar_init(acc_empty(a), 4);
+                ptx::mbar_init(acc_empty(a), CSPLIT ? 8 : 4);
             }
             ptx::fence_mbar_init();
         }
@@ -413,49 +418,49 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         }
     } else {
         // ---------------- epilogue (lane quarter = warp)
-        const int quarter = warp;
+        const int quarter = warp & 3, eg = warp >> 2;
         if (!fa.early_b) ptx::griddep_wait();   // (the bias may come from the previous kernel)
         if (fa.has_rq && fa.f16_tab) {   // per-column 16-bit offsets: negA = bias - (thr0 - 1)
             uint32_t bad = 0;
-            for (int i = threadIdx.x; i < (int)(fa.nq >> 1); i += 128) {
+            for (int i = threadIdx.x; i < (int)(fa.nq >> 1); i += NEPI * 32) {
                 const int64_t n0 = (int64_t)__ldg(rq.bias + 2 * i) - fa.f16_thr0m1;
                 const int64_t n1 = (int64_t)__ldg(rq.bias + 2 * i + 1) - fa.f16_thr0m1;
                 if ((n0 < 0 ? -n0 : n0) + fa.f16_accmax > 32767 || (n1 < 0 ? -n1 : n1) + fa.f16_accmax > 32767) bad = 1;
                 tab[i] = ((uint32_t)n0 & 0xFFFFu) | ((uint32_t)n1 << 16);
             }
             if (bad) *f16_bad = 1u;   // some offset overflows int16: every tile takes the exact path
-            ptx::named_bar_sync(CF_EPI_BAR, 128);
+            ptx::named_bar_sync(CF_EPI_BAR, NEPI * 32);
         }
         const bool f16_ok = fa.has_rq && *f16_bad == 0u;
         ptx::griddep_wait();
         const uint32_t tabs = sbase + CF_OFF_TAB;
-        uint32_t origin[32];
-#pragma unroll
-        for (int j = 0; j < 32; ++j) origin[j] = CF_ACC0;
         uint32_t tl = 0;
+        constexpr int RD_N = CSPLIT ? 1 : BN_ / 128;   // 128-column load rounds per warp and tile
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            if (NEPI == 8 && !CSPLIT && (int)(tl & 1u) != eg) continue;   // the other group's accumulator
             const int tq = t % fa.ntq, tp = t / fa.ntq;
             const int64_t p = (int64_t)tp * CF_BM + quarter * 32 + lane;
             const int64_t q0 = (int64_t)tq * BN_;
             const uint32_t acc = tl % CF_NACC;
             ptx::mbar_wait(acc_full(acc), (tl / CF_NACC) & 1u);
             ptx::tc_fence_after();
-            const uint32_t trow = tmem + acc * BN_ + ((uint32_t)(quarter * 32) << 16);
+            const int c0 = CSPLIT ? eg * 128 : 0;   // this warp's first column of the tile
+            const uint32_t trow = tmem + acc * BN_ + (uint32_t)c0 + ((uint32_t)(quarter * 32) << 16);
             if (f16_ok && q0 + BN_ <= fa.nq) {
 #pragma unroll 1
-              for (int rd = 0; rd < BN_ / 128; ++rd) {   // 128 columns per load round
+              for (int rd = 0; rd < RD_N; ++rd) {   // 128 columns per load round
                 const uint32_t trd = trow + (uint32_t)(rd * 128);
-                const int64_t q0r = q0 + rd * 128;
+                const int64_t q0r = q0 + c0 + rd * 128;
                 uint32_t r16[2][32];   // all 128 columns as 16-bit pairs (low halves = the integer values)
                 ptx::tmem_ld_32x32b_x32_pack16(trd, r16[0]);
                 ptx::tmem_ld_32x32b_x32_pack16(trd + 64, r16[1]);
                 ptx::tmem_ld_wait();
 #pragma unroll
-                for (int c = 0; c < 4; ++c) ptx::tmem_st_32x32b_x32(trd + 32 * c, origin);   // reset to the origin
+                for (int c = 0; c < 16; ++c) ptx::tmem_st_32x32b_x8_splat(trd + 8 * c, CF_ACC0);   // reset to the origin
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
-                if (lane == 0 && rd == BN_ / 128 - 1) ptx::mbar_arrive(acc_empty(acc));
+                if (lane == 0 && rd == RD_N - 1) ptx::mbar_arrive(acc_empty(acc));
                 if (p < fa.np) {
 #pragma unroll
                     for (int hh = 0; hh < 4; ++hh) {
@@ -482,7 +487,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
               }
             } else {   // int32 output, or the ragged last column tile with requant (exact 64-bit path)
-                cf_epilogue_general(fa, rq, trow, p, q0, BN_);
+                cf_epilogue_general(fa, rq, trow, p, q0 + c0, CSPLIT ? 128 : BN_);
                 ptx::tmem_st_wait();
                 ptx::tc_fence_before();
                 __syncwarp();
@@ -615,14 +620,20 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     // (the shared-memory-A form, TA = false, measured 5-20 % slower: kept in the source, not built)
     const bool ta = true;
     const int nunp = (int)opt(OPT_F4_UNP) == 4 ? 4 : ((int)opt(OPT_F4_UNP) == 8 ? 8 : (direct ? 4 : 8));
-    void (*kern)(const CUtensorMap, const CUtensorMap, const CfArgs, const RequantArgs) =
-        bnt == 256
-            ? (direct ? (nunp == 8 ? lut_conv_f4_kernel<true, 8, true, 256> : lut_conv_f4_kernel<true, 4, true, 256>)
-                      : (nunp == 8 ? lut_conv_f4_kernel<true, 8, false, 256> : lut_conv_f4_kernel<true, 4, false, 256>))
-            : (direct ? (nunp == 8 ? lut_conv_f4_kernel<true, 8, true, 128> : lut_conv_f4_kernel<true, 4, true, 128>)
-                      : (nunp == 8 ? lut_conv_f4_kernel<true, 8, false, 128> : lut_conv_f4_kernel<true, 4, false, 128>));
-    static bool attr[8] = {};
-    const int ai = (bnt == 256 ? 4 : 0) + (direct ? 2 : 0) + (nunp == 8 ? 1 : 0);
+    const int nepi = (int)opt(OPT_F4_EPI) == 4 ? 4 : 8;   // (auto: 8, measured -5..-20 % on every FP4 layer)
+    typedef void (*CfKern)(const CUtensorMap, const CUtensorMap, const CfArgs, const RequantArgs);
+    static const CfKern kerns[16] = {
+        lut_conv_f4_kernel<true, 4, false, 128, 4>, lut_conv_f4_kernel<true, 8, false, 128, 4>,
+        lut_conv_f4_kernel<true, 4, true, 128, 4>,  lut_conv_f4_kernel<true, 8, true, 128, 4>,
+        lut_conv_f4_kernel<true, 4, false, 256, 4>, lut_conv_f4_kernel<true, 8, false, 256, 4>,
+        lut_conv_f4_kernel<true, 4, true, 256, 4>,  lut_conv_f4_kernel<true, 8, true, 256, 4>,
+        lut_conv_f4_kernel<true, 4, false, 128, 8>, lut_conv_f4_kernel<true, 8, false, 128, 8>,
+        lut_conv_f4_kernel<true, 4, true, 128, 8>,  lut_conv_f4_kernel<true, 8, true, 128, 8>,
+        lut_conv_f4_kernel<true, 4, false, 256, 8>, lut_conv_f4_kernel<true, 8, false, 256, 8>,
+        lut_conv_f4_kernel<true, 4, true, 256, 8>,  lut_conv_f4_kernel<true, 8, true, 256, 8>};
+    static bool attr[16] = {};
+    const int ai = (nepi == 8 ? 8 : 0) + (bnt == 256 ? 4 : 0) + (direct ? 2 : 0) + (nunp == 8 ? 1 : 0);
+    const CfKern kern = kerns[ai];
     if (!attr[ai]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF_ALLOC) != cudaSuccess)
             return DG_ERR_CUDA;
@@ -633,7 +644,7 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     const int grid = (int)(nt < num_sms() ? nt : num_sms());
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)grid);
-    lc.blockDim = dim3((unsigned)(32 * (7 + nunp)));
+    lc.blockDim = dim3((unsigned)(32 * (3 + nepi + nunp)));
     lc.dynamicSmemBytes = CF_ALLOC;
     lc.stream = st;
     cudaLaunchAttribute la[1];
@@ -643,8 +654,8 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     lc.numAttrs = 1;
     if (cudaLaunchKernelEx(&lc, kern, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
     char tag[96];
-    snprintf(tag, sizeof(tag), "f4conv bn=%d %s unp=%d direct=%d rq=%d tab=%d early=%d", bnt,
-             ta ? (bnt == 256 ? "ta nacc=1" : "ta nacc=2") : "sa nacc=3", nunp, fa.direct, fa.has_rq, fa.f16_tab, fa.early_b);
+    snprintf(tag, sizeof(tag), "f4conv bn=%d %s unp=%d epi=%d direct=%d rq=%d tab=%d early=%d", bnt,
+             ta ? (bnt == 256 ? "ta nacc=1" : "ta nacc=2") : "sa nacc=3", nunp, nepi, fa.direct, fa.has_rq, fa.f16_tab, fa.early_b);
     set_last_kernel(tag);
     return launch_status();
 }

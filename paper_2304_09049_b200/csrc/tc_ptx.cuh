@@ -244,6 +244,11 @@ DG_DEV void tmem_st_32x32b_x32(uint32_t taddr, const uint32_t (&r)[32]) {
         "r"(r[25]), "r"(r[26]), "r"(r[27]), "r"(r[28]), "r"(r[29]), "r"(r[30]), "r"(r[31])
         : "memory");
 }
+// 32 lanes x 8 consecutive 32-bit columns, every column the same value (a reset to a constant:
+// eight registers instead of 32)
+DG_DEV void tmem_st_32x32b_x8_splat(uint32_t taddr, uint32_t v) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%1,%1,%1,%1,%1,%1,%1};" ::"r"(taddr), "r"(v) : "memory");
+}
 // 32 lanes x 32 consecutive 32-bit columns read as 16-bit halves: register i = column 2i in
 // bits [0,16) | column 2i+1 in bits [16,32) (low 16 bits of each column; measured,
 // tools/tmem_pack_test.cu)

@@ -913,13 +913,15 @@ F4_CONVS = [  # B, H, W, C, Cout, k, stride, pad, pad_code
 ]
 
 
+@pytest.mark.parametrize("epi", [4, 8])
 @pytest.mark.parametrize("bn", [128, 256])
 @pytest.mark.parametrize("wl", [(-2, -1, 0, 1), (-12, -3, 4, 8)])
 @pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", F4_CONVS)
-def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn):
-    """FP4 conv kernel vs O-CONV on both tile widths (128 channels, two accumulators; 256, one):
-    int32 output, fused 16-bit requant with a per-channel bias, a uniform-offset requant without
-    bias, and a bias whose 16-bit offsets overflow (exact path)."""
+def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn, epi):
+    """FP4 conv kernel vs O-CONV on both tile widths (128 channels, two accumulators; 256, one) and
+    both epilogue arrangements (4 warps; 8 warps splitting the 256-wide tiles' columns or owning
+    alternate 128-wide tiles): int32 output, fused 16-bit requant with a per-channel bias, a
+    uniform-offset requant without bias, and a bias whose 16-bit offsets overflow (exact path)."""
     if not _tc_available():
         pytest.skip("tc unavailable")
     wl = list(wl)
@@ -934,13 +936,13 @@ def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn):
     w4 = dg.expand_operand_f4(wp, k * k * Cp, wl)
     p = dg.conv_params(B, H, W, Cp, Cout, k, k, stride, pad, pad_code, ldw=wp.shape[1])
     dg.reset_options()
-    with dg.options(f4_bn=bn):
-        _conv_f4_cases(xp, w4, lut, p, exp, Cout, g, bn)
+    with dg.options(f4_bn=bn, f4_epi=epi):
+        _conv_f4_cases(xp, w4, lut, p, exp, Cout, g, bn, epi)
 
 
-def _conv_f4_cases(xp, w4, lut, p, exp, Cout, g, bn):
+def _conv_f4_cases(xp, w4, lut, p, exp, Cout, g, bn, epi):
     out = dg.lut_conv2d_f4_prepared(xp, w4, lut, p)
-    assert dg.last_kernel().startswith(f"f4conv bn={bn} "), dg.last_kernel()
+    assert dg.last_kernel().startswith(f"f4conv bn={bn} ") and f" epi={epi} " in dg.last_kernel(), dg.last_kernel()
     assert np.array_equal(host(out), exp)
     if Cout % 4:
         return
