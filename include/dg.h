@@ -106,6 +106,8 @@ DG_API uint64_t dg_kernel_launches(void);
  *   "f4_unp"    unpack warps of the FP4 conv kernel: 0 auto, 4 or 8         (0)
  *   "f4_epi"    epilogue warps of the FP4 conv kernel: 0 auto, 4 or 8       (0)
  *   "f4_bn"     FP4 conv tile width: 0 auto (256 when it divides Cout), 128, 256 (0)
+ *   "f4_omma"   FP4 conv accumulators start from an origin MMA (one per tile) instead of
+ *               tensor-memory reset stores                                   (1)
  */
 DG_API dg_status dg_set_option(const char *name, int64_t value);
 DG_API dg_status dg_get_option(const char *name, int64_t *value);

@@ -51,9 +51,33 @@ static_assert(CF_ALLOC <= 232448, "shared memory budget");
 constexpr int CF_HANDOFF_BAR = 1, CF_EPI_BAR = 2;
 constexpr uint32_t CF_SF_COL = 480;                // TMEM columns [480, 512): block scales (every byte 2^1)
 constexpr uint32_t CF_ACC0 = 0x4B400000u;          // fp32 1.5 * 2^23: the accumulators' integer origin
+// origin MMA (omma): A = 64 ones (e2m1 1.0) per row at TMEM columns [448, 456), B = 1.5 in every
+// element of a shared-memory block, scales 2^17 (A) and 2^0 (B): D = 64 * 1.5 * 2^17 = 1.5 * 2^23
+// exactly, written with enable-input-d = 0 as a tile's first MMA (instead of 128 KB of tcgen05.st
+// resets per 128 x 256 tile, the largest tensor-memory traffic of the short-K tiles)
+constexpr uint32_t CF_OA_COL = 448, CF_OSFA_COL = 456, CF_OSFB_COL = 464;
+
+#ifdef DG_TRACE
+// CTA 0 event timeline (tools/trace_f4.py): [event][stage or tile index] = clock(), in shared memory
+constexpr int CF_TN = 96, CF_TE = 16;
+__device__ long long g_cf_tl[CF_TE][CF_TN];
+__shared__ uint32_t s_cf_tl[CF_TE][CF_TN];
+#define CF_EV(e, i) do { if ((int)(i) < CF_TN) s_cf_tl[e][i] = (uint32_t)clock(); } while (0)
+#else
+#define CF_EV(e, i) do { } while (0)
+#endif
 
 __host__ __device__ constexpr uint32_t cf_idesc(int M, int N) {   // kind::mxf4, e2m1 x e2m1, ue8m0, K-major
     return (1u << 7) | (1u << 10) | ((uint32_t)(N >> 3) << 17) | (1u << 23) | ((uint32_t)(M >> 4) << 24);
+}
+
+DG_DEV void cf_mma_ts_init(uint32_t d, uint32_t a, uint64_t b, uint32_t idesc, uint32_t sfa, uint32_t sfb) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::mxf4.block_scale.block32 [%0], [%1], %2, %3, [%4], [%5], 0;\n\t}" ::"r"(d),
+        "r"(a), "l"(b), "r"(idesc), "r"(sfa), "r"(sfb)
+        : "memory");
 }
 
 // A operand in tensor memory (TA): the unpacked e2m1 stage is written with tcgen05.st, 8 columns
@@ -98,6 +122,7 @@ struct CfArgs {
     void *D;
     int64_t ldd;
     int32_t has_rq, early_b;
+    int32_t omma;                // 1: the accumulators' origin comes from one MMA per tile (no reset stores)
     // 16-bit SIMD requant (host-verified, f16_params): x = clamp(acc + negA, 0, W), code = (x m + c) >> 14
     uint32_t f16_m, f16_c2, f16_w2, f16_na2;
     int32_t f16_tab, f16_thr0m1, f16_accmax;
@@ -118,7 +143,7 @@ __device__ __noinline__ void cf_epilogue_general(const CfArgs &fa, const Requant
         uint32_t v[32];
         ptx::tmem_ld_32x32b_x32(trow + 32 * c, v);
         ptx::tmem_ld_wait();
-        ptx::tmem_st_32x32b_x32(trow + 32 * c, origin);
+        if (!fa.omma) ptx::tmem_st_32x32b_x32(trow + 32 * c, origin);
         const int64_t qc = q0 + c * 32;
         if (p >= fa.np || qc >= fa.nq) continue;
         int32_t a[32];
@@ -166,6 +191,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     static_assert(!TA || TA0 + 6 * 32 <= CF_SF_COL, "tensor memory budget");
     constexpr int CF_UNP0 = NEPI;
     constexpr bool CSPLIT = NEPI == 8 && BNT == 256;   // the two epilogue groups split every tile's columns
+    const int ntiles = fa.ntiles;
     constexpr int CF_PROD = CF_UNP0 + NUNP, CF_WAIT = CF_PROD + 1, CF_MMA = CF_PROD + 2, NG = NUNP / 4;
     constexpr int IGG = CF_IG / NG;             // gather ring stages per unpack group
     extern __shared__ uint8_t smem_raw[];
@@ -184,7 +210,6 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     uint32_t *tab = reinterpret_cast<uint32_t *>(smem + CF_OFF_TAB);
     volatile uint32_t *f16_bad = reinterpret_cast<volatile uint32_t *>(smem + CF_OFF_TMEM + 8);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int ntiles = fa.ntiles;
     if (threadIdx.x == 0) *f16_bad = 0u;
 
     if (warp == CF_PROD) {
@@ -223,10 +248,20 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 #pragma unroll
         for (int j = 0; j < 32; ++j) r[j] = 0x80808080u;
         ptx::tmem_st_32x32b_x32(tmem + CF_SF_COL + lanes, r);
+        if (fa.omma) {   // origin MMA operands: A ones, scales 2^17 (A) / 2^0 (B); B block of 1.5 in smem
+            ptx::tmem_st_32x32b_x8_splat(tmem + CF_OA_COL + lanes, 0x22222222u);
+            ptx::tmem_st_32x32b_x8_splat(tmem + CF_OSFA_COL + lanes, 0x90909090u);
+            ptx::tmem_st_32x32b_x8_splat(tmem + CF_OSFB_COL + lanes, 0x7F7F7F7Fu);
+            ptx::tmem_st_32x32b_x8_splat(tmem + CF_OSFB_COL + 8 + lanes, 0x7F7F7F7Fu);
+            for (int i = threadIdx.x; i < BN_ * 128 / 16; i += 128)
+                *reinterpret_cast<uint4 *>(smem + CF_OFF_A + 16 * i) = make_uint4(0x33333333u, 0x33333333u, 0x33333333u, 0x33333333u);
+            ptx::fence_proxy_async_smem();
+        } else {
 #pragma unroll
-        for (int j = 0; j < 32; ++j) r[j] = CF_ACC0;
+            for (int j = 0; j < 32; ++j) r[j] = CF_ACC0;
 #pragma unroll
-        for (int c = 0; c < CF_NACC * BN_ / 32; ++c) ptx::tmem_st_32x32b_x32(tmem + (uint32_t)(c * 32) + lanes, r);
+            for (int c = 0; c < CF_NACC * BN_ / 32; ++c) ptx::tmem_st_32x32b_x32(tmem + (uint32_t)(c * 32) + lanes, r);
+        }
         ptx::tmem_st_wait();
     }
     ptx::tc_fence_before();
@@ -256,6 +291,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 if (lane == 0) {
                     ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)B_STAGE_);
                     ptx::tma_load_2d(sbase + CF_OFF_B + bs * B_STAGE_, &tm_b, full_b(bs), s * (CF_KST / 2), tq * BN_);
+                    CF_EV(0, gb);
                 }
                 __syncwarp();
             }
@@ -264,9 +300,12 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             ptx::mbar_wait(acc_empty(tl % CF_NACC), ((tl / CF_NACC) & 1u) ^ 1u);
+            if (lane == 0) CF_EV(1, tl);
             for (int s = 0; s < fa.nstages; ++s, ++g) {
                 ptx::mbar_wait(full_a(g % CF_SA), (g / CF_SA) & 1u);
+                if (lane == 0) CF_EV(2, g);
                 ptx::mbar_wait(full_b(g % SB_), (g / SB_) & 1u);
+                if (lane == 0) CF_EV(3, g);
                 ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
             }
         }
@@ -274,6 +313,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         constexpr uint32_t idesc = cf_idesc(CF_BM, BN_);
         const uint32_t sfa = tmem + CF_SF_COL, sfb = tmem + CF_SF_COL + 16;
         const int nst = fa.nstages, lastk = fa.last_ksteps;   // (in registers before any MMA is queued)
+        const bool omma = fa.omma != 0;
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl % CF_NACC;
@@ -281,7 +321,11 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             for (int s = 0; s < nst; ++s, ++g) {
                 const int sa = (int)(g % CF_SA), bs = (int)(g % SB_);
                 ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
+                if (lane == 0) CF_EV(14, g);
                 ptx::tc_fence_after();
+                if (TA && omma && s == 0)
+                    cf_mma_ts_init(dt, tmem + CF_OA_COL, ptx::desc_k_sw128(sbase + CF_OFF_A), idesc, tmem + CF_OSFA_COL,
+                                   tmem + CF_OSFB_COL);
                 const uint64_t ad = ptx::desc_k_sw128(sbase + CF_OFF_A + sa * CF_A_STAGE);
                 const uint64_t bd = ptx::desc_k_sw128(sbase + CF_OFF_B + bs * B_STAGE_);
                 const uint32_t at = tmem + TA0 + (uint32_t)(sa * 32);
@@ -297,10 +341,12 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         else cf_mma(dt, ad + 2 * k, bd + 2 * k, idesc, sfa, sfb);
                     }
                 }
+                if (lane == 0) CF_EV(15, g);
                 ptx::mma_commit_warp(empty_a(sa));
                 ptx::mma_commit_warp(empty_b(bs));
                 if (s == nst - 1) ptx::mma_commit_warp(acc_full(acc));
                 __syncwarp();
+                if (lane == 0) CF_EV(4, g);
             }
         }
     } else if (warp >= CF_UNP0) {
@@ -364,6 +410,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 if (DIRECT) {
                     const int ps = (int)(gp % CF_SP), sub = s & 1;
                     ptx::mbar_wait(full_p(ps), (gp / CF_SP) & 1u);
+                    if (threadIdx.x == CF_UNP0 * 32) CF_EV(12, g);
                     const uint32_t pbase = sbase + CF_OFF_P + ps * CF_P_SLOT;
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {   // SW128 slot: 16-byte unit XOR row bits
@@ -397,6 +444,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
                 const int sa = (int)(g % CF_SA);
                 ptx::mbar_wait(empty_a(sa), ((g / CF_SA) & 1u) ^ 1u);
+                if (threadIdx.x == CF_UNP0 * 32) CF_EV(13, g);
                 if constexpr (TA) {   // row r = lane quarter (warp & 3) x 32 + lane: 32 columns of this stage
                     ptx::tc_fence_after();
                     ptx::tmem_st_32x32b_x32(tmem + TA0 + (uint32_t)(sa * 32) + ((uint32_t)((warp & 3) * 32) << 16), e);
@@ -414,6 +462,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(full_a(sa));
+                if (threadIdx.x == CF_UNP0 * 32) CF_EV(5, g);
             }
         }
     } else {
@@ -443,6 +492,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             const int64_t q0 = (int64_t)tq * BN_;
             const uint32_t acc = tl % CF_NACC;
             ptx::mbar_wait(acc_full(acc), (tl / CF_NACC) & 1u);
+            if (lane == 0 && quarter == 0) CF_EV(6 + 3 * eg, tl);
             ptx::tc_fence_after();
             const int c0 = CSPLIT ? eg * 128 : 0;   // this warp's first column of the tile
             const uint32_t trow = tmem + acc * BN_ + (uint32_t)c0 + ((uint32_t)(quarter * 32) << 16);
@@ -455,12 +505,15 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 ptx::tmem_ld_32x32b_x32_pack16(trd, r16[0]);
                 ptx::tmem_ld_32x32b_x32_pack16(trd + 64, r16[1]);
                 ptx::tmem_ld_wait();
+                if (!fa.omma) {
 #pragma unroll
-                for (int c = 0; c < 16; ++c) ptx::tmem_st_32x32b_x8_splat(trd + 8 * c, CF_ACC0);   // reset to the origin
-                ptx::tmem_st_wait();
+                    for (int c = 0; c < 16; ++c) ptx::tmem_st_32x32b_x8_splat(trd + 8 * c, CF_ACC0);   // reset to the origin
+                    ptx::tmem_st_wait();
+                }
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0 && rd == RD_N - 1) ptx::mbar_arrive(acc_empty(acc));
+                if (lane == 0 && quarter == 0) CF_EV(7 + 3 * eg, tl);
                 if (p < fa.np) {
 #pragma unroll
                     for (int hh = 0; hh < 4; ++hh) {
@@ -493,10 +546,15 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
             }
+            if (lane == 0 && quarter == 0) CF_EV(8 + 3 * eg, tl);
         }
     }
     ptx::tc_fence_before();
     __syncthreads();
+#ifdef DG_TRACE
+    if (blockIdx.x == 0)
+        for (int i = threadIdx.x; i < CF_TE * CF_TN; i += blockDim.x) (&g_cf_tl[0][0])[i] = (&s_cf_tl[0][0])[i];
+#endif
     if (warp == CF_PROD) ptx::tmem_dealloc(tmem, 512);
 }
 
@@ -539,6 +597,16 @@ const uint8_t *cf_pad_source(int pad_code) {
 }
 
 }  // namespace
+
+#ifdef DG_TRACE
+extern "C" __attribute__((visibility("default"))) int dg_debug_cf_timeline(long long *host, int reset) {
+    if (reset) {
+        static long long z[CF_TE * CF_TN];
+        return cudaMemcpyToSymbol(g_cf_tl, z, sizeof(z)) == cudaSuccess ? 0 : -1;
+    }
+    return cudaMemcpyFromSymbol(host, g_cf_tl, sizeof(long long) * CF_TE * CF_TN) == cudaSuccess ? 0 : -1;
+}
+#endif
 
 // Conv (or a 1x1 conv = GEMM in the conv orientation) on the FP4 path.  x: NHWC packed [B][H][W][C/4];
 // w4: e2m1 weights [Cout][ld4] (dg_expand_operand_f4 of the packed weights, K order (r, s, c));
@@ -593,6 +661,7 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     fa.ldd = ldd;
     fa.has_rq = rq ? 1 : 0;
     fa.early_b = (b_prepared && opt(OPT_EARLY_WEIGHTS)) ? 1 : 0;
+    fa.omma = opt(OPT_F4_OMMA) ? 1 : 0;
     if (rq) {   // the 16-bit SIMD requant (reading Q23) is the only requant form of this kernel
         const int64_t *t = rq->thr;
         uint32_t m16 = 0, c16 = 0;
@@ -653,9 +722,10 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     lc.attrs = la;
     lc.numAttrs = 1;
     if (cudaLaunchKernelEx(&lc, kern, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
-    char tag[96];
-    snprintf(tag, sizeof(tag), "f4conv bn=%d %s unp=%d epi=%d direct=%d rq=%d tab=%d early=%d", bnt,
-             ta ? (bnt == 256 ? "ta nacc=1" : "ta nacc=2") : "sa nacc=3", nunp, nepi, fa.direct, fa.has_rq, fa.f16_tab, fa.early_b);
+    char tag[128];
+    snprintf(tag, sizeof(tag), "f4conv bn=%d %s unp=%d epi=%d direct=%d rq=%d tab=%d early=%d omma=%d", bnt,
+             bnt == 256 ? "ta nacc=1" : "ta nacc=2", nunp, nepi, fa.direct, fa.has_rq,
+             fa.f16_tab, fa.early_b, fa.omma);
     set_last_kernel(tag);
     return launch_status();
 }

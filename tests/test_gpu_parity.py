@@ -913,11 +913,12 @@ F4_CONVS = [  # B, H, W, C, Cout, k, stride, pad, pad_code
 ]
 
 
+@pytest.mark.parametrize("omma", [0, 1])
 @pytest.mark.parametrize("epi", [4, 8])
 @pytest.mark.parametrize("bn", [128, 256])
 @pytest.mark.parametrize("wl", [(-2, -1, 0, 1), (-12, -3, 4, 8)])
 @pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", F4_CONVS)
-def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn, epi):
+def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn, epi, omma):
     """FP4 conv kernel vs O-CONV on both tile widths (128 channels, two accumulators; 256, one) and
     both epilogue arrangements (4 warps; 8 warps splitting the 256-wide tiles' columns or owning
     alternate 128-wide tiles): int32 output, fused 16-bit requant with a per-channel bias, a
@@ -936,8 +937,9 @@ def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn, e
     w4 = dg.expand_operand_f4(wp, k * k * Cp, wl)
     p = dg.conv_params(B, H, W, Cp, Cout, k, k, stride, pad, pad_code, ldw=wp.shape[1])
     dg.reset_options()
-    with dg.options(f4_bn=bn, f4_epi=epi):
+    with dg.options(f4_bn=bn, f4_epi=epi, f4_omma=omma):
         _conv_f4_cases(xp, w4, lut, p, exp, Cout, g, bn, epi)
+        assert dg.last_kernel().endswith(f" omma={omma}"), dg.last_kernel()
 
 
 def _conv_f4_cases(xp, w4, lut, p, exp, Cout, g, bn, epi):
