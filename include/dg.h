@@ -269,7 +269,7 @@ DG_API dg_status dg_lut_gemm_onehot(const uint8_t *d_w1h, int64_t ldw1h, const i
  *      C[m][n] = sum_{k<K} wl[W[m][k]] * A[k][n]     (= sum_k T[(W << 4) | A], T = wl x {0..15})
  * A 4-bit code is the two 2-bit digits a = a_l + 4 a_h, and a packed 4-bit row (code k in nibble
  * k&1 of byte k>>1, low nibble first: the same bytes as the 2-bit packing of the digit sequence
- * a_l0, a_h0, a_l1, ..., so dg_pack_codes of the digit codes packs it) is a packed 2-bit row of
+ * a_l0, a_h0, a_l1, ...: dg_pack_codes4 writes it) is a packed 2-bit row of
  * K' = 2K digits; the weights become Q'[2k] = wl[w_k], Q'[2k+1] = 4 wl[w_k] (dg_expand_digits4:
  * packed 4-bit weights [rows][ld] -> int8 [rows][ld_out], ld_out >= dg_expand_ld(2K), a multiple
  * of 128, 128-byte aligned; DG_ERR_RANGE if some |4 wl| > 127).  Out-of-image conv taps read
@@ -280,6 +280,12 @@ DG_API dg_status dg_lut_gemm_onehot(const uint8_t *d_w1h, int64_t ldw1h, const i
  * dg_lut_conv2d4_prepared: p->C = the number of 4-bit channels (x: [B][H][W][C/2] bytes),
  *      d_w8 = dg_expand_digits4 of the packed 4-bit weights [Cout][kh*kw*C] (K order r, s, c);
  *      p->pad_code must be 0; otherwise as dg_lut_conv2d_prepared.                            */
+/* Packs 4-bit codes (one per byte, [rows][ld_codes]; values > 15 are masked with &15 and counted
+ * into *d_err_count when non-NULL) into packed 4-bit rows [rows][ld]: code k in nibble k&1 of
+ * byte k>>1, low nibble first, zero beyond K; ld % 16 == 0, ld >= ceil(K/2), d_packed 16-byte
+ * aligned (DG_ERR_INVALID_ARG otherwise). */
+DG_API dg_status dg_pack_codes4(const uint8_t *d_codes, int64_t rows, int64_t K, int64_t ld_codes, uint8_t *d_packed,
+                                int64_t ld, int32_t *d_err_count, void *stream);
 DG_API dg_status dg_expand_digits4(const uint8_t *d_w4, int64_t rows, int64_t K, int64_t ld, const int32_t levels[16],
                                    int8_t *d_out, int64_t ld_out, void *stream);
 DG_API dg_status dg_lut_gemm4_prepared(const uint8_t *d_at4, int64_t lda, const int8_t *d_w8, int64_t ld8, int64_t N,

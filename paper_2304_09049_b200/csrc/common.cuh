@@ -206,6 +206,7 @@ enum OptId {
     OPT_F4_EPI,         // FP4 conv kernel epilogue warps: 0 auto, 4 or 8
     OPT_F4_BN,          // FP4 conv tile width: 0 auto (256 when 256 | Cout), 128 or 256
     OPT_F4_OMMA,        // FP4 conv kernel: accumulator origin from one MMA per tile (1) or reset stores (0)
+    OPT_F4_CT,          // FP4 conv kernel: CTAs per SM for 128-wide tiles (2) or 1 (0 / 1)
     OPT_COUNT
 };
 int64_t opt(OptId id);

@@ -47,6 +47,17 @@ constexpr int CF_OFF_TMEM = CF_OFF_BAR + CF_NBAR * 8;
 constexpr int CF_OFF_TAB = (CF_OFF_TMEM + 16 + 15) / 16 * 16;
 constexpr int CF_ALLOC = CF_OFF_TAB + CF_TAB_PAIRS * 4 + 1024;
 static_assert(CF_ALLOC <= 232448, "shared memory budget");
+// two CTAs per SM (CT = 2, 128-wide tiles): each CTA holds 3 B stages, the origin-MMA B block, 2 packed
+// P slots (or a 4-stage gather ring), and allocates 256 tensor-memory columns: one 128 x 128
+// accumulator [0, 128), three A stages [128, 224), origin scales A [224, 232) / B [232, 240), origin
+// A [240, 248), block scales [248, 256)
+constexpr int CF2_OFF_OB = 3 * CF_B_STAGE;
+constexpr int CF2_OFF_P = CF2_OFF_OB + 128 * 128;
+constexpr int CF2_OFF_BAR = CF2_OFF_P + 2 * CF_P_SLOT;
+constexpr int CF2_OFF_TMEM = CF2_OFF_BAR + CF_NBAR * 8;
+constexpr int CF2_OFF_TAB = (CF2_OFF_TMEM + 16 + 15) / 16 * 16;
+constexpr int CF2_ALLOC = CF2_OFF_TAB + CF_TAB_PAIRS * 4 + 1024;
+static_assert(2 * (CF2_ALLOC + 1024) <= 233472, "two CTAs per SM: shared memory budget");
 // warps: NEPI epilogue warps, then the unpack warps NEPI .. NEPI + NUNP - 1, then producer, waiter, MMA issuer
 constexpr int CF_HANDOFF_BAR = 1, CF_EPI_BAR = 2;
 constexpr uint32_t CF_SF_COL = 480;                // TMEM columns [480, 512): block scales (every byte 2^1)
@@ -181,34 +192,45 @@ __device__ __noinline__ void cf_epilogue_general(const CfArgs &fa, const Requant
 // NEPI: epilogue warps, 4 (one per lane quarter) or 8: two groups, which split each 256-wide tile's
 // columns (each group loads its 128 columns and releases them: the single accumulator is free after
 // one load round) or own alternate tiles of the 128-wide kernel's two accumulators
-template <bool TA, int NUNP, bool DIRECT, int BNT, int NEPI>
-__global__ void __launch_bounds__(32 * (3 + NEPI + NUNP), 1)
+// CT: CTAs per SM, 1, or 2 (BNT = 128, TA): two independent pipelines per SM on half the tensor and
+// shared memory each (one accumulator, three A stages per CTA)
+template <bool TA, int NUNP, bool DIRECT, int BNT, int NEPI, int CT>
+__global__ void __launch_bounds__(32 * (3 + NEPI + NUNP), CT)
 lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CfArgs fa, const __grid_constant__ RequantArgs rq) {
-    constexpr int BN_ = BNT, SB_ = BNT == 256 ? 3 : CF_SB, B_STAGE_ = BNT * CF_KST / 2;   // (96 KB of B stages)
-    constexpr int CF_NACC = TA ? (BNT == 256 ? 1 : 2) : 3, CF_SA = TA ? 6 : 4;
+    constexpr bool C2 = CT == 2;
+    static_assert(!C2 || (BNT == 128 && TA), "two CTAs per SM: 128-wide tiles, A in tensor memory");
+    constexpr int BN_ = BNT, SB_ = (C2 || BNT == 256) ? 3 : CF_SB, B_STAGE_ = BNT * CF_KST / 2;   // (96 KB of B stages)
+    constexpr int CF_NACC = TA ? ((C2 || BNT == 256) ? 1 : 2) : 3, CF_SA = TA ? (C2 ? 3 : 6) : 4;
     constexpr uint32_t TA0 = CF_NACC * BN_;   // first tensor-memory A column (TA)
-    static_assert(!TA || TA0 + 6 * 32 <= CF_SF_COL, "tensor memory budget");
+    constexpr uint32_t TCOLS = C2 ? 256 : 512;
+    constexpr uint32_t SF_COL = C2 ? 248 : CF_SF_COL, SFB_OFF = C2 ? 4 : 16;
+    constexpr uint32_t OA_COL = C2 ? 240 : CF_OA_COL, OSFA_COL = C2 ? 224 : CF_OSFA_COL, OSFB_COL = C2 ? 232 : CF_OSFB_COL;
+    static_assert(!TA || TA0 + CF_SA * 32 <= (C2 ? OSFA_COL : OA_COL), "tensor memory budget");
+    constexpr int SP_ = C2 ? 2 : CF_SP, IG_ = C2 ? 4 : CF_IG;
+    constexpr int OFF_OB = C2 ? CF2_OFF_OB : CF_OFF_A, OFF_P = C2 ? CF2_OFF_P : CF_OFF_P;
+    constexpr int OFF_BAR = C2 ? CF2_OFF_BAR : CF_OFF_BAR, OFF_TMEM = C2 ? CF2_OFF_TMEM : CF_OFF_TMEM;
+    constexpr int OFF_TAB = C2 ? CF2_OFF_TAB : CF_OFF_TAB;
     constexpr int CF_UNP0 = NEPI;
     constexpr bool CSPLIT = NEPI == 8 && BNT == 256;   // the two epilogue groups split every tile's columns
     const int ntiles = fa.ntiles;
     constexpr int CF_PROD = CF_UNP0 + NUNP, CF_WAIT = CF_PROD + 1, CF_MMA = CF_PROD + 2, NG = NUNP / 4;
-    constexpr int IGG = CF_IG / NG;             // gather ring stages per unpack group
+    constexpr int IGG = IG_ / NG;               // gather ring stages per unpack group
     extern __shared__ uint8_t smem_raw[];
     uint8_t *smem = reinterpret_cast<uint8_t *>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
     const uint32_t sbase = ptx::smem_u32(smem);
-    const uint32_t bar0 = sbase + CF_OFF_BAR;
+    const uint32_t bar0 = sbase + OFF_BAR;   // (barrier slots laid out for the largest counts)
     auto full_p = [&](int s) { return bar0 + 8 * s; };
     auto empty_p = [&](int s) { return bar0 + 8 * (CF_SP + s); };
     auto full_b = [&](int s) { return bar0 + 8 * (2 * CF_SP + s); };
     auto empty_b = [&](int s) { return bar0 + 8 * (2 * CF_SP + CF_SB + s); };
     auto full_a = [&](int s) { return bar0 + 8 * (2 * CF_SP + 2 * CF_SB + s); };
-    auto empty_a = [&](int s) { return bar0 + 8 * (2 * CF_SP + 2 * CF_SB + CF_SA + s); };
-    auto acc_full = [&](int a) { return bar0 + 8 * (2 * CF_SP + 2 * CF_SB + 2 * CF_SA + a); };
-    auto acc_empty = [&](int a) { return bar0 + 8 * (2 * CF_SP + 2 * CF_SB + 2 * CF_SA + CF_NACC + a); };
-    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + CF_OFF_TMEM);
-    uint32_t *tab = reinterpret_cast<uint32_t *>(smem + CF_OFF_TAB);
-    volatile uint32_t *f16_bad = reinterpret_cast<volatile uint32_t *>(smem + CF_OFF_TMEM + 8);
+    auto empty_a = [&](int s) { return bar0 + 8 * (2 * CF_SP + 2 * CF_SB + CF_SA_MAX + s); };
+    auto acc_full = [&](int a) { return bar0 + 8 * (2 * CF_SP + 2 * CF_SB + 2 * CF_SA_MAX + a); };
+    auto acc_empty = [&](int a) { return bar0 + 8 * (2 * CF_SP + 2 * CF_SB + 2 * CF_SA_MAX + CF_NACC_MAX + a); };
+    uint32_t *tmem_slot = reinterpret_cast<uint32_t *>(smem + OFF_TMEM);
+    uint32_t *tab = reinterpret_cast<uint32_t *>(smem + OFF_TAB);
+    volatile uint32_t *f16_bad = reinterpret_cast<volatile uint32_t *>(smem + OFF_TMEM + 8);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     if (threadIdx.x == 0) *f16_bad = 0u;
 
@@ -216,7 +238,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         if (lane == 0) {
             if (DIRECT) ptx::tma_prefetch(&tm_p);
             ptx::tma_prefetch(&tm_b);
-            for (int s = 0; s < CF_SP; ++s) {
+            for (int s = 0; s < SP_; ++s) {
                 ptx::mbar_init(full_p(s), 1);
                 ptx::mbar_init(empty_p(s), 8);   // 4 unpack warps x 2 stages per slot (count 2 for a lone stage)
             }
@@ -235,7 +257,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             ptx::fence_mbar_init();
         }
         __syncwarp();
-        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), 512);
+        ptx::tmem_alloc(ptx::smem_u32(tmem_slot), TCOLS);
     }
     ptx::tc_fence_before();
     __syncthreads();
@@ -247,14 +269,15 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         uint32_t r[32];
 #pragma unroll
         for (int j = 0; j < 32; ++j) r[j] = 0x80808080u;
-        ptx::tmem_st_32x32b_x32(tmem + CF_SF_COL + lanes, r);
+        if (C2) ptx::tmem_st_32x32b_x8_splat(tmem + SF_COL + lanes, 0x80808080u);
+        else ptx::tmem_st_32x32b_x32(tmem + SF_COL + lanes, r);
         if (fa.omma) {   // origin MMA operands: A ones, scales 2^17 (A) / 2^0 (B); B block of 1.5 in smem
-            ptx::tmem_st_32x32b_x8_splat(tmem + CF_OA_COL + lanes, 0x22222222u);
-            ptx::tmem_st_32x32b_x8_splat(tmem + CF_OSFA_COL + lanes, 0x90909090u);
-            ptx::tmem_st_32x32b_x8_splat(tmem + CF_OSFB_COL + lanes, 0x7F7F7F7Fu);
-            ptx::tmem_st_32x32b_x8_splat(tmem + CF_OSFB_COL + 8 + lanes, 0x7F7F7F7Fu);
+            ptx::tmem_st_32x32b_x8_splat(tmem + OA_COL + lanes, 0x22222222u);
+            ptx::tmem_st_32x32b_x8_splat(tmem + OSFA_COL + lanes, 0x90909090u);
+            ptx::tmem_st_32x32b_x8_splat(tmem + OSFB_COL + lanes, 0x7F7F7F7Fu);
+            if (!C2) ptx::tmem_st_32x32b_x8_splat(tmem + OSFB_COL + 8 + lanes, 0x7F7F7F7Fu);
             for (int i = threadIdx.x; i < BN_ * 128 / 16; i += 128)
-                *reinterpret_cast<uint4 *>(smem + CF_OFF_A + 16 * i) = make_uint4(0x33333333u, 0x33333333u, 0x33333333u, 0x33333333u);
+                *reinterpret_cast<uint4 *>(smem + OFF_OB + 16 * i) = make_uint4(0x33333333u, 0x33333333u, 0x33333333u, 0x33333333u);
             ptx::fence_proxy_async_smem();
         } else {
 #pragma unroll
@@ -277,11 +300,11 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             const int tq = t % fa.ntq, tp = t / fa.ntq;
             for (int s = 0; s < fa.nstages; ++s, ++gb) {
                 if (DIRECT && (s & 1) == 0) {   // a packed slot = 2 stages of every pixel row
-                    const int ps = (int)(gp % CF_SP);
-                    ptx::mbar_wait(empty_p(ps), ((gp / CF_SP) & 1u) ^ 1u);
+                    const int ps = (int)(gp % SP_);
+                    ptx::mbar_wait(empty_p(ps), ((gp / SP_) & 1u) ^ 1u);
                     if (lane == 0) {
                         ptx::mbar_arrive_expect_tx(full_p(ps), (uint32_t)CF_P_SLOT);
-                        ptx::tma_load_2d(sbase + CF_OFF_P + ps * CF_P_SLOT, &tm_p, full_p(ps), s * (CF_KST / 4), tp * CF_BM);
+                        ptx::tma_load_2d(sbase + OFF_P + ps * CF_P_SLOT, &tm_p, full_p(ps), s * (CF_KST / 4), tp * CF_BM);
                     }
                     __syncwarp();
                     ++gp;
@@ -311,7 +334,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         }
     } else if (warp == CF_MMA) {
         constexpr uint32_t idesc = cf_idesc(CF_BM, BN_);
-        const uint32_t sfa = tmem + CF_SF_COL, sfb = tmem + CF_SF_COL + 16;
+        const uint32_t sfa = tmem + SF_COL, sfb = tmem + SF_COL + SFB_OFF;
         const int nst = fa.nstages, lastk = fa.last_ksteps;   // (in registers before any MMA is queued)
         const bool omma = fa.omma != 0;
         uint32_t g = 0, tl = 0;
@@ -324,8 +347,8 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 if (lane == 0) CF_EV(14, g);
                 ptx::tc_fence_after();
                 if (TA && omma && s == 0)
-                    cf_mma_ts_init(dt, tmem + CF_OA_COL, ptx::desc_k_sw128(sbase + CF_OFF_A), idesc, tmem + CF_OSFA_COL,
-                                   tmem + CF_OSFB_COL);
+                    cf_mma_ts_init(dt, tmem + OA_COL, ptx::desc_k_sw128(sbase + OFF_OB), idesc, tmem + OSFA_COL,
+                                   tmem + OSFB_COL);
                 const uint64_t ad = ptx::desc_k_sw128(sbase + CF_OFF_A + sa * CF_A_STAGE);
                 const uint64_t bd = ptx::desc_k_sw128(sbase + CF_OFF_B + bs * B_STAGE_);
                 const uint32_t at = tmem + TA0 + (uint32_t)(sa * 32);
@@ -374,7 +397,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             while (gs >= fa.nstages && gt < ntiles) { gs -= fa.nstages; gt += gridDim.x; moved = true; }
             if (moved && gt < ntiles) pixel();
         };
-        const uint32_t ring = sbase + CF_OFF_P + (uint32_t)(grp * IGG * CF_RING) + (uint32_t)(r * 64);
+        const uint32_t ring = sbase + OFF_P + (uint32_t)(grp * IGG * CF_RING) + (uint32_t)(r * 64);
         auto fetch = [&](int slot) {   // the cursor's stage -> ring slot; advance the cursor by NG stages
             if (gt < ntiles) {
 #pragma unroll
@@ -408,10 +431,10 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
                 uint4 v[4];
                 if (DIRECT) {
-                    const int ps = (int)(gp % CF_SP), sub = s & 1;
-                    ptx::mbar_wait(full_p(ps), (gp / CF_SP) & 1u);
+                    const int ps = (int)(gp % SP_), sub = s & 1;
+                    ptx::mbar_wait(full_p(ps), (gp / SP_) & 1u);
                     if (threadIdx.x == CF_UNP0 * 32) CF_EV(12, g);
-                    const uint32_t pbase = sbase + CF_OFF_P + ps * CF_P_SLOT;
+                    const uint32_t pbase = sbase + OFF_P + ps * CF_P_SLOT;
 #pragma unroll
                     for (int c = 0; c < 4; ++c) {   // SW128 slot: 16-byte unit XOR row bits
                         const uint32_t lin = (uint32_t)(r * 128 + sub * 64 + 16 * c);
@@ -482,7 +505,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         }
         const bool f16_ok = fa.has_rq && *f16_bad == 0u;
         ptx::griddep_wait();
-        const uint32_t tabs = sbase + CF_OFF_TAB;
+        const uint32_t tabs = sbase + OFF_TAB;
         uint32_t tl = 0;
         constexpr int RD_N = CSPLIT ? 1 : BN_ / 128;   // 128-column load rounds per warp and tile
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
@@ -555,7 +578,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     if (blockIdx.x == 0)
         for (int i = threadIdx.x; i < CF_TE * CF_TN; i += blockDim.x) (&g_cf_tl[0][0])[i] = (&s_cf_tl[0][0])[i];
 #endif
-    if (warp == CF_PROD) ptx::tmem_dealloc(tmem, 512);
+    if (warp == CF_PROD) ptx::tmem_dealloc(tmem, TCOLS);
 }
 
 typedef CUresult (*CfEncode)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
@@ -688,33 +711,38 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     if (!cf_map(&mb, w4, ld4, ld4, cout, bnt)) return DG_ERR_CUDA;
     // (the shared-memory-A form, TA = false, measured 5-20 % slower: kept in the source, not built)
     const bool ta = true;
-    const int nunp = (int)opt(OPT_F4_UNP) == 4 ? 4 : ((int)opt(OPT_F4_UNP) == 8 ? 8 : (direct ? 4 : 8));
-    const int nepi = (int)opt(OPT_F4_EPI) == 4 ? 4 : 8;   // (auto: 8, measured -5..-20 % on every FP4 layer)
+    // two CTAs per SM (option f4_ct = 2; 128-wide tiles): 4 unpack and 4 epilogue warps per CTA
+    const int ct = (bnt == 128 && opt(OPT_F4_CT) == 2) ? 2 : 1;
+    const int nunp = ct == 2 ? 4 : ((int)opt(OPT_F4_UNP) == 4 ? 4 : ((int)opt(OPT_F4_UNP) == 8 ? 8 : (direct ? 4 : 8)));
+    const int nepi = ct == 2 ? 4 : ((int)opt(OPT_F4_EPI) == 4 ? 4 : 8);   // (auto: 8, measured -5..-20 % on every FP4 layer)
     typedef void (*CfKern)(const CUtensorMap, const CUtensorMap, const CfArgs, const RequantArgs);
-    static const CfKern kerns[16] = {
-        lut_conv_f4_kernel<true, 4, false, 128, 4>, lut_conv_f4_kernel<true, 8, false, 128, 4>,
-        lut_conv_f4_kernel<true, 4, true, 128, 4>,  lut_conv_f4_kernel<true, 8, true, 128, 4>,
-        lut_conv_f4_kernel<true, 4, false, 256, 4>, lut_conv_f4_kernel<true, 8, false, 256, 4>,
-        lut_conv_f4_kernel<true, 4, true, 256, 4>,  lut_conv_f4_kernel<true, 8, true, 256, 4>,
-        lut_conv_f4_kernel<true, 4, false, 128, 8>, lut_conv_f4_kernel<true, 8, false, 128, 8>,
-        lut_conv_f4_kernel<true, 4, true, 128, 8>,  lut_conv_f4_kernel<true, 8, true, 128, 8>,
-        lut_conv_f4_kernel<true, 4, false, 256, 8>, lut_conv_f4_kernel<true, 8, false, 256, 8>,
-        lut_conv_f4_kernel<true, 4, true, 256, 8>,  lut_conv_f4_kernel<true, 8, true, 256, 8>};
-    static bool attr[16] = {};
-    const int ai = (nepi == 8 ? 8 : 0) + (bnt == 256 ? 4 : 0) + (direct ? 2 : 0) + (nunp == 8 ? 1 : 0);
+    static const CfKern kerns[18] = {
+        lut_conv_f4_kernel<true, 4, false, 128, 4, 1>, lut_conv_f4_kernel<true, 8, false, 128, 4, 1>,
+        lut_conv_f4_kernel<true, 4, true, 128, 4, 1>,  lut_conv_f4_kernel<true, 8, true, 128, 4, 1>,
+        lut_conv_f4_kernel<true, 4, false, 256, 4, 1>, lut_conv_f4_kernel<true, 8, false, 256, 4, 1>,
+        lut_conv_f4_kernel<true, 4, true, 256, 4, 1>,  lut_conv_f4_kernel<true, 8, true, 256, 4, 1>,
+        lut_conv_f4_kernel<true, 4, false, 128, 8, 1>, lut_conv_f4_kernel<true, 8, false, 128, 8, 1>,
+        lut_conv_f4_kernel<true, 4, true, 128, 8, 1>,  lut_conv_f4_kernel<true, 8, true, 128, 8, 1>,
+        lut_conv_f4_kernel<true, 4, false, 256, 8, 1>, lut_conv_f4_kernel<true, 8, false, 256, 8, 1>,
+        lut_conv_f4_kernel<true, 4, true, 256, 8, 1>,  lut_conv_f4_kernel<true, 8, true, 256, 8, 1>,
+        lut_conv_f4_kernel<true, 4, false, 128, 4, 2>, lut_conv_f4_kernel<true, 4, true, 128, 4, 2>};
+    static bool attr[18] = {};
+    const int ai = ct == 2 ? 16 + (direct ? 1 : 0)
+                           : (nepi == 8 ? 8 : 0) + (bnt == 256 ? 4 : 0) + (direct ? 2 : 0) + (nunp == 8 ? 1 : 0);
     const CfKern kern = kerns[ai];
     if (!attr[ai]) {
-        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF_ALLOC) != cudaSuccess)
+        if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ct == 2 ? CF2_ALLOC : CF_ALLOC) !=
+            cudaSuccess)
             return DG_ERR_CUDA;
         attr[ai] = true;
     }
     RequantArgs dummy{};
     const RequantArgs rqv = rq ? *rq : dummy;
-    const int grid = (int)(nt < num_sms() ? nt : num_sms());
+    const int grid = (int)(nt < ct * num_sms() ? nt : ct * num_sms());
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)grid);
     lc.blockDim = dim3((unsigned)(32 * (3 + nepi + nunp)));
-    lc.dynamicSmemBytes = CF_ALLOC;
+    lc.dynamicSmemBytes = ct == 2 ? CF2_ALLOC : CF_ALLOC;
     lc.stream = st;
     cudaLaunchAttribute la[1];
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
@@ -724,7 +752,7 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     if (cudaLaunchKernelEx(&lc, kern, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
     char tag[128];
     snprintf(tag, sizeof(tag), "f4conv bn=%d %s unp=%d epi=%d direct=%d rq=%d tab=%d early=%d omma=%d", bnt,
-             bnt == 256 ? "ta nacc=1" : "ta nacc=2", nunp, nepi, fa.direct, fa.has_rq,
+             ct == 2 ? "ta nacc=1 ct=2" : (bnt == 256 ? "ta nacc=1" : "ta nacc=2"), nunp, nepi, fa.direct, fa.has_rq,
              fa.f16_tab, fa.early_b, fa.omma);
     set_last_kernel(tag);
     return launch_status();

@@ -1207,6 +1207,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         v[c] = c < nchunk ? ptx::lds128(row + ((c ^ ((r >> 1) & 3)) << 4)) : make_uint4(0, 0, 0, 0);
                 } else {
                     ptx::mbar_wait(full_p(slot), ph);
+                    if (lane == 0 && quarter == 0) TS_EV(20, g);
                     // TMA slots carry the 128-byte swizzle: the 16-byte unit (bits 4-6) of the
                     // slot's linear offset is XORed with bits 7-9 (conflict-free LDS.128)
                     const uint32_t pbase = sbase + C::OFF_P + slot * pslot;
@@ -1231,6 +1232,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         a[16 * c + 4 * i + 3] = o.w;
                     }
                 }
+                if (lane == 0 && quarter == 0) TS_EV(21, g);
                 if (ta.implicit) {   // the ring slot's data is consumed (values in registers): refill it
                     gc.issue<2 * C::HALVES>(ta, ring + (uint32_t)((consumed % IG_DEPTH) * BM * 64), r, ntiles, KST / 4);
                     gc.advance(ta, NUM_UGROUPS, r, ntiles);

@@ -67,6 +67,28 @@ __global__ void pack_kernel(const uint8_t *__restrict__ codes, int64_t rows, int
     if (err && bad) atomicAdd(err, bad);
 }
 
+// ---- 4-bit codes (Table 2): one code per byte -> nibble k&1 of byte k>>1, low nibble
+// first, zero beyond K.  One thread per output 16-byte chunk (32 codes).
+__global__ void pack4_kernel(const uint8_t *__restrict__ codes, int64_t rows, int64_t K, int64_t ld_codes,
+                             uint8_t *__restrict__ packed, int64_t ld, int32_t *__restrict__ err) {
+    const int64_t chunks_per_row = ld / 16;
+    const int64_t total = rows * chunks_per_row;
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t r = i / chunks_per_row;
+        const int64_t k0 = (i - r * chunks_per_row) * 32;
+        const uint8_t *src = codes + r * ld_codes;
+        uint32_t out[4] = {0, 0, 0, 0};
+        for (int64_t k = k0; k < k0 + 32 && k < K; ++k) {
+            const uint32_t c = src[k];
+            if (c > 15) bad += 1;
+            out[(k - k0) >> 3] |= (c & 15u) << (4 * ((k - k0) & 7));
+        }
+        *reinterpret_cast<uint4 *>(packed + r * ld + (k0 >> 1)) = make_uint4(out[0], out[1], out[2], out[3]);
+    }
+    if (err && bad) atomicAdd(err, bad);
+}
+
 __global__ void unpack_kernel(const uint8_t *__restrict__ packed, int64_t rows, int64_t K, int64_t ld,
                               uint8_t *__restrict__ codes) {
     const int64_t total = rows * K;
@@ -204,6 +226,17 @@ dg_status dg_pack_codes(const uint8_t *d_codes, int64_t rows, int64_t K, int64_t
 dg_status dg_pack_weights(const uint8_t *d_codes, int64_t rows, int64_t K, int64_t ld_codes,
                           uint8_t *d_packed, int64_t ld, int32_t *d_err_count, void *stream) {
     return pack_common(d_codes, rows, K, ld_codes, d_packed, ld, d_err_count, stream);
+}
+
+dg_status dg_pack_codes4(const uint8_t *d_codes, int64_t rows, int64_t K, int64_t ld_codes, uint8_t *d_packed, int64_t ld,
+                         int32_t *d_err_count, void *stream) {
+    if (!d_codes || !d_packed) return DG_ERR_INVALID_ARG;
+    if (rows < 0 || K <= 0 || ld_codes < K) return DG_ERR_SHAPE;
+    if (ld % 16 != 0 || ld * 2 < K || ((uintptr_t)d_packed & 15)) return DG_ERR_INVALID_ARG;
+    if (rows == 0) return DG_OK;
+    pack4_kernel<<<grid_for(rows * (ld / 16)), kThreads, 0, (cudaStream_t)stream>>>(d_codes, rows, K, ld_codes, d_packed,
+                                                                                  ld, d_err_count);
+    return launch_status();
 }
 
 dg_status dg_unpack_codes(const uint8_t *d_packed, int64_t rows, int64_t K, int64_t ld,

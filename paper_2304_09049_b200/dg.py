@@ -71,6 +71,7 @@ def lib():
             "dg_lut_from_table": ([P, i32, P], i32),
             "dg_packed_ld": ([i64], i64),
             "dg_pack_codes": ([P, i64, i64, i64, P, i64, P, P], i32),
+            "dg_pack_codes4": ([P, i64, i64, i64, P, i64, P, P], i32),
             "dg_pack_weights": ([P, i64, i64, i64, P, i64, P, P], i32),
             "dg_unpack_codes": ([P, i64, i64, i64, P, P], i32),
             "dg_quantize_pack_activations": ([P, i64, i64, ctypes.c_float, ctypes.c_float, i32, i32,
@@ -372,12 +373,18 @@ def lut_gemm_onehot(w1h: torch.Tensor, atc: torch.Tensor, M: int, N: int, K: int
     return out
 
 
-def pack_codes4(codes4: torch.Tensor, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
-    """4-bit codes [rows][K] -> packed [rows][ld] (code k in nibble k&1 of byte k>>1, low first):
-    the 2-bit packing of the digit sequence (c & 3, c >> 2) per code (dg.h, 4-bit operands)."""
+def pack_codes4(codes4: torch.Tensor, out: torch.Tensor | None = None, err: torch.Tensor | None = None,
+                stream=None) -> torch.Tensor:
+    """4-bit codes [rows][K] (one per byte) -> packed [rows][ld] (code k in nibble k&1 of byte
+    k>>1, low first; the 2-bit packing of the digit sequence (c & 3, c >> 2)): dg_pack_codes4."""
+    _dev(codes4, torch.uint8, "codes4")
     rows, K = codes4.shape
-    digits = torch.stack((codes4 & 3, codes4 >> 2), dim=2).reshape(rows, 2 * K).contiguous()
-    return pack_codes(digits, out=out, stream=stream)
+    ld = (K + 31) // 32 * 16
+    if out is None:
+        out = torch.empty((rows, ld), dtype=torch.uint8, device=codes4.device)
+    _check(lib().dg_pack_codes4(_ptr(codes4), rows, K, codes4.stride(0), _ptr(out), out.shape[1],
+                                _ptr(err), _stream(stream)), "dg_pack_codes4")
+    return out
 
 
 def expand_digits4(w4: torch.Tensor, K: int, levels, out: torch.Tensor | None = None, stream=None):

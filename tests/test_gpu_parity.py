@@ -762,6 +762,25 @@ def _levels16(seed, amp=31):
     return np.random.default_rng(seed).integers(-amp, amp + 1, 16).astype(np.int32)
 
 
+@pytest.mark.parametrize("K", [1, 37, 64, 101])
+def test_pack_codes4(K):
+    """dg_pack_codes4: nibble k&1 of byte k>>1 (low first), zero tail, values > 15 masked and
+    counted; the same bytes as the 2-bit packing of the digit sequence (c & 3, c >> 2)."""
+    g = np.random.default_rng(K)
+    codes = g.integers(0, 16, (9, K), dtype=np.uint8)
+    codes[3, 0] = 200
+    err = torch.zeros(1, dtype=torch.int32, device=DEV)
+    got = host(dg.pack_codes4(torch.from_numpy(codes).to(DEV), err=err))
+    assert int(err.item()) == 1
+    m = codes & 15
+    exp = np.zeros((9, got.shape[1]), np.uint8)
+    for k in range(K):
+        exp[:, k >> 1] |= (m[:, k] << (4 * (k & 1))).astype(np.uint8)
+    assert np.array_equal(got, exp)
+    digits = np.stack((m & 3, m >> 2), axis=2).reshape(9, 2 * K)
+    assert np.array_equal(host(dg.pack_codes(torch.from_numpy(np.ascontiguousarray(digits)).to(DEV))), got)
+
+
 @pytest.mark.parametrize("M,N,K", [(64, 196, 576), (130, 70, 300), (256, 384, 1152), (17, 9, 5)])
 def test_gemm4_vs_oracle(M, N, K):
     """4-bit weights (16 arbitrary int8 levels) x 4-bit unsigned activations: activation-major
@@ -914,7 +933,7 @@ F4_CONVS = [  # B, H, W, C, Cout, k, stride, pad, pad_code
 
 
 @pytest.mark.parametrize("omma", [0, 1])
-@pytest.mark.parametrize("epi", [4, 8])
+@pytest.mark.parametrize("epi", [4, 8, "ct2"])
 @pytest.mark.parametrize("bn", [128, 256])
 @pytest.mark.parametrize("wl", [(-2, -1, 0, 1), (-12, -3, 4, 8)])
 @pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", F4_CONVS)
@@ -937,8 +956,13 @@ def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn, e
     w4 = dg.expand_operand_f4(wp, k * k * Cp, wl)
     p = dg.conv_params(B, H, W, Cp, Cout, k, k, stride, pad, pad_code, ldw=wp.shape[1])
     dg.reset_options()
-    with dg.options(f4_bn=bn, f4_epi=epi, f4_omma=omma):
+    if epi == "ct2" and bn == 256:
+        pytest.skip("two CTAs per SM: 128-wide tiles only")
+    ct = 2 if epi == "ct2" else 1
+    epi = 4 if epi == "ct2" else epi
+    with dg.options(f4_bn=bn, f4_epi=epi, f4_omma=omma, f4_ct=ct):
         _conv_f4_cases(xp, w4, lut, p, exp, Cout, g, bn, epi)
+        assert (" ct=2 " in dg.last_kernel()) == (ct == 2), dg.last_kernel()
         assert dg.last_kernel().endswith(f" omma={omma}"), dg.last_kernel()
 
 

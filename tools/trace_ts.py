@@ -48,7 +48,7 @@ print(f"{M}x{N}x{K}: {e0.elapsed_time(e1):.3f} ms")
 t0 = a[a > 0].min()
 a = np.where(a > 0, a - t0, -1)
 nst = (K + 127) // 128
-names = {13: "P_loop", 14: "P_slot", 12: "P_tma", 0: "unp0", 1: "unp_rdy", 11: "emptyA", 2: "fullA", 4: "w_fullA", 5: "w_fullB", 6: "handoff"}
+names = {13: "P_loop", 12: "P_tma", 0: "unp0", 20: "P_ok", 21: "unp_alu", 1: "unp_rdy", 11: "emptyA", 2: "fullA", 4: "w_fullA", 5: "w_fullB", 6: "handoff"}
 print("stage " + " ".join(f"{v:>8s}" for v in names.values()))
 for g in list(range(0, int(os.environ.get('TRACE_STAGES', '40')))):
     print(f"{g:5d} " + " ".join(f"{a[e][g]:8d}" for e in names))
