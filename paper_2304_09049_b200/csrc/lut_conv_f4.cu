@@ -31,7 +31,7 @@ namespace {
 
 constexpr int CF_BM = 128, CF_BN = 128;
 constexpr int CF_KST = 256;                        // codes per stage: 128 bytes of e2m1 per row = 4 MMAs (K = 64)
-constexpr int CF_NACC_MAX = 3, CF_SA_MAX = 6, CF_SB = 6, CF_SP = 3, CF_IG = 6;
+constexpr int CF_NACC_MAX = 4, CF_SA_MAX = 6, CF_SB = 6, CF_SP = 3, CF_IG = 6;
 constexpr int CF_A_STAGE = CF_BM * CF_KST / 2;     // 16 KB, SW128 K-major
 constexpr int CF_B_STAGE = CF_BN * CF_KST / 2;     // 16 KB, SW128 K-major
 constexpr int CF_P_SLOT = CF_BM * 128;             // 16 KB: 512 packed codes of every row (2 stages)
@@ -200,8 +200,11 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                    const __grid_constant__ CfArgs fa, const __grid_constant__ RequantArgs rq) {
     constexpr bool C2 = CT == 2;
     static_assert(!C2 || (BNT == 128 && TA), "two CTAs per SM: 128-wide tiles, A in tensor memory");
-    constexpr int BN_ = BNT, SB_ = (C2 || BNT == 256) ? 3 : CF_SB, B_STAGE_ = BNT * CF_KST / 2;   // (96 KB of B stages)
-    constexpr int CF_NACC = TA ? ((C2 || BNT == 256) ? 1 : 2) : 3, CF_SA = TA ? (C2 ? 3 : 6) : 4;
+    static_assert(BNT == 256 || BNT == 128 || (BNT == 64 && TA), "tile widths 64 (A in tensor memory), 128, 256");
+    constexpr int BN_ = BNT, SB_ = (C2 || BNT == 256) ? 3 : CF_SB, B_STAGE_ = BNT * CF_KST / 2;   // (96 / 48 KB of B stages)
+    // accumulators: 256-wide 1, 128-wide 2 (two CTAs per SM: 1), 64-wide 4
+    constexpr int CF_NACC = TA ? ((C2 || BNT == 256) ? 1 : (BNT == 64 ? 4 : 2)) : 3, CF_SA = TA ? (C2 ? 3 : 6) : 4;
+    constexpr int RW = BNT < 128 ? BNT : 128;   // columns per epilogue load round
     constexpr uint32_t TA0 = CF_NACC * BN_;   // first tensor-memory A column (TA)
     constexpr uint32_t TCOLS = C2 ? 256 : 512;
     constexpr uint32_t SF_COL = C2 ? 248 : CF_SF_COL, SFB_OFF = C2 ? 4 : 16;
@@ -507,7 +510,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         ptx::griddep_wait();
         const uint32_t tabs = sbase + OFF_TAB;
         uint32_t tl = 0;
-        constexpr int RD_N = CSPLIT ? 1 : BN_ / 128;   // 128-column load rounds per warp and tile
+        constexpr int RD_N = CSPLIT ? 1 : BN_ / RW;   // load rounds per warp and tile
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             if (NEPI == 8 && !CSPLIT && (int)(tl & 1u) != eg) continue;   // the other group's accumulator
             const int tq = t % fa.ntq, tp = t / fa.ntq;
@@ -521,16 +524,16 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             const uint32_t trow = tmem + acc * BN_ + (uint32_t)c0 + ((uint32_t)(quarter * 32) << 16);
             if (f16_ok && q0 + BN_ <= fa.nq) {
 #pragma unroll 1
-              for (int rd = 0; rd < RD_N; ++rd) {   // 128 columns per load round
-                const uint32_t trd = trow + (uint32_t)(rd * 128);
-                const int64_t q0r = q0 + c0 + rd * 128;
-                uint32_t r16[2][32];   // all 128 columns as 16-bit pairs (low halves = the integer values)
-                ptx::tmem_ld_32x32b_x32_pack16(trd, r16[0]);
-                ptx::tmem_ld_32x32b_x32_pack16(trd + 64, r16[1]);
+              for (int rd = 0; rd < RD_N; ++rd) {   // RW columns per load round
+                const uint32_t trd = trow + (uint32_t)(rd * RW);
+                const int64_t q0r = q0 + c0 + rd * RW;
+                uint32_t r16[RW / 64][32];   // the round's columns as 16-bit pairs (low halves = the integer values)
+#pragma unroll
+                for (int l = 0; l < RW / 64; ++l) ptx::tmem_ld_32x32b_x32_pack16(trd + 64 * l, r16[l]);
                 ptx::tmem_ld_wait();
                 if (!fa.omma) {
 #pragma unroll
-                    for (int c = 0; c < 16; ++c) ptx::tmem_st_32x32b_x8_splat(trd + 8 * c, CF_ACC0);   // reset to the origin
+                    for (int c = 0; c < RW / 8; ++c) ptx::tmem_st_32x32b_x8_splat(trd + 8 * c, CF_ACC0);   // reset to the origin
                     ptx::tmem_st_wait();
                 }
                 ptx::tc_fence_before();
@@ -539,7 +542,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 if (lane == 0 && quarter == 0) CF_EV(7 + 3 * eg, tl);
                 if (p < fa.np) {
 #pragma unroll
-                    for (int hh = 0; hh < 4; ++hh) {
+                    for (int hh = 0; hh < RW / 32; ++hh) {
                         const int64_t qc = q0r + hh * 32;
                         uint32_t na[16];
                         if (fa.f16_tab) {
@@ -657,7 +660,7 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     // auto, 128, 256).  Measured per layer: the 3x3 convs over 256 channels
     // 28.5 -> 18.5 us against 26.3 us at 128 wide.
     const int fbn = (int)opt(OPT_F4_BN);
-    const int bnt = fbn == 128 ? 128 : (fbn == 256 ? 256 : (cout % 256 == 0 ? 256 : 128));
+    const int bnt = fbn == 64 ? 64 : fbn == 128 ? 128 : (fbn == 256 ? 256 : (cout % 256 == 0 ? 256 : (cout <= 64 ? 64 : 128)));
     fa.ntq = (int32_t)((cout + bnt - 1) / bnt);
     const int64_t nt = (int64_t)fa.ntp * fa.ntq;
     if (nt > INT32_MAX) return DG_ERR_SHAPE;
@@ -714,9 +717,9 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     // two CTAs per SM (option f4_ct = 2; 128-wide tiles): 4 unpack and 4 epilogue warps per CTA
     const int ct = (bnt == 128 && opt(OPT_F4_CT) == 2) ? 2 : 1;
     const int nunp = ct == 2 ? 4 : ((int)opt(OPT_F4_UNP) == 4 ? 4 : ((int)opt(OPT_F4_UNP) == 8 ? 8 : (direct ? 4 : 8)));
-    const int nepi = ct == 2 ? 4 : ((int)opt(OPT_F4_EPI) == 4 ? 4 : 8);   // (auto: 8, measured -5..-20 % on every FP4 layer)
+    const int nepi = ct == 2 ? 4 : (bnt == 64 ? 8 : ((int)opt(OPT_F4_EPI) == 4 ? 4 : 8));   // (auto: 8, measured -5..-20 % on every FP4 layer)
     typedef void (*CfKern)(const CUtensorMap, const CUtensorMap, const CfArgs, const RequantArgs);
-    static const CfKern kerns[18] = {
+    static const CfKern kerns[22] = {
         lut_conv_f4_kernel<true, 4, false, 128, 4, 1>, lut_conv_f4_kernel<true, 8, false, 128, 4, 1>,
         lut_conv_f4_kernel<true, 4, true, 128, 4, 1>,  lut_conv_f4_kernel<true, 8, true, 128, 4, 1>,
         lut_conv_f4_kernel<true, 4, false, 256, 4, 1>, lut_conv_f4_kernel<true, 8, false, 256, 4, 1>,
@@ -725,10 +728,13 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
         lut_conv_f4_kernel<true, 4, true, 128, 8, 1>,  lut_conv_f4_kernel<true, 8, true, 128, 8, 1>,
         lut_conv_f4_kernel<true, 4, false, 256, 8, 1>, lut_conv_f4_kernel<true, 8, false, 256, 8, 1>,
         lut_conv_f4_kernel<true, 4, true, 256, 8, 1>,  lut_conv_f4_kernel<true, 8, true, 256, 8, 1>,
-        lut_conv_f4_kernel<true, 4, false, 128, 4, 2>, lut_conv_f4_kernel<true, 4, true, 128, 4, 2>};
-    static bool attr[18] = {};
-    const int ai = ct == 2 ? 16 + (direct ? 1 : 0)
-                           : (nepi == 8 ? 8 : 0) + (bnt == 256 ? 4 : 0) + (direct ? 2 : 0) + (nunp == 8 ? 1 : 0);
+        lut_conv_f4_kernel<true, 4, false, 128, 4, 2>, lut_conv_f4_kernel<true, 4, true, 128, 4, 2>,
+        lut_conv_f4_kernel<true, 4, false, 64, 8, 1>,  lut_conv_f4_kernel<true, 8, false, 64, 8, 1>,
+        lut_conv_f4_kernel<true, 4, true, 64, 8, 1>,   lut_conv_f4_kernel<true, 8, true, 64, 8, 1>};
+    static bool attr[22] = {};
+    const int ai = ct == 2      ? 16 + (direct ? 1 : 0)
+                   : bnt == 64 ? 18 + (direct ? 2 : 0) + (nunp == 8 ? 1 : 0)
+                               : (nepi == 8 ? 8 : 0) + (bnt == 256 ? 4 : 0) + (direct ? 2 : 0) + (nunp == 8 ? 1 : 0);
     const CfKern kern = kerns[ai];
     if (!attr[ai]) {
         if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, ct == 2 ? CF2_ALLOC : CF_ALLOC) !=
@@ -752,7 +758,7 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     if (cudaLaunchKernelEx(&lc, kern, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
     char tag[128];
     snprintf(tag, sizeof(tag), "f4conv bn=%d %s unp=%d epi=%d direct=%d rq=%d tab=%d early=%d omma=%d", bnt,
-             ct == 2 ? "ta nacc=1 ct=2" : (bnt == 256 ? "ta nacc=1" : "ta nacc=2"), nunp, nepi, fa.direct, fa.has_rq,
+             ct == 2 ? "ta nacc=1 ct=2" : (bnt == 256 ? "ta nacc=1" : (bnt == 64 ? "ta nacc=4" : "ta nacc=2")), nunp, nepi, fa.direct, fa.has_rq,
              fa.f16_tab, fa.early_b, fa.omma);
     set_last_kernel(tag);
     return launch_status();

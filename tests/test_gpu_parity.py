@@ -929,16 +929,19 @@ F4_CONVS = [  # B, H, W, C, Cout, k, stride, pad, pad_code
     (1, 8, 8, 256, 384, 3, 1, 1, 1),     # implicit, 1 tap per stage, 3 column tiles, pad code 1
     (2, 12, 12, 256, 128, 1, 2, 0, 0),   # implicit 1x1 stride 2 (downsample)
     (1, 7, 7, 512, 136, 3, 1, 1, 3),     # ragged Cout, K = 4608
+    (2, 9, 9, 256, 64, 1, 1, 0, 0),      # direct into 64 channels (one 64-wide tile)
+    (2, 10, 10, 64, 64, 3, 1, 1, 2),     # implicit 3x3 64 -> 64, K = 576
 ]
 
 
 @pytest.mark.parametrize("omma", [0, 1])
 @pytest.mark.parametrize("epi", [4, 8, "ct2"])
-@pytest.mark.parametrize("bn", [128, 256])
+@pytest.mark.parametrize("bn", [64, 128, 256])
 @pytest.mark.parametrize("wl", [(-2, -1, 0, 1), (-12, -3, 4, 8)])
 @pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", F4_CONVS)
 def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn, epi, omma):
-    """FP4 conv kernel vs O-CONV on both tile widths (128 channels, two accumulators; 256, one) and
+    """FP4 conv kernel vs O-CONV on the three tile widths (64 channels, four accumulators; 128, two;
+    256, one) and
     both epilogue arrangements (4 warps; 8 warps splitting the 256-wide tiles' columns or owning
     alternate 128-wide tiles): int32 output, fused 16-bit requant with a per-channel bias, a
     uniform-offset requant without bias, and a bias whose 16-bit offsets overflow (exact path)."""
@@ -956,8 +959,10 @@ def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn, e
     w4 = dg.expand_operand_f4(wp, k * k * Cp, wl)
     p = dg.conv_params(B, H, W, Cp, Cout, k, k, stride, pad, pad_code, ldw=wp.shape[1])
     dg.reset_options()
-    if epi == "ct2" and bn == 256:
+    if epi == "ct2" and bn != 128:
         pytest.skip("two CTAs per SM: 128-wide tiles only")
+    if bn == 64 and epi != 8:
+        pytest.skip("64-wide tiles: 8 epilogue warps only")
     ct = 2 if epi == "ct2" else 1
     epi = 4 if epi == "ct2" else epi
     with dg.options(f4_bn=bn, f4_epi=epi, f4_omma=omma, f4_ct=ct):
