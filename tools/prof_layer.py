@@ -23,15 +23,16 @@ ap.add_argument("--iters", type=int, default=5)
 ap.add_argument("--reps", type=int, default=8)
 ap.add_argument("--opt", action="append", default=[])
 ap.add_argument("--sweep", default="")
-ap.add_argument("--f4", default="", help="comma-separated layer ids on the FP4 conv kernel ('all' = every layer given)")
+ap.add_argument("--f4", default="", help="comma-separated layer ids on the FP4 conv kernel ('all' = every layer given, "
+                                         "'default' = netrun.f4_default's routing; empty = int8 kernels only)")
 a = ap.parse_args()
 for o in a.opt:
     k, v = o.split("=")
     dg.set_option(k, int(v))
 batch = a.batch or (256 if a.cfg == 3 else 64)
 layers = [int(x) for x in a.layers.split(",")]
-f4 = None if not a.f4 else (set(layers) if a.f4 == "all" else {int(x) for x in a.f4.split(",")})
-r = netrun.NetRunner(a.cfg, range(batch), "cuda", layers=layers, f4=f4 if f4 is not None else set())
+f4 = set() if not a.f4 else (None if a.f4 == "default" else (set(layers) if a.f4 == "all" else {int(x) for x in a.f4.split(",")}))
+r = netrun.NetRunner(a.cfg, range(batch), "cuda", layers=layers, f4=f4)
 sweep = [("", [None])]
 if a.sweep:
     k, vs = a.sweep.split("=")
@@ -42,6 +43,7 @@ for key, vals in sweep:
         if key:
             dg.set_option(key, v)
         outs = []
+        total = 0.0
         for i, p in enumerate(r.plans):
             sub = netrun.NetRunner.__new__(netrun.NetRunner)
             sub.__dict__.update(r.__dict__)
@@ -63,8 +65,10 @@ for key, vals in sweep:
                 ts.append(e0.elapsed_time(e1) / a.reps)
             ms = sorted(ts)[len(ts) // 2]
             outs.append(p.out.clone())
+            total += ms * 1e3
             print(f"{key}={v} L{layers[i]:02d} {p.name:24s} rows={p.rows} cout={p.layer.cout} K={p.K} "
                   f"{ms * 1e3:7.1f} us {p.ops / ms / 1e9:7.1f} TOPS  [{tag}]", flush=True)
+        print(f"{key}={v}: sum over the layers {total:.1f} us", flush=True)
         if ref is None:
             ref = outs
         else:
