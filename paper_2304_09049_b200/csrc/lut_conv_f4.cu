@@ -134,6 +134,14 @@ struct CfArgs {
     int64_t ldd;
     int32_t has_rq, early_b;
     int32_t omma;                // 1: the accumulators' origin comes from one MMA per tile (no reset stores)
+    // shifted window (GM = 2; direct 3x3 / stride 1 / pad 1, C = 64 or 128): tiles of 128 PADDED
+    // pixels q in [0, nqv), nqv = B (H+2)(W+2); the window = the WR padded input pixels q0 - Wp - 1
+    // .. in e2m1, K chunk j (32 codes, 16 bytes) of row i at j * lbo + 16 i (no swizzle), so tap
+    // (r, s) is the view starting r * Wp + s rows down; fetched packed into 2 ring slots of wslot
+    // bytes (cp.async), nwin windows of wbytes after them
+    int32_t Wp, WR, lbo, wslot, wbytes, nwin;
+    int64_t nqv;
+    CfDiv fd_hpwp, fd_wp;
     // 16-bit SIMD requant (host-verified, f16_params): x = clamp(acc + negA, 0, W), code = (x m + c) >> 14
     uint32_t f16_m, f16_c2, f16_w2, f16_na2;
     int32_t f16_tab, f16_thr0m1, f16_accmax;
@@ -194,13 +202,21 @@ __device__ __noinline__ void cf_epilogue_general(const CfArgs &fa, const Requant
 // one load round) or own alternate tiles of the 128-wide kernel's two accumulators
 // CT: CTAs per SM, 1, or 2 (BNT = 128, TA): two independent pipelines per SM on half the tensor and
 // shared memory each (one accumulator, three A stages per CTA)
-template <bool TA, int NUNP, bool DIRECT, int BNT, int NEPI, int CT>
+// GM: how the activations arrive: 0 implicit im2col gather (cp.async ring per unpack group), 1 direct
+// (1x1 / stride 1: TMA slots of the NHWC tensor), 2 shifted window (3x3 / stride 1 / pad 1: each
+// padded input pixel unpacked once per tile into a shared-memory window, 9 row-shifted views of it
+// are the A operands of shared-memory MMAs)
+template <bool TA, int NUNP, int GM, int BNT, int NEPI, int CT>
 __global__ void __launch_bounds__(32 * (3 + NEPI + NUNP), CT)
 lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CfArgs fa, const __grid_constant__ RequantArgs rq) {
+    constexpr bool DIRECT = GM == 1, WINM = GM == 2;
     constexpr bool C2 = CT == 2;
     static_assert(!C2 || (BNT == 128 && TA), "two CTAs per SM: 128-wide tiles, A in tensor memory");
     static_assert(BNT == 256 || BNT == 128 || (BNT == 64 && TA), "tile widths 64 (A in tensor memory), 128, 256");
+    static_assert(!WINM || (TA && !C2), "shifted window: one CTA per SM");
+    // window mode: the windows and their packed fetch ring after the origin-MMA B block
+    constexpr int OFF_W = CF_OFF_A + BNT * 128;
     constexpr int BN_ = BNT, SB_ = (C2 || BNT == 256) ? 3 : CF_SB, B_STAGE_ = BNT * CF_KST / 2;   // (96 / 48 KB of B stages)
     // accumulators: 256-wide 1, 128-wide 2 (two CTAs per SM: 1), 64-wide 4
     constexpr int CF_NACC = TA ? ((C2 || BNT == 256) ? 1 : (BNT == 64 ? 4 : 2)) : 3, CF_SA = TA ? (C2 ? 3 : 6) : 4;
@@ -250,7 +266,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 ptx::mbar_init(empty_b(s), 1);
             }
             for (int s = 0; s < CF_SA; ++s) {
-                ptx::mbar_init(full_a(s), 4);
+                ptx::mbar_init(full_a(s), WINM ? NUNP : 4);   // (window: every unpack warp fills it)
                 ptx::mbar_init(empty_a(s), 1);
             }
             for (int a = 0; a < CF_NACC; ++a) {
@@ -327,8 +343,9 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             ptx::mbar_wait(acc_empty(tl % CF_NACC), ((tl / CF_NACC) & 1u) ^ 1u);
             if (lane == 0) CF_EV(1, tl);
+            if (WINM) ptx::mbar_wait(full_a((int)(tl % (uint32_t)fa.nwin)), (tl / (uint32_t)fa.nwin) & 1u);   // the tile's window
             for (int s = 0; s < fa.nstages; ++s, ++g) {
-                ptx::mbar_wait(full_a(g % CF_SA), (g / CF_SA) & 1u);
+                if (!WINM) ptx::mbar_wait(full_a(g % CF_SA), (g / CF_SA) & 1u);
                 if (lane == 0) CF_EV(2, g);
                 ptx::mbar_wait(full_b(g % SB_), (g / SB_) & 1u);
                 if (lane == 0) CF_EV(3, g);
@@ -340,10 +357,21 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const uint32_t sfa = tmem + SF_COL, sfb = tmem + SF_COL + SFB_OFF;
         const int nst = fa.nstages, lastk = fa.last_ksteps;   // (in registers before any MMA is queued)
         const bool omma = fa.omma != 0;
+        // window geometry in registers before any MMA is queued (a parameter load between two
+        // tcgen05.mma waits for the queued MMAs): tap (r, s) starts r * Wp + s rows down (16 B each);
+        // the second 64-code chunk of a 128-channel tap is 2 K chunks (2 lbo) further
+        uint32_t w_tap[9];
+#pragma unroll
+        for (int q = 0; q < 9; ++q) w_tap[q] = WINM ? (uint32_t)((q / 3) * fa.Wp + q % 3) : 0u;
+        const uint32_t w_c2 = WINM ? (uint32_t)(fa.lbo >> 3) : 0u, w_sh = WINM ? (uint32_t)(fa.Cb_log2 - 4) : 0u;
+        const uint32_t w_base = sbase + OFF_W + (WINM ? 2u * (uint32_t)fa.wslot : 0u), w_bytes = WINM ? (uint32_t)fa.wbytes : 0u;
+        const uint32_t w_nwin = WINM ? (uint32_t)fa.nwin : 1u, w_lbo = WINM ? (uint32_t)fa.lbo : 0u;
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl % CF_NACC;
             const uint32_t dt = tmem + acc * BN_;
+            const uint32_t wb = WINM ? tl % w_nwin : 0u;
+            const uint64_t aw = WINM ? ptx::desc_k_none(w_base + wb * w_bytes, w_lbo) : 0ull;
             for (int s = 0; s < nst; ++s, ++g) {
                 const int sa = (int)(g % CF_SA), bs = (int)(g % SB_);
                 ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
@@ -355,6 +383,26 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 const uint64_t ad = ptx::desc_k_sw128(sbase + CF_OFF_A + sa * CF_A_STAGE);
                 const uint64_t bd = ptx::desc_k_sw128(sbase + CF_OFF_B + bs * B_STAGE_);
                 const uint32_t at = tmem + TA0 + (uint32_t)(sa * 32);
+                if constexpr (WINM) {   // k-step j = 4 s + k: tap j >> w_sh, 64-code chunk j & w_sh of it
+                    const int nk = s < nst - 1 ? 4 : lastk;
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        if (k >= nk) break;
+                        const uint32_t j = (uint32_t)(4 * s + k), tap = j >> w_sh;
+                        uint32_t toff = w_tap[0];
+#pragma unroll
+                        for (int q = 1; q < 9; ++q) toff = tap == (uint32_t)q ? w_tap[q] : toff;
+                        cf_mma(dt, aw + (uint64_t)(toff + (j & w_sh) * w_c2), bd + 2 * k, idesc, sfa, sfb);
+                    }
+                    if (lane == 0) CF_EV(15, g);
+                    ptx::mma_commit_warp(empty_b(bs));
+                    if (s == nst - 1) {
+                        ptx::mma_commit_warp(empty_a((int)wb));   // the window is free again
+                        ptx::mma_commit_warp(acc_full(acc));
+                    }
+                    __syncwarp();
+                    continue;
+                }
                 if (s < nst - 1) {
 #pragma unroll
                     for (int k = 0; k < 4; ++k) {
@@ -374,6 +422,81 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 __syncwarp();
                 if (lane == 0) CF_EV(4, g);
             }
+        }
+    } else if (WINM && warp >= CF_UNP0) {
+        // ---------------- window fill: thread = window row(s) (padded input pixels q0 - Wp - 1 + row):
+        // the packed pixel (C/4 bytes) arrives by cp.async two tiles ahead (ring of 2 slots), becomes
+        // e2m1 nibbles (the two masks per 16 codes) and is stored as C/32 16-byte K chunks (chunk j
+        // at j * lbo + 16 * row); all NUNP warps fill each tile's window
+        ptx::griddep_wait();
+        constexpr int NT = NUNP * 32, WMAXR = 3;
+        const int tid = (warp - CF_UNP0) * 32 + lane;
+        const int cb = 1 << fa.Cb_log2, nch = cb >> 4;   // packed bytes per pixel (16 / 32), 16-byte chunks
+        const int nrt = (fa.WR + NT - 1) / NT;            // window rows per thread (host: <= 3)
+        const uint32_t ring = sbase + OFF_W, wins = ring + 2u * (uint32_t)fa.wslot;
+        auto fetch = [&](int t, int slot) {
+            if (t < ntiles) {
+                const int tp = t / fa.ntq;
+                for (int i = 0; i < nrt; ++i) {
+                    const int row = tid + i * NT;
+                    if (row >= fa.WR) break;
+                    const int64_t q = (int64_t)tp * CF_BM - (fa.Wp + 1) + row;   // padded pixel of this row
+                    const uint8_t *src = nullptr;
+                    if (q >= 0 && q < fa.nqv) {
+                        const uint32_t b = cf_fdiv((uint32_t)q, fa.fd_hpwp);
+                        const uint32_t rem = (uint32_t)q - b * (uint32_t)((fa.H + 2) * fa.Wp);
+                        const uint32_t hp = cf_fdiv(rem, fa.fd_wp), wp = rem - hp * (uint32_t)fa.Wp;
+                        if (hp >= 1 && hp <= (uint32_t)fa.H && wp >= 1 && wp <= (uint32_t)fa.W)
+                            src = fa.X + ((((int64_t)b * fa.H + hp - 1) * fa.W + wp - 1) << fa.Cb_log2);
+                    }
+                    const uint32_t dst = ring + (uint32_t)(slot * fa.wslot + row * cb);
+                    for (int c = 0; c < nch; ++c) ptx::cp_async16(dst + 16 * c, src ? src + 16 * c : fa.padsrc);
+                }
+            }
+            ptx::cp_async_commit();
+        };
+        fetch(blockIdx.x, 0);
+        fetch(blockIdx.x + gridDim.x, 1);
+        uint32_t tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const int slot = (int)(tl & 1u), wb = (int)(tl % (uint32_t)fa.nwin);
+            ptx::cp_async_wait<1>();   // this tile's copies (the older group; each thread reads its own rows)
+            uint32_t e[WMAXR][16];
+#pragma unroll
+            for (int i = 0; i < WMAXR; ++i) {
+                const int row = tid + i * NT;
+#pragma unroll
+                for (int c = 0; c < 2; ++c) {
+                    const uint4 v = (i < nrt && row < fa.WR && c < nch) ? ptx::lds128(ring + (uint32_t)(slot * fa.wslot + row * cb + 16 * c))
+                                                                        : make_uint4(0, 0, 0, 0);
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        e[i][8 * c + 2 * k] = w[k] & 0x33333333u;
+                        e[i][8 * c + 2 * k + 1] = (w[k] >> 2) & 0x33333333u;
+                    }
+                }
+            }
+            fetch(t + 2 * (int)gridDim.x, slot);   // the slot's bytes are in registers: refill it
+            ptx::mbar_wait(empty_a(wb), ((tl / (uint32_t)fa.nwin) & 1u) ^ 1u);   // the window's previous tile finished
+            if (threadIdx.x == CF_UNP0 * 32) CF_EV(13, tl);
+#pragma unroll
+            for (int i = 0; i < WMAXR; ++i) {
+                const int row = tid + i * NT;
+                if (i >= nrt || row >= fa.WR) break;
+                const uint32_t wdst = wins + (uint32_t)(wb * fa.wbytes + row * 16);
+#pragma unroll
+                for (int j = 0; j < 4; ++j) {
+                    if (j >= 2 * nch) break;
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(wdst + (uint32_t)(j * fa.lbo)),
+                                 "r"(e[i][4 * j]), "r"(e[i][4 * j + 1]), "r"(e[i][4 * j + 2]), "r"(e[i][4 * j + 3])
+                                 : "memory");
+                }
+            }
+            ptx::fence_proxy_async_smem();   // generic-proxy stores -> visible to the tensor core
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(full_a(wb));
+            if (threadIdx.x == CF_UNP0 * 32) CF_EV(5, tl);
         }
     } else if (warp >= CF_UNP0) {
         // thread = pixel row r of the tile: 64 packed bytes (256 codes) per stage -> 32 words of e2m1
@@ -514,7 +637,18 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             if (NEPI == 8 && !CSPLIT && (int)(tl & 1u) != eg) continue;   // the other group's accumulator
             const int tq = t % fa.ntq, tp = t / fa.ntq;
-            const int64_t p = (int64_t)tp * CF_BM + quarter * 32 + lane;
+            int64_t p = (int64_t)tp * CF_BM + quarter * 32 + lane;
+            if (WINM) {   // padded pixel -> output pixel row, or np (not stored) for a padding position
+                const int64_t q = p;
+                p = fa.np;
+                if (q < fa.nqv) {
+                    const uint32_t b = cf_fdiv((uint32_t)q, fa.fd_hpwp);
+                    const uint32_t rem = (uint32_t)q - b * (uint32_t)((fa.H + 2) * fa.Wp);
+                    const uint32_t hp = cf_fdiv(rem, fa.fd_wp), wp = rem - hp * (uint32_t)fa.Wp;
+                    if (hp >= 1 && hp <= (uint32_t)fa.H && wp >= 1 && wp <= (uint32_t)fa.W)
+                        p = ((int64_t)b * fa.H + hp - 1) * fa.W + wp - 1;
+                }
+            }
             const int64_t q0 = (int64_t)tq * BN_;
             const uint32_t acc = tl % CF_NACC;
             ptx::mbar_wait(acc_full(acc), (tl / CF_NACC) & 1u);
@@ -662,6 +796,28 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     const int fbn = (int)opt(OPT_F4_BN);
     const int bnt = fbn == 64 ? 64 : fbn == 128 ? 128 : (fbn == 256 ? 256 : (cout % 256 == 0 ? 256 : (cout <= 64 ? 64 : 128)));
     fa.ntq = (int32_t)((cout + bnt - 1) / bnt);
+    // shifted window (option f4_win: 1 for every direct 3x3 / stride 1 / pad 1 conv over 64 or 128
+    // channels, 0 never): tiles over the padded pixel space, one window per tile
+    const bool win = !direct && opt(OPT_F4_WIN) > 0 && cv.kh == 3 && cv.kw == 3 && cv.stride == 1 && cv.pad == 1 &&
+                     (cb == 16 || cb == 32) && cv.Ho == cv.H && cv.Wo == cv.W;
+    if (win) {
+        const int64_t Wp = cv.W + 2, Hp = cv.H + 2, B = rows / ((int64_t)cv.H * cv.W);
+        fa.Wp = (int32_t)Wp;
+        fa.nqv = B * Hp * Wp;
+        if (fa.nqv >= ((int64_t)1 << 31)) return DG_ERR_SHAPE;
+        fa.ntp = (int32_t)((fa.nqv + CF_BM - 1) / CF_BM);
+        fa.WR = (int32_t)((CF_BM + 2 * Wp + 2 + 7) / 8 * 8);   // multiple of 8 rows: lbo a multiple of 128 B
+        if (fa.WR > 3 * 8 * 32) return DG_ERR_UNSUPPORTED;      // (at most 3 window rows per fill thread)
+        fa.lbo = fa.WR * 16;
+        fa.wslot = (fa.WR * cb + 127) / 128 * 128;
+        fa.wbytes = (cb / 8) * fa.lbo;                           // 2 Cb e2m1 bytes per row = Cb / 8 K chunks
+        const int region = CF_OFF_BAR - (CF_OFF_A + bnt * 128);
+        fa.nwin = (region - 2 * fa.wslot) / fa.wbytes;
+        if (fa.nwin > 3) fa.nwin = 3;
+        if (fa.nwin < 1) return DG_ERR_UNSUPPORTED;
+        fa.fd_hpwp = cf_div((uint32_t)(Hp * Wp));
+        fa.fd_wp = cf_div((uint32_t)Wp);
+    }
     const int64_t nt = (int64_t)fa.ntp * fa.ntq;
     if (nt > INT32_MAX) return DG_ERR_SHAPE;
     fa.ntiles = (int32_t)nt;
@@ -715,24 +871,27 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     // (the shared-memory-A form, TA = false, measured 5-20 % slower: kept in the source, not built)
     const bool ta = true;
     // two CTAs per SM (option f4_ct = 2; 128-wide tiles): 4 unpack and 4 epilogue warps per CTA
-    const int ct = (bnt == 128 && opt(OPT_F4_CT) == 2) ? 2 : 1;
-    const int nunp = ct == 2 ? 4 : ((int)opt(OPT_F4_UNP) == 4 ? 4 : ((int)opt(OPT_F4_UNP) == 8 ? 8 : (direct ? 4 : 8)));
-    const int nepi = ct == 2 ? 4 : (bnt == 64 ? 8 : ((int)opt(OPT_F4_EPI) == 4 ? 4 : 8));   // (auto: 8, measured -5..-20 % on every FP4 layer)
+    const int ct = (!win && bnt == 128 && opt(OPT_F4_CT) == 2) ? 2 : 1;
+    const int nunp = (ct == 2) ? 4 : win ? 8 : ((int)opt(OPT_F4_UNP) == 4 ? 4 : ((int)opt(OPT_F4_UNP) == 8 ? 8 : (direct ? 4 : 8)));
+    const int nepi = ct == 2 ? 4 : ((bnt == 64 || win) ? 8 : ((int)opt(OPT_F4_EPI) == 4 ? 4 : 8));   // (auto: 8, measured -5..-20 % on every FP4 layer)
     typedef void (*CfKern)(const CUtensorMap, const CUtensorMap, const CfArgs, const RequantArgs);
-    static const CfKern kerns[22] = {
-        lut_conv_f4_kernel<true, 4, false, 128, 4, 1>, lut_conv_f4_kernel<true, 8, false, 128, 4, 1>,
-        lut_conv_f4_kernel<true, 4, true, 128, 4, 1>,  lut_conv_f4_kernel<true, 8, true, 128, 4, 1>,
-        lut_conv_f4_kernel<true, 4, false, 256, 4, 1>, lut_conv_f4_kernel<true, 8, false, 256, 4, 1>,
-        lut_conv_f4_kernel<true, 4, true, 256, 4, 1>,  lut_conv_f4_kernel<true, 8, true, 256, 4, 1>,
-        lut_conv_f4_kernel<true, 4, false, 128, 8, 1>, lut_conv_f4_kernel<true, 8, false, 128, 8, 1>,
-        lut_conv_f4_kernel<true, 4, true, 128, 8, 1>,  lut_conv_f4_kernel<true, 8, true, 128, 8, 1>,
-        lut_conv_f4_kernel<true, 4, false, 256, 8, 1>, lut_conv_f4_kernel<true, 8, false, 256, 8, 1>,
-        lut_conv_f4_kernel<true, 4, true, 256, 8, 1>,  lut_conv_f4_kernel<true, 8, true, 256, 8, 1>,
-        lut_conv_f4_kernel<true, 4, false, 128, 4, 2>, lut_conv_f4_kernel<true, 4, true, 128, 4, 2>,
-        lut_conv_f4_kernel<true, 4, false, 64, 8, 1>,  lut_conv_f4_kernel<true, 8, false, 64, 8, 1>,
-        lut_conv_f4_kernel<true, 4, true, 64, 8, 1>,   lut_conv_f4_kernel<true, 8, true, 64, 8, 1>};
-    static bool attr[22] = {};
-    const int ai = ct == 2      ? 16 + (direct ? 1 : 0)
+    static const CfKern kerns[25] = {
+        lut_conv_f4_kernel<true, 4, 0, 128, 4, 1>, lut_conv_f4_kernel<true, 8, 0, 128, 4, 1>,
+        lut_conv_f4_kernel<true, 4, 1, 128, 4, 1>,  lut_conv_f4_kernel<true, 8, 1, 128, 4, 1>,
+        lut_conv_f4_kernel<true, 4, 0, 256, 4, 1>, lut_conv_f4_kernel<true, 8, 0, 256, 4, 1>,
+        lut_conv_f4_kernel<true, 4, 1, 256, 4, 1>,  lut_conv_f4_kernel<true, 8, 1, 256, 4, 1>,
+        lut_conv_f4_kernel<true, 4, 0, 128, 8, 1>, lut_conv_f4_kernel<true, 8, 0, 128, 8, 1>,
+        lut_conv_f4_kernel<true, 4, 1, 128, 8, 1>,  lut_conv_f4_kernel<true, 8, 1, 128, 8, 1>,
+        lut_conv_f4_kernel<true, 4, 0, 256, 8, 1>, lut_conv_f4_kernel<true, 8, 0, 256, 8, 1>,
+        lut_conv_f4_kernel<true, 4, 1, 256, 8, 1>,  lut_conv_f4_kernel<true, 8, 1, 256, 8, 1>,
+        lut_conv_f4_kernel<true, 4, 0, 128, 4, 2>, lut_conv_f4_kernel<true, 4, 1, 128, 4, 2>,
+        lut_conv_f4_kernel<true, 4, 0, 64, 8, 1>,  lut_conv_f4_kernel<true, 8, 0, 64, 8, 1>,
+        lut_conv_f4_kernel<true, 4, 1, 64, 8, 1>,   lut_conv_f4_kernel<true, 8, 1, 64, 8, 1>,
+        lut_conv_f4_kernel<true, 8, 2, 64, 8, 1>,   lut_conv_f4_kernel<true, 8, 2, 128, 8, 1>,
+        lut_conv_f4_kernel<true, 8, 2, 256, 8, 1>};
+    static bool attr[25] = {};
+    const int ai = win          ? (bnt == 64 ? 22 : bnt == 128 ? 23 : 24)
+                   : ct == 2    ? 16 + (direct ? 1 : 0)
                    : bnt == 64 ? 18 + (direct ? 2 : 0) + (nunp == 8 ? 1 : 0)
                                : (nepi == 8 ? 8 : 0) + (bnt == 256 ? 4 : 0) + (direct ? 2 : 0) + (nunp == 8 ? 1 : 0);
     const CfKern kern = kerns[ai];
@@ -757,7 +916,7 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     lc.numAttrs = 1;
     if (cudaLaunchKernelEx(&lc, kern, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
     char tag[128];
-    snprintf(tag, sizeof(tag), "f4conv bn=%d %s unp=%d epi=%d direct=%d rq=%d tab=%d early=%d omma=%d", bnt,
+    snprintf(tag, sizeof(tag), "f4conv bn=%d %s%s unp=%d epi=%d direct=%d rq=%d tab=%d early=%d omma=%d", bnt, win ? "win " : "",
              ct == 2 ? "ta nacc=1 ct=2" : (bnt == 256 ? "ta nacc=1" : (bnt == 64 ? "ta nacc=4" : "ta nacc=2")), nunp, nepi, fa.direct, fa.has_rq,
              fa.f16_tab, fa.early_b, fa.omma);
     set_last_kernel(tag);

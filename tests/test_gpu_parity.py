@@ -991,6 +991,58 @@ def _conv_f4_cases(xp, w4, lut, p, exp, Cout, g, bn, epi):
         assert np.array_equal(oracle_codes_of(codes, exp.shape[0], Cout), expc)
 
 
+F4_WIN_CONVS = [  # B, H, W, C, Cout, pad_code (3x3 / stride 1 / pad 1)
+    (2, 10, 10, 64, 64, 0),
+    (3, 7, 9, 128, 256, 1),
+    (1, 20, 30, 64, 200, 2),      # ragged Cout
+    (2, 5, 5, 128, 128, 3),       # tiles mostly padding
+    (4, 28, 28, 64, 128, 0),      # many tiles per CTA: window ring reuse
+    (1, 56, 56, 128, 256, 1),
+    (1, 3, 200, 64, 64, 2),       # wide rows: 3 window rows per fill thread
+]
+
+
+@pytest.mark.parametrize("omma", [0, 1])
+@pytest.mark.parametrize("wl", [(-2, -1, 0, 1), (-12, -3, 4, 8)])
+@pytest.mark.parametrize("B,H,W,C,Cout,pad_code", F4_WIN_CONVS)
+def test_conv_f4_window_vs_oracle(B, H, W, C, Cout, pad_code, omma, wl):
+    """FP4 conv, shifted-window mode (each padded input pixel unpacked once per tile into a shared-
+    memory window; the 9 taps are row-shifted views, shared-memory MMAs) vs O-CONV: int32 and the
+    fused requant with a per-channel bias (levels -2..1: every case has a 16-bit requant form), the
+    instance asserted by its tag."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    wl = list(wl)
+    lut = dg.build_lut(wl, AL, 8)
+    T = oracle.build_lut16(wl, AL)
+    g = np.random.default_rng(B + H + W + C + Cout + pad_code)
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, 3, 3, C), dtype=np.uint8)
+    exp = oracle.conv2d_direct(x, w, T, 1, 1, pad_code).reshape(-1, Cout)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    w4 = dg.expand_operand_f4(wp, 9 * Cp, wl)
+    p = dg.conv_params(B, H, W, Cp, Cout, 3, 3, 1, 1, pad_code, ldw=wp.shape[1])
+    dg.reset_options()
+    with dg.options(f4_win=1, f4_omma=omma):
+        out = dg.lut_conv2d_f4_prepared(xp, w4, lut, p)
+        tag = dg.last_kernel()
+        assert " win " in tag, tag
+        assert np.array_equal(host(out), exp)
+        if Cout % 4 == 0:
+            bias = (-int(np.round(exp.mean())) + g.integers(-40, 40, Cout)).astype(np.int32)
+            mult = max(1, int(round((1 << 20) * 1.2 / max(1.0, float(exp.std())))))
+            rq = dg.Requant(mult, 20, 1, 0, 3, bias=torch.from_numpy(bias).to(DEV), bias_axis=0)
+            try:
+                codes = dg.lut_conv2d_f4_prepared(xp, w4, lut, p, rq=rq)
+            except dg.DGError as e:   # (no 16-bit form of these parameters: the caller takes the int8 path)
+                assert "UNSUPPORTED" in str(e) and wl[0] == -12
+                return
+            assert " win " in dg.last_kernel(), dg.last_kernel()
+            expc = oracle.requantize(exp, mult, 20, 1, 0, 3, bias=bias, bias_axis=0)
+            assert np.array_equal(oracle_codes_of(codes, exp.shape[0], Cout), expc)
+
+
 def test_conv_f4_accumulator_origin_at_the_bound():
     """The FP4 conv accumulates from 1.5 * 2^23: at the largest K the API admits (K * 36 < 2^22 for
     weight level -12 and activation level 3), all-max products first then a random tail, positive and
