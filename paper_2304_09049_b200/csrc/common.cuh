@@ -207,6 +207,7 @@ enum OptId {
     OPT_F4_BN,          // FP4 conv tile width: 0 auto (256 when 256 | Cout), 128 or 256
     OPT_F4_OMMA,        // FP4 conv kernel: accumulator origin from one MMA per tile (1) or reset stores (0)
     OPT_F4_CT,          // FP4 conv kernel: CTAs per SM for 128-wide tiles (2) or 1 (0 / 1)
+    OPT_SKFUSE,         // split-K slices reduced by the GEMM kernel itself after a grid barrier (1) or a second kernel (0, default)
     OPT_F4_WIN,         // FP4 conv kernel: shifted window for direct 3x3 s1 p1 convs over 64 / 128 channels (1), 0 off
     OPT_COUNT
 };

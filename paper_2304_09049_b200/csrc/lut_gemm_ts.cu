@@ -18,6 +18,7 @@
 //                 contiguous bulk copy when rows are <= 32 B) and int8 B stages (TMA, SW128)
 //   warp 13       waiter: waits on the MMA-side mbarriers, hands stages to warp 14 by bar.sync
 //   warp 14       MMA issuer (one thread): tcgen05.mma [D], [A_tmem], B_desc, 4 k-steps/stage
+#include <cooperative_groups.h>
 #include <cuda.h>
 #include <stdio.h>
 #include <stdlib.h>
@@ -152,8 +153,11 @@ struct TsArgs {
     int32_t group;         // tile rasterisation: GROUP row blocks x all column blocks, column-major inside
     // split-K (few output tiles, long K): work item t = output tile t / sk, K stages of split t % sk;
     // each split stores its partial sums to its own slice ws_acc[ks] (int32 [sk][np][nq]); the
-    // splitk_reduce_kernel launched right behind sums the slices and requantises / stores
+    // slices are summed and requantised / stored either by the same (cooperatively launched) kernel
+    // after a grid-wide barrier (sk_fused: no second launch on the latency-bound chains) or by the
+    // splitk_reduce_kernel launched right behind
     int32_t sk, nwork;   // nwork = ntp * ntq * sk work items
+    int32_t sk_fused;
     // fused all-gather (int32 output): every output tile is also stored to npeer extra
     // destinations (peer GPUs' C buffers, P2P-mapped, already offset to this rank's rows)
     int32_t npeer;
@@ -429,13 +433,11 @@ __device__ __noinline__ void ts_epilogue_splitk(const TsArgs &ta, uint32_t trow,
 // split-K reduction: one thread per (row p, 4 consecutive columns): sum the sk <= 8 slices (all
 // loads in flight at once), then requantise to one byte of codes (4 columns, LSB first; columns
 // past nq give zero bits, as the fused epilogue writes them) or store the int32 sums.
-__global__ void __launch_bounds__(256) splitk_reduce_kernel(const int32_t *__restrict__ ws, int64_t np, int64_t nq,
-                                                            int32_t sk, void *D, int64_t ldd, int32_t has_rq,
-                                                            RequantArgs rq) {
-    ptx::griddep_wait();   // the split-K GEMM's slices are complete and visible
+DG_DEV void splitk_reduce_range(const int32_t *__restrict__ ws, int64_t np, int64_t nq, int32_t sk, void *D, int64_t ldd,
+                                int32_t has_rq, const RequantArgs &rq, int64_t i0, int64_t di) {
     const int64_t ng = (nq + 3) >> 2, n = np * ng, slice = np * nq;
     const bool vec = (nq & 3) == 0;
-    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t i = i0; i < n; i += di) {
         const int64_t p = i / ng, q = (i - p * ng) * 4;
         const int32_t *src = ws + p * nq + q;
         int32_t v[4] = {0, 0, 0, 0};
@@ -464,6 +466,14 @@ __global__ void __launch_bounds__(256) splitk_reduce_kernel(const int32_t *__res
             reinterpret_cast<uint8_t *>(D)[p * ldd + (q >> 2)] = (uint8_t)b;
         }
     }
+}
+
+__global__ void __launch_bounds__(256) splitk_reduce_kernel(const int32_t *__restrict__ ws, int64_t np, int64_t nq,
+                                                            int32_t sk, void *D, int64_t ldd, int32_t has_rq,
+                                                            RequantArgs rq) {
+    ptx::griddep_wait();   // the split-K GEMM's slices are complete and visible
+    splitk_reduce_range(ws, np, nq, sk, D, ldd, has_rq, rq, (int64_t)blockIdx.x * blockDim.x + threadIdx.x,
+                        (int64_t)gridDim.x * blockDim.x);
 }
 
 // 16-bit SIMD requant of one tile (S7): RES = 0 no residual, 1 identity shortcut over packed
@@ -1458,6 +1468,13 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         for (int i = threadIdx.x; i < TL_E * TL_N; i += blockDim.x) (&g_ts_tl[0][0])[i] = (&s_tl[0][0])[i];
 #endif
     if (warp == PRODUCER_WARP) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+    if (SK && ta.sk > 1 && ta.sk_fused) {
+        // every split's slice is stored (grid-wide barrier of the cooperative launch, with its memory
+        // ordering): all threads of the grid sum the slices and requantise / store
+        cooperative_groups::this_grid().sync();
+        splitk_reduce_range(ta.ws_acc, ta.np, ta.nq, ta.sk, ta.D, ta.ldd, ta.has_rq, rq,
+                            (int64_t)blockIdx.x * blockDim.x + threadIdx.x, (int64_t)gridDim.x * blockDim.x);
+    }
 }
 
 // ---- Q expansion: packed codes -> int8 levels in the unpack16_levels order, zero beyond K.
@@ -1753,6 +1770,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
             ta.sk = (int32_t)sk;
             ta.fd_sk = make_fastdiv((uint32_t)sk);
             ta.ws_acc = reinterpret_cast<int32_t *>(skws);
+            ta.sk_fused = opt(OPT_SKFUSE) ? 1 : 0;
         }
     }
     RequantArgs dummy{};
@@ -1766,14 +1784,16 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     lc.blockDim = dim3((unsigned)Roles<NEPI, NUNP, EM>::NT);
     lc.dynamicSmemBytes = C::ALLOC;
     lc.stream = st;
-    cudaLaunchAttribute la[1];
+    cudaLaunchAttribute la[2];
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     la[0].val.programmaticStreamSerializationAllowed = opt(OPT_PDL) ? 1 : 0;
+    la[1].id = cudaLaunchAttributeCooperative;   // (grid <= one CTA per SM: always co-resident)
+    la[1].val.cooperative = 1;
     lc.attrs = la;
-    lc.numAttrs = 1;
+    lc.numAttrs = ta.sk_fused ? 2 : 1;
     if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK, EM>, mp, mb, md, pmaps, ta, rqv) != cudaSuccess)
         return DG_ERR_CUDA;
-    if (ta.sk > 1) {
+    if (ta.sk > 1 && !ta.sk_fused) {
         const int64_t thr = np * ((nq + 3) >> 2);
         int64_t blocks = (thr + 255) / 256;
         if (blocks > (int64_t)num_sms() * 8) blocks = (int64_t)num_sms() * 8;
@@ -1786,10 +1806,10 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     }
     char tag[160];
     snprintf(tag, sizeof(tag), "ts bn=%d epi=%d unp=%d kst=%d%s%s%s em=%d nwin=%d wpair=%d sk=%d bres=%d f16=%d implicit=%d bulk=%d early=%d tmad=%d",
-             BN, NEPI, NUNP, KST, WIN ? " win" : "", ASM ? " asm" : "", SK ? " skinst" : "", EM, ta.nwin, ta.wpair, ta.sk,
+             BN, NEPI, NUNP, KST, WIN ? " win" : "", ASM ? " asm" : "", SK ? (ta.sk_fused ? " skinst fused" : " skinst") : "", EM, ta.nwin, ta.wpair, ta.sk,
              ta.bres, ta.f16, ta.implicit, ta.bulk, ta.early_b, ta.tma_d);
     set_last_kernel(tag);
-    return launch_status(ta.sk > 1 ? 2 : 1);
+    return launch_status(ta.sk > 1 && !ta.sk_fused ? 2 : 1);
 }
 
 }  // namespace

@@ -577,13 +577,18 @@ SPLITK_CONVS = [  # B, H, C, Cout, k, stride: few output tiles, long K -> split-
 ]
 
 
+@pytest.mark.parametrize("skfuse", [1, 0])
 @pytest.mark.parametrize("B,H,C,Cout,k,stride", SPLITK_CONVS)
-def test_conv_splitk_vs_oracle(B, H, C, Cout, k, stride):
+def test_conv_splitk_vs_oracle(B, H, C, Cout, k, stride, skfuse):
     """Small-batch convs (ResNet-18 b1 shapes) whose few output tiles run as split-K: each split
-    writes its int32 partial slice into the workspace tail (garbage on entry), the reduce kernel
-    sums them and requantises; int32 output, fused requant and an int32 residual."""
+    writes its int32 partial slice into the workspace tail (garbage on entry); the slices are summed
+    and requantised by the GEMM kernel itself after a grid-wide barrier (cooperative launch,
+    skfuse = 1, one launch) or by the reduce kernel (skfuse = 0, two launches); int32 output, fused
+    requant and an int32 residual."""
     if not _tc_available():
         pytest.skip("tc unavailable")
+    dg.reset_options()
+    dg.set_option("skfuse", skfuse)
     lut = dg.build_lut(WL, AL, 8)
     T = oracle.build_lut16(WL, AL)
     g = np.random.default_rng(B * 100 + H + C + Cout + k)
@@ -598,9 +603,10 @@ def test_conv_splitk_vs_oracle(B, H, C, Cout, k, stride):
     ws = torch.full((dg.conv_workspace_size(p),), 0xA5, dtype=torch.uint8, device=DEV)
     n0 = dg.kernel_launches()
     out = dg.lut_conv2d_prepared(xp, w8, lut, p, ws=ws)
-    if k == 3:   # implicit GEMM split over K + the reduce kernel
-        assert dg.kernel_launches() - n0 == 2
+    if k == 3:   # implicit GEMM split over K (+ the reduce kernel)
+        assert dg.kernel_launches() - n0 == (1 if skfuse else 2)
         assert "skinst" in dg.last_kernel() and "sk=1 " not in dg.last_kernel(), dg.last_kernel()
+        assert (" fused " in dg.last_kernel()) == bool(skfuse), dg.last_kernel()
     assert np.array_equal(host(out).reshape(exp.shape), exp)
     if Cout % 4:
         return
@@ -614,6 +620,7 @@ def test_conv_splitk_vs_oracle(B, H, C, Cout, k, stride):
     outr = dg.lut_conv2d_prepared(xp, w8, lut, p, rq=dg.Requant(mult=20000, shift=20, res=torch.from_numpy(res).to(DEV)), ws=ws)
     expr = oracle.requantize(e2, 20000, 20, 0, 0, 3, res=res)
     assert np.array_equal(oracle_codes_of(outr, expr.shape[0], Cout), expr)
+    dg.reset_options()
 
 
 # ---- block-scaled FP4 path (tcgen05 kind::mxf4) -------------------------
