@@ -89,6 +89,31 @@ def f4_case():
     return dg.last_kernel(), np.array_equal(C.cpu().numpy(), oracle.lut_gemm(W, A, oracle.build_lut16(WL, AL)))
 
 
+def f4conv_case(B, H, W, C, Cout, k, stride, opts, seed=6):
+    """FP4 conv kernel instance (dg_lut_conv2d_f4_prepared): int32 and the fused 16-bit requant."""
+    g = np.random.default_rng(seed + B + H + C + Cout + k)
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, k, k, C), dtype=np.uint8)
+    pad = k // 2
+    T = oracle.build_lut16(WL, AL)
+    exp = oracle.conv2d_direct(x, w, T, stride, pad, 0).reshape(-1, Cout)
+    xp = pack(x.reshape(-1, C))[:, : C // 4].contiguous()
+    wp = pack(w.reshape(Cout, -1), True)
+    w4 = dg.expand_operand_f4(wp, k * k * C, WL)
+    p = dg.conv_params(B, H, W, C, Cout, k, k, stride, pad, 0, ldw=wp.shape[1])
+    lut = dg.build_lut(WL, AL, 8)
+    bias = (-int(np.round(exp.mean())) + g.integers(-30, 30, Cout)).astype(np.int32)
+    rq = dg.Requant(20000, 20, 1, 0, 3, bias=torch.from_numpy(bias).to(DEV), bias_axis=0)
+    with dg.options(**opts):
+        out = dg.lut_conv2d_f4_prepared(xp, w4, lut, p)
+        tag = dg.last_kernel()
+        codes = dg.lut_conv2d_f4_prepared(xp, w4, lut, p, rq=rq)
+    torch.cuda.synchronize()
+    ok = np.array_equal(out.cpu().numpy(), exp) and np.array_equal(
+        codes_of(codes, exp.shape[0], Cout), oracle.requantize(exp, 20000, 20, 1, 0, 3, bias=bias, bias_axis=0))
+    return tag, ok
+
+
 def onehot_case():
     g = np.random.default_rng(4)
     M, N, K = 130, 200, 300
@@ -134,6 +159,15 @@ CASES = {
     "splitk_res": lambda: conv_case(1, 7, 7, 256, 128, 3, 1, {"win": -1}, ws_fill=0xA5, res=False),
     "direct_res": lambda: conv_case(2, 6, 6, 64, 64, 1, 1, {}, res=True),
     "f4": f4_case,
+    "f4conv_bn256": lambda: f4conv_case(2, 9, 9, 256, 512, 1, 1, {}),
+    "f4conv_bn256_e4": lambda: f4conv_case(2, 9, 9, 256, 256, 1, 1, {"f4_epi": 4, "f4_omma": 0}),
+    "f4conv_bn128": lambda: f4conv_case(2, 9, 9, 256, 128, 1, 1, {}),
+    "f4conv_bn64": lambda: f4conv_case(2, 9, 9, 256, 64, 1, 1, {}),
+    "f4conv_gather": lambda: f4conv_case(1, 8, 8, 256, 256, 3, 1, {}),
+    "f4conv_gather_s2": lambda: f4conv_case(2, 9, 9, 128, 128, 3, 2, {}),
+    "f4conv_ct2": lambda: f4conv_case(2, 9, 9, 256, 128, 1, 1, {"f4_ct": 2}),
+    "f4conv_win": lambda: f4conv_case(2, 10, 10, 64, 128, 3, 1, {"f4_win": 1}),
+    "splitk_fused": lambda: conv_case(1, 7, 7, 256, 256, 3, 1, {"win": -1, "skfuse": 1}, ws_fill=0xA5),
     "onehot": onehot_case,
     "cc": lambda: variant_case("cc"),
     "tc_ss": lambda: variant_case("tc_ss"),
