@@ -574,6 +574,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     if (slot_end) ++gp;
                 } else {
                     ptx::cp_async_wait<IGG - 1>();   // this stage's copies (the oldest group) landed
+                    if ((warp & 3) == 0 && lane == 0) CF_EV(12, g);
                     const int slot = (int)(own % IGG);
 #pragma unroll
                     for (int c = 0; c < 4; ++c)
@@ -593,7 +594,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
                 const int sa = (int)(g % CF_SA);
                 ptx::mbar_wait(empty_a(sa), ((g / CF_SA) & 1u) ^ 1u);
-                if (threadIdx.x == CF_UNP0 * 32) CF_EV(13, g);
+                if ((warp & 3) == 0 && lane == 0) CF_EV(13, g);
                 if constexpr (TA) {   // row r = lane quarter (warp & 3) x 32 + lane: 32 columns of this stage
                     ptx::tc_fence_after();
                     ptx::tmem_st_32x32b_x32(tmem + TA0 + (uint32_t)(sa * 32) + ((uint32_t)((warp & 3) * 32) << 16), e);
@@ -611,7 +612,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(full_a(sa));
-                if (threadIdx.x == CF_UNP0 * 32) CF_EV(5, g);
+                if ((warp & 3) == 0 && lane == 0) CF_EV(5, g);
             }
         }
     } else {
