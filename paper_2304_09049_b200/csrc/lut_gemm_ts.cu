@@ -953,24 +953,33 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         // wide images (window > one row per thread, C = 64 only): thread tid owns rows tid + i*NUNP*32
         constexpr int WMAXR = 3;
         const int nrt = (ta.WR + NUNP * 32 - 1) / (NUNP * 32);
+        // window row -> source pixel, in 32-bit arithmetic (host: B (H+2)(W+2) < 2^31 and the NHWC byte
+        // offsets < 2^31): the fill warps' address chains paced the C = 64 layers (trace: ~1200 cycles
+        // of each fill's ~2400 went to this fetch with 64-bit index math)
+        const uint32_t w_hpwp = (uint32_t)((ta.H + 2) * ta.Wp), w_nqv = (uint32_t)ta.nqv, w_wp = (uint32_t)ta.Wp;
+        const uint32_t w_h = (uint32_t)ta.H, w_w = (uint32_t)ta.W, w_sh = (uint32_t)(ta.clog2 - 2);
         auto fetch = [&](int t, int slot) {
             if (t < ntiles) {
                 int tp, tq;
                 tile_coords(ta, t, tp, tq);
+                const uint32_t q0 = ((uint32_t)tp << ta.wpair) * BM - (w_wp + 1u);   // (wraps for the first rows)
                 for (int i = 0; i < nrt; ++i) {
                     const int row = tid + i * NUNP * 32;
                     if (row >= ta.WR) break;
-                    const int64_t q = ((int64_t)tp << ta.wpair) * BM - (ta.Wp + 1) + row;   // padded pixel of this row
-                    const uint8_t *src = nullptr;
-                    if (q >= 0 && q < ta.nqv) {
-                        const uint32_t b = fdiv((uint32_t)q, ta.fd_hpwp);
-                        const uint32_t rem = (uint32_t)q - b * (uint32_t)((ta.H + 2) * ta.Wp);
-                        const uint32_t hp = fdiv(rem, ta.fd_wp), wp = rem - hp * (uint32_t)ta.Wp;
-                        if (hp >= 1 && hp <= (uint32_t)ta.H && wp >= 1 && wp <= (uint32_t)ta.W)
-                            src = ta.X + ((((int64_t)b * ta.H + hp - 1) * ta.W + wp - 1) << (ta.clog2 - 2));
+                    const uint32_t q = q0 + (uint32_t)row;   // padded pixel of this row
+                    const uint8_t *src = ta.padsrc;
+                    uint32_t step = 0;
+                    if (q < w_nqv) {
+                        const uint32_t b = fdiv(q, ta.fd_hpwp);
+                        const uint32_t rem = q - b * w_hpwp;
+                        const uint32_t hp = fdiv(rem, ta.fd_wp), wp = rem - hp * w_wp;
+                        if (hp - 1u < w_h && wp - 1u < w_w) {
+                            src = ta.X + (((b * w_h + hp - 1u) * w_w + wp - 1u) << w_sh);
+                            step = 16;
+                        }
                     }
                     const uint32_t dst = ring + (uint32_t)(slot * ta.wslot + row * cb);
-                    for (int c = 0; c < nch; ++c) ptx::cp_async16(dst + 16 * c, src ? src + 16 * c : ta.padsrc);
+                    for (int c = 0; c < nch; ++c) ptx::cp_async16(dst + 16 * c, src + c * step);
                 }
             }
             ptx::cp_async_commit();
@@ -1601,6 +1610,7 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         ta.Wp = (int32_t)Wp;
         ta.nqv = B * Hp * Wp;
         if (ta.nqv >= ((int64_t)1 << 31)) return DG_ERR_SHAPE;
+        if (np * cv->Cb >= ((int64_t)1 << 32)) return DG_ERR_UNSUPPORTED;   // (32-bit window fetch offsets)
         ta.ntp = (int32_t)((ta.nqv + BM - 1) / BM);
         // pair mode (tile mode on 64-wide tiles: C = 64, Cout <= 64, K = 576, weights resident): one window feeds 2 row blocks, so the halo rows are filled once per 2 blocks
         ta.wpair = ((BN == 64 || BN == 128) && KST == 256 && cv->Cb == 16 && K == 576 && nq <= BN && opt(OPT_WPAIR)) ? 1 : 0;

@@ -60,9 +60,9 @@ if len(sys.argv) > 2 and sys.argv[2] == "--win":
     print("stage: waiter_fullA w_fullB handoff mma_start mma_end")
     for g in range(0, 30):
         print(f"{g:4d} " + " ".join(f"{a[e][g]:8d}" for e in (4, 5, 6, 14, 15)))
-    print("tile unp0 cpa_ok unp_done emptyW fullW_arr waiter_fullW  w_start epi0 epi_accfull epi_done")
+    print("tile unp0 cpa_ok unpacked fetched emptyW fullW_arr waiter_fullW  w_start epi0 epi_accfull epi_done")
     for t in range(0, 40):
-        print(f"{t:4d} " + " ".join(f"{a[e][t]:8d}" for e in (0, 12, 1, 11, 2, 13, 3, 8, 9, 10)))
+        print(f"{t:4d} " + " ".join(f"{a[e][t]:8d}" for e in (0, 12, 21, 1, 11, 2, 13, 3, 8, 9, 10)))
 print("tile  w_start  epi0   epi_accfull  ld0_ok  r0_done  ld1_ok  r1_done  epi_done   (warp 0: even tiles)")
 for t in list(range(0, 16)) + list(range(38, 43)):
     print(f"{t:4d} " + " ".join(f"{a[e][t]:8d}" for e in (3, 8, 9, 16, 17, 18, 19, 10)))
