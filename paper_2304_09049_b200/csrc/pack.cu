@@ -162,6 +162,68 @@ __global__ void __launch_bounds__(256) im2col_kernel(const uint8_t *__restrict__
     }
 }
 
+// Narrow pixels (C/4 % 4 != 0, e.g. VGG conv1_1's C = 3 -> 4: one packed byte per pixel), short rows
+// (ld <= 64 bytes): one thread per output ROW forms (b, ho, wo) once and assembles the row's
+// kh*kw*Cb bytes in registers, then writes it with 16-byte stores (the byte-per-thread form above
+// did two divisions and a byte store per output byte: 260 us for VGG conv1_1 at batch 64).
+template <int KH, int KW, int CB>   // 0: runtime (kh, kw, Cb)
+__global__ void __launch_bounds__(256) im2col_rows_kernel(const uint8_t *__restrict__ x, int32_t H, int32_t W,
+                                                          int32_t Cb_, int32_t kh_, int32_t kw_, int32_t stride,
+                                                          int32_t pad, uint32_t pad_byte, int32_t Ho, int32_t Wo,
+                                                          int32_t rows, uint8_t *__restrict__ cols, int32_t ld) {
+    const int32_t kh = KH ? KH : kh_, kw = KW ? KW : kw_, Cb = CB ? CB : Cb_;
+    (void)kh;
+    (void)kw;
+    for (int32_t row = blockIdx.x * blockDim.x + threadIdx.x; row < rows; row += gridDim.x * blockDim.x) {
+        const int32_t t = row / Wo, wo = row - t * Wo;
+        const int32_t b = t / Ho, ho = t - b * Ho;
+        uint32_t w[16];
+#pragma unroll
+        for (int j = 0; j < 16; ++j) w[j] = 0;
+        const uint8_t *img = x + (int64_t)b * H * W * Cb;
+        if constexpr (KH && KW && CB) {   // every byte index a compile-time constant
+#pragma unroll
+            for (int32_t r = 0; r < KH; ++r) {
+                const int32_t hi = ho * stride - pad + r;
+#pragma unroll
+                for (int32_t s = 0; s < KW; ++s) {
+                    const int32_t wi = wo * stride - pad + s;
+                    const bool in = (uint32_t)hi < (uint32_t)H && (uint32_t)wi < (uint32_t)W;
+                    const uint8_t *src = img + (hi * W + wi) * CB;
+#pragma unroll
+                    for (int32_t c = 0; c < CB; ++c) {
+                        const int32_t idx = (r * KW + s) * CB + c;
+                        w[idx >> 2] |= (in ? (uint32_t)__ldg(src + c) : pad_byte) << (8 * (idx & 3));
+                    }
+                }
+            }
+        } else {
+            int32_t idx = 0;
+#pragma unroll 1
+            for (int32_t r = 0; r < kh; ++r) {
+                const int32_t hi = ho * stride - pad + r;
+#pragma unroll 1
+                for (int32_t s = 0; s < kw; ++s) {
+                    const int32_t wi = wo * stride - pad + s;
+                    const bool in = (uint32_t)hi < (uint32_t)H && (uint32_t)wi < (uint32_t)W;
+                    const uint8_t *src = img + (hi * W + wi) * Cb;
+#pragma unroll 1
+                    for (int32_t c = 0; c < Cb; ++c, ++idx) {
+                        const uint32_t v = in ? (uint32_t)__ldg(src + c) : pad_byte;
+#pragma unroll
+                        for (int j = 0; j < 16; ++j)   // (register-resident: word idx >> 2 by compare)
+                            if (j == (idx >> 2)) w[j] |= v << (8 * (idx & 3));
+                    }
+                }
+            }
+        }
+        uint4 *dst = reinterpret_cast<uint4 *>(cols + (int64_t)row * ld);
+#pragma unroll
+        for (int j = 0; j < 4; ++j)
+            if (16 * j < ld) dst[j] = make_uint4(w[4 * j], w[4 * j + 1], w[4 * j + 2], w[4 * j + 3]);
+    }
+}
+
 template <int V>
 void launch_im2col(const uint8_t *x, int32_t B, int32_t H, int32_t W, int32_t Cb, int32_t kh, int32_t kw, int32_t stride,
                    int32_t pad, uint32_t pad_byte, int32_t Ho, int32_t Wo, uint8_t *cols, int64_t ld, cudaStream_t st) {
@@ -279,6 +341,16 @@ dg_status dg_im2col(const uint8_t *d_x, int32_t B, int32_t H, int32_t W, int32_t
         launch_im2col<16>(d_x, B, H, W, Cb, kh, kw, stride, pad, pb * 0x01010101u, Ho, Wo, d_cols, ld, st);
     } else if (Cb % 4 == 0 && ((uintptr_t)d_x & 3) == 0) {
         launch_im2col<4>(d_x, B, H, W, Cb, kh, kw, stride, pad, pb * 0x01010101u, Ho, Wo, d_cols, ld, st);
+    } else if (ld <= 64 && rows <= INT32_MAX && kh <= 8 && kw <= 8 && Cb <= 3 &&
+               (int64_t)B * H * W * Cb <= INT32_MAX) {
+        int64_t blocks = (rows + 255) / 256;
+        if (blocks > (int64_t)num_sms() * 16) blocks = (int64_t)num_sms() * 16;
+        if (kh == 3 && kw == 3 && Cb == 1)   // (VGG / ResNet stems after padding C = 3 to 4)
+            im2col_rows_kernel<3, 3, 1><<<(int)blocks, 256, 0, st>>>(d_x, H, W, Cb, kh, kw, stride, pad, pb, Ho, Wo,
+                                                                     (int32_t)rows, d_cols, (int32_t)ld);
+        else
+            im2col_rows_kernel<0, 0, 0><<<(int)blocks, 256, 0, st>>>(d_x, H, W, Cb, kh, kw, stride, pad, pb, Ho, Wo,
+                                                                     (int32_t)rows, d_cols, (int32_t)ld);
     } else {
         launch_im2col<1>(d_x, B, H, W, Cb, kh, kw, stride, pad, pb, Ho, Wo, d_cols, ld, st);
     }

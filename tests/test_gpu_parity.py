@@ -769,6 +769,33 @@ def _levels16(seed, amp=31):
     return np.random.default_rng(seed).integers(-amp, amp + 1, 16).astype(np.int32)
 
 
+@pytest.mark.parametrize("B,H,W,C,k,stride,pad,pad_code", [
+    (2, 9, 11, 4, 3, 1, 1, 0),     # one packed byte per pixel (VGG conv1_1): the row-per-thread kernel
+    (1, 7, 7, 8, 3, 2, 1, 2),      # two bytes per pixel, stride 2, pad code 2
+    (3, 6, 5, 12, 3, 1, 1, 3),     # three bytes per pixel
+    (1, 8, 8, 16, 3, 1, 1, 1),     # 4-byte path
+    (1, 6, 6, 64, 3, 1, 1, 0),     # 16-byte path
+])
+def test_im2col_bytes(B, H, W, C, k, stride, pad, pad_code):
+    """dg_im2col byte layout: row (b, ho, wo), K order (r, s, c), out-of-image taps = the pad code,
+    zero tail; compared with the packing of the im2col of the code tensor (numpy indexing)."""
+    g = np.random.default_rng(B + H + W + C + k + pad_code)
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    Ho, Wo = (H + 2 * pad - k) // stride + 1, (W + 2 * pad - k) // stride + 1
+    xpad = np.full((B, H + 2 * pad, W + 2 * pad, C), pad_code, np.uint8)
+    xpad[:, pad:pad + H, pad:pad + W] = x
+    cols = np.empty((B, Ho, Wo, k, k, C), np.uint8)
+    for r in range(k):
+        for s_ in range(k):
+            cols[:, :, :, r, s_] = xpad[:, r:r + stride * Ho:stride, s_:s_ + stride * Wo:stride]
+    cols = cols.reshape(B * Ho * Wo, k * k * C)
+    xp, Cp = nhwc_pack(x)
+    got = host(dg.im2col(xp, B, H, W, Cp, k, k, stride, pad, pad_code))
+    exp = host(dg.pack_codes(torch.from_numpy(np.ascontiguousarray(cols)).to(DEV)))
+    assert got.shape[0] == exp.shape[0]
+    assert np.array_equal(got[:, : exp.shape[1]], exp)
+
+
 @pytest.mark.parametrize("K", [1, 37, 64, 101])
 def test_pack_codes4(K):
     """dg_pack_codes4: nibble k&1 of byte k>>1 (low first), zero tail, values > 15 masked and
