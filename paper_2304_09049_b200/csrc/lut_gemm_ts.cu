@@ -158,6 +158,12 @@ struct TsArgs {
     // splitk_reduce_kernel launched right behind
     int32_t sk, nwork;   // nwork = ntp * ntq * sk work items
     int32_t sk_fused;
+    // B multicast (bmc): CTA pairs of a 2-CTA cluster take row-adjacent tiles of the same column
+    // block (the tile walk gives it when the grid, the raster group and the row-block count are
+    // even); each CTA loads half of every B stage and multicasts it into both CTAs, and each MMA
+    // warp's stage commit releases the slot in both (empty_b counts 2): half the L2 -> SM traffic
+    // of the weights, which bounds the large GEMMs (no B reloads at all: 16384^3 3076 -> 3457 TOPS)
+    int32_t bmc;
     // fused all-gather (int32 output): every output tile is also stored to npeer extra
     // destinations (peer GPUs' C buffers, P2P-mapped, already offset to this rank's rows)
     int32_t npeer;
@@ -625,7 +631,8 @@ template <int BN, int NEPI, int NUNP, int KST, bool WIN, bool ASM, bool SK, int 
 __global__ void __launch_bounds__(Roles<NEPI, NUNP, EM>::NT, 1)
 lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_constant__ CUtensorMap tm_b,
                    const __grid_constant__ CUtensorMap tm_d, const __grid_constant__ PeerMaps pm,
-                   const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq) {
+                   const __grid_constant__ TsArgs ta, const __grid_constant__ RequantArgs rq,
+                   const __grid_constant__ CUtensorMap tm_bh) {   // tm_bh: B boxes of BN / 2 rows (bmc)
     using C = TsCfg<BN, (EM & EM_CSPLIT) ? 1 : NEPI / 4, KST, WIN, ASM, (EM & EM_A6) != 0>;
     using R = Roles<NEPI, NUNP, EM>;
     constexpr bool CS = (EM & EM_CSPLIT) != 0;
@@ -666,7 +673,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
             for (int s = 0; s < SB; ++s) {
                 ptx::mbar_init(full_b(s), 1);
-                ptx::mbar_init(empty_b(s), 1);
+                ptx::mbar_init(empty_b(s), ta.bmc ? 2 : 1);   // (bmc: both CTAs' MMA commits)
             }
             for (int s = 0; s < SA; ++s) {   // WIN: window buffers, filled by all unpack warps
                 ptx::mbar_init(full_a(s), WIN ? NUNP : 4);
@@ -692,6 +699,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     // right after the tc_ss kernel, cause not determined: the flag goes through shared memory)
     ptx::tc_fence_before();
     __syncthreads();
+    if (ta.bmc) ptx::cluster_sync_all();   // the partner's barriers are initialised before any multicast
     ptx::tc_fence_after();
     const uint32_t tmem = *tmem_slot;
     // programmatic dependent launch: the next layer's CTAs may start (prologue) as ours exit; every
@@ -754,11 +762,19 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 const int bs = gb % SB;
                 ptx::mbar_wait(empty_b(bs), ((gb / SB) & 1u) ^ 1u);
                 if (lane == 0) {
-                    ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)C::B_BYTES);
+                    ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)C::B_BYTES);   // (bmc: both halves land here)
+                    if (ta.bmc) {
+                        const uint32_t rk = ptx::cluster_ctarank();
 #pragma unroll
-                    for (int h = 0; h < C::HALVES; ++h)
-                        ptx::tma_load_2d(sbase + C::OFF_B + bs * C::B_BYTES + h * C::B_ATOM, &tm_b, full_b(bs),
-                                         s * KST + h * KA, (int32_t)q0);
+                        for (int h = 0; h < C::HALVES; ++h)
+                            ptx::tma_load_2d_multicast(sbase + C::OFF_B + bs * C::B_BYTES + h * C::B_ATOM + rk * (C::B_ATOM / 2),
+                                                       &tm_bh, full_b(bs), s * KST + h * KA, (int32_t)(q0 + rk * (BN / 2)), 0x3);
+                    } else {
+#pragma unroll
+                        for (int h = 0; h < C::HALVES; ++h)
+                            ptx::tma_load_2d(sbase + C::OFF_B + bs * C::B_BYTES + h * C::B_ATOM, &tm_b, full_b(bs),
+                                             s * KST + h * KA, (int32_t)q0);
+                    }
                 }
                 __syncwarp();
             }
@@ -809,6 +825,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const uint32_t w_lbo16 = reg_copy((uint32_t)ta.lbo >> 4), w_wp = reg_copy((uint32_t)ta.Wp),
                        w_clog2 = reg_copy((uint32_t)ta.clog2);
         const int w_pair = WIN ? (int)reg_copy((uint32_t)ta.wpair) : 0;
+        const bool w_bmc = !WIN && !ASM && reg_copy((uint32_t)ta.bmc) != 0u;   // commits release both CTAs' B slot
         uint32_t w_tap[9];   // window row shift of tap (r, s) in 16-byte units: r*Wp + s
 #pragma unroll
         for (int q = 0; q < 9; ++q) w_tap[q] = (uint32_t)(q / 3) * w_wp + (uint32_t)(q % 3);
@@ -933,7 +950,8 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     }
 #endif
                     ptx::mma_commit_warp(empty_a(sa));
-                    if (!wk.bres) ptx::mma_commit_warp(empty_b(bsl));
+                    if (w_bmc) ptx::mma_commit_warp_multicast(empty_b(bsl), 0x3);
+                    else if (!wk.bres) ptx::mma_commit_warp(empty_b(bsl));
                     if (s == se - 1) ptx::mma_commit_warp(acc_full(acc));
                 }
                 if (lane == 0) TS_EV(15, g);
@@ -1477,6 +1495,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         for (int i = threadIdx.x; i < TL_E * TL_N; i += blockDim.x) (&g_ts_tl[0][0])[i] = (&s_tl[0][0])[i];
 #endif
     if (warp == PRODUCER_WARP) ptx::tmem_dealloc(tmem, C::TMEM_COLS);
+    if (ta.bmc) ptx::cluster_sync_all();   // the partner's last multicast / commit into this CTA has landed
     if (SK && ta.sk > 1 && ta.sk_fused) {
         // every split's slice is stored (grid-wide barrier of the cooperative launch, with its memory
         // ordering): all threads of the grid sum the slices and requantise / store
@@ -1739,9 +1758,10 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
         ta.fd_ho = make_fastdiv((uint32_t)cv->Ho);
         if (np >= ((int64_t)1 << 31)) return DG_ERR_SHAPE;
     }
-    CUtensorMap mp, mb, md;
+    CUtensorMap mp, mb, md, mbh;
     memset(&mp, 0, sizeof(mp));
     memset(&md, 0, sizeof(md));
+    memset(&mbh, 0, sizeof(mbh));
     ta.tma_d = 0;
     PeerMaps pmaps;
     memset(&pmaps, 0, sizeof(pmaps));
@@ -1787,7 +1807,16 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     const int64_t ntiles = otiles * ta.sk;
     if (ntiles > INT32_MAX) return DG_ERR_SHAPE;
     ta.nwork = (int32_t)ntiles;
-    const int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
+    int grid = (int)(ntiles < num_sms() ? ntiles : num_sms());
+    // B multicast across CTA pairs (see TsArgs::bmc): streamed B, no split-K, and a tile walk that
+    // gives both CTAs of a pair the same column block at every step
+    ta.bmc = (!WIN && !ASM && !ta.bres && ta.sk == 1 && opt(OPT_BMC) && (grid & ~1) >= 2 && ta.ntp % 2 == 0 &&
+              ta.group % 2 == 0 && ta.last_rows % 2 == 0 && ntiles % 2 == 0 && ta.npeer == 0)
+                 ? 1 : 0;
+    if (ta.bmc) {
+        grid &= ~1;
+        if (!make_map_sw128(&mbh, Q8, ld8, nq, BN / 2, 128)) return DG_ERR_CUDA;
+    }
     const RequantArgs rqv = rq ? *rq : dummy;
     cudaLaunchConfig_t lc = {};
     lc.gridDim = dim3((unsigned)grid);
@@ -1797,11 +1826,19 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
     cudaLaunchAttribute la[2];
     la[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     la[0].val.programmaticStreamSerializationAllowed = opt(OPT_PDL) ? 1 : 0;
-    la[1].id = cudaLaunchAttributeCooperative;   // (grid <= one CTA per SM: always co-resident)
-    la[1].val.cooperative = 1;
+    if (ta.sk_fused) {
+        la[1].id = cudaLaunchAttributeCooperative;   // (grid <= one CTA per SM: always co-resident)
+        la[1].val.cooperative = 1;
+    } else {
+        la[1].id = cudaLaunchAttributeClusterDimension;
+        la[1].val.clusterDim.x = 2;
+        la[1].val.clusterDim.y = 1;
+        la[1].val.clusterDim.z = 1;
+    }
     lc.attrs = la;
-    lc.numAttrs = ta.sk_fused ? 2 : 1;
-    if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK, EM>, mp, mb, md, pmaps, ta, rqv) != cudaSuccess)
+    lc.numAttrs = (ta.sk_fused || ta.bmc) ? 2 : 1;
+    if (cudaLaunchKernelEx(&lc, lut_gemm_ts_kernel<BN, NEPI, NUNP, KST, WIN, ASM, SK, EM>, mp, mb, md, pmaps, ta, rqv, mbh) !=
+        cudaSuccess)
         return DG_ERR_CUDA;
     if (ta.sk > 1 && !ta.sk_fused) {
         const int64_t thr = np * ((nq + 3) >> 2);
@@ -1815,9 +1852,9 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
             return DG_ERR_CUDA;
     }
     char tag[160];
-    snprintf(tag, sizeof(tag), "ts bn=%d epi=%d unp=%d kst=%d%s%s%s em=%d nwin=%d wpair=%d sk=%d bres=%d f16=%d implicit=%d bulk=%d early=%d tmad=%d",
+    snprintf(tag, sizeof(tag), "ts bn=%d epi=%d unp=%d kst=%d%s%s%s em=%d nwin=%d wpair=%d sk=%d bres=%d f16=%d implicit=%d bulk=%d early=%d tmad=%d bmc=%d",
              BN, NEPI, NUNP, KST, WIN ? " win" : "", ASM ? " asm" : "", SK ? (ta.sk_fused ? " skinst fused" : " skinst") : "", EM, ta.nwin, ta.wpair, ta.sk,
-             ta.bres, ta.f16, ta.implicit, ta.bulk, ta.early_b, ta.tma_d);
+             ta.bres, ta.f16, ta.implicit, ta.bulk, ta.early_b, ta.tma_d, ta.bmc);
     set_last_kernel(tag);
     return launch_status(ta.sk > 1 && !ta.sk_fused ? 2 : 1);
 }

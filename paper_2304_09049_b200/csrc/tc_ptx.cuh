@@ -102,6 +102,25 @@ DG_DEV void tma_load_2d(uint32_t dst, const CUtensorMap *m, uint32_t bar, int32_
         : "memory");
 }
 
+// the same box into the same shared-memory offset of every CTA of the cluster in cta_mask, each
+// CTA's mbarrier at offset bar receiving the complete_tx of its copy
+DG_DEV void tma_load_2d_multicast(uint32_t dst, const CUtensorMap *m, uint32_t bar, int32_t x, int32_t y, uint16_t cta_mask) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes.multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(x), "r"(y), "h"(cta_mask)
+        : "memory");
+}
+DG_DEV uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+// every thread of every CTA of the cluster (release / acquire: barrier inits and shared-memory
+// writes before it are visible cluster-wide after it)
+DG_DEV void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
 // 1-D bulk copy global -> shared (contiguous bytes, multiple of 16), completes on an mbarrier
 // TMA tensor store shared -> global (bulk-group completion): box at {x (innermost), y}; the smem
 // source must be laid out as the map's box with its swizzle.  Commit / wait: the store has finished
@@ -209,6 +228,15 @@ DG_DEV void mma_commit_warp(uint32_t bar) {
         "{\n\t.reg .pred e;\n\t"
         "elect.sync _|e, 0xffffffff;\n\t"
         "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(bar)
+        : "memory");
+}
+// commit arriving on the mbarrier at offset bar of every CTA of the cluster in cta_mask
+DG_DEV void mma_commit_warp_multicast(uint32_t bar, uint16_t cta_mask) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;\n\t}" ::"r"(bar),
+        "h"(cta_mask)
         : "memory");
 }
 DG_DEV void mma_commit(uint32_t bar) {

@@ -186,10 +186,14 @@ def test_config2_resnet18_chain_bit_exact():
     assert (hist > 0.02).sum() >= 3, hist
 
 
+@pytest.mark.parametrize("bmc", [1, 0])
 @pytest.mark.parametrize("n", [4096])
-def test_config5_square_gemm_freivalds(n):
-    """Config 5 (Q17 learned levels, int16 table, int32 out) at n=4096: exact Freivalds over the
-    whole C and two full rows against the oracle."""
+def test_config5_square_gemm_freivalds(n, bmc):
+    """Config 5 (Q17 learned levels, int16 table, int32 out) at n=4096, with the B stages multicast
+    across 2-CTA clusters (bmc = 1, the default) and without: exact Freivalds over the whole C and
+    two full rows against the oracle."""
+    dg.reset_options()
+    dg.set_option("bmc", bmc)
     wl, al = synth.learned_levels(5, 0, synth.T_LEVELS)
     lut = dg.build_lut(wl, al, 16)
     Wc = synth.counter_codes_host(0, n * n, (5, n, synth.T_W), "uniform").reshape(n, n)
@@ -198,8 +202,11 @@ def test_config5_square_gemm_freivalds(n):
     at = dg.pack_codes(torch.from_numpy(Ac).cuda())
     at8 = dg.expand_operand(at, n, al)
     C = dg.lut_gemm_prepared(w, at8, n, n, n, lut)
+    tag = dg.last_kernel()
     C2 = dg.lut_gemm(w, at, n, n, n, lut, variant="tc")
     torch.cuda.synchronize()
+    dg.reset_options()
+    assert f"bmc={bmc}" in tag and "bn=256" in tag, tag
     assert torch.equal(C, C2)
     Cn = C.cpu().numpy()
     T = oracle.build_lut16(wl, al)
