@@ -109,7 +109,7 @@ DG_API uint64_t dg_kernel_launches(void);
  *   "f4_omma"   FP4 conv accumulators start from an origin MMA (one per tile) instead of
  *               tensor-memory reset stores                                   (1)
  *   "bmc"       streamed-B GEMM/conv tiles: B stages multicast across 2-CTA clusters when the
- *               tile walk pairs row-adjacent tiles of one column block       (1)
+ *               tile walk pairs row-adjacent tiles of one column block       (0)
  *   "skfuse"    split-K: the GEMM kernel sums its slices itself after a grid-wide barrier
  *               (cooperative launch) instead of a second reduce kernel       (0)
  *   "f4_ct"     FP4 conv: 2 = two CTAs per SM for the 128-wide tiles        (0)

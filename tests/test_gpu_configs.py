@@ -190,7 +190,7 @@ def test_config2_resnet18_chain_bit_exact():
 @pytest.mark.parametrize("n", [4096])
 def test_config5_square_gemm_freivalds(n, bmc):
     """Config 5 (Q17 learned levels, int16 table, int32 out) at n=4096, with the B stages multicast
-    across 2-CTA clusters (bmc = 1, the default) and without: exact Freivalds over the whole C and
+    across 2-CTA clusters (bmc = 1) and without (the default): exact Freivalds over the whole C and
     two full rows against the oracle."""
     dg.reset_options()
     dg.set_option("bmc", bmc)

@@ -922,10 +922,10 @@ INSTANCES = [  # np (pixels), nq (channels), K, options, tags the instance must 
     (300, 128, 1152, {"bres": 0}, ["bres=0"]),
     (300, 128, 576, {"pdl": 0, "early_weights": 1}, ["early=1"]),
     # B multicast across 2-CTA clusters (even row-block count and raster group, streamed B)
-    (512, 1280, 1024, {}, ["epi=4 unp=8", "bmc=1"]),
-    (1000, 2048, 2048, {}, ["epi=4 unp=8", "bmc=1"]),                 # ragged last row block
-    (512, 1280, 1024, {"bmc": 0}, ["epi=4 unp=8", "bmc=0"]),
-    (300, 1280, 1024, {}, ["bmc=0"]),                                   # odd row-block count
+    (512, 1280, 1024, {"bmc": 1}, ["epi=4 unp=8", "bmc=1"]),
+    (1000, 2048, 2048, {"bmc": 1}, ["epi=4 unp=8", "bmc=1"]),         # ragged last row block
+    (512, 1280, 1024, {}, ["epi=4 unp=8", "bmc=0"]),
+    (300, 1280, 1024, {"bmc": 1}, ["bmc=0"]),                           # odd row-block count
 ]
 
 
