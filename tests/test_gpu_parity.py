@@ -214,6 +214,32 @@ def test_gemm_errors():
         dg.lut_gemm(w, w, 4, 4, 8, big)
 
 
+@pytest.mark.parametrize("variant", ["cc", "tc", "auto"])
+@pytest.mark.parametrize("M,N,K", [(1, 1, 1), (1, 300, 577), (300, 1, 577), (130, 70, 1), (5, 3, 3)])
+def test_gemm_degenerate_shapes(variant, M, N, K):
+    """Degenerate GEMMs (a single output row / column, K = 1, K not a multiple of 4) on every
+    variant: bit-exact against the oracle; all-zero activation codes (level 0) give C = 0 exactly
+    (the invariant of the oracle pins), including with the fused requant."""
+    lut = dg.build_lut(WL, AL, 8)
+    T = oracle.build_lut16(WL, AL)
+    g = np.random.default_rng(M * 31 + N * 7 + K)
+    W = g.integers(0, 4, (M, K), dtype=np.uint8)
+    A = g.integers(0, 4, (K, N), dtype=np.uint8)
+    w, at = gpu_pack(W, weights=True), gpu_pack(np.ascontiguousarray(A.T))
+    try:
+        C = host(dg.lut_gemm(w, at, M, N, K, lut, variant=variant))
+    except dg.DGError as e:
+        assert variant == "tc" and "UNSUPPORTED" in str(e), e
+        return
+    assert np.array_equal(C, oracle.lut_gemm(W, A, T))
+    z = gpu_pack(np.zeros((N, K), np.uint8))
+    assert not host(dg.lut_gemm(w, z, M, N, K, lut, variant=variant)).any()
+    rq = dg.Requant(30000, 20, 1, 0, 3)
+    codes = dg.lut_gemm(w, z, M, N, K, lut, variant=variant, rq=rq)
+    exp = oracle.requantize(np.zeros((M, N), np.int32), 30000, 20, 1, 0, 3)
+    assert np.array_equal(oracle_codes_of(codes, M, N), exp)
+
+
 # ---------------------------------------------------------------- conv
 def nhwc_pack(x):
     B, H, W, C = x.shape
