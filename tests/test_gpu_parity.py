@@ -214,6 +214,33 @@ def test_gemm_errors():
         dg.lut_gemm(w, w, 4, 4, 8, big)
 
 
+@pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", [
+    (1, 1, 1, 64, 64, 3, 1, 1, 2),    # a 1x1 image: every tap but the centre is padding
+    (3, 2, 5, 64, 128, 3, 2, 1, 1),   # stride 2 on a 2-row image
+    (2, 3, 3, 256, 256, 3, 1, 0, 0),  # no padding: one output pixel per image
+    (1, 1, 7, 128, 64, 1, 1, 0, 0),   # a single image row, 1x1
+])
+def test_conv_degenerate_images(B, H, W, C, Cout, k, stride, pad, pad_code):
+    """Tiny / degenerate images through the int8 prepared conv and the FP4 conv, bit-exact."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    wl = [-2, -1, 0, 1]
+    T = oracle.build_lut16(wl, AL)
+    lut = dg.build_lut(wl, AL, 8)
+    g = np.random.default_rng(B + H + W + C + Cout + k + pad_code)
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, k, k, C), dtype=np.uint8)
+    exp = oracle.conv2d_direct(x, w, T, stride, pad, pad_code).reshape(-1, Cout)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    p = dg.conv_params(B, H, W, Cp, Cout, k, k, stride, pad, pad_code, ldw=wp.shape[1])
+    ws = torch.empty(dg.conv_workspace_size(p), dtype=torch.uint8, device=DEV)
+    w8 = dg.expand_operand(wp, k * k * Cp, wl)
+    assert np.array_equal(host(dg.lut_conv2d_prepared(xp, w8, lut, p, ws=ws)).reshape(exp.shape), exp)
+    w4 = dg.expand_operand_f4(wp, k * k * Cp, wl)
+    assert np.array_equal(host(dg.lut_conv2d_f4_prepared(xp, w4, lut, p)), exp)
+
+
 @pytest.mark.parametrize("variant", ["cc", "tc", "auto"])
 @pytest.mark.parametrize("M,N,K", [(1, 1, 1), (1, 300, 577), (300, 1, 577), (130, 70, 1), (5, 3, 3)])
 def test_gemm_degenerate_shapes(variant, M, N, K):
