@@ -108,6 +108,8 @@ DG_API uint64_t dg_kernel_launches(void);
  *   "f4_bn"     FP4 conv tile width: 0 auto (256 when it divides Cout), 128, 256 (0)
  *   "f4_omma"   FP4 conv accumulators start from an origin MMA (one per tile) instead of
  *               tensor-memory reset stores                                   (1)
+ *   "offs"      short-K shared-memory-A tiles start their accumulators at the columns' 16-bit
+ *               requant offsets through one extra MMA (no offset loads in the epilogue)  (1)
  *   "bmc"       streamed-B GEMM/conv tiles: B stages multicast across 2-CTA clusters when the
  *               tile walk pairs row-adjacent tiles of one column block       (0)
  *   "skfuse"    split-K: the GEMM kernel sums its slices itself after a grid-wide barrier

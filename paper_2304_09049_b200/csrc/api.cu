@@ -31,7 +31,7 @@ const OptDesc kOpts[dg::OPT_COUNT] = {
     {"f4_unp", "DG_F4_UNP", 0, -1},     {"f4_epi", "DG_F4_EPI", 0, -1},
     {"f4_bn", "DG_F4_BN", 0, -1},       {"f4_omma", "DG_F4_OMMA", 1, -1},
     {"f4_ct", "DG_F4_CT", 0, -1},       {"skfuse", "DG_SKFUSE", 0, 1},   {"f4_win", "DG_F4_WIN", 0, -1},
-    {"bmc", "DG_BMC", 0, 1},
+    {"offs", "DG_NO_OFFS", 1, 0},       {"bmc", "DG_BMC", 0, 1},
 };
 
 int64_t *opt_table() {

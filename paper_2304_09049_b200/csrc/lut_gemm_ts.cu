@@ -107,12 +107,17 @@ struct TsCfg {
     static constexpr int NBAR = 2 * SP_MAX + 2 * SB + 2 * SA + 2 * NACC;
     static constexpr int OFF_TMEM = OFF_BAR + NBAR * 8;
     static constexpr int OFF_WALK = OFF_TMEM + 16;           // 32 words: the MMA warp's copy of the tile walk
-    static constexpr int OFF_TAB = (OFF_WALK + 128 + 15) / 16 * 16;   // 16-bit requant offsets, one u32 per column pair
+    static constexpr int OFF_OBAR = OFF_WALK + 128;          // offs: the offset block is ready (mbarrier)
+    static constexpr int OFF_TAB = (OFF_OBAR + 16 + 15) / 16 * 16;   // 16-bit requant offsets, one u32 per column pair
     // int32-output staging for the TMA tensor store (4 epilogue warps x one 32 x 32 int32 chunk,
     // 128-byte swizzle, 1024-aligned) in the instances with one epilogue group and room for it
     static constexpr int STG_BYTES = (EG == 1 && !WIN && !ASM) ? 4 * 4096 : 0;
     static constexpr int OFF_STG = (OFF_TAB + TAB_PAIRS * 4 + 1023) / 1024 * 1024;
-    static constexpr int ALLOC = OFF_STG + STG_BYTES + 1024;
+    // offs operands (no-swizzle K-major, 2 K chunks of 16 bytes): B rows per column tile (2 tiles),
+    // then the constant A rows
+    static constexpr int OFFS_BYTES = ASM ? 2 * BN * 32 + BM * 32 : 0;
+    static constexpr int OFF_OFFS = (OFF_STG + STG_BYTES + 1023) / 1024 * 1024;
+    static constexpr int ALLOC = OFF_OFFS + OFFS_BYTES + 1024;
     static_assert(((ASM || WIN) ? NACC * BN : TMEM_A0 + SA * ACOLS) <= TMEM_COLS && SA >= 2, "TMEM budget");
     static_assert(ALLOC <= 232448, "shared memory budget");
 };
@@ -164,6 +169,11 @@ struct TsArgs {
     // warp's stage commit releases the slot in both (empty_b counts 2): half the L2 -> SM traffic
     // of the weights, which bounds the large GEMMs (no B reloads at all: 16384^3 3076 -> 3457 TOPS)
     int32_t bmc;
+    // offs (short-K shared-memory-A instance, per-column requant offsets, <= 2 column tiles): each
+    // tile's accumulator starts at its columns' 16-bit requant offsets n = bias - (t0 - 1) through
+    // one extra K = 32 MMA (A rows [127, 1, 0...], B rows [q, r, 0...], n = 127 q + r), so the
+    // epilogue's clamp takes no per-column offset loads (they were ~10 % of these layers)
+    int32_t offs;
     // fused all-gather (int32 output): every output tile is also stored to npeer extra
     // destinations (peer GPUs' C buffers, P2P-mapped, already offset to this rank's rows)
     int32_t npeer;
@@ -683,6 +693,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 ptx::mbar_init(acc_full(a), 1);
                 ptx::mbar_init(acc_empty(a), CS ? NEPI : 4);   // the 4 warps of the owning group (CS: all)
             }
+            if (ASM && ta.offs) ptx::mbar_init(sbase + C::OFF_OBAR, NEPI);   // every epilogue warp's offsets written
             ptx::fence_mbar_init();
         }
         __syncwarp();
@@ -690,8 +701,10 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     }
     uint32_t *f16tab = reinterpret_cast<uint32_t *>(smem + C::OFF_TAB);
     volatile uint32_t *f16_flag = reinterpret_cast<volatile uint32_t *>(smem + C::OFF_TMEM + 8);
+    volatile uint32_t *offs_bad = reinterpret_cast<volatile uint32_t *>(smem + C::OFF_OBAR + 8);
     if (threadIdx.x == 0) {
         *f16_flag = 0u;
+        *offs_bad = 0u;
         *reinterpret_cast<volatile uint32_t *>(smem + C::OFF_TMEM + 12) = 0u;   // the MMA warp's opaque zero
         put_walk(ta, reinterpret_cast<volatile uint32_t *>(smem + C::OFF_WALK));
     }
@@ -825,6 +838,13 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const uint32_t w_lbo16 = reg_copy((uint32_t)ta.lbo >> 4), w_wp = reg_copy((uint32_t)ta.Wp),
                        w_clog2 = reg_copy((uint32_t)ta.clog2);
         const int w_pair = WIN ? (int)reg_copy((uint32_t)ta.wpair) : 0;
+        // offs: wait once for the epilogue warps' offset rows; the same flags decide their epilogue form
+        bool w_offs = false;
+        if (ASM && reg_copy((uint32_t)ta.offs) != 0u) {
+            ptx::mbar_wait(sbase + C::OFF_OBAR, 0u);
+            w_offs = *f16_flag == 0u && *offs_bad == 0u;
+        }
+        const uint64_t one_desc = ptx::desc_k_none(sbase + C::OFF_OFFS + 2 * BN * 32, BM * 16);
         const bool w_bmc = !WIN && !ASM && reg_copy((uint32_t)ta.bmc) != 0u;   // commits release both CTAs' B slot
         uint32_t w_tap[9];   // window row shift of tap (r, s) in 16-byte units: r*Wp + s
 #pragma unroll
@@ -918,18 +938,22 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     }
                 } else if (ASM) {
                     const uint64_t ad = ptx::desc_k_none(sbase + C::OFF_A + (uint32_t)(sa * C::A_STAGE), BM * 16);
+                    // offs: the tile's first MMA writes the columns' requant offsets into the accumulator
+                    if (w_offs && s == sb)
+                        ptx::mma_i8_ss_warp(dt, one_desc, ptx::desc_k_none(sbase + C::OFF_OFFS + (uint32_t)(tq * BN * 32), BN * 16),
+                                            idesc, 0u);
                     // k-step k: A K-chunks 2k, 2k+1 (+2k * BM*16 bytes), B atom k/4, +32 B per k-step inside
                     if (nk == C::KSTEPS) {
 #pragma unroll
                         for (int k = 0; k < C::KSTEPS; ++k)
                             ptx::mma_i8_ss_warp(dt, ad + (uint64_t)((2 * k * BM * 16) >> 4),
                                                 bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3), idesc,
-                                                (s > sb || k > 0) ? 1u : 0u);
+                                                (w_offs || s > sb || k > 0) ? 1u : 0u);
                     } else {
                         for (int k = 0; k < nk; ++k)
                             ptx::mma_i8_ss_warp(dt, ad + (uint64_t)((2 * k * BM * 16) >> 4),
                                                 bd + (uint64_t)(((k >> 2) * C::B_ATOM) >> 4) + 2 * (k & 3), idesc,
-                                                (s > sb || k > 0) ? 1u : 0u);
+                                                (w_offs || s > sb || k > 0) ? 1u : 0u);
                     }
                     ptx::mma_commit_warp(empty_a(sa));
                     if (!wk.bres) ptx::mma_commit_warp(empty_b(bsl));
@@ -1334,11 +1358,32 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 const int64_t n1 = (rq.bias ? (int64_t)__ldg(rq.bias + 2 * i + 1) : 0) - ta.f16_thr0m1;
                 if ((n0 < 0 ? -n0 : n0) + ta.f16_accmax > 32767 || (n1 < 0 ? -n1 : n1) + ta.f16_accmax > 32767) bad = 1;
                 f16tab[i] = ((uint32_t)n0 & 0xFFFFu) | ((uint32_t)n1 << 16);
+                if (ASM && ta.offs) {   // offset MMA operand rows 2i, 2i+1: n = 127 q + r, |r| <= 63
+                    const int32_t qa = (int32_t)((n0 + (n0 >= 0 ? 63 : -63)) / 127), qb = (int32_t)((n1 + (n1 >= 0 ? 63 : -63)) / 127);
+                    const int32_t ra = (int32_t)n0 - 127 * qa, rb = (int32_t)n1 - 127 * qb;
+                    if (qa < -127 || qa > 127 || qb < -127 || qb > 127) *offs_bad = 1u;
+                    const int c = 2 * i % BN, tb = 2 * i / BN;
+                    uint8_t *blk = smem + C::OFF_OFFS + tb * BN * 32;
+                    *reinterpret_cast<uint4 *>(blk + c * 16) = make_uint4((uint32_t)(qa & 0xFF) | ((uint32_t)(ra & 0xFF) << 8), 0, 0, 0);
+                    *reinterpret_cast<uint4 *>(blk + (c + 1) * 16) = make_uint4((uint32_t)(qb & 0xFF) | ((uint32_t)(rb & 0xFF) << 8), 0, 0, 0);
+                    *reinterpret_cast<uint4 *>(blk + BN * 16 + c * 16) = make_uint4(0, 0, 0, 0);
+                    *reinterpret_cast<uint4 *>(blk + BN * 16 + (c + 1) * 16) = make_uint4(0, 0, 0, 0);
+                }
             }
             if (bad) *f16_flag = 1u;
+            if (ASM && ta.offs) {   // the constant A rows [127, 1, 0, ...] (second K chunk zero)
+                uint8_t *one = smem + C::OFF_OFFS + 2 * BN * 32;
+                for (int m = threadIdx.x - EPI_WARP0 * 32; m < BM; m += NEPI * 32) {
+                    *reinterpret_cast<uint4 *>(one + m * 16) = make_uint4(0x17Fu, 0, 0, 0);
+                    *reinterpret_cast<uint4 *>(one + BM * 16 + m * 16) = make_uint4(0, 0, 0, 0);
+                }
+                ptx::fence_proxy_async_smem();   // generic-proxy writes -> visible to the tensor core
+            }
         }
         if (ta.f16 && (ta.f16_tab || ta.f16_res == 1)) ptx::named_bar_sync(EPI_BAR, NEPI * 32);
+        if (ASM && ta.offs && lane == 0) ptx::mbar_arrive(sbase + C::OFF_OBAR);
         const bool f16_ok = ta.f16 && *f16_flag == 0u;
+        const bool use_offs = ASM && ta.offs && f16_ok && *offs_bad == 0u;
         ptx::griddep_wait();
         if (!WIN && ((SK && ta.sk > 1) || ta.f16_res)) {
             epilogue_loop_rare<BN, NACC, EG, WIN, CS>(ta, rq, tmem, sbase + C::OFF_TAB, acc_full(0), ntiles, warp - EPI_WARP0,
@@ -1392,8 +1437,8 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 use16 = __all_sync(0xFFFFFFFFu, (n < 0 ? -n : n) + ta.f16_accmax <= 32767);
             }
             if (use16) {
-                if (ta.f16_tab) epi16_tile<HALF, 0, true>(ta, rq, trow, p, q0, na_row, sbase + C::OFF_TAB, lane, acc_empty(acc), tl);
-                else epi16_tile<HALF, 0, false>(ta, rq, trow, p, q0, na_row, sbase + C::OFF_TAB, lane, acc_empty(acc), tl);
+                if (ta.f16_tab && !use_offs) epi16_tile<HALF, 0, true>(ta, rq, trow, p, q0, na_row, sbase + C::OFF_TAB, lane, acc_empty(acc), tl);
+                else epi16_tile<HALF, 0, false>(ta, rq, trow, p, q0, use_offs ? 0u : na_row, sbase + C::OFF_TAB, lane, acc_empty(acc), tl);
             } else if (C::STG_BYTES > 0 && ta.tma_d && !ta.has_rq && q0 + HALF <= ta.nq) {
                 // int32 tile through the TMA tensor store: per 32-column chunk the warp's 32 rows x
                 // 128 bytes go to its staging buffer (128-byte swizzle: 16-byte unit u of row r at
@@ -1737,6 +1782,10 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
             ta.f16_tab = (!rq->bias || rq->bias_axis == 0) ? 1 : 0;   // else: per-row offsets
         }
     }
+    // per-column offsets in the accumulator (see TsArgs::offs): every tile takes the 16-bit path
+    ta.offs = (ASM && rq && ta.f16 && ta.f16_tab && ta.fast_rq && !ta.f16_res && nq % BN == 0 && nq / BN <= 2 &&
+               opt(OPT_OFFS))
+                  ? 1 : 0;
     if (cv) {
         ta.implicit = WIN ? 0 : 1;
         ta.X = cv->x;
@@ -1852,9 +1901,9 @@ dg_status launch_ts(const uint8_t *P, int64_t ldp, const int8_t *Q8, int64_t ld8
             return DG_ERR_CUDA;
     }
     char tag[160];
-    snprintf(tag, sizeof(tag), "ts bn=%d epi=%d unp=%d kst=%d%s%s%s em=%d nwin=%d wpair=%d sk=%d bres=%d f16=%d implicit=%d bulk=%d early=%d tmad=%d bmc=%d",
+    snprintf(tag, sizeof(tag), "ts bn=%d epi=%d unp=%d kst=%d%s%s%s em=%d nwin=%d wpair=%d sk=%d bres=%d f16=%d implicit=%d bulk=%d early=%d tmad=%d bmc=%d offs=%d",
              BN, NEPI, NUNP, KST, WIN ? " win" : "", ASM ? " asm" : "", SK ? (ta.sk_fused ? " skinst fused" : " skinst") : "", EM, ta.nwin, ta.wpair, ta.sk,
-             ta.bres, ta.f16, ta.implicit, ta.bulk, ta.early_b, ta.tma_d, ta.bmc);
+             ta.bres, ta.f16, ta.implicit, ta.bulk, ta.early_b, ta.tma_d, ta.bmc, ta.offs);
     set_last_kernel(tag);
     return launch_status(ta.sk > 1 && !ta.sk_fused ? 2 : 1);
 }

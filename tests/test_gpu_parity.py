@@ -961,8 +961,10 @@ INSTANCES = [  # np (pixels), nq (channels), K, options, tags the instance must 
     (300, 64, 256, {}, ["bn=64 epi=8 unp=8 kst=256"]),
     (300, 128, 128, {}, ["bn=128 epi=8 unp=4 kst=128"]),
     (300, 128, 256, {}, ["bn=128 epi=8 unp=4 kst=256"]),
-    (300, 256, 64, {}, ["bn=256 epi=8 unp=4 kst=128 asm"]),
-    (260, 512, 256, {}, ["bn=256 epi=8 unp=4 kst=128 asm"]),
+    (300, 256, 64, {}, ["bn=256 epi=8 unp=4 kst=128 asm", "offs=1"]),
+    (260, 512, 256, {}, ["bn=256 epi=8 unp=4 kst=128 asm", "offs=1"]),
+    (300, 256, 64, {"offs": 0}, ["bn=256 epi=8 unp=4 kst=128 asm", "offs=0"]),
+    (300, 768, 64, {}, ["asm", "offs=0"]),                               # 3 column tiles: table path
     (300, 256, 3200, {}, ["bn=256 epi=4 unp=8 kst=128", "sk=1"]),
     (300, 128, 1152, {}, ["bn=128 epi=4 unp=8 kst=256"]),
     (300, 64, 1152, {}, ["bn=64 epi=4 unp=8 kst=256"]),
@@ -980,6 +982,34 @@ INSTANCES = [  # np (pixels), nq (channels), K, options, tags the instance must 
     (512, 1280, 1024, {}, ["epi=4 unp=8", "bmc=0"]),
     (300, 1280, 1024, {"bmc": 1}, ["bmc=0"]),                           # odd row-block count
 ]
+
+
+@pytest.mark.parametrize("big", [False, True])
+def test_asm_offset_mma_and_fallback(big):
+    """Short-K shared-memory-A instance with the per-column requant offsets written into the
+    accumulator by one MMA per tile (n = 127 q + r): bit-exact against the oracle; with offsets
+    beyond that range (|n| > 16192, still within the 16-bit form) every CTA falls back to the
+    offset-table path, also bit-exact."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    np_, nq, K = 700, 512, 64
+    g = np.random.default_rng(5 + big)
+    A = g.integers(0, 4, (np_, K), dtype=np.uint8)
+    Wt = g.integers(0, 4, (nq, K), dtype=np.uint8)
+    acc = oracle.lut_gemm(Wt, np.ascontiguousarray(A.T), oracle.build_lut16(WL, AL)).T
+    a_p, w8 = gpu_pack(A), dg.expand_operand(gpu_pack(Wt, weights=True), K, WL)
+    lut_t = dg.build_lut(AL, WL, 8)
+    base = 20000 if big else -int(np.round(acc.mean()))
+    bias = (base + g.integers(-300, 300, nq)).astype(np.int32)
+    mult = 40000
+    rq = dg.Requant(mult, 20, 1, 0, 3, bias=torch.from_numpy(bias).to(DEV), bias_axis=0)
+    dg.reset_options()
+    codes = dg.lut_gemm_prepared(a_p, w8, np_, nq, K, lut_t, rq=rq)
+    assert "asm" in dg.last_kernel() and "offs=1" in dg.last_kernel(), dg.last_kernel()
+    exp = oracle.requantize(np.ascontiguousarray(acc), mult, 20, 1, 0, 3, bias=bias, bias_axis=0)
+    assert np.array_equal(oracle_codes_of(codes, np_, nq), exp)
+    if not big:
+        assert len(np.unique(exp)) == 4   # (every code occurs: a real test of the thresholds)
 
 
 @pytest.mark.parametrize("np_,nq,K,opts,tags", INSTANCES)
