@@ -742,41 +742,91 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             __syncwarp();
             if (ta.early_b) ptx::griddep_wait();
         }
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        // the loop's parameters in registers (warp shuffles: ptxas cannot rematerialise them from
+        // the parameter bank inside the loop)
+        const Walk wk = get_walk(reinterpret_cast<volatile uint32_t *>(smem + C::OFF_WALK));
+        const bool p_load = !WIN && ptx::opaque((uint32_t)ta.implicit) == 0u;
+        const bool p_bulk = ptx::opaque((uint32_t)ta.bulk) != 0u, p_bres = ptx::opaque((uint32_t)ta.bres) != 0u,
+                   p_bmc = ptx::opaque((uint32_t)ta.bmc) != 0u;
+        const int64_t p_np = (int64_t)ptx::opaque64((uint64_t)ta.np), p_ldp = (int64_t)ptx::opaque64((uint64_t)ta.ldp);
+        const uint8_t *p_src = reinterpret_cast<const uint8_t *>(ptx::opaque64(reinterpret_cast<uint64_t>(ta.P)));
+        const int p_pks = (int)ptx::opaque((uint32_t)ta.pks), p_nsub = (int)ptx::opaque((uint32_t)nsub),
+                  p_nsp = (int)ptx::opaque((uint32_t)nsp);
+        const uint32_t p_slot = ptx::opaque(pslot);
+        const int p_ntl = wk.ntiles, p_grid = wk.grid;
+        int t_first = blockIdx.x;
+        if (p_load && p_bres && wk.nstages == 1) {
+            // one-slot tiles with resident weights (the short-K 1x1 layers): the loop is a chain of
+            // dependent instructions (~900 cycles per tile measured, tools/trace_ts.py --prod), the
+            // pace of the whole pipeline.  Lane i < PB takes the round's i-th tile: its coordinates,
+            // slot wait and copy issue run side by side with the other lanes'
+            const int PB = p_nsp < 8 ? p_nsp : 8;
+            for (int t0 = blockIdx.x; t0 < p_ntl; t0 += PB * p_grid) {
+                const int t = t0 + lane * p_grid;
+                const int cnt = (p_ntl - t0 + p_grid - 1) / p_grid < PB ? (p_ntl - t0 + p_grid - 1) / p_grid : PB;
+                if (lane < cnt) {
+                    int tp, tq, sb, se;
+                    work_item<SK>(wk, t, tp, tq, sb, se);
+                    const int64_t p0 = (int64_t)tp * BM;
+                    const uint32_t li = pslot_i + (uint32_t)lane;
+                    const bool wrap = li >= (uint32_t)p_nsp;
+                    const int slot = (int)(wrap ? li - (uint32_t)p_nsp : li);
+                    ptx::mbar_wait(empty_p(slot), (pphase ^ (wrap ? 1u : 0u)) ^ 1u);
+                    const uint32_t dst = sbase + C::OFF_P + (uint32_t)slot * p_slot;
+                    if (p_bulk) {
+                        const int64_t rows = p_np - p0 < BM ? p_np - p0 : BM;
+                        const uint32_t bytes = (uint32_t)(rows * p_ldp);
+                        ptx::mbar_arrive_expect_tx(full_p(slot), bytes);
+                        ptx::bulk_load(dst, p_src + p0 * p_ldp, bytes, full_p(slot));
+                    } else {
+                        ptx::mbar_arrive_expect_tx(full_p(slot), p_slot);
+                        ptx::tma_load_2d(dst, &tm_p, full_p(slot), 0, (int32_t)p0);
+                    }
+                }
+                __syncwarp();
+                pslot_i += (uint32_t)cnt;
+                if (pslot_i >= (uint32_t)p_nsp) { pslot_i -= (uint32_t)p_nsp; pphase ^= 1u; }
+                gb += (uint32_t)cnt;
+            }
+            t_first = p_ntl;
+        }
+        for (int t = t_first; t < p_ntl; t += p_grid) {
             int tp, tq, sb, se;
-            work_item<SK>(ta, t, tp, tq, sb, se);
+            work_item<SK>(wk, t, tp, tq, sb, se);
+            if (lane == 0) TS_EV(23, gb);
             const int64_t p0 = (int64_t)tp * BM, q0 = (int64_t)tq * BN;
             int sub = 0, ps = 0;
             for (int s = sb; s < se; ++s, ++gb) {
-                if (sub == 0 && !ta.implicit && !WIN) {   // next packed P slot (up to 512 codes of every row)
+                if (sub == 0 && p_load) {   // next packed P slot (up to 512 codes of every row)
                     const int slot = (int)pslot_i;
                     if (lane == 0) TS_EV(13, gb);
                     ptx::mbar_wait(empty_p(slot), pphase ^ 1u);
                     if (lane == 0) {
                         TS_EV(14, gb);
-                        const uint32_t dst = sbase + C::OFF_P + slot * pslot;
-                        if (ta.bulk) {   // (a TMA box of narrow rows issues one request per row: slow)
-                            const int64_t rows = ta.np - p0 < BM ? ta.np - p0 : BM;
-                            const uint32_t bytes = (uint32_t)(rows * ta.ldp);
+                        const uint32_t dst = sbase + C::OFF_P + slot * p_slot;
+                        if (p_bulk) {   // (a TMA box of narrow rows issues one request per row: slow)
+                            const int64_t rows = p_np - p0 < BM ? p_np - p0 : BM;
+                            const uint32_t bytes = (uint32_t)(rows * p_ldp);
                             ptx::mbar_arrive_expect_tx(full_p(slot), bytes);
-                            ptx::bulk_load(dst, ta.P + p0 * ta.ldp, bytes, full_p(slot));
+                            ptx::bulk_load(dst, p_src + p0 * p_ldp, bytes, full_p(slot));
                         } else {
-                            ptx::mbar_arrive_expect_tx(full_p(slot), pslot);
-                            ptx::tma_load_2d(dst, &tm_p, full_p(slot), sb * (KST / 4) + ps * ta.pks, (int32_t)p0);
+                            ptx::mbar_arrive_expect_tx(full_p(slot), p_slot);
+                            ptx::tma_load_2d(dst, &tm_p, full_p(slot), sb * (KST / 4) + ps * p_pks, (int32_t)p0);
                         }
                         TS_EV(12, gb);
                     }
                     __syncwarp();
-                    if (++pslot_i == (uint32_t)nsp) { pslot_i = 0; pphase ^= 1u; }
+                    if (lane == 0) TS_EV(22, gb);
+                    if (++pslot_i == (uint32_t)p_nsp) { pslot_i = 0; pphase ^= 1u; }
                     ++ps;
                 }
-                if (++sub == nsub) sub = 0;
-                if (ta.bres) continue;
+                if (++sub == p_nsub) sub = 0;
+                if (p_bres) continue;
                 const int bs = gb % SB;
                 ptx::mbar_wait(empty_b(bs), ((gb / SB) & 1u) ^ 1u);
                 if (lane == 0) {
                     ptx::mbar_arrive_expect_tx(full_b(bs), (uint32_t)C::B_BYTES);   // (bmc: both halves land here)
-                    if (ta.bmc) {
+                    if (p_bmc) {
                         const uint32_t rk = ptx::cluster_ctarank();
 #pragma unroll
                         for (int h = 0; h < C::HALVES; ++h)

@@ -77,6 +77,14 @@ DG_DEV bool mbar_test_wait(uint32_t bar, uint32_t parity) {
         : "memory");
     return ok != 0;
 }
+// a value ptxas must keep in a register (the whole warp, converged): a shuffle result cannot be
+// rematerialised, unlike a kernel parameter, which ptxas otherwise reloads from the constant bank
+// inside loops of async-copy or MMA issues, where such loads wait behind the queued operations
+DG_DEV uint32_t opaque(uint32_t x) { return __shfl_sync(0xffffffffu, x, 0); }
+DG_DEV uint64_t opaque64(uint64_t x) {
+    return (uint64_t)opaque((uint32_t)x) | ((uint64_t)opaque((uint32_t)(x >> 32)) << 32);
+}
+
 DG_DEV void mbar_wait(uint32_t bar, uint32_t parity) {
 #ifdef DG_MBAR_SPIN
     while (!mbar_test_wait(bar, parity)) {   // non-suspending probe loop

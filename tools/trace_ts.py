@@ -52,6 +52,10 @@ names = {13: "P_loop", 12: "P_tma", 0: "unp0", 20: "P_ok", 21: "unp_alu", 1: "un
 print("stage " + " ".join(f"{v:>8s}" for v in names.values()))
 for g in list(range(0, int(os.environ.get('TRACE_STAGES', '40')))):
     print(f"{g:5d} " + " ".join(f"{a[e][g]:8d}" for e in names))
+if "--prod" in sys.argv:
+    print("stage  work_item  P_loop  wait_ok  issued  synced   (producer warp)")
+    for g in range(0, 40):
+        print(f"{g:5d} " + " ".join(f"{a[e][g]:8d}" for e in (23, 13, 14, 12, 22)))
 if len(sys.argv) > 2 and sys.argv[2] == "--short":
     print("tile  P_loop P_tma unp0 unp_done w_start w_fullA handoff epi0 epi_accfull epi_done")
     for t in range(0, 40):
