@@ -967,7 +967,9 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                         wad[k] = ad + (uint64_t)(chunk * w_lbo16 + rr * w_wp + (tap - 3u * rr));
                     }
                 }
+                if (lane == 0) TS_EV(13, g);
                 ptx::named_bar_sync(HANDOFF_BAR, 64);
+                if (lane == 0) TS_EV(7, g);
                 ptx::tc_fence_after();
                 if (lane == 0) TS_EV(14, g);
                 if (WIN) {

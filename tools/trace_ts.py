@@ -61,9 +61,9 @@ if len(sys.argv) > 2 and sys.argv[2] == "--short":
     for t in range(0, 40):
         print(f"{t:4d} " + " ".join(f"{a[e][t]:8d}" for e in (13, 12, 0, 2, 3, 4, 6, 8, 9, 10)))
 if len(sys.argv) > 2 and sys.argv[2] == "--win":
-    print("stage: waiter_fullA w_fullB handoff mma_start mma_end")
+    print("stage: waiter_fullA w_fullB handoff mma_prebar mma_bar mma_start mma_end")
     for g in range(0, 30):
-        print(f"{g:4d} " + " ".join(f"{a[e][g]:8d}" for e in (4, 5, 6, 14, 15)))
+        print(f"{g:4d} " + " ".join(f"{a[e][g]:8d}" for e in (4, 5, 6, 13, 7, 14, 15)))
     print("tile unp0 cpa_ok unpacked fetched emptyW fullW_arr waiter_fullW  w_start epi0 epi_accfull epi_done")
     for t in range(0, 40):
         print(f"{t:4d} " + " ".join(f"{a[e][t]:8d}" for e in (0, 12, 21, 1, 11, 2, 13, 3, 8, 9, 10)))
