@@ -341,7 +341,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     } else if (warp == CF_WAIT) {
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-            ptx::mbar_wait(acc_empty(tl % CF_NACC), ((tl / CF_NACC) & 1u) ^ 1u);
+            if (CF_NACC > 1) ptx::mbar_wait(acc_empty(tl % CF_NACC), ((tl / CF_NACC) & 1u) ^ 1u);
             if (lane == 0) CF_EV(1, tl);
             if (WINM) ptx::mbar_wait(full_a((int)(tl % (uint32_t)fa.nwin)), (tl / (uint32_t)fa.nwin) & 1u);   // the tile's window
             for (int s = 0; s < fa.nstages; ++s, ++g) {
@@ -372,6 +372,11 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             const uint32_t dt = tmem + acc * BN_;
             const uint32_t wb = WINM ? tl % w_nwin : 0u;
             const uint64_t aw = WINM ? ptx::desc_k_none(w_base + wb * w_bytes, w_lbo) : 0ull;
+            // a single accumulator (256-wide tiles) is waited for here, in parallel with the waiter's
+            // stage-0 operand waits (-0.3..0.7 us per layer); with several, the MMA warp must not
+            // block (an mbarrier probe here waits behind its queued MMAs: +2 us on the 64 / 128-wide
+            // K = 256 layers), the waiter takes it
+            if (CF_NACC == 1) ptx::mbar_wait(acc_empty(acc), (tl & 1u) ^ 1u);
             for (int s = 0; s < nst; ++s, ++g) {
                 const int sa = (int)(g % CF_SA), bs = (int)(g % SB_);
                 ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
