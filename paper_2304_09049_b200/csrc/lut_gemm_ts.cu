@@ -852,7 +852,7 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t u0 = WIN ? (tl << ta.wpair) : tl;   // accumulator use index (WIN pairs: 2 per item)
-            ptx::mbar_wait(acc_empty(u0 % NACC), ((u0 / NACC) & 1u) ^ 1u);
+            if (NACC > 1) ptx::mbar_wait(acc_empty(u0 % NACC), ((u0 / NACC) & 1u) ^ 1u);   // (NACC 1: the MMA warp)
             int tp, tq, sb, se;
             work_item<SK>(ta, t, tp, tq, sb, se);
             if (WIN) ptx::mbar_wait(full_a(tl % ta.nwin), (tl / ta.nwin) & 1u);   // the tile's window
@@ -941,6 +941,10 @@ lut_gemm_ts_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 __syncwarp();
                 continue;
             }
+            // a single accumulator (128 x 256 tiles) is waited for here, in parallel with the waiter's
+            // operand waits; with several, the MMA warp must not block (its mbarrier probes wait
+            // behind its queued MMAs), the waiter takes them
+            if (NACC == 1) ptx::mbar_wait(acc_empty(0), (tl & 1u) ^ 1u);
             for (int s = sb; s < se; ++s, ++g) {
                 const int sa = g % SA;
                 const int bsl = wk.bres ? tq * wk.nstages + s : (int)(g % SB);   // B smem stage
