@@ -542,8 +542,9 @@ def _win_check(B, H, W, C, Cout, pad_code, expect, exact_images=None):
     assert np.array_equal(oracle_codes_of(outc, expc.shape[0], Cout), expc)
 
 
-@pytest.mark.parametrize("win128", [0, 1])
-@pytest.mark.parametrize("B,H,W,C,Cout,pad_code", WIN_CONVS)
+@pytest.mark.parametrize("B,H,W,C,Cout,pad_code,win128",
+                         [c + (0,) for c in WIN_CONVS] +
+                         [c + (1,) for c in WIN_CONVS if c[3] == 128 and c[4] <= 128])
 def test_conv_window_path_vs_oracle(win128, B, H, W, C, Cout, pad_code):
     """Direct 3x3 conv through the shifted-window kernel, FORCED (dg_set_option win=1) on shapes
     below its two-wave auto threshold: one unpacked window of padded input pixels per tile, every
@@ -551,8 +552,6 @@ def test_conv_window_path_vs_oracle(win128, B, H, W, C, Cout, pad_code):
     C = 128 / Cout <= 128 runs the C = 128 tile mode (win128=1) or the 256-code stage form."""
     if not _tc_available():
         pytest.skip("tc unavailable")
-    if win128 and not (C == 128 and Cout <= 128):
-        pytest.skip("win128 applies to C = 128, Cout <= 128")
     expect = [" win "] + (["kst=128"] if win128 else ["kst=256"])
     with dg.options(win=1, win128=win128):
         _win_check(B, H, W, C, Cout, pad_code, expect)
@@ -1056,9 +1055,13 @@ F4_CONVS = [  # B, H, W, C, Cout, k, stride, pad, pad_code
 ]
 
 
+# (tile width, epilogue arrangement): 64-wide tiles run 8 epilogue warps only, two CTAs per SM
+# ("ct2") 128-wide tiles only
+F4_BN_EPI = [(64, 8), (128, 4), (128, 8), (128, "ct2"), (256, 4), (256, 8)]
+
+
 @pytest.mark.parametrize("omma", [0, 1])
-@pytest.mark.parametrize("epi", [4, 8, "ct2"])
-@pytest.mark.parametrize("bn", [64, 128, 256])
+@pytest.mark.parametrize("bn,epi", F4_BN_EPI)
 @pytest.mark.parametrize("wl", [(-2, -1, 0, 1), (-12, -3, 4, 8)])
 @pytest.mark.parametrize("B,H,W,C,Cout,k,stride,pad,pad_code", F4_CONVS)
 def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn, epi, omma):
@@ -1081,10 +1084,6 @@ def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn, e
     w4 = dg.expand_operand_f4(wp, k * k * Cp, wl)
     p = dg.conv_params(B, H, W, Cp, Cout, k, k, stride, pad, pad_code, ldw=wp.shape[1])
     dg.reset_options()
-    if epi == "ct2" and bn != 128:
-        pytest.skip("two CTAs per SM: 128-wide tiles only")
-    if bn == 64 and epi != 8:
-        pytest.skip("64-wide tiles: 8 epilogue warps only")
     ct = 2 if epi == "ct2" else 1
     epi = 4 if epi == "ct2" else epi
     with dg.options(f4_bn=bn, f4_epi=epi, f4_omma=omma, f4_ct=ct):
