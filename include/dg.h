@@ -116,7 +116,12 @@ DG_API uint64_t dg_kernel_launches(void);
  *               (cooperative launch) instead of a second reduce kernel       (0)
  *   "f4_ct"     FP4 conv: 2 = two CTAs per SM for the 128-wide tiles        (0)
  *   "f4_win"    FP4 conv: shifted-window mode for direct 3x3 / stride 1 / pad 1 convs over
- *               64 or 128 channels                                           (0)
+ *               64 or 128 channels: 2 where the weights stay resident (one column block whose
+ *               stages fit the B ring), 1 always, 0 never                    (2)
+ *   "f4_wbres"  FP4 conv shifted window: all weight stages resident in shared memory (loaded
+ *               once per CTA, one MMA hand-off per tile) when the layer is one column block (1)
+ *   "f4_wpair"  FP4 conv shifted window with resident 64-wide tiles: one window of 256 padded
+ *               pixels + halo feeds two 128-row blocks into two accumulators (1)
  */
 DG_API dg_status dg_set_option(const char *name, int64_t value);
 DG_API dg_status dg_get_option(const char *name, int64_t *value);

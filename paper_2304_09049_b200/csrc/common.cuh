@@ -208,9 +208,11 @@ enum OptId {
     OPT_F4_OMMA,        // FP4 conv kernel: accumulator origin from one MMA per tile (1) or reset stores (0)
     OPT_F4_CT,          // FP4 conv kernel: CTAs per SM for 128-wide tiles (2) or 1 (0 / 1)
     OPT_SKFUSE,         // split-K slices reduced by the GEMM kernel itself after a grid barrier (1) or a second kernel (0, default)
-    OPT_F4_WIN,         // FP4 conv kernel: shifted window for direct 3x3 s1 p1 convs over 64 / 128 channels (1), 0 off
+    OPT_F4_WIN,         // FP4 conv kernel: shifted window for direct 3x3 s1 p1 convs over 64 / 128 channels: 2 auto (resident weights), 1 always, 0 off
     OPT_OFFS,           // short-K shared-memory-A instance: per-column requant offsets from one MMA per tile (1), 0 off
     OPT_BMC,            // TS kernel: B stages multicast across 2-CTA clusters where the tile walk allows (1), 0 off (default)
+    OPT_F4_WBRES,       // FP4 conv shifted window: weights resident when one column block fits the B ring (1), 0 off
+    OPT_F4_WPAIR,       // FP4 conv shifted window, 64-wide resident tiles: one window per two 128-row blocks (1), 0 off
     OPT_COUNT
 };
 int64_t opt(OptId id);

@@ -137,9 +137,13 @@ struct CfArgs {
     // shifted window (GM = 2; direct 3x3 / stride 1 / pad 1, C = 64 or 128): tiles of 128 PADDED
     // pixels q in [0, nqv), nqv = B (H+2)(W+2); the window = the WR padded input pixels q0 - Wp - 1
     // .. in e2m1, K chunk j (32 codes, 16 bytes) of row i at j * lbo + 16 i (no swizzle), so tap
-    // (r, s) is the view starting r * Wp + s rows down; fetched packed into 2 ring slots of wslot
+    // (r, s) is the view starting r * Wp + s rows down; fetched packed into wring ring slots of wslot
     // bytes (cp.async), nwin windows of wbytes after them
     int32_t Wp, WR, lbo, wslot, wbytes, nwin;
+    int32_t wring;               // packed fetch ring slots (2 or 4): the fill's copies run wring tiles ahead
+    int32_t wbres;               // window mode, one column block: all weight stages resident (slot s = stage s)
+    int32_t wpair;               // window pair mode (64-wide tiles, resident weights): a work item = 256 padded
+                                 // pixels, one window feeds two 128-row blocks into two accumulators
     int64_t nqv;
     CfDiv fd_hpwp, fd_wp;
     // 16-bit SIMD requant (host-verified, f16_params): x = clamp(acc + negA, 0, W), code = (x m + c) >> 14
@@ -315,6 +319,14 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         // (weights are read before the programmatic-dependent-launch wait only under early_weights)
         if (!fa.early_b || DIRECT) ptx::griddep_wait();
         uint32_t gp = 0, gb = 0;
+        if (WINM && fa.wbres) {   // resident weights: every stage loaded once, into slot s (one column block)
+            if (lane == 0 && (int)blockIdx.x < ntiles)
+                for (int s = 0; s < fa.nstages; ++s) {
+                    ptx::mbar_arrive_expect_tx(full_b(s), (uint32_t)B_STAGE_);
+                    ptx::tma_load_2d(sbase + CF_OFF_B + s * B_STAGE_, &tm_b, full_b(s), s * (CF_KST / 2), 0);
+                }
+            __syncwarp();
+        } else
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
             const int tq = t % fa.ntq, tp = t / fa.ntq;
             for (int s = 0; s < fa.nstages; ++s, ++gb) {
@@ -341,9 +353,21 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     } else if (warp == CF_WAIT) {
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-            if (CF_NACC > 1) ptx::mbar_wait(acc_empty(tl % CF_NACC), ((tl / CF_NACC) & 1u) ^ 1u);
+            if (BNT == 64 && WINM && fa.wpair) {   // both accumulators of the pair
+                ptx::mbar_wait(acc_empty((2 * tl) % CF_NACC), (((2 * tl) / CF_NACC) & 1u) ^ 1u);
+                ptx::mbar_wait(acc_empty((2 * tl + 1) % CF_NACC), (((2 * tl + 1) / CF_NACC) & 1u) ^ 1u);
+            } else if (CF_NACC > 1) {
+                ptx::mbar_wait(acc_empty(tl % CF_NACC), ((tl / CF_NACC) & 1u) ^ 1u);
+            }
             if (lane == 0) CF_EV(1, tl);
             if (WINM) ptx::mbar_wait(full_a((int)(tl % (uint32_t)fa.nwin)), (tl / (uint32_t)fa.nwin) & 1u);   // the tile's window
+            if (WINM && fa.wbres) {   // resident weights: waited for once; one hand-off per tile
+                if (lane == 0) CF_EV(2, tl);
+                if (tl == 0)
+                    for (int s = 0; s < fa.nstages; ++s) ptx::mbar_wait(full_b(s), 0u);
+                ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
+                continue;
+            }
             for (int s = 0; s < fa.nstages; ++s, ++g) {
                 if (!WINM) ptx::mbar_wait(full_a(g % CF_SA), (g / CF_SA) & 1u);
                 if (lane == 0) CF_EV(2, g);
@@ -364,8 +388,9 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
 #pragma unroll
         for (int q = 0; q < 9; ++q) w_tap[q] = WINM ? (uint32_t)((q / 3) * fa.Wp + q % 3) : 0u;
         const uint32_t w_c2 = WINM ? (uint32_t)(fa.lbo >> 3) : 0u, w_sh = WINM ? (uint32_t)(fa.Cb_log2 - 4) : 0u;
-        const uint32_t w_base = sbase + OFF_W + (WINM ? 2u * (uint32_t)fa.wslot : 0u), w_bytes = WINM ? (uint32_t)fa.wbytes : 0u;
+        const uint32_t w_base = sbase + OFF_W + (WINM ? (uint32_t)(fa.wring * fa.wslot) : 0u), w_bytes = WINM ? (uint32_t)fa.wbytes : 0u;
         const uint32_t w_nwin = WINM ? (uint32_t)fa.nwin : 1u, w_lbo = WINM ? (uint32_t)fa.lbo : 0u;
+        const bool wbres = WINM && fa.wbres != 0, wpair = WINM && fa.wpair != 0;
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl % CF_NACC;
@@ -377,6 +402,62 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             // block (an mbarrier probe here waits behind its queued MMAs: +2 us on the 64 / 128-wide
             // K = 256 layers), the waiter takes it
             if (CF_NACC == 1) ptx::mbar_wait(acc_empty(acc), (tl & 1u) ^ 1u);
+            if constexpr (WINM) {
+                if (wbres) {   // resident weights (stage s in slot s): the tile's MMAs after one hand-off
+                    ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
+                    if (lane == 0) CF_EV(14, tl);
+                    ptx::tc_fence_after();
+                    if (omma && !(BNT == 64 && wpair))
+                        cf_mma_ts_init(dt, tmem + OA_COL, ptx::desc_k_sw128(sbase + OFF_OB), idesc, tmem + OSFA_COL,
+                                       tmem + OSFB_COL);
+                    // fully unrolled (C = 64: 9 k-steps of 64 codes, one per tap; C = 128: 18, two per
+                    // tap): every descriptor is the tile's window / the resident B base plus a constant
+                    // (a select chain per MMA paced the warp at ~175 cycles per MMA)
+                    const uint64_t bd0 = ptx::desc_k_sw128(sbase + CF_OFF_B);
+                    if (BNT == 64 && wpair) {   // two 128-row blocks of one window: rows [128 h, 128 h + 128)
+#pragma unroll 1
+                        for (uint32_t h = 0; h < 2; ++h) {
+                            const uint32_t va = (2 * tl + h) % CF_NACC, dth = tmem + va * BN_;
+                            const uint64_t awh = aw + 128u * h;   // 128 rows x 16 B further down
+                            if (omma)
+                                cf_mma_ts_init(dth, tmem + OA_COL, ptx::desc_k_sw128(sbase + OFF_OB), idesc,
+                                               tmem + OSFA_COL, tmem + OSFB_COL);
+                            if (w_sh == 0) {
+#pragma unroll
+                                for (int j = 0; j < 9; ++j)
+                                    cf_mma(dth, awh + (uint64_t)w_tap[j],
+                                           bd0 + (uint64_t)(((j >> 2) * B_STAGE_) >> 4) + 2 * (j & 3), idesc, sfa, sfb);
+                            } else {
+#pragma unroll
+                                for (int j = 0; j < 18; ++j)
+                                    cf_mma(dth, awh + (uint64_t)(w_tap[j >> 1] + (j & 1) * w_c2),
+                                           bd0 + (uint64_t)(((j >> 2) * B_STAGE_) >> 4) + 2 * (j & 3), idesc, sfa, sfb);
+                            }
+                            ptx::mma_commit_warp(acc_full((int)va));
+                        }
+                        if (lane == 0) CF_EV(15, tl);
+                        ptx::mma_commit_warp(empty_a((int)wb));   // the window is free again
+                        __syncwarp();
+                        continue;
+                    }
+                    if (w_sh == 0) {
+#pragma unroll
+                        for (int j = 0; j < 9; ++j)
+                            cf_mma(dt, aw + (uint64_t)w_tap[j], bd0 + (uint64_t)(((j >> 2) * B_STAGE_) >> 4) + 2 * (j & 3),
+                                   idesc, sfa, sfb);
+                    } else {
+#pragma unroll
+                        for (int j = 0; j < 18; ++j)
+                            cf_mma(dt, aw + (uint64_t)(w_tap[j >> 1] + (j & 1) * w_c2),
+                                   bd0 + (uint64_t)(((j >> 2) * B_STAGE_) >> 4) + 2 * (j & 3), idesc, sfa, sfb);
+                    }
+                    if (lane == 0) CF_EV(15, tl);
+                    ptx::mma_commit_warp(empty_a((int)wb));   // the window is free again
+                    ptx::mma_commit_warp(acc_full(acc));
+                    __syncwarp();
+                    continue;
+                }
+            }
             for (int s = 0; s < nst; ++s, ++g) {
                 const int sa = (int)(g % CF_SA), bs = (int)(g % SB_);
                 ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
@@ -438,14 +519,15 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const int tid = (warp - CF_UNP0) * 32 + lane;
         const int cb = 1 << fa.Cb_log2, nch = cb >> 4;   // packed bytes per pixel (16 / 32), 16-byte chunks
         const int nrt = (fa.WR + NT - 1) / NT;            // window rows per thread (host: <= 3)
-        const uint32_t ring = sbase + OFF_W, wins = ring + 2u * (uint32_t)fa.wslot;
+        const uint32_t ring = sbase + OFF_W, wins = ring + (uint32_t)(fa.wring * fa.wslot);
+        const int wring = fa.wring;
         auto fetch = [&](int t, int slot) {
             if (t < ntiles) {
                 const int tp = t / fa.ntq;
                 for (int i = 0; i < nrt; ++i) {
                     const int row = tid + i * NT;
                     if (row >= fa.WR) break;
-                    const int64_t q = (int64_t)tp * CF_BM - (fa.Wp + 1) + row;   // padded pixel of this row
+                    const int64_t q = (int64_t)tp * (fa.wpair ? 2 * CF_BM : CF_BM) - (fa.Wp + 1) + row;   // padded pixel of this row
                     const uint8_t *src = nullptr;
                     if (q >= 0 && q < fa.nqv) {
                         const uint32_t b = cf_fdiv((uint32_t)q, fa.fd_hpwp);
@@ -460,12 +542,14 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             }
             ptx::cp_async_commit();
         };
-        fetch(blockIdx.x, 0);
-        fetch(blockIdx.x + gridDim.x, 1);
+        for (int i = 0; i < wring; ++i) fetch(blockIdx.x + i * (int)gridDim.x, i);
         uint32_t tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-            const int slot = (int)(tl & 1u), wb = (int)(tl % (uint32_t)fa.nwin);
-            ptx::cp_async_wait<1>();   // this tile's copies (the older group; each thread reads its own rows)
+            const int slot = (int)(tl % (uint32_t)wring), wb = (int)(tl % (uint32_t)fa.nwin);
+            // this tile's copies (the oldest group; each thread reads its own rows)
+            if (wring == 4) ptx::cp_async_wait<3>();
+            else ptx::cp_async_wait<1>();
+            if (threadIdx.x == (CF_UNP0 + NUNP - 1) * 32) CF_EV(12, tl);
             uint32_t e[WMAXR][16];
 #pragma unroll
             for (int i = 0; i < WMAXR; ++i) {
@@ -482,7 +566,6 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     }
                 }
             }
-            fetch(t + 2 * (int)gridDim.x, slot);   // the slot's bytes are in registers: refill it
             ptx::mbar_wait(empty_a(wb), ((tl / (uint32_t)fa.nwin) & 1u) ^ 1u);   // the window's previous tile finished
             if (threadIdx.x == CF_UNP0 * 32) CF_EV(13, tl);
 #pragma unroll
@@ -502,6 +585,10 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             __syncwarp();
             if (lane == 0) ptx::mbar_arrive(full_a(wb));
             if (threadIdx.x == CF_UNP0 * 32) CF_EV(5, tl);
+            if (threadIdx.x == (CF_UNP0 + NUNP - 1) * 32) CF_EV(0, tl);
+            // the slot's bytes are in registers: refill it, after the window's proxy fence (a fence
+            // behind freshly issued cp.async copies waited for them to land: ~1000 cycles per tile)
+            fetch(t + wring * (int)gridDim.x, slot);
         }
     } else if (warp >= CF_UNP0) {
         // thread = pixel row r of the tile: 64 packed bytes (256 codes) per stage -> 32 words of e2m1
@@ -640,9 +727,13 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const uint32_t tabs = sbase + OFF_TAB;
         uint32_t tl = 0;
         constexpr int RD_N = CSPLIT ? 1 : BN_ / RW;   // load rounds per warp and tile
-        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-            if (NEPI == 8 && !CSPLIT && (int)(tl & 1u) != eg) continue;   // the other group's accumulator
-            const int tq = t % fa.ntq, tp = t / fa.ntq;
+        const bool epair = BNT == 64 && WINM && fa.wpair != 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl)
+        for (int h = 0; h < (epair ? 2 : 1); ++h) {
+            // v: the accumulator sequence number (pair mode: two 128-row blocks per work item)
+            const uint32_t v = epair ? 2 * tl + (uint32_t)h : tl;
+            if (NEPI == 8 && !CSPLIT && (int)(v & 1u) != eg) continue;   // the other group's accumulator
+            const int tq = t % fa.ntq, tp = epair ? 2 * (t / fa.ntq) + h : t / fa.ntq;
             int64_t p = (int64_t)tp * CF_BM + quarter * 32 + lane;
             if (WINM) {   // padded pixel -> output pixel row, or np (not stored) for a padding position
                 const int64_t q = p;
@@ -656,9 +747,9 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 }
             }
             const int64_t q0 = (int64_t)tq * BN_;
-            const uint32_t acc = tl % CF_NACC;
-            ptx::mbar_wait(acc_full(acc), (tl / CF_NACC) & 1u);
-            if (lane == 0 && quarter == 0) CF_EV(6 + 3 * eg, tl);
+            const uint32_t acc = v % CF_NACC;
+            ptx::mbar_wait(acc_full(acc), (v / CF_NACC) & 1u);
+            if (lane == 0 && quarter == 0) CF_EV(6 + 3 * eg, v);
             ptx::tc_fence_after();
             const int c0 = CSPLIT ? eg * 128 : 0;   // this warp's first column of the tile
             const uint32_t trow = tmem + acc * BN_ + (uint32_t)c0 + ((uint32_t)(quarter * 32) << 16);
@@ -679,7 +770,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 ptx::tc_fence_before();
                 __syncwarp();
                 if (lane == 0 && rd == RD_N - 1) ptx::mbar_arrive(acc_empty(acc));
-                if (lane == 0 && quarter == 0) CF_EV(7 + 3 * eg, tl);
+                if (lane == 0 && quarter == 0) CF_EV(7 + 3 * eg, v);
                 if (p < fa.np) {
 #pragma unroll
                     for (int hh = 0; hh < RW / 32; ++hh) {
@@ -712,7 +803,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 __syncwarp();
                 if (lane == 0) ptx::mbar_arrive(acc_empty(acc));
             }
-            if (lane == 0 && quarter == 0) CF_EV(8 + 3 * eg, tl);
+            if (lane == 0 && quarter == 0) CF_EV(8 + 3 * eg, v);
         }
     }
     ptx::tc_fence_before();
@@ -802,23 +893,35 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     const int fbn = (int)opt(OPT_F4_BN);
     const int bnt = fbn == 64 ? 64 : fbn == 128 ? 128 : (fbn == 256 ? 256 : (cout % 256 == 0 ? 256 : (cout <= 64 ? 64 : 128)));
     fa.ntq = (int32_t)((cout + bnt - 1) / bnt);
-    // shifted window (option f4_win: 1 for every direct 3x3 / stride 1 / pad 1 conv over 64 or 128
-    // channels, 0 never): tiles over the padded pixel space, one window per tile
-    const bool win = !direct && opt(OPT_F4_WIN) > 0 && cv.kh == 3 && cv.kw == 3 && cv.stride == 1 && cv.pad == 1 &&
-                     (cb == 16 || cb == 32) && cv.Ho == cv.H && cv.Wo == cv.W;
+    // shifted window (option f4_win: 2 (default) for the direct 3x3 / stride 1 / pad 1 convs over 64 or
+    // 128 channels whose weights can stay resident (one column block, all stages in the B ring), 1 for
+    // every such conv, 0 never): tiles over the padded pixel space, one window per tile (or pair)
+    const int64_t fwin = opt(OPT_F4_WIN);
+    const bool res_ok = fa.ntq == 1 && fa.nstages <= (bnt == 256 ? 3 : CF_SB) && opt(OPT_F4_WBRES) > 0;
+    const bool win = !direct && (fwin == 1 || (fwin == 2 && res_ok)) && cv.kh == 3 && cv.kw == 3 && cv.stride == 1 &&
+                     cv.pad == 1 && (cb == 16 || cb == 32) && cv.Ho == cv.H && cv.Wo == cv.W;
     if (win) {
         const int64_t Wp = cv.W + 2, Hp = cv.H + 2, B = rows / ((int64_t)cv.H * cv.W);
         fa.Wp = (int32_t)Wp;
         fa.nqv = B * Hp * Wp;
         if (fa.nqv >= ((int64_t)1 << 31)) return DG_ERR_SHAPE;
-        fa.ntp = (int32_t)((fa.nqv + CF_BM - 1) / CF_BM);
-        fa.WR = (int32_t)((CF_BM + 2 * Wp + 2 + 7) / 8 * 8);   // multiple of 8 rows: lbo a multiple of 128 B
+        // one column block whose weight stages all fit the B ring: loaded once, one hand-off per tile
+        // (option f4_wbres); with 64-wide tiles, pair mode (option f4_wpair): one window of 256 + halo
+        // rows feeds two 128-row blocks (the halo unpacked once per 256 rows, one hand-off per pair)
+        fa.wbres = res_ok ? 1 : 0;
+        fa.wpair = (fa.wbres && bnt == 64 && opt(OPT_F4_WPAIR) > 0 && 2 * CF_BM + 2 * Wp + 2 <= 3 * 8 * 32) ? 1 : 0;
+        const int64_t wrows = fa.wpair ? 2 * CF_BM : CF_BM;
+        fa.ntp = (int32_t)((fa.nqv + wrows - 1) / wrows);
+        fa.WR = (int32_t)((wrows + 2 * Wp + 2 + 7) / 8 * 8);   // multiple of 8 rows: lbo a multiple of 128 B
         if (fa.WR > 3 * 8 * 32) return DG_ERR_UNSUPPORTED;      // (at most 3 window rows per fill thread)
         fa.lbo = fa.WR * 16;
         fa.wslot = (fa.WR * cb + 127) / 128 * 128;
         fa.wbytes = (cb / 8) * fa.lbo;                           // 2 Cb e2m1 bytes per row = Cb / 8 K chunks
         const int region = CF_OFF_BAR - (CF_OFF_A + bnt * 128);
-        fa.nwin = (region - 2 * fa.wslot) / fa.wbytes;
+        // fetch ring: 4 slots (copies 4 tiles ahead: their latency under load exceeded two tiles) when
+        // that leaves room for a window, else 2
+        fa.wring = (region - 4 * fa.wslot) / fa.wbytes >= 1 ? 4 : 2;
+        fa.nwin = (region - fa.wring * fa.wslot) / fa.wbytes;
         if (fa.nwin > 3) fa.nwin = 3;
         if (fa.nwin < 1) return DG_ERR_UNSUPPORTED;
         fa.fd_hpwp = cf_div((uint32_t)(Hp * Wp));
@@ -922,7 +1025,8 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     lc.numAttrs = 1;
     if (cudaLaunchKernelEx(&lc, kern, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
     char tag[128];
-    snprintf(tag, sizeof(tag), "f4conv bn=%d %s%s unp=%d epi=%d direct=%d rq=%d tab=%d early=%d omma=%d", bnt, win ? "win " : "",
+    snprintf(tag, sizeof(tag), "f4conv bn=%d %s%s unp=%d epi=%d direct=%d rq=%d tab=%d early=%d omma=%d", bnt,
+             win ? (fa.wpair ? "win wbres wpair " : fa.wbres ? "win wbres " : "win ") : "",
              ct == 2 ? "ta nacc=1 ct=2" : (bnt == 256 ? "ta nacc=1" : (bnt == 64 ? "ta nacc=4" : "ta nacc=2")), nunp, nepi, fa.direct, fa.has_rq,
              fa.f16_tab, fa.early_b, fa.omma);
     set_last_kernel(tag);

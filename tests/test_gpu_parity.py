@@ -1086,7 +1086,9 @@ def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn, e
     dg.reset_options()
     ct = 2 if epi == "ct2" else 1
     epi = 4 if epi == "ct2" else epi
-    with dg.options(f4_bn=bn, f4_epi=epi, f4_omma=omma, f4_ct=ct):
+    # (f4_win=0: the gathered / direct instances; the shifted-window ones, the default for the 3x3
+    # s1 convs over 64 / 128 channels with resident weights, are test_conv_f4_window_vs_oracle's)
+    with dg.options(f4_bn=bn, f4_epi=epi, f4_omma=omma, f4_ct=ct, f4_win=0):
         _conv_f4_cases(xp, w4, lut, p, exp, Cout, g, bn, epi)
         assert (" ct=2 " in dg.last_kernel()) == (ct == 2), dg.last_kernel()
         assert dg.last_kernel().endswith(f" omma={omma}"), dg.last_kernel()
@@ -1123,14 +1125,16 @@ F4_WIN_CONVS = [  # B, H, W, C, Cout, pad_code (3x3 / stride 1 / pad 1)
 ]
 
 
+@pytest.mark.parametrize("wbres", [0, 1])   # (1: pair mode too where the tiles are 64 wide)
 @pytest.mark.parametrize("omma", [0, 1])
 @pytest.mark.parametrize("wl", [(-2, -1, 0, 1), (-12, -3, 4, 8)])
 @pytest.mark.parametrize("B,H,W,C,Cout,pad_code", F4_WIN_CONVS)
-def test_conv_f4_window_vs_oracle(B, H, W, C, Cout, pad_code, omma, wl):
+def test_conv_f4_window_vs_oracle(B, H, W, C, Cout, pad_code, omma, wl, wbres):
     """FP4 conv, shifted-window mode (each padded input pixel unpacked once per tile into a shared-
     memory window; the 9 taps are row-shifted views, shared-memory MMAs) vs O-CONV: int32 and the
     fused requant with a per-channel bias (levels -2..1: every case has a 16-bit requant form), the
-    instance asserted by its tag."""
+    instance asserted by its tag; with and without resident weights (option f4_wbres: one column
+    block whose weight stages fit the B ring is loaded once, one MMA hand-off per tile)."""
     if not _tc_available():
         pytest.skip("tc unavailable")
     wl = list(wl)
@@ -1145,10 +1149,14 @@ def test_conv_f4_window_vs_oracle(B, H, W, C, Cout, pad_code, omma, wl):
     w4 = dg.expand_operand_f4(wp, 9 * Cp, wl)
     p = dg.conv_params(B, H, W, Cp, Cout, 3, 3, 1, 1, pad_code, ldw=wp.shape[1])
     dg.reset_options()
-    with dg.options(f4_win=1, f4_omma=omma):
+    bnt = 256 if Cout % 256 == 0 else (64 if Cout <= 64 else 128)
+    resident = wbres == 1 and -(-Cout // bnt) == 1 and -(-9 * Cp // 256) <= (3 if bnt == 256 else 6)
+    with dg.options(f4_win=1, f4_omma=omma, f4_wbres=wbres):
         out = dg.lut_conv2d_f4_prepared(xp, w4, lut, p)
         tag = dg.last_kernel()
         assert " win " in tag, tag
+        assert ("wbres" in tag) == resident, tag
+        assert ("wpair" in tag) == (resident and bnt == 64), tag
         assert np.array_equal(host(out), exp)
         if Cout % 4 == 0:
             bias = (-int(np.round(exp.mean())) + g.integers(-40, 40, Cout)).astype(np.int32)
