@@ -120,6 +120,9 @@ DG_API uint64_t dg_kernel_launches(void);
  *               stages fit the B ring), 1 always, 0 never                    (2)
  *   "f4_wbres"  FP4 conv shifted window: all weight stages resident in shared memory (loaded
  *               once per CTA, one MMA hand-off per tile) when the layer is one column block (1)
+ *   "f4_i2c"    FP4 conv: strided 1x1 convs (downsample) read their pixels through an
+ *               im2col-mode TMA tensor map (element strides = the conv stride) on the direct
+ *               path instead of the per-thread gather                        (1)
  *   "f4_wpair"  FP4 conv shifted window with resident 64-wide tiles: one window of 256 padded
  *               pixels + halo feeds two 128-row blocks into two accumulators (1)
  */

@@ -125,6 +125,8 @@ struct CfArgs {
     int64_t np, nq;              // output pixels (rows), output channels (columns)
     int32_t nstages, last_ksteps, ntp, ntq, ntiles;
     int32_t direct;              // 1: 1x1 / stride 1: the NHWC tensor is the im2col matrix (TMA slots)
+    int32_t i2c;                 // direct mode of a strided 1x1 conv: the slots come through an im2col-mode
+                                 // tensor map (element strides = the conv stride; input pixel (n, s ho, s wo))
     // implicit im2col (direct == 0): x [B][H][W][Cb] packed, Cb = C/4 a power of two >= 16
     const uint8_t *X;
     int32_t H, W, Cb_log2, kw, kw_recip, stride, pad, Ho, Wo, kb;
@@ -335,7 +337,14 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     ptx::mbar_wait(empty_p(ps), ((gp / SP_) & 1u) ^ 1u);
                     if (lane == 0) {
                         ptx::mbar_arrive_expect_tx(full_p(ps), (uint32_t)CF_P_SLOT);
-                        ptx::tma_load_2d(sbase + OFF_P + ps * CF_P_SLOT, &tm_p, full_p(ps), s * (CF_KST / 4), tp * CF_BM);
+                        if (fa.i2c) {   // the tile's first output pixel (n, ho, wo) -> input (n, s ho, s wo)
+                            const uint32_t p0 = (uint32_t)tp * CF_BM, tt = cf_fdiv(p0, fa.fd_wo), n = cf_fdiv(tt, fa.fd_ho);
+                            ptx::tma_load_im2col_4d(sbase + OFF_P + ps * CF_P_SLOT, &tm_p, full_p(ps), s * (CF_KST / 4),
+                                                    (int32_t)(p0 - tt * (uint32_t)fa.Wo) * fa.stride,
+                                                    (int32_t)(tt - n * (uint32_t)fa.Ho) * fa.stride, (int32_t)n);
+                        } else {
+                            ptx::tma_load_2d(sbase + OFF_P + ps * CF_P_SLOT, &tm_p, full_p(ps), s * (CF_KST / 4), tp * CF_BM);
+                        }
                     }
                     __syncwarp();
                     ++gp;
@@ -871,13 +880,44 @@ extern "C" __attribute__((visibility("default"))) int dg_debug_cf_timeline(long 
 // for what this kernel does not cover (the caller then runs the int8 tensor-core path):
 // residuals, bias per row, requant parameters without a 16-bit form, channel counts whose taps are
 // not 16-byte power-of-two chunks.
+typedef CUresult (*CfEncodeIm2col)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                   const cuuint64_t *, const int *, const int *, cuuint32_t, cuuint32_t,
+                                   const cuuint32_t *, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                   CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+// im2col-mode map of a strided 1x1 conv's NHWC input (C = cb bytes per pixel): 128 output pixels x
+// 128 channel bytes per load in the direct slots' 128-byte-swizzled row layout
+bool cf_map_im2col(CUtensorMap *m, const void *base, int64_t cb, int64_t W, int64_t H, int64_t N, int stride) {
+    static CfEncodeIm2col fn = nullptr;
+    static bool tried = false;
+    if (!tried) {
+        tried = true;
+        void *p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeIm2col", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<CfEncodeIm2col>(p);
+    }
+    if (!fn) return false;
+    cuuint64_t dims[4] = {(cuuint64_t)cb, (cuuint64_t)W, (cuuint64_t)H, (cuuint64_t)N};
+    cuuint64_t strides[3] = {(cuuint64_t)cb, (cuuint64_t)(W * cb), (cuuint64_t)(H * W * cb)};
+    int lo[2] = {0, 0}, hi[2] = {0, 0};   // 1x1, no padding: the bounding box is the image
+    cuuint32_t es[4] = {1, (cuuint32_t)stride, (cuuint32_t)stride, 1};
+    return fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 4, const_cast<void *>(base), dims, strides, lo, hi, 128, CF_BM, es,
+              CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const TsConv &cv, int64_t rows, int64_t cout,
                       int64_t K, int64_t acc_bound, void *out, int64_t ldd, const RequantArgs *rq, cudaStream_t st,
                       bool b_prepared) {
     if (rq && (rq->res || rq->res_codes || (rq->bias && rq->bias_axis != 0) || rq->dir <= 0)) return DG_ERR_UNSUPPORTED;
     if (cout > 2 * CF_TAB_PAIRS || rows >= ((int64_t)1 << 31)) return DG_ERR_UNSUPPORTED;
-    const bool direct = cv.kh == 1 && cv.kw == 1 && cv.stride == 1 && cv.pad == 0;
     const int32_t cb = cv.Cb;
+    // strided 1x1 convs (downsample) on the direct path through an im2col-mode tensor map (option f4_i2c)
+    const bool i2c = cv.kh == 1 && cv.kw == 1 && cv.pad == 0 && cv.stride > 1 && cb % 16 == 0 && opt(OPT_F4_I2C) > 0 &&
+                     cv.H < 65536 && cv.W < 65536 && ((uintptr_t)x & 15) == 0;
+    const bool direct = cv.kh == 1 && cv.kw == 1 && cv.pad == 0 && (cv.stride == 1 || i2c);
     if (!direct && !(cb >= 16 && (cb & (cb - 1)) == 0 && cv.kh * cv.kw <= 64)) return DG_ERR_UNSUPPORTED;
     if (direct && (cb % 16 || ((uintptr_t)x & 15))) return DG_ERR_UNSUPPORTED;
     CfArgs fa{};
@@ -931,6 +971,7 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     if (nt > INT32_MAX) return DG_ERR_SHAPE;
     fa.ntiles = (int32_t)nt;
     fa.direct = direct ? 1 : 0;
+    fa.i2c = i2c ? 1 : 0;
     fa.X = x;
     fa.H = cv.H;
     fa.W = cv.W;
@@ -975,7 +1016,11 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     }
     CUtensorMap mp, mb;
     memset(&mp, 0, sizeof(mp));
-    if (direct && !cf_map(&mp, x, cb, cb, rows, CF_BM)) return DG_ERR_CUDA;
+    if (i2c) {
+        if (!cf_map_im2col(&mp, x, cb, cv.W, cv.H, rows / ((int64_t)cv.Ho * cv.Wo), cv.stride)) return DG_ERR_CUDA;
+    } else if (direct && !cf_map(&mp, x, cb, cb, rows, CF_BM)) {
+        return DG_ERR_CUDA;
+    }
     if (!cf_map(&mb, w4, ld4, ld4, cout, bnt)) return DG_ERR_CUDA;
     // (the shared-memory-A form, TA = false, measured 5-20 % slower: kept in the source, not built)
     const bool ta = true;
@@ -1025,9 +1070,10 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     lc.numAttrs = 1;
     if (cudaLaunchKernelEx(&lc, kern, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
     char tag[128];
-    snprintf(tag, sizeof(tag), "f4conv bn=%d %s%s unp=%d epi=%d direct=%d rq=%d tab=%d early=%d omma=%d", bnt,
+    snprintf(tag, sizeof(tag), "f4conv bn=%d %s%s unp=%d epi=%d direct=%d%s rq=%d tab=%d early=%d omma=%d", bnt,
              win ? (fa.wpair ? "win wbres wpair " : fa.wbres ? "win wbres " : "win ") : "",
-             ct == 2 ? "ta nacc=1 ct=2" : (bnt == 256 ? "ta nacc=1" : (bnt == 64 ? "ta nacc=4" : "ta nacc=2")), nunp, nepi, fa.direct, fa.has_rq,
+             ct == 2 ? "ta nacc=1 ct=2" : (bnt == 256 ? "ta nacc=1" : (bnt == 64 ? "ta nacc=4" : "ta nacc=2")), nunp, nepi, fa.direct,
+             fa.i2c ? " i2c" : "", fa.has_rq,
              fa.f16_tab, fa.early_b, fa.omma);
     set_last_kernel(tag);
     return launch_status();

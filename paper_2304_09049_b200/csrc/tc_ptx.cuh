@@ -110,6 +110,17 @@ DG_DEV void tma_load_2d(uint32_t dst, const CUtensorMap *m, uint32_t bar, int32_
         : "memory");
 }
 
+// im2col mode over a 4-d NHWC tensor map (C bytes, W, H, N): the map's pixelsPerColumn output
+// pixels from input position (n, h, w) on, channel bytes [c, c + channelsPerPixel), stepping by the
+// map's element strides (the conv stride), tap offset (0, 0): a strided 1x1 conv's im2col rows
+DG_DEV void tma_load_im2col_4d(uint32_t dst, const CUtensorMap *m, uint32_t bar, int32_t c, int32_t w, int32_t h,
+                               int32_t n) {
+    asm volatile(
+        "cp.async.bulk.tensor.4d.shared::cluster.global.im2col.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5, %6}], [%2], {%7, %7};" ::"r"(dst),
+        "l"(reinterpret_cast<uint64_t>(m)), "r"(bar), "r"(c), "r"(w), "r"(h), "r"(n), "h"((uint16_t)0)
+        : "memory");
+}
+
 // the same box into the same shared-memory offset of every CTA of the cluster in cta_mask, each
 // CTA's mbarrier at offset bar receiving the complete_tx of its copy
 DG_DEV void tma_load_2d_multicast(uint32_t dst, const CUtensorMap *m, uint32_t bar, int32_t x, int32_t y, uint16_t cta_mask) {

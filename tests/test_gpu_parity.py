@@ -1094,6 +1094,48 @@ def test_conv_f4_vs_oracle(wl, B, H, W, C, Cout, k, stride, pad, pad_code, bn, e
         assert dg.last_kernel().endswith(f" omma={omma}"), dg.last_kernel()
 
 
+F4_STRIDED_1X1 = [  # B, H, W, C, Cout, stride, pad_code: strided 1x1 convs (downsample)
+    (2, 12, 12, 256, 128, 2, 0),
+    (1, 13, 11, 128, 256, 2, 1),     # odd input: Ho = 7, Wo = 6 (the traversal skips the last column)
+    (3, 14, 14, 512, 64, 2, 0),
+    (2, 10, 10, 64, 128, 3, 0),      # stride 3, 16-byte pixels (half of every 128-byte slot row is beyond C)
+    (4, 28, 28, 1024, 256, 2, 0),    # K = 1024: two packed slots per tile, tiles across images
+]
+
+
+@pytest.mark.parametrize("i2c", [0, 1])
+@pytest.mark.parametrize("B,H,W,C,Cout,stride,pad_code", F4_STRIDED_1X1)
+def test_conv_f4_strided_1x1_vs_oracle(B, H, W, C, Cout, stride, pad_code, i2c):
+    """Strided 1x1 convs on the FP4 kernel: the direct path whose slots arrive through an
+    im2col-mode TMA tensor map (element strides = the conv stride; option f4_i2c) and the per-thread
+    gather, vs O-CONV (int32 and fused requant), the instance asserted by its tag."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    wl = [-2, -1, 0, 1]
+    lut = dg.build_lut(wl, AL, 8)
+    T = oracle.build_lut16(wl, AL)
+    g = np.random.default_rng(B + H + W + C + Cout + stride)
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, 1, 1, C), dtype=np.uint8)
+    exp = oracle.conv2d_direct(x, w, T, stride, 0, pad_code).reshape(-1, Cout)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    w4 = dg.expand_operand_f4(wp, Cp, wl)
+    p = dg.conv_params(B, H, W, Cp, Cout, 1, 1, stride, 0, pad_code, ldw=wp.shape[1])
+    dg.reset_options()
+    with dg.options(f4_i2c=i2c):
+        out = dg.lut_conv2d_f4_prepared(xp, w4, lut, p)
+        tag = dg.last_kernel()
+        assert (" direct=1 i2c " in tag) == (i2c == 1) and (" direct=0 " in tag) == (i2c == 0), tag
+        assert np.array_equal(host(out), exp)
+        bias = (-int(np.round(exp.mean())) + g.integers(-40, 40, Cout)).astype(np.int32)
+        mult = max(1, int(round((1 << 20) * 1.2 / max(1.0, float(exp.std())))))
+        rq = dg.Requant(mult, 20, 1, 0, 3, bias=torch.from_numpy(bias).to(DEV), bias_axis=0)
+        codes = dg.lut_conv2d_f4_prepared(xp, w4, lut, p, rq=rq)
+        expc = oracle.requantize(exp, mult, 20, 1, 0, 3, bias=bias, bias_axis=0)
+        assert np.array_equal(oracle_codes_of(codes, exp.shape[0], Cout), expc)
+
+
 def _conv_f4_cases(xp, w4, lut, p, exp, Cout, g, bn, epi):
     out = dg.lut_conv2d_f4_prepared(xp, w4, lut, p)
     assert dg.last_kernel().startswith(f"f4conv bn={bn} ") and f" epi={epi} " in dg.last_kernel(), dg.last_kernel()
