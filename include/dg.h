@@ -123,7 +123,7 @@ DG_API uint64_t dg_kernel_launches(void);
  *   "f4_i2c"    FP4 conv: strided 1x1 convs (downsample) read their pixels through an
  *               im2col-mode TMA tensor map (element strides = the conv stride) on the direct
  *               path instead of the per-thread gather                        (1)
- *   "f4_wpair"  FP4 conv shifted window with resident 64-wide tiles: one window of 256 padded
+ *   "f4_wpair"  FP4 conv shifted window with resident 64 / 128-wide tiles: one window of 256 padded
  *               pixels + halo feeds two 128-row blocks into two accumulators (1)
  */
 DG_API dg_status dg_set_option(const char *name, int64_t value);

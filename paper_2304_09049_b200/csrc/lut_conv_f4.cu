@@ -225,13 +225,15 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     constexpr int OFF_W = CF_OFF_A + BNT * 128;
     constexpr int BN_ = BNT, SB_ = (C2 || BNT == 256) ? 3 : CF_SB, B_STAGE_ = BNT * CF_KST / 2;   // (96 / 48 KB of B stages)
     // accumulators: 256-wide 1, 128-wide 2 (two CTAs per SM: 1), 64-wide 4
-    constexpr int CF_NACC = TA ? ((C2 || BNT == 256) ? 1 : (BNT == 64 ? 4 : 2)) : 3, CF_SA = TA ? (C2 ? 3 : 6) : 4;
+    // (shifted window, 128 wide: 3, so that window pairs of two accumulators are double-buffered; the
+    // window is the shared-memory A operand, the tensor-memory A stages are unused)
+    constexpr int CF_NACC = TA ? ((C2 || BNT == 256) ? 1 : (BNT == 64 ? 4 : (WINM ? 3 : 2))) : 3, CF_SA = TA ? (C2 ? 3 : 6) : 4;
     constexpr int RW = BNT < 128 ? BNT : 128;   // columns per epilogue load round
     constexpr uint32_t TA0 = CF_NACC * BN_;   // first tensor-memory A column (TA)
     constexpr uint32_t TCOLS = C2 ? 256 : 512;
     constexpr uint32_t SF_COL = C2 ? 248 : CF_SF_COL, SFB_OFF = C2 ? 4 : 16;
     constexpr uint32_t OA_COL = C2 ? 240 : CF_OA_COL, OSFA_COL = C2 ? 224 : CF_OSFA_COL, OSFB_COL = C2 ? 232 : CF_OSFB_COL;
-    static_assert(!TA || TA0 + CF_SA * 32 <= (C2 ? OSFA_COL : OA_COL), "tensor memory budget");
+    static_assert(!TA || (WINM ? TA0 : TA0 + CF_SA * 32) <= (C2 ? OSFA_COL : OA_COL), "tensor memory budget");
     constexpr int SP_ = C2 ? 2 : CF_SP, IG_ = C2 ? 4 : CF_IG;
     constexpr int OFF_OB = C2 ? CF2_OFF_OB : CF_OFF_A, OFF_P = C2 ? CF2_OFF_P : CF_OFF_P;
     constexpr int OFF_BAR = C2 ? CF2_OFF_BAR : CF_OFF_BAR, OFF_TMEM = C2 ? CF2_OFF_TMEM : CF_OFF_TMEM;
@@ -362,7 +364,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
     } else if (warp == CF_WAIT) {
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
-            if (BNT == 64 && WINM && fa.wpair) {   // both accumulators of the pair
+            if (BNT <= 128 && WINM && fa.wpair) {   // both accumulators of the pair
                 ptx::mbar_wait(acc_empty((2 * tl) % CF_NACC), (((2 * tl) / CF_NACC) & 1u) ^ 1u);
                 ptx::mbar_wait(acc_empty((2 * tl + 1) % CF_NACC), (((2 * tl + 1) / CF_NACC) & 1u) ^ 1u);
             } else if (CF_NACC > 1) {
@@ -416,14 +418,14 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     ptx::named_bar_sync(CF_HANDOFF_BAR, 64);
                     if (lane == 0) CF_EV(14, tl);
                     ptx::tc_fence_after();
-                    if (omma && !(BNT == 64 && wpair))
+                    if (omma && !(BNT <= 128 && wpair))
                         cf_mma_ts_init(dt, tmem + OA_COL, ptx::desc_k_sw128(sbase + OFF_OB), idesc, tmem + OSFA_COL,
                                        tmem + OSFB_COL);
                     // fully unrolled (C = 64: 9 k-steps of 64 codes, one per tap; C = 128: 18, two per
                     // tap): every descriptor is the tile's window / the resident B base plus a constant
                     // (a select chain per MMA paced the warp at ~175 cycles per MMA)
                     const uint64_t bd0 = ptx::desc_k_sw128(sbase + CF_OFF_B);
-                    if (BNT == 64 && wpair) {   // two 128-row blocks of one window: rows [128 h, 128 h + 128)
+                    if (BNT <= 128 && wpair) {   // two 128-row blocks of one window: rows [128 h, 128 h + 128)
 #pragma unroll 1
                         for (uint32_t h = 0; h < 2; ++h) {
                             const uint32_t va = (2 * tl + h) % CF_NACC, dth = tmem + va * BN_;
@@ -736,7 +738,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const uint32_t tabs = sbase + OFF_TAB;
         uint32_t tl = 0;
         constexpr int RD_N = CSPLIT ? 1 : BN_ / RW;   // load rounds per warp and tile
-        const bool epair = BNT == 64 && WINM && fa.wpair != 0;
+        const bool epair = BNT <= 128 && WINM && fa.wpair != 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl)
         for (int h = 0; h < (epair ? 2 : 1); ++h) {
             // v: the accumulator sequence number (pair mode: two 128-row blocks per work item)
@@ -946,10 +948,10 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
         fa.nqv = B * Hp * Wp;
         if (fa.nqv >= ((int64_t)1 << 31)) return DG_ERR_SHAPE;
         // one column block whose weight stages all fit the B ring: loaded once, one hand-off per tile
-        // (option f4_wbres); with 64-wide tiles, pair mode (option f4_wpair): one window of 256 + halo
+        // (option f4_wbres); with 64 / 128-wide tiles, pair mode (option f4_wpair): one window of 256 + halo
         // rows feeds two 128-row blocks (the halo unpacked once per 256 rows, one hand-off per pair)
         fa.wbres = res_ok ? 1 : 0;
-        fa.wpair = (fa.wbres && bnt == 64 && opt(OPT_F4_WPAIR) > 0 && 2 * CF_BM + 2 * Wp + 2 <= 3 * 8 * 32) ? 1 : 0;
+        fa.wpair = (fa.wbres && bnt <= 128 && opt(OPT_F4_WPAIR) > 0 && 2 * CF_BM + 2 * Wp + 2 <= 3 * 8 * 32) ? 1 : 0;
         const int64_t wrows = fa.wpair ? 2 * CF_BM : CF_BM;
         fa.ntp = (int32_t)((fa.nqv + wrows - 1) / wrows);
         fa.WR = (int32_t)((wrows + 2 * Wp + 2 + 7) / 8 * 8);   // multiple of 8 rows: lbo a multiple of 128 B
@@ -960,7 +962,7 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
         const int region = CF_OFF_BAR - (CF_OFF_A + bnt * 128);
         // fetch ring: 4 slots (copies 4 tiles ahead: their latency under load exceeded two tiles) when
         // that leaves room for a window, else 2
-        fa.wring = (region - 4 * fa.wslot) / fa.wbytes >= 1 ? 4 : 2;
+        fa.wring = (region - 4 * fa.wslot) / fa.wbytes >= 2 ? 4 : 2;   // (two windows at least)
         fa.nwin = (region - fa.wring * fa.wslot) / fa.wbytes;
         if (fa.nwin > 3) fa.nwin = 3;
         if (fa.nwin < 1) return DG_ERR_UNSUPPORTED;
@@ -1072,7 +1074,7 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     char tag[128];
     snprintf(tag, sizeof(tag), "f4conv bn=%d %s%s unp=%d epi=%d direct=%d%s rq=%d tab=%d early=%d omma=%d", bnt,
              win ? (fa.wpair ? "win wbres wpair " : fa.wbres ? "win wbres " : "win ") : "",
-             ct == 2 ? "ta nacc=1 ct=2" : (bnt == 256 ? "ta nacc=1" : (bnt == 64 ? "ta nacc=4" : "ta nacc=2")), nunp, nepi, fa.direct,
+             ct == 2 ? "ta nacc=1 ct=2" : (bnt == 256 ? "ta nacc=1" : (bnt == 64 ? "ta nacc=4" : (win ? "ta nacc=3" : "ta nacc=2"))), nunp, nepi, fa.direct,
              fa.i2c ? " i2c" : "", fa.has_rq,
              fa.f16_tab, fa.early_b, fa.omma);
     set_last_kernel(tag);

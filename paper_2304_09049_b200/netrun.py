@@ -60,16 +60,16 @@ def f4_default(layer, Cp: int) -> bool:
     warps) takes by default, from per-layer measurements against the int8 kernels (DESIGN.md
     §6.4): 1x1 convs with K >= 256 (stride 1 or 2, Cout = 64 or >= 128) or into 64 channels, the
     gathered 3x3 convs over >= 256 channels, the 3x3 convs over 128 channels that are strided or
-    produce a multiple of 256 channels, and the 3x3 s1 convs 64 -> 64 / 128 -> 128 (shifted window
-    with resident weights; 64 -> 64 in pair mode).  The short-K wide 1x1 layers (K <= 128 into
-    >= 128 channels) and the 3x3 64 -> 128 convs (int8 shifted-window pair mode) stay on int8."""
+    produce a multiple of 256 channels, and the 3x3 s1 convs from 64 / 128 into 64 / 128 channels
+    (shifted window with resident weights, one window per two 128-row blocks).  The short-K wide 1x1
+    layers (K <= 128 into >= 128 channels) stay on int8."""
     K = layer.k * layer.k * Cp
     if layer.cout % 4 or not (layer.cout >= 128 or layer.cout == 64):
         return False
     if layer.k == 1 and layer.pad == 0:
         return K >= 256 or layer.cout == 64
-    if layer.k == 3 and layer.stride == 1 and layer.pad == 1 and Cp in (64, 128) and layer.cout == Cp:
-        return True   # shifted window, resident weights (64 -> 64: pair mode)
+    if layer.k == 3 and layer.stride == 1 and layer.pad == 1 and Cp in (64, 128) and layer.cout in (64, 128):
+        return True   # shifted window, resident weights, window pairs
     return layer.cout >= 128 and layer.k == 3 and (Cp >= 256 or (Cp >= 128 and (layer.cout % 256 == 0 or layer.stride == 2)))
 
 
