@@ -323,6 +323,8 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         // (weights are read before the programmatic-dependent-launch wait only under early_weights)
         if (!fa.early_b || DIRECT) ptx::griddep_wait();
         uint32_t gp = 0, gb = 0;
+        // (pinned in a register: a kernel-parameter load inside the loop slowed the one-slot tiles' producer)
+        const uint32_t pi2c = DIRECT ? __shfl_sync(0xffffffffu, (uint32_t)fa.i2c, 0) : 0u;
         if (WINM && fa.wbres) {   // resident weights: every stage loaded once, into slot s (one column block)
             if (lane == 0 && (int)blockIdx.x < ntiles)
                 for (int s = 0; s < fa.nstages; ++s) {
@@ -339,7 +341,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                     ptx::mbar_wait(empty_p(ps), ((gp / SP_) & 1u) ^ 1u);
                     if (lane == 0) {
                         ptx::mbar_arrive_expect_tx(full_p(ps), (uint32_t)CF_P_SLOT);
-                        if (fa.i2c) {   // the tile's first output pixel (n, ho, wo) -> input (n, s ho, s wo)
+                        if (pi2c) {   // the tile's first output pixel (n, ho, wo) -> input (n, s ho, s wo)
                             const uint32_t p0 = (uint32_t)tp * CF_BM, tt = cf_fdiv(p0, fa.fd_wo), n = cf_fdiv(tt, fa.fd_ho);
                             ptx::tma_load_im2col_4d(sbase + OFF_P + ps * CF_P_SLOT, &tm_p, full_p(ps), s * (CF_KST / 4),
                                                     (int32_t)(p0 - tt * (uint32_t)fa.Wo) * fa.stride,
