@@ -89,3 +89,84 @@ def test_conv_chain_graph_replays_bit_exact():
             assert np.array_equal(got, e), (rep, li, frag)
     # the chain's codes stay spread (it did not collapse to a constant)
     assert (np.bincount(exp[-1].ravel(), minlength=4) > exp[-1].size // 50).sum() >= 3
+
+
+# the same regime on the FP4 conv kernel (dg_lut_conv2d_f4_prepared): shifted-window pairs (64- and
+# 128-wide, resident weights), direct 1x1 tiles of every width, the im2col-mode strided 1x1, the
+# gathered stride-2 3x3; input 24 x 40 x 40 x 64 codes
+F4_CHAIN = [
+    (64, 3, 1, "bn=64 win wbres wpair"),
+    (128, 3, 1, "bn=128 win wbres wpair"),
+    (128, 3, 1, "bn=128 win wbres wpair"),
+    (256, 1, 2, "direct=1 i2c"),
+    (64, 1, 1, "bn=64 ta nacc=4"),
+    (256, 1, 1, "bn=256 ta nacc=1"),
+    (256, 3, 2, "direct=0"),
+    (512, 1, 1, "bn=256 ta nacc=1"),
+]
+
+
+def test_f4_conv_chain_graph_replays_bit_exact():
+    g = np.random.default_rng(2025)
+    B, H, C = 24, 40, 64
+    T = oracle.build_lut16(WL, AL)
+    x = g.integers(0, 4, (B, H, H, C), dtype=np.uint8)
+    lut = dg.build_lut(WL, AL, 8)
+    dev = "cuda"
+    cur = dg.pack_codes(torch.from_numpy(x.reshape(-1, C)).to(dev))[:, : C // 4].contiguous()
+    layers, exp = [], []
+    xo, h, c = x, H, C
+    for cout, k, s, frag in F4_CHAIN:
+        w = g.integers(0, 4, (cout, k, k, c), dtype=np.uint8)
+        pad = k // 2
+        acc = oracle.conv2d_direct(xo, w, T, s, pad, 0)
+        ho = acc.shape[1]
+        a2 = acc.reshape(-1, cout).astype(np.float64)
+        bias = (-np.round(a2.mean(axis=0))).astype(np.int32)
+        wp = dg.pack_weights(torch.from_numpy(w.reshape(cout, -1)).to(dev))
+        w4 = dg.expand_operand_f4(wp, k * k * c, WL)
+        p = dg.conv_params(B, h, h, c, cout, k, k, s, pad, 0, ldw=wp.shape[1])
+        out = torch.empty((B * ho * ho, cout // 4), dtype=torch.uint8, device=dev)
+        bias_d = torch.from_numpy(bias).to(dev)
+        # the FP4 kernel takes only requant maps with a 16-bit form (host-verified): the first
+        # multiplier from the calibrated one up that has one
+        mult = int(round((1 << 20) / max(1.0, float((a2 + bias).std()))))
+        for _ in range(64):
+            rq = dg.Requant(mult, 20, 1, 0, 3, bias=bias_d, bias_axis=0)
+            try:
+                dg.lut_conv2d_f4_prepared(cur, w4, lut, p, rq=rq, out=out)
+                break
+            except dg.DGError:
+                mult += 7
+        else:
+            raise AssertionError(("no 16-bit requant form near", frag))
+        codes = oracle.requantize(acc.reshape(-1, cout), mult, 20, 1, 0, 3, bias=bias, bias_axis=0)
+        layers.append((cur, w4, p, rq, out, frag))
+        exp.append(codes)
+        cur, xo, h, c = out, codes.reshape(B, ho, ho, cout), ho, cout
+    torch.cuda.synchronize()
+
+    def step():
+        tags = []
+        for li, (xin, w4, p, rq, out, frag) in enumerate(layers):
+            dg.lut_conv2d_f4_prepared(xin, w4, lut, p, rq=rq, out=out)
+            tags.append(dg.last_kernel())
+        return tags
+
+    dg.reset_options()
+    with dg.options(early_weights=1):
+        tags = step()
+        for t, (*_, frag) in zip(tags, layers):
+            assert frag in t, (frag, t)
+        graph = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(graph):
+            step()
+    for rep in range(25):
+        for (*_, out, frag) in layers:
+            out.fill_(0x5A)                  # poison: a premature read would see this
+        graph.replay()
+        torch.cuda.synchronize()
+        for li, ((*_, out, frag), e) in enumerate(zip(layers, exp)):
+            got = oracle.unpack_codes(out.cpu().numpy(), e.shape[0], e.shape[1], out.shape[1])
+            assert np.array_equal(got, e), (rep, li, frag)
+    assert (np.bincount(exp[-1].ravel(), minlength=4) > exp[-1].size // 50).sum() >= 3
