@@ -123,6 +123,9 @@ DG_API uint64_t dg_kernel_launches(void);
  *   "f4_i2c"    FP4 conv: strided 1x1 convs (downsample) read their pixels through an
  *               im2col-mode TMA tensor map (element strides = the conv stride) on the direct
  *               path instead of the per-thread gather                        (1)
+ *   "f4_w1x1"   FP4 conv: 1x1 stride-1 convs into 64 / 128 channels as window pairs (a
+ *               pair's 256 pixel rows are the shared-memory A window): 1 over 64 input
+ *               channels, 2 over 64 / 128 / 256, 0 never                    (1)
  *   "f4_wpair"  FP4 conv shifted window with resident 64 / 128-wide tiles: one window of 256 padded
  *               pixels + halo feeds two 128-row blocks into two accumulators (1)
  */

@@ -32,7 +32,7 @@ const OptDesc kOpts[dg::OPT_COUNT] = {
     {"f4_bn", "DG_F4_BN", 0, -1},       {"f4_omma", "DG_F4_OMMA", 1, -1},
     {"f4_ct", "DG_F4_CT", 0, -1},       {"skfuse", "DG_SKFUSE", 0, 1},   {"f4_win", "DG_F4_WIN", 2, -1},
     {"offs", "DG_NO_OFFS", 1, 0},       {"bmc", "DG_BMC", 0, 1},         {"f4_wbres", "DG_F4_NO_WBRES", 1, 0},
-    {"f4_i2c", "DG_F4_NO_I2C", 1, 0},   {"f4_wpair", "DG_F4_NO_WPAIR", 1, 0},
+    {"f4_i2c", "DG_F4_NO_I2C", 1, 0},   {"f4_w1x1", "DG_F4_W1X1", 1, 2},   {"f4_wpair", "DG_F4_NO_WPAIR", 1, 0},
 };
 
 int64_t *opt_table() {

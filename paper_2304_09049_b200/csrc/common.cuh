@@ -213,6 +213,7 @@ enum OptId {
     OPT_BMC,            // TS kernel: B stages multicast across 2-CTA clusters where the tile walk allows (1), 0 off (default)
     OPT_F4_WBRES,       // FP4 conv shifted window: weights resident when one column block fits the B ring (1), 0 off
     OPT_F4_I2C,         // FP4 conv: strided 1x1 convs on the direct path through an im2col-mode tensor map (1), 0 gathered
+    OPT_F4_W1X1,        // FP4 conv: 1x1 stride-1 convs into 64 / 128 channels as window pairs: 1 over 64 channels, 2 over <= 256, 0 never
     OPT_F4_WPAIR,       // FP4 conv shifted window, 64 / 128-wide resident tiles: one window per two 128-row blocks (1), 0 off
     OPT_COUNT
 };

@@ -144,6 +144,8 @@ struct CfArgs {
     int32_t Wp, WR, lbo, wslot, wbytes, nwin;
     int32_t wring;               // packed fetch ring slots (2 or 4): the fill's copies run wring tiles ahead
     int32_t wbres;               // window mode, one column block: all weight stages resident (slot s = stage s)
+    int32_t w1x1;                // window mode of a 1x1 stride-1 conv: the window is the pair's own 256 pixel
+                                 // rows (no halo, no padding), K = C / 64 MMA k-steps per 128-row block
     int32_t wpair;               // window pair mode (64-wide tiles, resident weights): a work item = 256 padded
                                  // pixels, one window feeds two 128-row blocks into two accumulators
     int64_t nqv;
@@ -403,7 +405,8 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
         const uint32_t w_c2 = WINM ? (uint32_t)(fa.lbo >> 3) : 0u, w_sh = WINM ? (uint32_t)(fa.Cb_log2 - 4) : 0u;
         const uint32_t w_base = sbase + OFF_W + (WINM ? (uint32_t)(fa.wring * fa.wslot) : 0u), w_bytes = WINM ? (uint32_t)fa.wbytes : 0u;
         const uint32_t w_nwin = WINM ? (uint32_t)fa.nwin : 1u, w_lbo = WINM ? (uint32_t)fa.lbo : 0u;
-        const bool wbres = WINM && fa.wbres != 0, wpair = WINM && fa.wpair != 0;
+        const bool wbres = WINM && fa.wbres != 0, wpair = WINM && fa.wpair != 0, w1x1 = WINM && fa.w1x1 != 0;
+        const int w_nks = WINM ? (1 << fa.Cb_log2) / 16 : 0;   // (1x1: 64-code k-steps per row)
         uint32_t g = 0, tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
             const uint32_t acc = tl % CF_NACC;
@@ -435,7 +438,13 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                             if (omma)
                                 cf_mma_ts_init(dth, tmem + OA_COL, ptx::desc_k_sw128(sbase + OFF_OB), idesc,
                                                tmem + OSFA_COL, tmem + OSFB_COL);
-                            if (w_sh == 0) {
+                            if (w1x1) {   // 1x1: k-step j = 64-code chunk j of the pixel's own row
+#pragma unroll
+                                for (int j = 0; j < 4; ++j) {
+                                    if (j >= w_nks) break;
+                                    cf_mma(dth, awh + (uint64_t)(j * w_c2), bd0 + 2 * j, idesc, sfa, sfb);
+                                }
+                            } else if (w_sh == 0) {
 #pragma unroll
                                 for (int j = 0; j < 9; ++j)
                                     cf_mma(dth, awh + (uint64_t)w_tap[j],
@@ -521,6 +530,52 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
                 __syncwarp();
                 if (lane == 0) CF_EV(4, g);
             }
+        }
+    } else if (WINM && warp >= CF_UNP0 && fa.w1x1) {
+        // ---------------- 1x1 window fill: thread = one of the pair's 256 pixel rows; its packed pixel
+        // (C/4 bytes, up to 64) arrives by cp.async two pairs ahead, becomes e2m1 nibbles chunk by
+        // chunk (16 packed bytes -> two 16-byte K chunks at j * lbo + 16 * row)
+        ptx::griddep_wait();
+        const int tid = (warp - CF_UNP0) * 32 + lane;
+        const int cb = 1 << fa.Cb_log2, nch = cb >> 4;
+        const uint32_t ring = sbase + OFF_W, wins = ring + 2u * (uint32_t)fa.wslot;
+        auto fetch = [&](int t, int slot) {
+            if (t < ntiles && tid < fa.WR) {
+                const int64_t q = (int64_t)(t / fa.ntq) * (2 * CF_BM) + tid;
+                const uint8_t *src = q < fa.nqv ? fa.X + (q << fa.Cb_log2) : fa.padsrc;
+                const uint32_t dst = ring + (uint32_t)(slot * fa.wslot + tid * cb);
+                for (int c = 0; c < nch; ++c) ptx::cp_async16(dst + 16 * c, q < fa.nqv ? src + 16 * c : fa.padsrc);
+            }
+            ptx::cp_async_commit();
+        };
+        fetch(blockIdx.x, 0);
+        fetch(blockIdx.x + gridDim.x, 1);
+        uint32_t tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const int slot = (int)(tl & 1u), wb = (int)(tl % (uint32_t)fa.nwin);
+            ptx::cp_async_wait<1>();
+            ptx::mbar_wait(empty_a(wb), ((tl / (uint32_t)fa.nwin) & 1u) ^ 1u);   // the window's previous pair finished
+            if (tid < fa.WR) {
+                const uint32_t wdst = wins + (uint32_t)(wb * fa.wbytes + tid * 16);
+                for (int c = 0; c < nch; ++c) {
+                    const uint4 v = ptx::lds128(ring + (uint32_t)(slot * fa.wslot + tid * cb + 16 * c));
+                    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+                    uint32_t e[8];
+#pragma unroll
+                    for (int k = 0; k < 4; ++k) {
+                        e[2 * k] = w[k] & 0x33333333u;
+                        e[2 * k + 1] = (w[k] >> 2) & 0x33333333u;
+                    }
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(wdst + (uint32_t)(2 * c * fa.lbo)),
+                                 "r"(e[0]), "r"(e[1]), "r"(e[2]), "r"(e[3]) : "memory");
+                    asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(wdst + (uint32_t)((2 * c + 1) * fa.lbo)),
+                                 "r"(e[4]), "r"(e[5]), "r"(e[6]), "r"(e[7]) : "memory");
+                }
+            }
+            ptx::fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) ptx::mbar_arrive(full_a(wb));
+            fetch(t + 2 * (int)gridDim.x, slot);   // (after the fence: see the 3x3 fill)
         }
     } else if (WINM && warp >= CF_UNP0) {
         // ---------------- window fill: thread = window row(s) (padded input pixels q0 - Wp - 1 + row):
@@ -748,7 +803,7 @@ lut_conv_f4_kernel(const __grid_constant__ CUtensorMap tm_p, const __grid_consta
             if (NEPI == 8 && !CSPLIT && (int)(v & 1u) != eg) continue;   // the other group's accumulator
             const int tq = t % fa.ntq, tp = epair ? 2 * (t / fa.ntq) + h : t / fa.ntq;
             int64_t p = (int64_t)tp * CF_BM + quarter * 32 + lane;
-            if (WINM) {   // padded pixel -> output pixel row, or np (not stored) for a padding position
+            if (WINM && !fa.w1x1) {   // padded pixel -> output pixel row, or np (not stored) for a padding position
                 const int64_t q = p;
                 p = fa.np;
                 if (q < fa.nqv) {
@@ -921,7 +976,7 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     // strided 1x1 convs (downsample) on the direct path through an im2col-mode tensor map (option f4_i2c)
     const bool i2c = cv.kh == 1 && cv.kw == 1 && cv.pad == 0 && cv.stride > 1 && cb % 16 == 0 && opt(OPT_F4_I2C) > 0 &&
                      cv.H < 65536 && cv.W < 65536 && ((uintptr_t)x & 15) == 0;
-    const bool direct = cv.kh == 1 && cv.kw == 1 && cv.pad == 0 && (cv.stride == 1 || i2c);
+    bool direct = cv.kh == 1 && cv.kw == 1 && cv.pad == 0 && (cv.stride == 1 || i2c);
     if (!direct && !(cb >= 16 && (cb & (cb - 1)) == 0 && cv.kh * cv.kw <= 64)) return DG_ERR_UNSUPPORTED;
     if (direct && (cb % 16 || ((uintptr_t)x & 15))) return DG_ERR_UNSUPPORTED;
     CfArgs fa{};
@@ -942,9 +997,34 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     // every such conv, 0 never): tiles over the padded pixel space, one window per tile (or pair)
     const int64_t fwin = opt(OPT_F4_WIN);
     const bool res_ok = fa.ntq == 1 && fa.nstages <= (bnt == 256 ? 3 : CF_SB) && opt(OPT_F4_WBRES) > 0;
-    const bool win = !direct && (fwin == 1 || (fwin == 2 && res_ok)) && cv.kh == 3 && cv.kw == 3 && cv.stride == 1 &&
-                     cv.pad == 1 && (cb == 16 || cb == 32) && cv.Ho == cv.H && cv.Wo == cv.W;
-    if (win) {
+    const bool win3 = !direct && (fwin == 1 || (fwin == 2 && res_ok)) && cv.kh == 3 && cv.kw == 3 && cv.stride == 1 &&
+                      cv.pad == 1 && (cb == 16 || cb == 32) && cv.Ho == cv.H && cv.Wo == cv.W;
+    // 1x1 stride-1 convs into 64 / 128 channels as window pairs (option f4_w1x1: 1 (default) over 64
+    // input channels, 2 over 64 / 128 / 256): the direct path's per-128-row hand-off chain bounds these
+    // narrow tiles; a pair's 256 pixel rows are the window.  Measured (ResNet-50 b256): 64 -> 64
+    // 24.6 -> 23.1 us; over 256 channels slower (the fill's 4 chunks per row: 25.8 -> 32.3 us)
+    const int64_t fw1 = opt(OPT_F4_W1X1);
+    const bool w1x1 = direct && !i2c && res_ok && bnt <= 128 && (cb == 16 || (fw1 == 2 && (cb == 32 || cb == 64))) &&
+                      fw1 > 0 && opt(OPT_F4_WPAIR) > 0 && fwin != 0;
+    const bool win = win3 || w1x1;
+    if (w1x1) direct = false;
+    if (w1x1) {   // the pixel rows themselves: no halo, no padding, always pairs
+        fa.w1x1 = 1;
+        fa.Wp = 0;
+        fa.nqv = rows;
+        fa.wbres = 1;
+        fa.wpair = 1;
+        fa.ntp = (int32_t)((rows + 2 * CF_BM - 1) / (2 * CF_BM));
+        fa.WR = 2 * CF_BM;
+        fa.lbo = fa.WR * 16;
+        fa.wslot = (fa.WR * cb + 127) / 128 * 128;
+        fa.wbytes = (cb / 8) * fa.lbo;
+        const int region = CF_OFF_BAR - (CF_OFF_A + bnt * 128);
+        fa.wring = 2;
+        fa.nwin = (region - 2 * fa.wslot) / fa.wbytes;
+        if (fa.nwin > 3) fa.nwin = 3;
+        if (fa.nwin < 1) return DG_ERR_UNSUPPORTED;
+    } else if (win) {
         const int64_t Wp = cv.W + 2, Hp = cv.H + 2, B = rows / ((int64_t)cv.H * cv.W);
         fa.Wp = (int32_t)Wp;
         fa.nqv = B * Hp * Wp;
@@ -1075,7 +1155,7 @@ dg_status lut_conv_f4(const uint8_t *x, const uint8_t *w4, int64_t ld4, const Ts
     if (cudaLaunchKernelEx(&lc, kern, mp, mb, fa, rqv) != cudaSuccess) return DG_ERR_CUDA;
     char tag[128];
     snprintf(tag, sizeof(tag), "f4conv bn=%d %s%s unp=%d epi=%d direct=%d%s rq=%d tab=%d early=%d omma=%d", bnt,
-             win ? (fa.wpair ? "win wbres wpair " : fa.wbres ? "win wbres " : "win ") : "",
+             win ? (fa.w1x1 ? "win1x1 wbres wpair " : fa.wpair ? "win wbres wpair " : fa.wbres ? "win wbres " : "win ") : "",
              ct == 2 ? "ta nacc=1 ct=2" : (bnt == 256 ? "ta nacc=1" : (bnt == 64 ? "ta nacc=4" : (win ? "ta nacc=3" : "ta nacc=2"))), nunp, nepi, fa.direct,
              fa.i2c ? " i2c" : "", fa.has_rq,
              fa.f16_tab, fa.early_b, fa.omma);

@@ -119,6 +119,7 @@ def test_config3_resnet50_every_layer_full_batch():
     assert any(t.startswith("f4conv bn=256") and "direct=0" in t for t in tags), tags         # 3x3 C >= 256: FP4
     assert any(t.startswith("f4conv bn=128") and "direct=0" in t for t in tags), tags         # 3x3 s2 128: FP4
     assert any(t.startswith("f4conv bn=64") and "direct=1" in t for t in tags), tags          # 1x1 256 -> 64: FP4
+    assert any(t.startswith("f4conv bn=64 win1x1 ") for t in tags), tags                      # 1x1 64 -> 64: window pairs
 
 
 def test_config4_vgg16_every_layer_full_batch():

@@ -1136,6 +1136,48 @@ def test_conv_f4_strided_1x1_vs_oracle(B, H, W, C, Cout, stride, pad_code, i2c):
         assert np.array_equal(oracle_codes_of(codes, exp.shape[0], Cout), expc)
 
 
+F4_1X1_WIN = [  # B, H, W, C, Cout: 1x1 stride-1 convs into 64 / 128 channels (K <= 256)
+    (2, 10, 10, 64, 64),
+    (1, 9, 7, 128, 128),       # 63 rows: one ragged pair
+    (3, 14, 14, 256, 64),      # 588 rows: pairs across images, ragged last pair
+    (2, 28, 28, 256, 128),     # many pairs per CTA: window ring reuse
+    (1, 5, 5, 64, 100),        # ragged Cout (exact epilogue path on the last columns)
+]
+
+
+@pytest.mark.parametrize("B,H,W,C,Cout", F4_1X1_WIN)
+def test_conv_f4_1x1_window_pairs_vs_oracle(B, H, W, C, Cout):
+    """1x1 stride-1 convs on the FP4 kernel's window-pair form (option f4_w1x1 = 2: a pair's 256 pixel
+    rows are the shared-memory A window, resident weights, two 128-row accumulators per hand-off)
+    vs O-CONV: int32 and the fused requant, the instance asserted by its tag."""
+    if not _tc_available():
+        pytest.skip("tc unavailable")
+    wl = [-2, -1, 0, 1]
+    lut = dg.build_lut(wl, AL, 8)
+    T = oracle.build_lut16(wl, AL)
+    g = np.random.default_rng(B + H + W + C + Cout)
+    x = g.integers(0, 4, (B, H, W, C), dtype=np.uint8)
+    w = g.integers(0, 4, (Cout, 1, 1, C), dtype=np.uint8)
+    exp = oracle.conv2d_direct(x, w, T, 1, 0, 0).reshape(-1, Cout)
+    xp, Cp = nhwc_pack(x)
+    wp = conv_weights_pack(w, Cp)
+    w4 = dg.expand_operand_f4(wp, Cp, wl)
+    p = dg.conv_params(B, H, W, Cp, Cout, 1, 1, 1, 0, 0, ldw=wp.shape[1])
+    dg.reset_options()
+    with dg.options(f4_w1x1=2):   # (2: every channel count; the default takes C = 64 only)
+        out = dg.lut_conv2d_f4_prepared(xp, w4, lut, p)
+        assert " win1x1 " in dg.last_kernel(), dg.last_kernel()
+        assert np.array_equal(host(out), exp)
+        if Cout % 4 == 0:
+            bias = (-int(np.round(exp.mean())) + g.integers(-40, 40, Cout)).astype(np.int32)
+            mult = max(1, int(round((1 << 20) * 1.2 / max(1.0, float(exp.std())))))
+            rq = dg.Requant(mult, 20, 1, 0, 3, bias=torch.from_numpy(bias).to(DEV), bias_axis=0)
+            codes = dg.lut_conv2d_f4_prepared(xp, w4, lut, p, rq=rq)
+            assert " win1x1 " in dg.last_kernel(), dg.last_kernel()
+            expc = oracle.requantize(exp, mult, 20, 1, 0, 3, bias=bias, bias_axis=0)
+            assert np.array_equal(oracle_codes_of(codes, exp.shape[0], Cout), expc)
+
+
 def _conv_f4_cases(xp, w4, lut, p, exp, Cout, g, bn, epi):
     out = dg.lut_conv2d_f4_prepared(xp, w4, lut, p)
     assert dg.last_kernel().startswith(f"f4conv bn={bn} ") and f" epi={epi} " in dg.last_kernel(), dg.last_kernel()

@@ -92,10 +92,11 @@ def test_conv_chain_graph_replays_bit_exact():
 
 
 # the same regime on the FP4 conv kernel (dg_lut_conv2d_f4_prepared): shifted-window pairs (64- and
-# 128-wide, resident weights), direct 1x1 tiles of every width, the im2col-mode strided 1x1, the
+# 128-wide, resident weights; the 1x1 64 -> 64 window pairs), direct 1x1 tiles of every width, the im2col-mode strided 1x1, the
 # gathered stride-2 3x3; input 24 x 40 x 40 x 64 codes
 F4_CHAIN = [
     (64, 3, 1, "bn=64 win wbres wpair"),
+    (64, 1, 1, "bn=64 win1x1 wbres wpair"),
     (128, 3, 1, "bn=128 win wbres wpair"),
     (128, 3, 1, "bn=128 win wbres wpair"),
     (256, 1, 2, "direct=1 i2c"),
